@@ -1,0 +1,366 @@
+"""Seeded synthetic inputs shared by the oracle (tests) and the CUDA product path.
+
+This module holds NONE of the method's arithmetic: no ray generation, tracing, routing or
+shading.  It builds scene parts (triangle meshes, spheres, structured-volume bricks), the
+camera basis handed to both sides as float32 ("the harness computes the
+basis in double ... each component is rounded once to f32"), frame descriptors, and the
+application-level partition of a world over ranks (S2.2: "distribute the scene
+data in a very simple way").  Every generator is a pure function of its arguments.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass, field, replace
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libdpr_inputs.so")
+_lib = None
+
+
+def build_lib(force: bool = False) -> str:
+    src = os.path.join(_HERE, "gen.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-pthread", "-ffp-contract=off",
+                               "-o", _LIB_PATH, src, "-lm"])
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build_lib()
+        _lib = ctypes.CDLL(_LIB_PATH)
+        _lib.dpri_gyroid_mt.restype = ctypes.c_int64
+        _lib.dpri_gyroid_mt.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_void_p,
+                                        ctypes.c_int64, ctypes.c_int]
+        _lib.dpri_volume_field.restype = ctypes.c_int
+        _lib.dpri_volume_field.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_int]
+    return _lib
+
+
+# ----------------------------------------------------------------------------------------
+# Scene description types (mirrors the boundary's dpr_part_desc; include/dpr.h)
+# ----------------------------------------------------------------------------------------
+TRIS, SPHERES, BRICK = 0, 1, 2
+
+
+@dataclass
+class Part:
+    """One rank-local world part (S3.1.2: world content is rank-local)."""
+    rank: int
+    kind: int
+    albedo: Sequence[float] = (0.8, 0.8, 0.8)
+    verts: Optional[np.ndarray] = None      # (n,3) float32
+    idx: Optional[np.ndarray] = None        # (m,3) int32
+    spheres: Optional[np.ndarray] = None    # (n,4) float32: cx cy cz r
+    gdims: Sequence[int] = (0, 0, 0)
+    origin: Sequence[float] = (0.0, 0.0, 0.0)
+    spacing: Sequence[float] = (1.0, 1.0, 1.0)
+    cell_lo: Sequence[int] = (0, 0, 0)
+    cell_hi: Sequence[int] = (0, 0, 0)
+    voxels: Optional[np.ndarray] = None     # float32, x fastest, shape (nz,ny,nx)
+    tf: Optional[np.ndarray] = None         # (256,4) float32
+    tf_lo: float = 0.0
+    tf_hi: float = 1.0
+    density_scale: float = 1.0
+
+    def nprims(self) -> int:
+        if self.kind == TRIS:
+            return int(self.idx.shape[0])
+        if self.kind == SPHERES:
+            return int(self.spheres.shape[0])
+        return 0
+
+
+@dataclass
+class Camera:
+    E: np.ndarray
+    L: np.ndarray
+    U: np.ndarray
+    V: np.ndarray
+
+
+@dataclass
+class Frame:
+    W: int
+    H: int
+    spp: int = 1
+    spp_batch: int = 1
+    max_depth: int = 1
+    ao_k: int = 0
+    ao_radius: float = float("inf")
+    light_dir: Sequence[float] = (0.0, 1.0, 0.0)
+    E: Sequence[float] = (1.0, 1.0, 1.0)
+    A: Sequence[float] = (0.0, 0.0, 0.0)
+    B: Sequence[float] = (0.0, 0.0, 0.0)
+    dt: float = 0.0
+    seed: int = 7
+    flags: int = 0   # bit0: fixed jitter 0.5 (test mode)
+
+
+@dataclass
+class Scene:
+    name: str
+    parts: List[Part]
+    nranks: int
+    camera: Camera
+    frame: Frame
+    meta: dict = field(default_factory=dict)
+
+
+def f32(v) -> np.ndarray:
+    return np.asarray(v, dtype=np.float64).astype(np.float32)
+
+
+def normalize(v) -> np.ndarray:
+    v = np.asarray(v, dtype=np.float64)
+    return v / np.linalg.norm(v)
+
+
+def camera_basis(pos, look_at, up, fovy_deg: float, W: int, H: int) -> Camera:
+    """w=dir/|dir|, u=cross(w,up)/|.|, v=cross(u,w), h=tan(fovy*pi/360);
+    U=2h*aspect*u, V=2h*v, L=w-h*aspect*u-h*v; each rounded once to f32; E=pos."""
+    pos = np.asarray(pos, np.float64)
+    w = normalize(np.asarray(look_at, np.float64) - pos)
+    u = np.cross(w, np.asarray(up, np.float64))
+    u = u / np.linalg.norm(u)
+    v = np.cross(u, w)
+    h = math.tan(fovy_deg * math.pi / 360.0)
+    aspect = W / H
+    return Camera(E=f32(pos), L=f32(w - h * aspect * u - h * v), U=f32(2 * h * aspect * u),
+                  V=f32(2 * h * v))
+
+
+def camera_from_dir(pos, direction, up, fovy_deg, W, H) -> Camera:
+    return camera_basis(pos, np.asarray(pos, np.float64) + np.asarray(direction, np.float64),
+                        up, fovy_deg, W, H)
+
+
+# ----------------------------------------------------------------------------------------
+# Geometry generators
+# ----------------------------------------------------------------------------------------
+def gyroid_mesh(G: int, k: float = 4 * math.pi, nthreads: Optional[int] = None):
+    """Marching-tetrahedra gyroid on a G^3 point grid over [-1,1]^3 -> (verts, idx) soup."""
+    lib = _load()
+    nt = nthreads or os.cpu_count() or 1
+    n = lib.dpri_gyroid_mt(G, k, None, 0, nt)
+    if n < 0:
+        raise RuntimeError("gyroid count failed")
+    out = np.empty((n, 9), np.float32)
+    m = lib.dpri_gyroid_mt(G, k, out.ctypes.data, n, nt)
+    if m != n:
+        raise RuntimeError("gyroid generation failed")
+    verts = out.reshape(-1, 3)
+    idx = np.arange(3 * n, dtype=np.int32).reshape(-1, 3)
+    return verts, idx
+
+
+def quad_tris(corners) -> tuple:
+    v = f32(corners)
+    return v, np.array([[0, 1, 2], [0, 2, 3]], np.int32)
+
+
+def sphere_clusters(n_clusters: int, per_cluster: int, sigma: float, rmin: float, rmax: float,
+                    seed: int) -> np.ndarray:
+    rng = np.random.Generator(np.random.Philox(seed))
+    centres = rng.uniform(-1, 1, size=(n_clusters, 3))
+    pts = centres[:, None, :] + sigma * rng.standard_normal((n_clusters, per_cluster, 3))
+    r = rng.uniform(rmin, rmax, size=(n_clusters, per_cluster, 1))
+    return f32(np.concatenate([pts, r], axis=2).reshape(-1, 4))
+
+
+def volume_field(G: int, lo=(0, 0, 0), hi=None, nthreads: Optional[int] = None) -> np.ndarray:
+    """Procedural field on the G^3 grid over [-1,1]^3; returns the inclusive sub-box
+    [lo, hi] as float32 (nz, ny, nx)."""
+    lib = _load()
+    if hi is None:
+        hi = (G - 1, G - 1, G - 1)
+    lo = np.asarray(lo, np.int32)
+    hi = np.asarray(hi, np.int32)
+    shape = tuple(int(x) for x in (hi - lo + 1)[::-1])
+    out = np.empty(shape, np.float32)
+    lib.dpri_volume_field(G, lo.ctypes.data, hi.ctypes.data, out.ctypes.data,
+                          nthreads or os.cpu_count() or 1)
+    return out
+
+
+def default_tf(alpha_max: float = 0.02, s0: float = 0.3) -> np.ndarray:
+    """SURVEY 8(d) C3 TF: alpha=0 below s0, rising linearly to alpha_max at s=1; rgb ramp
+    blue -> white.  256 entries over [0,1]."""
+    s = np.arange(256, dtype=np.float64) / 255.0
+    a = np.where(s < s0, 0.0, (s - s0) / (1.0 - s0) * alpha_max)
+    rgb = np.stack([s, s, np.ones_like(s)], axis=1) * 0.5 + 0.5 * np.stack([s, s, s], axis=1)
+    return f32(np.concatenate([rgb, a[:, None]], axis=1))
+
+
+# ----------------------------------------------------------------------------------------
+# Partitioning (application side)
+# ----------------------------------------------------------------------------------------
+def bisect_partition(points: np.ndarray, nparts: int) -> np.ndarray:
+    """Recursive median bisection of points on the longest axis into nparts groups.
+    Returns the group index of each point (stable, deterministic)."""
+    n = points.shape[0]
+    out = np.zeros(n, np.int32)
+
+    def rec(sel: np.ndarray, first: int, count: int):
+        if count == 1 or sel.size == 0:
+            out[sel] = first
+            return
+        p = points[sel]
+        ext = p.max(axis=0) - p.min(axis=0)
+        ax = int(np.argmax(ext))
+        left_parts = count // 2
+        k = (sel.size * left_parts) // count
+        order = np.lexsort((sel, p[:, ax]))
+        rec(sel[order[:k]], first, left_parts)
+        rec(sel[order[k:]], first + left_parts, count - left_parts)
+
+    rec(np.arange(n), 0, nparts)
+    return out
+
+
+def split_mesh(verts: np.ndarray, idx: np.ndarray, nranks: int, albedo) -> List[Part]:
+    """Spatial partition of a triangle mesh by centroid bisection."""
+    tri = verts[idx]                      # (m,3,3)
+    cen = tri.astype(np.float64).mean(axis=1)
+    grp = bisect_partition(cen, nranks)
+    parts = []
+    for r in range(nranks):
+        sel = np.nonzero(grp == r)[0]
+        t = tri[sel].reshape(-1, 3)
+        parts.append(Part(rank=r, kind=TRIS, albedo=albedo, verts=np.ascontiguousarray(t),
+                          idx=np.arange(t.shape[0], dtype=np.int32).reshape(-1, 3)))
+    return parts
+
+
+def brick_boxes(cells, nparts: int):
+    """Recursive bisection of the cell domain [0,cells)^3 into nparts boxes (lo, hi)."""
+    boxes = [((0, 0, 0), tuple(cells), nparts)]
+    out = []
+    while boxes:
+        lo, hi, n = boxes.pop(0)
+        if n == 1:
+            out.append((lo, hi))
+            continue
+        ext = [hi[c] - lo[c] for c in range(3)]
+        ax = int(np.argmax(ext))
+        nl = n // 2
+        mid = lo[ax] + (ext[ax] * nl) // n
+        hl = list(hi); hl[ax] = mid
+        lr = list(lo); lr[ax] = mid
+        boxes.append((lo, tuple(hl), nl))
+        boxes.append((tuple(lr), hi, n - nl))
+    return out
+
+
+def volume_bricks(G: int, nranks: int, tf: np.ndarray, density_scale: float = 1.0,
+                  field_fn=None) -> List[Part]:
+    """Split the G^3 grid ((G-1)^3 cells) into nranks bricks; each brick stores voxels
+    [cell_lo, cell_hi] inclusive (one ghost layer).  Origin -1, spacing 2/(G-1)."""
+    h = np.float32(2.0 / (G - 1))
+    parts = []
+    boxes = brick_boxes((G - 1, G - 1, G - 1), nranks)
+    for r, (lo, hi) in enumerate(boxes):
+        vox = (field_fn or volume_field)(G, lo, hi)
+        parts.append(Part(rank=r, kind=BRICK, albedo=(1, 1, 1), gdims=(G, G, G),
+                          origin=(-1.0, -1.0, -1.0), spacing=(float(h),) * 3, cell_lo=lo,
+                          cell_hi=hi, voxels=np.ascontiguousarray(vox), tf=tf, tf_lo=0.0,
+                          tf_hi=1.0, density_scale=density_scale))
+    return parts
+
+
+def reassign(parts: List[Part], nranks: int) -> List[Part]:
+    return [replace(p, rank=p.rank % nranks) for p in parts]
+
+
+def union_parts(parts: List[Part]) -> List[Part]:
+    """The merged world on one rank, in rank order (global ids of the
+    union are the concatenation in rank order)."""
+    out = []
+    for r in sorted({p.rank for p in parts}):
+        out += [replace(p, rank=0) for p in parts if p.rank == r]
+    return out
+
+
+# ----------------------------------------------------------------------------------------
+# Configs (BASELINE.json configs; concretised in SURVEY 8(d))
+# ----------------------------------------------------------------------------------------
+C1_SPHERES = [((-1.5, 0.5, 0.0), 0.5, (0.9, 0.2, 0.2)),
+              ((-0.6, 0.8, 1.2), 0.8, (0.2, 0.9, 0.2)),
+              ((0.9, 0.4, -0.8), 0.4, (0.2, 0.2, 0.9)),
+              ((1.8, 1.0, 0.7), 1.0, (0.9, 0.9, 0.2))]
+
+
+def config1(W: int = 64, H: int = 64) -> Scene:
+    """configs[0]: two-rank world of 4 spheres + ground plane split by x-half, 64x64, 1 spp,
+    AO 4 rays, depth 2."""
+    parts = []
+    for r, (x0, x1) in enumerate([(-4.0, 0.0), (0.0, 4.0)]):
+        v, i = quad_tris([(x0, 0, -4), (x1, 0, -4), (x1, 0, 4), (x0, 0, 4)])
+        parts.append(Part(rank=r, kind=TRIS, albedo=(0.8, 0.8, 0.8), verts=v, idx=i))
+    for j, (c, rad, rho) in enumerate(C1_SPHERES):
+        r = 0 if j < 2 else 1
+        parts.append(Part(rank=r, kind=SPHERES, albedo=rho,
+                          spheres=f32([[c[0], c[1], c[2], rad]])))
+    # commit order within a rank: ground half, then its spheres
+    parts = [parts[0], parts[2], parts[3], parts[1], parts[4], parts[5]]
+    cam = camera_basis((0, 2.5, -7), (0, 0.6, 0), (0, 1, 0), 40.0, W, H)
+    fr = Frame(W=W, H=H, spp=1, spp_batch=1, max_depth=2, ao_k=4, ao_radius=float("inf"),
+               light_dir=f32(normalize((1, 0.8, -0.3))), E=(1, 1, 1), A=(0.3, 0.3, 0.3),
+               B=(0.05, 0.05, 0.1), seed=7)
+    return Scene("C1", parts, 2, cam, fr)
+
+
+C2_G = 301
+
+
+def config2(nranks: int = 1, G: int = C2_G, W: int = 1024, H: int = 1024, spp: int = 16,
+            spp_batch: int = 16) -> Scene:
+    """configs[1]: synthetic ~10M-triangle gyroid spatially partitioned over N ranks,
+    1024x1024, 16 spp, shadows + AO (K=4, aoRadius 0.25, depth 1)."""
+    verts, idx = gyroid_mesh(G)
+    parts = split_mesh(verts, idx, nranks, (0.75, 0.75, 0.75))
+    cam = camera_basis((2.2, 1.6, 2.8), (0, 0, 0), (0, 1, 0), 45.0, W, H)
+    fr = Frame(W=W, H=H, spp=spp, spp_batch=spp_batch, max_depth=1, ao_k=4, ao_radius=0.25,
+               light_dir=f32(normalize((1, 1.5, 0.5))), E=(1, 1, 1), A=(0.4, 0.4, 0.4),
+               B=(0.05, 0.05, 0.05), seed=7)
+    return Scene("C2", parts, nranks, cam, fr, meta={"G": G, "ntris": int(idx.shape[0])})
+
+
+def config3(nranks: int = 1, G: int = 1024, W: int = 1920, H: int = 1080) -> Scene:
+    """configs[2]: structured G^3 float32 volume split into per-rank bricks, DVR with volume
+    shadows (1 spp, depth 1), 1920x1080."""
+    tf = default_tf()
+    parts = volume_bricks(G, nranks, tf)
+    cam = camera_basis((0, 0.5, 3.2), (0, 0, 0), (0, 1, 0), 40.0, W, H)
+    h = float(np.float32(2.0 / (G - 1)))
+    fr = Frame(W=W, H=H, spp=1, spp_batch=1, max_depth=1, ao_k=0, ao_radius=0.0,
+               light_dir=f32(normalize((1, 2, 1))), E=(1, 1, 1), A=(0, 0, 0), B=(0, 0, 0),
+               dt=h, seed=7)
+    return Scene("C3", parts, nranks, cam, fr, meta={"G": G})
+
+
+def routing_hand_case(which: str) -> Scene:
+    """SURVEY 8(c).4 hand cases H1-H3 (1x1 image, jitter 0.5, d = (0,0,1) exactly)."""
+    cam = Camera(E=f32((0.2, 0.2, -1)), L=f32((-0.05, -0.05, 1)), U=f32((0.1, 0, 0)),
+                 V=f32((0, 0.1, 0)))
+    r0 = Part(rank=0, kind=TRIS, albedo=(0.5, 0.6, 0.7),
+              verts=f32([(-1, -1, 3), (1, -1, 3), (1, 1, 3), (-1, 1, 3)]),
+              idx=np.array([[0, 1, 2], [0, 2, 3]], np.int32))
+    if which in ("H1", "H3"):
+        r1v = f32([(-.5, -.5, 2), (.5, -.5, 2), (-.5, .5, 2)])
+    else:  # H2: rank 1's triangle covers (0.2, 0.2)
+        r1v = f32([(-.5, -.5, 2), (1, -.5, 2), (-.5, 1, 2)])
+    r1 = Part(rank=1, kind=TRIS, albedo=(0.9, 0.3, 0.1), verts=r1v,
+              idx=np.array([[0, 1, 2]], np.int32))
+    l = (0, 0, 1) if which == "H3" else (0, 0, -1)
+    fr = Frame(W=1, H=1, spp=1, spp_batch=1, max_depth=1, ao_k=0, light_dir=f32(l),
+               E=(1, 1, 1), A=(0, 0, 0), B=(0, 0, 0), seed=7, flags=1)
+    return Scene(which, [r0, r1], 2, cam, fr)
