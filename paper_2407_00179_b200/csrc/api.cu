@@ -1,0 +1,1159 @@
+// api.cu -- the C ABI of include/dpr.h and the host orchestration of the wavefront loop.
+//
+// One process per GPU; every rank owns a dpr_device.  A frame (S3.2) is:
+//   1. consistency: allgather of a 64-bit digest of camera+frame
+//   2. allgather of {rank box, prim count, part table} -> routing table (P8), global id
+//      bases (P12), global part->albedo table (shading at the resolving rank, reading A3)
+//   3. per spp batch: k_gen_primary, then lock-step steps {k_trace_path, k_trace_occl ->
+//      allgather of the per-destination counts -> grouped ncclSend/ncclRecv of the ray
+//      records} until every queue on every rank is empty (S2.2)
+//   4. ncclReduce(sum) of the float4 framebuffers (and debug dumps) to rank 0
+//   5. allgather of per-rank counters -> global routing matrices / visits / timings
+// The loopback group runs the same loop over N virtual ranks on one GPU with device copies
+// in place of NCCL (test fixture).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dpr.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace dpr;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Dev;
+
+struct Buf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+struct PartStore {
+    int kind = 0;
+    float albedo[3] = {0, 0, 0};
+    Buf verts, idx, spheres, vox, tf, mc;
+    int64_t nv = 0, nt = 0, ns = 0;
+    int gdims[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, mc_dims[3] = {0, 0, 0};
+    float origin[3] = {0, 0, 0}, spacing[3] = {1, 1, 1};
+    float tf_lo = 0, tf_hi = 1, dscale = 1;
+    int has_hint = 0;
+    float hint[6] = {0, 0, 0, 0, 0, 0};
+    int64_t nprims() const { return kind == DPR_PART_TRIANGLES ? nt : (kind == DPR_PART_SPHERES ? ns : 0); }
+};
+
+struct LoopGroup {
+    std::vector<Dev *> devs;
+};
+
+constexpr int MAXP = 1024;  // parts per rank in the frame allgather
+
+struct PartInfo {
+    uint32_t first, count;
+    float albedo[3];
+    float pad;
+};
+
+struct RankInfo {
+    uint64_t digest;
+    float box[6];
+    int32_t nonempty;
+    uint32_t nprims;
+    int32_t nparts;
+    int32_t pad;
+    PartInfo parts[MAXP];
+};
+
+struct StatsMsg {
+    int64_t V[3];
+    int64_t S[3][DPR_MAX_RANKS];
+    int64_t gen[3];
+    double ms_frame;
+};
+
+struct Dev {
+    int rank = 0, nranks = 1, cuda_dev = 0, nsm = 148;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    LoopGroup *group = nullptr;
+    dpr_allocator alloc{};
+    bool has_alloc = false;
+    std::vector<PartStore> parts;
+    // world
+    bool world_ready = false;
+    int64_t nprims = 0;
+    float box[6];
+    bool nonempty = false;
+    Buf b_prims_u, b_blo, b_bhi, b_keys[2], b_vals[2], b_tile, b_left, b_right, b_parent, b_rlo,
+        b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_nodes, b_bounds, b_hist;
+    std::vector<PartInfo> local_parts;
+    // frame
+    dpr_camera_basis cam{};
+    dpr_frame_desc fr{};
+    bool cam_set = false, fr_set = false;
+    Buf b_fb, b_fb_out, b_events, b_occl, b_ctr, b_counts, b_in_count, b_fetch, b_part_lo,
+        b_part_alb, b_scratch;
+    Buf b_path[2], b_occlq[2], b_send_path[DPR_MAX_RANKS], b_send_occl[DPR_MAX_RANKS];
+    uint32_t path_cap = 0, occl_cap = 0;
+    uint32_t *h_counts = nullptr;  // pinned: [N][2N+1]
+    uint32_t *h_in = nullptr;      // pinned: [2]
+    int frame_done = 0;
+    int mapped_w = 0, mapped_h = 0;
+    int64_t build_launches = 0, frame_launches = 0, frame_exch_bytes = 0, tpl = 0, tol = 0;
+    double ms_build = 0;
+    bool dumps_valid = false;
+    dpr_stats stats{};
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+};
+
+// ---------------------------------------------------------------------------------------
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(e_ == cudaErrorMemoryAllocation ? DPR_ERR_OOM : DPR_ERR_CUDA,           \
+                        std::string(#x) + ": " + cudaGetErrorString(e_));                       \
+    } while (0)
+
+#define NK(x)                                                                                   \
+    do {                                                                                        \
+        ncclResult_t r_ = (x);                                                                  \
+        if (r_ != ncclSuccess) return fail(DPR_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+#define RET(x)                    \
+    do {                          \
+        int rc_ = (x);            \
+        if (rc_ != DPR_OK) return rc_; \
+    } while (0)
+
+void *dmalloc(Dev *d, size_t bytes) {
+    if (bytes == 0) return nullptr;
+    if (d->has_alloc) return d->alloc.alloc(d->alloc.ctx, bytes, d->stream);
+    void *p = nullptr;
+    if (cudaMallocAsync(&p, bytes, d->stream) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void dfree(Dev *d, Buf &b) {
+    if (!b.p) return;
+    if (d->has_alloc) d->alloc.free(d->alloc.ctx, b.p, b.bytes, d->stream);
+    else cudaFreeAsync(b.p, d->stream);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
+int ensure(Dev *d, Buf &b, size_t bytes) {
+    if (b.bytes >= bytes && (b.p || bytes == 0)) return DPR_OK;
+    dfree(d, b);
+    if (bytes == 0) return DPR_OK;
+    b.p = dmalloc(d, bytes);
+    if (!b.p) return fail(DPR_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+    b.bytes = bytes;
+    return DPR_OK;
+}
+
+template <class T> T *P(Buf &b) { return reinterpret_cast<T *>(b.p); }
+
+cudaEvent_t next_event(Dev *d) {
+    if (d->ev_used == d->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        d->ev_pool.push_back(e);
+    }
+    return d->ev_pool[d->ev_used++];
+}
+
+uint64_t fnv1a(const void *p, size_t n, uint64_t h = 1469598103934665603ull) {
+    const unsigned char *c = (const unsigned char *)p;
+    for (size_t i = 0; i < n; ++i) { h ^= c[i]; h *= 1099511628211ull; }
+    return h;
+}
+
+uint64_t frame_digest(const Dev *d) {
+    uint64_t h = fnv1a(&d->cam, sizeof(d->cam));
+    dpr_frame_desc f = d->fr;
+    return fnv1a(&f, sizeof(f), h);
+}
+
+bool valid_dev(dpr_device h) { return h != nullptr; }
+
+// ---------------------------------------------------------------------------------------
+// Collectives (NCCL or loopback).  `L` is the list of local ranks (1 for NCCL mode).
+// ---------------------------------------------------------------------------------------
+int allgather_host(std::vector<Dev *> &L, const std::vector<const void *> &send, size_t bytes,
+                   std::vector<std::vector<char>> &out) {
+    Dev *d0 = L[0];
+    int N = d0->nranks;
+    if (d0->group || N == 1) {
+        std::vector<char> all((size_t)N * bytes);
+        for (size_t i = 0; i < L.size(); ++i) memcpy(all.data() + (size_t)L[i]->rank * bytes, send[i], bytes);
+        out.assign(L.size(), all);
+        return DPR_OK;
+    }
+    RET(ensure(d0, d0->b_scratch, bytes * (N + 1)));
+    char *sbuf = P<char>(d0->b_scratch), *rbuf = sbuf + bytes;
+    CK(cudaMemcpyAsync(sbuf, send[0], bytes, cudaMemcpyHostToDevice, d0->stream));
+    NK(ncclAllGather(sbuf, rbuf, bytes, ncclUint8, d0->comm, d0->stream));
+    out.assign(1, std::vector<char>((size_t)N * bytes));
+    CK(cudaMemcpyAsync(out[0].data(), rbuf, bytes * N, cudaMemcpyDeviceToHost, d0->stream));
+    CK(cudaStreamSynchronize(d0->stream));
+    return DPR_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// World build (a1).
+// ---------------------------------------------------------------------------------------
+int build_world(Dev *d) {
+    cudaStream_t s = d->stream;
+    int64_t n = 0;
+    for (auto &p : d->parts) n += p.nprims();
+    if (n >= (int64_t)0x7fffffff) return fail(DPR_ERR_INVALID_ARG, "too many primitives on one rank");
+    d->nprims = n;
+    int np = (int)d->parts.size();
+    // per-part bounds + overall centroid box
+    RET(ensure(d, d->b_bounds, sizeof(int) * 12 * (np + 1)));
+    std::vector<int> binit(12 * (np + 1));
+    for (int k = 0; k <= np; ++k)
+        for (int c = 0; c < 12; ++c) binit[12 * k + c] = (c % 6) < 3 ? 0x7fffffff : (int)0x80000000;
+    CK(cudaMemcpyAsync(d->b_bounds.p, binit.data(), binit.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    if (n > 0) {
+        RET(ensure(d, d->b_prims_u, sizeof(float4) * 3 * n));
+        RET(ensure(d, d->b_blo, sizeof(float4) * n));
+        RET(ensure(d, d->b_bhi, sizeof(float4) * n));
+    }
+    int64_t off = 0;
+    int launches = 0;
+    for (int k = 0; k < np; ++k) {
+        PartStore &p = d->parts[k];
+        if (p.kind == DPR_PART_TRIANGLES) {
+            launch_tri_prims(P<float>(p.verts), P<int32_t>(p.idx), p.nt, (uint32_t)off,
+                             P<float4>(d->b_prims_u), P<float4>(d->b_blo), P<float4>(d->b_bhi), s);
+        } else if (p.kind == DPR_PART_SPHERES) {
+            launch_sphere_prims(P<float4>(p.spheres), p.ns, (uint32_t)off, P<float4>(d->b_prims_u),
+                                P<float4>(d->b_blo), P<float4>(d->b_bhi), s);
+        }
+        int64_t cnt = p.nprims();
+        if (cnt > 0) {
+            launch_bounds(P<float4>(d->b_blo) + off, P<float4>(d->b_bhi) + off, cnt,
+                          P<int>(d->b_bounds) + 12 * (k + 1), d->nsm, s);
+            launches += 2;
+        }
+        off += cnt;
+    }
+    if (n > 0) { launch_bounds(P<float4>(d->b_blo), P<float4>(d->b_bhi), n, P<int>(d->b_bounds), d->nsm, s); launches++; }
+    // Morton keys + all digit histograms
+    std::vector<unsigned long long> hist(8 * 256, 0);
+    if (n > 0) {
+        for (int i = 0; i < 2; ++i) {
+            RET(ensure(d, d->b_keys[i], sizeof(uint64_t) * n));
+            RET(ensure(d, d->b_vals[i], sizeof(uint32_t) * n));
+        }
+        launch_morton(P<float4>(d->b_blo), P<float4>(d->b_bhi), n, P<int>(d->b_bounds),
+                      P<uint64_t>(d->b_keys[0]), P<uint32_t>(d->b_vals[0]), s);
+        RET(ensure(d, d->b_hist, sizeof(unsigned long long) * 8 * 256));
+        CK(cudaMemsetAsync(d->b_hist.p, 0, sizeof(unsigned long long) * 8 * 256, s));
+        launch_digit_hist_all(P<uint64_t>(d->b_keys[0]), n, P<unsigned long long>(d->b_hist), d->nsm, s);
+        launches += 2;
+        CK(cudaMemcpyAsync(hist.data(), d->b_hist.p, sizeof(unsigned long long) * 8 * 256, cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<int> bnd(12 * (np + 1));
+    CK(cudaMemcpyAsync(bnd.data(), d->b_bounds.p, bnd.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    auto ord2f = [](int i) { int j = i >= 0 ? i : i ^ 0x7fffffff; float f; memcpy(&f, &j, 4); return f; };
+    // rank box = exact union of prim boxes and brick cell-domain boxes (P8)
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    d->local_parts.clear();
+    off = 0;
+    for (int k = 0; k < np; ++k) {
+        PartStore &p = d->parts[k];
+        float plo[3], phi[3];
+        bool have = false;
+        if (p.kind == DPR_PART_BRICK) {
+            for (int c = 0; c < 3; ++c) {
+                plo[c] = p.origin[c] + (float)p.lo[c] * p.spacing[c];
+                phi[c] = p.origin[c] + (float)p.hi[c] * p.spacing[c];
+            }
+            have = true;
+        } else if (p.nprims() > 0) {
+            for (int c = 0; c < 3; ++c) { plo[c] = ord2f(bnd[12 * (k + 1) + c]); phi[c] = ord2f(bnd[12 * (k + 1) + 3 + c]); }
+            have = true;
+            PartInfo pi{};
+            pi.first = (uint32_t)off;
+            pi.count = (uint32_t)p.nprims();
+            for (int c = 0; c < 3; ++c) pi.albedo[c] = p.albedo[c];
+            d->local_parts.push_back(pi);
+        }
+        if (have) {
+            if (p.has_hint)
+                for (int c = 0; c < 3; ++c)
+                    if (!(p.hint[c] <= plo[c] && p.hint[3 + c] >= phi[c]))
+                        return fail(DPR_ERR_INVALID_ARG, "part " + std::to_string(k) + ": bounds_hint does not contain the part");
+            for (int c = 0; c < 3; ++c) { lo[c] = fminf(lo[c], plo[c]); hi[c] = fmaxf(hi[c], phi[c]); }
+        }
+        off += p.nprims();
+    }
+    if ((int)d->local_parts.size() > MAXP) return fail(DPR_ERR_INVALID_ARG, "too many parts on one rank");
+    d->nonempty = lo[0] <= hi[0];
+    for (int c = 0; c < 3; ++c) { d->box[c] = lo[c]; d->box[3 + c] = hi[c]; }
+    if (n > 0) {
+        // LSD radix sort; constant-digit passes skipped (order preserved by stability)
+        int cur = 0;
+        int64_t ntiles = radix_tiles(n);
+        RET(ensure(d, d->b_tile, sizeof(uint32_t) * 256 * ntiles));
+        for (int pass = 0; pass < 8; ++pass) {
+            bool constant = false;
+            for (int b = 0; b < 256; ++b) if (hist[pass * 256 + b] == (unsigned long long)n) constant = true;
+            if (constant) continue;
+            launch_radix_pass(P<uint64_t>(d->b_keys[cur]), P<uint32_t>(d->b_vals[cur]),
+                              P<uint64_t>(d->b_keys[cur ^ 1]), P<uint32_t>(d->b_vals[cur ^ 1]), n,
+                              8 * pass, P<uint32_t>(d->b_tile), s, &launches);
+            cur ^= 1;
+        }
+        uint64_t *keys = P<uint64_t>(d->b_keys[cur]);
+        uint32_t *perm = P<uint32_t>(d->b_vals[cur]);
+        RET(ensure(d, d->b_prims, sizeof(float4) * 3 * n));
+        RET(ensure(d, d->b_slo, sizeof(float4) * n));
+        RET(ensure(d, d->b_shi, sizeof(float4) * n));
+        launch_gather_prims(P<float4>(d->b_prims_u), perm, n, P<float4>(d->b_prims), P<float4>(d->b_blo),
+                            P<float4>(d->b_bhi), P<float4>(d->b_slo), P<float4>(d->b_shi), s);
+        launches++;
+        int64_t ni = std::max<int64_t>(n - 1, 1);
+        RET(ensure(d, d->b_nodes, sizeof(BVHNode) * ni));
+        if (n > 1) {
+            RET(ensure(d, d->b_left, sizeof(int) * (n - 1)));
+            RET(ensure(d, d->b_right, sizeof(int) * (n - 1)));
+            RET(ensure(d, d->b_rlo, sizeof(int) * (n - 1)));
+            RET(ensure(d, d->b_rhi, sizeof(int) * (n - 1)));
+            RET(ensure(d, d->b_parent, sizeof(int) * (2 * n - 1)));
+            RET(ensure(d, d->b_nlo, sizeof(float4) * (n - 1)));
+            RET(ensure(d, d->b_nhi, sizeof(float4) * (n - 1)));
+            RET(ensure(d, d->b_arrive, sizeof(int) * (n - 1)));
+            CK(cudaMemsetAsync(d->b_arrive.p, 0, sizeof(int) * (n - 1), s));
+            launch_karras(keys, n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_parent),
+                          P<int>(d->b_rlo), P<int>(d->b_rhi), s);
+            launch_refit(n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_parent), P<float4>(d->b_slo),
+                         P<float4>(d->b_shi), P<float4>(d->b_nlo), P<float4>(d->b_nhi), P<int>(d->b_arrive), s);
+            launches += 2;
+        }
+        launch_emit(n, 4, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_rlo), P<int>(d->b_rhi),
+                    P<float4>(d->b_slo), P<float4>(d->b_shi), P<float4>(d->b_nlo), P<float4>(d->b_nhi),
+                    P<BVHNode>(d->b_nodes), s);
+        launches++;
+    }
+    // bricks: macrocells
+    for (auto &p : d->parts) {
+        if (p.kind != DPR_PART_BRICK) continue;
+        int nx = p.hi[0] - p.lo[0] + 1, ny = p.hi[1] - p.lo[1] + 1, nz = p.hi[2] - p.lo[2] + 1;
+        for (int c = 0; c < 3; ++c) p.mc_dims[c] = (p.hi[c] - p.lo[c] + MC_SIZE - 1) / MC_SIZE;
+        size_t nm = (size_t)p.mc_dims[0] * p.mc_dims[1] * p.mc_dims[2];
+        RET(ensure(d, p.mc, std::max<size_t>(nm, 1)));
+        launch_macrocells(P<float>(p.vox), nx, ny, nz, p.mc_dims[0], p.mc_dims[1], p.mc_dims[2],
+                          P<float4>(p.tf), p.tf_lo, p.tf_hi, p.dscale, P<uint8_t>(p.mc), s);
+        launches++;
+    }
+    CK(cudaGetLastError());
+    d->build_launches = launches;
+    d->world_ready = true;
+    return DPR_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Frame.
+// ---------------------------------------------------------------------------------------
+struct FrameCtx {
+    Routing R;
+    std::vector<uint32_t> id_base;
+    std::vector<uint32_t> part_lo;
+    std::vector<float4> part_alb;
+};
+
+int frame_setup(std::vector<Dev *> &L, FrameCtx &fc) {
+    Dev *d0 = L[0];
+    const int N = d0->nranks;
+    std::vector<RankInfo> infos(L.size());
+    std::vector<const void *> sends;
+    for (size_t i = 0; i < L.size(); ++i) {
+        Dev *d = L[i];
+        RankInfo &ri = infos[i];
+        memset(&ri, 0, sizeof(ri));
+        ri.digest = frame_digest(d);
+        for (int c = 0; c < 6; ++c) ri.box[c] = d->box[c];
+        ri.nonempty = d->nonempty;
+        ri.nprims = (uint32_t)d->nprims;
+        ri.nparts = (int)d->local_parts.size();
+        for (int k = 0; k < ri.nparts; ++k) ri.parts[k] = d->local_parts[k];
+        sends.push_back(&ri);
+    }
+    std::vector<std::vector<char>> out;
+    RET(allgather_host(L, sends, sizeof(RankInfo), out));
+    const RankInfo *all = reinterpret_cast<const RankInfo *>(out[0].data());
+    for (int r = 1; r < N; ++r)
+        if (all[r].digest != all[0].digest)
+            return fail(DPR_ERR_CONSISTENCY, "camera/frame parameters differ between ranks (rank " +
+                                                 std::to_string(r) + " vs rank 0)");
+    fc.R.nranks = N;
+    fc.id_base.assign(N, 0);
+    uint64_t base = 0;
+    for (int r = 0; r < N; ++r) {
+        fc.id_base[r] = (uint32_t)base;
+        base += all[r].nprims;
+        fc.R.nonempty[r] = all[r].nonempty;
+        for (int c = 0; c < 3; ++c) {  // P8 padding, f32 host arithmetic
+            fc.R.box[r][c] = all[r].box[c] - 1e-4f;
+            fc.R.box[r][3 + c] = all[r].box[3 + c] + 1e-4f;
+        }
+        for (int k = 0; k < all[r].nparts; ++k) {
+            const PartInfo &pi = all[r].parts[k];
+            fc.part_lo.push_back(fc.id_base[r] + pi.first);
+            fc.part_alb.push_back(make_float4(pi.albedo[0], pi.albedo[1], pi.albedo[2], 0.0f));
+        }
+    }
+    if (base >= 0x7fffffffull) return fail(DPR_ERR_INVALID_ARG, "more than 2^31-1 primitives in the world");
+    if (fc.part_lo.empty()) { fc.part_lo.push_back(0); fc.part_alb.push_back(make_float4(0, 0, 0, 0)); }
+    return DPR_OK;
+}
+
+int frame_buffers(Dev *d, const FrameCtx &fc) {
+    const dpr_frame_desc &f = d->fr;
+    const int N = d->nranks;
+    int64_t P_ = (int64_t)f.W * f.H;
+    int64_t rays = P_ * f.spp_batch;
+    if (rays > 0xfffffff0ll) return fail(DPR_ERR_INVALID_ARG, "W*H*spp_batch too large for 32-bit queues");
+    uint32_t pcap = (uint32_t)rays;
+    int64_t ocap64 = rays * (1 + f.ao_k) * f.max_depth;
+    if (ocap64 > 0xfffffff0ll) ocap64 = 0xfffffff0ll;
+    uint32_t ocap = (uint32_t)ocap64;
+    RET(ensure(d, d->b_fb, sizeof(float4) * P_));
+    RET(ensure(d, d->b_fb_out, sizeof(float4) * P_));
+    if (f.flags & DPR_FLAG_DEBUG_DUMPS) {
+        size_t nd = (size_t)f.spp * f.max_depth * P_;
+        RET(ensure(d, d->b_events, sizeof(uint32_t) * nd));
+        RET(ensure(d, d->b_occl, sizeof(uint32_t) * nd));
+    }
+    for (int i = 0; i < 2; ++i) {
+        RET(ensure(d, d->b_path[i], sizeof(PathRec) * (size_t)pcap));
+        RET(ensure(d, d->b_occlq[i], sizeof(OcclRec) * (size_t)ocap));
+    }
+    for (int r = 0; r < N; ++r) {
+        if (r == d->rank) continue;
+        RET(ensure(d, d->b_send_path[r], sizeof(PathRec) * (size_t)pcap));
+        RET(ensure(d, d->b_send_occl[r], sizeof(OcclRec) * (size_t)ocap));
+    }
+    d->path_cap = pcap;
+    d->occl_cap = ocap;
+    RET(ensure(d, d->b_ctr, sizeof(Counters)));
+    RET(ensure(d, d->b_counts, sizeof(uint32_t) * (2 * N + 1)));
+    RET(ensure(d, d->b_in_count, sizeof(uint32_t) * 2));
+    RET(ensure(d, d->b_fetch, sizeof(uint32_t) * 2));
+    RET(ensure(d, d->b_part_lo, sizeof(uint32_t) * fc.part_lo.size()));
+    RET(ensure(d, d->b_part_alb, sizeof(float4) * fc.part_alb.size()));
+    if (!d->h_counts) {
+        CK(cudaMallocHost(&d->h_counts, sizeof(uint32_t) * DPR_MAX_RANKS * (2 * DPR_MAX_RANKS + 1)));
+        CK(cudaMallocHost(&d->h_in, sizeof(uint32_t) * 2));
+    }
+    cudaStream_t s = d->stream;
+    CK(cudaMemcpyAsync(d->b_part_lo.p, fc.part_lo.data(), sizeof(uint32_t) * fc.part_lo.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d->b_part_alb.p, fc.part_alb.data(), sizeof(float4) * fc.part_alb.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(d->b_fb.p, 0, sizeof(float4) * P_, s));
+    if (f.flags & DPR_FLAG_DEBUG_DUMPS) {
+        size_t nd = (size_t)f.spp * f.max_depth * P_;
+        CK(cudaMemsetAsync(d->b_events.p, 0, sizeof(uint32_t) * nd, s));
+        CK(cudaMemsetAsync(d->b_occl.p, 0, sizeof(uint32_t) * nd, s));
+    }
+    CK(cudaMemsetAsync(d->b_ctr.p, 0, sizeof(Counters), s));
+    return DPR_OK;
+}
+
+StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
+    StepArgs a;
+    memset(&a, 0, sizeof(a));
+    const dpr_frame_desc &f = d->fr;
+    a.F.W = f.W; a.F.H = f.H; a.F.P = f.W * f.H; a.F.spp = f.spp; a.F.max_depth = f.max_depth;
+    a.F.ao_k = f.ao_k; a.F.ao_radius = f.ao_radius; a.F.dt = f.dt; a.F.seed = f.seed; a.F.flags = f.flags;
+    for (int c = 0; c < 3; ++c) {
+        a.F.l[c] = f.light_dir[c]; a.F.E[c] = f.E[c]; a.F.A[c] = f.A[c]; a.F.B[c] = f.B[c];
+        a.F.cE[c] = d->cam.E[c]; a.F.cL[c] = d->cam.L[c]; a.F.cU[c] = d->cam.U[c]; a.F.cV[c] = d->cam.V[c];
+    }
+    a.R = fc.R;
+    a.R.self = d->rank;
+    a.W.nodes = P<BVHNode>(d->b_nodes);
+    a.W.prims = P<float4>(d->b_prims);
+    a.W.nprims = d->nprims;
+    a.W.id_base = fc.id_base[d->rank];
+    a.W.nbricks = 0;
+    for (auto &p : d->parts) {
+        if (p.kind != DPR_PART_BRICK || a.W.nbricks >= MAX_BRICKS) continue;
+        BrickDev &B = a.W.bricks[a.W.nbricks++];
+        for (int c = 0; c < 3; ++c) {
+            B.lo[c] = p.lo[c]; B.hi[c] = p.hi[c]; B.mc_dims[c] = p.mc_dims[c];
+            B.O[c] = p.origin[c]; B.h[c] = p.spacing[c];
+            B.box_lo[c] = p.origin[c] + (float)p.lo[c] * p.spacing[c];
+            B.box_hi[c] = p.origin[c] + (float)p.hi[c] * p.spacing[c];
+        }
+        B.vox = P<float>(p.vox); B.mc = P<uint8_t>(p.mc); B.tf = P<float4>(p.tf);
+        B.tf_lo = p.tf_lo; B.tf_hi = p.tf_hi; B.dscale = p.dscale;
+    }
+    a.T.n = (int)fc.part_lo.size();
+    a.T.id_lo = P<uint32_t>(d->b_part_lo);
+    a.T.albedo = P<float4>(d->b_part_alb);
+    int nxt = cur ^ 1;
+    a.Q.path_in = P<PathRec>(d->b_path[cur]);
+    a.Q.occl_in = P<OcclRec>(d->b_occlq[cur]);
+    a.Q.in_count = P<uint32_t>(d->b_in_count);
+    for (int r = 0; r < d->nranks; ++r) {
+        a.Q.path_out[r] = r == d->rank ? P<PathRec>(d->b_path[nxt]) : P<PathRec>(d->b_send_path[r]);
+        a.Q.occl_out[r] = r == d->rank ? P<OcclRec>(d->b_occlq[nxt]) : P<OcclRec>(d->b_send_occl[r]);
+    }
+    a.Q.out_count = P<uint32_t>(d->b_counts);
+    a.Q.path_cap = d->path_cap;
+    a.Q.occl_cap = d->occl_cap;
+    a.Q.fetch = P<uint32_t>(d->b_fetch);
+    a.fb = P<float4>(d->b_fb);
+    a.events = (f.flags & DPR_FLAG_DEBUG_DUMPS) ? P<uint32_t>(d->b_events) : nullptr;
+    a.occl = (f.flags & DPR_FLAG_DEBUG_DUMPS) ? P<uint32_t>(d->b_occl) : nullptr;
+    a.ctr = P<Counters>(d->b_ctr);
+    return a;
+}
+
+// counts[k][src][dst] for the step just finished; also returns the overflow flags.
+int gather_counts(std::vector<Dev *> &L, std::vector<int64_t> &C, unsigned &overflow) {
+    Dev *d0 = L[0];
+    const int N = d0->nranks;
+    const size_t W = 2 * N + 1;
+    C.assign((size_t)2 * N * N, 0);
+    overflow = 0;
+    std::vector<const uint32_t *> rows(N, nullptr);
+    if (d0->group || N == 1) {
+        for (Dev *d : L) {
+            // the overflow word lives in the Counters block; mirror it into the counts tail
+            CK(cudaMemcpyAsync(P<uint32_t>(d->b_counts) + 2 * N, &P<Counters>(d->b_ctr)->overflow,
+                               sizeof(uint32_t), cudaMemcpyDeviceToDevice, d->stream));
+            CK(cudaMemcpyAsync(d->h_counts, d->b_counts.p, sizeof(uint32_t) * W, cudaMemcpyDeviceToHost,
+                               d->stream));
+        }
+        for (Dev *d : L) CK(cudaStreamSynchronize(d->stream));
+        for (Dev *d : L) rows[d->rank] = d->h_counts;
+    } else {
+        RET(ensure(d0, d0->b_scratch, sizeof(uint32_t) * W * (N + 1)));
+        uint32_t *recv = P<uint32_t>(d0->b_scratch);
+        CK(cudaMemcpyAsync(P<uint32_t>(d0->b_counts) + 2 * N, &P<Counters>(d0->b_ctr)->overflow,
+                           sizeof(uint32_t), cudaMemcpyDeviceToDevice, d0->stream));
+        NK(ncclAllGather(d0->b_counts.p, recv, W, ncclUint32, d0->comm, d0->stream));
+        CK(cudaMemcpyAsync(d0->h_counts, recv, sizeof(uint32_t) * W * N, cudaMemcpyDeviceToHost, d0->stream));
+        CK(cudaStreamSynchronize(d0->stream));
+        for (int r = 0; r < N; ++r) rows[r] = d0->h_counts + (size_t)r * W;
+    }
+    for (int src = 0; src < N; ++src)
+        for (int k = 0; k < 2; ++k)
+            for (int dst = 0; dst < N; ++dst) C[((size_t)k * N + src) * N + dst] = rows[src][k * N + dst];
+    for (int src = 0; src < N; ++src) overflow |= rows[src][2 * N];
+    return DPR_OK;
+}
+
+int render_group(std::vector<Dev *> &L) {
+    Dev *d0 = L[0];
+    const int N = d0->nranks;
+    for (Dev *d : L) {
+        if (!d->world_ready) return fail(DPR_ERR_STATE, "dpr_commit_world has not been called");
+        if (!d->cam_set || !d->fr_set) return fail(DPR_ERR_STATE, "camera and frame must be set before rendering");
+        d->ev_used = 0;
+        d->frame_done = 0;
+        d->dumps_valid = false;
+    }
+    const dpr_frame_desc &f = d0->fr;
+    for (Dev *d : L) { d->frame_launches = 0; d->frame_exch_bytes = 0; d->tpl = 0; d->tol = 0; }
+    cudaEvent_t ev_f0 = next_event(d0), ev_f1;
+    CK(cudaEventRecord(ev_f0, d0->stream));
+    FrameCtx fc;
+    memset(&fc.R, 0, sizeof(fc.R));
+    RET(frame_setup(L, fc));
+    for (Dev *d : L) RET(frame_buffers(d, fc));
+    const int64_t P_ = (int64_t)f.W * f.H;
+    const int nb = (f.spp + f.spp_batch - 1) / f.spp_batch;
+    int64_t steps = 0;
+    int64_t launches = 0;
+    std::vector<int> cur(L.size(), 0);
+    std::vector<int> grid_p(L.size()), grid_o(L.size());
+    for (size_t i = 0; i < L.size(); ++i) {
+        grid_p[i] = std::max(1, trace_path_occupancy(TRACE_BLOCK)) * L[i]->nsm;
+        grid_o[i] = std::max(1, trace_occl_occupancy(TRACE_BLOCK)) * L[i]->nsm;
+    }
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_path, t_occl, t_exch, t_gen;
+    std::vector<int64_t> C;
+    for (int b = 0; b < nb; ++b) {
+        int s0 = b * f.spp_batch, ns = std::min(f.spp_batch, f.spp - s0);
+        for (size_t i = 0; i < L.size(); ++i) {
+            Dev *d = L[i];
+            CK(cudaMemsetAsync(d->b_counts.p, 0, sizeof(uint32_t) * (2 * N + 1), d->stream));
+            StepArgs a = make_args(d, fc, cur[i]);
+            cudaEvent_t e0 = next_event(d), e1 = next_event(d);
+            CK(cudaEventRecord(e0, d->stream));
+            launch_gen_primary(a, s0, ns, d->stream);
+            CK(cudaEventRecord(e1, d->stream));
+            if (i == 0) t_gen.push_back({e0, e1});
+            launches++;
+            CK(cudaGetLastError());
+        }
+        for (;;) {
+            unsigned ovf = 0;
+            RET(gather_counts(L, C, ovf));
+            if (ovf & 1u) return fail(DPR_ERR_QUEUE_OVERFLOW, "ray queue capacity exceeded; lower spp_batch");
+            if (ovf & 2u) return fail(DPR_ERR_STATE, "BVH traversal stack overflow");
+            int64_t total = 0;
+            for (int64_t v : C) total += v;
+            if (total == 0) break;
+            // exchange: records for other ranks -> their next input queues
+            cudaEvent_t ex0 = next_event(d0), ex1 = next_event(d0);
+            CK(cudaEventRecord(ex0, d0->stream));
+            std::vector<std::vector<int64_t>> offs(L.size() * 2);
+            for (size_t i = 0; i < L.size(); ++i) {
+                Dev *d = L[i];
+                for (int k = 0; k < 2; ++k) {
+                    std::vector<int64_t> off(N);
+                    int64_t tin = 0, gt = 0;
+                    int64_t cap = k == 0 ? d->path_cap : d->occl_cap;
+                    int rc = dpr_exchange_plan(N, d->rank, C.data() + (size_t)k * N * N, cap, off.data(), &tin, &gt);
+                    if (rc != DPR_OK) return fail(rc, "ray queue capacity exceeded on receive; lower spp_batch");
+                    d->h_in[k] = (uint32_t)tin;
+                    offs[2 * i + k] = off;
+                }
+            }
+            if (N > 1) {
+                const size_t rs[2] = {sizeof(PathRec), sizeof(OcclRec)};
+                if (d0->group) {
+                    for (size_t i = 0; i < L.size(); ++i) {
+                        Dev *dst = L[i];
+                        int nxt = cur[i] ^ 1;
+                        for (int k = 0; k < 2; ++k) {
+                            char *base = k == 0 ? P<char>(dst->b_path[nxt]) : P<char>(dst->b_occlq[nxt]);
+                            for (int src = 0; src < N; ++src) {
+                                if (src == dst->rank) continue;
+                                int64_t cnt = C[((size_t)k * N + src) * N + dst->rank];
+                                if (!cnt) continue;
+                                Dev *sd = L[src];
+                                const void *from = k == 0 ? sd->b_send_path[dst->rank].p : sd->b_send_occl[dst->rank].p;
+                                CK(cudaMemcpyAsync(base + offs[2 * i + k][src] * rs[k], from, cnt * rs[k],
+                                                   cudaMemcpyDeviceToDevice, dst->stream));
+                                sd->frame_exch_bytes += cnt * rs[k];
+                            }
+                        }
+                    }
+                } else {
+                    Dev *d = d0;
+                    int nxt = cur[0] ^ 1;
+                    NK(ncclGroupStart());
+                    for (int k = 0; k < 2; ++k) {
+                        char *base = k == 0 ? P<char>(d->b_path[nxt]) : P<char>(d->b_occlq[nxt]);
+                        for (int peer = 0; peer < N; ++peer) {
+                            if (peer == d->rank) continue;
+                            int64_t sc = C[((size_t)k * N + d->rank) * N + peer];
+                            int64_t rc = C[((size_t)k * N + peer) * N + d->rank];
+                            if (sc) {
+                                const void *from = k == 0 ? d->b_send_path[peer].p : d->b_send_occl[peer].p;
+                                NK(ncclSend(from, sc * rs[k], ncclUint8, peer, d->comm, d->stream));
+                                d->frame_exch_bytes += sc * rs[k];
+                            }
+                            if (rc) NK(ncclRecv(base + offs[k][peer] * rs[k], rc * rs[k], ncclUint8, peer, d->comm, d->stream));
+                        }
+                    }
+                    NK(ncclGroupEnd());
+                }
+            }
+            CK(cudaEventRecord(ex1, d0->stream));
+            t_exch.push_back({ex0, ex1});
+            // next step: swap queues, trace
+            for (size_t i = 0; i < L.size(); ++i) {
+                Dev *d = L[i];
+                cur[i] ^= 1;
+                CK(cudaMemcpyAsync(d->b_in_count.p, d->h_in, sizeof(uint32_t) * 2, cudaMemcpyHostToDevice, d->stream));
+                CK(cudaMemsetAsync(d->b_counts.p, 0, sizeof(uint32_t) * (2 * N + 1), d->stream));
+                CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 2, d->stream));
+                StepArgs a = make_args(d, fc, cur[i]);
+                if (d->h_in[0]) {
+                    cudaEvent_t e0 = next_event(d), e1 = next_event(d);
+                    CK(cudaEventRecord(e0, d->stream));
+                    launch_trace_path(a, grid_p[i], d->stream);
+                    CK(cudaEventRecord(e1, d->stream));
+                    if (i == 0) t_path.push_back({e0, e1});
+                    launches++;
+                    d->tpl++;
+                }
+                if (d->h_in[1]) {
+                    cudaEvent_t e0 = next_event(d), e1 = next_event(d);
+                    CK(cudaEventRecord(e0, d->stream));
+                    launch_trace_occl(a, grid_o[i], d->stream);
+                    CK(cudaEventRecord(e1, d->stream));
+                    if (i == 0) t_occl.push_back({e0, e1});
+                    launches++;
+                    d->tol++;
+                }
+                CK(cudaGetLastError());
+            }
+            steps++;
+        }
+    }
+    // a7: framebuffer (+ dumps) reduction to rank 0, normalisation by spp
+    cudaEvent_t r0 = next_event(d0), r1 = next_event(d0);
+    CK(cudaEventRecord(r0, d0->stream));
+    const size_t nd = (size_t)f.spp * f.max_depth * P_;
+    const bool dumps = f.flags & DPR_FLAG_DEBUG_DUMPS;
+    if (N > 1 && d0->group) {
+        Dev *root = L[0];
+        for (int r = 1; r < N; ++r) {
+            launch_fb_accumulate(P<float4>(root->b_fb), P<float4>(L[r]->b_fb), P_, root->stream);
+            launches++;
+            if (dumps) {
+                launch_u32_accumulate(P<uint32_t>(root->b_events), P<uint32_t>(L[r]->b_events), nd, root->stream);
+                launch_u32_accumulate(P<uint32_t>(root->b_occl), P<uint32_t>(L[r]->b_occl), nd, root->stream);
+                launches += 2;
+            }
+        }
+    } else if (N > 1) {
+        Dev *d = d0;
+        NK(ncclGroupStart());
+        NK(ncclReduce(d->b_fb.p, d->b_fb.p, 4 * P_, ncclFloat, ncclSum, 0, d->comm, d->stream));
+        if (dumps) {
+            NK(ncclReduce(d->b_events.p, d->b_events.p, nd, ncclUint32, ncclSum, 0, d->comm, d->stream));
+            NK(ncclReduce(d->b_occl.p, d->b_occl.p, nd, ncclUint32, ncclSum, 0, d->comm, d->stream));
+        }
+        NK(ncclGroupEnd());
+    }
+    for (Dev *d : L) {
+        if (d->rank != 0) continue;
+        launch_fb_normalize(P<float4>(d->b_fb_out), P<float4>(d->b_fb), P_, (float)f.spp, d->stream);
+        launches++;
+        d->dumps_valid = dumps;
+    }
+    CK(cudaEventRecord(r1, d0->stream));
+    ev_f1 = next_event(d0);
+    CK(cudaEventRecord(ev_f1, d0->stream));
+    CK(cudaStreamSynchronize(d0->stream));
+    CK(cudaGetLastError());
+    // stats
+    auto sum_ms = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v) {
+        double t = 0;
+        for (auto &e : v) { float ms = 0; cudaEventElapsedTime(&ms, e.first, e.second); t += ms; }
+        return t;
+    };
+    float fms = 0;
+    cudaEventElapsedTime(&fms, ev_f0, ev_f1);
+    std::vector<StatsMsg> msgs(L.size());
+    std::vector<Counters> ctr(L.size());
+    for (size_t i = 0; i < L.size(); ++i) {
+        CK(cudaMemcpy(&ctr[i], L[i]->b_ctr.p, sizeof(Counters), cudaMemcpyDeviceToHost));
+        StatsMsg &m = msgs[i];
+        memset(&m, 0, sizeof(m));
+        for (int k = 0; k < 3; ++k) {
+            m.V[k] = (int64_t)ctr[i].V[k];
+            m.gen[k] = (int64_t)ctr[i].gen[k];
+            for (int r = 0; r < N; ++r) m.S[k][r] = (int64_t)ctr[i].S[k][r];
+        }
+        m.ms_frame = fms;
+    }
+    std::vector<const void *> sends;
+    for (auto &m : msgs) sends.push_back(&m);
+    std::vector<std::vector<char>> out;
+    RET(allgather_host(L, sends, sizeof(StatsMsg), out));
+    const StatsMsg *all = reinterpret_cast<const StatsMsg *>(out[0].data());
+    for (size_t i = 0; i < L.size(); ++i) {
+        Dev *d = L[i];
+        dpr_stats &st = d->stats;
+        memset(&st, 0, sizeof(st));
+        st.nranks = N;
+        st.rank = d->rank;
+        st.kernel_launches_local = d->build_launches + (i == 0 ? launches : 0);
+        st.exchanged_bytes_local = d->frame_exch_bytes;
+        st.trace_path_launches = d->tpl;
+        st.trace_occl_launches = d->tol;
+        st.steps = steps;
+        double mx = 0;
+        for (int r = 0; r < N; ++r) {
+            for (int k = 0; k < 3; ++k) {
+                st.V[k][r] = all[r].V[k];
+                st.rays[k] += all[r].gen[k];
+                for (int q = 0; q < N; ++q) st.S[k][r][q] = all[r].S[k][q];
+            }
+            mx = std::max(mx, all[r].ms_frame);
+        }
+        const KernelCounters &a = ctr[i].kc[0], &o = ctr[i].kc[1];
+        st.node_visits_local = (int64_t)(a.nodes + o.nodes);
+        st.tri_tests_local = (int64_t)(a.tris + o.tris);
+        st.sphere_tests_local = (int64_t)(a.sphs + o.sphs);
+        st.vol_samples_local = (int64_t)(a.vols + o.vols);
+        st.records_in_local = (int64_t)(a.rin + o.rin);
+        st.records_out_local = (int64_t)(a.rout_path + a.rout_occl + o.rout_occl);
+        // algorithmic bytes: records read + written, node fetches
+        // (64 B), triangle tests (48 B), sphere tests (16 B), volume samples (8 voxels, 32 B)
+        st.path_bytes_alg_local = (int64_t)(a.rin * 64 + a.rout_path * 64 + a.rout_occl * 48 +
+                                            a.nodes * 64 + a.tris * 48 + a.sphs * 16 + a.vols * 32);
+        st.occl_bytes_alg_local = (int64_t)(o.rin * 48 + o.rout_occl * 48 + o.nodes * 64 +
+                                            o.tris * 48 + o.sphs * 16 + o.vols * 32);
+        st.ms_frame = fms;
+        st.ms_frame_max = mx;
+        if (i == 0) {
+            st.ms_gen = sum_ms(t_gen);
+            st.ms_trace_path = sum_ms(t_path);
+            st.ms_trace_occl = sum_ms(t_occl);
+            st.ms_exchange = sum_ms(t_exch);
+            float rms = 0;
+            cudaEventElapsedTime(&rms, r0, r1);
+            st.ms_reduce = rms;
+        }
+        d->frame_done = 1;
+        d->mapped_w = d->rank == 0 ? f.W : 0;
+        d->mapped_h = d->rank == 0 ? f.H : 0;
+    }
+    return DPR_OK;
+}
+
+int check_part(const dpr_part_desc *p) {
+    if (!p) return fail(DPR_ERR_INVALID_ARG, "null part");
+    if (p->memory != DPR_MEMORY_HOST && p->memory != DPR_MEMORY_DEVICE) return fail(DPR_ERR_INVALID_ARG, "bad memory kind");
+    switch (p->kind) {
+    case DPR_PART_TRIANGLES:
+        if (p->n_tris < 0 || p->n_verts < 0 || (p->n_tris > 0 && (!p->verts || !p->idx)))
+            return fail(DPR_ERR_INVALID_ARG, "triangle part: bad arrays");
+        break;
+    case DPR_PART_SPHERES:
+        if (p->n_spheres < 0 || (p->n_spheres > 0 && !p->spheres)) return fail(DPR_ERR_INVALID_ARG, "sphere part: bad arrays");
+        break;
+    case DPR_PART_BRICK:
+        if (!p->voxels || !p->tf) return fail(DPR_ERR_INVALID_ARG, "brick part: null voxels/tf");
+        for (int c = 0; c < 3; ++c)
+            if (p->cell_lo[c] < 0 || p->cell_hi[c] <= p->cell_lo[c] || p->cell_hi[c] > p->gdims[c] - 1 || !(p->spacing[c] > 0))
+                return fail(DPR_ERR_INVALID_ARG, "brick part: bad cell range / spacing");
+        if (!(p->tf_hi > p->tf_lo)) return fail(DPR_ERR_INVALID_ARG, "brick part: tf_hi must exceed tf_lo");
+        break;
+    default:
+        return fail(DPR_ERR_INVALID_ARG, "bad part kind");
+    }
+    return DPR_OK;
+}
+
+int copy_in(Dev *d, Buf &b, const void *src, size_t bytes, int memory) {
+    RET(ensure(d, b, bytes));
+    if (bytes)
+        CK(cudaMemcpyAsync(b.p, src, bytes, memory == DPR_MEMORY_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, d->stream));
+    return DPR_OK;
+}
+
+int init_dev(Dev *d, int rank, int nranks, int cuda_device, void *stream, const dpr_allocator *alloc) {
+    d->rank = rank;
+    d->nranks = nranks;
+    d->cuda_dev = cuda_device;
+    d->stream = (cudaStream_t)stream;
+    if (alloc && alloc->alloc && alloc->free) { d->alloc = *alloc; d->has_alloc = true; }
+    CK(cudaSetDevice(cuda_device));
+    CK(cudaDeviceGetAttribute(&d->nsm, cudaDevAttrMultiProcessorCount, cuda_device));
+    for (int c = 0; c < 3; ++c) { d->box[c] = INFINITY; d->box[3 + c] = -INFINITY; }
+    return DPR_OK;
+}
+
+void release_bufs(Dev *d) {
+    for (auto &p : d->parts) { dfree(d, p.verts); dfree(d, p.idx); dfree(d, p.spheres); dfree(d, p.vox); dfree(d, p.tf); dfree(d, p.mc); }
+    d->parts.clear();
+    Buf *bs[] = {&d->b_prims_u, &d->b_blo, &d->b_bhi, &d->b_keys[0], &d->b_keys[1], &d->b_vals[0],
+                 &d->b_vals[1], &d->b_tile, &d->b_left, &d->b_right, &d->b_parent, &d->b_rlo, &d->b_rhi,
+                 &d->b_nlo, &d->b_nhi, &d->b_arrive, &d->b_prims, &d->b_slo, &d->b_shi, &d->b_nodes,
+                 &d->b_bounds, &d->b_hist, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
+                 &d->b_counts, &d->b_in_count, &d->b_fetch, &d->b_part_lo, &d->b_part_alb, &d->b_scratch,
+                 &d->b_path[0], &d->b_path[1], &d->b_occlq[0], &d->b_occlq[1]};
+    for (Buf *b : bs) dfree(d, *b);
+    for (int r = 0; r < DPR_MAX_RANKS; ++r) { dfree(d, d->b_send_path[r]); dfree(d, d->b_send_occl[r]); }
+    if (d->h_counts) cudaFreeHost(d->h_counts);
+    if (d->h_in) cudaFreeHost(d->h_in);
+    d->h_counts = nullptr;
+    d->h_in = nullptr;
+    for (auto e : d->ev_pool) cudaEventDestroy(e);
+    d->ev_pool.clear();
+}
+
+}  // namespace
+
+struct dpr_device_s {
+    Dev d;
+};
+
+// =======================================================================================
+// C ABI
+// =======================================================================================
+extern "C" {
+
+int dpr_get_unique_id(uint8_t out[DPR_UNIQUE_ID_BYTES]) {
+    if (!out) return fail(DPR_ERR_INVALID_ARG, "null out");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == DPR_UNIQUE_ID_BYTES, "unique id size");
+    memcpy(out, &id, DPR_UNIQUE_ID_BYTES);
+    return DPR_OK;
+}
+
+int dpr_create_device(int rank, int nranks, int cuda_device, const uint8_t *uid, void *cuda_stream,
+                      const dpr_allocator *alloc, dpr_device *out) {
+    if (!out || nranks < 1 || nranks > DPR_MAX_RANKS || rank < 0 || rank >= nranks)
+        return fail(DPR_ERR_INVALID_ARG, "bad rank/nranks/out");
+    if (nranks > 1 && !uid) return fail(DPR_ERR_INVALID_ARG, "uid required for nranks > 1");
+    dpr_device h = new dpr_device_s();
+    int rc = init_dev(&h->d, rank, nranks, cuda_device, cuda_stream, alloc);
+    if (rc != DPR_OK) { delete h; return rc; }
+    if (nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, uid, DPR_UNIQUE_ID_BYTES);
+        ncclResult_t r = ncclCommInitRank(&h->d.comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            delete h;
+            return fail(DPR_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        }
+    }
+    *out = h;
+    return DPR_OK;
+}
+
+int dpr_create_loopback_group(int nranks, int cuda_device, void *cuda_stream, const dpr_allocator *alloc,
+                              dpr_device *out) {
+    if (!out || nranks < 1 || nranks > DPR_MAX_RANKS) return fail(DPR_ERR_INVALID_ARG, "bad nranks/out");
+    LoopGroup *g = new LoopGroup();
+    for (int r = 0; r < nranks; ++r) {
+        dpr_device h = new dpr_device_s();
+        int rc = init_dev(&h->d, r, nranks, cuda_device, cuda_stream, alloc);
+        if (rc != DPR_OK) return rc;
+        h->d.group = g;
+        g->devs.push_back(&h->d);
+        out[r] = h;
+    }
+    return DPR_OK;
+}
+
+int dpr_release_device(dpr_device dev) {
+    if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
+    Dev *d = &dev->d;
+    cudaSetDevice(d->cuda_dev);
+    cudaStreamSynchronize(d->stream);
+    release_bufs(d);
+    cudaStreamSynchronize(d->stream);
+    if (d->comm) ncclCommDestroy(d->comm);
+    if (d->group) {
+        auto &v = d->group->devs;
+        v[d->rank] = nullptr;
+        bool empty = true;
+        for (auto *x : v) if (x) empty = false;
+        if (empty) delete d->group;
+    }
+    delete dev;
+    return DPR_OK;
+}
+
+int dpr_commit_part(dpr_device dev, const dpr_part_desc *part) {
+    if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
+    RET(check_part(part));
+    Dev *d = &dev->d;
+    CK(cudaSetDevice(d->cuda_dev));
+    PartStore p;
+    p.kind = part->kind;
+    for (int c = 0; c < 3; ++c) p.albedo[c] = part->albedo[c];
+    p.has_hint = part->has_bounds_hint;
+    for (int c = 0; c < 6; ++c) p.hint[c] = part->bounds_hint[c];
+    if (p.kind == DPR_PART_TRIANGLES) {
+        p.nv = part->n_verts;
+        p.nt = part->n_tris;
+        if (part->memory == DPR_MEMORY_HOST)
+            for (int64_t i = 0; i < 3 * p.nt; ++i)
+                if (part->idx[i] < 0 || part->idx[i] >= p.nv) return fail(DPR_ERR_INVALID_ARG, "triangle index out of range");
+        RET(copy_in(d, p.verts, part->verts, sizeof(float) * 3 * p.nv, part->memory));
+        RET(copy_in(d, p.idx, part->idx, sizeof(int32_t) * 3 * p.nt, part->memory));
+    } else if (p.kind == DPR_PART_SPHERES) {
+        p.ns = part->n_spheres;
+        RET(copy_in(d, p.spheres, part->spheres, sizeof(float) * 4 * p.ns, part->memory));
+    } else {
+        for (int c = 0; c < 3; ++c) {
+            p.gdims[c] = part->gdims[c]; p.lo[c] = part->cell_lo[c]; p.hi[c] = part->cell_hi[c];
+            p.origin[c] = part->origin[c]; p.spacing[c] = part->spacing[c];
+        }
+        for (auto &q : d->parts)
+            if (q.kind == DPR_PART_BRICK)
+                for (int c = 0; c < 3; ++c)
+                    if (q.gdims[c] != p.gdims[c] || q.origin[c] != p.origin[c] || q.spacing[c] != p.spacing[c])
+                        return fail(DPR_ERR_INVALID_ARG, "bricks of one world must share gdims/origin/spacing");
+        int nb = 0;
+        for (auto &q : d->parts) nb += q.kind == DPR_PART_BRICK;
+        if (nb >= MAX_BRICKS) return fail(DPR_ERR_INVALID_ARG, "too many bricks on one rank");
+        p.tf_lo = part->tf_lo; p.tf_hi = part->tf_hi; p.dscale = part->density_scale;
+        size_t nvox = (size_t)(p.hi[0] - p.lo[0] + 1) * (p.hi[1] - p.lo[1] + 1) * (p.hi[2] - p.lo[2] + 1);
+        RET(copy_in(d, p.vox, part->voxels, sizeof(float) * nvox, part->memory));
+        RET(copy_in(d, p.tf, part->tf, sizeof(float) * 4 * 256, part->memory));
+    }
+    d->parts.push_back(p);
+    d->world_ready = false;
+    return DPR_OK;
+}
+
+int dpr_clear_parts(dpr_device dev) {
+    if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
+    Dev *d = &dev->d;
+    for (auto &p : d->parts) { dfree(d, p.verts); dfree(d, p.idx); dfree(d, p.spheres); dfree(d, p.vox); dfree(d, p.tf); dfree(d, p.mc); }
+    d->parts.clear();
+    d->world_ready = false;
+    return DPR_OK;
+}
+
+int dpr_commit_world(dpr_device dev) {
+    if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
+    Dev *d = &dev->d;
+    CK(cudaSetDevice(d->cuda_dev));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, d->stream);
+    int rc = build_world(d);
+    cudaEventRecord(e1, d->stream);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    d->ms_build = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rc;
+}
+
+int dpr_get_world_bounds(dpr_device dev, float lohi_host[6]) {
+    if (!valid_dev(dev) || !lohi_host) return fail(DPR_ERR_INVALID_ARG, "null argument");
+    Dev *d = &dev->d;
+    if (!d->world_ready) return fail(DPR_ERR_STATE, "dpr_commit_world has not been called");
+    std::vector<Dev *> L;
+    if (d->group) {
+        for (Dev *x : d->group->devs) if (!x || !x->world_ready) return fail(DPR_ERR_STATE, "group member world not ready");
+        L = d->group->devs;
+    } else {
+        L = {d};
+    }
+    std::vector<const void *> sends;
+    for (Dev *x : L) sends.push_back(x->box);
+    std::vector<std::vector<char>> out;
+    RET(allgather_host(L, sends, sizeof(float) * 6, out));
+    const float *b = reinterpret_cast<const float *>(out[0].data());
+    for (int c = 0; c < 3; ++c) { lohi_host[c] = INFINITY; lohi_host[3 + c] = -INFINITY; }
+    for (int r = 0; r < d->nranks; ++r)
+        for (int c = 0; c < 3; ++c) {
+            lohi_host[c] = fminf(lohi_host[c], b[6 * r + c]);
+            lohi_host[3 + c] = fmaxf(lohi_host[3 + c], b[6 * r + 3 + c]);
+        }
+    return DPR_OK;
+}
+
+int dpr_set_camera(dpr_device dev, const dpr_camera_basis *cam) {
+    if (!valid_dev(dev) || !cam) return fail(DPR_ERR_INVALID_ARG, "null argument");
+    dev->d.cam = *cam;
+    dev->d.cam_set = true;
+    return DPR_OK;
+}
+
+int dpr_set_frame(dpr_device dev, const dpr_frame_desc *fr) {
+    if (!valid_dev(dev) || !fr) return fail(DPR_ERR_INVALID_ARG, "null argument");
+    if (fr->W <= 0 || fr->H <= 0 || fr->spp <= 0 || fr->spp > 65535 || fr->spp_batch <= 0 || fr->max_depth <= 0 ||
+        fr->max_depth > 200 || fr->ao_k < 0 || fr->ao_k > 30)
+        return fail(DPR_ERR_INVALID_ARG, "bad frame parameters");
+    dev->d.fr = *fr;
+    if (dev->d.fr.spp_batch > fr->spp) dev->d.fr.spp_batch = fr->spp;
+    dev->d.fr_set = true;
+    return DPR_OK;
+}
+
+int dpr_render_frame(dpr_device dev) {
+    if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
+    Dev *d = &dev->d;
+    if (d->group) return fail(DPR_ERR_STATE, "loopback devices render with dpr_render_frame_group");
+    CK(cudaSetDevice(d->cuda_dev));
+    std::vector<Dev *> L = {d};
+    return render_group(L);
+}
+
+int dpr_render_frame_group(dpr_device *devs, int n) {
+    if (!devs || n < 1) return fail(DPR_ERR_INVALID_ARG, "bad group");
+    std::vector<Dev *> L;
+    for (int i = 0; i < n; ++i) {
+        if (!devs[i] || !devs[i]->d.group || devs[i]->d.rank != i || devs[i]->d.nranks != n)
+            return fail(DPR_ERR_INVALID_ARG, "devices must be a full loopback group in rank order");
+        L.push_back(&devs[i]->d);
+    }
+    CK(cudaSetDevice(L[0]->cuda_dev));
+    return render_group(L);
+}
+
+int dpr_frame_ready(dpr_device dev, int wait) {
+    (void)wait;
+    if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
+    return dev->d.frame_done;
+}
+
+int dpr_map_frame(dpr_device dev, const float **rgba, int *w, int *h, int *undefined) {
+    if (!valid_dev(dev) || !rgba || !w || !h || !undefined) return fail(DPR_ERR_INVALID_ARG, "null argument");
+    Dev *d = &dev->d;
+    if (!d->frame_done) return fail(DPR_ERR_STATE, "no frame rendered");
+    if (d->rank != 0) {
+        *rgba = nullptr; *w = 0; *h = 0; *undefined = 1;
+        return DPR_OK;
+    }
+    *rgba = P<float>(d->b_fb_out);
+    *w = d->mapped_w;
+    *h = d->mapped_h;
+    *undefined = 0;
+    return DPR_OK;
+}
+
+int dpr_get_debug(dpr_device dev, const uint32_t **events, const uint32_t **occl) {
+    if (!valid_dev(dev) || !events || !occl) return fail(DPR_ERR_INVALID_ARG, "null argument");
+    Dev *d = &dev->d;
+    if (d->rank != 0 || !d->dumps_valid) return fail(DPR_ERR_STATE, "no debug dumps (rank 0, DPR_FLAG_DEBUG_DUMPS)");
+    *events = P<uint32_t>(d->b_events);
+    *occl = P<uint32_t>(d->b_occl);
+    return DPR_OK;
+}
+
+int dpr_get_stats(dpr_device dev, dpr_stats *out) {
+    if (!valid_dev(dev) || !out) return fail(DPR_ERR_INVALID_ARG, "null argument");
+    *out = dev->d.stats;
+    out->ms_build = dev->d.ms_build;
+    return DPR_OK;
+}
+
+const char *dpr_last_error(dpr_device dev) {
+    (void)dev;
+    return g_err.c_str();
+}
+
+int dpr_exchange_plan(int nranks, int rank, const int64_t *counts, int64_t capacity, int64_t *recv_offset,
+                      int64_t *total_in, int64_t *global_total) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || !counts || !recv_offset || !total_in || !global_total)
+        return fail(DPR_ERR_INVALID_ARG, "bad exchange plan arguments");
+    int64_t g = 0;
+    for (int i = 0; i < nranks * nranks; ++i) {
+        if (counts[i] < 0) return fail(DPR_ERR_INVALID_ARG, "negative count");
+        g += counts[i];
+    }
+    int64_t off = counts[(int64_t)rank * nranks + rank];
+    for (int src = 0; src < nranks; ++src) {
+        if (src == rank) { recv_offset[src] = 0; continue; }
+        recv_offset[src] = off;
+        off += counts[(int64_t)src * nranks + rank];
+    }
+    *total_in = off;
+    *global_total = g;
+    if (off > capacity) return fail(DPR_ERR_QUEUE_OVERFLOW, "receive exceeds queue capacity");
+    return DPR_OK;
+}
+
+}  // extern "C"

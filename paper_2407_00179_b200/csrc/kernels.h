@@ -1,0 +1,84 @@
+// kernels.h -- launch wrappers shared between the kernels and the host orchestration.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace dpr {
+
+// ---- lbvh.cu ---------------------------------------------------------------------------
+void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, uint32_t local0,
+                      float4 *prims, float4 *blo, float4 *bhi, cudaStream_t s);
+void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims,
+                         float4 *blo, float4 *bhi, cudaStream_t s);
+void launch_bounds(const float4 *blo, const float4 *bhi, int64_t n, int *bounds, int nsm,
+                   cudaStream_t s);
+void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
+                   uint64_t *keys, uint32_t *vals, cudaStream_t s);
+void launch_digit_hist_all(const uint64_t *keys, int64_t n, unsigned long long *hist, int nsm,
+                           cudaStream_t s);
+int64_t radix_tiles(int64_t n);
+void launch_radix_pass(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout,
+                       int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches);
+void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
+                   int *rhi, cudaStream_t s);
+void launch_refit(int64_t n, const int *left, const int *right, const int *parent,
+                  const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
+                  cudaStream_t s);
+void launch_emit(int64_t n, int leaf_max, const int *left, const int *right, const int *rlo,
+                 const int *rhi, const float4 *slo, const float4 *shi, const float4 *nlo,
+                 const float4 *nhi, BVHNode *out, cudaStream_t s);
+void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
+                         const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,
+                         cudaStream_t s);
+void launch_macrocells(const float *vox, int nx, int ny, int nz, int mcx, int mcy, int mcz,
+                       const float4 *tf, float tf_lo, float tf_hi, float dscale, uint8_t *mc,
+                       cudaStream_t s);
+
+// ---- trace.cu --------------------------------------------------------------------------
+struct FrameDev {
+    int W, H, P, spp, max_depth, ao_k;
+    float ao_radius;
+    float l[3], E[3], A[3], B[3];
+    float dt;
+    uint64_t seed;
+    uint32_t flags;
+    float cE[3], cL[3], cU[3], cV[3];  // camera basis (P2)
+};
+
+struct QueuesDev {
+    PathRec *path_in;
+    OcclRec *occl_in;
+    const uint32_t *in_count;   // [2]: path, occl
+    PathRec *path_out[DPR_MAX_RANKS];
+    OcclRec *occl_out[DPR_MAX_RANKS];
+    uint32_t *out_count;        // [2][nranks]
+    uint32_t path_cap, occl_cap;
+    uint32_t *fetch;            // [2] persistent-kernel fetch heads
+};
+
+struct StepArgs {
+    FrameDev F;
+    Routing R;
+    WorldDev W;
+    PartTable T;
+    QueuesDev Q;
+    float4 *fb;
+    uint32_t *events;  // debug dumps or nullptr
+    uint32_t *occl;
+    Counters *ctr;
+};
+
+void launch_gen_primary(const StepArgs &a, int s0, int nsamp, cudaStream_t s);
+void launch_trace_path(const StepArgs &a, int grid, cudaStream_t s);
+void launch_trace_occl(const StepArgs &a, int grid, cudaStream_t s);
+int trace_path_occupancy(int block);
+int trace_occl_occupancy(int block);
+constexpr int TRACE_BLOCK = 128;
+
+void launch_fb_accumulate(float4 *dst, const float4 *src, int64_t n, cudaStream_t s);
+void launch_u32_accumulate(uint32_t *dst, const uint32_t *src, int64_t n, cudaStream_t s);
+void launch_fb_normalize(float4 *out, const float4 *in, int64_t n, float spp, cudaStream_t s);
+
+}  // namespace dpr

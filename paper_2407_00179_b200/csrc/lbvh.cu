@@ -1,0 +1,467 @@
+// lbvh.cu -- per-rank acceleration-structure build on the GPU.
+//
+// The paper's method needs only "negligible pre-processing" (S2.2): each rank
+// builds a local structure over its own parts.  B200 has no RT cores, so the
+// structure and its traversal are hand-written: a linear BVH (Karras 2012, "Maximizing
+// parallelism in the construction of BVHs, octrees and k-d trees"):
+//   1. k_tri_prims / k_sphere_prims: prim records + exact AABBs (min/max, no rounding)
+//   2. k_bounds: rank box and centroid box (order-preserving integer atomics)
+//   3. k_morton: 63-bit Morton code of the centroid (21 bits per axis)
+//   4. LSD radix sort of (key u64, index u32), 8-bit digits, stable per-tile ranking with
+//      warp match + shared-memory digit prefix; passes whose digit is constant are skipped
+//   5. k_karras: internal nodes, duplicate keys broken by index
+//   6. k_refit: bottom-up boxes with arrival counters
+//   7. k_emit: 64-byte two-child nodes (Aila-Laine layout), small subtrees collapsed into
+//      leaves, child boxes padded outward (conservative traversal)
+//   8. k_macrocells: per 16^3 macrocell "alpha may be > 0" flags for exact empty-space
+//      skipping in bricks
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dpr {
+
+__device__ __forceinline__ int f2ord(float f) {
+    int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+// ---------------------------------------------------------------------------------------
+__global__ void k_tri_prims(const float *__restrict__ verts, const int32_t *__restrict__ idx,
+                            int64_t n, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int64_t i0 = idx[3 * t], i1 = idx[3 * t + 1], i2 = idx[3 * t + 2];
+    f3 v0 = mk(verts[3 * i0], verts[3 * i0 + 1], verts[3 * i0 + 2]);
+    f3 v1 = mk(verts[3 * i1], verts[3 * i1 + 1], verts[3 * i1 + 2]);
+    f3 v2 = mk(verts[3 * i2], verts[3 * i2 + 1], verts[3 * i2 + 2]);
+    f3 e1 = sub(v1, v0), e2 = sub(v2, v0);
+    int64_t g = local0 + t;
+    prims[3 * g + 0] = make_float4(v0.x, v0.y, v0.z, __uint_as_float((uint32_t)g));
+    prims[3 * g + 1] = make_float4(e1.x, e1.y, e1.z, 0.0f);
+    prims[3 * g + 2] = make_float4(e2.x, e2.y, e2.z, 0.0f);
+    blo[g] = make_float4(fminf(fminf(v0.x, v1.x), v2.x), fminf(fminf(v0.y, v1.y), v2.y),
+                         fminf(fminf(v0.z, v1.z), v2.z), 0.0f);
+    bhi[g] = make_float4(fmaxf(fmaxf(v0.x, v1.x), v2.x), fmaxf(fmaxf(v0.y, v1.y), v2.y),
+                         fmaxf(fmaxf(v0.z, v1.z), v2.z), 0.0f);
+}
+
+__global__ void k_sphere_prims(const float4 *__restrict__ sph, int64_t n, uint32_t local0,
+                               float4 *prims, float4 *blo, float4 *bhi) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    float4 s = sph[t];
+    int64_t g = local0 + t;
+    prims[3 * g + 0] = make_float4(s.x, s.y, s.z, __uint_as_float((uint32_t)g | SPHERE_BIT));
+    prims[3 * g + 1] = make_float4(s.w, 0.0f, 0.0f, 0.0f);
+    prims[3 * g + 2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    blo[g] = make_float4(s.x - s.w, s.y - s.w, s.z - s.w, 0.0f);
+    bhi[g] = make_float4(s.x + s.w, s.y + s.w, s.z + s.w, 0.0f);
+}
+
+// bounds[0..5] = box lo/hi (ordered ints), bounds[6..11] = centroid lo/hi
+__global__ void k_bounds(const float4 *__restrict__ blo, const float4 *__restrict__ bhi, int64_t n,
+                         int *bounds) {
+    int v[12];
+    for (int c = 0; c < 3; ++c) {
+        v[c] = 0x7fffffff; v[3 + c] = (int)0x80000000;
+        v[6 + c] = 0x7fffffff; v[9 + c] = (int)0x80000000;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float4 lo = blo[i], hi = bhi[i];
+        float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
+        for (int c = 0; c < 3; ++c) {
+            float cen = (l[c] + h[c]) * 0.5f;
+            v[c] = min(v[c], f2ord(l[c]));
+            v[3 + c] = max(v[3 + c], f2ord(h[c]));
+            v[6 + c] = min(v[6 + c], f2ord(cen));
+            v[9 + c] = max(v[9 + c], f2ord(cen));
+        }
+    }
+    for (int k = 0; k < 12; ++k) {
+        bool isMin = (k % 6) < 3;
+        for (int o = 16; o > 0; o >>= 1) {
+            int w = __shfl_xor_sync(0xffffffffu, v[k], o);
+            v[k] = isMin ? min(v[k], w) : max(v[k], w);
+        }
+    }
+    if ((threadIdx.x & 31) == 0)
+        for (int k = 0; k < 12; ++k) {
+            if ((k % 6) < 3) atomicMin(&bounds[k], v[k]);
+            else atomicMax(&bounds[k], v[k]);
+        }
+}
+
+__device__ __forceinline__ uint64_t expand21(uint64_t v) {
+    v &= 0x1fffffull;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+
+__global__ void k_morton(const float4 *__restrict__ blo, const float4 *__restrict__ bhi, int64_t n,
+                         const int *__restrict__ bounds, uint64_t *keys, uint32_t *vals) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 lo = blo[i], hi = bhi[i];
+    float c[3] = {(lo.x + hi.x) * 0.5f, (lo.y + hi.y) * 0.5f, (lo.z + hi.z) * 0.5f};
+    uint64_t q[3];
+    for (int a = 0; a < 3; ++a) {
+        float mn = ord2f(bounds[6 + a]), mx = ord2f(bounds[9 + a]);
+        float ext = mx - mn;
+        float x = ext > 0.0f ? (c[a] - mn) / ext * 2097152.0f : 0.0f;
+        x = fminf(fmaxf(x, 0.0f), 2097151.0f);
+        q[a] = (uint64_t)x;
+    }
+    keys[i] = (expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]);
+    vals[i] = (uint32_t)i;
+}
+
+// ---------------------------------------------------------------------------------------
+// LSD radix sort, 8-bit digits.
+// ---------------------------------------------------------------------------------------
+constexpr int RS_THREADS = 256;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
+
+// All 8 digit histograms in one read of the keys (to find constant-digit passes).
+__global__ void k_digit_hist_all(const uint64_t *__restrict__ keys, int64_t n,
+                                 unsigned long long *hist /*8*256*/) {
+    __shared__ unsigned int h[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        for (int p = 0; p < 8; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
+        if ((&h[0][0])[i]) atomicAdd(&hist[i], (unsigned long long)(&h[0][0])[i]);
+}
+
+__global__ void k_tile_hist(const uint64_t *__restrict__ keys, int64_t n, int shift,
+                            uint32_t *tile_hist, int ntiles) {
+    __shared__ unsigned int h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        int64_t i = base + j * RS_THREADS + threadIdx.x;
+        if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    tile_hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Exclusive scan of m uint32 values in one block (m = 256 * ntiles).
+__global__ void k_scan_single(uint32_t *data, int64_t m) {
+    __shared__ uint32_t part[1024];
+    int64_t chunk = (m + blockDim.x - 1) / blockDim.x;
+    int64_t b = threadIdx.x * chunk, e = min(m, b + chunk);
+    uint32_t s = 0;
+    for (int64_t i = b; i < e; ++i) s += data[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+        uint32_t v = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+    for (int64_t i = b; i < e; ++i) {
+        uint32_t v = data[i];
+        data[i] = run;
+        run += v;
+    }
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+k_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *kout,
+          uint32_t *vout, int64_t n, int shift, const uint32_t *__restrict__ tile_off, int ntiles) {
+    __shared__ uint32_t wcnt[RS_THREADS / 32][256];
+    __shared__ uint32_t run[256];
+    __shared__ uint32_t goff[256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    goff[threadIdx.x] = tile_off[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+    run[threadIdx.x] = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        for (int w = 0; w < RS_THREADS / 32; ++w) wcnt[w][threadIdx.x] = 0;
+        __syncthreads();
+        int64_t i = base + j * RS_THREADS + threadIdx.x;
+        bool valid = i < n;
+        uint64_t k = valid ? kin[i] : 0;
+        uint32_t v = valid ? vin[i] : 0;
+        int d = valid ? (int)((k >> shift) & 255) : 256 + lane;  // invalid lanes: unique groups
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        uint32_t rank = __popc(peers & lt);
+        if (valid && rank == 0) wcnt[warp][d] = __popc(peers);
+        __syncthreads();
+        {  // thread = digit: prefix over warps
+            uint32_t r = run[threadIdx.x];
+            for (int w = 0; w < RS_THREADS / 32; ++w) {
+                uint32_t c = wcnt[w][threadIdx.x];
+                wcnt[w][threadIdx.x] = r;
+                r += c;
+            }
+            run[threadIdx.x] = r;
+        }
+        __syncthreads();
+        if (valid) {
+            uint32_t pos = goff[d] + wcnt[warp][d] + rank;
+            kout[pos] = k;
+            vout[pos] = v;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Karras 2012 hierarchy.  Internal nodes 0..n-2; child c < n-1 -> internal, else leaf
+// (c-(n-1)) in sorted order.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int delta(const uint64_t *keys, int64_t n, int64_t i, int64_t j) {
+    if (j < 0 || j >= n) return -1;
+    uint64_t a = keys[i], b = keys[j];
+    if (a == b) return 64 + __clz((uint32_t)(i ^ j));
+    return __clzll(a ^ b);
+}
+
+__global__ void k_karras(const uint64_t *__restrict__ keys, int64_t n, int *left, int *right,
+                         int *parent, int *rlo, int *rhi) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    int d = delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1) >= 0 ? 1 : -1;
+    int dmin = delta(keys, n, i, i - d);
+    int64_t lmax = 2;
+    while (delta(keys, n, i, i + lmax * d) > dmin) lmax *= 2;
+    int64_t l = 0;
+    for (int64_t t = lmax / 2; t >= 1; t /= 2)
+        if (delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+    int64_t j = i + l * d;
+    int dnode = delta(keys, n, i, j);
+    int64_t s = 0;
+    for (int64_t div = 2;; div *= 2) {
+        int64_t t = (l + div - 1) / div;
+        if (delta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+        if (t <= 1) break;
+    }
+    int64_t g = i + s * d + min(d, 0);
+    int64_t lo = min(i, j), hi = max(i, j);
+    int lc = (lo == g) ? (int)(n - 1 + g) : (int)g;
+    int rc = (hi == g + 1) ? (int)(n - 1 + g + 1) : (int)(g + 1);
+    left[i] = lc;
+    right[i] = rc;
+    parent[lc] = (int)i;
+    parent[rc] = (int)i;
+    rlo[i] = (int)lo;
+    rhi[i] = (int)hi;
+}
+
+__global__ void k_refit(int64_t n, const int *__restrict__ left, const int *__restrict__ right,
+                        const int *__restrict__ parent, const float4 *__restrict__ slo,
+                        const float4 *__restrict__ shi, float4 *nlo, float4 *nhi, int *arrive) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int node = parent[n - 1 + j];
+    while (true) {
+        __threadfence();
+        if (atomicAdd(&arrive[node], 1) == 0) return;
+        __threadfence();
+        int c[2] = {left[node], right[node]};
+        float4 lo = make_float4(0, 0, 0, 0), hi = lo;
+        for (int k = 0; k < 2; ++k) {
+            float4 a, b;
+            if (c[k] >= n - 1) { a = slo[c[k] - (n - 1)]; b = shi[c[k] - (n - 1)]; }
+            else { a = __ldcg(nlo + c[k]); b = __ldcg(nhi + c[k]); }
+            if (k == 0) { lo = a; hi = b; }
+            else {
+                lo = make_float4(fminf(lo.x, a.x), fminf(lo.y, a.y), fminf(lo.z, a.z), 0.0f);
+                hi = make_float4(fmaxf(hi.x, b.x), fmaxf(hi.y, b.y), fmaxf(hi.z, b.z), 0.0f);
+            }
+        }
+        __stcg(nlo + node, lo);
+        __stcg(nhi + node, hi);
+        if (node == 0) return;
+        node = parent[node];
+    }
+}
+
+// Outward padding: |x| + 4 scaled by 2^-18 (>= 1.5e-5 absolute).  Covers the FMA box test
+// error and MT hit-point rounding.
+__device__ __forceinline__ float pad_lo(float x) { return x - (fabsf(x) + 4.0f) * 0x1p-18f; }
+__device__ __forceinline__ float pad_hi(float x) { return x + (fabsf(x) + 4.0f) * 0x1p-18f; }
+
+__global__ void k_emit(int64_t n, int leaf_max, const int *__restrict__ left,
+                       const int *__restrict__ right, const int *__restrict__ rlo,
+                       const int *__restrict__ rhi, const float4 *__restrict__ slo,
+                       const float4 *__restrict__ shi, const float4 *__restrict__ nlo,
+                       const float4 *__restrict__ nhi, BVHNode *out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    int c[2] = {left[i], right[i]};
+    float4 lo[2], hi[2];
+    int ref[2], cnt[2];
+    for (int k = 0; k < 2; ++k) {
+        if (c[k] >= n - 1) {
+            int64_t j = c[k] - (n - 1);
+            lo[k] = slo[j]; hi[k] = shi[j];
+            ref[k] = ~(int)j; cnt[k] = 1;
+        } else {
+            lo[k] = nlo[c[k]]; hi[k] = nhi[c[k]];
+            int size = rhi[c[k]] - rlo[c[k]] + 1;
+            if (size <= leaf_max) { ref[k] = ~rlo[c[k]]; cnt[k] = size; }
+            else { ref[k] = c[k]; cnt[k] = 0; }
+        }
+    }
+    BVHNode nd;
+    nd.n0 = make_float4(pad_lo(lo[0].x), pad_hi(hi[0].x), pad_lo(lo[0].y), pad_hi(hi[0].y));
+    nd.n1 = make_float4(pad_lo(lo[1].x), pad_hi(hi[1].x), pad_lo(lo[1].y), pad_hi(hi[1].y));
+    nd.n2 = make_float4(pad_lo(lo[0].z), pad_hi(hi[0].z), pad_lo(lo[1].z), pad_hi(hi[1].z));
+    nd.n3 = make_int4(ref[0], ref[1], cnt[0], cnt[1]);
+    out[i] = nd;
+}
+
+// n == 1: a root with one leaf child and one empty child.
+__global__ void k_emit_single(const float4 *slo, const float4 *shi, BVHNode *out) {
+    float4 lo = slo[0], hi = shi[0];
+    const float inf = __int_as_float(0x7f800000);
+    BVHNode nd;
+    nd.n0 = make_float4(pad_lo(lo.x), pad_hi(hi.x), pad_lo(lo.y), pad_hi(hi.y));
+    nd.n1 = make_float4(inf, -inf, inf, -inf);
+    nd.n2 = make_float4(pad_lo(lo.z), pad_hi(hi.z), inf, -inf);
+    nd.n3 = make_int4(~0, ~0, 1, 0);
+    out[0] = nd;
+}
+
+__global__ void k_gather_prims(const float4 *__restrict__ in, const uint32_t *__restrict__ perm,
+                               int64_t n, float4 *out, const float4 *__restrict__ blo,
+                               const float4 *__restrict__ bhi, float4 *slo, float4 *shi) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t s = perm[i];
+    out[3 * i + 0] = in[3 * (int64_t)s + 0];
+    out[3 * i + 1] = in[3 * (int64_t)s + 1];
+    out[3 * i + 2] = in[3 * (int64_t)s + 2];
+    slo[i] = blo[s];
+    shi[i] = bhi[s];
+}
+
+// ---------------------------------------------------------------------------------------
+// Macrocells: one block per 16^3 macrocell.  A sample owned by the brick with
+// floor(g) in cell c reads voxels c..c+1; a macrocell covers cells [m*16, m*16+16) so it
+// reads voxels [m*16, m*16+16] (clamped to the stored range).  Active iff some TF entry in
+// the index range that the value range maps to (widened by one entry on each side) has
+// alpha > 0 -- exact skipping (u >= 0 is never < 0).
+// ---------------------------------------------------------------------------------------
+__global__ void k_macrocells(const float *__restrict__ vox, int nx, int ny, int nz, int mcx,
+                             int mcy, int mcz, const float4 *__restrict__ tf, float tf_lo,
+                             float tf_hi, float dscale, uint8_t *mc) {
+    int m = blockIdx.x;
+    int mx = m % mcx, my = (m / mcx) % mcy, mz = m / (mcx * mcy);
+    int x0 = mx * MC_SIZE, y0 = my * MC_SIZE, z0 = mz * MC_SIZE;
+    int x1 = min(x0 + MC_SIZE, nx - 1), y1 = min(y0 + MC_SIZE, ny - 1), z1 = min(z0 + MC_SIZE, nz - 1);
+    int sx = x1 - x0 + 1, sy = y1 - y0 + 1, sz = z1 - z0 + 1;
+    float vmin = __int_as_float(0x7f800000), vmax = -vmin;
+    for (int t = threadIdx.x; t < sx * sy * sz; t += blockDim.x) {
+        int x = x0 + t % sx, y = y0 + (t / sx) % sy, z = z0 + t / (sx * sy);
+        float v = vox[(int64_t)x + (int64_t)nx * ((int64_t)y + (int64_t)ny * z)];
+        vmin = fminf(vmin, v);
+        vmax = fmaxf(vmax, v);
+    }
+    __shared__ float smin[32], smax[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = vmin; smax[threadIdx.x >> 5] = vmax; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { vmin = fminf(vmin, smin[w]); vmax = fmaxf(vmax, smax[w]); }
+        float xa = fminf(fmaxf((vmin - tf_lo) / (tf_hi - tf_lo), 0.0f), 1.0f) * 255.0f;
+        float xb = fminf(fmaxf((vmax - tf_lo) / (tf_hi - tf_lo), 0.0f), 1.0f) * 255.0f;
+        int ja = max((int)floorf(xa) - 1, 0), jb = min((int)floorf(xb) + 2, 255);
+        bool active = false;
+        for (int j = ja; j <= jb; ++j) active |= tf[j].w * dscale > 0.0f || tf[j].w != 0.0f;
+        if (!(vmin == vmin) || !(vmax == vmax)) active = true;  // NaN voxels: never skip
+        mc[m] = active ? 1 : 0;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Host-side launchers.
+// ---------------------------------------------------------------------------------------
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, uint32_t local0,
+                      float4 *prims, float4 *blo, float4 *bhi, cudaStream_t s) {
+    if (n > 0) k_tri_prims<<<nblk(n, 256), 256, 0, s>>>(verts, idx, n, local0, prims, blo, bhi);
+}
+void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims,
+                         float4 *blo, float4 *bhi, cudaStream_t s) {
+    if (n > 0) k_sphere_prims<<<nblk(n, 256), 256, 0, s>>>(sph, n, local0, prims, blo, bhi);
+}
+void launch_bounds(const float4 *blo, const float4 *bhi, int64_t n, int *bounds, int nsm,
+                   cudaStream_t s) {
+    unsigned g = (unsigned)std::min<int64_t>(nblk(n, 256), (int64_t)nsm * 8);
+    if (g == 0) g = 1;
+    k_bounds<<<g, 256, 0, s>>>(blo, bhi, n, bounds);
+}
+void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
+                   uint64_t *keys, uint32_t *vals, cudaStream_t s) {
+    if (n > 0) k_morton<<<nblk(n, 256), 256, 0, s>>>(blo, bhi, n, bounds, keys, vals);
+}
+void launch_digit_hist_all(const uint64_t *keys, int64_t n, unsigned long long *hist, int nsm,
+                           cudaStream_t s) {
+    unsigned g = (unsigned)std::min<int64_t>(nblk(n, 256), (int64_t)nsm * 4);
+    if (g == 0) g = 1;
+    k_digit_hist_all<<<g, 256, 0, s>>>(keys, n, hist);
+}
+int64_t radix_tiles(int64_t n) { return (n + RS_TILE - 1) / RS_TILE; }
+void launch_radix_pass(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout,
+                       int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches) {
+    int ntiles = (int)radix_tiles(n);
+    k_tile_hist<<<ntiles, RS_THREADS, 0, s>>>(kin, n, shift, tile_hist, ntiles);
+    k_scan_single<<<1, 1024, 0, s>>>(tile_hist, (int64_t)256 * ntiles);
+    k_scatter<<<ntiles, RS_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, tile_hist, ntiles);
+    *launches += 3;
+}
+void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
+                   int *rhi, cudaStream_t s) {
+    if (n > 1) k_karras<<<nblk(n - 1, 256), 256, 0, s>>>(keys, n, left, right, parent, rlo, rhi);
+}
+void launch_refit(int64_t n, const int *left, const int *right, const int *parent,
+                  const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
+                  cudaStream_t s) {
+    if (n > 1) k_refit<<<nblk(n, 256), 256, 0, s>>>(n, left, right, parent, slo, shi, nlo, nhi, arrive);
+}
+void launch_emit(int64_t n, int leaf_max, const int *left, const int *right, const int *rlo,
+                 const int *rhi, const float4 *slo, const float4 *shi, const float4 *nlo,
+                 const float4 *nhi, BVHNode *out, cudaStream_t s) {
+    if (n > 1) k_emit<<<nblk(n - 1, 256), 256, 0, s>>>(n, leaf_max, left, right, rlo, rhi, slo, shi, nlo, nhi, out);
+    else if (n == 1) k_emit_single<<<1, 1, 0, s>>>(slo, shi, out);
+}
+void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
+                         const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,
+                         cudaStream_t s) {
+    if (n > 0) k_gather_prims<<<nblk(n, 256), 256, 0, s>>>(in, perm, n, out, blo, bhi, slo, shi);
+}
+void launch_macrocells(const float *vox, int nx, int ny, int nz, int mcx, int mcy, int mcz,
+                       const float4 *tf, float tf_lo, float tf_hi, float dscale, uint8_t *mc,
+                       cudaStream_t s) {
+    int n = mcx * mcy * mcz;
+    if (n > 0) k_macrocells<<<n, 128, 0, s>>>(vox, nx, ny, nz, mcx, mcy, mcz, tf, tf_lo, tf_hi, dscale, mc);
+}
+
+}  // namespace dpr

@@ -1,0 +1,596 @@
+// trace.cu -- the wavefront kernels of one lock-step step.
+//
+//   k_gen_primary   (a2) every rank generates the FULL primary wave-front of the batch and
+//                   keeps the rays whose first candidate rank is itself -- "generate full
+//                   wave-fronts on all ranks ... discard some of the rays ... by testing
+//                   them for visibility against their geometry" (S2.2).
+//   k_trace_path    (a3+a4+a6 fused) closest hit against the rank's LBVH + bricks, then in
+//                   the same thread: forward to the next candidate rank (P8) or resolve,
+//                   shade (P6) and spawn shadow/AO/bounce rays into per-destination queues.
+//   k_trace_occl    (a3+a4 fused) any-hit; occluded rays are dropped, unoccluded ones are
+//                   forwarded or resolved into the framebuffer.
+// Queues are appended with warp-aggregated atomics (__match_any_sync per destination).
+// Kernels are persistent: grid = resident CTAs, each warp fetches 32 rays at a time from a
+// device-side head, so launch shape never depends on host-known counts.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dpr {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int STACK_SIZE = 96;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ void fb_add(float4 *p, float4 v) {
+#if __CUDA_ARCH__ >= 900
+    atomicAdd(p, v);
+#else
+    atomicAdd(&p->x, v.x); atomicAdd(&p->y, v.y); atomicAdd(&p->z, v.z); atomicAdd(&p->w, v.w);
+#endif
+}
+
+// Warp-aggregated queue append; all 32 lanes must call.  Returns the slot or ~0u.
+// S_row (may be null) receives the per-destination forward counts (dest != self).
+__device__ __forceinline__ uint32_t warp_append(bool want, int dest, uint32_t *counts, uint32_t cap,
+                                                unsigned *overflow, unsigned long long *S_row,
+                                                int self) {
+    unsigned act = __ballot_sync(FULL, want);
+    uint32_t pos = 0xffffffffu;
+    if (want) {
+        unsigned peers = __match_any_sync(act, dest);
+        int leader = __ffs(peers) - 1;
+        int lane = threadIdx.x & 31;
+        uint32_t base = 0;
+        if (lane == leader) {
+            base = atomicAdd(&counts[dest], (uint32_t)__popc(peers));
+            if (S_row && dest != self) atomicAdd(&S_row[dest], (unsigned long long)__popc(peers));
+        }
+        base = __shfl_sync(peers, base, leader);
+        pos = base + __popc(peers & lanemask_lt());
+        if (pos >= cap) {
+            atomicOr(overflow, 1u);
+            pos = 0xffffffffu;
+        }
+    }
+    return pos;
+}
+
+// Warp-aggregated counter add keyed by an int (all lanes call).
+__device__ __forceinline__ void warp_count(bool want, int key, unsigned long long *base) {
+    unsigned act = __ballot_sync(FULL, want);
+    if (want) {
+        unsigned peers = __match_any_sync(act, key);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&base[key], (unsigned long long)__popc(peers));
+    }
+}
+
+__device__ __forceinline__ void flush(unsigned long long *dst, uint32_t v) {
+    v = __reduce_add_sync(FULL, v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, (unsigned long long)v);
+}
+
+// ---------------------------------------------------------------------------------------
+// Traversal of the rank's LBVH (closest or any hit).  Equals brute force over the rank's
+// prims with the P9 rule; box tests are conservative (padded boxes, FMA slabs).
+// ---------------------------------------------------------------------------------------
+struct Hit {
+    float t;
+    uint32_t id;  // global id / VOL_BIT|i / NO_HIT
+    int prim;     // local (sorted) prim index of a hit found at THIS rank, or -1
+};
+
+struct TraceCounters { uint32_t nodes, tris, sphs, vols; };
+
+template <bool ANY>
+__device__ __forceinline__ bool traverse(const WorldDev &W, f3 o, f3 d, float tmax, Hit &h,
+                                         TraceCounters &tc, unsigned *overflow) {
+    if (W.nprims == 0) return false;
+    const float tiny = 1e-20f;
+    f3 id3 = mk(1.0f / (fabsf(d.x) > tiny ? d.x : copysignf(tiny, d.x)),
+                1.0f / (fabsf(d.y) > tiny ? d.y : copysignf(tiny, d.y)),
+                1.0f / (fabsf(d.z) > tiny ? d.z : copysignf(tiny, d.z)));
+    f3 oid = mk(o.x * id3.x, o.y * id3.y, o.z * id3.z);
+    int stack[STACK_SIZE];
+    int sp = 0;
+    int node = 0;
+    for (;;) {
+        const BVHNode *nd = W.nodes + node;
+        float4 n0 = __ldg(&nd->n0), n1 = __ldg(&nd->n1), n2 = __ldg(&nd->n2);
+        int4 n3 = __ldg(&nd->n3);
+        tc.nodes++;
+        float bound = ANY ? tmax : h.t;
+        float a0 = __fmaf_rn(n0.x, id3.x, -oid.x), a1 = __fmaf_rn(n0.y, id3.x, -oid.x);
+        float a2 = __fmaf_rn(n0.z, id3.y, -oid.y), a3 = __fmaf_rn(n0.w, id3.y, -oid.y);
+        float a4 = __fmaf_rn(n2.x, id3.z, -oid.z), a5 = __fmaf_rn(n2.y, id3.z, -oid.z);
+        float tn0 = fmaxf(fmaxf(fminf(a0, a1), fminf(a2, a3)), fmaxf(fminf(a4, a5), 0.0f));
+        float tf0 = fminf(fminf(fmaxf(a0, a1), fmaxf(a2, a3)), fminf(fmaxf(a4, a5), bound));
+        float b0 = __fmaf_rn(n1.x, id3.x, -oid.x), b1 = __fmaf_rn(n1.y, id3.x, -oid.x);
+        float b2 = __fmaf_rn(n1.z, id3.y, -oid.y), b3 = __fmaf_rn(n1.w, id3.y, -oid.y);
+        float b4 = __fmaf_rn(n2.z, id3.z, -oid.z), b5 = __fmaf_rn(n2.w, id3.z, -oid.z);
+        float tn1 = fmaxf(fmaxf(fminf(b0, b1), fminf(b2, b3)), fmaxf(fminf(b4, b5), 0.0f));
+        float tf1 = fminf(fminf(fmaxf(b0, b1), fmaxf(b2, b3)), fminf(fmaxf(b4, b5), bound));
+        bool hit[2] = {tn0 <= tf0, tn1 <= tf1};
+        int ref[2] = {n3.x, n3.y};
+        int cnt[2] = {n3.z, n3.w};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            if (!(hit[c] && ref[c] < 0)) continue;
+            hit[c] = false;
+            int start = ~ref[c];
+            for (int k = start; k < start + cnt[c]; ++k) {
+                const float4 *pr = W.prims + 3 * (int64_t)k;
+                float4 a = __ldg(pr);
+                uint32_t idw = __float_as_uint(a.w);
+                float t;
+                bool ok;
+                if (idw & SPHERE_BIT) {
+                    float4 b = __ldg(pr + 1);
+                    tc.sphs++;
+                    ok = sphere_hit(o, d, tmax, xyz(a), b.x, t);
+                } else {
+                    float4 b = __ldg(pr + 1), e = __ldg(pr + 2);
+                    tc.tris++;
+                    ok = tri_hit(o, d, tmax, xyz(a), xyz(b), xyz(e), t);
+                }
+                if (!ok) continue;
+                if (ANY) return true;
+                uint32_t gid = W.id_base + (idw & ~SPHERE_BIT);
+                if (t < h.t || (t == h.t && gid < h.id)) {
+                    h.t = t;
+                    h.id = gid;
+                    h.prim = k;
+                }
+            }
+        }
+        if (hit[0] && hit[1]) {
+            bool first0 = tn0 <= tn1;
+            if (sp < STACK_SIZE) stack[sp++] = first0 ? ref[1] : ref[0];
+            else atomicOr(overflow, 2u);
+            node = first0 ? ref[0] : ref[1];
+        } else if (hit[0]) {
+            node = ref[0];
+        } else if (hit[1]) {
+            node = ref[1];
+        } else {
+            if (sp == 0) break;
+            node = stack[--sp];
+        }
+    }
+    return false;
+}
+
+__device__ __forceinline__ f3 prim_normal(const WorldDev &W, int k, f3 o, f3 d, float t) {
+    const float4 *pr = W.prims + 3 * (int64_t)k;
+    float4 a = __ldg(pr), b = __ldg(pr + 1);
+    if (__float_as_uint(a.w) & SPHERE_BIT) return sphere_normal(o, d, t, xyz(a), b.x);
+    float4 e = __ldg(pr + 2);
+    return tri_normal(xyz(b), xyz(e), d);
+}
+
+// ---------------------------------------------------------------------------------------
+// P10 brick march (identical sample set and decisions to the oracle's per-rank march).
+// ---------------------------------------------------------------------------------------
+template <bool ANY>
+__device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float tmax, float bound,
+                                            float dt, uint64_t seed, uint32_t p, uint32_t s,
+                                            uint32_t depth, uint32_t purpose, uint32_t subhi,
+                                            float &t_out, uint32_t &i_out, f3 &rgb_out,
+                                            uint32_t &nsamples) {
+    float plo[3], phi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { plo[c] = B.box_lo[c] - B.h[c]; phi[c] = B.box_hi[c] + B.h[c]; }
+    float t0, t1;
+    if (!slab(plo, phi, o, d, tmax, t0, t1)) return false;
+    float a = floorf(t0 / dt - 0.5f);
+    float bb = ceilf(t1 / dt);
+    if (bb > 1.0e9f) bb = 1.0e9f;
+    int64_t i0 = (int64_t)a - 1;
+    if (i0 < 0) i0 = 0;
+    int64_t i1 = (int64_t)bb + 1;
+    const int nx = B.hi[0] - B.lo[0] + 1, ny = B.hi[1] - B.lo[1] + 1;
+    uint4 rr = make_uint4(0, 0, 0, 0);
+    int64_t rblk = -1;
+    for (int64_t i = i0; i <= i1; ++i) {
+        float ti = sample_t(i, dt);
+        if (!(ti < bound)) return false;
+        f3 pt = mk(o.x + ti * d.x, o.y + ti * d.y, o.z + ti * d.z);
+        f3 g = mk((pt.x - B.O[0]) / B.h[0], (pt.y - B.O[1]) / B.h[1], (pt.z - B.O[2]) / B.h[2]);
+        if (!(g.x >= (float)B.lo[0] && g.x < (float)B.hi[0] && g.y >= (float)B.lo[1] &&
+              g.y < (float)B.hi[1] && g.z >= (float)B.lo[2] && g.z < (float)B.hi[2]))
+            continue;
+        float fx0 = floorf(g.x), fy0 = floorf(g.y), fz0 = floorf(g.z);
+        int ix = (int)fx0 - B.lo[0], iy = (int)fy0 - B.lo[1], iz = (int)fz0 - B.lo[2];
+        if (!__ldg(B.mc + ((iz / MC_SIZE) * B.mc_dims[1] + iy / MC_SIZE) * B.mc_dims[0] + ix / MC_SIZE))
+            continue;  // exact skip: alpha == 0 for every sample in this macrocell
+        nsamples++;
+        float fx = g.x - fx0, fy = g.y - fy0, fz = g.z - fz0;
+        const float *v = B.vox + (int64_t)ix + (int64_t)nx * ((int64_t)iy + (int64_t)ny * iz);
+        const int64_t sy = nx, sz = (int64_t)nx * ny;
+        float v000 = __ldg(v), v100 = __ldg(v + 1), v010 = __ldg(v + sy), v110 = __ldg(v + sy + 1);
+        float v001 = __ldg(v + sz), v101 = __ldg(v + sz + 1), v011 = __ldg(v + sz + sy),
+              v111 = __ldg(v + sz + sy + 1);
+        float c00 = lerpf(v000, v100, fx), c10 = lerpf(v010, v110, fx);
+        float c01 = lerpf(v001, v101, fx), c11 = lerpf(v011, v111, fx);
+        float c0 = lerpf(c00, c10, fy), c1 = lerpf(c01, c11, fy);
+        float sv = lerpf(c0, c1, fz);
+        f3 rgb;
+        float alpha = tf_alpha_rgb(B, sv, ANY ? nullptr : &rgb);
+        if ((i >> 2) != rblk) {
+            rblk = i >> 2;
+            rr = rng4(seed, p, s, depth, purpose, subhi | (uint32_t)(i >> 2));
+        }
+        uint32_t x = (i & 3) == 0 ? rr.x : ((i & 3) == 1 ? rr.y : ((i & 3) == 2 ? rr.z : rr.w));
+        if (u01(x) < alpha) {
+            t_out = ti;
+            i_out = (uint32_t)i;
+            if (!ANY) rgb_out = rgb;
+            return true;
+        }
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------------------
+// a2: primary generation + visibility discard.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ StepArgs A, int s0,
+                                                     int nsamp) {
+    const FrameDev &F = A.F;
+    const int tiles_x = (F.W + 7) / 8, tiles_y = (F.H + 3) / 4;
+    const int64_t per_sample = (int64_t)tiles_x * tiles_y * 32;
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((t & ~31ll) >= per_sample * nsamp) return;  // whole warps only
+    uint32_t s = (uint32_t)(s0 + t / per_sample);
+    int64_t within = t % per_sample;
+    int64_t tile = within >> 5;
+    int li = (int)(within & 31);
+    int x = (int)(tile % tiles_x) * 8 + (li & 7);
+    int y = (int)(tile / tiles_x) * 4 + (li >> 3);
+    bool inimg = x < F.W && y < F.H;
+    const int self = A.R.self;
+    uint32_t p = (uint32_t)(y * F.W + x);
+    f3 o = mk(F.cE[0], F.cE[1], F.cE[2]), d = mk(0, 0, 0);
+    int first = -2;
+    if (inimg) {
+        float jx = 0.5f, jy = 0.5f;
+        if (!(F.flags & DPR_FLAG_JITTER_CENTER)) {
+            uint4 r = rng4(F.seed, p, s, 0, PUR_CAMERA, 0);
+            jx = u01(r.x);
+            jy = u01(r.y);
+        }
+        float sx = ((float)x + jx) / (float)F.W;
+        float sy = ((float)y + jy) / (float)F.H;
+        f3 q = mk((F.cL[0] + sx * F.cU[0]) + sy * F.cV[0], (F.cL[1] + sx * F.cU[1]) + sy * F.cV[1],
+                  (F.cL[2] + sx * F.cU[2]) + sy * F.cV[2]);
+        float len = sqrtf(dot(q, q));
+        d = mk(q.x / len, q.y / len, q.z / len);
+        first = first_candidate(A.R, o, d, __int_as_float(0x7f800000));
+    }
+    bool keep = first == self;
+    bool owner_keep = false;
+    if (inimg && first == -1) {
+        int owner = (int)(((int64_t)p * A.R.nranks) / F.P);
+        owner_keep = owner == self;
+    }
+    if (owner_keep) {
+        fb_add(A.fb + p, make_float4(F.B[0], F.B[1], F.B[2], 0.0f));
+        if (A.events) A.events[((int64_t)s * F.max_depth) * F.P + p] = 1u;
+    }
+    uint32_t gen = __popc(__ballot_sync(FULL, keep || owner_keep));
+    if ((threadIdx.x & 31) == 0 && gen) atomicAdd(&A.ctr->gen[K_PATH], (unsigned long long)gen);
+    uint32_t pos = warp_append(keep, self, A.Q.out_count, A.Q.path_cap, &A.ctr->overflow, nullptr, self);
+    if (keep && pos != 0xffffffffu) {
+        PathRec *r = A.Q.path_out[self] + pos;
+        r->a = make_float4(o.x, o.y, o.z, __int_as_float(0x7f800000));
+        r->b = make_float4(d.x, d.y, d.z, __uint_as_float(NO_HIT));
+        r->c = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(p));
+        r->e = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(s));
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// a3 + a4 + a6: path rays.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TRACE_BLOCK) k_trace_path(const __grid_constant__ StepArgs A) {
+    const FrameDev &F = A.F;
+    const int self = A.R.self, N = A.R.nranks;
+    const int lane = threadIdx.x & 31;
+    const float INF = __int_as_float(0x7f800000);
+    const uint32_t n_in = A.Q.in_count[0];
+    uint32_t *cnt_path = A.Q.out_count;
+    uint32_t *cnt_occl = A.Q.out_count + N;
+    TraceCounters tc = {0, 0, 0, 0};
+    uint32_t visits = 0, gen_p = 0, gen_s = 0, gen_a = 0, rin = 0, rout_p = 0, rout_o = 0;
+    const f3 L = mk(F.l[0], F.l[1], F.l[2]);
+    const int K = F.ao_k;
+    for (;;) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&A.Q.fetch[0], 32u);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= n_in) break;
+        uint32_t idx = base + lane;
+        bool active = idx < n_in;
+        PathRec r;
+        if (active) {
+            const PathRec *src = A.Q.path_in + idx;
+            r.a = __ldcs(&src->a); r.b = __ldcs(&src->b); r.c = __ldcs(&src->c); r.e = __ldcs(&src->e);
+            rin++;
+            visits++;
+        } else {
+            r.a = r.b = r.c = r.e = make_float4(0, 0, 0, 0);
+        }
+        f3 o = xyz(r.a), d = xyz(r.b);
+        Hit h = {r.a.w, __float_as_uint(r.b.w), -1};
+        f3 nrm = xyz(r.e);
+        const uint32_t p = __float_as_uint(r.c.w);
+        const uint32_t meta = __float_as_uint(r.e.w);
+        const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
+        int next = -1;
+        if (active) {
+            traverse<false>(A.W, o, d, INF, h, tc, &A.ctr->overflow);
+            if (h.prim >= 0) nrm = prim_normal(A.W, h.prim, o, d, h.t);
+            for (int b = 0; b < A.W.nbricks; ++b) {
+                float ti; uint32_t ii; f3 rgb;
+                if (march_brick<false>(A.W.bricks[b], o, d, INF, h.t, F.dt, F.seed, p, s, depth,
+                                       PUR_VOL_PATH, 0u, ti, ii, rgb, tc.vols)) {
+                    h.t = ti; h.id = VOL_BIT | ii; h.prim = -1; nrm = rgb;
+                }
+            }
+            next = next_candidate(A.R, self, o, d, INF, h.t);
+        }
+        // forward (P8: next candidate rank)
+        bool fwd = active && next >= 0;
+        uint32_t pos = warp_append(fwd, next, cnt_path, A.Q.path_cap, &A.ctr->overflow,
+                                   A.ctr->S[K_PATH], self);
+        if (fwd && pos != 0xffffffffu) {
+            PathRec *dst = A.Q.path_out[next] + pos;
+            dst->a = make_float4(o.x, o.y, o.z, h.t);
+            dst->b = make_float4(d.x, d.y, d.z, __uint_as_float(h.id));
+            dst->c = r.c;
+            dst->e = make_float4(nrm.x, nrm.y, nrm.z, r.e.w);
+            rout_p++;
+        }
+        // resolve here: events, background / coverage (P6, P13)
+        bool res = active && next < 0;
+        bool evt = res && h.id != NO_HIT;
+        bool vol = evt && (h.id & VOL_BIT);
+        if (res) {
+            if (A.events) {
+                uint32_t code = h.id == NO_HIT ? 1u : (vol ? h.id : 2u + h.id);
+                A.events[((int64_t)s * F.max_depth + depth) * F.P + p] = code;
+            }
+            if (!evt && depth == 0) fb_add(A.fb + p, make_float4(F.B[0], F.B[1], F.B[2], 0.0f));
+            if (evt && depth == 0) fb_add(A.fb + p, make_float4(0.0f, 0.0f, 0.0f, 1.0f));
+        }
+        f3 hp = mk(o.x + h.t * d.x, o.y + h.t * d.y, o.z + h.t * d.z);  // P5
+        f3 org = hp, br = mk(0, 0, 0);
+        float c = 0.0f;
+        if (evt) {
+            f3 beta = xyz(r.c);
+            if (!vol) {
+                f3 rho = part_albedo(A.T, h.id);
+                org = mk(hp.x + 1e-4f * nrm.x, hp.y + 1e-4f * nrm.y, hp.z + 1e-4f * nrm.z);
+                br = mul(beta, rho);
+                c = dot(nrm, L);
+            } else {
+                br = mul(beta, nrm);  // TF rgb travels in the normal slot
+            }
+        }
+        // children: slot 0 shadow, 1..K AO, K+1 bounce (warp-uniform loop)
+        for (int slot = 0; slot < K + 2; ++slot) {
+            bool has = false;
+            f3 cd = mk(0, 0, 0), w = mk(0, 0, 0);
+            float ctmax = INF;
+            if (evt) {
+                if (slot == 0) {
+                    if (!vol) {
+                        has = c > 0.0f;
+                        w = scale(mul(br, mk(F.E[0], F.E[1], F.E[2])), c);
+                    } else {
+                        has = true;
+                        w = mul(br, mk(F.E[0], F.E[1], F.E[2]));
+                    }
+                    cd = L;
+                } else if (slot <= K) {
+                    if (!vol) {
+                        has = true;
+                        cd = cosine_dir(nrm, F.seed, p, s, depth, PUR_AO, (uint32_t)(slot - 1) << 4);
+                        ctmax = F.ao_radius;
+                        w = scale(mul(br, mk(F.A[0], F.A[1], F.A[2])), 1.0f / (float)K);
+                    }
+                } else {
+                    has = (int)depth + 1 < F.max_depth;
+                    if (has) {
+                        cd = vol ? iso_dir(F.seed, p, s, depth)
+                                 : cosine_dir(nrm, F.seed, p, s, depth, PUR_BOUNCE, 0u);
+                        w = br;
+                    }
+                }
+            }
+            int first = has ? first_candidate(A.R, org, cd, ctmax) : -1;
+            bool app = has && first >= 0;
+            bool imm = has && first < 0;  // no candidate: resolves immediately here
+            const bool is_path = slot == K + 1;
+            if (has) {
+                if (is_path) gen_p++;
+                else if (slot == 0) gen_s++;
+                else gen_a++;
+            }
+            if (imm) {
+                if (is_path) {
+                    if (A.events) A.events[((int64_t)s * F.max_depth + depth + 1) * F.P + p] = 1u;
+                } else {
+                    fb_add(A.fb + p, make_float4(w.x, w.y, w.z, 0.0f));
+                    if (A.occl) atomicOr(A.occl + ((int64_t)s * F.max_depth + depth) * F.P + p, 1u << slot);
+                }
+            }
+            if (is_path) {
+                uint32_t q = warp_append(app, first, cnt_path, A.Q.path_cap, &A.ctr->overflow,
+                                         A.ctr->S[K_PATH], self);
+                if (app && q != 0xffffffffu) {
+                    PathRec *dst = A.Q.path_out[first] + q;
+                    dst->a = make_float4(org.x, org.y, org.z, INF);
+                    dst->b = make_float4(cd.x, cd.y, cd.z, __uint_as_float(NO_HIT));
+                    dst->c = make_float4(w.x, w.y, w.z, __uint_as_float(p));
+                    dst->e = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(s | ((depth + 1) << 16)));
+                    rout_p++;
+                }
+            } else {
+                uint32_t q = warp_append(app, first, cnt_occl, A.Q.occl_cap, &A.ctr->overflow,
+                                         A.ctr->S[slot == 0 ? K_SHADOW : K_AO], self);
+                if (app && q != 0xffffffffu) {
+                    OcclRec *dst = A.Q.occl_out[first] + q;
+                    dst->a = make_float4(org.x, org.y, org.z, ctmax);
+                    dst->b = make_float4(cd.x, cd.y, cd.z, __uint_as_float(p));
+                    dst->c = make_float4(w.x, w.y, w.z,
+                                         __uint_as_float(s | (depth << 16) | ((uint32_t)slot << 24)));
+                    rout_o++;
+                }
+            }
+        }
+    }
+    flush(&A.ctr->V[K_PATH], visits);
+    flush(&A.ctr->gen[K_PATH], gen_p);
+    flush(&A.ctr->gen[K_SHADOW], gen_s);
+    flush(&A.ctr->gen[K_AO], gen_a);
+    KernelCounters *kc = &A.ctr->kc[0];
+    flush(&kc->nodes, tc.nodes);
+    flush(&kc->tris, tc.tris);
+    flush(&kc->sphs, tc.sphs);
+    flush(&kc->vols, tc.vols);
+    flush(&kc->rin, rin);
+    flush(&kc->rout_path, rout_p);
+    flush(&kc->rout_occl, rout_o);
+}
+
+// ---------------------------------------------------------------------------------------
+// a3 + a4: occlusion (shadow / AO) rays.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TRACE_BLOCK) k_trace_occl(const __grid_constant__ StepArgs A) {
+    const FrameDev &F = A.F;
+    const int self = A.R.self, N = A.R.nranks;
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_in = A.Q.in_count[1];
+    uint32_t *cnt_occl = A.Q.out_count + N;
+    TraceCounters tc = {0, 0, 0, 0};
+    uint32_t v_s = 0, v_a = 0, rin = 0, rout = 0;
+    for (;;) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&A.Q.fetch[1], 32u);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= n_in) break;
+        uint32_t idx = base + lane;
+        bool active = idx < n_in;
+        OcclRec r;
+        if (active) {
+            const OcclRec *src = A.Q.occl_in + idx;
+            r.a = __ldcs(&src->a); r.b = __ldcs(&src->b); r.c = __ldcs(&src->c);
+            rin++;
+        } else {
+            r.a = r.b = r.c = make_float4(0, 0, 0, 0);
+        }
+        f3 o = xyz(r.a), d = xyz(r.b);
+        float tmax = r.a.w;
+        const uint32_t p = __float_as_uint(r.b.w);
+        const uint32_t meta = __float_as_uint(r.c.w);
+        const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
+        bool occluded = false;
+        int next = -1;
+        if (active) {
+            if (slot == 0) v_s++; else v_a++;
+            Hit h = {tmax, NO_HIT, -1};
+            occluded = traverse<true>(A.W, o, d, tmax, h, tc, &A.ctr->overflow);
+            for (int b = 0; b < A.W.nbricks && !occluded; ++b) {
+                float ti; uint32_t ii; f3 rgb;
+                occluded = march_brick<true>(A.W.bricks[b], o, d, tmax, tmax, F.dt, F.seed, p, s,
+                                             depth, slot == 0 ? PUR_VOL_SHADOW : PUR_VOL_AO,
+                                             slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
+            }
+            if (!occluded) next = next_candidate(A.R, self, o, d, tmax, tmax);
+        }
+        bool fwd = active && !occluded && next >= 0;
+        warp_count(fwd, (slot == 0 ? K_SHADOW : K_AO) * DPR_MAX_RANKS + next, &A.ctr->S[0][0]);
+        uint32_t pos = warp_append(fwd, next, cnt_occl, A.Q.occl_cap, &A.ctr->overflow, nullptr, self);
+        if (fwd && pos != 0xffffffffu) {
+            OcclRec *dst = A.Q.occl_out[next] + pos;
+            dst->a = r.a; dst->b = r.b; dst->c = r.c;
+            rout++;
+        }
+        if (active && !occluded && next < 0) {
+            fb_add(A.fb + p, make_float4(r.c.x, r.c.y, r.c.z, 0.0f));
+            if (A.occl) atomicOr(A.occl + ((int64_t)s * F.max_depth + depth) * F.P + p, 1u << slot);
+        }
+    }
+    flush(&A.ctr->V[K_SHADOW], v_s);
+    flush(&A.ctr->V[K_AO], v_a);
+    KernelCounters *kc = &A.ctr->kc[1];
+    flush(&kc->nodes, tc.nodes);
+    flush(&kc->tris, tc.tris);
+    flush(&kc->sphs, tc.sphs);
+    flush(&kc->vols, tc.vols);
+    flush(&kc->rin, rin);
+    flush(&kc->rout_occl, rout);
+}
+
+// ---------------------------------------------------------------------------------------
+// a7 helpers (the collective itself is ncclReduce, or loopback accumulation).
+// ---------------------------------------------------------------------------------------
+__global__ void k_fb_accumulate(float4 *dst, const float4 *__restrict__ src, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 a = dst[i], b = src[i];
+    dst[i] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__global__ void k_u32_accumulate(uint32_t *dst, const uint32_t *__restrict__ src, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] += src[i];
+}
+__global__ void k_fb_normalize(float4 *out, const float4 *__restrict__ in, int64_t n, float spp) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 a = in[i];
+    out[i] = make_float4(a.x / spp, a.y / spp, a.z / spp, a.w / spp);
+}
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void launch_gen_primary(const StepArgs &a, int s0, int nsamp, cudaStream_t s) {
+    int64_t per = (int64_t)((a.F.W + 7) / 8) * ((a.F.H + 3) / 4) * 32;
+    int64_t total = per * nsamp;
+    if (total > 0) k_gen_primary<<<nblk(total, 256), 256, 0, s>>>(a, s0, nsamp);
+}
+void launch_trace_path(const StepArgs &a, int grid, cudaStream_t s) {
+    k_trace_path<<<grid, TRACE_BLOCK, 0, s>>>(a);
+}
+void launch_trace_occl(const StepArgs &a, int grid, cudaStream_t s) {
+    k_trace_occl<<<grid, TRACE_BLOCK, 0, s>>>(a);
+}
+int trace_path_occupancy(int block) {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_trace_path, block, 0);
+    return n;
+}
+int trace_occl_occupancy(int block) {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_trace_occl, block, 0);
+    return n;
+}
+void launch_fb_accumulate(float4 *dst, const float4 *src, int64_t n, cudaStream_t s) {
+    if (n > 0) k_fb_accumulate<<<nblk(n, 256), 256, 0, s>>>(dst, src, n);
+}
+void launch_u32_accumulate(uint32_t *dst, const uint32_t *src, int64_t n, cudaStream_t s) {
+    if (n > 0) k_u32_accumulate<<<nblk(n, 256), 256, 0, s>>>(dst, src, n);
+}
+void launch_fb_normalize(float4 *out, const float4 *in, int64_t n, float spp, cudaStream_t s) {
+    if (n > 0) k_fb_normalize<<<nblk(n, 256), 256, 0, s>>>(out, in, n, spp);
+}
+
+}  // namespace dpr

@@ -1,0 +1,148 @@
+"""CUDA path (libdpr.so through the C ABI) vs the oracle, element by element on the same
+seeded inputs.  Bit-exact: hit/event codes, occlusion bits, rays generated, routing
+matrices S, visits V, step counts.  Pixels: max-abs 1e-3 / mean-abs 1e-4 per channel
+(north_star).  N>1 runs the SAME kernels as N virtual ranks on one GPU (loopback group)."""
+import numpy as np
+import pytest
+
+import dpr_inputs as di
+from tests.gpu_helpers import assert_parity, gpu_render, oracle_render
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config1_single_rank_union():
+    """configs[0] union world on one rank (one rank == plain renderer)."""
+    sc = di.config1()
+    parts = di.union_parts(sc.parts)
+    g = gpu_render(parts, 1, sc.camera, sc.frame)
+    o = oracle_render(parts, 1, sc.camera, sc.frame)
+    assert_parity(g, o)
+
+
+def test_config1_two_ranks():
+    """configs[0] as specified: two ranks split by x-half, ray forwarding with cross-rank
+    shadows; routing matrices bit-exact against the oracle's routing simulator."""
+    sc = di.config1()
+    g = gpu_render(sc.parts, 2, sc.camera, sc.frame)
+    o = oracle_render(sc.parts, 2, sc.camera, sc.frame)
+    assert_parity(g, o)
+    assert o.S[1].sum() > 0
+
+
+@pytest.mark.parametrize("case", ["H1", "H2", "H3"])
+def test_routing_hand_cases(case):
+    sc = di.routing_hand_case(case)
+    g = gpu_render(sc.parts, 2, sc.camera, sc.frame)
+    o = oracle_render(sc.parts, 2, sc.camera, sc.frame)
+    assert_parity(g, o)
+
+
+def _random_world(seed, nranks, ntri=300, nsph=80):
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-1, 1, size=(ntri, 1, 3))
+    v = (c + rng.uniform(-0.25, 0.25, size=(ntri, 3, 3))).astype(np.float32)
+    sp = np.concatenate([rng.uniform(-1, 1, (nsph, 3)), rng.uniform(0.05, 0.2, (nsph, 1))], 1).astype(np.float32)
+    tr = rng.integers(0, nranks, ntri)
+    srk = rng.integers(0, nranks, nsph)
+    parts = []
+    for r in range(nranks):
+        tv = v[tr == r].reshape(-1, 3)
+        if tv.shape[0]:
+            parts.append(di.Part(r, di.TRIS, albedo=(0.6, 0.5 + 0.03 * r, 0.4), verts=tv,
+                                 idx=np.arange(tv.shape[0], dtype=np.int32).reshape(-1, 3)))
+        s = sp[srk == r]
+        if s.shape[0]:
+            parts.append(di.Part(r, di.SPHERES, albedo=(0.3, 0.7, 0.2), spheres=s))
+    return parts
+
+
+@pytest.mark.parametrize("nranks,seed", [(1, 0), (2, 1), (3, 2), (4, 3), (8, 4)])
+def test_random_world_partitions(nranks, seed):
+    """Overlapping random partitions (not spatial), depth 3, AO + shadows + bounces."""
+    parts = _random_world(seed, nranks)
+    W = H = 48
+    cam = di.camera_basis((0.3, 0.8, -3.5), (0, 0, 0), (0, 1, 0), 45.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=3, spp_batch=2, max_depth=3, ao_k=2, ao_radius=0.6,
+                  light_dir=di.f32(di.normalize((0.4, 1, -0.3))), E=(1, 1, 1), A=(0.3, 0.3, 0.3),
+                  B=(0.1, 0.1, 0.2))
+    g = gpu_render(parts, nranks, cam, fr)
+    o = oracle_render(parts, nranks, cam, fr)
+    assert_parity(g, o)
+
+
+def _volume_scene(G, nbricks, nranks, alpha_max=0.6):
+    field = di.volume_field(G)
+    tf = di.default_tf(alpha_max=alpha_max, s0=0.2)
+    h = np.float32(2.0 / (G - 1))
+    parts = []
+    for r, (lo, hi) in enumerate(di.brick_boxes((G - 1,) * 3, nbricks)):
+        vox = field[lo[2]:hi[2] + 1, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1]
+        parts.append(di.Part(r % nranks, di.BRICK, gdims=(G,) * 3, origin=(-1, -1, -1),
+                             spacing=(float(h),) * 3, cell_lo=lo, cell_hi=hi,
+                             voxels=np.ascontiguousarray(vox), tf=tf))
+    return parts, float(h)
+
+
+@pytest.mark.parametrize("nbricks,nranks", [(1, 1), (4, 1), (2, 2), (4, 4), (8, 8)])
+def test_volume_bricks(nbricks, nranks):
+    """P10 stochastic DVR + binary volume shadows + isotropic bounce, bricks per rank."""
+    parts, h = _volume_scene(41, nbricks, nranks)
+    W = H = 40
+    cam = di.camera_basis((0.4, 0.7, 2.6), (0, 0, 0), (0, 1, 0), 40.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=2, spp_batch=2, max_depth=2, dt=h,
+                  light_dir=di.f32(di.normalize((1, 2, 1))), E=(1, 1, 1))
+    g = gpu_render(parts, nranks, cam, fr)
+    o = oracle_render(parts, nranks, cam, fr)
+    assert ((o.events & 0x80000000) != 0).sum() > 100
+    assert_parity(g, o)
+
+
+def test_mixed_surfaces_and_volume():
+    parts, h = _volume_scene(33, 2, 2, alpha_max=0.3)
+    parts.append(di.Part(1, di.SPHERES, albedo=(0.9, 0.1, 0.1), spheres=di.f32([[0.2, 0.1, 0.0, 0.4]])))
+    v, i = di.quad_tris([(-3, -1.2, -3), (3, -1.2, -3), (3, -1.2, 3), (-3, -1.2, 3)])
+    parts.append(di.Part(0, di.TRIS, albedo=(0.5, 0.5, 0.5), verts=v, idx=i))
+    W = H = 32
+    cam = di.camera_basis((0.3, 1.5, -3.0), (0, -0.5, 0), (0, 1, 0), 50.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=2, spp_batch=1, max_depth=2, ao_k=1, ao_radius=0.3, dt=h,
+                  light_dir=di.f32(di.normalize((0.2, 1, 0.1))), E=(1, 1, 1), A=(0.2, 0.2, 0.2))
+    g = gpu_render(parts, 2, cam, fr)
+    o = oracle_render(parts, 2, cam, fr)
+    assert_parity(g, o)
+
+
+@pytest.mark.parametrize("nranks", [1, 4])
+def test_config2_family_small(nranks):
+    """configs[1] family at a size the oracle finishes in seconds: ~180k-triangle gyroid,
+    spatially bisected over N ranks, 96x80 (ragged tiles), 4 spp in 2 batches, shadows +
+    AO (K=4, r=0.25, depth 1)."""
+    sc = di.config2(nranks=nranks, G=41, W=96, H=80, spp=4, spp_batch=2)
+    g = gpu_render(sc.parts, nranks, sc.camera, sc.frame)
+    o = oracle_render(sc.parts, nranks, sc.camera, sc.frame)
+    assert_parity(g, o)
+
+
+def test_empty_world_and_empty_rank():
+    """Degenerate cases: an empty world (background, coverage 0) and a rank with no parts."""
+    W = H = 16
+    cam = di.camera_basis((0, 0, -4), (0, 0, 0), (0, 1, 0), 40.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=2, max_depth=2, ao_k=2, B=(0.2, 0.4, 0.6))
+    g = gpu_render([], 1, cam, fr)
+    assert np.allclose(g[0], [0.2, 0.4, 0.6, 0.0], atol=1e-6)
+    parts = [di.Part(1, di.SPHERES, albedo=(1, 1, 1), spheres=di.f32([[0, 0, 0, 1]]))]
+    g = gpu_render(parts, 3, cam, fr)
+    o = oracle_render(parts, 3, cam, fr)
+    assert_parity(g, o)
+
+
+def test_single_triangle_and_single_sphere():
+    W = H = 16
+    cam = di.camera_basis((0, 0, -4), (0, 0, 0), (0, 1, 0), 40.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=1, max_depth=2, ao_k=1, light_dir=(0, 0, -1), E=(1, 1, 1), A=(0.2, 0.2, 0.2))
+    for part in [di.Part(0, di.TRIS, verts=di.f32([(-1, -1, 0), (1, -1, 0), (0, 1, 0)]),
+                         idx=np.array([[0, 1, 2]], np.int32)),
+                 di.Part(0, di.SPHERES, spheres=di.f32([[0, 0, 0, 0.7]]))]:
+        g = gpu_render([part], 1, cam, fr)
+        o = oracle_render([part], 1, cam, fr)
+        assert_parity(g, o)
