@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark: rays/sec and ms/frame of the data-parallel wavefront ray tracer (BASELINE.json
+metric) on BASELINE configs[1]: a ~10M-triangle gyroid mesh spatially partitioned over the N
+ranks, 1024x1024, 16 spp, shadows + ambient occlusion (K=4, r=0.25, depth 1).
+
+One step = one pass of the whole hot path: dpr_commit_world (GPU LBVH rebuild from the
+resident parts, row a1) + dpr_render_frame (rows a2-a7: primary generation, trace, route,
+shade/spawn, exchange, framebuffer reduce).  Timed with CUDA events on the library's stream,
+barrier + synchronize on both sides, max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  N>1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+--impl reference times the CPU oracle (oracle/, the definition the CUDA path is checked
+against) on a bounded pixel sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import dpr_inputs as di  # noqa: E402
+
+METRIC = "rays/sec and ms/frame (device-timed, max over ranks)"
+WORKLOAD = ("configs[1]: synthetic ~10M-triangle gyroid (marching tetrahedra G=301) spatially "
+            "partitioned over N ranks, 1024x1024, 16 spp, shadows+AO (K=4, r=0.25, depth 1)")
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profile_traffic():
+    """dram bytes per launch from the committed ncu --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return None
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        loaded = [x for x in sm if x > 0.5 * (mx or 1)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------
+def oracle_sample(scene, seconds: float = 12.0):
+    """Time the oracle (as it stands) on a random pixel subset of the workload, all samples
+    of each pixel (paths are independent under Philox, so a subset is an exact sample)."""
+    import oracle as orc
+    t0 = time.time()
+    parts = di.union_parts(scene.parts)
+    osc = orc.OracleScene(parts, 1)
+    t_build = time.time() - t0
+    P = scene.frame.W * scene.frame.H
+    rng = np.random.default_rng(1)
+    n = 64
+    while True:
+        pix = np.sort(rng.choice(P, size=n, replace=False))
+        t1 = time.time()
+        r = orc.render(osc, scene.camera, scene.frame, pixels=pix, dp=False, dumps=False)
+        dt = time.time() - t1
+        if dt >= seconds or n >= P:
+            break
+        n = int(min(P, max(2 * n, n * seconds / max(dt, 1e-3) * 1.1)))
+    rays = int(r.gen.sum())
+    return {"value": rays / dt, "unit": "rays/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{n} random pixels x {scene.frame.spp} spp of the workload ({rays} rays) in "
+                      f"{dt:.1f} s; oracle BVH build over {osc.nprims} prims {t_build:.1f} s not included",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    scene = di.config2(nranks=1)
+    import oracle as orc
+    parts = di.union_parts(scene.parts)
+    osc = orc.OracleScene(parts, 1)
+    P = scene.frame.W * scene.frame.H
+    rng = np.random.default_rng(2)
+    npix = int(os.environ.get("DPR_REF_PIXELS", "8192"))
+    times, rays = [], []
+    for i in range(args.warmup + args.steps):
+        pix = np.sort(rng.choice(P, size=npix, replace=False))
+        t0 = time.time()
+        r = orc.render(osc, scene.camera, scene.frame, pixels=pix, dp=False, dumps=False)
+        dt = time.time() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            rays.append(int(r.gen.sum()))
+    value = sum(rays) / sum(times)
+    frame_rays_est = np.mean(rays) * P / npix
+    line = {"metric": METRIC, "value": value, "unit": "rays/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * float(np.mean(times)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "step": f"oracle on {npix} random pixels x 16 spp",
+                       "est_ms_per_full_frame": 1000 * frame_rays_est / value},
+            "cpu_baseline": {"value": value, "unit": "rays/s", "cores": os.cpu_count(),
+                             "kind": "oracle", "sample": f"{npix} random pixels x 16 spp per step"},
+            "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2407_00179_b200 import dpr
+    scene = di.config2(nranks=world)
+    my_parts = [p for p in scene.parts if p.rank == rank]
+    if world > 1:
+        dev = dpr.Device.create_distributed(local)
+    else:
+        dev = dpr.Device.create(0, 1, local)
+    for p in my_parts:
+        dev.commit_part(p)
+    dev.commit_world()
+    dev.set_camera(scene.camera)
+    dev.set_frame(scene.frame)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident step: LBVH rebuild + collective render -----------------------
+    for _ in range(args.warmup):
+        dev.commit_world()
+        dev.render_frame()
+    barrier()
+    acc = {"rays": 0, "launches": 0, "ms_path": 0.0, "n_path": 0, "ms_occl": 0.0, "n_occl": 0,
+           "b_path": 0, "b_occl": 0, "ms_frame": [], "ms_build": [], "steps": 0, "exch": 0,
+           "ms_exch": 0.0, "nodes": 0, "tris": 0}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        time.sleep(0.3)
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            dev.commit_world()
+            dev.render_frame()
+            st = dev.get_stats()
+            acc["rays"] += int(st["rays"].sum())
+            acc["launches"] += st["kernel_launches_local"]
+            acc["ms_path"] += st["ms_trace_path"]; acc["n_path"] += st["trace_path_launches"]
+            acc["ms_occl"] += st["ms_trace_occl"]; acc["n_occl"] += st["trace_occl_launches"]
+            acc["b_path"] += st["path_bytes_alg_local"]; acc["b_occl"] += st["occl_bytes_alg_local"]
+            acc["ms_frame"].append(st["ms_frame_max"]); acc["ms_build"].append(st["ms_build"])
+            acc["steps"] += st["steps"]; acc["exch"] += st["exchanged_bytes_local"]
+            acc["ms_exch"] += st["ms_exchange"]
+            acc["nodes"] += st["node_visits_local"]; acc["tris"] += st["tri_tests_local"]
+        e1.record(stream)
+        barrier()
+    elapsed_ms = max_over_ranks(e0.elapsed_time(e1))
+    clocks = clk.summary()
+    rays_per_frame = acc["rays"] / args.steps  # global (stats are gathered over ranks)
+    value = rays_per_frame * args.steps / (elapsed_ms / 1000.0)
+    ms_per_step = elapsed_ms / args.steps
+
+    # roofline of the dominant kernel (rank 0's launches)
+    peak, peak_src = measured_peaks()
+    if acc["ms_path"] >= acc["ms_occl"]:
+        kname, ms, n, b = "k_trace_path", acc["ms_path"], acc["n_path"], acc["b_path"]
+    else:
+        kname, ms, n, b = "k_trace_occl", acc["ms_occl"], acc["n_occl"], acc["b_occl"]
+    avg_s = ms / max(n, 1) / 1000.0
+    bytes_per_launch = b / max(n, 1)
+    achieved = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
+    tr = profile_traffic()
+    traffic = None
+    if tr and kname in tr:
+        traffic = tr[kname].get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_s * 1000,
+                "share_of_step": (ms / args.steps) / ms_per_step,
+                "other_kernel_ms_per_step": ((acc["ms_occl"] if kname == "k_trace_path" else acc["ms_path"]) / args.steps)}
+
+    # ---- e2e: through the public API from pinned HOST buffers ---------------------------
+    pinned = []
+    h2d = 0
+    for p in my_parts:
+        q = di.Part(**p.__dict__)
+        if p.kind == di.TRIS:
+            v = torch.from_numpy(np.ascontiguousarray(p.verts)).pin_memory()
+            i = torch.from_numpy(np.ascontiguousarray(p.idx)).pin_memory()
+            q.verts, q.idx = v.numpy(), i.numpy()
+            h2d += v.numel() * 4 + i.numel() * 4
+        pinned.append(q)
+    fb_host = torch.empty((scene.frame.H, scene.frame.W, 4), dtype=torch.float32).pin_memory()
+    d2h = fb_host.numel() * 4 if rank == 0 else 0
+
+    def e2e_step():
+        dev.clear_parts()
+        for q in pinned:
+            dev.commit_part(q)
+        dev.commit_world()
+        dev.render_frame()
+        img = dev.map_frame()
+        if img is not None:
+            fb_host.copy_(img, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    if not args.no_e2e:
+        for _ in range(max(1, args.warmup // 2)):
+            e2e_step()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    else:
+        e2e_ms = float("nan")
+    e2e_value = rays_per_frame * args.steps / (e2e_ms / 1000.0)
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = oracle_sample(scene, seconds=args.cpu_seconds)
+        line = {
+            "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "resolution": [scene.frame.W, scene.frame.H],
+                       "spp": scene.frame.spp, "spp_batch": scene.frame.spp_batch,
+                       "triangles": scene.meta["ntris"], "parallelism": f"dp{world} (world partitioned, ray forwarding)",
+                       "l2": "inputs larger than L2 (BVH+prims ~1.1 GB, ray queues ~5 GB per step)",
+                       "step": "dpr_commit_world (LBVH rebuild) + dpr_render_frame"},
+            "ms_per_frame": float(np.median(acc["ms_frame"])),
+            "ms_build": float(np.median(acc["ms_build"])),
+            "rays_per_frame": rays_per_frame,
+            "wavefront_steps_per_frame": acc["steps"] / args.steps,
+            "exchange_bytes_per_frame_rank0": acc["exch"] / args.steps,
+            "ms_exchange_per_frame_rank0": acc["ms_exch"] / args.steps,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
+            "gpu_launches": int(acc["launches"]),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dev.release()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dpr", choices=["dpr", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
