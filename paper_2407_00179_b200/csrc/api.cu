@@ -221,7 +221,7 @@ int build_world(Dev *d) {
     cudaStream_t s = d->stream;
     int64_t n = 0;
     for (auto &p : d->parts) n += p.nprims();
-    if (n >= (int64_t)0x7fffffff) return fail(DPR_ERR_INVALID_ARG, "too many primitives on one rank");
+    if (n >= (int64_t)0x0fffffff) return fail(DPR_ERR_INVALID_ARG, "too many primitives on one rank (max 2^28-2)");
     d->nprims = n;
     int np = (int)d->parts.size();
     // per-part bounds + overall centroid box
@@ -313,7 +313,7 @@ int build_world(Dev *d) {
         // LSD radix sort; constant-digit passes skipped (order preserved by stability)
         int cur = 0;
         int64_t ntiles = radix_tiles(n);
-        RET(ensure(d, d->b_tile, sizeof(uint32_t) * 256 * ntiles));
+        RET(ensure(d, d->b_tile, sizeof(uint32_t) * 256 * (ntiles + 1)));
         for (int pass = 0; pass < 8; ++pass) {
             bool constant = false;
             for (int b = 0; b < 256; ++b) if (hist[pass * 256 + b] == (unsigned long long)n) constant = true;
@@ -349,7 +349,7 @@ int build_world(Dev *d) {
                          P<float4>(d->b_shi), P<float4>(d->b_nlo), P<float4>(d->b_nhi), P<int>(d->b_arrive), s);
             launches += 2;
         }
-        launch_emit(n, 4, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_rlo), P<int>(d->b_rhi),
+        launch_emit(n, LEAF_MAX, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_rlo), P<int>(d->b_rhi),
                     P<float4>(d->b_slo), P<float4>(d->b_shi), P<float4>(d->b_nlo), P<float4>(d->b_nhi),
                     P<BVHNode>(d->b_nodes), s);
         launches++;
@@ -683,13 +683,15 @@ int render_group(std::vector<Dev *> &L) {
                 CK(cudaMemsetAsync(d->b_counts.p, 0, sizeof(uint32_t) * (2 * N + 1), d->stream));
                 CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 2, d->stream));
                 StepArgs a = make_args(d, fc, cur[i]);
+                const int grid_r = d->nsm * 8;
                 if (d->h_in[0]) {
                     cudaEvent_t e0 = next_event(d), e1 = next_event(d);
                     CK(cudaEventRecord(e0, d->stream));
                     launch_trace_path(a, grid_p[i], d->stream);
                     CK(cudaEventRecord(e1, d->stream));
+                    launch_shade_path(a, grid_r, d->stream);
                     if (i == 0) t_path.push_back({e0, e1});
-                    launches++;
+                    launches += 2;
                     d->tpl++;
                 }
                 if (d->h_in[1]) {
@@ -697,8 +699,9 @@ int render_group(std::vector<Dev *> &L) {
                     CK(cudaEventRecord(e0, d->stream));
                     launch_trace_occl(a, grid_o[i], d->stream);
                     CK(cudaEventRecord(e1, d->stream));
+                    launch_resolve_occl(a, grid_r, d->stream);
                     if (i == 0) t_occl.push_back({e0, e1});
-                    launches++;
+                    launches += 2;
                     d->tol++;
                 }
                 CK(cudaGetLastError());

@@ -73,9 +73,12 @@ struct StepArgs {
 void launch_gen_primary(const StepArgs &a, int s0, int nsamp, cudaStream_t s);
 void launch_trace_path(const StepArgs &a, int grid, cudaStream_t s);
 void launch_trace_occl(const StepArgs &a, int grid, cudaStream_t s);
+void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s);
+void launch_resolve_occl(const StepArgs &a, int grid, cudaStream_t s);
 int trace_path_occupancy(int block);
 int trace_occl_occupancy(int block);
 constexpr int TRACE_BLOCK = 128;
+constexpr int TRACE_MINB = 8;  // 8 x 128 threads per SM -> <= 64 registers
 
 void launch_fb_accumulate(float4 *dst, const float4 *src, int64_t n, cudaStream_t s);
 void launch_u32_accumulate(uint32_t *dst, const uint32_t *src, int64_t n, cudaStream_t s);

@@ -4,14 +4,15 @@
 //                   keeps the rays whose first candidate rank is itself -- "generate full
 //                   wave-fronts on all ranks ... discard some of the rays ... by testing
 //                   them for visibility against their geometry" (S2.2).
-//   k_trace_path    (a3+a4+a6 fused) closest hit against the rank's LBVH + bricks, then in
-//                   the same thread: forward to the next candidate rank (P8) or resolve,
-//                   shade (P6) and spawn shadow/AO/bounce rays into per-destination queues.
-//   k_trace_occl    (a3+a4 fused) any-hit; occluded rays are dropped, unoccluded ones are
-//                   forwarded or resolved into the framebuffer.
+//   k_trace_path    (a3) closest hit against the rank's LBVH + bricks; persistent warps
+//                   with per-lane ray replacement; result written into the record.
+//   k_shade_path    (a4+a6) forward to the next candidate rank (P8) or resolve, shade (P6)
+//                   and spawn shadow/AO/bounce rays into per-destination queues.
+//   k_trace_occl    (a3) any hit; marks occluded records.
+//   k_resolve_occl  (a4) drops occluded rays; forwards or resolves unoccluded ones.
 // Queues are appended with warp-aggregated atomics (__match_any_sync per destination).
-// Kernels are persistent: grid = resident CTAs, each warp fetches 32 rays at a time from a
-// device-side head, so launch shape never depends on host-known counts.
+// All kernels read their input count from device memory, so launch shapes never depend on
+// host-known counts.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -72,14 +73,57 @@ __device__ __forceinline__ void warp_count(bool want, int key, unsigned long lon
     }
 }
 
+// Block-aggregated queue append: all threads of the block must call it (block-uniform
+// control flow).  One global atomicAdd per (block, destination) instead of one per warp:
+// at N=1 every append targets the same counter, so per-warp atomics serialise in L2.
+// smem: cnt[DPR_MAX_RANKS], base[DPR_MAX_RANKS] provided by the caller.
+__device__ __forceinline__ uint32_t block_append(bool want, int dest, uint32_t *counts, uint32_t cap,
+                                                 unsigned *overflow, unsigned long long *S_row,
+                                                 int self, int nranks, uint32_t *s_cnt, uint32_t *s_base) {
+    const int lane = threadIdx.x & 31;
+    unsigned act = __ballot_sync(FULL, want);
+    uint32_t off = 0;
+    unsigned peers = 0;
+    int leader = 0;
+    if (want) {
+        peers = __match_any_sync(act, dest);
+        leader = __ffs(peers) - 1;
+        if (lane == leader) off = atomicAdd(&s_cnt[dest], (uint32_t)__popc(peers));
+        off = __shfl_sync(peers, off, leader) + __popc(peers & lanemask_lt());
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < nranks) {
+        uint32_t c = s_cnt[threadIdx.x];
+        uint32_t b = 0;
+        if (c) {
+            b = atomicAdd(&counts[threadIdx.x], c);
+            if (S_row && (int)threadIdx.x != self) atomicAdd(&S_row[threadIdx.x], (unsigned long long)c);
+        }
+        s_base[threadIdx.x] = b;
+        s_cnt[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    if (!want) return 0xffffffffu;
+    uint32_t pos = s_base[dest] + off;
+    if (pos >= cap) {
+        atomicOr(overflow, 1u);
+        return 0xffffffffu;
+    }
+    return pos;
+}
+
 __device__ __forceinline__ void flush(unsigned long long *dst, uint32_t v) {
     v = __reduce_add_sync(FULL, v);
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, (unsigned long long)v);
 }
 
 // ---------------------------------------------------------------------------------------
-// Traversal of the rank's LBVH (closest or any hit).  Equals brute force over the rank's
-// prims with the P9 rule; box tests are conservative (padded boxes, FMA slabs).
+// a3: traversal of the rank's LBVH.  Result == brute force over the rank's prims with the P9
+// rule (box tests are conservative: padded boxes, FMA slabs; they only decide what to
+// skip).  Aila & Laine 2009 "while-while" loop with leaf postponing, run inside a persistent
+// loop that REPLACES finished rays per lane (dynamic fetch), so a warp is not held by its
+// slowest ray.  Results are written back into the ray record in place; routing / shading
+// happen in the coherent resolve kernels that follow.
 // ---------------------------------------------------------------------------------------
 struct Hit {
     float t;
@@ -89,24 +133,45 @@ struct Hit {
 
 struct TraceCounters { uint32_t nodes, tris, sphs, vols; };
 
+constexpr int NO_LEAF = 0;       // leaf refs are negative
+constexpr int REFILL_MIN = 8;    // refill a warp's finished lanes once this many are idle
+
+struct TravState {
+    f3 o, d, id3, oid;
+    float tmax;
+    Hit h;
+    int node, leaf, sp;
+};
+
+__device__ __forceinline__ void trav_init(TravState &S, f3 o, f3 d, float tmax, Hit h, int64_t nprims) {
+    S.o = o; S.d = d; S.tmax = tmax; S.h = h;
+    const float tiny = 1e-20f;  // zero direction components -> finite reciprocal (box tests only)
+    S.id3 = mk(1.0f / (fabsf(d.x) > tiny ? d.x : copysignf(tiny, d.x)),
+               1.0f / (fabsf(d.y) > tiny ? d.y : copysignf(tiny, d.y)),
+               1.0f / (fabsf(d.z) > tiny ? d.z : copysignf(tiny, d.z)));
+    S.oid = mk(o.x * S.id3.x, o.y * S.id3.y, o.z * S.id3.z);
+    S.node = nprims > 0 ? 0 : REF_DONE;
+    S.leaf = NO_LEAF;
+    S.sp = 0;
+}
+
+// One outer while-while iteration.  Called by ALL 32 lanes (finished / idle lanes carry
+// node == REF_DONE, leaf == NO_LEAF); both inner loops are warp-uniform so the warp stays
+// converged (independent thread scheduling would otherwise let lanes drift apart and run
+// the leaf loop almost one lane at a time).  Returns true when the lane is finished.
 template <bool ANY>
-__device__ __forceinline__ bool traverse(const WorldDev &W, f3 o, f3 d, float tmax, Hit &h,
-                                         TraceCounters &tc, unsigned *overflow) {
-    if (W.nprims == 0) return false;
-    const float tiny = 1e-20f;
-    f3 id3 = mk(1.0f / (fabsf(d.x) > tiny ? d.x : copysignf(tiny, d.x)),
-                1.0f / (fabsf(d.y) > tiny ? d.y : copysignf(tiny, d.y)),
-                1.0f / (fabsf(d.z) > tiny ? d.z : copysignf(tiny, d.z)));
-    f3 oid = mk(o.x * id3.x, o.y * id3.y, o.z * id3.z);
-    int stack[STACK_SIZE];
-    int sp = 0;
-    int node = 0;
-    for (;;) {
-        const BVHNode *nd = W.nodes + node;
+__device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, int *stack,
+                                          TraceCounters &tc, unsigned *overflow) {
+    // inner loop 1: descend until every lane holds a postponed leaf or is done; lanes that
+    // already hold one keep descending speculatively (their next leaf stays in `node`)
+    while (__any_sync(FULL, S.node >= 0 && S.leaf == NO_LEAF)) {
+        if (S.node < 0) continue;
+        const BVHNode *nd = W.nodes + S.node;
         float4 n0 = __ldg(&nd->n0), n1 = __ldg(&nd->n1), n2 = __ldg(&nd->n2);
         int4 n3 = __ldg(&nd->n3);
         tc.nodes++;
-        float bound = ANY ? tmax : h.t;
+        const float bound = ANY ? S.tmax : S.h.t;
+        const f3 id3 = S.id3, oid = S.oid;
         float a0 = __fmaf_rn(n0.x, id3.x, -oid.x), a1 = __fmaf_rn(n0.y, id3.x, -oid.x);
         float a2 = __fmaf_rn(n0.z, id3.y, -oid.y), a3 = __fmaf_rn(n0.w, id3.y, -oid.y);
         float a4 = __fmaf_rn(n2.x, id3.z, -oid.z), a5 = __fmaf_rn(n2.y, id3.z, -oid.z);
@@ -117,54 +182,66 @@ __device__ __forceinline__ bool traverse(const WorldDev &W, f3 o, f3 d, float tm
         float b4 = __fmaf_rn(n2.z, id3.z, -oid.z), b5 = __fmaf_rn(n2.w, id3.z, -oid.z);
         float tn1 = fmaxf(fmaxf(fminf(b0, b1), fminf(b2, b3)), fmaxf(fminf(b4, b5), 0.0f));
         float tf1 = fminf(fminf(fmaxf(b0, b1), fmaxf(b2, b3)), fminf(fmaxf(b4, b5), bound));
-        bool hit[2] = {tn0 <= tf0, tn1 <= tf1};
-        int ref[2] = {n3.x, n3.y};
-        int cnt[2] = {n3.z, n3.w};
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            if (!(hit[c] && ref[c] < 0)) continue;
-            hit[c] = false;
-            int start = ~ref[c];
-            for (int k = start; k < start + cnt[c]; ++k) {
-                const float4 *pr = W.prims + 3 * (int64_t)k;
-                float4 a = __ldg(pr);
-                uint32_t idw = __float_as_uint(a.w);
-                float t;
-                bool ok;
-                if (idw & SPHERE_BIT) {
-                    float4 b = __ldg(pr + 1);
-                    tc.sphs++;
-                    ok = sphere_hit(o, d, tmax, xyz(a), b.x, t);
-                } else {
-                    float4 b = __ldg(pr + 1), e = __ldg(pr + 2);
-                    tc.tris++;
-                    ok = tri_hit(o, d, tmax, xyz(a), xyz(b), xyz(e), t);
-                }
-                if (!ok) continue;
-                if (ANY) return true;
-                uint32_t gid = W.id_base + (idw & ~SPHERE_BIT);
-                if (t < h.t || (t == h.t && gid < h.id)) {
-                    h.t = t;
-                    h.id = gid;
-                    h.prim = k;
-                }
-            }
-        }
-        if (hit[0] && hit[1]) {
-            bool first0 = tn0 <= tn1;
-            if (sp < STACK_SIZE) stack[sp++] = first0 ? ref[1] : ref[0];
-            else atomicOr(overflow, 2u);
-            node = first0 ? ref[0] : ref[1];
-        } else if (hit[0]) {
-            node = ref[0];
-        } else if (hit[1]) {
-            node = ref[1];
+        bool h0 = tn0 <= tf0, h1 = tn1 <= tf1;
+        if (!h0 && !h1) {
+            S.node = S.sp > 0 ? stack[--S.sp] : REF_DONE;
         } else {
-            if (sp == 0) break;
-            node = stack[--sp];
+            int nearr = h0 ? n3.x : n3.y;
+            if (h0 && h1) {
+                int farr = n3.y;
+                if (tn1 < tn0) { farr = n3.x; nearr = n3.y; }
+                if (S.sp < STACK_SIZE) stack[S.sp++] = farr;
+                else atomicOr(overflow, 2u);
+            }
+            S.node = nearr;
+        }
+        if (S.node < 0 && S.node != REF_DONE && S.leaf == NO_LEAF) {  // postpone the leaf
+            S.leaf = S.node;
+            S.node = S.sp > 0 ? stack[--S.sp] : REF_DONE;
         }
     }
-    return false;
+    // inner loop 2: intersect postponed leaves (warp-uniform)
+    while (__any_sync(FULL, S.leaf != NO_LEAF)) {
+        if (S.leaf == NO_LEAF) continue;
+        const int start = leaf_start(S.leaf), cnt = leaf_count(S.leaf);
+        bool found = false;
+        for (int k = start; k < start + cnt; ++k) {
+            const float4 *pr = W.prims + 3 * (int64_t)k;
+            float4 a = __ldg(pr);
+            uint32_t idw = __float_as_uint(a.w);
+            float t;
+            bool ok;
+            if (idw & SPHERE_BIT) {
+                float4 b = __ldg(pr + 1);
+                tc.sphs++;
+                ok = sphere_hit(S.o, S.d, S.tmax, xyz(a), b.x, t);
+            } else {
+                float4 b = __ldg(pr + 1), e = __ldg(pr + 2);
+                tc.tris++;
+                ok = tri_hit(S.o, S.d, S.tmax, xyz(a), xyz(b), xyz(e), t);
+            }
+            if (!ok) continue;
+            if (ANY) {
+                S.h.prim = k;
+                found = true;
+                break;
+            }
+            uint32_t gid = W.id_base + (idw & ~SPHERE_BIT);
+            if (t < S.h.t || (t == S.h.t && gid < S.h.id)) {
+                S.h.t = t;
+                S.h.id = gid;
+                S.h.prim = k;
+            }
+        }
+        S.leaf = NO_LEAF;
+        if (ANY && found) {
+            S.node = REF_DONE;
+        } else if (S.node < 0 && S.node != REF_DONE) {
+            S.leaf = S.node;
+            S.node = S.sp > 0 ? stack[--S.sp] : REF_DONE;
+        }
+    }
+    return S.node == REF_DONE;
 }
 
 __device__ __forceinline__ f3 prim_normal(const WorldDev &W, int k, f3 o, f3 d, float t) {
@@ -247,14 +324,17 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
     const int tiles_x = (F.W + 7) / 8, tiles_y = (F.H + 3) / 4;
     const int64_t per_sample = (int64_t)tiles_x * tiles_y * 32;
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if ((t & ~31ll) >= per_sample * nsamp) return;  // whole warps only
+    __shared__ uint32_t s_cnt[DPR_MAX_RANKS], s_base[DPR_MAX_RANKS];
+    if (threadIdx.x < DPR_MAX_RANKS) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const bool valid = t < per_sample * nsamp;  // per_sample is a multiple of 32
     uint32_t s = (uint32_t)(s0 + t / per_sample);
     int64_t within = t % per_sample;
     int64_t tile = within >> 5;
     int li = (int)(within & 31);
     int x = (int)(tile % tiles_x) * 8 + (li & 7);
     int y = (int)(tile / tiles_x) * 4 + (li >> 3);
-    bool inimg = x < F.W && y < F.H;
+    bool inimg = valid && x < F.W && y < F.H;
     const int self = A.R.self;
     uint32_t p = (uint32_t)(y * F.W + x);
     f3 o = mk(F.cE[0], F.cE[1], F.cE[2]), d = mk(0, 0, 0);
@@ -286,7 +366,8 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
     }
     uint32_t gen = __popc(__ballot_sync(FULL, keep || owner_keep));
     if ((threadIdx.x & 31) == 0 && gen) atomicAdd(&A.ctr->gen[K_PATH], (unsigned long long)gen);
-    uint32_t pos = warp_append(keep, self, A.Q.out_count, A.Q.path_cap, &A.ctr->overflow, nullptr, self);
+    uint32_t pos = block_append(keep, self, A.Q.out_count, A.Q.path_cap, &A.ctr->overflow, nullptr, self,
+                                A.R.nranks, s_cnt, s_base);
     if (keep && pos != 0xffffffffu) {
         PathRec *r = A.Q.path_out[self] + pos;
         r->a = make_float4(o.x, o.y, o.z, __int_as_float(0x7f800000));
@@ -297,86 +378,178 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
 }
 
 // ---------------------------------------------------------------------------------------
-// a3 + a4 + a6: path rays.
+// a3: path-ray trace kernel (closest hit + brick march); results in place:
+// a.w = bestT, b.w = bestId, e.xyz = normal (surface) or TF rgb (volume).
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TRACE_BLOCK) k_trace_path(const __grid_constant__ StepArgs A) {
+template <bool ANY>
+__device__ __forceinline__ void trace_loop(const StepArgs &A) {
+    const FrameDev &F = A.F;
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_in = A.Q.in_count[ANY ? 1 : 0];
+    uint32_t *fetch = A.Q.fetch + (ANY ? 1 : 0);
+    const float INF = __int_as_float(0x7f800000);
+    int stack[STACK_SIZE];
+    TravState S;
+    S.node = REF_DONE; S.leaf = NO_LEAF; S.sp = 0;
+    uint32_t idx = 0;
+    bool alive = false, exhausted = false;
+    TraceCounters tc = {0, 0, 0, 0};
+    uint32_t rin = 0;
+    for (;;) {
+        unsigned dead = __ballot_sync(FULL, !alive);
+        int ndead = __popc(dead);
+        if (!exhausted && ndead >= REFILL_MIN) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(fetch, (uint32_t)ndead);
+            base = __shfl_sync(FULL, base, 0);
+            if (base + (uint32_t)ndead >= n_in) exhausted = true;
+            if (!alive) {
+                idx = base + __popc(dead & lanemask_lt());
+                if (idx < n_in) {
+                    alive = true;
+                    rin++;
+                    if (ANY) {
+                        const OcclRec *r = A.Q.occl_in + idx;
+                        float4 a = __ldcg(&r->a), b = __ldcg(&r->b);
+                        Hit h = {a.w, NO_HIT, -1};
+                        trav_init(S, xyz(a), xyz(b), a.w, h, A.W.nprims);
+                    } else {
+                        const PathRec *r = A.Q.path_in + idx;
+                        float4 a = __ldcg(&r->a), b = __ldcg(&r->b);
+                        Hit h = {a.w, __float_as_uint(b.w), -1};
+                        trav_init(S, xyz(a), xyz(b), INF, h, A.W.nprims);
+                    }
+                    S.sp = 0;
+                }
+            }
+        }
+        if (!__any_sync(FULL, alive)) {
+            if (exhausted) break;
+            continue;
+        }
+        if (!alive) { S.node = REF_DONE; S.leaf = NO_LEAF; }
+        bool fin = trav_step<ANY>(A.W, S, stack, tc, &A.ctr->overflow);
+        if (!(alive && fin)) continue;
+        // finished: volume march, then write the result back into the record
+        alive = false;
+        if (ANY) {
+            OcclRec *r = A.Q.occl_in + idx;
+            bool occluded = S.h.prim >= 0;
+            if (!occluded && A.W.nbricks > 0) {
+                const uint32_t p = __float_as_uint(r->b.w), meta = __float_as_uint(r->c.w);
+                const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
+                for (int b = 0; b < A.W.nbricks && !occluded; ++b) {
+                    float ti; uint32_t ii; f3 rgb;
+                    occluded = march_brick<true>(A.W.bricks[b], S.o, S.d, S.tmax, S.tmax, F.dt, F.seed, p, s,
+                                                 depth, slot == 0 ? PUR_VOL_SHADOW : PUR_VOL_AO,
+                                                 slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
+                }
+            }
+            if (occluded) r->a.w = -1.0f;  // occluded marker for k_resolve_occl
+        } else {
+            PathRec *r = A.Q.path_in + idx;
+            bool changed = S.h.prim >= 0;
+            f3 nrm = mk(0, 0, 0);
+            if (changed) nrm = prim_normal(A.W, S.h.prim, S.o, S.d, S.h.t);
+            if (A.W.nbricks > 0) {
+                const uint32_t p = __float_as_uint(r->c.w), meta = __float_as_uint(r->e.w);
+                const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
+                for (int b = 0; b < A.W.nbricks; ++b) {
+                    float ti; uint32_t ii; f3 rgb;
+                    if (march_brick<false>(A.W.bricks[b], S.o, S.d, INF, S.h.t, F.dt, F.seed, p, s, depth,
+                                           PUR_VOL_PATH, 0u, ti, ii, rgb, tc.vols)) {
+                        S.h.t = ti; S.h.id = VOL_BIT | ii; nrm = rgb; changed = true;
+                    }
+                }
+            }
+            if (changed) {
+                r->a.w = S.h.t;
+                r->b.w = __uint_as_float(S.h.id);
+                r->e.x = nrm.x; r->e.y = nrm.y; r->e.z = nrm.z;
+            }
+        }
+    }
+    KernelCounters *kc = &A.ctr->kc[ANY ? 1 : 0];
+    flush(&kc->nodes, tc.nodes);
+    flush(&kc->tris, tc.tris);
+    flush(&kc->sphs, tc.sphs);
+    flush(&kc->vols, tc.vols);
+    flush(&kc->rin, rin);
+}
+
+__global__ void __launch_bounds__(TRACE_BLOCK, TRACE_MINB) k_trace_path(const __grid_constant__ StepArgs A) {
+    trace_loop<false>(A);
+}
+__global__ void __launch_bounds__(TRACE_BLOCK, TRACE_MINB) k_trace_occl(const __grid_constant__ StepArgs A) {
+    trace_loop<true>(A);
+}
+
+// ---------------------------------------------------------------------------------------
+// a4 + a6: path rays after the trace -- forward to the next candidate rank (P8) or resolve
+// here: events, background/coverage, shading (P6) and spawning of shadow / AO / bounce rays
+// into per-destination queues (warp-aggregated appends; every lane of a warp participates).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_shade_path(const __grid_constant__ StepArgs A) {
     const FrameDev &F = A.F;
     const int self = A.R.self, N = A.R.nranks;
-    const int lane = threadIdx.x & 31;
     const float INF = __int_as_float(0x7f800000);
     const uint32_t n_in = A.Q.in_count[0];
     uint32_t *cnt_path = A.Q.out_count;
     uint32_t *cnt_occl = A.Q.out_count + N;
-    TraceCounters tc = {0, 0, 0, 0};
-    uint32_t visits = 0, gen_p = 0, gen_s = 0, gen_a = 0, rin = 0, rout_p = 0, rout_o = 0;
+    uint32_t visits = 0, gen_p = 0, gen_s = 0, gen_a = 0, rout_p = 0, rout_o = 0;
     const f3 L = mk(F.l[0], F.l[1], F.l[2]);
     const int K = F.ao_k;
-    for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&A.Q.fetch[0], 32u);
-        base = __shfl_sync(FULL, base, 0);
-        if (base >= n_in) break;
-        uint32_t idx = base + lane;
+    __shared__ uint32_t s_cnt[DPR_MAX_RANKS], s_base[DPR_MAX_RANKS];
+    if (threadIdx.x < DPR_MAX_RANKS) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint32_t tile = blockIdx.x; tile * blockDim.x < n_in; tile += gridDim.x) {
+        uint32_t idx = tile * blockDim.x + threadIdx.x;
         bool active = idx < n_in;
         PathRec r;
         if (active) {
             const PathRec *src = A.Q.path_in + idx;
             r.a = __ldcs(&src->a); r.b = __ldcs(&src->b); r.c = __ldcs(&src->c); r.e = __ldcs(&src->e);
-            rin++;
             visits++;
         } else {
             r.a = r.b = r.c = r.e = make_float4(0, 0, 0, 0);
         }
-        f3 o = xyz(r.a), d = xyz(r.b);
-        Hit h = {r.a.w, __float_as_uint(r.b.w), -1};
-        f3 nrm = xyz(r.e);
+        const f3 o = xyz(r.a), d = xyz(r.b);
+        const float bt = r.a.w;
+        const uint32_t bid = __float_as_uint(r.b.w);
+        const f3 nrm = xyz(r.e);
         const uint32_t p = __float_as_uint(r.c.w);
         const uint32_t meta = __float_as_uint(r.e.w);
         const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
-        int next = -1;
-        if (active) {
-            traverse<false>(A.W, o, d, INF, h, tc, &A.ctr->overflow);
-            if (h.prim >= 0) nrm = prim_normal(A.W, h.prim, o, d, h.t);
-            for (int b = 0; b < A.W.nbricks; ++b) {
-                float ti; uint32_t ii; f3 rgb;
-                if (march_brick<false>(A.W.bricks[b], o, d, INF, h.t, F.dt, F.seed, p, s, depth,
-                                       PUR_VOL_PATH, 0u, ti, ii, rgb, tc.vols)) {
-                    h.t = ti; h.id = VOL_BIT | ii; h.prim = -1; nrm = rgb;
-                }
-            }
-            next = next_candidate(A.R, self, o, d, INF, h.t);
-        }
-        // forward (P8: next candidate rank)
+        int next = active ? next_candidate(A.R, self, o, d, INF, bt) : -1;
         bool fwd = active && next >= 0;
-        uint32_t pos = warp_append(fwd, next, cnt_path, A.Q.path_cap, &A.ctr->overflow,
-                                   A.ctr->S[K_PATH], self);
+        uint32_t pos = 0xffffffffu;
+        if (__syncthreads_or(fwd))
+            pos = block_append(fwd, next, cnt_path, A.Q.path_cap, &A.ctr->overflow, A.ctr->S[K_PATH],
+                               self, N, s_cnt, s_base);
         if (fwd && pos != 0xffffffffu) {
             PathRec *dst = A.Q.path_out[next] + pos;
-            dst->a = make_float4(o.x, o.y, o.z, h.t);
-            dst->b = make_float4(d.x, d.y, d.z, __uint_as_float(h.id));
-            dst->c = r.c;
-            dst->e = make_float4(nrm.x, nrm.y, nrm.z, r.e.w);
+            dst->a = r.a; dst->b = r.b; dst->c = r.c; dst->e = r.e;
             rout_p++;
         }
-        // resolve here: events, background / coverage (P6, P13)
         bool res = active && next < 0;
-        bool evt = res && h.id != NO_HIT;
-        bool vol = evt && (h.id & VOL_BIT);
+        bool evt = res && bid != NO_HIT;
+        bool vol = evt && (bid & VOL_BIT);
         if (res) {
             if (A.events) {
-                uint32_t code = h.id == NO_HIT ? 1u : (vol ? h.id : 2u + h.id);
+                uint32_t code = bid == NO_HIT ? 1u : (vol ? bid : 2u + bid);
                 A.events[((int64_t)s * F.max_depth + depth) * F.P + p] = code;
             }
             if (!evt && depth == 0) fb_add(A.fb + p, make_float4(F.B[0], F.B[1], F.B[2], 0.0f));
             if (evt && depth == 0) fb_add(A.fb + p, make_float4(0.0f, 0.0f, 0.0f, 1.0f));
         }
-        f3 hp = mk(o.x + h.t * d.x, o.y + h.t * d.y, o.z + h.t * d.z);  // P5
+        if (!__syncthreads_or(evt)) continue;
+        f3 hp = mk(o.x + bt * d.x, o.y + bt * d.y, o.z + bt * d.z);  // P5
         f3 org = hp, br = mk(0, 0, 0);
         float c = 0.0f;
         if (evt) {
             f3 beta = xyz(r.c);
             if (!vol) {
-                f3 rho = part_albedo(A.T, h.id);
+                f3 rho = part_albedo(A.T, bid);
                 org = mk(hp.x + 1e-4f * nrm.x, hp.y + 1e-4f * nrm.y, hp.z + 1e-4f * nrm.z);
                 br = mul(beta, rho);
                 c = dot(nrm, L);
@@ -432,9 +605,10 @@ __global__ void __launch_bounds__(TRACE_BLOCK) k_trace_path(const __grid_constan
                     if (A.occl) atomicOr(A.occl + ((int64_t)s * F.max_depth + depth) * F.P + p, 1u << slot);
                 }
             }
+            if (!__syncthreads_or(app)) continue;
             if (is_path) {
-                uint32_t q = warp_append(app, first, cnt_path, A.Q.path_cap, &A.ctr->overflow,
-                                         A.ctr->S[K_PATH], self);
+                uint32_t q = block_append(app, first, cnt_path, A.Q.path_cap, &A.ctr->overflow,
+                                          A.ctr->S[K_PATH], self, N, s_cnt, s_base);
                 if (app && q != 0xffffffffu) {
                     PathRec *dst = A.Q.path_out[first] + q;
                     dst->a = make_float4(org.x, org.y, org.z, INF);
@@ -444,8 +618,8 @@ __global__ void __launch_bounds__(TRACE_BLOCK) k_trace_path(const __grid_constan
                     rout_p++;
                 }
             } else {
-                uint32_t q = warp_append(app, first, cnt_occl, A.Q.occl_cap, &A.ctr->overflow,
-                                         A.ctr->S[slot == 0 ? K_SHADOW : K_AO], self);
+                uint32_t q = block_append(app, first, cnt_occl, A.Q.occl_cap, &A.ctr->overflow,
+                                          A.ctr->S[slot == 0 ? K_SHADOW : K_AO], self, N, s_cnt, s_base);
                 if (app && q != 0xffffffffu) {
                     OcclRec *dst = A.Q.occl_out[first] + q;
                     dst->a = make_float4(org.x, org.y, org.z, ctmax);
@@ -461,64 +635,46 @@ __global__ void __launch_bounds__(TRACE_BLOCK) k_trace_path(const __grid_constan
     flush(&A.ctr->gen[K_PATH], gen_p);
     flush(&A.ctr->gen[K_SHADOW], gen_s);
     flush(&A.ctr->gen[K_AO], gen_a);
-    KernelCounters *kc = &A.ctr->kc[0];
-    flush(&kc->nodes, tc.nodes);
-    flush(&kc->tris, tc.tris);
-    flush(&kc->sphs, tc.sphs);
-    flush(&kc->vols, tc.vols);
-    flush(&kc->rin, rin);
-    flush(&kc->rout_path, rout_p);
-    flush(&kc->rout_occl, rout_o);
+    flush(&A.ctr->kc[0].rout_path, rout_p);
+    flush(&A.ctr->kc[0].rout_occl, rout_o);
 }
 
 // ---------------------------------------------------------------------------------------
-// a3 + a4: occlusion (shadow / AO) rays.
+// a4: occlusion rays after the trace -- drop occluded, forward or resolve unoccluded.
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TRACE_BLOCK) k_trace_occl(const __grid_constant__ StepArgs A) {
+__global__ void __launch_bounds__(256) k_resolve_occl(const __grid_constant__ StepArgs A) {
     const FrameDev &F = A.F;
     const int self = A.R.self, N = A.R.nranks;
-    const int lane = threadIdx.x & 31;
     const uint32_t n_in = A.Q.in_count[1];
     uint32_t *cnt_occl = A.Q.out_count + N;
-    TraceCounters tc = {0, 0, 0, 0};
-    uint32_t v_s = 0, v_a = 0, rin = 0, rout = 0;
-    for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&A.Q.fetch[1], 32u);
-        base = __shfl_sync(FULL, base, 0);
-        if (base >= n_in) break;
-        uint32_t idx = base + lane;
+    uint32_t v_s = 0, v_a = 0, rout = 0;
+    __shared__ uint32_t s_cnt[DPR_MAX_RANKS], s_base[DPR_MAX_RANKS];
+    if (threadIdx.x < DPR_MAX_RANKS) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint32_t tile = blockIdx.x; tile * blockDim.x < n_in; tile += gridDim.x) {
+        uint32_t idx = tile * blockDim.x + threadIdx.x;
         bool active = idx < n_in;
         OcclRec r;
         if (active) {
             const OcclRec *src = A.Q.occl_in + idx;
             r.a = __ldcs(&src->a); r.b = __ldcs(&src->b); r.c = __ldcs(&src->c);
-            rin++;
         } else {
             r.a = r.b = r.c = make_float4(0, 0, 0, 0);
         }
-        f3 o = xyz(r.a), d = xyz(r.b);
-        float tmax = r.a.w;
+        const f3 o = xyz(r.a), d = xyz(r.b);
+        const float tmax = r.a.w;
         const uint32_t p = __float_as_uint(r.b.w);
         const uint32_t meta = __float_as_uint(r.c.w);
         const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
-        bool occluded = false;
-        int next = -1;
-        if (active) {
-            if (slot == 0) v_s++; else v_a++;
-            Hit h = {tmax, NO_HIT, -1};
-            occluded = traverse<true>(A.W, o, d, tmax, h, tc, &A.ctr->overflow);
-            for (int b = 0; b < A.W.nbricks && !occluded; ++b) {
-                float ti; uint32_t ii; f3 rgb;
-                occluded = march_brick<true>(A.W.bricks[b], o, d, tmax, tmax, F.dt, F.seed, p, s,
-                                             depth, slot == 0 ? PUR_VOL_SHADOW : PUR_VOL_AO,
-                                             slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
-            }
-            if (!occluded) next = next_candidate(A.R, self, o, d, tmax, tmax);
-        }
+        const bool occluded = tmax < 0.0f;
+        if (active) { if (slot == 0) v_s++; else v_a++; }
+        int next = (active && !occluded) ? next_candidate(A.R, self, o, d, tmax, tmax) : -1;
         bool fwd = active && !occluded && next >= 0;
         warp_count(fwd, (slot == 0 ? K_SHADOW : K_AO) * DPR_MAX_RANKS + next, &A.ctr->S[0][0]);
-        uint32_t pos = warp_append(fwd, next, cnt_occl, A.Q.occl_cap, &A.ctr->overflow, nullptr, self);
+        uint32_t pos = 0xffffffffu;
+        if (__syncthreads_or(fwd))
+            pos = block_append(fwd, next, cnt_occl, A.Q.occl_cap, &A.ctr->overflow, nullptr, self, N,
+                               s_cnt, s_base);
         if (fwd && pos != 0xffffffffu) {
             OcclRec *dst = A.Q.occl_out[next] + pos;
             dst->a = r.a; dst->b = r.b; dst->c = r.c;
@@ -531,13 +687,7 @@ __global__ void __launch_bounds__(TRACE_BLOCK) k_trace_occl(const __grid_constan
     }
     flush(&A.ctr->V[K_SHADOW], v_s);
     flush(&A.ctr->V[K_AO], v_a);
-    KernelCounters *kc = &A.ctr->kc[1];
-    flush(&kc->nodes, tc.nodes);
-    flush(&kc->tris, tc.tris);
-    flush(&kc->sphs, tc.sphs);
-    flush(&kc->vols, tc.vols);
-    flush(&kc->rin, rin);
-    flush(&kc->rout_occl, rout);
+    flush(&A.ctr->kc[1].rout_occl, rout);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -572,6 +722,12 @@ void launch_trace_path(const StepArgs &a, int grid, cudaStream_t s) {
 }
 void launch_trace_occl(const StepArgs &a, int grid, cudaStream_t s) {
     k_trace_occl<<<grid, TRACE_BLOCK, 0, s>>>(a);
+}
+void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s) {
+    k_shade_path<<<grid, 256, 0, s>>>(a);
+}
+void launch_resolve_occl(const StepArgs &a, int grid, cudaStream_t s) {
+    k_resolve_occl<<<grid, 256, 0, s>>>(a);
 }
 int trace_path_occupancy(int block) {
     int n = 0;
