@@ -242,6 +242,11 @@ def run_gpu(args):
             acc["steps"] += st["steps"]; acc["exch"] += st["exchanged_bytes_local"]
             acc["ms_exch"] += st["ms_exchange"]
             acc["nodes"] += st["node_visits_local"]; acc["tris"] += st["tri_tests_local"]
+            for k in range(2):
+                for f in ("rays", "nodes", "tris"):
+                    acc.setdefault(f"k{k}_{f}", 0)
+                    acc[f"k{k}_{f}"] += st[f"kernel_{f}_local"][k]
+            acc["bvh_nodes"] = st["bvh_nodes_local"]; acc["bvh_levels"] = st["bvh_levels_local"]
         e1.record(stream)
         barrier()
     elapsed_ms = max_over_ranks(e0.elapsed_time(e1))
@@ -327,6 +332,11 @@ def run_gpu(args):
             "wavefront_steps_per_frame": acc["steps"] / args.steps,
             "exchange_bytes_per_frame_rank0": acc["exch"] / args.steps,
             "ms_exchange_per_frame_rank0": acc["ms_exch"] / args.steps,
+            "work_rank0": {kn: {"rays_per_frame": acc[f"k{k}_rays"] / args.steps,
+                                "nodes_per_ray": acc[f"k{k}_nodes"] / max(acc[f"k{k}_rays"], 1),
+                                "tris_per_ray": acc[f"k{k}_tris"] / max(acc[f"k{k}_rays"], 1)}
+                           for k, kn in enumerate(["k_trace_path", "k_trace_occl"])},
+            "bvh": {"wide_nodes": acc["bvh_nodes"], "collapse_levels": acc["bvh_levels"]},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d,

@@ -148,6 +148,11 @@ typedef struct {
     double ms_frame, ms_build, ms_gen, ms_trace_path, ms_trace_occl, ms_exchange, ms_reduce;
     double ms_frame_max; /* max over ranks of ms_frame */
     int64_t path_bytes_alg_local, occl_bytes_alg_local; /* algorithmic bytes */
+    /* per trace kernel (0 = k_trace_path, 1 = k_trace_occl), this rank: rays traced, wide-node
+     * visits, triangle tests, sphere tests, volume samples */
+    int64_t kernel_rays_local[2], kernel_nodes_local[2], kernel_tris_local[2], kernel_sphs_local[2],
+        kernel_vols_local[2];
+    int64_t bvh_nodes_local, bvh_levels_local; /* wide-BVH size of this rank's world */
 } dpr_stats;
 
 /* ---- device lifetime ------------------------------------------------------------------ */

@@ -43,14 +43,16 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """defines: extra -D flags for tuning sweeps (tools/sweep.sh); `out` another .so path."""
+    if out == LIB and not force and not stale():
         return LIB
     inc, lib = nccl_paths()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-prec-div=true",
            "-prec-sqrt=true", "-ftz=false", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
-           "-I", os.path.join(ROOT, "include"), "-I", inc, "-o", LIB + ".tmp", *sources(),
+           "-I", os.path.join(ROOT, "include"), "-I", inc, *[f"-D{d}" for d in defines],
+           "-o", out + ".tmp", *sources(),
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -60,10 +62,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=outs[0] if outs else LIB,
+                defines=defs))

@@ -92,7 +92,10 @@ struct Dev {
     float box[6];
     bool nonempty = false;
     Buf b_prims_u, b_blo, b_bhi, b_keys[2], b_vals[2], b_tile, b_left, b_right, b_parent, b_rlo,
-        b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_nodes, b_bounds, b_hist;
+        b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_nodes, b_bounds, b_hist, b_wnodes,
+        b_prims_w, b_items[2], b_wcnt, b_wperm;
+    int64_t wnodes_count = 0;
+    int bvh_levels = 0;
     std::vector<PartInfo> local_parts;
     // frame
     dpr_camera_basis cam{};
@@ -325,14 +328,11 @@ int build_world(Dev *d) {
         }
         uint64_t *keys = P<uint64_t>(d->b_keys[cur]);
         uint32_t *perm = P<uint32_t>(d->b_vals[cur]);
-        RET(ensure(d, d->b_prims, sizeof(float4) * 3 * n));
         RET(ensure(d, d->b_slo, sizeof(float4) * n));
         RET(ensure(d, d->b_shi, sizeof(float4) * n));
-        launch_gather_prims(P<float4>(d->b_prims_u), perm, n, P<float4>(d->b_prims), P<float4>(d->b_blo),
+        launch_gather_prims(P<float4>(d->b_prims_u), perm, n, nullptr, P<float4>(d->b_blo),
                             P<float4>(d->b_bhi), P<float4>(d->b_slo), P<float4>(d->b_shi), s);
         launches++;
-        int64_t ni = std::max<int64_t>(n - 1, 1);
-        RET(ensure(d, d->b_nodes, sizeof(BVHNode) * ni));
         if (n > 1) {
             RET(ensure(d, d->b_left, sizeof(int) * (n - 1)));
             RET(ensure(d, d->b_right, sizeof(int) * (n - 1)));
@@ -349,10 +349,42 @@ int build_world(Dev *d) {
                          P<float4>(d->b_shi), P<float4>(d->b_nlo), P<float4>(d->b_nhi), P<int>(d->b_arrive), s);
             launches += 2;
         }
-        launch_emit(n, LEAF_MAX, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_rlo), P<int>(d->b_rhi),
-                    P<float4>(d->b_slo), P<float4>(d->b_shi), P<float4>(d->b_nlo), P<float4>(d->b_nhi),
-                    P<BVHNode>(d->b_nodes), s);
+        // collapse into compressed 8-wide nodes, one BFS level per launch
+        const int node_cap = (int)std::max<int64_t>(n, 2);
+        RET(ensure(d, d->b_wnodes, sizeof(WNode) * node_cap));
+        RET(ensure(d, d->b_prims_w, sizeof(float4) * 3 * n));
+        RET(ensure(d, d->b_wperm, sizeof(uint32_t) * n));
+        RET(ensure(d, d->b_items[0], sizeof(int2) * node_cap));
+        RET(ensure(d, d->b_items[1], sizeof(int2) * node_cap));
+        RET(ensure(d, d->b_wcnt, sizeof(int) * 4));
+        int h_cnt[4] = {0, 1, 0, 0};
+        int2 root = make_int2(0, n > 1 ? 0 : -1);
+        CK(cudaMemcpyAsync(d->b_wcnt.p, h_cnt, sizeof(h_cnt), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d->b_items[0].p, &root, sizeof(root), cudaMemcpyHostToDevice, s));
+        CollapseArgs ca;
+        ca.n = n; ca.left = P<int>(d->b_left); ca.right = P<int>(d->b_right); ca.rlo = P<int>(d->b_rlo);
+        ca.rhi = P<int>(d->b_rhi); ca.nlo = P<float4>(d->b_nlo); ca.nhi = P<float4>(d->b_nhi);
+        ca.slo = P<float4>(d->b_slo); ca.shi = P<float4>(d->b_shi);
+        ca.perm = P<uint32_t>(d->b_wperm); ca.nodes = P<WNode>(d->b_wnodes); ca.counters = P<int>(d->b_wcnt);
+        ca.node_cap = node_cap;
+        int nitems = 1, cur_items = 0, levels = 0;
+        while (nitems > 0) {
+            int zero = 0;
+            CK(cudaMemcpyAsync(P<int>(d->b_wcnt), &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+            launch_collapse_level(ca, P<int2>(d->b_items[cur_items]), nitems, P<int2>(d->b_items[cur_items ^ 1]), s);
+            launches++;
+            levels++;
+            CK(cudaMemcpyAsync(h_cnt, d->b_wcnt.p, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (h_cnt[3]) return fail(DPR_ERR_STATE, "wide BVH node capacity exceeded");
+            nitems = h_cnt[0];
+            cur_items ^= 1;
+        }
+        if (h_cnt[2] != n) return fail(DPR_ERR_STATE, "wide BVH collapse lost primitives");
+        launch_permute_prims(P<float4>(d->b_prims_u), P<uint32_t>(d->b_wperm), perm, n, P<float4>(d->b_prims_w), s);
         launches++;
+        d->wnodes_count = h_cnt[1];
+        d->bvh_levels = levels;
     }
     // bricks: macrocells
     for (auto &p : d->parts) {
@@ -491,7 +523,8 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.R = fc.R;
     a.R.self = d->rank;
     a.W.nodes = P<BVHNode>(d->b_nodes);
-    a.W.prims = P<float4>(d->b_prims);
+    a.W.wnodes = P<WNode>(d->b_wnodes);
+    a.W.prims = P<float4>(d->b_prims_w);
     a.W.nprims = d->nprims;
     a.W.id_base = fc.id_base[d->rank];
     a.W.nbricks = 0;
@@ -800,11 +833,21 @@ int render_group(std::vector<Dev *> &L) {
         st.records_in_local = (int64_t)(a.rin + o.rin);
         st.records_out_local = (int64_t)(a.rout_path + a.rout_occl + o.rout_occl);
         // algorithmic bytes: records read + written, node fetches
-        // (64 B), triangle tests (48 B), sphere tests (16 B), volume samples (8 voxels, 32 B)
+        // (80 B wide nodes), triangle tests (48 B), sphere tests (16 B), volume samples (8 voxels, 32 B)
         st.path_bytes_alg_local = (int64_t)(a.rin * 64 + a.rout_path * 64 + a.rout_occl * 48 +
-                                            a.nodes * 64 + a.tris * 48 + a.sphs * 16 + a.vols * 32);
-        st.occl_bytes_alg_local = (int64_t)(o.rin * 48 + o.rout_occl * 48 + o.nodes * 64 +
+                                            a.nodes * 80 + a.tris * 48 + a.sphs * 16 + a.vols * 32);
+        st.occl_bytes_alg_local = (int64_t)(o.rin * 48 + o.rout_occl * 48 + o.nodes * 80 +
                                             o.tris * 48 + o.sphs * 16 + o.vols * 32);
+        for (int k = 0; k < 2; ++k) {
+            const KernelCounters &kc = ctr[i].kc[k];
+            st.kernel_rays_local[k] = (int64_t)kc.rin;
+            st.kernel_nodes_local[k] = (int64_t)kc.nodes;
+            st.kernel_tris_local[k] = (int64_t)kc.tris;
+            st.kernel_sphs_local[k] = (int64_t)kc.sphs;
+            st.kernel_vols_local[k] = (int64_t)kc.vols;
+        }
+        st.bvh_nodes_local = d->wnodes_count;
+        st.bvh_levels_local = d->bvh_levels;
         st.ms_frame = fms;
         st.ms_frame_max = mx;
         if (i == 0) {
@@ -872,7 +915,7 @@ void release_bufs(Dev *d) {
     Buf *bs[] = {&d->b_prims_u, &d->b_blo, &d->b_bhi, &d->b_keys[0], &d->b_keys[1], &d->b_vals[0],
                  &d->b_vals[1], &d->b_tile, &d->b_left, &d->b_right, &d->b_parent, &d->b_rlo, &d->b_rhi,
                  &d->b_nlo, &d->b_nhi, &d->b_arrive, &d->b_prims, &d->b_slo, &d->b_shi, &d->b_nodes,
-                 &d->b_bounds, &d->b_hist, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
+                 &d->b_bounds, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
                  &d->b_counts, &d->b_in_count, &d->b_fetch, &d->b_part_lo, &d->b_part_alb, &d->b_scratch,
                  &d->b_path[0], &d->b_path[1], &d->b_occlq[0], &d->b_occlq[1]};
     for (Buf *b : bs) dfree(d, *b);

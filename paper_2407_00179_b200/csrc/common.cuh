@@ -91,9 +91,17 @@ __device__ __forceinline__ bool tri_hit(f3 o, f3 d, float tmax, f3 v0, f3 e1, f3
     f3 pv = cross(d, e2);
     float det = dot(e1, pv);
     if (det == 0.0f) return false;
-    float inv = 1.0f / det;
     f3 tv = sub(o, v0);
-    float u = dot(tv, pv) * inv;
+    float un = dot(tv, pv);
+    // Exact early rejects before the IEEE division (they only skip cases the pinned test
+    // rejects): u = un*(1/det) has the sign of un*det when it cannot
+    // underflow to zero, and |u| > 1 when |un| > |det|*(1+2^-19).
+    if (fabsf(un) >= 0x1p-100f && fabsf(det) <= 0x1p40f &&
+        ((__float_as_uint(un) ^ __float_as_uint(det)) & 0x80000000u))
+        return false;
+    if (fabsf(un) > fabsf(det) * 1.0000019f) return false;
+    float inv = 1.0f / det;
+    float u = un * inv;
     if (u < 0.0f || u > 1.0f) return false;
     f3 qv = cross(tv, e1);
     float v = dot(d, qv) * inv;
@@ -234,7 +242,10 @@ __device__ __forceinline__ f3 iso_dir(uint64_t seed, uint32_t p, uint32_t s, uin
 // ref >= 0: internal node index; ref < 0: leaf_ref(start, count) = ~(start<<3 | count-1),
 // count in [1, 8] (start < 2^28 - 1; REF_DONE = INT_MIN is the "stack empty" sentinel).
 struct BVHNode { float4 n0, n1, n2; int4 n3; };
-constexpr int LEAF_MAX = 4;
+#ifndef DPR_LEAF_MAX
+#define DPR_LEAF_MAX 3
+#endif
+constexpr int LEAF_MAX = DPR_LEAF_MAX;  // <= 4 (2-bit count in the wide-node meta)
 constexpr int REF_DONE = (int)0x80000000;
 __host__ __device__ __forceinline__ int leaf_ref(int start, int cnt) { return ~((start << 3) | (cnt - 1)); }
 __host__ __device__ __forceinline__ int leaf_start(int ref) { return (~ref) >> 3; }
@@ -257,7 +268,22 @@ struct BrickDev {
 constexpr int MC_SIZE = 16;
 constexpr int MAX_BRICKS = 8;
 
+// Compressed 8-wide node (80 B; layout in the spirit of Ylitie, Karras, Laine 2017
+// "Efficient incoherent ray traversal on GPUs through compressed wide BVHs"):
+//   w0 = (p.x, p.y, p.z, bits ex | ey<<8 | ez<<16 | imask<<24)   origin + per-axis 2^(e-127)
+//   w1 = (child_base, prim_base, meta[0..3], meta[4..7])
+//   w2 = (qlo_x[0..3], qlo_x[4..7], qlo_y[0..3], qlo_y[4..7])
+//   w3 = (qlo_z[0..3], qlo_z[4..7], qhi_x[0..3], qhi_x[4..7])
+//   w4 = (qhi_y[0..3], qhi_y[4..7], qhi_z[0..3], qhi_z[4..7])
+// child box = p + q * 2^(e-127) (quantised outward from already-padded boxes: conservative).
+// imask bit s: slot s is an internal child, stored at child_base + popc(imask & ((1<<s)-1)).
+// meta[s] for a leaf: 0x80 | (count-1)<<5 | offset (prims prim_base+offset .. +count-1);
+// 0 = empty slot.  Slots are assigned by octant so that visiting s' = 0..7 with
+// slot = s' ^ octant(ray) is approximately front to back.
+struct WNode { float4 w0; uint4 w1, w2, w3, w4; };
+
 struct WorldDev {
+    const WNode *wnodes;
     const BVHNode *nodes;
     const float4 *prims;
     int64_t nprims;

@@ -32,6 +32,18 @@ void launch_emit(int64_t n, int leaf_max, const int *left, const int *right, con
 void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
                          const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,
                          cudaStream_t s);
+struct CollapseArgs {
+    int64_t n;
+    const int *left, *right, *rlo, *rhi;
+    const float4 *nlo, *nhi, *slo, *shi;
+    uint32_t *perm;  // per-wide-node contiguous prim order: perm[dst] = sorted prim index
+    WNode *nodes;
+    int *counters;
+    int node_cap;
+};
+void launch_collapse_level(const CollapseArgs &a, const int2 *items, int nitems, int2 *next, cudaStream_t s);
+void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t *sortperm, int64_t n,
+                          float4 *out, cudaStream_t s);
 void launch_macrocells(const float *vox, int nx, int ny, int nz, int mcx, int mcy, int mcz,
                        const float4 *tf, float tf_lo, float tf_hi, float dscale, uint8_t *mc,
                        cudaStream_t s);
@@ -78,7 +90,10 @@ void launch_resolve_occl(const StepArgs &a, int grid, cudaStream_t s);
 int trace_path_occupancy(int block);
 int trace_occl_occupancy(int block);
 constexpr int TRACE_BLOCK = 128;
-constexpr int TRACE_MINB = 8;  // 8 x 128 threads per SM -> <= 64 registers
+#ifndef DPR_TRACE_MINB
+#define DPR_TRACE_MINB 8
+#endif
+constexpr int TRACE_MINB = DPR_TRACE_MINB;  // 8 x 128 threads per SM -> <= 64 registers (sweep r01)
 
 void launch_fb_accumulate(float4 *dst, const float4 *src, int64_t n, cudaStream_t s);
 void launch_u32_accumulate(uint32_t *dst, const uint32_t *src, int64_t n, cudaStream_t s);

@@ -24,6 +24,8 @@
 
 namespace dpr {
 
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
 __device__ __forceinline__ int f2ord(float f) {
     int i = __float_as_int(f);
     return i >= 0 ? i : i ^ 0x7fffffff;
@@ -379,11 +381,176 @@ __global__ void k_gather_prims(const float4 *__restrict__ in, const uint32_t *__
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     uint32_t s = perm[i];
-    out[3 * i + 0] = in[3 * (int64_t)s + 0];
-    out[3 * i + 1] = in[3 * (int64_t)s + 1];
-    out[3 * i + 2] = in[3 * (int64_t)s + 2];
+    if (out) {
+        out[3 * i + 0] = in[3 * (int64_t)s + 0];
+        out[3 * i + 1] = in[3 * (int64_t)s + 1];
+        out[3 * i + 2] = in[3 * (int64_t)s + 2];
+    }
     slo[i] = blo[s];
     shi[i] = bhi[s];
+}
+
+// ---------------------------------------------------------------------------------------
+// Collapse of the binary LBVH into compressed 8-wide nodes (WNode, common.cuh), one BFS
+// level per launch: each thread turns one binary subtree root into one wide node by
+// repeatedly opening its largest-area child that is still an internal node with more
+// than LEAF_MAX prims, until 8 children or nothing left to open.  Leaf children's prims
+// are copied contiguously per wide node (prim_base + offset, offset < 32).
+// ---------------------------------------------------------------------------------------
+
+__device__ __forceinline__ void bin_child(const CollapseArgs &a, int id, float lo[3], float hi[3], int &r0, int &r1) {
+    float4 l, h;
+    if (id >= a.n - 1) {
+        int j = id - (int)(a.n - 1);
+        l = a.slo[j]; h = a.shi[j]; r0 = r1 = j;
+    } else {
+        l = a.nlo[id]; h = a.nhi[id]; r0 = a.rlo[id]; r1 = a.rhi[id];
+    }
+    lo[0] = pad_lo(l.x); lo[1] = pad_lo(l.y); lo[2] = pad_lo(l.z);
+    hi[0] = pad_hi(h.x); hi[1] = pad_hi(h.y); hi[2] = pad_hi(h.z);
+}
+
+__global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items, int nitems, int2 *next) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nitems) return;
+    const int wnode = items[t].x, b = items[t].y;
+    int cid[8], c0[8], c1[8];
+    float lo[8][3], hi[8][3];
+    int nc = 0;
+    if (b < 0) {  // single-prim world: the root holds one leaf
+        cid[0] = (int)(a.n - 1);
+        bin_child(a, cid[0], lo[0], hi[0], c0[0], c1[0]);
+        nc = 1;
+    } else {
+        cid[0] = a.left[b]; bin_child(a, cid[0], lo[0], hi[0], c0[0], c1[0]);
+        cid[1] = a.right[b]; bin_child(a, cid[1], lo[1], hi[1], c0[1], c1[1]);
+        nc = 2;
+    }
+    while (nc < 8) {
+        int best = -1;
+        float ba = -1.0f;
+        for (int i = 0; i < nc; ++i) {
+            if (cid[i] >= a.n - 1 || c1[i] - c0[i] + 1 <= LEAF_MAX) continue;
+            float ex = hi[i][0] - lo[i][0], ey = hi[i][1] - lo[i][1], ez = hi[i][2] - lo[i][2];
+            float area = ex * ey + ey * ez + ez * ex;
+            if (area > ba) { ba = area; best = i; }
+        }
+        if (best < 0) break;
+        int c = cid[best];
+        cid[best] = a.left[c]; bin_child(a, cid[best], lo[best], hi[best], c0[best], c1[best]);
+        cid[nc] = a.right[c]; bin_child(a, cid[nc], lo[nc], hi[nc], c0[nc], c1[nc]);
+        nc++;
+    }
+    // node box and octant slot assignment (greedy on dot(child centre - node centre, octant))
+    float nlo_[3], nhi_[3];
+    for (int c = 0; c < 3; ++c) {
+        nlo_[c] = lo[0][c]; nhi_[c] = hi[0][c];
+        for (int i = 1; i < nc; ++i) { nlo_[c] = fminf(nlo_[c], lo[i][c]); nhi_[c] = fmaxf(nhi_[c], hi[i][c]); }
+    }
+    int slot_of[8];
+    unsigned used_slots = 0, done_child = 0;
+    for (int k = 0; k < nc; ++k) {
+        float bc = -3.4e38f;
+        int bi = 0, bs = 0;
+        for (int i = 0; i < nc; ++i) {
+            if (done_child >> i & 1) continue;
+            float dx = (lo[i][0] + hi[i][0]) - (nlo_[0] + nhi_[0]);
+            float dy = (lo[i][1] + hi[i][1]) - (nlo_[1] + nhi_[1]);
+            float dz = (lo[i][2] + hi[i][2]) - (nlo_[2] + nhi_[2]);
+            for (int sl = 0; sl < 8; ++sl) {
+                if (used_slots >> sl & 1) continue;
+                float cost = ((sl & 4) ? dx : -dx) + ((sl & 2) ? dy : -dy) + ((sl & 1) ? dz : -dz);
+                if (cost > bc) { bc = cost; bi = i; bs = sl; }
+            }
+        }
+        slot_of[bi] = bs;
+        used_slots |= 1u << bs;
+        done_child |= 1u << bi;
+    }
+    // internal vs leaf children, allocation
+    int n_int = 0, n_prims = 0;
+    unsigned imask = 0;
+    for (int i = 0; i < nc; ++i) {
+        bool leaf = cid[i] >= a.n - 1 || c1[i] - c0[i] + 1 <= LEAF_MAX;
+        if (leaf) n_prims += c1[i] - c0[i] + 1;
+        else { n_int++; imask |= 1u << slot_of[i]; }
+    }
+    int child_base = n_int ? atomicAdd(&a.counters[1], n_int) : 0;
+    int prim_base = atomicAdd(&a.counters[2], n_prims);
+    if (child_base + n_int > a.node_cap) { atomicOr(&a.counters[3], 1); return; }
+    // quantisation (outward): e = ceil(log2(extent/255))
+    float p[3];
+    int e[3];
+    double sc[3];
+    for (int c = 0; c < 3; ++c) {
+        p[c] = nlo_[c];
+        double ext = (double)nhi_[c] - (double)p[c];
+        int ee = -126;
+        if (ext > 0) {
+            ee = (int)ceil(log2(ext / 255.0));
+            while (ldexp(255.0, ee) < ext) ee++;
+            if (ee < -126) ee = -126;
+            if (ee > 127) ee = 127;
+        }
+        e[c] = ee;
+        sc[c] = ldexp(1.0, ee);
+    }
+    uint8_t meta[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint8_t q[6][8];
+    for (int k = 0; k < 6; ++k) for (int sl = 0; sl < 8; ++sl) q[k][sl] = 0;
+    int off = 0;
+    // slot-ordered traversal so internal children are stored in slot order
+    for (int sl = 0; sl < 8; ++sl) {
+        int i = -1;
+        for (int j = 0; j < nc; ++j) if (slot_of[j] == sl) i = j;
+        if (i < 0) continue;
+        for (int c = 0; c < 3; ++c) {
+            double ql = floor(((double)lo[i][c] - (double)p[c]) / sc[c]);
+            double qh = ceil(((double)hi[i][c] - (double)p[c]) / sc[c]);
+            q[c][sl] = (uint8_t)fmin(fmax(ql, 0.0), 255.0);
+            q[3 + c][sl] = (uint8_t)fmin(fmax(qh, 0.0), 255.0);
+        }
+        if (imask >> sl & 1) {
+            int rank = __popc(imask & ((1u << sl) - 1));
+            int k = atomicAdd(&a.counters[0], 1);
+            next[k] = make_int2(child_base + rank, cid[i]);
+        } else {
+            int cnt = c1[i] - c0[i] + 1;
+            meta[sl] = (uint8_t)(0x80 | ((cnt - 1) << 5) | off);
+            for (int j = 0; j < cnt; ++j) a.perm[prim_base + off + j] = (uint32_t)(c0[i] + j);
+            off += cnt;
+        }
+    }
+    auto pack4 = [](const uint8_t *v) {
+        return (uint32_t)v[0] | ((uint32_t)v[1] << 8) | ((uint32_t)v[2] << 16) | ((uint32_t)v[3] << 24);
+    };
+    WNode nd;
+    uint32_t bits = (uint32_t)(e[0] + 127) | ((uint32_t)(e[1] + 127) << 8) | ((uint32_t)(e[2] + 127) << 16) | (imask << 24);
+    nd.w0 = make_float4(p[0], p[1], p[2], __uint_as_float(bits));
+    nd.w1 = make_uint4((uint32_t)child_base, (uint32_t)prim_base, pack4(meta), pack4(meta + 4));
+    nd.w2 = make_uint4(pack4(q[0]), pack4(q[0] + 4), pack4(q[1]), pack4(q[1] + 4));
+    nd.w3 = make_uint4(pack4(q[2]), pack4(q[2] + 4), pack4(q[3]), pack4(q[3] + 4));
+    nd.w4 = make_uint4(pack4(q[4]), pack4(q[4] + 4), pack4(q[5]), pack4(q[5] + 4));
+    a.nodes[wnode] = nd;
+}
+
+void launch_collapse_level(const CollapseArgs &a, const int2 *items, int nitems, int2 *next, cudaStream_t s) {
+    if (nitems > 0) k_collapse<<<nblk(nitems, 128), 128, 0, s>>>(a, items, nitems, next);
+}
+
+// prims_out[i] = prims_in[perm[i]] (3 float4 each): one thread per float4, coalesced writes.
+// The two permutations compose: wide-node order -> Morton order (perm) -> input order (sortperm).
+__global__ void k_permute_prims(const float4 *__restrict__ in, const uint32_t *__restrict__ perm,
+                                const uint32_t *__restrict__ sortperm, int64_t n, float4 *out) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 3 * n) return;
+    int64_t i = t / 3;
+    out[t] = in[3 * (int64_t)sortperm[perm[i]] + (t - 3 * i)];
+}
+
+void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t *sortperm, int64_t n,
+                          float4 *out, cudaStream_t s) {
+    if (n > 0) k_permute_prims<<<nblk(3 * n, 256), 256, 0, s>>>(in, perm, sortperm, n, out);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -430,7 +597,6 @@ __global__ void k_macrocells(const float *__restrict__ vox, int nx, int ny, int 
 // ---------------------------------------------------------------------------------------
 // Host-side launchers.
 // ---------------------------------------------------------------------------------------
-static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, uint32_t local0,
                       float4 *prims, float4 *blo, float4 *bhi, cudaStream_t s) {

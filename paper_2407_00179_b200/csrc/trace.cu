@@ -133,14 +133,25 @@ struct Hit {
 
 struct TraceCounters { uint32_t nodes, tris, sphs, vols; };
 
-constexpr int NO_LEAF = 0;       // leaf refs are negative
-constexpr int REFILL_MIN = 8;    // refill a warp's finished lanes once this many are idle
+#ifndef DPR_REFILL_MIN
+#define DPR_REFILL_MIN 8
+#endif
+constexpr int REFILL_MIN = DPR_REFILL_MIN;  // refill a warp's finished lanes once this many are idle
+constexpr int WSTACK = 32;       // node-group stack entries (wide BVH depth bound)
 
+// Traversal state of one ray over the compressed 8-wide BVH.  A "node group" is the set of
+// not-yet-visited internal children of one visited node: (child_base, hit bits in traversal
+// order s' = slot ^ octant, parent imask).  A "prim group" is a 32-bit mask of prims at
+// prim_base.. of one visited node's hit leaves.
 struct TravState {
-    f3 o, d, id3, oid;
+    f3 o, d, id3;
     float tmax;
     Hit h;
-    int node, leaf, sp;
+    uint32_t oct;
+    uint2 ng;        // x = child_base, y = hits (bits 0..7) | imask << 8
+    uint32_t tbase, tmask;    // prim group being tested
+    uint32_t tbase2, tmask2;  // speculative second prim group
+    int sp;
 };
 
 __device__ __forceinline__ void trav_init(TravState &S, f3 o, f3 d, float tmax, Hit h, int64_t nprims) {
@@ -149,99 +160,149 @@ __device__ __forceinline__ void trav_init(TravState &S, f3 o, f3 d, float tmax, 
     S.id3 = mk(1.0f / (fabsf(d.x) > tiny ? d.x : copysignf(tiny, d.x)),
                1.0f / (fabsf(d.y) > tiny ? d.y : copysignf(tiny, d.y)),
                1.0f / (fabsf(d.z) > tiny ? d.z : copysignf(tiny, d.z)));
-    S.oid = mk(o.x * S.id3.x, o.y * S.id3.y, o.z * S.id3.z);
-    S.node = nprims > 0 ? 0 : REF_DONE;
-    S.leaf = NO_LEAF;
+    S.oct = (d.x < 0.0f ? 4u : 0u) | (d.y < 0.0f ? 2u : 0u) | (d.z < 0.0f ? 1u : 0u);
+    // virtual root group: one internal child (slot 0, imask 1) at index 0
+    S.ng = make_uint2(0u, nprims > 0 ? ((1u << S.oct) | (1u << 8)) : 0u);
+    S.tbase = 0;
+    S.tmask = 0;
+    S.tbase2 = 0;
+    S.tmask2 = 0;
     S.sp = 0;
 }
 
-// One outer while-while iteration.  Called by ALL 32 lanes (finished / idle lanes carry
-// node == REF_DONE, leaf == NO_LEAF); both inner loops are warp-uniform so the warp stays
-// converged (independent thread scheduling would otherwise let lanes drift apart and run
-// the leaf loop almost one lane at a time).  Returns true when the lane is finished.
+__device__ __forceinline__ bool trav_done(const TravState &S) {
+    return (S.ng.y & 0xffu) == 0 && S.sp == 0 && S.tmask == 0 && S.tmask2 == 0;
+}
+
+__device__ __forceinline__ float qbyte(uint32_t w, int b) {
+    // exact int->float of byte b of w: 0x4b0000xx = 2^23 + xx
+    return __uint_as_float(__byte_perm(w, 0x4b00u, (uint32_t)b | 0x5440u)) - 8388608.0f;
+}
+
+// One outer iteration, called by ALL 32 lanes (idle lanes have an empty state).  Phase 1
+// visits nodes until every lane holds a prim group or has nothing left; phase 2 tests the
+// prim groups.  Both loops are warp-uniform.  Returns true when the lane is finished.
 template <bool ANY>
-__device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, int *stack,
+__device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2 *stack,
                                           TraceCounters &tc, unsigned *overflow) {
-    // inner loop 1: descend until every lane holds a postponed leaf or is done; lanes that
-    // already hold one keep descending speculatively (their next leaf stays in `node`)
-    while (__any_sync(FULL, S.node >= 0 && S.leaf == NO_LEAF)) {
-        if (S.node < 0) continue;
-        const BVHNode *nd = W.nodes + S.node;
-        float4 n0 = __ldg(&nd->n0), n1 = __ldg(&nd->n1), n2 = __ldg(&nd->n2);
-        int4 n3 = __ldg(&nd->n3);
+    for (;;) {
+        // descend while some lane has no prim group yet; lanes that already hold one keep
+        // descending speculatively into the second slot (keeps the phase-1 warp full)
+        const bool work = (S.ng.y & 0xffu) != 0 || S.sp > 0;
+        if (!__any_sync(FULL, work && S.tmask == 0)) break;
+        if (!(work && S.tmask2 == 0)) continue;
+        if ((S.ng.y & 0xffu) == 0) S.ng = stack[--S.sp];
+        uint32_t hits = S.ng.y & 0xffu, pimask = S.ng.y >> 8;
+        int sp_ = __ffs(hits) - 1;
+        hits &= hits - 1;
+        int slot = sp_ ^ (int)S.oct;
+        int node = (int)S.ng.x + __popc(pimask & ((1u << slot) - 1u));
+        if (hits) {
+            if (S.sp < WSTACK) stack[S.sp++] = make_uint2(S.ng.x, hits | (pimask << 8));
+            else atomicOr(overflow, 2u);
+        }
+        // visit the node: test its (up to) 8 children
+        const WNode *nd = W.wnodes + node;
+        float4 w0 = __ldg(&nd->w0);
+        uint4 w1 = __ldg(&nd->w1), w2 = __ldg(&nd->w2), w3 = __ldg(&nd->w3), w4 = __ldg(&nd->w4);
         tc.nodes++;
+        const uint32_t bits = __float_as_uint(w0.w);
+        const uint32_t nimask = bits >> 24;
+        // ray-space plane t = q*ps + po.  Bytes are read as f = 2^23 + q (one PRMT, exact), so
+        // t = f*ps + (po - 2^23*ps); rounding that offset costs at most |ps|/2, so near planes
+        // use offset - |ps| and far planes offset + |ps|: conservative by construction (the
+        // remaining relative error is covered by the (|x|+4)*2^-18 box padding).
+        const float psx = __uint_as_float((bits & 0xffu) << 23) * S.id3.x;
+        const float psy = __uint_as_float(((bits >> 8) & 0xffu) << 23) * S.id3.y;
+        const float psz = __uint_as_float(((bits >> 16) & 0xffu) << 23) * S.id3.z;
+        const float pox = __fmaf_rn(-8388608.0f, psx, (w0.x - S.o.x) * S.id3.x);
+        const float poy = __fmaf_rn(-8388608.0f, psy, (w0.y - S.o.y) * S.id3.y);
+        const float poz = __fmaf_rn(-8388608.0f, psz, (w0.z - S.o.z) * S.id3.z);
+        const float onx = pox - fabsf(psx), ofx = pox + fabsf(psx);
+        const float ony = poy - fabsf(psy), ofy = poy + fabsf(psy);
+        const float onz = poz - fabsf(psz), ofz = poz + fabsf(psz);
+        // near/far planes per axis by ray direction sign
+        uint32_t nx0 = w2.x, nx1 = w2.y, fx0 = w3.z, fx1 = w3.w;
+        uint32_t ny0 = w2.z, ny1 = w2.w, fy0 = w4.x, fy1 = w4.y;
+        uint32_t nz0 = w3.x, nz1 = w3.y, fz0 = w4.z, fz1 = w4.w;
+        if (S.id3.x < 0.0f) { uint32_t t0 = nx0, t1 = nx1; nx0 = fx0; nx1 = fx1; fx0 = t0; fx1 = t1; }
+        if (S.id3.y < 0.0f) { uint32_t t0 = ny0, t1 = ny1; ny0 = fy0; ny1 = fy1; fy0 = t0; fy1 = t1; }
+        if (S.id3.z < 0.0f) { uint32_t t0 = nz0, t1 = nz1; nz0 = fz0; nz1 = fz1; fz0 = t0; fz1 = t1; }
         const float bound = ANY ? S.tmax : S.h.t;
-        const f3 id3 = S.id3, oid = S.oid;
-        float a0 = __fmaf_rn(n0.x, id3.x, -oid.x), a1 = __fmaf_rn(n0.y, id3.x, -oid.x);
-        float a2 = __fmaf_rn(n0.z, id3.y, -oid.y), a3 = __fmaf_rn(n0.w, id3.y, -oid.y);
-        float a4 = __fmaf_rn(n2.x, id3.z, -oid.z), a5 = __fmaf_rn(n2.y, id3.z, -oid.z);
-        float tn0 = fmaxf(fmaxf(fminf(a0, a1), fminf(a2, a3)), fmaxf(fminf(a4, a5), 0.0f));
-        float tf0 = fminf(fminf(fmaxf(a0, a1), fmaxf(a2, a3)), fminf(fmaxf(a4, a5), bound));
-        float b0 = __fmaf_rn(n1.x, id3.x, -oid.x), b1 = __fmaf_rn(n1.y, id3.x, -oid.x);
-        float b2 = __fmaf_rn(n1.z, id3.y, -oid.y), b3 = __fmaf_rn(n1.w, id3.y, -oid.y);
-        float b4 = __fmaf_rn(n2.z, id3.z, -oid.z), b5 = __fmaf_rn(n2.w, id3.z, -oid.z);
-        float tn1 = fmaxf(fmaxf(fminf(b0, b1), fminf(b2, b3)), fmaxf(fminf(b4, b5), 0.0f));
-        float tf1 = fminf(fminf(fmaxf(b0, b1), fmaxf(b2, b3)), fminf(fmaxf(b4, b5), bound));
-        bool h0 = tn0 <= tf0, h1 = tn1 <= tf1;
-        if (!h0 && !h1) {
-            S.node = S.sp > 0 ? stack[--S.sp] : REF_DONE;
+        uint32_t hitm = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t sel = (uint32_t)(c & 3) | 0x5440u;
+            float tnx = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? nx0 : nx1, 0x4b00u, sel)), psx, onx);
+            float tfx = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? fx0 : fx1, 0x4b00u, sel)), psx, ofx);
+            float tny = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? ny0 : ny1, 0x4b00u, sel)), psy, ony);
+            float tfy = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? fy0 : fy1, 0x4b00u, sel)), psy, ofy);
+            float tnz = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? nz0 : nz1, 0x4b00u, sel)), psz, onz);
+            float tfz = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? fz0 : fz1, 0x4b00u, sel)), psz, ofz);
+            float tn = fmaxf(fmaxf(tnx, tny), fmaxf(tnz, 0.0f));
+            float tf = fminf(fminf(tfx, tfy), fminf(tfz, bound));
+            hitm |= (tn <= tf ? 1u : 0u) << c;
+        }
+        // valid slots: internal children or non-empty leaf metas
+        // gather one bit per non-zero meta byte: (x & 0x01010101) * 0x01020408 puts byte i's
+        // bit at position 24+i with no carries (all partial products land on distinct bits)
+        const uint32_t leafm = ((((__vcmpne4(w1.z, 0u) & 0x01010101u) * 0x01020408u) >> 24) & 0xfu) |
+                               ((((__vcmpne4(w1.w, 0u) & 0x01010101u) * 0x01020408u) >> 20) & 0xf0u);
+        uint32_t ih = hitm & nimask;
+        uint32_t lh = hitm & leafm & ~nimask;
+        // internal hits into traversal order s' = slot ^ octant (bit permutation)
+        if (S.oct & 4u) ih = ((ih & 0x0fu) << 4) | ((ih & 0xf0u) >> 4);
+        if (S.oct & 2u) ih = ((ih & 0x33u) << 2) | ((ih & 0xccu) >> 2);
+        if (S.oct & 1u) ih = ((ih & 0x55u) << 1) | ((ih & 0xaau) >> 1);
+        uint32_t ihits = ih, tmask = 0;
+        while (lh) {
+            const int c = __ffs(lh) - 1;
+            lh &= lh - 1;
+            const uint32_t meta = ((c < 4 ? w1.z : w1.w) >> (8 * (c & 3))) & 0xffu;
+            tmask |= ((1u << (((meta >> 5) & 3u) + 1u)) - 1u) << (meta & 31u);
+        }
+        S.ng = make_uint2(w1.x, ihits | (nimask << 8));
+        if (tmask) {
+            if (S.tmask == 0) { S.tbase = w1.y; S.tmask = tmask; }
+            else { S.tbase2 = w1.y; S.tmask2 = tmask; }
+        }
+    }
+    // phase 2: prim groups (one prim per lane per iteration)
+    while (__any_sync(FULL, (S.tmask | S.tmask2) != 0)) {
+        if (S.tmask == 0) {
+            if (S.tmask2 == 0) continue;
+            S.tbase = S.tbase2; S.tmask = S.tmask2; S.tmask2 = 0;
+        }
+        int k = (int)S.tbase + __ffs(S.tmask) - 1;
+        S.tmask &= S.tmask - 1;
+        const float4 *pr = W.prims + 3 * (int64_t)k;
+        float4 a = __ldg(pr);
+        uint32_t idw = __float_as_uint(a.w);
+        float t;
+        bool ok;
+        if (idw & SPHERE_BIT) {
+            float4 b = __ldg(pr + 1);
+            tc.sphs++;
+            ok = sphere_hit(S.o, S.d, S.tmax, xyz(a), b.x, t);
         } else {
-            int nearr = h0 ? n3.x : n3.y;
-            if (h0 && h1) {
-                int farr = n3.y;
-                if (tn1 < tn0) { farr = n3.x; nearr = n3.y; }
-                if (S.sp < STACK_SIZE) stack[S.sp++] = farr;
-                else atomicOr(overflow, 2u);
-            }
-            S.node = nearr;
+            float4 b = __ldg(pr + 1), e = __ldg(pr + 2);
+            tc.tris++;
+            ok = tri_hit(S.o, S.d, S.tmax, xyz(a), xyz(b), xyz(e), t);
         }
-        if (S.node < 0 && S.node != REF_DONE && S.leaf == NO_LEAF) {  // postpone the leaf
-            S.leaf = S.node;
-            S.node = S.sp > 0 ? stack[--S.sp] : REF_DONE;
+        if (!ok) continue;
+        if (ANY) {
+            S.h.prim = k;
+            S.ng.y = 0; S.sp = 0; S.tmask = 0; S.tmask2 = 0;
+            continue;
         }
-    }
-    // inner loop 2: intersect postponed leaves (warp-uniform)
-    while (__any_sync(FULL, S.leaf != NO_LEAF)) {
-        if (S.leaf == NO_LEAF) continue;
-        const int start = leaf_start(S.leaf), cnt = leaf_count(S.leaf);
-        bool found = false;
-        for (int k = start; k < start + cnt; ++k) {
-            const float4 *pr = W.prims + 3 * (int64_t)k;
-            float4 a = __ldg(pr);
-            uint32_t idw = __float_as_uint(a.w);
-            float t;
-            bool ok;
-            if (idw & SPHERE_BIT) {
-                float4 b = __ldg(pr + 1);
-                tc.sphs++;
-                ok = sphere_hit(S.o, S.d, S.tmax, xyz(a), b.x, t);
-            } else {
-                float4 b = __ldg(pr + 1), e = __ldg(pr + 2);
-                tc.tris++;
-                ok = tri_hit(S.o, S.d, S.tmax, xyz(a), xyz(b), xyz(e), t);
-            }
-            if (!ok) continue;
-            if (ANY) {
-                S.h.prim = k;
-                found = true;
-                break;
-            }
-            uint32_t gid = W.id_base + (idw & ~SPHERE_BIT);
-            if (t < S.h.t || (t == S.h.t && gid < S.h.id)) {
-                S.h.t = t;
-                S.h.id = gid;
-                S.h.prim = k;
-            }
-        }
-        S.leaf = NO_LEAF;
-        if (ANY && found) {
-            S.node = REF_DONE;
-        } else if (S.node < 0 && S.node != REF_DONE) {
-            S.leaf = S.node;
-            S.node = S.sp > 0 ? stack[--S.sp] : REF_DONE;
+        uint32_t gid = W.id_base + (idw & ~SPHERE_BIT);
+        if (t < S.h.t || (t == S.h.t && gid < S.h.id)) {
+            S.h.t = t;
+            S.h.id = gid;
+            S.h.prim = k;
         }
     }
-    return S.node == REF_DONE;
+    return trav_done(S);
 }
 
 __device__ __forceinline__ f3 prim_normal(const WorldDev &W, int k, f3 o, f3 d, float t) {
@@ -388,9 +449,9 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
     const uint32_t n_in = A.Q.in_count[ANY ? 1 : 0];
     uint32_t *fetch = A.Q.fetch + (ANY ? 1 : 0);
     const float INF = __int_as_float(0x7f800000);
-    int stack[STACK_SIZE];
+    uint2 stack[WSTACK];
     TravState S;
-    S.node = REF_DONE; S.leaf = NO_LEAF; S.sp = 0;
+    S.ng = make_uint2(0, 0); S.sp = 0; S.tmask = 0; S.tmask2 = 0;
     uint32_t idx = 0;
     bool alive = false, exhausted = false;
     TraceCounters tc = {0, 0, 0, 0};
@@ -419,7 +480,6 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                         Hit h = {a.w, __float_as_uint(b.w), -1};
                         trav_init(S, xyz(a), xyz(b), INF, h, A.W.nprims);
                     }
-                    S.sp = 0;
                 }
             }
         }
@@ -427,7 +487,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
             if (exhausted) break;
             continue;
         }
-        if (!alive) { S.node = REF_DONE; S.leaf = NO_LEAF; }
+        if (!alive) { S.ng.y = 0; S.sp = 0; S.tmask = 0; S.tmask2 = 0; }
         bool fin = trav_step<ANY>(A.W, S, stack, tc, &A.ctr->overflow);
         if (!(alive && fin)) continue;
         // finished: volume march, then write the result back into the record

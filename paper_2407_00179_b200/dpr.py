@@ -16,7 +16,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdpr.so")
+LIB_PATH = os.environ.get("DPR_LIB") or os.path.join(HERE, "libdpr.so")
 
 DPR_OK = 0
 DPR_MAX_RANKS = 16
@@ -76,13 +76,20 @@ class dpr_stats(_c.Structure):
                 ("ms_trace_path", _c.c_double), ("ms_trace_occl", _c.c_double),
                 ("ms_exchange", _c.c_double), ("ms_reduce", _c.c_double),
                 ("ms_frame_max", _c.c_double), ("path_bytes_alg_local", _c.c_int64),
-                ("occl_bytes_alg_local", _c.c_int64)]
+                ("occl_bytes_alg_local", _c.c_int64), ("kernel_rays_local", _c.c_int64 * 2),
+                ("kernel_nodes_local", _c.c_int64 * 2), ("kernel_tris_local", _c.c_int64 * 2),
+                ("kernel_sphs_local", _c.c_int64 * 2), ("kernel_vols_local", _c.c_int64 * 2),
+                ("bvh_nodes_local", _c.c_int64), ("bvh_levels_local", _c.c_int64)]
 
     def to_dict(self) -> dict:
         n = self.nranks
         S = np.frombuffer(self.S, np.int64).reshape(3, R, R)[:, :n, :n].copy()
         V = np.frombuffer(self.V, np.int64).reshape(3, R)[:, :n].copy()
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("S", "V", "rays")}
+        arrays = ("S", "V", "rays", "kernel_rays_local", "kernel_nodes_local", "kernel_tris_local",
+                  "kernel_sphs_local", "kernel_vols_local")
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in arrays}
+        for k in arrays[3:]:
+            d[k] = list(getattr(self, k))
         d.update(S=S, V=V, rays=np.frombuffer(self.rays, np.int64).copy())
         return d
 
