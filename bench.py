@@ -191,7 +191,9 @@ def run_gpu(args):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2407_00179_b200 import dpr
-    scene = di.config2(nranks=world)
+    # one 16-spp batch on one GPU; 2 batches of 8 spp when the world is split (bounds the
+    # per-peer send queues: worst case every ray of a batch goes to one peer)
+    scene = di.config2(nranks=world, spp_batch=16 if world == 1 else 8)
     my_parts = [p for p in scene.parts if p.rank == rank]
     if world > 1:
         dev = dpr.Device.create_distributed(local)

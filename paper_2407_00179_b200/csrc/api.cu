@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -201,7 +202,7 @@ int allgather_host(std::vector<Dev *> &L, const std::vector<const void *> &send,
                    std::vector<std::vector<char>> &out) {
     Dev *d0 = L[0];
     int N = d0->nranks;
-    if (d0->group || N == 1) {
+    if (!d0->comm) {  // loopback group or single rank without NCCL
         std::vector<char> all((size_t)N * bytes);
         for (size_t i = 0; i < L.size(); ++i) memcpy(all.data() + (size_t)L[i]->rank * bytes, send[i], bytes);
         out.assign(L.size(), all);
@@ -570,7 +571,7 @@ int gather_counts(std::vector<Dev *> &L, std::vector<int64_t> &C, unsigned &over
     C.assign((size_t)2 * N * N, 0);
     overflow = 0;
     std::vector<const uint32_t *> rows(N, nullptr);
-    if (d0->group || N == 1) {
+    if (!d0->comm) {
         for (Dev *d : L) {
             // the overflow word lives in the Counters block; mirror it into the counts tail
             CK(cudaMemcpyAsync(P<uint32_t>(d->b_counts) + 2 * N, &P<Counters>(d->b_ctr)->overflow,
@@ -665,7 +666,7 @@ int render_group(std::vector<Dev *> &L) {
                     offs[2 * i + k] = off;
                 }
             }
-            if (N > 1) {
+            if (N > 1 || d0->comm) {
                 const size_t rs[2] = {sizeof(PathRec), sizeof(OcclRec)};
                 if (d0->group) {
                     for (size_t i = 0; i < L.size(); ++i) {
@@ -758,7 +759,7 @@ int render_group(std::vector<Dev *> &L) {
                 launches += 2;
             }
         }
-    } else if (N > 1) {
+    } else if (d0->comm) {
         Dev *d = d0;
         NK(ncclGroupStart());
         NK(ncclReduce(d->b_fb.p, d->b_fb.p, 4 * P_, ncclFloat, ncclSum, 0, d->comm, d->stream));
@@ -956,9 +957,14 @@ int dpr_create_device(int rank, int nranks, int cuda_device, const uint8_t *uid,
     dpr_device h = new dpr_device_s();
     int rc = init_dev(&h->d, rank, nranks, cuda_device, cuda_stream, alloc);
     if (rc != DPR_OK) { delete h; return rc; }
-    if (nranks > 1) {
+    // DPR_FORCE_NCCL=1: use NCCL even for a single rank (exercises the collective code paths
+    // -- allgathers, grouped exchange, reduce -- on a one-GPU box)
+    const char *force = getenv("DPR_FORCE_NCCL");
+    const bool use_nccl = nranks > 1 || (force && force[0] == '1');
+    if (use_nccl) {
         ncclUniqueId id;
-        memcpy(&id, uid, DPR_UNIQUE_ID_BYTES);
+        if (nranks > 1) memcpy(&id, uid, DPR_UNIQUE_ID_BYTES);
+        else if (ncclGetUniqueId(&id) != ncclSuccess) { delete h; return fail(DPR_ERR_NCCL, "ncclGetUniqueId failed"); }
         ncclResult_t r = ncclCommInitRank(&h->d.comm, nranks, id, rank);
         if (r != ncclSuccess) {
             delete h;

@@ -1,0 +1,69 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+* configs[1] (the bench workload: ~10M-triangle gyroid, 1024x1024, 16 spp in one batch,
+  shadows + AO) at N=1: EVERY event code and occlusion bit of the frame bit-exact against
+  the oracle's full-frame render, pixels within the north_star tolerance, ray counts equal.
+* configs[1] split over 4 ranks (loopback group, spp batches of 4): routing matrices S,
+  visits V and step counts bit-exact against the oracle's routing simulator, full frame.
+* configs[2] (1024^3 float32 volume in bricks, 1920x1080, DVR + volume shadows): sampled
+  pixels (the oracle evaluates any pixel subset exactly: paths are Philox-keyed).
+* the NCCL code path (DPR_FORCE_NCCL=1 makes a single rank use NCCL collectives).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import dpr_inputs as di
+from tests.gpu_helpers import assert_parity, assert_pixels_close, gpu_render, oracle_render
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c2_scene():
+    return di.config2(nranks=1)
+
+
+def test_config2_full_frame_single_rank(c2_scene):
+    sc = c2_scene
+    g = gpu_render(sc.parts, 1, sc.camera, sc.frame)
+    o = oracle_render(sc.parts, 1, sc.camera, sc.frame, dp=False)
+    assert_parity(g, o, check_routing=False)
+    assert g[3]["steps"] == 2
+
+
+def test_config2_full_frame_four_ranks():
+    sc = di.config2(nranks=4, spp_batch=4)
+    g = gpu_render(sc.parts, 4, sc.camera, sc.frame)
+    o = oracle_render(sc.parts, 4, sc.camera, sc.frame, dp=True)
+    assert_parity(g, o)
+    assert o.S.sum() > 1_000_000
+
+
+def test_config3_full_size_sampled():
+    sc = di.config3(nranks=1)
+    # GPU: whole frame; oracle: 400 random pixels (+ the centre row segment)
+    g = gpu_render(sc.parts, 1, sc.camera, sc.frame)
+    P = sc.frame.W * sc.frame.H
+    rng = np.random.default_rng(3)
+    pix = np.unique(np.concatenate([rng.choice(P, 400, replace=False),
+                                    (sc.frame.H // 2) * sc.frame.W + np.arange(800, 1120)]))
+    o = oracle_render(sc.parts, 1, sc.camera, sc.frame, pixels=pix, dp=False)
+    ev = g[1][:, :, pix]
+    oc = g[2][:, :, pix]
+    assert ((o.events & 0x80000000) != 0).sum() > 50
+    assert np.array_equal(ev, o.events)
+    assert np.array_equal(oc, o.occl)
+    assert_pixels_close(g[0][pix], o.rgba)
+
+
+def test_nccl_collectives_single_rank(monkeypatch):
+    """DPR_FORCE_NCCL=1: frame-setup allgather, counts allgather, (empty) grouped exchange
+    and ncclReduce of framebuffer + dumps all run through NCCL with one rank."""
+    monkeypatch.setenv("DPR_FORCE_NCCL", "1")
+    sc = di.config1()
+    parts = di.union_parts(sc.parts)
+    g = gpu_render(parts, 1, sc.camera, sc.frame)
+    o = oracle_render(parts, 1, sc.camera, sc.frame)
+    assert_parity(g, o)
