@@ -110,6 +110,7 @@ struct Dev {
     uint32_t *h_in = nullptr;      // pinned: [2]
     int frame_done = 0;
     int mapped_w = 0, mapped_h = 0;
+    int spw = 16;  // max samples per warp in primary generation (env DPR_SPW; sweep r01)
     int64_t build_launches = 0, frame_launches = 0, frame_exch_bytes = 0, tpl = 0, tol = 0;
     double ms_build = 0;
     bool dumps_valid = false;
@@ -525,6 +526,7 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.R.self = d->rank;
     a.W.nodes = P<BVHNode>(d->b_nodes);
     a.W.wnodes = P<WNode>(d->b_wnodes);
+    a.W.prmt_hi = 0x4b00u;
     a.W.prims = P<float4>(d->b_prims_w);
     a.W.nprims = d->nprims;
     a.W.id_base = fc.id_base[d->rank];
@@ -636,7 +638,7 @@ int render_group(std::vector<Dev *> &L) {
             StepArgs a = make_args(d, fc, cur[i]);
             cudaEvent_t e0 = next_event(d), e1 = next_event(d);
             CK(cudaEventRecord(e0, d->stream));
-            launch_gen_primary(a, s0, ns, d->stream);
+            launch_gen_primary(a, s0, ns, d->spw, d->stream);
             CK(cudaEventRecord(e1, d->stream));
             if (i == 0) t_gen.push_back({e0, e1});
             launches++;
@@ -907,6 +909,7 @@ int init_dev(Dev *d, int rank, int nranks, int cuda_device, void *stream, const 
     CK(cudaSetDevice(cuda_device));
     CK(cudaDeviceGetAttribute(&d->nsm, cudaDevAttrMultiProcessorCount, cuda_device));
     for (int c = 0; c < 3; ++c) { d->box[c] = INFINITY; d->box[3 + c] = -INFINITY; }
+    if (const char *e = getenv("DPR_SPW")) d->spw = std::max(1, atoi(e));
     return DPR_OK;
 }
 

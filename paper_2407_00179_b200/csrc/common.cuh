@@ -271,7 +271,7 @@ constexpr int MAX_BRICKS = 8;
 // Compressed 8-wide node (80 B; layout in the spirit of Ylitie, Karras, Laine 2017
 // "Efficient incoherent ray traversal on GPUs through compressed wide BVHs"):
 //   w0 = (p.x, p.y, p.z, bits ex | ey<<8 | ez<<16 | imask<<24)   origin + per-axis 2^(e-127)
-//   w1 = (child_base, prim_base, meta[0..3], meta[4..7])
+//   w1 = (child_base | leafmask[0..3] << 28, prim_base | leafmask[4..7] << 28, meta[0..3], meta[4..7])
 //   w2 = (qlo_x[0..3], qlo_x[4..7], qlo_y[0..3], qlo_y[4..7])
 //   w3 = (qlo_z[0..3], qlo_z[4..7], qhi_x[0..3], qhi_x[4..7])
 //   w4 = (qhi_y[0..3], qhi_y[4..7], qhi_z[0..3], qhi_z[4..7])
@@ -283,6 +283,8 @@ constexpr int MAX_BRICKS = 8;
 struct WNode { float4 w0; uint4 w1, w2, w3, w4; };
 
 struct WorldDev {
+    uint32_t prmt_hi;  // 0x4b00 (2^23 float pattern for byte decode), passed at run time so that
+                       // ptxas keeps the PRMT selector as the immediate operand
     const WNode *wnodes;
     const BVHNode *nodes;
     const float4 *prims;

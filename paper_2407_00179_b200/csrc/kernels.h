@@ -82,7 +82,7 @@ struct StepArgs {
     Counters *ctr;
 };
 
-void launch_gen_primary(const StepArgs &a, int s0, int nsamp, cudaStream_t s);
+void launch_gen_primary(const StepArgs &a, int s0, int nsamp, int spw_max, cudaStream_t s);
 void launch_trace_path(const StepArgs &a, int grid, cudaStream_t s);
 void launch_trace_occl(const StepArgs &a, int grid, cudaStream_t s);
 void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s);

@@ -306,9 +306,11 @@ __global__ void k_refit(int64_t n, const int *__restrict__ left, const int *__re
     if (j >= n) return;
     int node = parent[n - 1 + j];
     while (true) {
-        __threadfence();
-        if (atomicAdd(&arrive[node], 1) == 0) return;
-        __threadfence();
+        // acq_rel arrival counter: the first arriver's box stores are released by its
+        // increment and acquired by the second arriver (replaces two full fences)
+        int prev;
+        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(arrive + node) : "memory");
+        if (prev == 0) return;
         int c[2] = {left[node], right[node]};
         float4 lo = make_float4(0, 0, 0, 0), hi = lo;
         for (int k = 0; k < 2; ++k) {
@@ -448,24 +450,28 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
         for (int i = 1; i < nc; ++i) { nlo_[c] = fminf(nlo_[c], lo[i][c]); nhi_[c] = fmaxf(nhi_[c], hi[i][c]); }
     }
     int slot_of[8];
-    unsigned used_slots = 0, done_child = 0;
-    for (int k = 0; k < nc; ++k) {
-        float bc = -3.4e38f;
-        int bi = 0, bs = 0;
+    {
+        float cost[8][8];
         for (int i = 0; i < nc; ++i) {
-            if (done_child >> i & 1) continue;
             float dx = (lo[i][0] + hi[i][0]) - (nlo_[0] + nhi_[0]);
             float dy = (lo[i][1] + hi[i][1]) - (nlo_[1] + nhi_[1]);
             float dz = (lo[i][2] + hi[i][2]) - (nlo_[2] + nhi_[2]);
-            for (int sl = 0; sl < 8; ++sl) {
-                if (used_slots >> sl & 1) continue;
-                float cost = ((sl & 4) ? dx : -dx) + ((sl & 2) ? dy : -dy) + ((sl & 1) ? dz : -dz);
-                if (cost > bc) { bc = cost; bi = i; bs = sl; }
-            }
+            for (int sl = 0; sl < 8; ++sl)
+                cost[i][sl] = ((sl & 4) ? dx : -dx) + ((sl & 2) ? dy : -dy) + ((sl & 1) ? dz : -dz);
         }
-        slot_of[bi] = bs;
-        used_slots |= 1u << bs;
-        done_child |= 1u << bi;
+        unsigned used_slots = 0, done_child = 0;
+        for (int k = 0; k < nc; ++k) {
+            float bc = -3.4e38f;
+            int bi = 0, bs = 0;
+            for (int i = 0; i < nc; ++i) {
+                if (done_child >> i & 1) continue;
+                for (int sl = 0; sl < 8; ++sl)
+                    if (!(used_slots >> sl & 1) && cost[i][sl] > bc) { bc = cost[i][sl]; bi = i; bs = sl; }
+            }
+            slot_of[bi] = bs;
+            used_slots |= 1u << bs;
+            done_child |= 1u << bi;
+        }
     }
     // internal vs leaf children, allocation
     int n_int = 0, n_prims = 0;
@@ -527,7 +533,11 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
     WNode nd;
     uint32_t bits = (uint32_t)(e[0] + 127) | ((uint32_t)(e[1] + 127) << 8) | ((uint32_t)(e[2] + 127) << 16) | (imask << 24);
     nd.w0 = make_float4(p[0], p[1], p[2], __uint_as_float(bits));
-    nd.w1 = make_uint4((uint32_t)child_base, (uint32_t)prim_base, pack4(meta), pack4(meta + 4));
+    // leaf-slot mask in the spare top nibbles (child_base, prim_base < 2^28)
+    uint32_t lmask = 0;
+    for (int sl = 0; sl < 8; ++sl) lmask |= (meta[sl] != 0 ? 1u : 0u) << sl;
+    nd.w1 = make_uint4((uint32_t)child_base | ((lmask & 0xfu) << 28), (uint32_t)prim_base | ((lmask >> 4) << 28),
+                       pack4(meta), pack4(meta + 4));
     nd.w2 = make_uint4(pack4(q[0]), pack4(q[0] + 4), pack4(q[1]), pack4(q[1] + 4));
     nd.w3 = make_uint4(pack4(q[2]), pack4(q[2] + 4), pack4(q[3]), pack4(q[3] + 4));
     nd.w4 = make_uint4(pack4(q[4]), pack4(q[4] + 4), pack4(q[5]), pack4(q[5] + 4));

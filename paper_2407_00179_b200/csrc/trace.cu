@@ -231,25 +231,23 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         const float bound = ANY ? S.tmax : S.h.t;
         uint32_t hitm = 0;
 #pragma unroll
+        const uint32_t k4b = W.prmt_hi;
         for (int c = 0; c < 8; ++c) {
             const uint32_t sel = (uint32_t)(c & 3) | 0x5440u;
-            float tnx = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? nx0 : nx1, 0x4b00u, sel)), psx, onx);
-            float tfx = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? fx0 : fx1, 0x4b00u, sel)), psx, ofx);
-            float tny = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? ny0 : ny1, 0x4b00u, sel)), psy, ony);
-            float tfy = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? fy0 : fy1, 0x4b00u, sel)), psy, ofy);
-            float tnz = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? nz0 : nz1, 0x4b00u, sel)), psz, onz);
-            float tfz = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? fz0 : fz1, 0x4b00u, sel)), psz, ofz);
+            float tnx = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? nx0 : nx1, k4b, sel)), psx, onx);
+            float tfx = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? fx0 : fx1, k4b, sel)), psx, ofx);
+            float tny = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? ny0 : ny1, k4b, sel)), psy, ony);
+            float tfy = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? fy0 : fy1, k4b, sel)), psy, ofy);
+            float tnz = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? nz0 : nz1, k4b, sel)), psz, onz);
+            float tfz = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? fz0 : fz1, k4b, sel)), psz, ofz);
             float tn = fmaxf(fmaxf(tnx, tny), fmaxf(tnz, 0.0f));
             float tf = fminf(fminf(tfx, tfy), fminf(tfz, bound));
             hitm |= (tn <= tf ? 1u : 0u) << c;
         }
-        // valid slots: internal children or non-empty leaf metas
-        // gather one bit per non-zero meta byte: (x & 0x01010101) * 0x01020408 puts byte i's
-        // bit at position 24+i with no carries (all partial products land on distinct bits)
-        const uint32_t leafm = ((((__vcmpne4(w1.z, 0u) & 0x01010101u) * 0x01020408u) >> 24) & 0xfu) |
-                               ((((__vcmpne4(w1.w, 0u) & 0x01010101u) * 0x01020408u) >> 20) & 0xf0u);
+        // leaf slots (build time mask in the top nibbles of child_base / prim_base)
+        const uint32_t leafm = (w1.x >> 28) | ((w1.y >> 24) & 0xf0u);
         uint32_t ih = hitm & nimask;
-        uint32_t lh = hitm & leafm & ~nimask;
+        uint32_t lh = hitm & leafm;
         // internal hits into traversal order s' = slot ^ octant (bit permutation)
         if (S.oct & 4u) ih = ((ih & 0x0fu) << 4) | ((ih & 0xf0u) >> 4);
         if (S.oct & 2u) ih = ((ih & 0x33u) << 2) | ((ih & 0xccu) >> 2);
@@ -261,10 +259,10 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
             const uint32_t meta = ((c < 4 ? w1.z : w1.w) >> (8 * (c & 3))) & 0xffu;
             tmask |= ((1u << (((meta >> 5) & 3u) + 1u)) - 1u) << (meta & 31u);
         }
-        S.ng = make_uint2(w1.x, ihits | (nimask << 8));
+        S.ng = make_uint2(w1.x & 0x0fffffffu, ihits | (nimask << 8));
         if (tmask) {
-            if (S.tmask == 0) { S.tbase = w1.y; S.tmask = tmask; }
-            else { S.tbase2 = w1.y; S.tmask2 = tmask; }
+            if (S.tmask == 0) { S.tbase = w1.y & 0x0fffffffu; S.tmask = tmask; }
+            else { S.tbase2 = w1.y & 0x0fffffffu; S.tmask2 = tmask; }
         }
     }
     // phase 2: prim groups (one prim per lane per iteration)
@@ -380,21 +378,26 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
 // a2: primary generation + visibility discard.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ StepArgs A, int s0,
-                                                     int nsamp) {
+                                                     int nsamp, int spw, int tw, int th) {
+    // ray order: a warp holds spw samples of each of (32/spw) pixels of a tw x th tile, so the
+    // rays of a warp are nearly identical for spw > 1 (coherent traversal); warps walk tiles,
+    // then sample groups.
     const FrameDev &F = A.F;
-    const int tiles_x = (F.W + 7) / 8, tiles_y = (F.H + 3) / 4;
-    const int64_t per_sample = (int64_t)tiles_x * tiles_y * 32;
+    const int tiles_x = (F.W + tw - 1) / tw, tiles_y = (F.H + th - 1) / th;
+    const int64_t per_group = (int64_t)tiles_x * tiles_y * 32;
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     __shared__ uint32_t s_cnt[DPR_MAX_RANKS], s_base[DPR_MAX_RANKS];
     if (threadIdx.x < DPR_MAX_RANKS) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    const bool valid = t < per_sample * nsamp;  // per_sample is a multiple of 32
-    uint32_t s = (uint32_t)(s0 + t / per_sample);
-    int64_t within = t % per_sample;
+    const bool valid = t < per_group * (nsamp / spw);  // per_group is a multiple of 32
+    const int64_t g = t / per_group;
+    int64_t within = t % per_group;
     int64_t tile = within >> 5;
     int li = (int)(within & 31);
-    int x = (int)(tile % tiles_x) * 8 + (li & 7);
-    int y = (int)(tile / tiles_x) * 4 + (li >> 3);
+    uint32_t s = (uint32_t)(s0 + g * spw + (li % spw));
+    int pi = li / spw;
+    int x = (int)(tile % tiles_x) * tw + (pi % tw);
+    int y = (int)(tile / tiles_x) * th + (pi / tw);
     bool inimg = valid && x < F.W && y < F.H;
     const int self = A.R.self;
     uint32_t p = (uint32_t)(y * F.W + x);
@@ -772,10 +775,15 @@ __global__ void k_fb_normalize(float4 *out, const float4 *__restrict__ in, int64
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-void launch_gen_primary(const StepArgs &a, int s0, int nsamp, cudaStream_t s) {
-    int64_t per = (int64_t)((a.F.W + 7) / 8) * ((a.F.H + 3) / 4) * 32;
-    int64_t total = per * nsamp;
-    if (total > 0) k_gen_primary<<<nblk(total, 256), 256, 0, s>>>(a, s0, nsamp);
+void launch_gen_primary(const StepArgs &a, int s0, int nsamp, int spw_max, cudaStream_t s) {
+    int spw = 1;  // largest power of two <= spw_max dividing nsamp
+    while (spw * 2 <= spw_max && spw * 2 <= 32 && nsamp % (spw * 2) == 0) spw *= 2;
+    static const int TW[6] = {8, 4, 4, 2, 2, 1};  // tile width for spw = 1,2,4,8,16,32
+    int lg = __builtin_ctz(spw);
+    int tw = TW[lg], th = (32 / spw) / tw;
+    int64_t per = (int64_t)((a.F.W + tw - 1) / tw) * ((a.F.H + th - 1) / th) * 32;
+    int64_t total = per * (nsamp / spw);
+    if (total > 0) k_gen_primary<<<nblk(total, 256), 256, 0, s>>>(a, s0, nsamp, spw, tw, th);
 }
 void launch_trace_path(const StepArgs &a, int grid, cudaStream_t s) {
     k_trace_path<<<grid, TRACE_BLOCK, 0, s>>>(a);
