@@ -94,7 +94,9 @@ struct Dev {
     bool nonempty = false;
     Buf b_prims_u, b_blo, b_bhi, b_keys[2], b_vals[2], b_tile, b_left, b_right, b_parent, b_rlo,
         b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_nodes, b_bounds, b_hist, b_wnodes,
-        b_prims_w, b_items[2], b_wcnt, b_wperm;
+        b_prims_w, b_items[2], b_wcnt, b_wperm, b_witems[2], b_size;
+    int builder = 1;  // 0 PLOC, 1 Karras LBVH (default; env DPR_BUILDER=ploc|lbvh; sweep r01)
+    int build_iters = 0;
     int64_t wnodes_count = 0;
     int bvh_levels = 0;
     std::vector<PartInfo> local_parts;
@@ -335,37 +337,80 @@ int build_world(Dev *d) {
         launch_gather_prims(P<float4>(d->b_prims_u), perm, n, nullptr, P<float4>(d->b_blo),
                             P<float4>(d->b_bhi), P<float4>(d->b_slo), P<float4>(d->b_shi), s);
         launches++;
+        int root_id = 0;
         if (n > 1) {
             RET(ensure(d, d->b_left, sizeof(int) * (n - 1)));
             RET(ensure(d, d->b_right, sizeof(int) * (n - 1)));
-            RET(ensure(d, d->b_rlo, sizeof(int) * (n - 1)));
-            RET(ensure(d, d->b_rhi, sizeof(int) * (n - 1)));
-            RET(ensure(d, d->b_parent, sizeof(int) * (2 * n - 1)));
+            RET(ensure(d, d->b_size, sizeof(int) * (n - 1)));
             RET(ensure(d, d->b_nlo, sizeof(float4) * (n - 1)));
             RET(ensure(d, d->b_nhi, sizeof(float4) * (n - 1)));
-            RET(ensure(d, d->b_arrive, sizeof(int) * (n - 1)));
-            CK(cudaMemsetAsync(d->b_arrive.p, 0, sizeof(int) * (n - 1), s));
-            launch_karras(keys, n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_parent),
-                          P<int>(d->b_rlo), P<int>(d->b_rhi), s);
-            launch_refit(n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_parent), P<float4>(d->b_slo),
-                         P<float4>(d->b_shi), P<float4>(d->b_nlo), P<float4>(d->b_nhi), P<int>(d->b_arrive), s);
-            launches += 2;
+            if (d->builder == 0) {
+                // PLOC (default): locally-ordered agglomerative clustering on the Morton order
+                RET(ensure(d, d->b_items[0], sizeof(int) * n));  // reused as cluster lists
+                RET(ensure(d, d->b_items[1], sizeof(int) * n));
+                RET(ensure(d, d->b_parent, sizeof(int) * n));     // reused as nearest neighbours
+                int64_t nbmax = ploc_block_count(n);
+                RET(ensure(d, d->b_rlo, sizeof(int) * 2 * nbmax + 16));  // block counts + totals
+                PlocArgs pa;
+                pa.n = n; pa.slo = P<float4>(d->b_slo); pa.shi = P<float4>(d->b_shi);
+                pa.nlo = P<float4>(d->b_nlo); pa.nhi = P<float4>(d->b_nhi);
+                pa.left = P<int>(d->b_left); pa.right = P<int>(d->b_right); pa.size = P<int>(d->b_size);
+                int *cl[2] = {P<int>(d->b_items[0]), P<int>(d->b_items[1])};
+                int *nn = P<int>(d->b_parent);
+                int *bc = P<int>(d->b_rlo);
+                int *tot = bc + 2 * nbmax + 8;
+                launch_ploc_init(n, cl[0], s);
+                int64_t m = n;
+                int node_base = 0, c = 0, iters = 0;
+                int h_tot[2];
+                while (m > 1) {
+                    int64_t nb = ploc_block_count(m);
+                    launch_ploc_nn(pa, cl[c], m, nn, s);
+                    launch_ploc_count(nn, m, bc, s);
+                    launch_ploc_scan(bc, nb, tot, s);
+                    launch_ploc_write(pa, cl[c], nn, m, bc, node_base, cl[c ^ 1], s);
+                    launches += 4;
+                    CK(cudaMemcpyAsync(h_tot, tot, sizeof(h_tot), cudaMemcpyDeviceToHost, s));
+                    CK(cudaStreamSynchronize(s));
+                    if (h_tot[1] <= 0) return fail(DPR_ERR_STATE, "PLOC made no progress");
+                    m = h_tot[0];
+                    node_base += h_tot[1];
+                    c ^= 1;
+                    iters++;
+                }
+                if (node_base != n - 1) return fail(DPR_ERR_STATE, "PLOC produced a wrong node count");
+                CK(cudaMemcpyAsync(&root_id, cl[c], sizeof(int), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                d->build_iters = iters;
+            } else {
+                // Karras 2012 LBVH + bottom-up refit
+                RET(ensure(d, d->b_rlo, sizeof(int) * (n - 1)));
+                RET(ensure(d, d->b_rhi, sizeof(int) * (n - 1)));
+                RET(ensure(d, d->b_parent, sizeof(int) * (2 * n - 1)));
+                RET(ensure(d, d->b_arrive, sizeof(int) * (n - 1)));
+                CK(cudaMemsetAsync(d->b_arrive.p, 0, sizeof(int) * (n - 1), s));
+                launch_karras(keys, n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_parent),
+                              P<int>(d->b_rlo), P<int>(d->b_rhi), P<int>(d->b_size), s);
+                launch_refit(n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_parent), P<float4>(d->b_slo),
+                             P<float4>(d->b_shi), P<float4>(d->b_nlo), P<float4>(d->b_nhi), P<int>(d->b_arrive), s);
+                launches += 2;
+            }
         }
         // collapse into compressed 8-wide nodes, one BFS level per launch
         const int node_cap = (int)std::max<int64_t>(n, 2);
         RET(ensure(d, d->b_wnodes, sizeof(WNode) * node_cap));
         RET(ensure(d, d->b_prims_w, sizeof(float4) * 3 * n));
         RET(ensure(d, d->b_wperm, sizeof(uint32_t) * n));
-        RET(ensure(d, d->b_items[0], sizeof(int2) * node_cap));
-        RET(ensure(d, d->b_items[1], sizeof(int2) * node_cap));
+        RET(ensure(d, d->b_witems[0], sizeof(int2) * node_cap));
+        RET(ensure(d, d->b_witems[1], sizeof(int2) * node_cap));
         RET(ensure(d, d->b_wcnt, sizeof(int) * 4));
         int h_cnt[4] = {0, 1, 0, 0};
-        int2 root = make_int2(0, n > 1 ? 0 : -1);
+        int2 root = make_int2(0, n > 1 ? root_id : -1);
         CK(cudaMemcpyAsync(d->b_wcnt.p, h_cnt, sizeof(h_cnt), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(d->b_items[0].p, &root, sizeof(root), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d->b_witems[0].p, &root, sizeof(root), cudaMemcpyHostToDevice, s));
         CollapseArgs ca;
-        ca.n = n; ca.left = P<int>(d->b_left); ca.right = P<int>(d->b_right); ca.rlo = P<int>(d->b_rlo);
-        ca.rhi = P<int>(d->b_rhi); ca.nlo = P<float4>(d->b_nlo); ca.nhi = P<float4>(d->b_nhi);
+        ca.n = n; ca.left = P<int>(d->b_left); ca.right = P<int>(d->b_right); ca.size = P<int>(d->b_size);
+        ca.nlo = P<float4>(d->b_nlo); ca.nhi = P<float4>(d->b_nhi);
         ca.slo = P<float4>(d->b_slo); ca.shi = P<float4>(d->b_shi);
         ca.perm = P<uint32_t>(d->b_wperm); ca.nodes = P<WNode>(d->b_wnodes); ca.counters = P<int>(d->b_wcnt);
         ca.node_cap = node_cap;
@@ -373,7 +418,7 @@ int build_world(Dev *d) {
         while (nitems > 0) {
             int zero = 0;
             CK(cudaMemcpyAsync(P<int>(d->b_wcnt), &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-            launch_collapse_level(ca, P<int2>(d->b_items[cur_items]), nitems, P<int2>(d->b_items[cur_items ^ 1]), s);
+            launch_collapse_level(ca, P<int2>(d->b_witems[cur_items]), nitems, P<int2>(d->b_witems[cur_items ^ 1]), s);
             launches++;
             levels++;
             CK(cudaMemcpyAsync(h_cnt, d->b_wcnt.p, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
@@ -910,6 +955,7 @@ int init_dev(Dev *d, int rank, int nranks, int cuda_device, void *stream, const 
     CK(cudaDeviceGetAttribute(&d->nsm, cudaDevAttrMultiProcessorCount, cuda_device));
     for (int c = 0; c < 3; ++c) { d->box[c] = INFINITY; d->box[3 + c] = -INFINITY; }
     if (const char *e = getenv("DPR_SPW")) d->spw = std::max(1, atoi(e));
+    if (const char *e = getenv("DPR_BUILDER")) d->builder = strcmp(e, "ploc") == 0 ? 0 : 1;
     return DPR_OK;
 }
 
@@ -919,7 +965,7 @@ void release_bufs(Dev *d) {
     Buf *bs[] = {&d->b_prims_u, &d->b_blo, &d->b_bhi, &d->b_keys[0], &d->b_keys[1], &d->b_vals[0],
                  &d->b_vals[1], &d->b_tile, &d->b_left, &d->b_right, &d->b_parent, &d->b_rlo, &d->b_rhi,
                  &d->b_nlo, &d->b_nhi, &d->b_arrive, &d->b_prims, &d->b_slo, &d->b_shi, &d->b_nodes,
-                 &d->b_bounds, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
+                 &d->b_bounds, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_witems[0], &d->b_witems[1], &d->b_size, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
                  &d->b_counts, &d->b_in_count, &d->b_fetch, &d->b_part_lo, &d->b_part_alb, &d->b_scratch,
                  &d->b_path[0], &d->b_path[1], &d->b_occlq[0], &d->b_occlq[1]};
     for (Buf *b : bs) dfree(d, *b);

@@ -22,7 +22,7 @@ int64_t radix_tiles(int64_t n);
 void launch_radix_pass(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout,
                        int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches);
 void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
-                   int *rhi, cudaStream_t s);
+                   int *rhi, int *size, cudaStream_t s);
 void launch_refit(int64_t n, const int *left, const int *right, const int *parent,
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
                   cudaStream_t s);
@@ -34,7 +34,7 @@ void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, floa
                          cudaStream_t s);
 struct CollapseArgs {
     int64_t n;
-    const int *left, *right, *rlo, *rhi;
+    const int *left, *right, *size;  // binary internal nodes: children, subtree prim counts
     const float4 *nlo, *nhi, *slo, *shi;
     uint32_t *perm;  // per-wide-node contiguous prim order: perm[dst] = sorted prim index
     WNode *nodes;
@@ -44,6 +44,21 @@ struct CollapseArgs {
 void launch_collapse_level(const CollapseArgs &a, const int2 *items, int nitems, int2 *next, cudaStream_t s);
 void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t *sortperm, int64_t n,
                           float4 *out, cudaStream_t s);
+// ---- ploc.cu: PLOC binary builder (Meister & Bittner 2018) ------------------------------
+struct PlocArgs {
+    int64_t n;
+    const float4 *slo, *shi;  // leaf boxes (Morton order)
+    float4 *nlo, *nhi;        // internal node boxes
+    int *left, *right, *size; // internal nodes [0, n-1)
+};
+int64_t ploc_block_count(int64_t m);
+void launch_ploc_init(int64_t n, int *clusters, cudaStream_t s);
+void launch_ploc_nn(const PlocArgs &a, const int *clusters, int64_t m, int *nn, cudaStream_t s);
+void launch_ploc_count(const int *nn, int64_t m, int *block_counts, cudaStream_t s);
+void launch_ploc_scan(int *block_counts, int64_t nblocks, int *totals, cudaStream_t s);
+void launch_ploc_write(const PlocArgs &a, const int *clusters, const int *nn, int64_t m, const int *block_offsets,
+                       int node_base, int *next_clusters, cudaStream_t s);
+
 void launch_macrocells(const float *vox, int nx, int ny, int nz, int mcx, int mcy, int mcz,
                        const float4 *tf, float tf_lo, float tf_hi, float dscale, uint8_t *mc,
                        cudaStream_t s);

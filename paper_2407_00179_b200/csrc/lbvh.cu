@@ -269,7 +269,7 @@ __device__ __forceinline__ int delta(const uint64_t *keys, int64_t n, int64_t i,
 }
 
 __global__ void k_karras(const uint64_t *__restrict__ keys, int64_t n, int *left, int *right,
-                         int *parent, int *rlo, int *rhi) {
+                         int *parent, int *rlo, int *rhi, int *size) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n - 1) return;
     int d = delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1) >= 0 ? 1 : -1;
@@ -297,6 +297,7 @@ __global__ void k_karras(const uint64_t *__restrict__ keys, int64_t n, int *left
     parent[rc] = (int)i;
     rlo[i] = (int)lo;
     rhi[i] = (int)hi;
+    size[i] = (int)(hi - lo + 1);
 }
 
 __global__ void k_refit(int64_t n, const int *__restrict__ left, const int *__restrict__ right,
@@ -400,13 +401,14 @@ __global__ void k_gather_prims(const float4 *__restrict__ in, const uint32_t *__
 // are copied contiguously per wide node (prim_base + offset, offset < 32).
 // ---------------------------------------------------------------------------------------
 
-__device__ __forceinline__ void bin_child(const CollapseArgs &a, int id, float lo[3], float hi[3], int &r0, int &r1) {
+// Binary node ids: internal k in [0, n-1), leaf (sorted prim) j -> n-1+j.  sz = prim count.
+__device__ __forceinline__ void bin_child(const CollapseArgs &a, int id, float lo[3], float hi[3], int &sz) {
     float4 l, h;
     if (id >= a.n - 1) {
         int j = id - (int)(a.n - 1);
-        l = a.slo[j]; h = a.shi[j]; r0 = r1 = j;
+        l = a.slo[j]; h = a.shi[j]; sz = 1;
     } else {
-        l = a.nlo[id]; h = a.nhi[id]; r0 = a.rlo[id]; r1 = a.rhi[id];
+        l = a.nlo[id]; h = a.nhi[id]; sz = a.size[id];
     }
     lo[0] = pad_lo(l.x); lo[1] = pad_lo(l.y); lo[2] = pad_lo(l.z);
     hi[0] = pad_hi(h.x); hi[1] = pad_hi(h.y); hi[2] = pad_hi(h.z);
@@ -416,31 +418,31 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nitems) return;
     const int wnode = items[t].x, b = items[t].y;
-    int cid[8], c0[8], c1[8];
+    int cid[8], c1[8];  // c1 = subtree prim count
     float lo[8][3], hi[8][3];
     int nc = 0;
     if (b < 0) {  // single-prim world: the root holds one leaf
         cid[0] = (int)(a.n - 1);
-        bin_child(a, cid[0], lo[0], hi[0], c0[0], c1[0]);
+        bin_child(a, cid[0], lo[0], hi[0], c1[0]);
         nc = 1;
     } else {
-        cid[0] = a.left[b]; bin_child(a, cid[0], lo[0], hi[0], c0[0], c1[0]);
-        cid[1] = a.right[b]; bin_child(a, cid[1], lo[1], hi[1], c0[1], c1[1]);
+        cid[0] = a.left[b]; bin_child(a, cid[0], lo[0], hi[0], c1[0]);
+        cid[1] = a.right[b]; bin_child(a, cid[1], lo[1], hi[1], c1[1]);
         nc = 2;
     }
     while (nc < 8) {
         int best = -1;
         float ba = -1.0f;
         for (int i = 0; i < nc; ++i) {
-            if (cid[i] >= a.n - 1 || c1[i] - c0[i] + 1 <= LEAF_MAX) continue;
+            if (cid[i] >= a.n - 1 || c1[i] <= LEAF_MAX) continue;
             float ex = hi[i][0] - lo[i][0], ey = hi[i][1] - lo[i][1], ez = hi[i][2] - lo[i][2];
             float area = ex * ey + ey * ez + ez * ex;
             if (area > ba) { ba = area; best = i; }
         }
         if (best < 0) break;
         int c = cid[best];
-        cid[best] = a.left[c]; bin_child(a, cid[best], lo[best], hi[best], c0[best], c1[best]);
-        cid[nc] = a.right[c]; bin_child(a, cid[nc], lo[nc], hi[nc], c0[nc], c1[nc]);
+        cid[best] = a.left[c]; bin_child(a, cid[best], lo[best], hi[best], c1[best]);
+        cid[nc] = a.right[c]; bin_child(a, cid[nc], lo[nc], hi[nc], c1[nc]);
         nc++;
     }
     // node box and octant slot assignment (greedy on dot(child centre - node centre, octant))
@@ -477,29 +479,32 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
     int n_int = 0, n_prims = 0;
     unsigned imask = 0;
     for (int i = 0; i < nc; ++i) {
-        bool leaf = cid[i] >= a.n - 1 || c1[i] - c0[i] + 1 <= LEAF_MAX;
-        if (leaf) n_prims += c1[i] - c0[i] + 1;
+        bool leaf = cid[i] >= a.n - 1 || c1[i] <= LEAF_MAX;
+        if (leaf) n_prims += c1[i];
         else { n_int++; imask |= 1u << slot_of[i]; }
     }
     int child_base = n_int ? atomicAdd(&a.counters[1], n_int) : 0;
     int prim_base = atomicAdd(&a.counters[2], n_prims);
     if (child_base + n_int > a.node_cap) { atomicOr(&a.counters[3], 1); return; }
-    // quantisation (outward): e = ceil(log2(extent/255))
+    // quantisation (outward): smallest e with 255 * 2^e >= extent (frexp, no log2); the
+    // per-child planes below multiply by the exact power-of-two reciprocal (no division)
     float p[3];
     int e[3];
-    double sc[3];
+    double isc[3];
     for (int c = 0; c < 3; ++c) {
         p[c] = nlo_[c];
-        double ext = (double)nhi_[c] - (double)p[c];
+        double ext = (double)nhi_[c] - (double)p[c];  // exact (difference of two floats)
         int ee = -126;
         if (ext > 0) {
-            ee = (int)ceil(log2(ext / 255.0));
+            int ex;
+            frexp(ext / 255.0, &ex);  // ext/255 in [2^(ex-1), 2^ex)
+            ee = ex - 1;
             while (ldexp(255.0, ee) < ext) ee++;
             if (ee < -126) ee = -126;
             if (ee > 127) ee = 127;
         }
         e[c] = ee;
-        sc[c] = ldexp(1.0, ee);
+        isc[c] = ldexp(1.0, -ee);
     }
     uint8_t meta[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint8_t q[6][8];
@@ -511,8 +516,8 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
         for (int j = 0; j < nc; ++j) if (slot_of[j] == sl) i = j;
         if (i < 0) continue;
         for (int c = 0; c < 3; ++c) {
-            double ql = floor(((double)lo[i][c] - (double)p[c]) / sc[c]);
-            double qh = ceil(((double)hi[i][c] - (double)p[c]) / sc[c]);
+            double ql = floor(((double)lo[i][c] - (double)p[c]) * isc[c]);
+            double qh = ceil(((double)hi[i][c] - (double)p[c]) * isc[c]);
             q[c][sl] = (uint8_t)fmin(fmax(ql, 0.0), 255.0);
             q[3 + c][sl] = (uint8_t)fmin(fmax(qh, 0.0), 255.0);
         }
@@ -521,9 +526,15 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
             int k = atomicAdd(&a.counters[0], 1);
             next[k] = make_int2(child_base + rank, cid[i]);
         } else {
-            int cnt = c1[i] - c0[i] + 1;
+            int cnt = c1[i];
             meta[sl] = (uint8_t)(0x80 | ((cnt - 1) << 5) | off);
-            for (int j = 0; j < cnt; ++j) a.perm[prim_base + off + j] = (uint32_t)(c0[i] + j);
+            int st[8], sp = 0, k = 0;  // collect the (<= LEAF_MAX) prims of the binary subtree
+            st[sp++] = cid[i];
+            while (sp) {
+                int x = st[--sp];
+                if (x >= a.n - 1) a.perm[prim_base + off + k++] = (uint32_t)(x - (a.n - 1));
+                else { st[sp++] = a.right[x]; st[sp++] = a.left[x]; }
+            }
             off += cnt;
         }
     }
@@ -643,8 +654,8 @@ void launch_radix_pass(const uint64_t *kin, const uint32_t *vin, uint64_t *kout,
     *launches += 3;
 }
 void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
-                   int *rhi, cudaStream_t s) {
-    if (n > 1) k_karras<<<nblk(n - 1, 256), 256, 0, s>>>(keys, n, left, right, parent, rlo, rhi);
+                   int *rhi, int *size, cudaStream_t s) {
+    if (n > 1) k_karras<<<nblk(n - 1, 256), 256, 0, s>>>(keys, n, left, right, parent, rlo, rhi, size);
 }
 void launch_refit(int64_t n, const int *left, const int *right, const int *parent,
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,

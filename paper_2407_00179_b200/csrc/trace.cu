@@ -38,6 +38,27 @@ __device__ __forceinline__ void fb_add(float4 *p, float4 v) {
 #endif
 }
 
+// Framebuffer accumulation with a warp segmented reduction: lanes holding the same pixel in
+// consecutive lanes (16 samples of a pixel share a warp) are summed by a shuffle scan and the
+// last lane of each run issues ONE float4 atomic (same-address atomics would serialise).
+// All 32 lanes must call; inactive lanes pass active = false.
+__device__ __forceinline__ void fb_add_seg(float4 *fb, uint32_t p, float4 v, bool active) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t key = active ? p : (0x80000000u | (uint32_t)lane);  // unique when inactive
+    const uint32_t prev = __shfl_up_sync(FULL, key, 1);
+    const unsigned heads = __ballot_sync(FULL, lane == 0 || prev != key);
+    const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+    if (!active) v = make_float4(0, 0, 0, 0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        float x = __shfl_up_sync(FULL, v.x, o), y = __shfl_up_sync(FULL, v.y, o);
+        float z = __shfl_up_sync(FULL, v.z, o), w = __shfl_up_sync(FULL, v.w, o);
+        if (lane - o >= start) { v.x += x; v.y += y; v.z += z; v.w += w; }
+    }
+    const bool last = lane == 31 || ((heads >> (lane + 1)) & 1u);
+    if (active && last) fb_add(fb + p, v);
+}
+
 // Warp-aggregated queue append; all 32 lanes must call.  Returns the slot or ~0u.
 // S_row (may be null) receives the per-destination forward counts (dest != self).
 __device__ __forceinline__ uint32_t warp_append(bool want, int dest, uint32_t *counts, uint32_t cap,
@@ -424,10 +445,8 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
         int owner = (int)(((int64_t)p * A.R.nranks) / F.P);
         owner_keep = owner == self;
     }
-    if (owner_keep) {
-        fb_add(A.fb + p, make_float4(F.B[0], F.B[1], F.B[2], 0.0f));
-        if (A.events) A.events[((int64_t)s * F.max_depth) * F.P + p] = 1u;
-    }
+    fb_add_seg(A.fb, p, make_float4(F.B[0], F.B[1], F.B[2], 0.0f), owner_keep);
+    if (owner_keep && A.events) A.events[((int64_t)s * F.max_depth) * F.P + p] = 1u;
     uint32_t gen = __popc(__ballot_sync(FULL, keep || owner_keep));
     if ((threadIdx.x & 31) == 0 && gen) atomicAdd(&A.ctr->gen[K_PATH], (unsigned long long)gen);
     uint32_t pos = block_append(keep, self, A.Q.out_count, A.Q.path_cap, &A.ctr->overflow, nullptr, self,
@@ -552,7 +571,10 @@ __global__ void __launch_bounds__(TRACE_BLOCK, TRACE_MINB) k_trace_occl(const __
 // here: events, background/coverage, shading (P6) and spawning of shadow / AO / bounce rays
 // into per-destination queues (warp-aggregated appends; every lane of a warp participates).
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_shade_path(const __grid_constant__ StepArgs A) {
+#ifndef DPR_SHADE_MINB
+#define DPR_SHADE_MINB 4
+#endif
+__global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid_constant__ StepArgs A) {
     const FrameDev &F = A.F;
     const int self = A.R.self, N = A.R.nranks;
     const float INF = __int_as_float(0x7f800000);
@@ -597,14 +619,12 @@ __global__ void __launch_bounds__(256) k_shade_path(const __grid_constant__ Step
         bool res = active && next < 0;
         bool evt = res && bid != NO_HIT;
         bool vol = evt && (bid & VOL_BIT);
-        if (res) {
-            if (A.events) {
-                uint32_t code = bid == NO_HIT ? 1u : (vol ? bid : 2u + bid);
-                A.events[((int64_t)s * F.max_depth + depth) * F.P + p] = code;
-            }
-            if (!evt && depth == 0) fb_add(A.fb + p, make_float4(F.B[0], F.B[1], F.B[2], 0.0f));
-            if (evt && depth == 0) fb_add(A.fb + p, make_float4(0.0f, 0.0f, 0.0f, 1.0f));
+        if (res && A.events) {
+            uint32_t code = bid == NO_HIT ? 1u : (vol ? bid : 2u + bid);
+            A.events[((int64_t)s * F.max_depth + depth) * F.P + p] = code;
         }
+        if (res && depth == 0)
+            fb_add(A.fb + p, evt ? make_float4(0.0f, 0.0f, 0.0f, 1.0f) : make_float4(F.B[0], F.B[1], F.B[2], 0.0f));
         if (!__syncthreads_or(evt)) continue;
         f3 hp = mk(o.x + bt * d.x, o.y + bt * d.y, o.z + bt * d.z);  // P5
         f3 org = hp, br = mk(0, 0, 0);
@@ -743,10 +763,9 @@ __global__ void __launch_bounds__(256) k_resolve_occl(const __grid_constant__ St
             dst->a = r.a; dst->b = r.b; dst->c = r.c;
             rout++;
         }
-        if (active && !occluded && next < 0) {
-            fb_add(A.fb + p, make_float4(r.c.x, r.c.y, r.c.z, 0.0f));
-            if (A.occl) atomicOr(A.occl + ((int64_t)s * F.max_depth + depth) * F.P + p, 1u << slot);
-        }
+        const bool acc = active && !occluded && next < 0;
+        fb_add_seg(A.fb, p, make_float4(r.c.x, r.c.y, r.c.z, 0.0f), acc);
+        if (acc && A.occl) atomicOr(A.occl + ((int64_t)s * F.max_depth + depth) * F.P + p, 1u << slot);
     }
     flush(&A.ctr->V[K_SHADOW], v_s);
     flush(&A.ctr->V[K_AO], v_a);
