@@ -36,6 +36,26 @@ import dpr_inputs as di  # noqa: E402
 METRIC = "rays/sec and ms/frame (device-timed, max over ranks)"
 WORKLOAD = ("configs[1]: synthetic ~10M-triangle gyroid (marching tetrahedra G=301) spatially "
             "partitioned over N ranks, 1024x1024, 16 spp, shadows+AO (K=4, r=0.25, depth 1)")
+WORKLOADS = {
+    "c1": "configs[0]: two-rank world of 4 spheres + ground plane split by x-half, 64x64, 1 spp, AO 4, depth 2",
+    "c2": WORKLOAD,
+    "c3": "configs[2]: structured 1024^3 float32 volume split into per-rank bricks, DVR with volume "
+          "shadows (1 spp, depth 1), 1920x1080",
+}
+
+
+def make_scene(cfg: str, world: int):
+    if cfg == "c1":
+        sc = di.config1()
+        if world == 1:
+            sc.parts = di.union_parts(sc.parts)
+            sc.nranks = 1
+        return sc
+    if cfg == "c3":
+        return di.config3(nranks=world)
+    # one 16-spp batch on one GPU; 2 batches of 8 spp when the world is split (bounds the
+    # per-peer send queues: worst case every ray of a batch goes to one peer)
+    return di.config2(nranks=world, spp_batch=16 if world == 1 else 8)
 
 
 def dist_env():
@@ -191,9 +211,7 @@ def run_gpu(args):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2407_00179_b200 import dpr
-    # one 16-spp batch on one GPU; 2 batches of 8 spp when the world is split (bounds the
-    # per-peer send queues: worst case every ray of a batch goes to one peer)
-    scene = di.config2(nranks=world, spp_batch=16 if world == 1 else 8)
+    scene = make_scene(args.config, world)
     my_parts = [p for p in scene.parts if p.rank == rank]
     if world > 1:
         dev = dpr.Device.create_distributed(local)
@@ -323,9 +341,9 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "resolution": [scene.frame.W, scene.frame.H],
+            "config": {"workload": WORKLOADS[args.config], "resolution": [scene.frame.W, scene.frame.H],
                        "spp": scene.frame.spp, "spp_batch": scene.frame.spp_batch,
-                       "triangles": scene.meta["ntris"], "parallelism": f"dp{world} (world partitioned, ray forwarding)",
+                       "triangles": scene.meta.get("ntris", sum(p.nprims() for p in scene.parts)), "parallelism": f"dp{world} (world partitioned, ray forwarding)",
                        "l2": "inputs larger than L2 (BVH+prims ~1.1 GB, ray queues ~5 GB per step)",
                        "step": "dpr_commit_world (LBVH rebuild) + dpr_render_frame"},
             "ms_per_frame": float(np.median(acc["ms_frame"])),
@@ -360,6 +378,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dpr", choices=["dpr", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"],
+                    help="workload (default c2 = BASELINE configs[1], the metric's workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling)")
     args = ap.parse_args()
