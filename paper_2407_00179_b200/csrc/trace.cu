@@ -154,11 +154,17 @@ struct Hit {
 
 struct TraceCounters { uint32_t nodes, tris, sphs, vols; };
 
-#ifndef DPR_REFILL_MIN
-#define DPR_REFILL_MIN 8
+#ifndef DPR_REFILL_PATH
+#define DPR_REFILL_PATH 16
 #endif
-constexpr int REFILL_MIN = DPR_REFILL_MIN;  // refill a warp's finished lanes once this many are idle
+#ifndef DPR_REFILL_OCCL
+#define DPR_REFILL_OCCL 4
+#endif
+// refill a warp's finished lanes once this many are idle (sweeps r01: closest-hit rays prefer
+// bigger refill batches, any-hit rays smaller ones)
+constexpr int REFILL_PATH = DPR_REFILL_PATH, REFILL_OCCL = DPR_REFILL_OCCL;
 constexpr int WSTACK = 32;       // node-group stack entries (wide BVH depth bound)
+
 
 // Traversal state of one ray over the compressed 8-wide BVH.  A "node group" is the set of
 // not-yet-visited internal children of one visited node: (child_base, hit bits in traversal
@@ -169,9 +175,10 @@ struct TravState {
     float tmax;
     Hit h;
     uint32_t oct;
-    uint2 ng;        // x = child_base, y = hits (bits 0..7) | imask << 8
-    uint32_t tbase, tmask;    // prim group being tested
-    uint32_t tbase2, tmask2;  // speculative second prim group
+    uint2 ng;                  // x = child_base, y = hits (bits 0..7) | imask << 8
+    uint32_t tb0, tm0;         // prim group being tested
+    uint32_t tb1, tm1;         // speculative prim groups (filled while other lanes of the
+    uint32_t tb2, tm2;         //   warp are still descending; sweep r01: 3 slots > 2 >> 1)
     int sp;
 };
 
@@ -184,15 +191,21 @@ __device__ __forceinline__ void trav_init(TravState &S, f3 o, f3 d, float tmax, 
     S.oct = (d.x < 0.0f ? 4u : 0u) | (d.y < 0.0f ? 2u : 0u) | (d.z < 0.0f ? 1u : 0u);
     // virtual root group: one internal child (slot 0, imask 1) at index 0
     S.ng = make_uint2(0u, nprims > 0 ? ((1u << S.oct) | (1u << 8)) : 0u);
-    S.tbase = 0;
-    S.tmask = 0;
-    S.tbase2 = 0;
-    S.tmask2 = 0;
+    S.tb0 = S.tb1 = S.tb2 = 0;
+    S.tm0 = S.tm1 = S.tm2 = 0;
     S.sp = 0;
 }
 
+__device__ __forceinline__ uint32_t pending_prims(const TravState &S) { return S.tm0 | S.tm1 | S.tm2; }
+
+__device__ __forceinline__ void trav_clear(TravState &S) {
+    S.ng.y = 0;
+    S.sp = 0;
+    S.tm0 = S.tm1 = S.tm2 = 0;
+}
+
 __device__ __forceinline__ bool trav_done(const TravState &S) {
-    return (S.ng.y & 0xffu) == 0 && S.sp == 0 && S.tmask == 0 && S.tmask2 == 0;
+    return (S.ng.y & 0xffu) == 0 && S.sp == 0 && pending_prims(S) == 0;
 }
 
 __device__ __forceinline__ float qbyte(uint32_t w, int b) {
@@ -210,8 +223,12 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         // descend while some lane has no prim group yet; lanes that already hold one keep
         // descending speculatively into the second slot (keeps the phase-1 warp full)
         const bool work = (S.ng.y & 0xffu) != 0 || S.sp > 0;
-        if (!__any_sync(FULL, work && S.tmask == 0)) break;
-        if (!(work && S.tmask2 == 0)) continue;
+        if (!__any_sync(FULL, work && S.tm0 == 0)) break;
+#ifdef DPR_ANYFREE
+        if (!(work && (S.tm0 == 0 || S.tm1 == 0 || S.tm2 == 0))) continue;
+#else
+        if (!(work && S.tm2 == 0)) continue;
+#endif
         if ((S.ng.y & 0xffu) == 0) S.ng = stack[--S.sp];
         uint32_t hits = S.ng.y & 0xffu, pimask = S.ng.y >> 8;
         int sp_ = __ffs(hits) - 1;
@@ -282,18 +299,21 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         }
         S.ng = make_uint2(w1.x & 0x0fffffffu, ihits | (nimask << 8));
         if (tmask) {
-            if (S.tmask == 0) { S.tbase = w1.y & 0x0fffffffu; S.tmask = tmask; }
-            else { S.tbase2 = w1.y & 0x0fffffffu; S.tmask2 = tmask; }
+            const uint32_t pb = w1.y & 0x0fffffffu;
+            if (S.tm0 == 0) { S.tb0 = pb; S.tm0 = tmask; }
+            else if (S.tm1 == 0) { S.tb1 = pb; S.tm1 = tmask; }
+            else { S.tb2 = pb; S.tm2 = tmask; }
         }
     }
     // phase 2: prim groups (one prim per lane per iteration)
-    while (__any_sync(FULL, (S.tmask | S.tmask2) != 0)) {
-        if (S.tmask == 0) {
-            if (S.tmask2 == 0) continue;
-            S.tbase = S.tbase2; S.tmask = S.tmask2; S.tmask2 = 0;
+    while (__any_sync(FULL, pending_prims(S) != 0)) {
+        if (S.tm0 == 0) {  // take the next pending group (any order is exact)
+            if (S.tm1 != 0) { S.tb0 = S.tb1; S.tm0 = S.tm1; S.tm1 = 0; }
+            else if (S.tm2 != 0) { S.tb0 = S.tb2; S.tm0 = S.tm2; S.tm2 = 0; }
+            else continue;
         }
-        int k = (int)S.tbase + __ffs(S.tmask) - 1;
-        S.tmask &= S.tmask - 1;
+        int k = (int)S.tb0 + __ffs(S.tm0) - 1;
+        S.tm0 &= S.tm0 - 1;
         const float4 *pr = W.prims + 3 * (int64_t)k;
         float4 a = __ldg(pr);
         uint32_t idw = __float_as_uint(a.w);
@@ -311,7 +331,7 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         if (!ok) continue;
         if (ANY) {
             S.h.prim = k;
-            S.ng.y = 0; S.sp = 0; S.tmask = 0; S.tmask2 = 0;
+            trav_clear(S);
             continue;
         }
         uint32_t gid = W.id_base + (idw & ~SPHERE_BIT);
@@ -473,7 +493,8 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
     const float INF = __int_as_float(0x7f800000);
     uint2 stack[WSTACK];
     TravState S;
-    S.ng = make_uint2(0, 0); S.sp = 0; S.tmask = 0; S.tmask2 = 0;
+    S.ng = make_uint2(0, 0);
+    trav_clear(S);
     uint32_t idx = 0;
     bool alive = false, exhausted = false;
     TraceCounters tc = {0, 0, 0, 0};
@@ -481,7 +502,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
     for (;;) {
         unsigned dead = __ballot_sync(FULL, !alive);
         int ndead = __popc(dead);
-        if (!exhausted && ndead >= REFILL_MIN) {
+        if (!exhausted && ndead >= (ANY ? REFILL_OCCL : REFILL_PATH)) {
             uint32_t base = 0;
             if (lane == 0) base = atomicAdd(fetch, (uint32_t)ndead);
             base = __shfl_sync(FULL, base, 0);
@@ -509,7 +530,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
             if (exhausted) break;
             continue;
         }
-        if (!alive) { S.ng.y = 0; S.sp = 0; S.tmask = 0; S.tmask2 = 0; }
+        if (!alive) trav_clear(S);
         bool fin = trav_step<ANY>(A.W, S, stack, tc, &A.ctr->overflow);
         if (!(alive && fin)) continue;
         // finished: volume march, then write the result back into the record
