@@ -347,6 +347,72 @@ def config3(nranks: int = 1, G: int = 1024, W: int = 1920, H: int = 1080) -> Sce
     return Scene("C3", parts, nranks, cam, fr, meta={"G": G})
 
 
+def cluster_palette(n: int, seed: int = 11) -> np.ndarray:
+    rng = np.random.Generator(np.random.Philox(seed))
+    return f32(0.25 + 0.7 * rng.uniform(size=(n, 3)))
+
+
+def partition_parts_mixed(sph: np.ndarray, sph_cluster: np.ndarray, palette: np.ndarray,
+                          verts: np.ndarray, idx: np.ndarray, mesh_albedo, nranks: int) -> List[Part]:
+    """Bisection of the centroids of ALL prims (spheres + triangles) into nranks groups;
+    within a rank: the mesh part, then one sphere part per cluster (commit order)."""
+    tri = verts[idx]
+    cen = np.concatenate([sph[:, :3].astype(np.float64), tri.astype(np.float64).mean(axis=1)])
+    grp = bisect_partition(cen, nranks) if nranks > 1 else np.zeros(cen.shape[0], np.int32)
+    gs, gt = grp[:sph.shape[0]], grp[sph.shape[0]:]
+    parts = []
+    for r in range(nranks):
+        t = tri[gt == r].reshape(-1, 3)
+        if t.shape[0]:
+            parts.append(Part(rank=r, kind=TRIS, albedo=mesh_albedo, verts=np.ascontiguousarray(t),
+                              idx=np.arange(t.shape[0], dtype=np.int32).reshape(-1, 3)))
+        sel = np.nonzero(gs == r)[0]
+        cl = sph_cluster[sel]
+        order = np.argsort(cl, kind="stable")
+        sel, cl = sel[order], cl[order]
+        bounds = np.flatnonzero(np.diff(cl)) + 1
+        for chunk in np.split(np.arange(sel.size), bounds):
+            if chunk.size == 0:
+                continue
+            c = int(cl[chunk[0]])
+            parts.append(Part(rank=r, kind=SPHERES, albedo=palette[c],
+                              spheres=np.ascontiguousarray(sph[sel[chunk]])))
+    return parts
+
+
+def config4(nranks: int = 8, n_clusters: int = 1000, per_cluster: int = 50_000, G: int = 211,
+            W: int = 1920, H: int = 1080, spp: int = 1) -> Scene:
+    """configs[3]: mixed scene -- 50M spheres (1000 Gaussian clusters, sigma 0.05, r in
+    [0.002, 0.004]) + a gyroid iso-surface (G=211, ~5M triangles) over N ranks by centroid
+    bisection; path tracing depth 4, one AO ray (r=0.1), shadow + bounce per vertex."""
+    sph = sphere_clusters(n_clusters, per_cluster, 0.05, 0.002, 0.004, seed=5)
+    cl = np.repeat(np.arange(n_clusters, dtype=np.int32), per_cluster)
+    verts, idx = gyroid_mesh(G)
+    parts = partition_parts_mixed(sph, cl, cluster_palette(n_clusters), verts, idx, (0.75, 0.75, 0.75),
+                                  nranks)
+    cam = camera_basis((2.2, 1.6, 2.8), (0, 0, 0), (0, 1, 0), 45.0, W, H)
+    fr = Frame(W=W, H=H, spp=spp, spp_batch=spp, max_depth=4, ao_k=1, ao_radius=0.1,
+               light_dir=f32(normalize((1, 1.5, 0.5))), E=(1, 1, 1), A=(0.4, 0.4, 0.4),
+               B=(0.05, 0.05, 0.05), seed=7)
+    return Scene("C4", parts, nranks, cam, fr,
+                 meta={"spheres": int(sph.shape[0]), "ntris": int(idx.shape[0])})
+
+
+def config5(nranks: int = 8, G_mesh: int = 950, G_vol: int = 1024, W: int = 3840, H: int = 2160,
+            spp: int = 64, spp_batch: int = 4, alpha_max: float = 0.02) -> Scene:
+    """configs[4]: 4K, 64 spp, ~100M-triangle gyroid + the 1024^3 volume bricks over N ranks
+    (depth 2, K=1, aoRadius 0.25, batches of 4 spp)."""
+    verts, idx = gyroid_mesh(G_mesh)
+    parts = split_mesh(verts, idx, nranks, (0.75, 0.75, 0.75))
+    parts += volume_bricks(G_vol, nranks, default_tf(alpha_max=alpha_max))
+    cam = camera_basis((2.2, 1.6, 2.8), (0, 0, 0), (0, 1, 0), 45.0, W, H)
+    h = float(np.float32(2.0 / (G_vol - 1)))
+    fr = Frame(W=W, H=H, spp=spp, spp_batch=spp_batch, max_depth=2, ao_k=1, ao_radius=0.25,
+               light_dir=f32(normalize((1, 1.5, 0.5))), E=(1, 1, 1), A=(0.4, 0.4, 0.4),
+               B=(0.05, 0.05, 0.05), dt=h, seed=7)
+    return Scene("C5", parts, nranks, cam, fr, meta={"ntris": int(idx.shape[0]), "G_vol": G_vol})
+
+
 def routing_hand_case(which: str) -> Scene:
     """SURVEY 8(c).4 hand cases H1-H3 (1x1 image, jitter 0.5, d = (0,0,1) exactly)."""
     cam = Camera(E=f32((0.2, 0.2, -1)), L=f32((-0.05, -0.05, 1)), U=f32((0.1, 0, 0)),

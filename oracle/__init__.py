@@ -81,6 +81,7 @@ def lib():
         L.or_render_dp.restype = ctypes.c_int
         L.or_render_dp.argtypes = [_P, _P, _P, _P, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P,
                                    ctypes.c_int]
+        L.or_set_brute.argtypes = [ctypes.c_int]
         L.or_philox.argtypes = [_P, _P, _P]
         L.or_u01.restype = ctypes.c_float
         L.or_u01.argtypes = [ctypes.c_uint32]
@@ -237,6 +238,11 @@ def render(scene: OracleScene, cam: di.Camera, fr: di.Frame, pixels=None, dp: bo
     if rc != 0:
         raise ValueError("or_render_union failed")
     return RenderResult(rgba, ev, oc, gen)
+
+
+def set_brute(on: bool):
+    """Trace by brute force over all prims instead of the oracle BVH (tests / debugging)."""
+    lib().or_set_brute(1 if on else 0)
 
 
 # ---- single-operation wrappers (used by the pin tests) ----------------------------------

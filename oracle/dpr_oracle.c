@@ -159,13 +159,16 @@ static v3 tri_normal(v3 e1, v3 e2, v3 d)
     return orient(n, d);
 }
 
-/* P4: sphere. */
+/* P4: sphere, reading R-SPHERE: the discriminant is taken from the perpendicular
+ * distance, disc = r^2 - |f - b d|^2 (cancellation-free, Ray Tracing Gems I ch. 7), instead
+ * of b^2 - (|f|^2 - r^2), whose rounding error (~ulp(|f|^2)) rivals r^2 for small distant
+ * spheres and reports "hits" outside the sphere's own bounding box. */
 static int sphere_hit(v3 o, v3 d, float tmax, v3 c, float r, float *t_out)
 {
     v3 f = vsub(o, c);
     float b = vdot(f, d);
-    float cc = vdot(f, f) - r * r;
-    float disc = b * b - cc;
+    v3 q = V3(f.x - b * d.x, f.y - b * d.y, f.z - b * d.z);
+    float disc = r * r - vdot(q, q);
     if (disc < 0.0f) return 0;
     float sq = sqrtf(disc);
     float t = -b - sq;
@@ -487,10 +490,19 @@ static int prim_any(const OPrim *p, v3 o, v3 d, float tmax)
     return sphere_hit(o, d, tmax, p->a, p->b.x, &t);
 }
 
+/* Test switch: trace by brute force over the BVH's prim list instead of the BVH (the P9
+ * definition itself); used by tests to pin the BVH on large scenes. */
+static int g_brute = 0;
+OR_EXPORT void or_set_brute(int on) { g_brute = on; }
+
 /* Closest hit through the oracle BVH (equals brute force; pinned by tests). */
 static void bvh_closest(const OBVH *b, const OPrim *prims, v3 o, v3 d, float tmax, OHit *best)
 {
     if (b->n == 0) return;
+    if (g_brute) {
+        for (int64_t i = 0; i < b->n; ++i) prim_closest(&prims[b->ref[i]], o, d, tmax, best);
+        return;
+    }
     double od[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
     int64_t stack[128];
     int sp = 0;
@@ -513,6 +525,10 @@ static void bvh_closest(const OBVH *b, const OPrim *prims, v3 o, v3 d, float tma
 static int bvh_any(const OBVH *b, const OPrim *prims, v3 o, v3 d, float tmax)
 {
     if (b->n == 0) return 0;
+    if (g_brute) {
+        for (int64_t i = 0; i < b->n; ++i) if (prim_any(&prims[b->ref[i]], o, d, tmax)) return 1;
+        return 0;
+    }
     double od[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
     int64_t stack[128];
     int sp = 0;

@@ -121,11 +121,13 @@ __device__ __forceinline__ f3 tri_normal(f3 e1, f3 e2, f3 d) {
     return orient(mk(ng.x / len, ng.y / len, ng.z / len), d);
 }
 
+// P4 with reading R-SPHERE: disc = r^2 - |f - b d|^2 (cancellation-free; the
+// b^2 - (|f|^2 - r^2) form reports hits outside a small distant sphere's bounding box).
 __device__ __forceinline__ bool sphere_hit(f3 o, f3 d, float tmax, f3 c, float r, float &t) {
     f3 f = sub(o, c);
     float b = dot(f, d);
-    float cc = dot(f, f) - r * r;
-    float disc = b * b - cc;
+    f3 q = mk(f.x - b * d.x, f.y - b * d.y, f.z - b * d.z);
+    float disc = r * r - dot(q, q);
     if (disc < 0.0f) return false;
     float sq = sqrtf(disc);
     t = -b - sq;

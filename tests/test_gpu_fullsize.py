@@ -67,3 +67,16 @@ def test_nccl_collectives_single_rank(monkeypatch):
     g = gpu_render(parts, 1, sc.camera, sc.frame)
     o = oracle_render(parts, 1, sc.camera, sc.frame)
     assert_parity(g, o)
+
+
+def test_config4_full_size_sampled():
+    """configs[3] at full size on one rank (50M spheres in 1000 cluster parts + ~5M
+    triangles, 1920x1080, depth 4): every event/occlusion bit of 1500 sampled pixels."""
+    sc = di.config4(nranks=1)
+    g = gpu_render(sc.parts, 1, sc.camera, sc.frame)
+    P = sc.frame.W * sc.frame.H
+    pix = np.sort(np.random.default_rng(4).choice(P, 1500, replace=False))
+    o = oracle_render(sc.parts, 1, sc.camera, sc.frame, pixels=pix, dp=False)
+    assert np.array_equal(g[1][:, :, pix], o.events)
+    assert np.array_equal(g[2][:, :, pix], o.occl)
+    assert_pixels_close(g[0][pix], o.rgba)

@@ -146,3 +146,23 @@ def test_single_triangle_and_single_sphere():
         g = gpu_render([part], 1, cam, fr)
         o = oracle_render([part], 1, cam, fr)
         assert_parity(g, o)
+
+
+@pytest.mark.parametrize("nranks", [1, 8])
+def test_config4_family_small(nranks):
+    """configs[3] family: Gaussian sphere clusters (per-cluster albedo parts) + gyroid mesh,
+    partitioned over all prims by centroid bisection, path tracing depth 4, K=1 AO."""
+    sc = di.config4(nranks=nranks, n_clusters=24, per_cluster=400, G=41, W=72, H=40, spp=2)
+    g = gpu_render(sc.parts, nranks, sc.camera, sc.frame)
+    o = oracle_render(sc.parts, nranks, sc.camera, sc.frame)
+    assert (o.events[:, 3] != 0).sum() > 100  # paths reach depth 4
+    assert_parity(g, o)
+
+
+def test_config5_family_small():
+    """configs[4] family: gyroid mesh + volume bricks on 4 ranks, depth 2, K=1, spp batches."""
+    sc = di.config5(nranks=4, G_mesh=51, G_vol=49, W=80, H=45, spp=4, spp_batch=2, alpha_max=0.6)
+    g = gpu_render(sc.parts, 4, sc.camera, sc.frame)
+    o = oracle_render(sc.parts, 4, sc.camera, sc.frame)
+    assert ((o.events & 0x80000000) != 0).sum() > 20
+    assert_parity(g, o)

@@ -210,3 +210,47 @@ def test_transfer_function_examples():
     assert np.allclose(r[:3], 0.5, atol=1e-6) and r[3] == 1.0
     r = orc.tf_eval(tf, 0, 1, 0.5, 0.5)
     assert abs(r[3] - 0.25) < 1e-6
+
+
+def test_bvh_equals_brute_force_tiny_clustered_spheres():
+    """P9 on the configs[3] sphere family (dense Gaussian clusters of r ~ 0.003 spheres, rays
+    from inside and outside the clusters): oracle BVH closest/any == brute force.  This pins
+    reading R-SPHERE: with the b^2-(|f|^2-r^2) discriminant, rounding let small distant
+    spheres report hits outside their own bounding box, which no BVH can find."""
+    sph = di.sphere_clusters(6, 1500, 0.05, 0.002, 0.004, seed=5)
+    sc = orc.OracleScene([di.Part(0, di.SPHERES, spheres=sph)], 1)
+    rng = np.random.default_rng(9)
+    centres = sph[:, :3].astype(np.float64)
+    mism = 0
+    for k in range(6000):
+        if k % 2 == 0:   # from far away toward a random sphere
+            o = rng.uniform(-2.5, 2.5, 3)
+            tgt = centres[rng.integers(len(centres))] + rng.normal(0, 0.004, 3)
+        else:            # from inside a cluster
+            o = centres[rng.integers(len(centres))] + rng.normal(0, 0.01, 3)
+            tgt = o + rng.normal(0, 1, 3)
+        d = (tgt - o) / np.linalg.norm(tgt - o)
+        o, d = o.astype(np.float32), d.astype(np.float32)
+        tm = np.inf if k % 3 else 0.1
+        a = sc.closest(o, d, tm, brute=True)
+        b = sc.closest(o, d, tm)
+        mism += a != b
+        assert sc.any_hit(o, d, tm, True) == sc.any_hit(o, d, tm)
+    assert mism == 0
+
+
+def test_sphere_far_tangent_is_box_consistent():
+    """R-SPHERE: a reported hit lies within the sphere's box (up to float rounding) even for
+    a tiny sphere far from the ray origin."""
+    c = np.array([1.7, -0.3, 0.9], np.float32)
+    r = np.float32(0.003)
+    rng = np.random.default_rng(2)
+    for _ in range(4000):
+        o = rng.uniform(-2, 2, 3).astype(np.float32)
+        tgt = c + rng.uniform(-1.2, 1.2, 3) * r
+        d = ((tgt - o) / np.linalg.norm(tgt - o)).astype(np.float32)
+        h = orc.sphere_hit(o, d, c, float(r))
+        if h is None:
+            continue
+        p = o.astype(np.float64) + h[0] * d.astype(np.float64)
+        assert np.all(np.abs(p - c) <= r * (1 + 1e-3) + 1e-6), (p - c, r)
