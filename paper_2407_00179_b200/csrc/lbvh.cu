@@ -581,37 +581,58 @@ void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t
 // the index range that the value range maps to (widened by one entry on each side) has
 // alpha > 0 -- exact skipping (u >= 0 is never < 0).
 // ---------------------------------------------------------------------------------------
-__global__ void k_macrocells(const float *__restrict__ vox, int nx, int ny, int nz, int mcx,
-                             int mcy, int mcz, const float4 *__restrict__ tf, float tf_lo,
-                             float tf_hi, float dscale, uint8_t *mc) {
-    int m = blockIdx.x;
-    int mx = m % mcx, my = (m / mcx) % mcy, mz = m / (mcx * mcy);
-    int x0 = mx * MC_SIZE, y0 = my * MC_SIZE, z0 = mz * MC_SIZE;
-    int x1 = min(x0 + MC_SIZE, nx - 1), y1 = min(y0 + MC_SIZE, ny - 1), z1 = min(z0 + MC_SIZE, nz - 1);
-    int sx = x1 - x0 + 1, sy = y1 - y0 + 1, sz = z1 - z0 + 1;
-    float vmin = __int_as_float(0x7f800000), vmax = -vmin;
-    for (int t = threadIdx.x; t < sx * sy * sz; t += blockDim.x) {
-        int x = x0 + t % sx, y = y0 + (t / sx) % sy, z = z0 + t / (sx * sy);
-        float v = vox[(int64_t)x + (int64_t)nx * ((int64_t)y + (int64_t)ny * z)];
-        vmin = fminf(vmin, v);
-        vmax = fmaxf(vmax, v);
-    }
-    __shared__ float smin[32], smax[32];
-    for (int o = 16; o > 0; o >>= 1) {
-        vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
-        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-    }
-    if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = vmin; smax[threadIdx.x >> 5] = vmax; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { vmin = fminf(vmin, smin[w]); vmax = fmaxf(vmax, smax[w]); }
-        float xa = fminf(fmaxf((vmin - tf_lo) / (tf_hi - tf_lo), 0.0f), 1.0f) * 255.0f;
-        float xb = fminf(fmaxf((vmax - tf_lo) / (tf_hi - tf_lo), 0.0f), 1.0f) * 255.0f;
-        int ja = max((int)floorf(xa) - 1, 0), jb = min((int)floorf(xb) + 2, 255);
-        bool active = false;
-        for (int j = ja; j <= jb; ++j) active |= tf[j].w * dscale > 0.0f || tf[j].w != 0.0f;
-        if (!(vmin == vmin) || !(vmax == vmax)) active = true;  // NaN voxels: never skip
-        mc[m] = active ? 1 : 0;
+// One block per (macrocell row along x, macrocell y, macrocell z): threads sweep the voxel
+// rows of the slab with x fastest (coalesced), each thread keeps min/max of its x columns,
+// then per-macrocell reductions in shared memory.
+constexpr int MC_BLOCK = 256;
+__global__ void __launch_bounds__(MC_BLOCK) k_macrocells(const float *__restrict__ vox, int nx, int ny, int nz,
+                                                        int mcx, int mcy, int mcz, const float4 *__restrict__ tf,
+                                                        float tf_lo, float tf_hi, float dscale, uint8_t *mc) {
+    const int my = blockIdx.x, mz = blockIdx.y;
+    const int y0 = my * MC_SIZE, z0 = mz * MC_SIZE;
+    const int y1 = min(y0 + MC_SIZE, ny - 1), z1 = min(z0 + MC_SIZE, nz - 1);
+    __shared__ float smin[MC_BLOCK], smax[MC_BLOCK];
+    // process the x extent in chunks of MC_BLOCK voxels (each chunk covers MC_BLOCK/16
+    // macrocells; the +1 overlap voxel is read by the next macrocell's range too)
+    for (int xc = 0; xc < mcx * MC_SIZE; xc += MC_BLOCK - MC_BLOCK % MC_SIZE) {
+        const int x = xc + threadIdx.x;
+        float vmin = __int_as_float(0x7f800000), vmax = -vmin;
+        if (x < nx) {
+            for (int z = z0; z <= z1; ++z)
+                for (int y = y0; y <= y1; ++y) {
+                    float v = vox[(int64_t)x + (int64_t)nx * ((int64_t)y + (int64_t)ny * z)];
+                    vmin = fminf(vmin, v);
+                    vmax = fmaxf(vmax, v);
+                }
+        }
+        smin[threadIdx.x] = vmin;
+        smax[threadIdx.x] = vmax;
+        __syncthreads();
+        const int per = (MC_BLOCK - MC_BLOCK % MC_SIZE) / MC_SIZE;  // macrocells per chunk
+        if ((int)threadIdx.x < per) {
+            const int mx = xc / MC_SIZE + threadIdx.x;
+            if (mx < mcx) {
+                const int xa = mx * MC_SIZE - xc, xb = min(mx * MC_SIZE + MC_SIZE, nx - 1) - xc;
+                float a = __int_as_float(0x7f800000), b = -a;
+                for (int t = xa; t <= xb && t < MC_BLOCK; ++t) { a = fminf(a, smin[t]); b = fmaxf(b, smax[t]); }
+                if (xb >= MC_BLOCK) {  // the overlap voxel belongs to the next chunk: read it
+                    const int xg = xc + xb;
+                    for (int z = z0; z <= z1; ++z)
+                        for (int y = y0; y <= y1; ++y) {
+                            float v = vox[(int64_t)xg + (int64_t)nx * ((int64_t)y + (int64_t)ny * z)];
+                            a = fminf(a, v);
+                            b = fmaxf(b, v);
+                        }
+                }
+                float xa_ = fminf(fmaxf((a - tf_lo) / (tf_hi - tf_lo), 0.0f), 1.0f) * 255.0f;
+                float xb_ = fminf(fmaxf((b - tf_lo) / (tf_hi - tf_lo), 0.0f), 1.0f) * 255.0f;
+                int ja = max((int)floorf(xa_) - 1, 0), jb = min((int)floorf(xb_) + 2, 255);
+                bool active = !(a == a) || !(b == b);  // NaN voxels: never skip
+                for (int j = ja; j <= jb; ++j) active |= tf[j].w != 0.0f;
+                mc[((int64_t)mz * mcy + my) * mcx + mx] = active ? 1 : 0;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -676,8 +697,8 @@ void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, floa
 void launch_macrocells(const float *vox, int nx, int ny, int nz, int mcx, int mcy, int mcz,
                        const float4 *tf, float tf_lo, float tf_hi, float dscale, uint8_t *mc,
                        cudaStream_t s) {
-    int n = mcx * mcy * mcz;
-    if (n > 0) k_macrocells<<<n, 128, 0, s>>>(vox, nx, ny, nz, mcx, mcy, mcz, tf, tf_lo, tf_hi, dscale, mc);
+    if (mcx > 0 && mcy > 0 && mcz > 0)
+        k_macrocells<<<dim3(mcy, mcz), MC_BLOCK, 0, s>>>(vox, nx, ny, nz, mcx, mcy, mcz, tf, tf_lo, tf_hi, dscale, mc);
 }
 
 }  // namespace dpr

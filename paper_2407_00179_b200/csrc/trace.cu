@@ -385,8 +385,25 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
             continue;
         float fx0 = floorf(g.x), fy0 = floorf(g.y), fz0 = floorf(g.z);
         int ix = (int)fx0 - B.lo[0], iy = (int)fy0 - B.lo[1], iz = (int)fz0 - B.lo[2];
-        if (!__ldg(B.mc + ((iz / MC_SIZE) * B.mc_dims[1] + iy / MC_SIZE) * B.mc_dims[0] + ix / MC_SIZE))
-            continue;  // exact skip: alpha == 0 for every sample in this macrocell
+        const int mx = ix / MC_SIZE, my = iy / MC_SIZE, mz = iz / MC_SIZE;
+        if (!__ldg(B.mc + (mz * B.mc_dims[1] + my) * B.mc_dims[0] + mx)) {
+            // alpha == 0 for every sample in this macrocell: skipping is exact.  Jump to one
+            // sample before the ray leaves the macrocell's box (the margin of >= 1 voxel
+            // absorbs the rounding of t -> p -> g); the per-sample tests resume there.
+            float mlo[3], mhi[3];
+            const int mc3[3] = {mx, my, mz};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                int c0 = B.lo[c] + mc3[c] * MC_SIZE, c1 = min(c0 + MC_SIZE, B.hi[c]);
+                mlo[c] = B.O[c] + (float)c0 * B.h[c];
+                mhi[c] = B.O[c] + (float)c1 * B.h[c];
+            }
+            float m0, m1;
+            slab(mlo, mhi, o, d, tmax, m0, m1);
+            const int64_t jump = (int64_t)floorf(m1 / dt - 0.5f) - 2;
+            if (jump > i) i = jump;  // loop ++i resumes at jump + 1
+            continue;
+        }
         nsamples++;
         float fx = g.x - fx0, fy = g.y - fy0, fz = g.z - fz0;
         const float *v = B.vox + (int64_t)ix + (int64_t)nx * ((int64_t)iy + (int64_t)ny * iz);
