@@ -188,9 +188,12 @@ DPR_API int dpr_commit_part(dpr_device dev, const dpr_part_desc *part);
 DPR_API int dpr_clear_parts(dpr_device dev);
 
 /* LOCAL: (re)build the rank's acceleration structures from the committed parts, on the
- * GPU: per-prim AABBs, 63-bit Morton codes, LSD radix sort, Karras hierarchy, bottom-up
- * refit (LBVH; "negligible pre-processing time") and brick macrocells.  May
- * be called again to rebuild from the resident parts. */
+ * GPU: per-prim AABBs, 63-bit Morton codes, LSD radix sort, Karras hierarchy (or PLOC with
+ * env DPR_BUILDER=ploc), bottom-up refit, collapse into a compressed 8-wide BVH ("negligible
+ * pre-processing time") and brick macrocells.  May be called again to rebuild
+ * from the resident parts.  DPR_ERR_INVALID_ARG if a triangle index is out of range
+ * (validated on the GPU here, not at commit_part) or a bounds_hint does not contain its
+ * part; the world is then not ready. */
 DPR_API int dpr_commit_world(dpr_device dev);
 
 /* COLLECTIVE (getProperty(WAIT) on the world): union of all ranks' world

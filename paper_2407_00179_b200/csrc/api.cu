@@ -232,8 +232,8 @@ int build_world(Dev *d) {
     d->nprims = n;
     int np = (int)d->parts.size();
     // per-part bounds + overall centroid box
-    RET(ensure(d, d->b_bounds, sizeof(int) * 12 * (np + 1)));
-    std::vector<int> binit(12 * (np + 1));
+    RET(ensure(d, d->b_bounds, sizeof(int) * (12 * (np + 1) + 1)));
+    std::vector<int> binit(12 * (np + 1) + 1, 0);  // last word: bad triangle index flag
     for (int k = 0; k <= np; ++k)
         for (int c = 0; c < 12; ++c) binit[12 * k + c] = (c % 6) < 3 ? 0x7fffffff : (int)0x80000000;
     CK(cudaMemcpyAsync(d->b_bounds.p, binit.data(), binit.size() * sizeof(int), cudaMemcpyHostToDevice, s));
@@ -247,8 +247,9 @@ int build_world(Dev *d) {
     for (int k = 0; k < np; ++k) {
         PartStore &p = d->parts[k];
         if (p.kind == DPR_PART_TRIANGLES) {
-            launch_tri_prims(P<float>(p.verts), P<int32_t>(p.idx), p.nt, (uint32_t)off,
-                             P<float4>(d->b_prims_u), P<float4>(d->b_blo), P<float4>(d->b_bhi), s);
+            launch_tri_prims(P<float>(p.verts), P<int32_t>(p.idx), p.nt, p.nv, (uint32_t)off,
+                             P<float4>(d->b_prims_u), P<float4>(d->b_blo), P<float4>(d->b_bhi),
+                             P<int>(d->b_bounds) + 12 * (np + 1), s);
         } else if (p.kind == DPR_PART_SPHERES) {
             launch_sphere_prims(P<float4>(p.spheres), p.ns, (uint32_t)off, P<float4>(d->b_prims_u),
                                 P<float4>(d->b_blo), P<float4>(d->b_bhi), s);
@@ -277,9 +278,10 @@ int build_world(Dev *d) {
         launches += 2;
         CK(cudaMemcpyAsync(hist.data(), d->b_hist.p, sizeof(unsigned long long) * 8 * 256, cudaMemcpyDeviceToHost, s));
     }
-    std::vector<int> bnd(12 * (np + 1));
+    std::vector<int> bnd(12 * (np + 1) + 1);
     CK(cudaMemcpyAsync(bnd.data(), d->b_bounds.p, bnd.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (bnd[12 * (np + 1)]) return fail(DPR_ERR_INVALID_ARG, "triangle index out of range (checked on the GPU)");
     auto ord2f = [](int i) { int j = i >= 0 ? i : i ^ 0x7fffffff; float f; memcpy(&f, &j, 4); return f; };
     // rank box = exact union of prim boxes and brick cell-domain boxes (P8)
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -1071,9 +1073,6 @@ int dpr_commit_part(dpr_device dev, const dpr_part_desc *part) {
     if (p.kind == DPR_PART_TRIANGLES) {
         p.nv = part->n_verts;
         p.nt = part->n_tris;
-        if (part->memory == DPR_MEMORY_HOST)
-            for (int64_t i = 0; i < 3 * p.nt; ++i)
-                if (part->idx[i] < 0 || part->idx[i] >= p.nv) return fail(DPR_ERR_INVALID_ARG, "triangle index out of range");
         RET(copy_in(d, p.verts, part->verts, sizeof(float) * 3 * p.nv, part->memory));
         RET(copy_in(d, p.idx, part->idx, sizeof(int32_t) * 3 * p.nt, part->memory));
     } else if (p.kind == DPR_PART_SPHERES) {

@@ -34,10 +34,15 @@ __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i
 
 // ---------------------------------------------------------------------------------------
 __global__ void k_tri_prims(const float *__restrict__ verts, const int32_t *__restrict__ idx,
-                            int64_t n, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi) {
+                            int64_t n, int64_t nv, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi,
+                            int *bad_index) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     int64_t i0 = idx[3 * t], i1 = idx[3 * t + 1], i2 = idx[3 * t + 2];
+    if (i0 < 0 || i0 >= nv || i1 < 0 || i1 >= nv || i2 < 0 || i2 >= nv) {  // validated here, on the GPU
+        atomicExch(bad_index, 1);
+        i0 = i1 = i2 = 0;
+    }
     f3 v0 = mk(verts[3 * i0], verts[3 * i0 + 1], verts[3 * i0 + 2]);
     f3 v1 = mk(verts[3 * i1], verts[3 * i1 + 1], verts[3 * i1 + 2]);
     f3 v2 = mk(verts[3 * i2], verts[3 * i2 + 1], verts[3 * i2 + 2]);
@@ -640,9 +645,9 @@ __global__ void __launch_bounds__(MC_BLOCK) k_macrocells(const float *__restrict
 // Host-side launchers.
 // ---------------------------------------------------------------------------------------
 
-void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, uint32_t local0,
-                      float4 *prims, float4 *blo, float4 *bhi, cudaStream_t s) {
-    if (n > 0) k_tri_prims<<<nblk(n, 256), 256, 0, s>>>(verts, idx, n, local0, prims, blo, bhi);
+void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, int64_t nv, uint32_t local0,
+                      float4 *prims, float4 *blo, float4 *bhi, int *bad_index, cudaStream_t s) {
+    if (n > 0) k_tri_prims<<<nblk(n, 256), 256, 0, s>>>(verts, idx, n, nv, local0, prims, blo, bhi, bad_index);
 }
 void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims,
                          float4 *blo, float4 *bhi, cudaStream_t s) {
