@@ -35,6 +35,7 @@ struct Dev;
 struct Buf {
     void *p = nullptr;
     size_t bytes = 0;
+    bool raw = false;  // cudaMalloc'd (IPC-exportable), not from the allocator
 };
 
 struct PartStore {
@@ -113,6 +114,16 @@ struct Dev {
     int frame_done = 0;
     int mapped_w = 0, mapped_h = 0;
     int spw = 16;  // max samples per warp in primary generation (env DPR_SPW; sweep r01)
+    // exchange: 0 = per-step counts allgather + grouped ncclSend/ncclRecv (send-recv);
+    //           1 = fused: kernels append straight into the destination rank's next queue
+    //               (peer pointers, remote tail atomics); env DPR_EXCHANGE=fused|sendrecv
+    int exch = 0;
+    Buf b_tails;                                  // [parity][kind] next-queue tails (fused)
+    PathRec *peer_path[2][DPR_MAX_RANKS] = {};    // fused: every rank's queues, both parities
+    OcclRec *peer_occl[2][DPR_MAX_RANKS] = {};
+    uint32_t *peer_tails[DPR_MAX_RANKS] = {};
+    std::vector<void *> ipc_opened;               // peer mappings to close
+    uint64_t ipc_sig = 0;                         // signature of the exported buffers
     int64_t build_launches = 0, frame_launches = 0, frame_exch_bytes = 0, tpl = 0, tol = 0;
     double ms_build = 0;
     bool dumps_valid = false;
@@ -157,6 +168,14 @@ void *dmalloc(Dev *d, size_t bytes) {
 
 void dfree(Dev *d, Buf &b) {
     if (!b.p) return;
+    if (b.raw) {
+        cudaStreamSynchronize(d->stream);
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+        b.raw = false;
+        return;
+    }
     if (d->has_alloc) d->alloc.free(d->alloc.ctx, b.p, b.bytes, d->stream);
     else cudaFreeAsync(b.p, d->stream);
     b.p = nullptr;
@@ -170,6 +189,21 @@ int ensure(Dev *d, Buf &b, size_t bytes) {
     b.p = dmalloc(d, bytes);
     if (!b.p) return fail(DPR_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
     b.bytes = bytes;
+    return DPR_OK;
+}
+
+// cudaMalloc'd buffer (exportable with cudaIpcGetMemHandle for the fused NCCL exchange)
+int ensure_raw(Dev *d, Buf &b, size_t bytes, bool *changed) {
+    if (b.bytes >= bytes && b.p && b.raw) return DPR_OK;
+    dfree(d, b);
+    if (bytes == 0) return DPR_OK;
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+        b.p = nullptr;
+        return fail(DPR_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    }
+    b.bytes = bytes;
+    b.raw = true;
+    if (changed) *changed = true;
     return DPR_OK;
 }
 
@@ -525,14 +559,26 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
         RET(ensure(d, d->b_events, sizeof(uint32_t) * nd));
         RET(ensure(d, d->b_occl, sizeof(uint32_t) * nd));
     }
+    const bool ipc = d->exch && d->comm;
     for (int i = 0; i < 2; ++i) {
-        RET(ensure(d, d->b_path[i], sizeof(PathRec) * (size_t)pcap));
-        RET(ensure(d, d->b_occlq[i], sizeof(OcclRec) * (size_t)ocap));
+        if (ipc) {
+            RET(ensure_raw(d, d->b_path[i], sizeof(PathRec) * (size_t)pcap, nullptr));
+            RET(ensure_raw(d, d->b_occlq[i], sizeof(OcclRec) * (size_t)ocap, nullptr));
+        } else {
+            RET(ensure(d, d->b_path[i], sizeof(PathRec) * (size_t)pcap));
+            RET(ensure(d, d->b_occlq[i], sizeof(OcclRec) * (size_t)ocap));
+        }
     }
-    for (int r = 0; r < N; ++r) {
-        if (r == d->rank) continue;
-        RET(ensure(d, d->b_send_path[r], sizeof(PathRec) * (size_t)pcap));
-        RET(ensure(d, d->b_send_occl[r], sizeof(OcclRec) * (size_t)ocap));
+    if (d->exch) {
+        if (ipc) RET(ensure_raw(d, d->b_tails, sizeof(uint32_t) * 4, nullptr));
+        else RET(ensure(d, d->b_tails, sizeof(uint32_t) * 4));
+        CK(cudaMemsetAsync(d->b_tails.p, 0, sizeof(uint32_t) * 4, d->stream));
+    } else {
+        for (int r = 0; r < N; ++r) {
+            if (r == d->rank) continue;
+            RET(ensure(d, d->b_send_path[r], sizeof(PathRec) * (size_t)pcap));
+            RET(ensure(d, d->b_send_occl[r], sizeof(OcclRec) * (size_t)ocap));
+        }
     }
     d->path_cap = pcap;
     d->occl_cap = ocap;
@@ -597,11 +643,21 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.Q.path_in = P<PathRec>(d->b_path[cur]);
     a.Q.occl_in = P<OcclRec>(d->b_occlq[cur]);
     a.Q.in_count = P<uint32_t>(d->b_in_count);
+    a.Q.fused = d->exch;
     for (int r = 0; r < d->nranks; ++r) {
-        a.Q.path_out[r] = r == d->rank ? P<PathRec>(d->b_path[nxt]) : P<PathRec>(d->b_send_path[r]);
-        a.Q.occl_out[r] = r == d->rank ? P<OcclRec>(d->b_occlq[nxt]) : P<OcclRec>(d->b_send_occl[r]);
+        if (d->exch) {
+            a.Q.path_out[r] = d->peer_path[nxt][r];
+            a.Q.occl_out[r] = d->peer_occl[nxt][r];
+            a.Q.cnt_path[r] = d->peer_tails[r] + 2 * nxt;
+            a.Q.cnt_occl[r] = d->peer_tails[r] + 2 * nxt + 1;
+        } else {
+            a.Q.path_out[r] = r == d->rank ? P<PathRec>(d->b_path[nxt]) : P<PathRec>(d->b_send_path[r]);
+            a.Q.occl_out[r] = r == d->rank ? P<OcclRec>(d->b_occlq[nxt]) : P<OcclRec>(d->b_send_occl[r]);
+            a.Q.cnt_path[r] = P<uint32_t>(d->b_counts) + r;
+            a.Q.cnt_occl[r] = P<uint32_t>(d->b_counts) + d->nranks + r;
+        }
     }
-    a.Q.out_count = P<uint32_t>(d->b_counts);
+    if (d->exch) a.Q.in_count = P<uint32_t>(d->b_tails) + 2 * cur;
     a.Q.path_cap = d->path_cap;
     a.Q.occl_cap = d->occl_cap;
     a.Q.fetch = P<uint32_t>(d->b_fetch);
@@ -647,6 +703,104 @@ int gather_counts(std::vector<Dev *> &L, std::vector<int64_t> &C, unsigned &over
     return DPR_OK;
 }
 
+// Fused exchange: every rank learns every rank's next-queue pointers and tails.  Loopback:
+// the virtual ranks' buffers directly.  NCCL mode: cudaIpc handles of the cudaMalloc'd queues
+// are allgathered over NCCL and opened (NVLink peer mappings), re-done when buffers change.
+struct IpcMsg {
+    cudaIpcMemHandle_t h[5];  // path[0], path[1], occl[0], occl[1], tails
+    uint64_t sig;
+};
+
+int fused_peers(std::vector<Dev *> &L) {
+    Dev *d0 = L[0];
+    const int N = d0->nranks;
+    if (d0->group) {
+        for (Dev *d : L)
+            for (int r = 0; r < N; ++r) {
+                Dev *q = L[r];
+                for (int k = 0; k < 2; ++k) {
+                    d->peer_path[k][r] = P<PathRec>(q->b_path[k]);
+                    d->peer_occl[k][r] = P<OcclRec>(q->b_occlq[k]);
+                }
+                d->peer_tails[r] = P<uint32_t>(q->b_tails);
+            }
+        return DPR_OK;
+    }
+    Dev *d = d0;
+    void *mine[5] = {d->b_path[0].p, d->b_path[1].p, d->b_occlq[0].p, d->b_occlq[1].p, d->b_tails.p};
+    uint64_t sig = 1469598103934665603ull;
+    for (void *p : mine) sig = fnv1a(&p, sizeof(p), sig);
+    IpcMsg msg;
+    memset(&msg, 0, sizeof(msg));
+    for (int k = 0; k < 5; ++k) CK(cudaIpcGetMemHandle(&msg.h[k], mine[k]));
+    msg.sig = sig;
+    std::vector<const void *> sends = {&msg};
+    std::vector<std::vector<char>> out;
+    // every rank reallocates at the same frames (same frame descriptor); the signature check
+    // keeps the (collective) decision identical on all ranks anyway
+    uint64_t all_sig = 0;
+    {
+        std::vector<const void *> sg = {&sig};
+        std::vector<std::vector<char>> so;
+        RET(allgather_host(L, sg, sizeof(sig), so));
+        for (int r = 0; r < N; ++r) all_sig = fnv1a(so[0].data() + 8 * r, 8, all_sig);
+    }
+    if (all_sig == d->ipc_sig && d->peer_tails[d->rank]) return DPR_OK;
+    RET(allgather_host(L, sends, sizeof(IpcMsg), out));
+    for (void *p : d->ipc_opened) cudaIpcCloseMemHandle(p);
+    d->ipc_opened.clear();
+    const IpcMsg *all = reinterpret_cast<const IpcMsg *>(out[0].data());
+    for (int r = 0; r < N; ++r) {
+        void *ptr[5];
+        for (int k = 0; k < 5; ++k) {
+            if (r == d->rank) { ptr[k] = mine[k]; continue; }
+            CK(cudaIpcOpenMemHandle(&ptr[k], all[r].h[k], cudaIpcMemLazyEnablePeerAccess));
+            d->ipc_opened.push_back(ptr[k]);
+        }
+        d->peer_path[0][r] = (PathRec *)ptr[0];
+        d->peer_path[1][r] = (PathRec *)ptr[1];
+        d->peer_occl[0][r] = (OcclRec *)ptr[2];
+        d->peer_occl[1][r] = (OcclRec *)ptr[3];
+        d->peer_tails[r] = (uint32_t *)ptr[4];
+    }
+    d->ipc_sig = all_sig;
+    return DPR_OK;
+}
+
+// Fused step boundary: per-rank next-queue counts (path, occl) + overflow flags of all ranks.
+// NCCL mode: a 3-word allgather on the stream (it also orders every rank's appends of this
+// step before anyone's next step).  rows[r] = {path, occl, overflow}.
+int fused_sync(std::vector<Dev *> &L, const std::vector<int> &cur, std::vector<uint32_t> &rows) {
+    Dev *d0 = L[0];
+    const int N = d0->nranks;
+    rows.assign((size_t)3 * N, 0);
+    if (!d0->comm) {
+        for (size_t i = 0; i < L.size(); ++i) {
+            Dev *d = L[i];
+            int nxt = cur[i] ^ 1;
+            CK(cudaMemcpyAsync(d->h_counts, P<uint32_t>(d->b_tails) + 2 * nxt, sizeof(uint32_t) * 2,
+                               cudaMemcpyDeviceToHost, d->stream));
+            CK(cudaMemcpyAsync(d->h_counts + 2, &P<Counters>(d->b_ctr)->overflow, sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, d->stream));
+        }
+        for (Dev *d : L) CK(cudaStreamSynchronize(d->stream));
+        for (Dev *d : L)
+            for (int k = 0; k < 3; ++k) rows[3 * d->rank + k] = d->h_counts[k];
+        return DPR_OK;
+    }
+    Dev *d = d0;
+    int nxt = cur[0] ^ 1;
+    RET(ensure(d, d->b_scratch, sizeof(uint32_t) * 3 * (N + 1)));
+    uint32_t *sb = P<uint32_t>(d->b_scratch), *rb = sb + 3;
+    CK(cudaMemcpyAsync(sb, P<uint32_t>(d->b_tails) + 2 * nxt, sizeof(uint32_t) * 2, cudaMemcpyDeviceToDevice, d->stream));
+    CK(cudaMemcpyAsync(sb + 2, &P<Counters>(d->b_ctr)->overflow, sizeof(uint32_t), cudaMemcpyDeviceToDevice, d->stream));
+    NK(ncclAllGather(sb, rb, 3, ncclUint32, d->comm, d->stream));
+    CK(cudaMemcpyAsync(d->h_counts, rb, sizeof(uint32_t) * 3 * N, cudaMemcpyDeviceToHost, d->stream));
+    CK(cudaStreamSynchronize(d->stream));
+    for (int k = 0; k < 3 * N; ++k) rows[k] = d->h_counts[k];
+    return DPR_OK;
+}
+
 int render_group(std::vector<Dev *> &L) {
     Dev *d0 = L[0];
     const int N = d0->nranks;
@@ -665,6 +819,8 @@ int render_group(std::vector<Dev *> &L) {
     memset(&fc.R, 0, sizeof(fc.R));
     RET(frame_setup(L, fc));
     for (Dev *d : L) RET(frame_buffers(d, fc));
+    const bool fused = d0->exch != 0;
+    if (fused) RET(fused_peers(L));
     const int64_t P_ = (int64_t)f.W * f.H;
     const int nb = (f.spp + f.spp_batch - 1) / f.spp_batch;
     int64_t steps = 0;
@@ -681,7 +837,7 @@ int render_group(std::vector<Dev *> &L) {
         int s0 = b * f.spp_batch, ns = std::min(f.spp_batch, f.spp - s0);
         for (size_t i = 0; i < L.size(); ++i) {
             Dev *d = L[i];
-            CK(cudaMemsetAsync(d->b_counts.p, 0, sizeof(uint32_t) * (2 * N + 1), d->stream));
+            if (!fused) CK(cudaMemsetAsync(d->b_counts.p, 0, sizeof(uint32_t) * (2 * N + 1), d->stream));
             StepArgs a = make_args(d, fc, cur[i]);
             cudaEvent_t e0 = next_event(d), e1 = next_event(d);
             CK(cudaEventRecord(e0, d->stream));
@@ -691,7 +847,51 @@ int render_group(std::vector<Dev *> &L) {
             launches++;
             CK(cudaGetLastError());
         }
-        for (;;) {
+        while (fused) {
+            // step boundary: every rank's next-queue counts (the allgather is the barrier)
+            std::vector<uint32_t> rows;
+            RET(fused_sync(L, cur, rows));
+            unsigned ovf = 0;
+            int64_t total = 0;
+            for (int r = 0; r < N; ++r) { total += rows[3 * r] + rows[3 * r + 1]; ovf |= rows[3 * r + 2]; }
+            if (ovf & 1u) return fail(DPR_ERR_QUEUE_OVERFLOW, "ray queue capacity exceeded; lower spp_batch");
+            if (ovf & 2u) return fail(DPR_ERR_STATE, "BVH traversal stack overflow");
+            if (total == 0) break;
+            for (size_t i = 0; i < L.size(); ++i) {
+                Dev *d = L[i];
+                cur[i] ^= 1;
+                const uint32_t n_path = rows[3 * d->rank], n_occl = rows[3 * d->rank + 1];
+                CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 2, d->stream));
+                StepArgs a = make_args(d, fc, cur[i]);
+                const int grid_r = d->nsm * 8;
+                if (n_path) {
+                    cudaEvent_t e0 = next_event(d), e1 = next_event(d);
+                    CK(cudaEventRecord(e0, d->stream));
+                    launch_trace_path(a, grid_p[i], d->stream);
+                    CK(cudaEventRecord(e1, d->stream));
+                    launch_shade_path(a, grid_r, d->stream);
+                    if (i == 0) t_path.push_back({e0, e1});
+                    launches += 2;
+                    d->tpl++;
+                }
+                if (n_occl) {
+                    cudaEvent_t e0 = next_event(d), e1 = next_event(d);
+                    CK(cudaEventRecord(e0, d->stream));
+                    launch_trace_occl(a, grid_o[i], d->stream);
+                    CK(cudaEventRecord(e1, d->stream));
+                    launch_resolve_occl(a, grid_r, d->stream);
+                    if (i == 0) t_occl.push_back({e0, e1});
+                    launches += 2;
+                    d->tol++;
+                }
+                CK(cudaGetLastError());
+            }
+            // the consumed queue's tails become the append targets of the step after next
+            for (size_t i = 0; i < L.size(); ++i)
+                CK(cudaMemsetAsync(P<uint32_t>(L[i]->b_tails) + 2 * cur[i], 0, sizeof(uint32_t) * 2, L[i]->stream));
+            steps++;
+        }
+        while (!fused) {
             unsigned ovf = 0;
             RET(gather_counts(L, C, ovf));
             if (ovf & 1u) return fail(DPR_ERR_QUEUE_OVERFLOW, "ray queue capacity exceeded; lower spp_batch");
@@ -863,6 +1063,14 @@ int render_group(std::vector<Dev *> &L) {
         st.rank = d->rank;
         st.kernel_launches_local = d->build_launches + (i == 0 ? launches : 0);
         st.exchanged_bytes_local = d->frame_exch_bytes;
+        if (fused) {  // records written into peers' queues, from this rank's routing row
+            int64_t eb = 0;
+            for (int q = 0; q < N; ++q)
+                if (q != d->rank)
+                    eb += all[d->rank].S[0][q] * (int64_t)sizeof(PathRec) +
+                          (all[d->rank].S[1][q] + all[d->rank].S[2][q]) * (int64_t)sizeof(OcclRec);
+            st.exchanged_bytes_local = eb;
+        }
         st.trace_path_launches = d->tpl;
         st.trace_occl_launches = d->tol;
         st.steps = steps;
@@ -958,6 +1166,7 @@ int init_dev(Dev *d, int rank, int nranks, int cuda_device, void *stream, const 
     for (int c = 0; c < 3; ++c) { d->box[c] = INFINITY; d->box[3 + c] = -INFINITY; }
     if (const char *e = getenv("DPR_SPW")) d->spw = std::max(1, atoi(e));
     if (const char *e = getenv("DPR_BUILDER")) d->builder = strcmp(e, "ploc") == 0 ? 0 : 1;
+    if (const char *e = getenv("DPR_EXCHANGE")) d->exch = strcmp(e, "fused") == 0 ? 1 : 0;
     return DPR_OK;
 }
 
@@ -972,6 +1181,9 @@ void release_bufs(Dev *d) {
                  &d->b_path[0], &d->b_path[1], &d->b_occlq[0], &d->b_occlq[1]};
     for (Buf *b : bs) dfree(d, *b);
     for (int r = 0; r < DPR_MAX_RANKS; ++r) { dfree(d, d->b_send_path[r]); dfree(d, d->b_send_occl[r]); }
+    for (void *p : d->ipc_opened) cudaIpcCloseMemHandle(p);
+    d->ipc_opened.clear();
+    dfree(d, d->b_tails);
     if (d->h_counts) cudaFreeHost(d->h_counts);
     if (d->h_in) cudaFreeHost(d->h_in);
     d->h_counts = nullptr;
@@ -1035,6 +1247,7 @@ int dpr_create_loopback_group(int nranks, int cuda_device, void *cuda_stream, co
         int rc = init_dev(&h->d, r, nranks, cuda_device, cuda_stream, alloc);
         if (rc != DPR_OK) return rc;
         h->d.group = g;
+        if (!getenv("DPR_EXCHANGE")) h->d.exch = 1;  // loopback default: fused appends
         g->devs.push_back(&h->d);
         out[r] = h;
     }

@@ -80,7 +80,10 @@ struct QueuesDev {
     const uint32_t *in_count;   // [2]: path, occl
     PathRec *path_out[DPR_MAX_RANKS];
     OcclRec *occl_out[DPR_MAX_RANKS];
-    uint32_t *out_count;        // [2][nranks]
+    uint32_t *cnt_path[DPR_MAX_RANKS];  // append counter of each destination's path queue
+    uint32_t *cnt_occl[DPR_MAX_RANKS];  //   (send-recv mode: local counts; fused mode: the
+                                        //    destination's next-queue tail, possibly a peer's)
+    int fused;                          // 1: appends go straight into the destination's queue
     uint32_t path_cap, occl_cap;
     uint32_t *fetch;            // [2] persistent-kernel fetch heads
 };

@@ -98,9 +98,10 @@ __device__ __forceinline__ void warp_count(bool want, int key, unsigned long lon
 // control flow).  One global atomicAdd per (block, destination) instead of one per warp:
 // at N=1 every append targets the same counter, so per-warp atomics serialise in L2.
 // smem: cnt[DPR_MAX_RANKS], base[DPR_MAX_RANKS] provided by the caller.
-__device__ __forceinline__ uint32_t block_append(bool want, int dest, uint32_t *counts, uint32_t cap,
+__device__ __forceinline__ uint32_t block_append(bool want, int dest, uint32_t *const *counts, uint32_t cap,
                                                  unsigned *overflow, unsigned long long *S_row,
-                                                 int self, int nranks, uint32_t *s_cnt, uint32_t *s_base) {
+                                                 int self, int nranks, uint32_t *s_cnt, uint32_t *s_base,
+                                                 int sys_scope) {
     const int lane = threadIdx.x & 31;
     unsigned act = __ballot_sync(FULL, want);
     uint32_t off = 0;
@@ -117,7 +118,8 @@ __device__ __forceinline__ uint32_t block_append(bool want, int dest, uint32_t *
         uint32_t c = s_cnt[threadIdx.x];
         uint32_t b = 0;
         if (c) {
-            b = atomicAdd(&counts[threadIdx.x], c);
+            // fused exchange: the counter may live in a peer GPU's memory (NVLink)
+            b = sys_scope ? atomicAdd_system(counts[threadIdx.x], c) : atomicAdd(counts[threadIdx.x], c);
             if (S_row && (int)threadIdx.x != self) atomicAdd(&S_row[threadIdx.x], (unsigned long long)c);
         }
         s_base[threadIdx.x] = b;
@@ -486,8 +488,8 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
     if (owner_keep && A.events) A.events[((int64_t)s * F.max_depth) * F.P + p] = 1u;
     uint32_t gen = __popc(__ballot_sync(FULL, keep || owner_keep));
     if ((threadIdx.x & 31) == 0 && gen) atomicAdd(&A.ctr->gen[K_PATH], (unsigned long long)gen);
-    uint32_t pos = block_append(keep, self, A.Q.out_count, A.Q.path_cap, &A.ctr->overflow, nullptr, self,
-                                A.R.nranks, s_cnt, s_base);
+    uint32_t pos = block_append(keep, self, A.Q.cnt_path, A.Q.path_cap, &A.ctr->overflow, nullptr, self,
+                                A.R.nranks, s_cnt, s_base, A.Q.fused);
     if (keep && pos != 0xffffffffu) {
         PathRec *r = A.Q.path_out[self] + pos;
         r->a = make_float4(o.x, o.y, o.z, __int_as_float(0x7f800000));
@@ -617,8 +619,8 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
     const int self = A.R.self, N = A.R.nranks;
     const float INF = __int_as_float(0x7f800000);
     const uint32_t n_in = A.Q.in_count[0];
-    uint32_t *cnt_path = A.Q.out_count;
-    uint32_t *cnt_occl = A.Q.out_count + N;
+    uint32_t *const *cnt_path = A.Q.cnt_path;
+    uint32_t *const *cnt_occl = A.Q.cnt_occl;
     uint32_t visits = 0, gen_p = 0, gen_s = 0, gen_a = 0, rout_p = 0, rout_o = 0;
     const f3 L = mk(F.l[0], F.l[1], F.l[2]);
     const int K = F.ao_k;
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
         uint32_t pos = 0xffffffffu;
         if (__syncthreads_or(fwd))
             pos = block_append(fwd, next, cnt_path, A.Q.path_cap, &A.ctr->overflow, A.ctr->S[K_PATH],
-                               self, N, s_cnt, s_base);
+                               self, N, s_cnt, s_base, A.Q.fused);
         if (fwd && pos != 0xffffffffu) {
             PathRec *dst = A.Q.path_out[next] + pos;
             dst->a = r.a; dst->b = r.b; dst->c = r.c; dst->e = r.e;
@@ -729,7 +731,7 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
             if (!__syncthreads_or(app)) continue;
             if (is_path) {
                 uint32_t q = block_append(app, first, cnt_path, A.Q.path_cap, &A.ctr->overflow,
-                                          A.ctr->S[K_PATH], self, N, s_cnt, s_base);
+                                          A.ctr->S[K_PATH], self, N, s_cnt, s_base, A.Q.fused);
                 if (app && q != 0xffffffffu) {
                     PathRec *dst = A.Q.path_out[first] + q;
                     dst->a = make_float4(org.x, org.y, org.z, INF);
@@ -740,7 +742,8 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
                 }
             } else {
                 uint32_t q = block_append(app, first, cnt_occl, A.Q.occl_cap, &A.ctr->overflow,
-                                          A.ctr->S[slot == 0 ? K_SHADOW : K_AO], self, N, s_cnt, s_base);
+                                          A.ctr->S[slot == 0 ? K_SHADOW : K_AO], self, N, s_cnt, s_base,
+                                          A.Q.fused);
                 if (app && q != 0xffffffffu) {
                     OcclRec *dst = A.Q.occl_out[first] + q;
                     dst->a = make_float4(org.x, org.y, org.z, ctmax);
@@ -752,6 +755,7 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
             }
         }
     }
+    if (A.Q.fused) __threadfence_system();  // records written into peer queues are visible
     flush(&A.ctr->V[K_PATH], visits);
     flush(&A.ctr->gen[K_PATH], gen_p);
     flush(&A.ctr->gen[K_SHADOW], gen_s);
@@ -767,7 +771,7 @@ __global__ void __launch_bounds__(256) k_resolve_occl(const __grid_constant__ St
     const FrameDev &F = A.F;
     const int self = A.R.self, N = A.R.nranks;
     const uint32_t n_in = A.Q.in_count[1];
-    uint32_t *cnt_occl = A.Q.out_count + N;
+    uint32_t *const *cnt_occl = A.Q.cnt_occl;
     uint32_t v_s = 0, v_a = 0, rout = 0;
     __shared__ uint32_t s_cnt[DPR_MAX_RANKS], s_base[DPR_MAX_RANKS];
     if (threadIdx.x < DPR_MAX_RANKS) s_cnt[threadIdx.x] = 0;
@@ -795,7 +799,7 @@ __global__ void __launch_bounds__(256) k_resolve_occl(const __grid_constant__ St
         uint32_t pos = 0xffffffffu;
         if (__syncthreads_or(fwd))
             pos = block_append(fwd, next, cnt_occl, A.Q.occl_cap, &A.ctr->overflow, nullptr, self, N,
-                               s_cnt, s_base);
+                               s_cnt, s_base, A.Q.fused);
         if (fwd && pos != 0xffffffffu) {
             OcclRec *dst = A.Q.occl_out[next] + pos;
             dst->a = r.a; dst->b = r.b; dst->c = r.c;
@@ -805,6 +809,7 @@ __global__ void __launch_bounds__(256) k_resolve_occl(const __grid_constant__ St
         fb_add_seg(A.fb, p, make_float4(r.c.x, r.c.y, r.c.z, 0.0f), acc);
         if (acc && A.occl) atomicOr(A.occl + ((int64_t)s * F.max_depth + depth) * F.P + p, 1u << slot);
     }
+    if (A.Q.fused) __threadfence_system();
     flush(&A.ctr->V[K_SHADOW], v_s);
     flush(&A.ctr->V[K_AO], v_a);
     flush(&A.ctr->kc[1].rout_occl, rout);

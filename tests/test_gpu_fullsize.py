@@ -58,10 +58,13 @@ def test_config3_full_size_sampled():
     assert_pixels_close(g[0][pix], o.rgba)
 
 
-def test_nccl_collectives_single_rank(monkeypatch):
-    """DPR_FORCE_NCCL=1: frame-setup allgather, counts allgather, (empty) grouped exchange
-    and ncclReduce of framebuffer + dumps all run through NCCL with one rank."""
+@pytest.mark.parametrize("mode", ["sendrecv", "fused"])
+def test_nccl_collectives_single_rank(mode, monkeypatch):
+    """DPR_FORCE_NCCL=1: frame-setup allgather, counts allgather / fused step allgather,
+    (empty) grouped exchange, cudaIpc export of the fused queues, and ncclReduce of
+    framebuffer + dumps all run through NCCL with one rank."""
     monkeypatch.setenv("DPR_FORCE_NCCL", "1")
+    monkeypatch.setenv("DPR_EXCHANGE", mode)
     sc = di.config1()
     parts = di.union_parts(sc.parts)
     g = gpu_render(parts, 1, sc.camera, sc.frame)
