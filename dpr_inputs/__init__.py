@@ -413,6 +413,52 @@ def config5(nranks: int = 8, G_mesh: int = 950, G_vol: int = 1024, W: int = 3840
     return Scene("C5", parts, nranks, cam, fr, meta={"ntris": int(idx.shape[0]), "G_vol": G_vol})
 
 
+def box_tris(lo, hi) -> np.ndarray:
+    """12 triangles of an axis-aligned box, (12, 3, 3) float32."""
+    x0, y0, z0 = lo
+    x1, y1, z1 = hi
+    c = np.array([[x0, y0, z0], [x1, y0, z0], [x1, y1, z0], [x0, y1, z0],
+                  [x0, y0, z1], [x1, y0, z1], [x1, y1, z1], [x0, y1, z1]], np.float64)
+    f = [(0, 1, 2), (0, 2, 3), (4, 6, 5), (4, 7, 6), (0, 4, 5), (0, 5, 1),
+         (3, 2, 6), (3, 6, 7), (0, 3, 7), (0, 7, 4), (1, 5, 6), (1, 6, 2)]
+    return f32(c[np.array(f)])
+
+
+def boxes_scene(nranks: int = 4, n: int = 4, W: int = 256, H: int = 256, spp: int = 4,
+                seed: int = 3) -> Scene:
+    """PAPER Fig. composite-tests-diffuse (E5): 4^3 boxes pseudo-randomly
+    interleaved across 4 ranks, on a ground plane (rank 0), lit from the side so that boxes
+    of one rank shadow boxes and ground of another -- the global shadows a compositing device
+    cannot produce."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    owner = rng.integers(0, nranks, size=n ** 3)
+    palette = cluster_palette(nranks, seed=seed + 1)
+    tris = [[] for _ in range(nranks)]
+    k = 0
+    step = 1.6 / n
+    for ix in range(n):
+        for iy in range(n):
+            for iz in range(n):
+                lo = (-0.8 + ix * step + 0.05, -0.8 + iy * step + 0.05, -0.8 + iz * step + 0.05)
+                hi = (lo[0] + step * 0.62, lo[1] + step * 0.62, lo[2] + step * 0.62)
+                tris[owner[k]].append(box_tris(lo, hi))
+                k += 1
+    parts = []
+    for r in range(nranks):
+        if r == 0:
+            gv, gi = quad_tris([(-3, -0.85, -3), (3, -0.85, -3), (3, -0.85, 3), (-3, -0.85, 3)])
+            parts.append(Part(rank=0, kind=TRIS, albedo=(0.8, 0.8, 0.8), verts=gv, idx=gi))
+        if tris[r]:
+            t = np.concatenate(tris[r]).reshape(-1, 3)
+            parts.append(Part(rank=r, kind=TRIS, albedo=palette[r], verts=t,
+                              idx=np.arange(t.shape[0], dtype=np.int32).reshape(-1, 3)))
+    cam = camera_basis((2.6, 1.9, 3.3), (0, -0.2, 0), (0, 1, 0), 40.0, W, H)
+    fr = Frame(W=W, H=H, spp=spp, spp_batch=spp, max_depth=2, ao_k=2, ao_radius=0.5,
+               light_dir=f32(normalize((-1.0, 1.4, 0.3))), E=(1, 1, 1), A=(0.3, 0.3, 0.3),
+               B=(0.1, 0.1, 0.15), seed=7)
+    return Scene("E5", parts, nranks, cam, fr)
+
+
 def routing_hand_case(which: str) -> Scene:
     """SURVEY 8(c).4 hand cases H1-H3 (1x1 image, jitter 0.5, d = (0,0,1) exactly)."""
     cam = Camera(E=f32((0.2, 0.2, -1)), L=f32((-0.05, -0.05, 1)), U=f32((0.1, 0, 0)),

@@ -63,6 +63,8 @@ typedef enum { DPR_MEMORY_HOST = 0, DPR_MEMORY_DEVICE = 1 } dpr_memory;
 /* frame flags */
 #define DPR_FLAG_JITTER_CENTER 1u  /* camera jitter fixed at 0.5 (test mode) */
 #define DPR_FLAG_DEBUG_DUMPS 2u    /* record P13 event / occlusion dumps (parity mode) */
+#define DPR_FLAG_NO_BACKGROUND 4u  /* misses add no background (set internally for the local
+                                      renders of the compositing contrast device) */
 
 /* Device memory provider.  NULL allocator -> stream-ordered cudaMallocAsync.
  * The Python binding passes PyTorch's caching allocator (north_star: PyTorch owns device
@@ -211,6 +213,16 @@ DPR_API int dpr_render_frame(dpr_device dev);
 
 /* LOOPBACK only: one collective render over all virtual ranks of the group. */
 DPR_API int dpr_render_frame_group(dpr_device *devs, int n);
+
+/* COLLECTIVE: the contrast device of P:534-647 (S5.1 ANARI-Composite): every rank renders
+ * ONLY its local parts (local shading: no cross-rank shadows/AO/bounces) into colour +
+ * depth buffers (depth = min over samples of the primary hit distance), then deep
+ * compositing: parallel direct send of RGBA-z fragments so rank r receives all ranks'
+ * fragments of its pixel span [r*S, (r+1)*S), S = ceil(W*H/N); per pixel sort by depth (ties:
+ * lower rank) and composite front to back with "over" on premultiplied colour, background
+ * last; spans gathered to rank 0 (P:568-582 S5.1.1).  dpr_map_frame then returns this image. */
+DPR_API int dpr_render_frame_composite(dpr_device dev);
+DPR_API int dpr_render_frame_composite_group(dpr_device *devs, int n);  /* loopback */
 
 /* LOCAL: 1 if the last render completed (renders are synchronous; wait is ignored). */
 DPR_API int dpr_frame_ready(dpr_device dev, int wait);

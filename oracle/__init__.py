@@ -82,6 +82,8 @@ def lib():
         L.or_render_dp.argtypes = [_P, _P, _P, _P, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P,
                                    ctypes.c_int]
         L.or_set_brute.argtypes = [ctypes.c_int]
+        L.or_render_union_depth.restype = ctypes.c_int
+        L.or_render_union_depth.argtypes = [_P, _P, _P, _P, ctypes.c_int64, _P, _P, ctypes.c_int]
         L.or_philox.argtypes = [_P, _P, _P]
         L.or_u01.restype = ctypes.c_float
         L.or_u01.argtypes = [ctypes.c_uint32]
@@ -238,6 +240,47 @@ def render(scene: OracleScene, cam: di.Camera, fr: di.Frame, pixels=None, dp: bo
     if rc != 0:
         raise ValueError("or_render_union failed")
     return RenderResult(rgba, ev, oc, gen)
+
+
+FLAG_NO_BACKGROUND = 4
+
+
+def render_local_fragments(parts: List[di.Part], rank: int, cam: di.Camera, fr: di.Frame,
+                           nthreads: int = 0):
+    """The colour + depth buffers of one rank's LOCAL render (only its own parts, local
+    shading, no background) -- what a pass-through device hands to the compositing device
+    (S5.1.2).  rgba premultiplied by coverage (= sum/spp), depth = min primary t."""
+    local = [di.Part(**{**p.__dict__, "rank": 0}) for p in parts if p.rank == rank]
+    sc = OracleScene(local, 1)
+    f = di.Frame(**{**fr.__dict__, "flags": fr.flags | FLAG_NO_BACKGROUND})
+    n = f.W * f.H
+    pix = np.arange(n, dtype=np.int64)
+    rgba = np.zeros((n, 4), np.float64)
+    depth = np.zeros(n, np.float32)
+    c, ff = make_camera(cam), make_frame(f)
+    rc = lib().or_render_union_depth(sc.h, ctypes.byref(c), ctypes.byref(ff), pix.ctypes.data, n,
+                                     rgba.ctypes.data, depth.ctypes.data, nthreads)
+    if rc != 0:
+        raise ValueError("or_render_union_depth failed")
+    return rgba, depth
+
+
+def deep_composite(rgba: np.ndarray, depth: np.ndarray, background) -> np.ndarray:
+    """deepComp (S5.1.1): per pixel, sort the N ranks' RGBA-z fragments by depth
+    (ties: lower rank first) and composite front to back with the over operator on
+    premultiplied colour; the background fills the remaining transparency.
+    rgba: (N, P, 4) premultiplied, depth: (N, P).  Returns (P, 4)."""
+    N, P = depth.shape
+    order = np.lexsort((np.broadcast_to(np.arange(N)[:, None], (N, P)), depth), axis=0)
+    C = np.zeros((P, 3))
+    A = np.zeros(P)
+    cols = np.arange(P)
+    for k in range(N):
+        f = rgba[order[k], cols]
+        C += (1.0 - A)[:, None] * f[:, :3]
+        A += (1.0 - A) * f[:, 3]
+    C += (1.0 - A)[:, None] * np.asarray(background, np.float64)[None, :]
+    return np.concatenate([C, A[:, None]], axis=1)
 
 
 def set_brute(on: bool):

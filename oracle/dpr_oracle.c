@@ -67,7 +67,8 @@ typedef struct {
     float light_dir[3], E[3], A[3], B[3];
     float dt;
     uint64_t seed;
-    int32_t flags; /* bit0: jitter fixed at 0.5 */
+    int32_t flags; /* bit0: jitter fixed at 0.5; bit2: no background (local render of the
+                      compositing contrast device) */
 } or_frame;
 
 /* ------------------------------------------------------------------------------------ */
@@ -868,6 +869,7 @@ typedef struct {
     int dp;               /* 0: union renderer, 1: routing simulator */
     double *rgba;
     uint32_t *events, *occl;
+    float *depth;         /* optional: per listed pixel, min over samples of the primary event t */
     int64_t *S, *V, *gen, *steps; /* shared outputs, merged under lock */
     int64_t nbatches;
     int64_t next;         /* atomic work counter */
@@ -971,7 +973,7 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
     if (resolved_now) {
         /* no candidate: resolves as a miss at the pixel owner without being traced */
         if (J->events) J->events[((int64_t)s * fr->max_depth + 0) * J->npix + pi] = 1;
-        acc[0] += Bg.x; acc[1] += Bg.y; acc[2] += Bg.z;
+        if (!(fr->flags & 4)) { acc[0] += Bg.x; acc[1] += Bg.y; acc[2] += Bg.z; }
         return;
     }
     stack[sp++] = pr;
@@ -1001,10 +1003,13 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
             uint32_t code = best.id == 0xffffffffu ? 1u : ((best.id & 0x80000000u) ? best.id : 2u + best.id);
             if (J->events) J->events[((int64_t)s * fr->max_depth + ray.depth) * J->npix + pi] = code;
             if (best.id == 0xffffffffu) {
-                if (ray.depth == 0) { acc[0] += Bg.x; acc[1] += Bg.y; acc[2] += Bg.z; }
+                if (ray.depth == 0 && !(fr->flags & 4)) { acc[0] += Bg.x; acc[1] += Bg.y; acc[2] += Bg.z; }
                 continue;
             }
-            if (ray.depth == 0) acc[3] += 1.0;
+            if (ray.depth == 0) {
+                acc[3] += 1.0;
+                if (J->depth && best.t < J->depth[pi]) J->depth[pi] = best.t;
+            }
             ORay kids[40];
             int nk = 0;
             v3 hp = sample_p(ray.o, ray.d, best.t); /* P5: p.c = o.c + bestT*d.c */
@@ -1137,7 +1142,7 @@ static void *worker(void *arg)
 
 static int run(const OScene *sc, const or_camera *cam, const or_frame *fr, const int64_t *pix,
                int64_t npix, int dp, double *rgba, uint32_t *events, uint32_t *occl, int64_t *S,
-               int64_t *V, int64_t *gen, int64_t *steps, int nthreads)
+               int64_t *V, int64_t *gen, int64_t *steps, int nthreads, float *depth)
 {
     if (!sc || !cam || !fr || fr->W <= 0 || fr->H <= 0 || fr->spp <= 0 || fr->spp_batch <= 0 ||
         fr->max_depth <= 0 || fr->ao_k < 0 || fr->ao_k > 30)
@@ -1147,6 +1152,8 @@ static int run(const OScene *sc, const or_camera *cam, const or_frame *fr, const
     memset(&J, 0, sizeof(J));
     J.sc = sc; J.cam = cam; J.fr = fr; J.pix = pix; J.npix = npix; J.dp = dp;
     J.rgba = rgba; J.events = events; J.occl = occl; J.S = S; J.V = V; J.gen = gen; J.steps = steps;
+    J.depth = depth;
+    if (depth) for (int64_t i = 0; i < npix; ++i) depth[i] = INFINITY;
     J.nbatches = (fr->spp + fr->spp_batch - 1) / fr->spp_batch;
     pthread_mutex_init(&J.lock, NULL);
     if (events) memset(events, 0, (size_t)fr->spp * fr->max_depth * npix * sizeof(uint32_t));
@@ -1167,7 +1174,17 @@ OR_EXPORT int or_render_union(const OScene *sc, const or_camera *cam, const or_f
                               const int64_t *pix, int64_t npix, double *rgba, uint32_t *events,
                               uint32_t *occl, int64_t *gen, int nthreads)
 {
-    return run(sc, cam, fr, pix, npix, 0, rgba, events, occl, NULL, NULL, gen, NULL, nthreads);
+    return run(sc, cam, fr, pix, npix, 0, rgba, events, occl, NULL, NULL, gen, NULL, nthreads, NULL);
+}
+
+/* Union renderer with a per-pixel depth output (min over samples of the primary event t,
+ * +inf if none): the colour + depth buffers a pass-through device hands to the compositing
+ * device (S5.1.2). */
+OR_EXPORT int or_render_union_depth(const OScene *sc, const or_camera *cam, const or_frame *fr,
+                                    const int64_t *pix, int64_t npix, double *rgba, float *depth,
+                                    int nthreads)
+{
+    return run(sc, cam, fr, pix, npix, 0, rgba, NULL, NULL, NULL, NULL, NULL, NULL, nthreads, depth);
 }
 
 /* Routing simulator (P8/P8b).  S: 3*N*N, V: 3*N, steps: ceil(spp/spp_batch). */
@@ -1176,7 +1193,7 @@ OR_EXPORT int or_render_dp(const OScene *sc, const or_camera *cam, const or_fram
                            uint32_t *occl, int64_t *S, int64_t *V, int64_t *gen, int64_t *steps,
                            int nthreads)
 {
-    return run(sc, cam, fr, pix, npix, 1, rgba, events, occl, S, V, gen, steps, nthreads);
+    return run(sc, cam, fr, pix, npix, 1, rgba, events, occl, S, V, gen, steps, nthreads, NULL);
 }
 
 /* ------------------------------------------------------------------------------------ */

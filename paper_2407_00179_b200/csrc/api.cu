@@ -124,6 +124,11 @@ struct Dev {
     uint32_t *peer_tails[DPR_MAX_RANKS] = {};
     std::vector<void *> ipc_opened;               // peer mappings to close
     uint64_t ipc_sig = 0;                         // signature of the exported buffers
+    // compositing contrast device
+    bool want_depth = false;
+    Buf b_depth, b_frag_rgba, b_frag_z, b_comp, b_comp_out;
+    Dev *lv = nullptr;                            // local-only view of this rank's world
+    const float *frame_out = nullptr;             // what dpr_map_frame returns
     int64_t build_launches = 0, frame_launches = 0, frame_exch_bytes = 0, tpl = 0, tol = 0;
     double ms_build = 0;
     bool dumps_valid = false;
@@ -602,6 +607,10 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
         CK(cudaMemsetAsync(d->b_occl.p, 0, sizeof(uint32_t) * nd, s));
     }
     CK(cudaMemsetAsync(d->b_ctr.p, 0, sizeof(Counters), s));
+    if (d->want_depth) {
+        RET(ensure(d, d->b_depth, sizeof(uint32_t) * P_));
+        launch_depth_init(P<uint32_t>(d->b_depth), P_, s);
+    }
     return DPR_OK;
 }
 
@@ -664,6 +673,7 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.fb = P<float4>(d->b_fb);
     a.events = (f.flags & DPR_FLAG_DEBUG_DUMPS) ? P<uint32_t>(d->b_events) : nullptr;
     a.occl = (f.flags & DPR_FLAG_DEBUG_DUMPS) ? P<uint32_t>(d->b_occl) : nullptr;
+    a.depth = d->want_depth ? P<uint32_t>(d->b_depth) : nullptr;
     a.ctr = P<Counters>(d->b_ctr);
     return a;
 }
@@ -1120,6 +1130,7 @@ int render_group(std::vector<Dev *> &L) {
         d->frame_done = 1;
         d->mapped_w = d->rank == 0 ? f.W : 0;
         d->mapped_h = d->rank == 0 ? f.H : 0;
+        d->frame_out = d->rank == 0 ? P<float>(d->b_fb_out) : nullptr;
     }
     return DPR_OK;
 }
@@ -1170,7 +1181,12 @@ int init_dev(Dev *d, int rank, int nranks, int cuda_device, void *stream, const 
     return DPR_OK;
 }
 
+void release_local_view(Dev *d);
+
 void release_bufs(Dev *d) {
+    release_local_view(d);
+    Buf *cb[] = {&d->b_depth, &d->b_frag_rgba, &d->b_frag_z, &d->b_comp, &d->b_comp_out};
+    for (Buf *b : cb) dfree(d, *b);
     for (auto &p : d->parts) { dfree(d, p.verts); dfree(d, p.idx); dfree(d, p.spheres); dfree(d, p.vox); dfree(d, p.tf); dfree(d, p.mc); }
     d->parts.clear();
     Buf *bs[] = {&d->b_prims_u, &d->b_blo, &d->b_bhi, &d->b_keys[0], &d->b_keys[1], &d->b_vals[0],
@@ -1190,6 +1206,161 @@ void release_bufs(Dev *d) {
     d->h_in = nullptr;
     for (auto e : d->ev_pool) cudaEventDestroy(e);
     d->ev_pool.clear();
+}
+
+// ---------------------------------------------------------------------------------------
+// Compositing contrast device.
+// ---------------------------------------------------------------------------------------
+// A single-rank view of d's world (shares the world buffers, owns its frame buffers).
+Dev *local_view(Dev *d) {
+    if (!d->lv) {
+        Dev *v = new Dev();
+        v->rank = 0; v->nranks = 1; v->cuda_dev = d->cuda_dev; v->nsm = d->nsm; v->stream = d->stream;
+        v->alloc = d->alloc; v->has_alloc = d->has_alloc; v->exch = 0; v->spw = d->spw;
+        d->lv = v;
+    }
+    Dev *v = d->lv;
+    v->parts = d->parts;  // non-owning copies (detached before release)
+    v->world_ready = d->world_ready; v->nprims = d->nprims; memcpy(v->box, d->box, sizeof(v->box));
+    v->nonempty = d->nonempty; v->b_wnodes = d->b_wnodes; v->b_prims_w = d->b_prims_w;
+    v->local_parts = d->local_parts; v->wnodes_count = d->wnodes_count; v->bvh_levels = d->bvh_levels;
+    v->build_launches = 0;
+    v->cam = d->cam; v->cam_set = d->cam_set;
+    v->fr = d->fr; v->fr.flags |= DPR_FLAG_NO_BACKGROUND; v->fr_set = d->fr_set;
+    v->want_depth = true;
+    return v;
+}
+
+void release_bufs(Dev *d);
+
+void release_local_view(Dev *d) {
+    Dev *v = d->lv;
+    if (!v) return;
+    v->parts.clear();
+    v->b_wnodes = Buf();
+    v->b_prims_w = Buf();
+    release_bufs(v);
+    delete v;
+    d->lv = nullptr;
+}
+
+int render_composite(std::vector<Dev *> &L) {
+    Dev *d0 = L[0];
+    const int N = d0->nranks;
+    for (Dev *d : L) {
+        if (!d->world_ready) return fail(DPR_ERR_STATE, "dpr_commit_world has not been called");
+        if (!d->cam_set || !d->fr_set) return fail(DPR_ERR_STATE, "camera and frame must be set before rendering");
+        d->frame_done = 0;
+    }
+    cudaEvent_t e0, e1, e2;
+    cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
+    CK(cudaEventRecord(e0, d0->stream));
+    {   // collective consistency check (same digest on all ranks)
+        FrameCtx fc;
+        memset(&fc.R, 0, sizeof(fc.R));
+        RET(frame_setup(L, fc));
+    }
+    // 1. local renders: each rank sees only its own parts
+    int64_t rays = 0;
+    for (Dev *d : L) {
+        Dev *v = local_view(d);
+        std::vector<Dev *> one = {v};
+        RET(render_group(one));
+        rays += v->stats.rays[0] + v->stats.rays[1] + v->stats.rays[2];
+    }
+    CK(cudaEventRecord(e1, d0->stream));
+    const dpr_frame_desc &f = d0->fr;
+    const int64_t P_ = (int64_t)f.W * f.H, S = (P_ + N - 1) / N;
+    auto span_count = [&](int r) { return std::max<int64_t>(0, std::min<int64_t>(P_, (int64_t)(r + 1) * S) - (int64_t)r * S); };
+    for (Dev *d : L) {
+        RET(ensure(d, d->b_frag_rgba, sizeof(float4) * N * S));
+        RET(ensure(d, d->b_frag_z, sizeof(float) * N * S));
+        RET(ensure(d, d->b_comp, sizeof(float4) * S));
+        if (d->rank == 0) RET(ensure(d, d->b_comp_out, sizeof(float4) * P_));
+    }
+    // 2. parallel direct send: rank r receives every rank's fragments of its span
+    if (!d0->comm) {
+        for (Dev *dst : L)
+            for (Dev *src : L) {
+                int64_t c = span_count(dst->rank);
+                if (!c) continue;
+                CK(cudaMemcpyAsync(P<float4>(dst->b_frag_rgba) + (int64_t)src->rank * S,
+                                   P<float4>(src->lv->b_fb_out) + (int64_t)dst->rank * S, sizeof(float4) * c,
+                                   cudaMemcpyDeviceToDevice, dst->stream));
+                CK(cudaMemcpyAsync(P<float>(dst->b_frag_z) + (int64_t)src->rank * S,
+                                   P<float>(src->lv->b_depth) + (int64_t)dst->rank * S, sizeof(float) * c,
+                                   cudaMemcpyDeviceToDevice, dst->stream));
+            }
+    } else {
+        Dev *d = d0;
+        const int64_t mine = span_count(d->rank);
+        NK(ncclGroupStart());
+        for (int q = 0; q < N; ++q) {
+            const int64_t cq = span_count(q);
+            if (q == d->rank) continue;
+            if (cq) {
+                NK(ncclSend(P<float4>(d->lv->b_fb_out) + (int64_t)q * S, 4 * cq, ncclFloat, q, d->comm, d->stream));
+                NK(ncclSend(P<float>(d->lv->b_depth) + (int64_t)q * S, cq, ncclFloat, q, d->comm, d->stream));
+            }
+            if (mine) {
+                NK(ncclRecv(P<float4>(d->b_frag_rgba) + (int64_t)q * S, 4 * mine, ncclFloat, q, d->comm, d->stream));
+                NK(ncclRecv(P<float>(d->b_frag_z) + (int64_t)q * S, mine, ncclFloat, q, d->comm, d->stream));
+            }
+        }
+        NK(ncclGroupEnd());
+        if (mine) {
+            CK(cudaMemcpyAsync(P<float4>(d->b_frag_rgba) + (int64_t)d->rank * S, P<float4>(d->lv->b_fb_out) + (int64_t)d->rank * S,
+                               sizeof(float4) * mine, cudaMemcpyDeviceToDevice, d->stream));
+            CK(cudaMemcpyAsync(P<float>(d->b_frag_z) + (int64_t)d->rank * S, P<float>(d->lv->b_depth) + (int64_t)d->rank * S,
+                               sizeof(float) * mine, cudaMemcpyDeviceToDevice, d->stream));
+        }
+    }
+    // 3. composite each rank's span
+    for (Dev *d : L)
+        launch_composite(P<float4>(d->b_frag_rgba), P<float>(d->b_frag_z), N, S, span_count(d->rank), f.B[0],
+                         f.B[1], f.B[2], P<float4>(d->b_comp), d->stream);
+    // 4. gather the spans to rank 0
+    if (!d0->comm) {
+        for (Dev *d : L) {
+            int64_t c = span_count(d->rank);
+            if (c) CK(cudaMemcpyAsync(P<float4>(L[0]->b_comp_out) + (int64_t)d->rank * S, d->b_comp.p, sizeof(float4) * c,
+                                      cudaMemcpyDeviceToDevice, L[0]->stream));
+        }
+    } else {
+        Dev *d = d0;
+        NK(ncclGroupStart());
+        if (d->rank == 0) {
+            for (int q = 1; q < N; ++q)
+                if (span_count(q)) NK(ncclRecv(P<float4>(d->b_comp_out) + (int64_t)q * S, 4 * span_count(q), ncclFloat, q, d->comm, d->stream));
+        } else if (span_count(d->rank)) {
+            NK(ncclSend(d->b_comp.p, 4 * span_count(d->rank), ncclFloat, 0, d->comm, d->stream));
+        }
+        NK(ncclGroupEnd());
+        if (d->rank == 0 && span_count(0))
+            CK(cudaMemcpyAsync(d->b_comp_out.p, d->b_comp.p, sizeof(float4) * span_count(0), cudaMemcpyDeviceToDevice, d->stream));
+    }
+    CK(cudaEventRecord(e2, d0->stream));
+    CK(cudaStreamSynchronize(d0->stream));
+    CK(cudaGetLastError());
+    float ms_all = 0, ms_local = 0;
+    cudaEventElapsedTime(&ms_all, e0, e2);
+    cudaEventElapsedTime(&ms_local, e0, e1);
+    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
+    for (Dev *d : L) {
+        d->stats = d->lv->stats;
+        d->stats.nranks = N;
+        d->stats.rank = d->rank;
+        d->stats.ms_frame = ms_all;
+        d->stats.ms_frame_max = ms_all;
+        d->stats.ms_exchange = ms_all - ms_local;  // direct send + composite + gather
+        d->frame_done = 1;
+        d->dumps_valid = false;
+        d->mapped_w = d->rank == 0 ? f.W : 0;
+        d->mapped_h = d->rank == 0 ? f.H : 0;
+        d->frame_out = d->rank == 0 ? P<float>(d->b_comp_out) : nullptr;
+    }
+    (void)rays;
+    return DPR_OK;
 }
 
 }  // namespace
@@ -1406,6 +1577,27 @@ int dpr_render_frame_group(dpr_device *devs, int n) {
     return render_group(L);
 }
 
+int dpr_render_frame_composite(dpr_device dev) {
+    if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
+    Dev *d = &dev->d;
+    if (d->group) return fail(DPR_ERR_STATE, "loopback devices use dpr_render_frame_composite_group");
+    CK(cudaSetDevice(d->cuda_dev));
+    std::vector<Dev *> L = {d};
+    return render_composite(L);
+}
+
+int dpr_render_frame_composite_group(dpr_device *devs, int n) {
+    if (!devs || n < 1) return fail(DPR_ERR_INVALID_ARG, "bad group");
+    std::vector<Dev *> L;
+    for (int i = 0; i < n; ++i) {
+        if (!devs[i] || !devs[i]->d.group || devs[i]->d.rank != i || devs[i]->d.nranks != n)
+            return fail(DPR_ERR_INVALID_ARG, "devices must be a full loopback group in rank order");
+        L.push_back(&devs[i]->d);
+    }
+    CK(cudaSetDevice(L[0]->cuda_dev));
+    return render_composite(L);
+}
+
 int dpr_frame_ready(dpr_device dev, int wait) {
     (void)wait;
     if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
@@ -1420,7 +1612,7 @@ int dpr_map_frame(dpr_device dev, const float **rgba, int *w, int *h, int *undef
         *rgba = nullptr; *w = 0; *h = 0; *undefined = 1;
         return DPR_OK;
     }
-    *rgba = P<float>(d->b_fb_out);
+    *rgba = d->frame_out;
     *w = d->mapped_w;
     *h = d->mapped_h;
     *undefined = 0;

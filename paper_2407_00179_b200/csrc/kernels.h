@@ -97,6 +97,7 @@ struct StepArgs {
     float4 *fb;
     uint32_t *events;  // debug dumps or nullptr
     uint32_t *occl;
+    uint32_t *depth;   // per-pixel min primary hit t (float bits; +inf init) or nullptr
     Counters *ctr;
 };
 
@@ -116,5 +117,8 @@ constexpr int TRACE_MINB = DPR_TRACE_MINB;  // 8 x 128 threads per SM -> <= 64 r
 void launch_fb_accumulate(float4 *dst, const float4 *src, int64_t n, cudaStream_t s);
 void launch_u32_accumulate(uint32_t *dst, const uint32_t *src, int64_t n, cudaStream_t s);
 void launch_fb_normalize(float4 *out, const float4 *in, int64_t n, float spp, cudaStream_t s);
+void launch_depth_init(uint32_t *depth, int64_t n, cudaStream_t s);
+void launch_composite(const float4 *frag_rgba, const float *frag_z, int nranks, int64_t span, int64_t count,
+                      float br, float bg, float bb, float4 *out, cudaStream_t s);
 
 }  // namespace dpr

@@ -484,7 +484,8 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
         int owner = (int)(((int64_t)p * A.R.nranks) / F.P);
         owner_keep = owner == self;
     }
-    fb_add_seg(A.fb, p, make_float4(F.B[0], F.B[1], F.B[2], 0.0f), owner_keep);
+    fb_add_seg(A.fb, p, make_float4(F.B[0], F.B[1], F.B[2], 0.0f),
+               owner_keep && !(F.flags & DPR_FLAG_NO_BACKGROUND));
     if (owner_keep && A.events) A.events[((int64_t)s * F.max_depth) * F.P + p] = 1u;
     uint32_t gen = __popc(__ballot_sync(FULL, keep || owner_keep));
     if ((threadIdx.x & 31) == 0 && gen) atomicAdd(&A.ctr->gen[K_PATH], (unsigned long long)gen);
@@ -663,8 +664,14 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
             uint32_t code = bid == NO_HIT ? 1u : (vol ? bid : 2u + bid);
             A.events[((int64_t)s * F.max_depth + depth) * F.P + p] = code;
         }
-        if (res && depth == 0)
-            fb_add(A.fb + p, evt ? make_float4(0.0f, 0.0f, 0.0f, 1.0f) : make_float4(F.B[0], F.B[1], F.B[2], 0.0f));
+        if (res && depth == 0) {
+            if (evt) {
+                fb_add(A.fb + p, make_float4(0.0f, 0.0f, 0.0f, 1.0f));
+                if (A.depth) atomicMin(A.depth + p, __float_as_uint(bt));  // t > 0: bits order like floats
+            } else if (!(F.flags & DPR_FLAG_NO_BACKGROUND)) {
+                fb_add(A.fb + p, make_float4(F.B[0], F.B[1], F.B[2], 0.0f));
+            }
+        }
         if (!__syncthreads_or(evt)) continue;
         f3 hp = mk(o.x + bt * d.x, o.y + bt * d.y, o.z + bt * d.z);  // P5
         f3 org = hp, br = mk(0, 0, 0);
@@ -835,7 +842,47 @@ __global__ void k_fb_normalize(float4 *out, const float4 *__restrict__ in, int64
     out[i] = make_float4(a.x / spp, a.y / spp, a.z / spp, a.w / spp);
 }
 
+// ---------------------------------------------------------------------------------------
+// Compositing contrast device: per owned pixel, sort the N ranks' RGBA-z
+// fragments by depth (ties: lower rank) and composite front to back, background last.
+// ---------------------------------------------------------------------------------------
+__global__ void k_depth_init(uint32_t *depth, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) depth[i] = 0x7f800000u;  // +inf
+}
+
+__global__ void k_composite(const float4 *__restrict__ frag_rgba, const float *__restrict__ frag_z, int nranks,
+                            int64_t span, int64_t count, float br, float bg, float bb, float4 *out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    int ord[DPR_MAX_RANKS];
+    float z[DPR_MAX_RANKS];
+    for (int q = 0; q < nranks; ++q) {
+        z[q] = frag_z[(int64_t)q * span + i];
+        int k = q;  // insertion sort by (z, rank); ranks arrive in ascending order
+        while (k > 0 && z[ord[k - 1]] > z[q]) { ord[k] = ord[k - 1]; --k; }
+        ord[k] = q;
+    }
+    float cr = 0.0f, cg = 0.0f, cb = 0.0f, a = 0.0f;
+    for (int k = 0; k < nranks; ++k) {
+        float4 f = frag_rgba[(int64_t)ord[k] * span + i];
+        float t = 1.0f - a;
+        cr += t * f.x; cg += t * f.y; cb += t * f.z;
+        a += t * f.w;
+    }
+    float t = 1.0f - a;
+    out[i] = make_float4(cr + t * br, cg + t * bg, cb + t * bb, a);
+}
+
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void launch_depth_init(uint32_t *depth, int64_t n, cudaStream_t s) {
+    if (n > 0) k_depth_init<<<nblk(n, 256), 256, 0, s>>>(depth, n);
+}
+void launch_composite(const float4 *frag_rgba, const float *frag_z, int nranks, int64_t span, int64_t count,
+                      float br, float bg, float bb, float4 *out, cudaStream_t s) {
+    if (count > 0) k_composite<<<nblk(count, 256), 256, 0, s>>>(frag_rgba, frag_z, nranks, span, count, br, bg, bb, out);
+}
 
 void launch_gen_primary(const StepArgs &a, int s0, int nsamp, int spw_max, cudaStream_t s) {
     int spw = 1;  // largest power of two <= spw_max dividing nsamp

@@ -314,3 +314,31 @@ def test_mixed_surface_volume_tie_rules():
     _assert_same_image(r, u)
     ev = r.events[:, 0]
     assert ((ev & 0x80000000) != 0).any() and ((ev >= 2) & (ev < 0x80000000)).any()
+
+
+def test_deep_composite_over_operator():
+    """deepComp's over operator (SPEC S:452 worked example): a half-transparent
+    red fragment in front of an opaque blue one -> (0.5, 0, 0.5, 1); depth order, not rank
+    order, decides; the background fills what is left."""
+    red = [0.5, 0.0, 0.0, 0.5]   # premultiplied, alpha 0.5
+    blue = [0.0, 0.0, 1.0, 1.0]
+    rgba = np.array([[blue], [red]], np.float64)          # rank 0 blue, rank 1 red
+    depth = np.array([[2.0], [1.0]], np.float32)          # red is in front
+    out = orc.deep_composite(rgba, depth, (0.1, 0.2, 0.3))
+    assert np.allclose(out[0], [0.5, 0.0, 0.5, 1.0])
+    out = orc.deep_composite(rgba[:1] * 0, np.array([[np.inf]], np.float32), (0.1, 0.2, 0.3))
+    assert np.allclose(out[0], [0.1, 0.2, 0.3, 0.0])
+    # equal depth: lower rank first
+    two = np.array([[[0.2, 0, 0, 0.5]], [[0, 0.2, 0, 0.5]]])
+    out = orc.deep_composite(two, np.array([[1.0], [1.0]], np.float32), (0, 0, 0))
+    assert np.allclose(out[0], [0.2, 0.1, 0, 0.75])
+
+
+def test_local_fragments_union_invariance():
+    """One rank holding the whole boxes scene: local fragments composited == the plain
+    render (compositing is the identity for N=1)."""
+    sc = di.boxes_scene(nranks=1, W=24, H=24, spp=2)
+    rgba, depth = orc.render_local_fragments(sc.parts, 0, sc.camera, sc.frame)
+    comp = orc.deep_composite(rgba[None], depth[None], sc.frame.B)
+    u = orc.render(orc.OracleScene(sc.parts, 1), sc.camera, sc.frame)
+    assert np.allclose(comp, u.rgba, atol=1e-9)
