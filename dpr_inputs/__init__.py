@@ -226,11 +226,31 @@ def bisect_partition(points: np.ndarray, nparts: int) -> np.ndarray:
     return out
 
 
-def split_mesh(verts: np.ndarray, idx: np.ndarray, nranks: int, albedo) -> List[Part]:
-    """Spatial partition of a triangle mesh by centroid bisection."""
+PARTITIONS = ("spatial", "roundrobin", "binpack")
+
+
+def partition_groups(cen: np.ndarray, nranks: int, strategy: str = "spatial") -> np.ndarray:
+    """Prim -> rank assignment (S2.2: "distribute the scene data in a very simple
+    way -- e.g., round-robin, bin-packing until all GPU memory is used").
+      spatial    recursive median bisection of centroids (compact rank boxes)
+      roundrobin prim i -> rank i mod N (in the mesh's own order)
+      binpack    contiguous runs of the input order, equal sizes (fill a rank, then the next)"""
+    n = cen.shape[0]
+    if strategy == "spatial":
+        return bisect_partition(cen, nranks)
+    if strategy == "roundrobin":
+        return (np.arange(n) % nranks).astype(np.int32)
+    if strategy == "binpack":
+        return (np.arange(n) * nranks // max(n, 1)).astype(np.int32)
+    raise ValueError(strategy)
+
+
+def split_mesh(verts: np.ndarray, idx: np.ndarray, nranks: int, albedo,
+               strategy: str = "spatial") -> List[Part]:
+    """Partition of a triangle mesh over ranks (spatial bisection)."""
     tri = verts[idx]                      # (m,3,3)
     cen = tri.astype(np.float64).mean(axis=1)
-    grp = bisect_partition(cen, nranks)
+    grp = partition_groups(cen, nranks, strategy)
     parts = []
     for r in range(nranks):
         sel = np.nonzero(grp == r)[0]
@@ -322,11 +342,11 @@ C2_G = 301
 
 
 def config2(nranks: int = 1, G: int = C2_G, W: int = 1024, H: int = 1024, spp: int = 16,
-            spp_batch: int = 16) -> Scene:
+            spp_batch: int = 16, partition: str = "spatial") -> Scene:
     """configs[1]: synthetic ~10M-triangle gyroid spatially partitioned over N ranks,
     1024x1024, 16 spp, shadows + AO (K=4, aoRadius 0.25, depth 1)."""
     verts, idx = gyroid_mesh(G)
-    parts = split_mesh(verts, idx, nranks, (0.75, 0.75, 0.75))
+    parts = split_mesh(verts, idx, nranks, (0.75, 0.75, 0.75), partition)
     cam = camera_basis((2.2, 1.6, 2.8), (0, 0, 0), (0, 1, 0), 45.0, W, H)
     fr = Frame(W=W, H=H, spp=spp, spp_batch=spp_batch, max_depth=1, ao_k=4, ao_radius=0.25,
                light_dir=f32(normalize((1, 1.5, 0.5))), E=(1, 1, 1), A=(0.4, 0.4, 0.4),

@@ -193,3 +193,12 @@ def test_exchange_modes(mode, case, monkeypatch):
     st = g[3]
     rec = sum(int(st["S"][0, 0, q]) * 64 + int(st["S"][1:, 0, q].sum()) * 48 for q in range(1, n))
     assert st["exchanged_bytes_local"] == rec
+
+
+@pytest.mark.parametrize("strategy", ["roundrobin", "binpack"])
+def test_partition_strategies(strategy):
+    """NEXT f2: the paper's simple distributions render bit-identically."""
+    sc = di.config2(nranks=4, G=41, W=64, H=48, spp=2, spp_batch=2, partition=strategy)
+    g = gpu_render(sc.parts, 4, sc.camera, sc.frame)
+    o = oracle_render(sc.parts, 4, sc.camera, sc.frame)
+    assert_parity(g, o)
