@@ -94,7 +94,7 @@ struct Dev {
     float box[6];
     bool nonempty = false;
     Buf b_prims_u, b_blo, b_bhi, b_keys[2], b_vals[2], b_tile, b_left, b_right, b_parent, b_rlo,
-        b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_nodes, b_bounds, b_hist, b_wnodes,
+        b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_bounds, b_hist, b_wnodes,
         b_prims_w, b_items[2], b_wcnt, b_wperm, b_witems[2], b_size;
     int builder = 1;  // 0 PLOC, 1 Karras LBVH (default; env DPR_BUILDER=ploc|lbvh; sweep r01)
     int build_iters = 0;
@@ -129,7 +129,7 @@ struct Dev {
     Buf b_depth, b_frag_rgba, b_frag_z, b_comp, b_comp_out;
     Dev *lv = nullptr;                            // local-only view of this rank's world
     const float *frame_out = nullptr;             // what dpr_map_frame returns
-    int64_t build_launches = 0, frame_launches = 0, frame_exch_bytes = 0, tpl = 0, tol = 0;
+    int64_t build_launches = 0, frame_exch_bytes = 0, tpl = 0, tol = 0;
     double ms_build = 0;
     bool dumps_valid = false;
     dpr_stats stats{};
@@ -626,7 +626,6 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     }
     a.R = fc.R;
     a.R.self = d->rank;
-    a.W.nodes = P<BVHNode>(d->b_nodes);
     a.W.wnodes = P<WNode>(d->b_wnodes);
     a.W.prmt_hi = 0x4b00u;
     a.W.prims = P<float4>(d->b_prims_w);
@@ -822,7 +821,7 @@ int render_group(std::vector<Dev *> &L) {
         d->dumps_valid = false;
     }
     const dpr_frame_desc &f = d0->fr;
-    for (Dev *d : L) { d->frame_launches = 0; d->frame_exch_bytes = 0; d->tpl = 0; d->tol = 0; }
+    for (Dev *d : L) { d->frame_exch_bytes = 0; d->tpl = 0; d->tol = 0; }
     cudaEvent_t ev_f0 = next_event(d0), ev_f1;
     CK(cudaEventRecord(ev_f0, d0->stream));
     FrameCtx fc;
@@ -1191,7 +1190,7 @@ void release_bufs(Dev *d) {
     d->parts.clear();
     Buf *bs[] = {&d->b_prims_u, &d->b_blo, &d->b_bhi, &d->b_keys[0], &d->b_keys[1], &d->b_vals[0],
                  &d->b_vals[1], &d->b_tile, &d->b_left, &d->b_right, &d->b_parent, &d->b_rlo, &d->b_rhi,
-                 &d->b_nlo, &d->b_nhi, &d->b_arrive, &d->b_prims, &d->b_slo, &d->b_shi, &d->b_nodes,
+                 &d->b_nlo, &d->b_nhi, &d->b_arrive, &d->b_prims, &d->b_slo, &d->b_shi,
                  &d->b_bounds, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_witems[0], &d->b_witems[1], &d->b_size, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
                  &d->b_counts, &d->b_in_count, &d->b_fetch, &d->b_part_lo, &d->b_part_alb, &d->b_scratch,
                  &d->b_path[0], &d->b_path[1], &d->b_occlq[0], &d->b_occlq[1]};

@@ -237,21 +237,13 @@ __device__ __forceinline__ f3 iso_dir(uint64_t seed, uint32_t p, uint32_t s, uin
 // ---------------------------------------------------------------------------------------
 // Device world of one rank.
 // ---------------------------------------------------------------------------------------
-// BVH node (Aila-Laine 2009 layout, 64 B): both children's boxes in one node so one node
-// fetch (4 x 16 B, one 64 B segment) tests two boxes.
-//   n0 = (c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y)   n1 = (c1.lo.x, c1.hi.x, c1.lo.y, c1.hi.y)
-//   n2 = (c0.lo.z, c0.hi.z, c1.lo.z, c1.hi.z)   n3 = (ref0, ref1, count0, count1)
-// ref >= 0: internal node index; ref < 0: leaf_ref(start, count) = ~(start<<3 | count-1),
-// count in [1, 8] (start < 2^28 - 1; REF_DONE = INT_MIN is the "stack empty" sentinel).
-struct BVHNode { float4 n0, n1, n2; int4 n3; };
+// Leaf size bound of the wide-BVH collapse (binary subtrees with <= LEAF_MAX prims become
+// leaf children).
 #ifndef DPR_LEAF_MAX
 #define DPR_LEAF_MAX 3
 #endif
 constexpr int LEAF_MAX = DPR_LEAF_MAX;  // <= 4 (2-bit count in the wide-node meta)
-constexpr int REF_DONE = (int)0x80000000;
-__host__ __device__ __forceinline__ int leaf_ref(int start, int cnt) { return ~((start << 3) | (cnt - 1)); }
-__host__ __device__ __forceinline__ int leaf_start(int ref) { return (~ref) >> 3; }
-__host__ __device__ __forceinline__ int leaf_count(int ref) { return ((~ref) & 7) + 1; }
+
 
 // Prim record in BVH leaf order, 48 B (3 x float4):
 //   tri:    (v0.xyz, id) (e1.xyz, 0) (e2.xyz, 0)     id = local index
@@ -288,7 +280,6 @@ struct WorldDev {
     uint32_t prmt_hi;  // 0x4b00 (2^23 float pattern for byte decode), passed at run time so that
                        // ptxas keeps the PRMT selector as the immediate operand
     const WNode *wnodes;
-    const BVHNode *nodes;
     const float4 *prims;
     int64_t nprims;
     uint32_t id_base;       // global id of local prim 0 (P12)

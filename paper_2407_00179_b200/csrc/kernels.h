@@ -26,9 +26,6 @@ void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *
 void launch_refit(int64_t n, const int *left, const int *right, const int *parent,
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
                   cudaStream_t s);
-void launch_emit(int64_t n, int leaf_max, const int *left, const int *right, const int *rlo,
-                 const int *rhi, const float4 *slo, const float4 *shi, const float4 *nlo,
-                 const float4 *nhi, BVHNode *out, cudaStream_t s);
 void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
                          const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,
                          cudaStream_t s);

@@ -11,8 +11,8 @@
 //      warp match + shared-memory digit prefix; passes whose digit is constant are skipped
 //   5. k_karras: internal nodes, duplicate keys broken by index
 //   6. k_refit: bottom-up boxes with arrival counters
-//   7. k_emit: 64-byte two-child nodes (Aila-Laine layout), small subtrees collapsed into
-//      leaves, child boxes padded outward (conservative traversal)
+//   7. k_collapse: compressed 8-wide nodes (WNode) by greedy opening of the largest child,
+//      child boxes padded outward then quantised outward (conservative traversal)
 //   8. k_macrocells: per 16^3 macrocell "alpha may be > 0" flags for exact empty-space
 //      skipping in bricks
 #include <algorithm>
@@ -341,48 +341,6 @@ __global__ void k_refit(int64_t n, const int *__restrict__ left, const int *__re
 __device__ __forceinline__ float pad_lo(float x) { return x - (fabsf(x) + 4.0f) * 0x1p-18f; }
 __device__ __forceinline__ float pad_hi(float x) { return x + (fabsf(x) + 4.0f) * 0x1p-18f; }
 
-__global__ void k_emit(int64_t n, int leaf_max, const int *__restrict__ left,
-                       const int *__restrict__ right, const int *__restrict__ rlo,
-                       const int *__restrict__ rhi, const float4 *__restrict__ slo,
-                       const float4 *__restrict__ shi, const float4 *__restrict__ nlo,
-                       const float4 *__restrict__ nhi, BVHNode *out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n - 1) return;
-    int c[2] = {left[i], right[i]};
-    float4 lo[2], hi[2];
-    int ref[2], cnt[2];
-    for (int k = 0; k < 2; ++k) {
-        if (c[k] >= n - 1) {
-            int64_t j = c[k] - (n - 1);
-            lo[k] = slo[j]; hi[k] = shi[j];
-            ref[k] = leaf_ref((int)j, 1); cnt[k] = 1;
-        } else {
-            lo[k] = nlo[c[k]]; hi[k] = nhi[c[k]];
-            int size = rhi[c[k]] - rlo[c[k]] + 1;
-            if (size <= leaf_max) { ref[k] = leaf_ref(rlo[c[k]], size); cnt[k] = size; }
-            else { ref[k] = c[k]; cnt[k] = 0; }
-        }
-    }
-    BVHNode nd;
-    nd.n0 = make_float4(pad_lo(lo[0].x), pad_hi(hi[0].x), pad_lo(lo[0].y), pad_hi(hi[0].y));
-    nd.n1 = make_float4(pad_lo(lo[1].x), pad_hi(hi[1].x), pad_lo(lo[1].y), pad_hi(hi[1].y));
-    nd.n2 = make_float4(pad_lo(lo[0].z), pad_hi(hi[0].z), pad_lo(lo[1].z), pad_hi(hi[1].z));
-    nd.n3 = make_int4(ref[0], ref[1], cnt[0], cnt[1]);
-    out[i] = nd;
-}
-
-// n == 1: a root whose two children are the same one-prim leaf (a duplicate test of the
-// same prim cannot change the (t, id) result).
-__global__ void k_emit_single(const float4 *slo, const float4 *shi, BVHNode *out) {
-    float4 lo = slo[0], hi = shi[0];
-    BVHNode nd;
-    nd.n0 = make_float4(pad_lo(lo.x), pad_hi(hi.x), pad_lo(lo.y), pad_hi(hi.y));
-    nd.n1 = nd.n0;
-    nd.n2 = make_float4(pad_lo(lo.z), pad_hi(hi.z), pad_lo(lo.z), pad_hi(hi.z));
-    nd.n3 = make_int4(leaf_ref(0, 1), leaf_ref(0, 1), 1, 1);
-    out[0] = nd;
-}
-
 __global__ void k_gather_prims(const float4 *__restrict__ in, const uint32_t *__restrict__ perm,
                                int64_t n, float4 *out, const float4 *__restrict__ blo,
                                const float4 *__restrict__ bhi, float4 *slo, float4 *shi) {
@@ -687,12 +645,6 @@ void launch_refit(int64_t n, const int *left, const int *right, const int *paren
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
                   cudaStream_t s) {
     if (n > 1) k_refit<<<nblk(n, 256), 256, 0, s>>>(n, left, right, parent, slo, shi, nlo, nhi, arrive);
-}
-void launch_emit(int64_t n, int leaf_max, const int *left, const int *right, const int *rlo,
-                 const int *rhi, const float4 *slo, const float4 *shi, const float4 *nlo,
-                 const float4 *nhi, BVHNode *out, cudaStream_t s) {
-    if (n > 1) k_emit<<<nblk(n - 1, 256), 256, 0, s>>>(n, leaf_max, left, right, rlo, rhi, slo, shi, nlo, nhi, out);
-    else if (n == 1) k_emit_single<<<1, 1, 0, s>>>(slo, shi, out);
 }
 void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
                          const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,

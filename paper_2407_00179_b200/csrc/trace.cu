@@ -22,7 +22,6 @@
 namespace dpr {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int STACK_SIZE = 96;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
@@ -57,32 +56,6 @@ __device__ __forceinline__ void fb_add_seg(float4 *fb, uint32_t p, float4 v, boo
     }
     const bool last = lane == 31 || ((heads >> (lane + 1)) & 1u);
     if (active && last) fb_add(fb + p, v);
-}
-
-// Warp-aggregated queue append; all 32 lanes must call.  Returns the slot or ~0u.
-// S_row (may be null) receives the per-destination forward counts (dest != self).
-__device__ __forceinline__ uint32_t warp_append(bool want, int dest, uint32_t *counts, uint32_t cap,
-                                                unsigned *overflow, unsigned long long *S_row,
-                                                int self) {
-    unsigned act = __ballot_sync(FULL, want);
-    uint32_t pos = 0xffffffffu;
-    if (want) {
-        unsigned peers = __match_any_sync(act, dest);
-        int leader = __ffs(peers) - 1;
-        int lane = threadIdx.x & 31;
-        uint32_t base = 0;
-        if (lane == leader) {
-            base = atomicAdd(&counts[dest], (uint32_t)__popc(peers));
-            if (S_row && dest != self) atomicAdd(&S_row[dest], (unsigned long long)__popc(peers));
-        }
-        base = __shfl_sync(peers, base, leader);
-        pos = base + __popc(peers & lanemask_lt());
-        if (pos >= cap) {
-            atomicOr(overflow, 1u);
-            pos = 0xffffffffu;
-        }
-    }
-    return pos;
 }
 
 // Warp-aggregated counter add keyed by an int (all lanes call).
@@ -210,10 +183,6 @@ __device__ __forceinline__ bool trav_done(const TravState &S) {
     return (S.ng.y & 0xffu) == 0 && S.sp == 0 && pending_prims(S) == 0;
 }
 
-__device__ __forceinline__ float qbyte(uint32_t w, int b) {
-    // exact int->float of byte b of w: 0x4b0000xx = 2^23 + xx
-    return __uint_as_float(__byte_perm(w, 0x4b00u, (uint32_t)b | 0x5440u)) - 8388608.0f;
-}
 
 // One outer iteration, called by ALL 32 lanes (idle lanes have an empty state).  Phase 1
 // visits nodes until every lane holds a prim group or has nothing left; phase 2 tests the
