@@ -211,8 +211,18 @@ def run_gpu(args):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2407_00179_b200 import dpr
-    scene = make_scene(args.config, world)
-    my_parts = [p for p in scene.parts if p.rank == rank]
+    scene = make_scene(args.config, 1 if args.mode == "replicated" else world)
+    my_parts = [p for p in scene.parts if p.rank == rank or args.mode == "replicated"]
+    if args.mode == "replicated":
+        my_parts = [di.Part(**{**p.__dict__, "rank": rank}) for p in my_parts]
+
+    def render():
+        if args.mode == "replicated":
+            dev.render_frame_replicated()
+        elif args.mode == "composite":
+            dev.render_frame_composite()
+        else:
+            dev.render_frame()
     if world > 1:
         dev = dpr.Device.create_distributed(local)
     else:
@@ -239,7 +249,7 @@ def run_gpu(args):
     # ---- device-resident step: LBVH rebuild + collective render -----------------------
     for _ in range(args.warmup):
         dev.commit_world()
-        dev.render_frame()
+        render()
     barrier()
     acc = {"rays": 0, "launches": 0, "ms_path": 0.0, "n_path": 0, "ms_occl": 0.0, "n_occl": 0,
            "b_path": 0, "b_occl": 0, "ms_frame": [], "ms_build": [], "steps": 0, "exch": 0,
@@ -251,7 +261,7 @@ def run_gpu(args):
         e0.record(stream)
         for _ in range(args.steps):
             dev.commit_world()
-            dev.render_frame()
+            render()
             st = dev.get_stats()
             acc["rays"] += int(st["rays"].sum())
             acc["launches"] += st["kernel_launches_local"]
@@ -313,7 +323,7 @@ def run_gpu(args):
         for q in pinned:
             dev.commit_part(q)
         dev.commit_world()
-        dev.render_frame()
+        render()
         img = dev.map_frame()
         if img is not None:
             fb_host.copy_(img, non_blocking=True)
@@ -345,7 +355,8 @@ def run_gpu(args):
                        "spp": scene.frame.spp, "spp_batch": scene.frame.spp_batch,
                        "triangles": scene.meta.get("ntris", sum(p.nprims() for p in scene.parts)), "parallelism": f"dp{world} (world partitioned, ray forwarding)",
                        "l2": "inputs larger than L2 (BVH+prims ~1.1 GB, ray queues ~5 GB per step)",
-                       "step": "dpr_commit_world (LBVH rebuild) + dpr_render_frame"},
+                       "step": "dpr_commit_world (LBVH rebuild) + dpr_render_frame",
+                       "mode": args.mode},
             "ms_per_frame": float(np.median(acc["ms_frame"])),
             "ms_build": float(np.median(acc["ms_build"])),
             "rays_per_frame": rays_per_frame,
@@ -378,6 +389,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dpr", choices=["dpr", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--mode", default="dp", choices=["dp", "replicated", "composite"],
+                    help="dp = ray forwarding over a partitioned world (the method, default); "
+                         "replicated = whole world on every rank, pixels split (Barney mode, "
+                         "P:663-668); composite = local renders + deep compositing (P:534-647)")
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"],
                     help="workload (default c2 = BASELINE configs[1], the metric's workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

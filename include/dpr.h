@@ -224,6 +224,13 @@ DPR_API int dpr_render_frame_group(dpr_device *devs, int n);
 DPR_API int dpr_render_frame_composite(dpr_device dev);
 DPR_API int dpr_render_frame_composite_group(dpr_device *devs, int n);  /* loopback */
 
+/* COLLECTIVE: Barney's data-REPLICATED mode: every rank has committed
+ * the WHOLE world; pixel p is rendered only by rank (p*N)/(W*H) against its local copy (no
+ * forwarding), and the disjoint framebuffers (and P13 dumps) are summed to rank 0.  The image
+ * equals the data-parallel render of the same world. */
+DPR_API int dpr_render_frame_replicated(dpr_device dev);
+DPR_API int dpr_render_frame_replicated_group(dpr_device *devs, int n);  /* loopback */
+
 /* LOCAL: 1 if the last render completed (renders are synchronous; wait is ignored). */
 DPR_API int dpr_frame_ready(dpr_device dev, int wait);
 

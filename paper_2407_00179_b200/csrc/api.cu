@@ -129,6 +129,8 @@ struct Dev {
     Buf b_depth, b_frag_rgba, b_frag_z, b_comp, b_comp_out;
     Dev *lv = nullptr;                            // local-only view of this rank's world
     const float *frame_out = nullptr;             // what dpr_map_frame returns
+    bool replicated_frame = false;                // last frame: dumps live in the local view
+    int pix_rank = 0, pix_nranks = 1;             // replicated mode pixel split (local view)
     int64_t build_launches = 0, frame_exch_bytes = 0, tpl = 0, tol = 0;
     double ms_build = 0;
     bool dumps_valid = false;
@@ -620,6 +622,7 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     const dpr_frame_desc &f = d->fr;
     a.F.W = f.W; a.F.H = f.H; a.F.P = f.W * f.H; a.F.spp = f.spp; a.F.max_depth = f.max_depth;
     a.F.ao_k = f.ao_k; a.F.ao_radius = f.ao_radius; a.F.dt = f.dt; a.F.seed = f.seed; a.F.flags = f.flags;
+    a.F.pix_rank = d->pix_rank; a.F.pix_nranks = d->pix_nranks;
     for (int c = 0; c < 3; ++c) {
         a.F.l[c] = f.light_dir[c]; a.F.E[c] = f.E[c]; a.F.A[c] = f.A[c]; a.F.B[c] = f.B[c];
         a.F.cE[c] = d->cam.E[c]; a.F.cL[c] = d->cam.L[c]; a.F.cU[c] = d->cam.U[c]; a.F.cV[c] = d->cam.V[c];
@@ -1130,6 +1133,7 @@ int render_group(std::vector<Dev *> &L) {
         d->mapped_w = d->rank == 0 ? f.W : 0;
         d->mapped_h = d->rank == 0 ? f.H : 0;
         d->frame_out = d->rank == 0 ? P<float>(d->b_fb_out) : nullptr;
+        d->replicated_frame = false;
     }
     return DPR_OK;
 }
@@ -1211,7 +1215,7 @@ void release_bufs(Dev *d) {
 // Compositing contrast device.
 // ---------------------------------------------------------------------------------------
 // A single-rank view of d's world (shares the world buffers, owns its frame buffers).
-Dev *local_view(Dev *d) {
+Dev *local_view(Dev *d, bool replicated = false) {
     if (!d->lv) {
         Dev *v = new Dev();
         v->rank = 0; v->nranks = 1; v->cuda_dev = d->cuda_dev; v->nsm = d->nsm; v->stream = d->stream;
@@ -1225,9 +1229,99 @@ Dev *local_view(Dev *d) {
     v->local_parts = d->local_parts; v->wnodes_count = d->wnodes_count; v->bvh_levels = d->bvh_levels;
     v->build_launches = 0;
     v->cam = d->cam; v->cam_set = d->cam_set;
-    v->fr = d->fr; v->fr.flags |= DPR_FLAG_NO_BACKGROUND; v->fr_set = d->fr_set;
-    v->want_depth = true;
+    v->fr = d->fr; v->fr_set = d->fr_set;
+    if (replicated) {
+        v->want_depth = false;
+        v->pix_rank = d->rank;
+        v->pix_nranks = d->nranks;
+    } else {
+        v->fr.flags |= DPR_FLAG_NO_BACKGROUND;
+        v->want_depth = true;
+        v->pix_rank = 0;
+        v->pix_nranks = 1;
+    }
     return v;
+}
+
+// Data-replicated mode: local renders of disjoint pixel sets, summed to rank 0.
+int render_replicated(std::vector<Dev *> &L) {
+    Dev *d0 = L[0];
+    const int N = d0->nranks;
+    for (Dev *d : L) {
+        if (!d->world_ready) return fail(DPR_ERR_STATE, "dpr_commit_world has not been called");
+        if (!d->cam_set || !d->fr_set) return fail(DPR_ERR_STATE, "camera and frame must be set before rendering");
+        d->frame_done = 0;
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    CK(cudaEventRecord(e0, d0->stream));
+    {
+        FrameCtx fc;
+        memset(&fc.R, 0, sizeof(fc.R));
+        RET(frame_setup(L, fc));  // collective digest check
+    }
+    for (Dev *d : L) {
+        Dev *v = local_view(d, true);
+        std::vector<Dev *> one = {v};
+        RET(render_group(one));
+    }
+    const dpr_frame_desc &f = d0->fr;
+    const int64_t P_ = (int64_t)f.W * f.H;
+    const bool dumps = f.flags & DPR_FLAG_DEBUG_DUMPS;
+    const size_t nd = (size_t)f.spp * f.max_depth * P_;
+    if (!d0->comm) {
+        Dev *root = L[0];
+        for (size_t i = 1; i < L.size(); ++i) {
+            launch_fb_accumulate(P<float4>(root->lv->b_fb_out), P<float4>(L[i]->lv->b_fb_out), P_, root->stream);
+            if (dumps) {
+                launch_u32_accumulate(P<uint32_t>(root->lv->b_events), P<uint32_t>(L[i]->lv->b_events), nd, root->stream);
+                launch_u32_accumulate(P<uint32_t>(root->lv->b_occl), P<uint32_t>(L[i]->lv->b_occl), nd, root->stream);
+            }
+        }
+    } else {
+        Dev *d = d0;
+        NK(ncclGroupStart());
+        NK(ncclReduce(d->lv->b_fb_out.p, d->lv->b_fb_out.p, 4 * P_, ncclFloat, ncclSum, 0, d->comm, d->stream));
+        if (dumps) {
+            NK(ncclReduce(d->lv->b_events.p, d->lv->b_events.p, nd, ncclUint32, ncclSum, 0, d->comm, d->stream));
+            NK(ncclReduce(d->lv->b_occl.p, d->lv->b_occl.p, nd, ncclUint32, ncclSum, 0, d->comm, d->stream));
+        }
+        NK(ncclGroupEnd());
+    }
+    CK(cudaEventRecord(e1, d0->stream));
+    CK(cudaStreamSynchronize(d0->stream));
+    CK(cudaGetLastError());
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    // rays: sum of every rank's local count
+    std::vector<int64_t> mine(L.size() * 3);
+    std::vector<const void *> sends;
+    for (size_t i = 0; i < L.size(); ++i) {
+        for (int k = 0; k < 3; ++k) mine[3 * i + k] = L[i]->lv->stats.rays[k];
+        sends.push_back(&mine[3 * i]);
+    }
+    std::vector<std::vector<char>> out;
+    RET(allgather_host(L, sends, sizeof(int64_t) * 3, out));
+    const int64_t *all = reinterpret_cast<const int64_t *>(out[0].data());
+    for (Dev *d : L) {
+        d->stats = d->lv->stats;
+        d->stats.nranks = N;
+        d->stats.rank = d->rank;
+        for (int k = 0; k < 3; ++k) {
+            d->stats.rays[k] = 0;
+            for (int r = 0; r < N; ++r) d->stats.rays[k] += all[3 * r + k];
+        }
+        d->stats.ms_frame = ms;
+        d->stats.ms_frame_max = ms;
+        d->frame_done = 1;
+        d->dumps_valid = d->rank == 0 && dumps;
+        d->mapped_w = d->rank == 0 ? f.W : 0;
+        d->mapped_h = d->rank == 0 ? f.H : 0;
+        d->frame_out = d->rank == 0 ? P<float>(d->lv->b_fb_out) : nullptr;
+        d->replicated_frame = true;
+    }
+    return DPR_OK;
 }
 
 void release_bufs(Dev *d);
@@ -1357,6 +1451,7 @@ int render_composite(std::vector<Dev *> &L) {
         d->mapped_w = d->rank == 0 ? f.W : 0;
         d->mapped_h = d->rank == 0 ? f.H : 0;
         d->frame_out = d->rank == 0 ? P<float>(d->b_comp_out) : nullptr;
+        d->replicated_frame = false;
     }
     (void)rays;
     return DPR_OK;
@@ -1597,6 +1692,27 @@ int dpr_render_frame_composite_group(dpr_device *devs, int n) {
     return render_composite(L);
 }
 
+int dpr_render_frame_replicated(dpr_device dev) {
+    if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
+    Dev *d = &dev->d;
+    if (d->group) return fail(DPR_ERR_STATE, "loopback devices use dpr_render_frame_replicated_group");
+    CK(cudaSetDevice(d->cuda_dev));
+    std::vector<Dev *> L = {d};
+    return render_replicated(L);
+}
+
+int dpr_render_frame_replicated_group(dpr_device *devs, int n) {
+    if (!devs || n < 1) return fail(DPR_ERR_INVALID_ARG, "bad group");
+    std::vector<Dev *> L;
+    for (int i = 0; i < n; ++i) {
+        if (!devs[i] || !devs[i]->d.group || devs[i]->d.rank != i || devs[i]->d.nranks != n)
+            return fail(DPR_ERR_INVALID_ARG, "devices must be a full loopback group in rank order");
+        L.push_back(&devs[i]->d);
+    }
+    CK(cudaSetDevice(L[0]->cuda_dev));
+    return render_replicated(L);
+}
+
 int dpr_frame_ready(dpr_device dev, int wait) {
     (void)wait;
     if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
@@ -1622,8 +1738,9 @@ int dpr_get_debug(dpr_device dev, const uint32_t **events, const uint32_t **occl
     if (!valid_dev(dev) || !events || !occl) return fail(DPR_ERR_INVALID_ARG, "null argument");
     Dev *d = &dev->d;
     if (d->rank != 0 || !d->dumps_valid) return fail(DPR_ERR_STATE, "no debug dumps (rank 0, DPR_FLAG_DEBUG_DUMPS)");
-    *events = P<uint32_t>(d->b_events);
-    *occl = P<uint32_t>(d->b_occl);
+    Dev *src = d->replicated_frame ? d->lv : d;
+    *events = P<uint32_t>(src->b_events);
+    *occl = P<uint32_t>(src->b_occl);
     return DPR_OK;
 }
 

@@ -430,6 +430,8 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
     bool inimg = valid && x < F.W && y < F.H;
     const int self = A.R.self;
     uint32_t p = (uint32_t)(y * F.W + x);
+    if (F.pix_nranks > 1 && inimg)  // replicated mode: pixel ownership split
+        inimg = (int)(((int64_t)p * F.pix_nranks) / F.P) == F.pix_rank;
     f3 o = mk(F.cE[0], F.cE[1], F.cE[2]), d = mk(0, 0, 0);
     int first = -2;
     if (inimg) {

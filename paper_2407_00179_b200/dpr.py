@@ -106,6 +106,7 @@ EXPORTS = ["dpr_get_unique_id", "dpr_create_device", "dpr_create_loopback_group"
            "dpr_release_device", "dpr_commit_part", "dpr_clear_parts", "dpr_commit_world",
            "dpr_get_world_bounds", "dpr_set_camera", "dpr_set_frame", "dpr_render_frame",
            "dpr_render_frame_group", "dpr_render_frame_composite", "dpr_render_frame_composite_group",
+           "dpr_render_frame_replicated", "dpr_render_frame_replicated_group",
            "dpr_frame_ready", "dpr_map_frame", "dpr_get_debug",
            "dpr_get_stats", "dpr_last_error", "dpr_exchange_plan"]
 
@@ -124,9 +125,10 @@ def load(path: str = LIB_PATH):
     L.dpr_create_device.argtypes = [_c.c_int, _c.c_int, _c.c_int, _P, _P, _P, _P]
     L.dpr_create_loopback_group.argtypes = [_c.c_int, _c.c_int, _P, _P, _P]
     for n in ("dpr_release_device", "dpr_clear_parts", "dpr_commit_world", "dpr_render_frame",
-              "dpr_render_frame_composite"):
+              "dpr_render_frame_composite", "dpr_render_frame_replicated"):
         getattr(L, n).argtypes = [_P]
     L.dpr_render_frame_composite_group.argtypes = [_P, _c.c_int]
+    L.dpr_render_frame_replicated_group.argtypes = [_P, _c.c_int]
     L.dpr_commit_part.argtypes = [_P, _P]
     L.dpr_get_world_bounds.argtypes = [_P, _P]
     L.dpr_set_camera.argtypes = [_P, _P]
@@ -326,6 +328,10 @@ class Device:
         """Compositing contrast device: local renders + deep compositing."""
         _check(load().dpr_render_frame_composite(self.h), self.h)
 
+    def render_frame_replicated(self):
+        """Data-replicated mode: whole world on every rank, pixels split."""
+        _check(load().dpr_render_frame_replicated(self.h), self.h)
+
     def frame_ready(self) -> bool:
         return bool(_check(load().dpr_frame_ready(self.h, 1), self.h))
 
@@ -373,6 +379,11 @@ def loopback_group(nranks: int, cuda_device: int = 0, stream=None, torch_alloc: 
 def render_frame_group(devs: List[Device]):
     arr = (_P * len(devs))(*[d.h for d in devs])
     _check(load().dpr_render_frame_group(arr, len(devs)), devs[0].h)
+
+
+def render_frame_replicated_group(devs: List[Device]):
+    arr = (_P * len(devs))(*[d.h for d in devs])
+    _check(load().dpr_render_frame_replicated_group(arr, len(devs)), devs[0].h)
 
 
 def render_frame_composite_group(devs: List[Device]):
