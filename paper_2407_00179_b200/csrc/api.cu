@@ -298,12 +298,11 @@ int build_world(Dev *d) {
         int64_t cnt = p.nprims();
         if (cnt > 0) {
             launch_bounds(P<float4>(d->b_blo) + off, P<float4>(d->b_bhi) + off, cnt,
-                          P<int>(d->b_bounds) + 12 * (k + 1), d->nsm, s);
+                          P<int>(d->b_bounds) + 12 * (k + 1), P<int>(d->b_bounds), d->nsm, s);
             launches += 2;
         }
         off += cnt;
     }
-    if (n > 0) { launch_bounds(P<float4>(d->b_blo), P<float4>(d->b_bhi), n, P<int>(d->b_bounds), d->nsm, s); launches++; }
     // Morton keys + all digit histograms
     std::vector<unsigned long long> hist(8 * 256, 0);
     if (n > 0) {

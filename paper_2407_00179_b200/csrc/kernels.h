@@ -12,7 +12,7 @@ void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, int64_t
                       float4 *prims, float4 *blo, float4 *bhi, int *bad_index, cudaStream_t s);
 void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims,
                          float4 *blo, float4 *bhi, cudaStream_t s);
-void launch_bounds(const float4 *blo, const float4 *bhi, int64_t n, int *bounds, int nsm,
+void launch_bounds(const float4 *blo, const float4 *bhi, int64_t n, int *bounds, int *bounds_global, int nsm,
                    cudaStream_t s);
 void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
                    uint64_t *keys, uint32_t *vals, cudaStream_t s);

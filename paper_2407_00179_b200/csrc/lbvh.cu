@@ -26,6 +26,10 @@ namespace dpr {
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+#ifndef DPR_MORTON_BITS
+#define DPR_MORTON_BITS 10
+#endif
+
 __device__ __forceinline__ int f2ord(float f) {
     int i = __float_as_int(f);
     return i >= 0 ? i : i ^ 0x7fffffff;
@@ -72,7 +76,7 @@ __global__ void k_sphere_prims(const float4 *__restrict__ sph, int64_t n, uint32
 
 // bounds[0..5] = box lo/hi (ordered ints), bounds[6..11] = centroid lo/hi
 __global__ void k_bounds(const float4 *__restrict__ blo, const float4 *__restrict__ bhi, int64_t n,
-                         int *bounds) {
+                         int *bounds, int *bounds_global) {
     int v[12];
     for (int c = 0; c < 3; ++c) {
         v[c] = 0x7fffffff; v[3 + c] = (int)0x80000000;
@@ -99,8 +103,8 @@ __global__ void k_bounds(const float4 *__restrict__ blo, const float4 *__restric
     }
     if ((threadIdx.x & 31) == 0)
         for (int k = 0; k < 12; ++k) {
-            if ((k % 6) < 3) atomicMin(&bounds[k], v[k]);
-            else atomicMax(&bounds[k], v[k]);
+            if ((k % 6) < 3) { atomicMin(&bounds[k], v[k]); if (bounds_global) atomicMin(&bounds_global[k], v[k]); }
+            else { atomicMax(&bounds[k], v[k]); if (bounds_global) atomicMax(&bounds_global[k], v[k]); }
         }
 }
 
@@ -124,8 +128,11 @@ __global__ void k_morton(const float4 *__restrict__ blo, const float4 *__restric
     for (int a = 0; a < 3; ++a) {
         float mn = ord2f(bounds[6 + a]), mx = ord2f(bounds[9 + a]);
         float ext = mx - mn;
-        float x = ext > 0.0f ? (c[a] - mn) / ext * 2097152.0f : 0.0f;
-        x = fminf(fmaxf(x, 0.0f), 2097151.0f);
+        // DPR_MORTON_BITS per axis (<= 21); high digit passes of the radix sort are skipped
+        // automatically when the keys are shorter (constant digits)
+        const float cells = (float)(1u << DPR_MORTON_BITS);
+        float x = ext > 0.0f ? (c[a] - mn) / ext * cells : 0.0f;
+        x = fminf(fmaxf(x, 0.0f), cells - 1.0f);
         q[a] = (uint64_t)x;
     }
     keys[i] = (expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]);
@@ -611,11 +618,11 @@ void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *
                          float4 *blo, float4 *bhi, cudaStream_t s) {
     if (n > 0) k_sphere_prims<<<nblk(n, 256), 256, 0, s>>>(sph, n, local0, prims, blo, bhi);
 }
-void launch_bounds(const float4 *blo, const float4 *bhi, int64_t n, int *bounds, int nsm,
+void launch_bounds(const float4 *blo, const float4 *bhi, int64_t n, int *bounds, int *bounds_global, int nsm,
                    cudaStream_t s) {
     unsigned g = (unsigned)std::min<int64_t>(nblk(n, 256), (int64_t)nsm * 8);
     if (g == 0) g = 1;
-    k_bounds<<<g, 256, 0, s>>>(blo, bhi, n, bounds);
+    k_bounds<<<g, 256, 0, s>>>(blo, bhi, n, bounds, bounds_global);
 }
 void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
                    uint64_t *keys, uint32_t *vals, cudaStream_t s) {

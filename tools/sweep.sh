@@ -5,7 +5,7 @@ mkdir -p gpurun_out/sweep
 for spec in "$@"; do
   name=${spec%%:*}; defs=${spec#*:}
   python paper_2407_00179_b200/build.py --force --out=/tmp/libdpr_$name.so $defs > gpurun_out/sweep/$name.build 2>&1 || { echo "$name BUILD FAILED"; continue; }
-  DPR_LIB=/tmp/libdpr_$name.so python bench.py --steps 5 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/sweep/$name.json 2> gpurun_out/sweep/$name.err
+  DPR_LIB=/tmp/libdpr_$name.so python bench.py $SWEEP_ARGS --steps 5 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/sweep/$name.json 2> gpurun_out/sweep/$name.err
   python - "$name" <<'PY'
 import json, sys
 n = sys.argv[1]
