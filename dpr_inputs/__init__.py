@@ -37,8 +37,8 @@ def _load():
         build_lib()
         _lib = ctypes.CDLL(_LIB_PATH)
         _lib.dpri_gyroid_mt.restype = ctypes.c_int64
-        _lib.dpri_gyroid_mt.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_void_p,
-                                        ctypes.c_int64, ctypes.c_int]
+        _lib.dpri_gyroid_mt.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p]
         _lib.dpri_volume_field.restype = ctypes.c_int
         _lib.dpri_volume_field.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_int]
@@ -147,18 +147,19 @@ def camera_from_dir(pos, direction, up, fovy_deg, W, H) -> Camera:
 # Geometry generators
 # ----------------------------------------------------------------------------------------
 def gyroid_mesh(G: int, k: float = 4 * math.pi, nthreads: Optional[int] = None):
-    """Marching-tetrahedra gyroid on a G^3 point grid over [-1,1]^3 -> (verts, idx) soup."""
+    """Marching-tetrahedra gyroid on a G^3 point grid over [-1,1]^3 -> indexed mesh
+    (verts (nv,3) f32, one per cut grid edge and shared by its triangles; idx (nt,3) i32)."""
     lib = _load()
-    nt = nthreads or os.cpu_count() or 1
-    n = lib.dpri_gyroid_mt(G, k, None, 0, nt)
+    nth = nthreads or os.cpu_count() or 1
+    nv = ctypes.c_int64(0)
+    n = lib.dpri_gyroid_mt(G, k, None, None, 0, 0, nth, ctypes.byref(nv))
     if n < 0:
         raise RuntimeError("gyroid count failed")
-    out = np.empty((n, 9), np.float32)
-    m = lib.dpri_gyroid_mt(G, k, out.ctypes.data, n, nt)
+    verts = np.empty((nv.value, 3), np.float32)
+    idx = np.empty((n, 3), np.int32)
+    m = lib.dpri_gyroid_mt(G, k, verts.ctypes.data, idx.ctypes.data, nv.value, n, nth, None)
     if m != n:
         raise RuntimeError("gyroid generation failed")
-    verts = out.reshape(-1, 3)
-    idx = np.arange(3 * n, dtype=np.int32).reshape(-1, 3)
     return verts, idx
 
 
@@ -248,16 +249,30 @@ def partition_groups(cen: np.ndarray, nranks: int, strategy: str = "spatial") ->
 def split_mesh(verts: np.ndarray, idx: np.ndarray, nranks: int, albedo,
                strategy: str = "spatial") -> List[Part]:
     """Partition of a triangle mesh over ranks (spatial bisection)."""
-    tri = verts[idx]                      # (m,3,3)
-    cen = tri.astype(np.float64).mean(axis=1)
+    cen = tri_centroids(verts, idx)
     grp = partition_groups(cen, nranks, strategy)
     parts = []
     for r in range(nranks):
-        sel = np.nonzero(grp == r)[0]
-        t = tri[sel].reshape(-1, 3)
-        parts.append(Part(rank=r, kind=TRIS, albedo=albedo, verts=np.ascontiguousarray(t),
-                          idx=np.arange(t.shape[0], dtype=np.int32).reshape(-1, 3)))
+        v, i = submesh(verts, idx, np.nonzero(grp == r)[0])
+        parts.append(Part(rank=r, kind=TRIS, albedo=albedo, verts=v, idx=i))
     return parts
+
+
+def tri_centroids(verts: np.ndarray, idx: np.ndarray) -> np.ndarray:
+    """Triangle centroids in float64 (the partitioning key), chunked to bound memory."""
+    out = np.empty((idx.shape[0], 3), np.float64)
+    for b in range(0, idx.shape[0], 1 << 22):
+        out[b:b + (1 << 22)] = verts[idx[b:b + (1 << 22)]].astype(np.float64).mean(axis=1)
+    return out
+
+
+def submesh(verts: np.ndarray, idx: np.ndarray, sel: np.ndarray):
+    """Triangles `sel` of an indexed mesh with their vertices compacted (vertex order kept)."""
+    t = idx[sel]
+    used = np.zeros(verts.shape[0], bool)
+    used[t.ravel()] = True
+    remap = np.cumsum(used, dtype=np.int64) - 1
+    return np.ascontiguousarray(verts[used]), remap[t].astype(np.int32)
 
 
 def brick_boxes(cells, nparts: int):
@@ -376,16 +391,15 @@ def partition_parts_mixed(sph: np.ndarray, sph_cluster: np.ndarray, palette: np.
                           verts: np.ndarray, idx: np.ndarray, mesh_albedo, nranks: int) -> List[Part]:
     """Bisection of the centroids of ALL prims (spheres + triangles) into nranks groups;
     within a rank: the mesh part, then one sphere part per cluster (commit order)."""
-    tri = verts[idx]
-    cen = np.concatenate([sph[:, :3].astype(np.float64), tri.astype(np.float64).mean(axis=1)])
+    cen = np.concatenate([sph[:, :3].astype(np.float64), tri_centroids(verts, idx)])
     grp = bisect_partition(cen, nranks) if nranks > 1 else np.zeros(cen.shape[0], np.int32)
     gs, gt = grp[:sph.shape[0]], grp[sph.shape[0]:]
     parts = []
     for r in range(nranks):
-        t = tri[gt == r].reshape(-1, 3)
-        if t.shape[0]:
-            parts.append(Part(rank=r, kind=TRIS, albedo=mesh_albedo, verts=np.ascontiguousarray(t),
-                              idx=np.arange(t.shape[0], dtype=np.int32).reshape(-1, 3)))
+        tsel = np.nonzero(gt == r)[0]
+        if tsel.size:
+            v, i = submesh(verts, idx, tsel)
+            parts.append(Part(rank=r, kind=TRIS, albedo=mesh_albedo, verts=v, idx=i))
         sel = np.nonzero(gs == r)[0]
         cl = sph_cluster[sel]
         order = np.argsort(cl, kind="stable")

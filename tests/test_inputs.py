@@ -21,6 +21,23 @@ def test_gyroid_count_scaling_and_determinism():
     assert (area > 0).all()
 
 
+def test_gyroid_indexed_mesh_is_welded_manifold():
+    """One shared vertex per cut grid edge: ~T/2 vertices, every mesh edge used by at most
+    two triangles and almost all (all but the domain boundary / dropped slivers) by two."""
+    v, i = di.gyroid_mesh(41)
+    assert i.min() >= 0 and i.max() < v.shape[0]
+    assert 0.45 < v.shape[0] / i.shape[0] < 0.6
+    e = np.sort(np.concatenate([i[:, [0, 1]], i[:, [1, 2]], i[:, [2, 0]]]), axis=1)
+    _, c = np.unique(e, axis=0, return_counts=True)
+    assert c.max() == 2 and (c == 2).mean() > 0.9
+    # the split keeps the geometry: the parts' triangles are exactly the mesh's triangles
+    parts = di.split_mesh(v, i, 3, (1, 1, 1))
+    got = np.concatenate([p.verts[p.idx].reshape(-1, 9) for p in parts])
+    ref = v[i].reshape(-1, 9)
+    key = lambda a: a[np.lexsort(a.T[::-1])]
+    assert np.array_equal(key(got), key(ref))
+
+
 def test_bisect_partition_balanced():
     rng = np.random.default_rng(0)
     pts = rng.uniform(-1, 1, (1000, 3))
