@@ -85,6 +85,8 @@ class Camera:
     L: np.ndarray
     U: np.ndarray
     V: np.ndarray
+    lens_radius: float = 0.0   # thin-lens depth of field (reading R-DOF); 0 = pinhole
+    focus_dist: float = 0.0
 
 
 @dataclass

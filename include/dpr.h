@@ -63,6 +63,12 @@ typedef enum { DPR_MEMORY_HOST = 0, DPR_MEMORY_DEVICE = 1 } dpr_memory;
 /* frame flags */
 #define DPR_FLAG_JITTER_CENTER 1u  /* camera jitter fixed at 0.5 (test mode) */
 #define DPR_FLAG_DEBUG_DUMPS 2u    /* record P13 event / occlusion dumps (parity mode) */
+#define DPR_FLAG_RING 8u            /* ring schedule instead of the visit rule ("wave-fronts
+                                      are exchanged in a ring buffer"; reading R-RING):
+                                      every ray of pixel p starts at rank floor(p*N/(W*H)), is
+                                      traced by every rank in ring order without culling or
+                                      early-out, resolves at the last one; children go home.
+                                      Same image, events and occlusion bits as the visit rule */
 #define DPR_FLAG_NO_BACKGROUND 4u  /* misses add no background (set internally for the local
                                       renders of the compositing contrast device) */
 
@@ -110,10 +116,15 @@ typedef struct {
     float bounds_hint[6]; /* lo xyz, hi xyz */
 } dpr_part_desc;
 
-/* Pinhole camera basis, float32, identical on all ranks.  Primary ray through
- * pixel (x,y) (bottom-left origin, row-major) with jitter (jx,jy):
- * dir = normalize(L + ((x+jx)/W)*U + ((y+jy)/H)*V), origin E. */
-typedef struct { float E[3], L[3], U[3], V[3]; } dpr_camera_basis;
+/* Camera basis, float32, identical on all ranks.  Primary ray through pixel
+ * (x,y) (bottom-left origin, row-major) with jitter (jx,jy):
+ *   q = L + ((x+jx)/W)*U + ((y+jy)/H)*V;  dir = normalize(q), origin E.
+ * Depth of field ("rendered with depth of field"; reading R-DOF): with
+ * lens_radius > 0 the origin is a point of the thin lens (radius lens_radius, in the plane
+ * spanned by U and V, sampled by Philox purpose 1) and the ray passes through the point
+ * E + focus_dist*q of the focal plane (distance focus_dist along the view axis).
+ * lens_radius == 0 is the pinhole camera bit for bit; focus_dist must then be ignored. */
+typedef struct { float E[3], L[3], U[3], V[3]; float lens_radius, focus_dist; } dpr_camera_basis;
 
 /* Frame / renderer parameters, identical on all ranks.
  *   W,H pixels; spp samples per pixel, traced in batches of spp_batch samples (bounded

@@ -49,7 +49,8 @@ class or_part(ctypes.Structure):
 
 class or_camera(ctypes.Structure):
     _fields_ = [("E", ctypes.c_float * 3), ("L", ctypes.c_float * 3),
-                ("U", ctypes.c_float * 3), ("V", ctypes.c_float * 3)]
+                ("U", ctypes.c_float * 3), ("V", ctypes.c_float * 3),
+                ("lens_radius", ctypes.c_float), ("focus_dist", ctypes.c_float)]
 
 
 class or_frame(ctypes.Structure):
@@ -148,6 +149,7 @@ def make_part(p: di.Part, keep: list) -> or_part:
 def make_camera(c: di.Camera) -> or_camera:
     o = or_camera()
     o.E, o.L, o.U, o.V = _fa(c.E), _fa(c.L), _fa(c.U), _fa(c.V)
+    o.lens_radius, o.focus_dist = float(c.lens_radius), float(c.focus_dist)
     return o
 
 

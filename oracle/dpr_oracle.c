@@ -59,7 +59,7 @@ typedef struct {
     float tf_lo, tf_hi, density_scale;
 } or_part;
 
-typedef struct { float E[3], L[3], U[3], V[3]; } or_camera;
+typedef struct { float E[3], L[3], U[3], V[3]; float lens_radius, focus_dist; } or_camera;
 
 typedef struct {
     int32_t W, H, spp, spp_batch, max_depth, ao_k;
@@ -67,7 +67,8 @@ typedef struct {
     float light_dir[3], E[3], A[3], B[3];
     float dt;
     uint64_t seed;
-    int32_t flags; /* bit0: jitter fixed at 0.5; bit2: no background (local render of the
+    int32_t flags; /* bit0: jitter fixed at 0.5; bit3: ring schedule (routing simulator);
+                      bit2: no background (local render of the
                       compositing contrast device) */
 } or_frame;
 
@@ -96,7 +97,7 @@ static void philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], ui
 /* u = (float)(x>>8) * 2^-24, in [0, 1-2^-24] exactly (P1). */
 static float u01(uint32_t x) { return (float)(x >> 8) * 0x1p-24f; }
 
-enum { PUR_CAMERA = 0, PUR_AO = 2, PUR_BOUNCE = 3, PUR_VOL_PATH = 4, PUR_VOL_SHADOW = 5,
+enum { PUR_CAMERA = 0, PUR_LENS = 1, PUR_AO = 2, PUR_BOUNCE = 3, PUR_VOL_PATH = 4, PUR_VOL_SHADOW = 5,
        PUR_VOL_AO = 6, PUR_ISO = 7 };
 
 /* Counter = (p, s, (depth<<8)|purpose, sub); key = (seed lo, seed hi)  (P1). */
@@ -803,9 +804,38 @@ static void camera_ray(const or_camera *cam, const or_frame *fr, uint32_t p, uin
     float sy = ((float)y + jy) / (float)fr->H;
     v3 L = vload(cam->L), U = vload(cam->U), Vv = vload(cam->V);
     v3 q = V3((L.x + sx * U.x) + sy * Vv.x, (L.y + sx * U.y) + sy * Vv.y, (L.z + sx * U.z) + sy * Vv.z);
-    float len = sqrtf(vdot(q, q));
-    *d = V3(q.x / len, q.y / len, q.z / len);
-    *o = vload(cam->E);
+    v3 E = vload(cam->E);
+    if (!(cam->lens_radius > 0.0f)) {
+        /* pinhole (P2) */
+        float len = sqrtf(vdot(q, q));
+        *d = V3(q.x / len, q.y / len, q.z / len);
+        *o = E;
+        return;
+    }
+    /* Thin lens ("rendered with depth of field"; reading R-DOF).
+     * 1. lens point (lx, ly) uniform in the unit disc: the first of 16 Philox draws
+     *    (purpose 1, sub = attempt) with lx^2 + ly^2 <= 1, else the centre;
+     * 2. lens axes: U and V normalised;
+     * 3. origin o = E + (r*lx) Uhat + (r*ly) Vhat;
+     * 4. the pinhole ray's point on the focal plane F = E + focus_dist * q (q has unit
+     *    component along the view axis, so F lies focus_dist in front of the lens);
+     * 5. direction d = normalize(F - o). */
+    float lx = 0.0f, ly = 0.0f;
+    for (uint32_t a = 0; a < 16; ++a) {
+        uint32_t r[4];
+        rng4(fr->seed, p, s, 0, PUR_LENS, a, r);
+        float ax = 2.0f * u01(r[0]) - 1.0f, ay = 2.0f * u01(r[1]) - 1.0f;
+        if (ax * ax + ay * ay <= 1.0f) { lx = ax; ly = ay; break; }
+    }
+    float lu = sqrtf(vdot(U, U)), lv = sqrtf(vdot(Vv, Vv));
+    v3 Uh = V3(U.x / lu, U.y / lu, U.z / lu), Vh = V3(Vv.x / lv, Vv.y / lv, Vv.z / lv);
+    float a = cam->lens_radius * lx, b = cam->lens_radius * ly;
+    v3 oo = V3((E.x + a * Uh.x) + b * Vh.x, (E.y + a * Uh.y) + b * Vh.y, (E.z + a * Uh.z) + b * Vh.z);
+    v3 F = V3(E.x + cam->focus_dist * q.x, E.y + cam->focus_dist * q.y, E.z + cam->focus_dist * q.z);
+    v3 g = V3(F.x - oo.x, F.y - oo.y, F.z - oo.z);
+    float lg = sqrtf(vdot(g, g));
+    *d = V3(g.x / lg, g.y / lg, g.z / lg);
+    *o = oo;
 }
 
 /* Cosine-weighted direction about n by rejection (P7) + Duff et al. 2017 frame. */
@@ -967,7 +997,14 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
     pr.w = V3(1.0f, 1.0f, 1.0f);
     pr.depth = 0;
     L->gen[K_PATH]++;
-    pr.rank = dp ? first_candidate(sc, pr.o, pr.d, INFINITY) : -1;
+    /* ring schedule (frame flag bit3; "wave-fronts are exchanged in a ring buffer";
+     * reading R-RING): every ray of pixel p starts at its home rank
+     * home(p) = floor(p*N/(W*H)) and is traced by home, home+1, ..., home+N-1 (mod N)
+     * without culling or early-out; it resolves at the last of them and its children are
+     * sent home. */
+    const int ring = dp && (fr->flags & 8);
+    const int home = (int)(((int64_t)p * N) / ((int64_t)fr->W * fr->H));
+    pr.rank = ring ? home : dp ? first_candidate(sc, pr.o, pr.d, INFINITY) : -1;
     pr.step = 0;
     int resolved_now = dp && pr.rank < 0;
     if (resolved_now) {
@@ -992,7 +1029,8 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
                     L->V[K_PATH * N + at]++;
                     note_step(L, batch, ray.step);
                     trace_path_at(J, at, &ray, &vk, &best);
-                    int nx = next_candidate(sc, at, ray.o, ray.d, ray.tmax, best.t);
+                    int nx = ring ? ((at + 1) % N == home ? -1 : (at + 1) % N)
+                                  : next_candidate(sc, at, ray.o, ray.d, ray.tmax, best.t);
                     if (nx < 0) break;
                     L->S[(K_PATH * N + at) * N + nx]++;
                     at = nx;
@@ -1061,7 +1099,7 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
                 ORay ch = kids[i];
                 L->gen[ch.kind]++;
                 if (dp) {
-                    int first = first_candidate(sc, ch.o, ch.d, ch.tmax);
+                    int first = ring ? home : first_candidate(sc, ch.o, ch.d, ch.tmax);
                     if (first < 0) {
                         /* resolves immediately at `at` */
                         if (ch.kind == K_PATH) {
@@ -1092,8 +1130,12 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
                 for (;;) {
                     L->V[ray.kind * N + at]++;
                     note_step(L, batch, ray.step);
-                    if (trace_occl_at(J, at, &ray, &vk)) { occluded = 1; break; }
-                    int nx = next_candidate(sc, at, ray.o, ray.d, ray.tmax, ray.tmax);
+                    if (!occluded && trace_occl_at(J, at, &ray, &vk)) {
+                        occluded = 1;
+                        if (!ring) break;   /* ring: no early-out, the ray completes the ring */
+                    }
+                    int nx = ring ? ((at + 1) % N == home ? -1 : (at + 1) % N)
+                                  : next_candidate(sc, at, ray.o, ray.d, ray.tmax, ray.tmax);
                     if (nx < 0) break;
                     L->S[(ray.kind * N + at) * N + nx]++;
                     at = nx;

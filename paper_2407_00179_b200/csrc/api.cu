@@ -625,6 +625,8 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     for (int c = 0; c < 3; ++c) {
         a.F.l[c] = f.light_dir[c]; a.F.E[c] = f.E[c]; a.F.A[c] = f.A[c]; a.F.B[c] = f.B[c];
         a.F.cE[c] = d->cam.E[c]; a.F.cL[c] = d->cam.L[c]; a.F.cU[c] = d->cam.U[c]; a.F.cV[c] = d->cam.V[c];
+    a.F.lens_radius = d->cam.lens_radius;
+    a.F.focus_dist = d->cam.focus_dist;
     }
     a.R = fc.R;
     a.R.self = d->rank;
@@ -1633,6 +1635,8 @@ int dpr_get_world_bounds(dpr_device dev, float lohi_host[6]) {
 
 int dpr_set_camera(dpr_device dev, const dpr_camera_basis *cam) {
     if (!valid_dev(dev) || !cam) return fail(DPR_ERR_INVALID_ARG, "null argument");
+    if (!(cam->lens_radius >= 0.0f) || (cam->lens_radius > 0.0f && !(cam->focus_dist > 0.0f)))
+        return fail(DPR_ERR_INVALID_ARG, "lens_radius must be >= 0 and focus_dist > 0 when lens_radius > 0");
     dev->d.cam = *cam;
     dev->d.cam_set = true;
     return DPR_OK;

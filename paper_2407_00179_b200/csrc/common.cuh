@@ -29,7 +29,7 @@ constexpr uint32_t VOL_BIT = 0x80000000u;
 constexpr uint32_t SPHERE_BIT = 0x80000000u;  // in a prim record's id word
 
 enum Kind { K_PATH = 0, K_SHADOW = 1, K_AO = 2 };
-enum Purpose { PUR_CAMERA = 0, PUR_AO = 2, PUR_BOUNCE = 3, PUR_VOL_PATH = 4,
+enum Purpose { PUR_CAMERA = 0, PUR_LENS = 1, PUR_AO = 2, PUR_BOUNCE = 3, PUR_VOL_PATH = 4,
                PUR_VOL_SHADOW = 5, PUR_VOL_AO = 6, PUR_ISO = 7 };
 
 // Per-kernel work counters (kc[0] = k_trace_path, kc[1] = k_trace_occl): the inputs of the

@@ -69,6 +69,7 @@ struct FrameDev {
     uint64_t seed;
     uint32_t flags;
     float cE[3], cL[3], cU[3], cV[3];  // camera basis (P2)
+    float lens_radius, focus_dist;     // thin lens (reading R-DOF); 0 = pinhole
     int pix_rank, pix_nranks;          // replicated mode: generate only pixels owned by pix_rank
 };
 

@@ -445,13 +445,35 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
         float sy = ((float)y + jy) / (float)F.H;
         f3 q = mk((F.cL[0] + sx * F.cU[0]) + sy * F.cV[0], (F.cL[1] + sx * F.cU[1]) + sy * F.cV[1],
                   (F.cL[2] + sx * F.cU[2]) + sy * F.cV[2]);
-        float len = sqrtf(dot(q, q));
-        d = mk(q.x / len, q.y / len, q.z / len);
-        first = first_candidate(A.R, o, d, __int_as_float(0x7f800000));
+        if (F.lens_radius > 0.0f) {
+            // thin lens (reading R-DOF): rejection-sampled disc point, focal point E + fd*q
+            float lx = 0.0f, ly = 0.0f;
+            for (uint32_t att = 0; att < 16; ++att) {
+                uint4 r = rng4(F.seed, p, s, 0, PUR_LENS, att);
+                float ax = 2.0f * u01(r.x) - 1.0f, ay = 2.0f * u01(r.y) - 1.0f;
+                if (ax * ax + ay * ay <= 1.0f) { lx = ax; ly = ay; break; }
+            }
+            f3 U = mk(F.cU[0], F.cU[1], F.cU[2]), V = mk(F.cV[0], F.cV[1], F.cV[2]);
+            float lu = sqrtf(dot(U, U)), lv = sqrtf(dot(V, V));
+            f3 Uh = mk(U.x / lu, U.y / lu, U.z / lu), Vh = mk(V.x / lv, V.y / lv, V.z / lv);
+            float a = F.lens_radius * lx, b = F.lens_radius * ly;
+            o = mk((F.cE[0] + a * Uh.x) + b * Vh.x, (F.cE[1] + a * Uh.y) + b * Vh.y, (F.cE[2] + a * Uh.z) + b * Vh.z);
+            f3 g = mk((F.cE[0] + F.focus_dist * q.x) - o.x, (F.cE[1] + F.focus_dist * q.y) - o.y,
+                      (F.cE[2] + F.focus_dist * q.z) - o.z);
+            float lg = sqrtf(dot(g, g));
+            d = mk(g.x / lg, g.y / lg, g.z / lg);
+        } else {
+            float len = sqrtf(dot(q, q));
+            d = mk(q.x / len, q.y / len, q.z / len);
+        }
+        if (!(F.flags & DPR_FLAG_RING)) first = first_candidate(A.R, o, d, __int_as_float(0x7f800000));
     }
     bool keep = first == self;
     bool owner_keep = false;
-    if (inimg && first == -1) {
+    if (F.flags & DPR_FLAG_RING) {
+        // ring schedule (reading R-RING): the home rank generates its pixels, no culling
+        keep = inimg && (int)(((int64_t)p * A.R.nranks) / F.P) == self;
+    } else if (inimg && first == -1) {
         int owner = (int)(((int64_t)p * A.R.nranks) / F.P);
         owner_keep = owner == self;
     }
@@ -617,7 +639,11 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
         const uint32_t p = __float_as_uint(r.c.w);
         const uint32_t meta = __float_as_uint(r.e.w);
         const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
-        int next = active ? next_candidate(A.R, self, o, d, INF, bt) : -1;
+        const bool ring = F.flags & DPR_FLAG_RING;
+        const int home = (int)(((int64_t)p * N) / F.P);
+        int next = -1;
+        if (ring) next = (active && (self + 1) % N != home) ? (self + 1) % N : -1;  // R-RING
+        else if (active) next = next_candidate(A.R, self, o, d, INF, bt);
         bool fwd = active && next >= 0;
         uint32_t pos = 0xffffffffu;
         if (__syncthreads_or(fwd))
@@ -689,7 +715,7 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
                     }
                 }
             }
-            int first = has ? first_candidate(A.R, org, cd, ctmax) : -1;
+            int first = has ? (ring ? home : first_candidate(A.R, org, cd, ctmax)) : -1;
             bool app = has && first >= 0;
             bool imm = has && first < 0;  // no candidate: resolves immediately here
             const bool is_path = slot == K + 1;
@@ -771,8 +797,15 @@ __global__ void __launch_bounds__(256) k_resolve_occl(const __grid_constant__ St
         const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
         const bool occluded = tmax < 0.0f;
         if (active) { if (slot == 0) v_s++; else v_a++; }
-        int next = (active && !occluded) ? next_candidate(A.R, self, o, d, tmax, tmax) : -1;
-        bool fwd = active && !occluded && next >= 0;
+        int next = -1;
+        if (F.flags & DPR_FLAG_RING) {
+            // ring (reading R-RING): occluded or not, the ray completes the ring
+            const int home = (int)(((int64_t)p * N) / F.P);
+            next = (active && (self + 1) % N != home) ? (self + 1) % N : -1;
+        } else if (active && !occluded) {
+            next = next_candidate(A.R, self, o, d, tmax, tmax);
+        }
+        bool fwd = active && next >= 0;
         warp_count(fwd, (slot == 0 ? K_SHADOW : K_AO) * DPR_MAX_RANKS + next, &A.ctr->S[0][0]);
         uint32_t pos = 0xffffffffu;
         if (__syncthreads_or(fwd))

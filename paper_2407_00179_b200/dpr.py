@@ -22,6 +22,7 @@ DPR_OK = 0
 DPR_MAX_RANKS = 16
 DPR_FLAG_JITTER_CENTER = 1
 DPR_FLAG_DEBUG_DUMPS = 2
+DPR_FLAG_RING = 8
 ERRORS = {-1: "DPR_ERR_INVALID_ARG", -2: "DPR_ERR_STATE", -3: "DPR_ERR_CUDA", -4: "DPR_ERR_NCCL",
           -5: "DPR_ERR_CONSISTENCY", -6: "DPR_ERR_OOM", -7: "DPR_ERR_QUEUE_OVERFLOW"}
 
@@ -49,7 +50,7 @@ class dpr_part_desc(_c.Structure):
 
 class dpr_camera_basis(_c.Structure):
     _fields_ = [("E", _c.c_float * 3), ("L", _c.c_float * 3), ("U", _c.c_float * 3),
-                ("V", _c.c_float * 3)]
+                ("V", _c.c_float * 3), ("lens_radius", _c.c_float), ("focus_dist", _c.c_float)]
 
 
 class dpr_frame_desc(_c.Structure):
@@ -240,6 +241,7 @@ def part_desc(p, keep: list, device_arrays: bool = False) -> dpr_part_desc:
 def camera_struct(cam) -> dpr_camera_basis:
     c = dpr_camera_basis()
     c.E, c.L, c.U, c.V = [(_c.c_float * 3)(*[float(x) for x in v]) for v in (cam.E, cam.L, cam.U, cam.V)]
+    c.lens_radius, c.focus_dist = float(getattr(cam, "lens_radius", 0.0)), float(getattr(cam, "focus_dist", 0.0))
     return c
 
 

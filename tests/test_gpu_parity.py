@@ -202,3 +202,55 @@ def test_partition_strategies(strategy):
     g = gpu_render(sc.parts, 4, sc.camera, sc.frame)
     o = oracle_render(sc.parts, 4, sc.camera, sc.frame)
     assert_parity(g, o)
+
+
+@pytest.mark.parametrize("nranks", [1, 3])
+def test_depth_of_field(nranks):
+    """NEXT f4: thin-lens camera (reading R-DOF).  Primary origins vary per sample,
+    so the first-candidate rank of each primary differs too: events, occlusion bits and
+    routing bit-exact on the config2 family and on configs[0]."""
+    import dataclasses
+    sc = di.config2(nranks=nranks, G=41, W=72, H=56, spp=4, spp_batch=2)
+    cam = dataclasses.replace(sc.camera, lens_radius=0.15, focus_dist=3.2)
+    g = gpu_render(sc.parts, nranks, cam, sc.frame)
+    o = oracle_render(sc.parts, nranks, cam, sc.frame)
+    assert_parity(g, o)
+    c1 = di.config1()
+    cam1 = dataclasses.replace(c1.camera, lens_radius=0.3, focus_dist=5.0)
+    fr1 = di.Frame(**{**c1.frame.__dict__, "spp": 4, "spp_batch": 4})
+    g = gpu_render(c1.parts, 2, cam1, fr1)
+    o = oracle_render(c1.parts, 2, cam1, fr1)
+    assert_parity(g, o)
+
+
+@pytest.mark.parametrize("nranks,mode", [(1, "sendrecv"), (3, "sendrecv"), (4, "fused"), (8, "sendrecv")])
+def test_ring_schedule(nranks, mode, monkeypatch):
+    """NEXT f4: ring schedule (reading R-RING, DPR_FLAG_RING): every ray visits every
+    rank in ring order.  Events/occlusion bits/pixels equal the visit rule's, and the ring's
+    own routing matrices, visit counts and step counts equal the oracle's simulator."""
+    monkeypatch.setenv("DPR_EXCHANGE", mode)
+    parts = _random_world(nranks + 10, nranks)
+    W = H = 40
+    cam = di.camera_basis((0.3, 0.8, -3.5), (0, 0, 0), (0, 1, 0), 45.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=3, spp_batch=2, max_depth=3, ao_k=2, ao_radius=0.6,
+                  light_dir=di.f32(di.normalize((0.4, 1, -0.3))), E=(1, 1, 1), A=(0.3, 0.3, 0.3),
+                  B=(0.1, 0.1, 0.2), flags=8)
+    g = gpu_render(parts, nranks, cam, fr)
+    o = oracle_render(parts, nranks, cam, fr)
+    assert_parity(g, o)
+    if nranks > 1:
+        assert (o.V == o.gen[:, None]).all()
+
+
+def test_ring_schedule_volume_and_config2():
+    """Ring schedule with bricks (stochastic DVR, binary volume shadows) and on the config2
+    family over 4 spatial ranks."""
+    parts, h = _volume_scene(33, 4, 4)
+    W = H = 32
+    cam = di.camera_basis((0.3, 1.5, -3.0), (0, -0.2, 0), (0, 1, 0), 50.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=2, spp_batch=2, max_depth=2, ao_k=1, ao_radius=0.3, dt=h,
+                  light_dir=di.f32(di.normalize((0.2, 1, 0.1))), E=(1, 1, 1), A=(0.2, 0.2, 0.2), flags=8)
+    assert_parity(gpu_render(parts, 4, cam, fr), oracle_render(parts, 4, cam, fr))
+    sc = di.config2(nranks=4, G=41, W=64, H=48, spp=2, spp_batch=2)
+    fr = di.Frame(**{**sc.frame.__dict__, "flags": 8})
+    assert_parity(gpu_render(sc.parts, 4, sc.camera, fr), oracle_render(sc.parts, 4, sc.camera, fr))
