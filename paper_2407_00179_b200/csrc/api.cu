@@ -96,7 +96,7 @@ struct Dev {
     Buf b_prims_u, b_blo, b_bhi, b_keys[2], b_vals[2], b_tile, b_left, b_right, b_parent, b_rlo,
         b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_bounds, b_hist, b_wnodes,
         b_prims_w, b_items[2], b_wcnt, b_wperm, b_witems[2], b_size;
-    int builder = 1;  // 0 PLOC, 1 Karras LBVH (default; env DPR_BUILDER=ploc|lbvh; sweep r01)
+    int builder = 1;  // 0 PLOC, 1 agglomerative LBVH (default), 2 Karras + refit (env DPR_BUILDER=ploc|karras)
     int build_iters = 0;
     int64_t wnodes_count = 0;
     int bvh_levels = 0;
@@ -290,17 +290,15 @@ int build_world(Dev *d) {
         if (p.kind == DPR_PART_TRIANGLES) {
             launch_tri_prims(P<float>(p.verts), P<int32_t>(p.idx), p.nt, p.nv, (uint32_t)off,
                              P<float4>(d->b_prims_u), P<float4>(d->b_blo), P<float4>(d->b_bhi),
-                             P<int>(d->b_bounds) + 12 * (np + 1), s);
+                             P<int>(d->b_bounds) + 12 * (np + 1), P<int>(d->b_bounds) + 12 * (k + 1),
+                             P<int>(d->b_bounds), d->nsm, s);
         } else if (p.kind == DPR_PART_SPHERES) {
             launch_sphere_prims(P<float4>(p.spheres), p.ns, (uint32_t)off, P<float4>(d->b_prims_u),
-                                P<float4>(d->b_blo), P<float4>(d->b_bhi), s);
+                                P<float4>(d->b_blo), P<float4>(d->b_bhi), P<int>(d->b_bounds) + 12 * (k + 1),
+                                P<int>(d->b_bounds), d->nsm, s);
         }
         int64_t cnt = p.nprims();
-        if (cnt > 0) {
-            launch_bounds(P<float4>(d->b_blo) + off, P<float4>(d->b_bhi) + off, cnt,
-                          P<int>(d->b_bounds) + 12 * (k + 1), P<int>(d->b_bounds), d->nsm, s);
-            launches += 2;
-        }
+        if (cnt > 0) launches += 1;
         off += cnt;
     }
     // Morton keys + all digit histograms
@@ -424,6 +422,16 @@ int build_world(Dev *d) {
                 CK(cudaMemcpyAsync(&root_id, cl[c], sizeof(int), cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
                 d->build_iters = iters;
+            } else if (d->builder == 1) {
+                // agglomerative LBVH (default): topology + boxes in one bottom-up pass
+                RET(ensure(d, d->b_arrive, sizeof(int) * (n - 1) + sizeof(int)));
+                int *other = P<int>(d->b_arrive);
+                CK(cudaMemsetAsync(other, 0xff, sizeof(int) * (n - 1), s));
+                launch_agglo(keys, n, P<float4>(d->b_slo), P<float4>(d->b_shi), P<int>(d->b_left), P<int>(d->b_right),
+                             P<int>(d->b_size), P<float4>(d->b_nlo), P<float4>(d->b_nhi), other, other + (n - 1), s);
+                launches++;
+                CK(cudaMemcpyAsync(&root_id, other + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
             } else {
                 // Karras 2012 LBVH + bottom-up refit
                 RET(ensure(d, d->b_rlo, sizeof(int) * (n - 1)));
@@ -1180,7 +1188,8 @@ int init_dev(Dev *d, int rank, int nranks, int cuda_device, void *stream, const 
     CK(cudaDeviceGetAttribute(&d->nsm, cudaDevAttrMultiProcessorCount, cuda_device));
     for (int c = 0; c < 3; ++c) { d->box[c] = INFINITY; d->box[3 + c] = -INFINITY; }
     if (const char *e = getenv("DPR_SPW")) d->spw = std::max(1, atoi(e));
-    if (const char *e = getenv("DPR_BUILDER")) d->builder = strcmp(e, "ploc") == 0 ? 0 : 1;
+    if (const char *e = getenv("DPR_BUILDER"))
+        d->builder = strcmp(e, "ploc") == 0 ? 0 : strcmp(e, "karras") == 0 ? 2 : 1;
     if (const char *e = getenv("DPR_EXCHANGE")) d->exch = strcmp(e, "fused") == 0 ? 1 : 0;
     return DPR_OK;
 }

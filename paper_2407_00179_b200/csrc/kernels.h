@@ -9,11 +9,10 @@ namespace dpr {
 
 // ---- lbvh.cu ---------------------------------------------------------------------------
 void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, int64_t nv, uint32_t local0,
-                      float4 *prims, float4 *blo, float4 *bhi, int *bad_index, cudaStream_t s);
-void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims,
-                         float4 *blo, float4 *bhi, cudaStream_t s);
-void launch_bounds(const float4 *blo, const float4 *bhi, int64_t n, int *bounds, int *bounds_global, int nsm,
-                   cudaStream_t s);
+                      float4 *prims, float4 *blo, float4 *bhi, int *bad_index, int *bounds, int *bounds_global,
+                      int nsm, cudaStream_t s);
+void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi,
+                         int *bounds, int *bounds_global, int nsm, cudaStream_t s);
 void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
                    uint64_t *keys, uint32_t *vals, cudaStream_t s);
 void launch_digit_hist_all(const uint64_t *keys, int64_t n, unsigned long long *hist, int nsm,
@@ -26,6 +25,8 @@ void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *
 void launch_refit(int64_t n, const int *left, const int *right, const int *parent,
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
                   cudaStream_t s);
+void launch_agglo(const uint64_t *keys, int64_t n, const float4 *slo, const float4 *shi, int *left, int *right,
+                  int *size, float4 *nlo, float4 *nhi, int *other, int *root_out, cudaStream_t s);
 void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
                          const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,
                          cudaStream_t s);

@@ -4,8 +4,9 @@
 // builds a local structure over its own parts.  B200 has no RT cores, so the
 // structure and its traversal are hand-written: a linear BVH (Karras 2012, "Maximizing
 // parallelism in the construction of BVHs, octrees and k-d trees"):
-//   1. k_tri_prims / k_sphere_prims: prim records + exact AABBs (min/max, no rounding)
-//   2. k_bounds: rank box and centroid box (order-preserving integer atomics)
+//   1. k_tri_prims / k_sphere_prims: prim records + exact AABBs (min/max, no rounding), and
+//      in the same pass the part's / rank's box and centroid box (order-preserving integer
+//      atomics after a warp reduction)
 //   3. k_morton: 63-bit Morton code of the centroid (21 bits per axis)
 //   4. LSD radix sort of (key u64, index u32), 8-bit digits, stable per-tile ranking with
 //      warp match + shared-memory digit prefix; passes whose digit is constant are skipped
@@ -37,54 +38,18 @@ __device__ __forceinline__ int f2ord(float f) {
 __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
 
 // ---------------------------------------------------------------------------------------
-__global__ void k_tri_prims(const float *__restrict__ verts, const int32_t *__restrict__ idx,
-                            int64_t n, int64_t nv, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi,
-                            int *bad_index) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    int64_t i0 = idx[3 * t], i1 = idx[3 * t + 1], i2 = idx[3 * t + 2];
-    if (i0 < 0 || i0 >= nv || i1 < 0 || i1 >= nv || i2 < 0 || i2 >= nv) {  // validated here, on the GPU
-        atomicExch(bad_index, 1);
-        i0 = i1 = i2 = 0;
-    }
-    f3 v0 = mk(verts[3 * i0], verts[3 * i0 + 1], verts[3 * i0 + 2]);
-    f3 v1 = mk(verts[3 * i1], verts[3 * i1 + 1], verts[3 * i1 + 2]);
-    f3 v2 = mk(verts[3 * i2], verts[3 * i2 + 1], verts[3 * i2 + 2]);
-    f3 e1 = sub(v1, v0), e2 = sub(v2, v0);
-    int64_t g = local0 + t;
-    prims[3 * g + 0] = make_float4(v0.x, v0.y, v0.z, __uint_as_float((uint32_t)g));
-    prims[3 * g + 1] = make_float4(e1.x, e1.y, e1.z, 0.0f);
-    prims[3 * g + 2] = make_float4(e2.x, e2.y, e2.z, 0.0f);
-    blo[g] = make_float4(fminf(fminf(v0.x, v1.x), v2.x), fminf(fminf(v0.y, v1.y), v2.y),
-                         fminf(fminf(v0.z, v1.z), v2.z), 0.0f);
-    bhi[g] = make_float4(fmaxf(fmaxf(v0.x, v1.x), v2.x), fmaxf(fmaxf(v0.y, v1.y), v2.y),
-                         fmaxf(fmaxf(v0.z, v1.z), v2.z), 0.0f);
-}
-
-__global__ void k_sphere_prims(const float4 *__restrict__ sph, int64_t n, uint32_t local0,
-                               float4 *prims, float4 *blo, float4 *bhi) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    float4 s = sph[t];
-    int64_t g = local0 + t;
-    prims[3 * g + 0] = make_float4(s.x, s.y, s.z, __uint_as_float((uint32_t)g | SPHERE_BIT));
-    prims[3 * g + 1] = make_float4(s.w, 0.0f, 0.0f, 0.0f);
-    prims[3 * g + 2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    blo[g] = make_float4(s.x - s.w, s.y - s.w, s.z - s.w, 0.0f);
-    bhi[g] = make_float4(s.x + s.w, s.y + s.w, s.z + s.w, 0.0f);
-}
-
-// bounds[0..5] = box lo/hi (ordered ints), bounds[6..11] = centroid lo/hi
-__global__ void k_bounds(const float4 *__restrict__ blo, const float4 *__restrict__ bhi, int64_t n,
-                         int *bounds, int *bounds_global) {
+// Prim records + exact AABBs, with the part's box and centroid box reduced in the same pass:
+// bounds[0..5] = box lo/hi, bounds[6..11] = centroid lo/hi (order-preserving ints), merged
+// into the part's slot and the global slot by one warp reduction + atomics per warp.
+struct BoundsAcc {
     int v[12];
-    for (int c = 0; c < 3; ++c) {
-        v[c] = 0x7fffffff; v[3 + c] = (int)0x80000000;
-        v[6 + c] = 0x7fffffff; v[9 + c] = (int)0x80000000;
+    __device__ __forceinline__ void init() {
+        for (int c = 0; c < 3; ++c) {
+            v[c] = 0x7fffffff; v[3 + c] = (int)0x80000000;
+            v[6 + c] = 0x7fffffff; v[9 + c] = (int)0x80000000;
+        }
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        float4 lo = blo[i], hi = bhi[i];
+    __device__ __forceinline__ void add(f3 lo, f3 hi) {
         float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
         for (int c = 0; c < 3; ++c) {
             float cen = (l[c] + h[c]) * 0.5f;
@@ -94,18 +59,66 @@ __global__ void k_bounds(const float4 *__restrict__ blo, const float4 *__restric
             v[9 + c] = max(v[9 + c], f2ord(cen));
         }
     }
-    for (int k = 0; k < 12; ++k) {
-        bool isMin = (k % 6) < 3;
-        for (int o = 16; o > 0; o >>= 1) {
-            int w = __shfl_xor_sync(0xffffffffu, v[k], o);
-            v[k] = isMin ? min(v[k], w) : max(v[k], w);
-        }
-    }
-    if ((threadIdx.x & 31) == 0)
+    __device__ __forceinline__ void flush(int *bounds, int *bounds_global) {
         for (int k = 0; k < 12; ++k) {
-            if ((k % 6) < 3) { atomicMin(&bounds[k], v[k]); if (bounds_global) atomicMin(&bounds_global[k], v[k]); }
-            else { atomicMax(&bounds[k], v[k]); if (bounds_global) atomicMax(&bounds_global[k], v[k]); }
+            bool isMin = (k % 6) < 3;
+            for (int o = 16; o > 0; o >>= 1) {
+                int w = __shfl_xor_sync(0xffffffffu, v[k], o);
+                v[k] = isMin ? min(v[k], w) : max(v[k], w);
+            }
         }
+        if ((threadIdx.x & 31) == 0)
+            for (int k = 0; k < 12; ++k) {
+                if ((k % 6) < 3) { atomicMin(&bounds[k], v[k]); atomicMin(&bounds_global[k], v[k]); }
+                else { atomicMax(&bounds[k], v[k]); atomicMax(&bounds_global[k], v[k]); }
+            }
+    }
+};
+
+__global__ void k_tri_prims(const float *__restrict__ verts, const int32_t *__restrict__ idx,
+                            int64_t n, int64_t nv, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi,
+                            int *bad_index, int *bounds, int *bounds_global) {
+    BoundsAcc acc;
+    acc.init();
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i0 = idx[3 * t], i1 = idx[3 * t + 1], i2 = idx[3 * t + 2];
+        if (i0 < 0 || i0 >= nv || i1 < 0 || i1 >= nv || i2 < 0 || i2 >= nv) {  // validated here, on the GPU
+            atomicExch(bad_index, 1);
+            i0 = i1 = i2 = 0;
+        }
+        f3 v0 = mk(verts[3 * i0], verts[3 * i0 + 1], verts[3 * i0 + 2]);
+        f3 v1 = mk(verts[3 * i1], verts[3 * i1 + 1], verts[3 * i1 + 2]);
+        f3 v2 = mk(verts[3 * i2], verts[3 * i2 + 1], verts[3 * i2 + 2]);
+        f3 e1 = sub(v1, v0), e2 = sub(v2, v0);
+        int64_t g = local0 + t;
+        prims[3 * g + 0] = make_float4(v0.x, v0.y, v0.z, __uint_as_float((uint32_t)g));
+        prims[3 * g + 1] = make_float4(e1.x, e1.y, e1.z, 0.0f);
+        prims[3 * g + 2] = make_float4(e2.x, e2.y, e2.z, 0.0f);
+        f3 lo = mk(fminf(fminf(v0.x, v1.x), v2.x), fminf(fminf(v0.y, v1.y), v2.y), fminf(fminf(v0.z, v1.z), v2.z));
+        f3 hi = mk(fmaxf(fmaxf(v0.x, v1.x), v2.x), fmaxf(fmaxf(v0.y, v1.y), v2.y), fmaxf(fmaxf(v0.z, v1.z), v2.z));
+        blo[g] = make_float4(lo.x, lo.y, lo.z, 0.0f);
+        bhi[g] = make_float4(hi.x, hi.y, hi.z, 0.0f);
+        acc.add(lo, hi);
+    }
+    acc.flush(bounds, bounds_global);
+}
+
+__global__ void k_sphere_prims(const float4 *__restrict__ sph, int64_t n, uint32_t local0,
+                               float4 *prims, float4 *blo, float4 *bhi, int *bounds, int *bounds_global) {
+    BoundsAcc acc;
+    acc.init();
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        float4 s = sph[t];
+        int64_t g = local0 + t;
+        prims[3 * g + 0] = make_float4(s.x, s.y, s.z, __uint_as_float((uint32_t)g | SPHERE_BIT));
+        prims[3 * g + 1] = make_float4(s.w, 0.0f, 0.0f, 0.0f);
+        prims[3 * g + 2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        f3 lo = mk(s.x - s.w, s.y - s.w, s.z - s.w), hi = mk(s.x + s.w, s.y + s.w, s.z + s.w);
+        blo[g] = make_float4(lo.x, lo.y, lo.z, 0.0f);
+        bhi[g] = make_float4(hi.x, hi.y, hi.z, 0.0f);
+        acc.add(lo, hi);
+    }
+    acc.flush(bounds, bounds_global);
 }
 
 __device__ __forceinline__ uint64_t expand21(uint64_t v) {
@@ -340,6 +353,49 @@ __global__ void k_refit(int64_t n, const int *__restrict__ left, const int *__re
         __stcg(nhi + node, hi);
         if (node == 0) return;
         node = parent[node];
+    }
+}
+
+// Agglomerative single pass (Apetrei 2014, "Fast and Simple Agglomerative LBVH Construction"):
+// the same binary radix tree as k_karras + k_refit, built bottom-up in one kernel.  A node
+// covering sorted leaves [l, r] is the left child of internal node r if keys r, r+1 are closer
+// (longer common prefix, ties impossible with index-augmented keys) than keys l-1, l, else the
+// right child of internal node l-1; internal node p is the split between leaves p and p+1.
+// The first child to arrive at p deposits its outer range bound and leaves; the second
+// (acq_rel exchange) merges both boxes and continues.  The root is reported in *root_out.
+__global__ void k_agglo(const uint64_t *__restrict__ keys, int64_t n, const float4 *__restrict__ slo,
+                        const float4 *__restrict__ shi, int *left, int *right, int *size, float4 *nlo,
+                        float4 *nhi, int *other, int *root_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t l = i, r = i;
+    int cur = (int)(n - 1 + i);
+    float4 lo = slo[i], hi = shi[i];
+    for (;;) {
+        bool is_left;
+        if (l == 0) is_left = true;
+        else if (r == n - 1) is_left = false;
+        else is_left = delta(keys, n, r, r + 1) > delta(keys, n, l - 1, l);
+        const int64_t p = is_left ? r : l - 1;
+        if (is_left) left[p] = cur;
+        else right[p] = cur;
+        int prev;
+        const int val = is_left ? (int)l : (int)r;
+        asm volatile("atom.exch.acq_rel.gpu.b32 %0, [%1], %2;" : "=r"(prev) : "l"(other + p), "r"(val) : "memory");
+        if (prev < 0) return;  // first arrival: the sibling finishes the node
+        const int sib = is_left ? __ldcg(right + p) : __ldcg(left + p);
+        float4 a, b;
+        if (sib >= n - 1) { a = slo[sib - (n - 1)]; b = shi[sib - (n - 1)]; }
+        else { a = __ldcg(nlo + sib); b = __ldcg(nhi + sib); }
+        lo = make_float4(fminf(lo.x, a.x), fminf(lo.y, a.y), fminf(lo.z, a.z), 0.0f);
+        hi = make_float4(fmaxf(hi.x, b.x), fmaxf(hi.y, b.y), fmaxf(hi.z, b.z), 0.0f);
+        if (is_left) r = prev;
+        else l = prev;
+        __stcg(nlo + p, lo);
+        __stcg(nhi + p, hi);
+        size[p] = (int)(r - l + 1);
+        cur = (int)p;
+        if (l == 0 && r == n - 1) { *root_out = cur; return; }
     }
 }
 
@@ -610,19 +666,21 @@ __global__ void __launch_bounds__(MC_BLOCK) k_macrocells(const float *__restrict
 // Host-side launchers.
 // ---------------------------------------------------------------------------------------
 
-void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, int64_t nv, uint32_t local0,
-                      float4 *prims, float4 *blo, float4 *bhi, int *bad_index, cudaStream_t s) {
-    if (n > 0) k_tri_prims<<<nblk(n, 256), 256, 0, s>>>(verts, idx, n, nv, local0, prims, blo, bhi, bad_index);
-}
-void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims,
-                         float4 *blo, float4 *bhi, cudaStream_t s) {
-    if (n > 0) k_sphere_prims<<<nblk(n, 256), 256, 0, s>>>(sph, n, local0, prims, blo, bhi);
-}
-void launch_bounds(const float4 *blo, const float4 *bhi, int64_t n, int *bounds, int *bounds_global, int nsm,
-                   cudaStream_t s) {
+static unsigned prim_grid(int64_t n, int nsm) {
     unsigned g = (unsigned)std::min<int64_t>(nblk(n, 256), (int64_t)nsm * 8);
-    if (g == 0) g = 1;
-    k_bounds<<<g, 256, 0, s>>>(blo, bhi, n, bounds, bounds_global);
+    return g ? g : 1;
+}
+void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, int64_t nv, uint32_t local0,
+                      float4 *prims, float4 *blo, float4 *bhi, int *bad_index, int *bounds, int *bounds_global,
+                      int nsm, cudaStream_t s) {
+    if (n > 0)
+        k_tri_prims<<<prim_grid(n, nsm), 256, 0, s>>>(verts, idx, n, nv, local0, prims, blo, bhi, bad_index, bounds,
+                                                      bounds_global);
+}
+void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi,
+                         int *bounds, int *bounds_global, int nsm, cudaStream_t s) {
+    if (n > 0)
+        k_sphere_prims<<<prim_grid(n, nsm), 256, 0, s>>>(sph, n, local0, prims, blo, bhi, bounds, bounds_global);
 }
 void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
                    uint64_t *keys, uint32_t *vals, cudaStream_t s) {
@@ -652,6 +710,10 @@ void launch_refit(int64_t n, const int *left, const int *right, const int *paren
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
                   cudaStream_t s) {
     if (n > 1) k_refit<<<nblk(n, 256), 256, 0, s>>>(n, left, right, parent, slo, shi, nlo, nhi, arrive);
+}
+void launch_agglo(const uint64_t *keys, int64_t n, const float4 *slo, const float4 *shi, int *left, int *right,
+                  int *size, float4 *nlo, float4 *nhi, int *other, int *root_out, cudaStream_t s) {
+    if (n > 1) k_agglo<<<nblk(n, 256), 256, 0, s>>>(keys, n, slo, shi, left, right, size, nlo, nhi, other, root_out);
 }
 void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
                          const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,
