@@ -94,7 +94,7 @@ struct Dev {
     float box[6];
     bool nonempty = false;
     Buf b_prims_u, b_blo, b_bhi, b_keys[2], b_vals[2], b_tile, b_left, b_right, b_parent, b_rlo,
-        b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_bounds, b_hist, b_wnodes,
+        b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_bounds, b_hist, b_wnodes, b_chunks,
         b_prims_w, b_items[2], b_wcnt, b_wperm, b_witems[2], b_size;
     int builder = 1;  // 0 PLOC, 1 agglomerative LBVH (default), 2 Karras + refit (env DPR_BUILDER=ploc|karras)
     int build_iters = 0;
@@ -285,21 +285,31 @@ int build_world(Dev *d) {
     }
     int64_t off = 0;
     int launches = 0;
+    // all parts' prim records, boxes and bounds in one launch (one block per chunk)
+    std::vector<PrimChunk> chunks;
     for (int k = 0; k < np; ++k) {
         PartStore &p = d->parts[k];
-        if (p.kind == DPR_PART_TRIANGLES) {
-            launch_tri_prims(P<float>(p.verts), P<int32_t>(p.idx), p.nt, p.nv, (uint32_t)off,
-                             P<float4>(d->b_prims_u), P<float4>(d->b_blo), P<float4>(d->b_bhi),
-                             P<int>(d->b_bounds) + 12 * (np + 1), P<int>(d->b_bounds) + 12 * (k + 1),
-                             P<int>(d->b_bounds), d->nsm, s);
-        } else if (p.kind == DPR_PART_SPHERES) {
-            launch_sphere_prims(P<float4>(p.spheres), p.ns, (uint32_t)off, P<float4>(d->b_prims_u),
-                                P<float4>(d->b_blo), P<float4>(d->b_bhi), P<int>(d->b_bounds) + 12 * (k + 1),
-                                P<int>(d->b_bounds), d->nsm, s);
+        const int64_t cnt = p.nprims();
+        for (int64_t st = 0; st < cnt; st += PRIM_CHUNK) {
+            PrimChunk c;
+            c.src = p.kind == DPR_PART_TRIANGLES ? (const void *)P<float>(p.verts) : (const void *)P<float4>(p.spheres);
+            c.idx = p.kind == DPR_PART_TRIANGLES ? P<int32_t>(p.idx) : nullptr;
+            c.nv = p.nv;
+            c.start = st;
+            c.g0 = (uint32_t)(off + st);
+            c.count = (int)std::min<int64_t>(PRIM_CHUNK, cnt - st);
+            c.kind = p.kind;
+            c.slot = k + 1;
+            chunks.push_back(c);
         }
-        int64_t cnt = p.nprims();
-        if (cnt > 0) launches += 1;
         off += cnt;
+    }
+    if (!chunks.empty()) {
+        RET(ensure(d, d->b_chunks, sizeof(PrimChunk) * chunks.size()));
+        CK(cudaMemcpyAsync(d->b_chunks.p, chunks.data(), sizeof(PrimChunk) * chunks.size(), cudaMemcpyHostToDevice, s));
+        launch_part_prims(P<PrimChunk>(d->b_chunks), (int)chunks.size(), P<float4>(d->b_prims_u), P<float4>(d->b_blo),
+                          P<float4>(d->b_bhi), P<int>(d->b_bounds), P<int>(d->b_bounds) + 12 * (np + 1), s);
+        launches++;
     }
     // Morton keys + all digit histograms
     std::vector<unsigned long long> hist(8 * 256, 0);
@@ -1205,7 +1215,7 @@ void release_bufs(Dev *d) {
     Buf *bs[] = {&d->b_prims_u, &d->b_blo, &d->b_bhi, &d->b_keys[0], &d->b_keys[1], &d->b_vals[0],
                  &d->b_vals[1], &d->b_tile, &d->b_left, &d->b_right, &d->b_parent, &d->b_rlo, &d->b_rhi,
                  &d->b_nlo, &d->b_nhi, &d->b_arrive, &d->b_prims, &d->b_slo, &d->b_shi,
-                 &d->b_bounds, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_witems[0], &d->b_witems[1], &d->b_size, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
+                 &d->b_bounds, &d->b_chunks, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_witems[0], &d->b_witems[1], &d->b_size, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
                  &d->b_counts, &d->b_in_count, &d->b_fetch, &d->b_part_lo, &d->b_part_alb, &d->b_scratch,
                  &d->b_path[0], &d->b_path[1], &d->b_occlq[0], &d->b_occlq[1]};
     for (Buf *b : bs) dfree(d, *b);

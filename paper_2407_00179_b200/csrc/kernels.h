@@ -8,11 +8,18 @@
 namespace dpr {
 
 // ---- lbvh.cu ---------------------------------------------------------------------------
-void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, int64_t nv, uint32_t local0,
-                      float4 *prims, float4 *blo, float4 *bhi, int *bad_index, int *bounds, int *bounds_global,
-                      int nsm, cudaStream_t s);
-void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi,
-                         int *bounds, int *bounds_global, int nsm, cudaStream_t s);
+// one block of k_part_prims: prims [start, start+count) of one part (global ids g0...)
+struct PrimChunk {
+    const void *src;       // float verts[3*nv] (triangles) or float4 spheres[]
+    const int32_t *idx;    // triangles: int32 idx[3*nt]
+    int64_t nv;            // triangles: vertex count (index validation)
+    int64_t start;         // first prim of the chunk within its part
+    uint32_t g0;           // global (rank-local) id of that prim
+    int count, kind, slot; // prims in the chunk, DPR_PART_*, bounds slot (part k -> k+1)
+};
+constexpr int PRIM_CHUNK = 4096;
+void launch_part_prims(const PrimChunk *chunks, int nchunks, float4 *prims, float4 *blo, float4 *bhi, int *bounds,
+                       int *bad_index, cudaStream_t s);
 void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
                    uint64_t *keys, uint32_t *vals, cudaStream_t s);
 void launch_digit_hist_all(const uint64_t *keys, int64_t n, unsigned long long *hist, int nsm,

@@ -4,9 +4,9 @@
 // builds a local structure over its own parts.  B200 has no RT cores, so the
 // structure and its traversal are hand-written: a linear BVH (Karras 2012, "Maximizing
 // parallelism in the construction of BVHs, octrees and k-d trees"):
-//   1. k_tri_prims / k_sphere_prims: prim records + exact AABBs (min/max, no rounding), and
-//      in the same pass the part's / rank's box and centroid box (order-preserving integer
-//      atomics after a warp reduction)
+//   1. k_part_prims: prim records + exact AABBs (min/max, no rounding) of every part in one
+//      launch (one block per chunk), and in the same pass each part's and the rank's box and
+//      centroid box (order-preserving integer atomics after a block reduction)
 //   3. k_morton: 63-bit Morton code of the centroid (21 bits per axis)
 //   4. LSD radix sort of (key u64, index u32), 8-bit digits, stable per-tile ranking with
 //      warp match + shared-memory digit prefix; passes whose digit is constant are skipped
@@ -59,7 +59,10 @@ struct BoundsAcc {
             v[9 + c] = max(v[9 + c], f2ord(cen));
         }
     }
-    __device__ __forceinline__ void flush(int *bounds, int *bounds_global) {
+    // block-wide reduction (warp shuffles, then across warps in shared memory), then one
+    // atomic per bound word into the part's slot and the global slot
+    __device__ __forceinline__ void block_flush(int *bounds, int *bounds_global) {
+        __shared__ int sm[32][12];
         for (int k = 0; k < 12; ++k) {
             bool isMin = (k % 6) < 3;
             for (int o = 16; o > 0; o >>= 1) {
@@ -67,58 +70,61 @@ struct BoundsAcc {
                 v[k] = isMin ? min(v[k], w) : max(v[k], w);
             }
         }
+        const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
         if ((threadIdx.x & 31) == 0)
-            for (int k = 0; k < 12; ++k) {
-                if ((k % 6) < 3) { atomicMin(&bounds[k], v[k]); atomicMin(&bounds_global[k], v[k]); }
-                else { atomicMax(&bounds[k], v[k]); atomicMax(&bounds_global[k], v[k]); }
-            }
+            for (int k = 0; k < 12; ++k) sm[warp][k] = v[k];
+        __syncthreads();
+        if (threadIdx.x < 12) {
+            const int k = threadIdx.x;
+            const bool isMin = (k % 6) < 3;
+            int x = sm[0][k];
+            for (int w = 1; w < nw; ++w) x = isMin ? min(x, sm[w][k]) : max(x, sm[w][k]);
+            if (isMin) { atomicMin(&bounds[k], x); atomicMin(&bounds_global[k], x); }
+            else { atomicMax(&bounds[k], x); atomicMax(&bounds_global[k], x); }
+        }
     }
 };
 
-__global__ void k_tri_prims(const float *__restrict__ verts, const int32_t *__restrict__ idx,
-                            int64_t n, int64_t nv, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi,
-                            int *bad_index, int *bounds, int *bounds_global) {
+// One block per chunk of one part (all parts of the rank in a single launch): triangle
+// records (v0, e1, e2; triangle indices validated here, on the GPU) or sphere records, their
+// exact AABBs, and the part's box / centroid box.
+__global__ void __launch_bounds__(256) k_part_prims(const PrimChunk *__restrict__ chunks, float4 *prims,
+                                                    float4 *blo, float4 *bhi, int *bounds, int *bad_index) {
+    const PrimChunk c = chunks[blockIdx.x];
     BoundsAcc acc;
     acc.init();
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i0 = idx[3 * t], i1 = idx[3 * t + 1], i2 = idx[3 * t + 2];
-        if (i0 < 0 || i0 >= nv || i1 < 0 || i1 >= nv || i2 < 0 || i2 >= nv) {  // validated here, on the GPU
-            atomicExch(bad_index, 1);
-            i0 = i1 = i2 = 0;
+    for (int j = threadIdx.x; j < c.count; j += blockDim.x) {
+        const int64_t t = c.start + j, g = (int64_t)c.g0 + j;
+        f3 lo, hi;
+        if (c.kind == DPR_PART_TRIANGLES) {
+            const float *verts = (const float *)c.src;
+            int64_t i0 = c.idx[3 * t], i1 = c.idx[3 * t + 1], i2 = c.idx[3 * t + 2];
+            if (i0 < 0 || i0 >= c.nv || i1 < 0 || i1 >= c.nv || i2 < 0 || i2 >= c.nv) {
+                atomicExch(bad_index, 1);
+                i0 = i1 = i2 = 0;
+            }
+            f3 v0 = mk(verts[3 * i0], verts[3 * i0 + 1], verts[3 * i0 + 2]);
+            f3 v1 = mk(verts[3 * i1], verts[3 * i1 + 1], verts[3 * i1 + 2]);
+            f3 v2 = mk(verts[3 * i2], verts[3 * i2 + 1], verts[3 * i2 + 2]);
+            f3 e1 = sub(v1, v0), e2 = sub(v2, v0);
+            prims[3 * g + 0] = make_float4(v0.x, v0.y, v0.z, __uint_as_float((uint32_t)g));
+            prims[3 * g + 1] = make_float4(e1.x, e1.y, e1.z, 0.0f);
+            prims[3 * g + 2] = make_float4(e2.x, e2.y, e2.z, 0.0f);
+            lo = mk(fminf(fminf(v0.x, v1.x), v2.x), fminf(fminf(v0.y, v1.y), v2.y), fminf(fminf(v0.z, v1.z), v2.z));
+            hi = mk(fmaxf(fmaxf(v0.x, v1.x), v2.x), fmaxf(fmaxf(v0.y, v1.y), v2.y), fmaxf(fmaxf(v0.z, v1.z), v2.z));
+        } else {
+            const float4 s = ((const float4 *)c.src)[t];
+            prims[3 * g + 0] = make_float4(s.x, s.y, s.z, __uint_as_float((uint32_t)g | SPHERE_BIT));
+            prims[3 * g + 1] = make_float4(s.w, 0.0f, 0.0f, 0.0f);
+            prims[3 * g + 2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            lo = mk(s.x - s.w, s.y - s.w, s.z - s.w);
+            hi = mk(s.x + s.w, s.y + s.w, s.z + s.w);
         }
-        f3 v0 = mk(verts[3 * i0], verts[3 * i0 + 1], verts[3 * i0 + 2]);
-        f3 v1 = mk(verts[3 * i1], verts[3 * i1 + 1], verts[3 * i1 + 2]);
-        f3 v2 = mk(verts[3 * i2], verts[3 * i2 + 1], verts[3 * i2 + 2]);
-        f3 e1 = sub(v1, v0), e2 = sub(v2, v0);
-        int64_t g = local0 + t;
-        prims[3 * g + 0] = make_float4(v0.x, v0.y, v0.z, __uint_as_float((uint32_t)g));
-        prims[3 * g + 1] = make_float4(e1.x, e1.y, e1.z, 0.0f);
-        prims[3 * g + 2] = make_float4(e2.x, e2.y, e2.z, 0.0f);
-        f3 lo = mk(fminf(fminf(v0.x, v1.x), v2.x), fminf(fminf(v0.y, v1.y), v2.y), fminf(fminf(v0.z, v1.z), v2.z));
-        f3 hi = mk(fmaxf(fmaxf(v0.x, v1.x), v2.x), fmaxf(fmaxf(v0.y, v1.y), v2.y), fmaxf(fmaxf(v0.z, v1.z), v2.z));
         blo[g] = make_float4(lo.x, lo.y, lo.z, 0.0f);
         bhi[g] = make_float4(hi.x, hi.y, hi.z, 0.0f);
         acc.add(lo, hi);
     }
-    acc.flush(bounds, bounds_global);
-}
-
-__global__ void k_sphere_prims(const float4 *__restrict__ sph, int64_t n, uint32_t local0,
-                               float4 *prims, float4 *blo, float4 *bhi, int *bounds, int *bounds_global) {
-    BoundsAcc acc;
-    acc.init();
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        float4 s = sph[t];
-        int64_t g = local0 + t;
-        prims[3 * g + 0] = make_float4(s.x, s.y, s.z, __uint_as_float((uint32_t)g | SPHERE_BIT));
-        prims[3 * g + 1] = make_float4(s.w, 0.0f, 0.0f, 0.0f);
-        prims[3 * g + 2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        f3 lo = mk(s.x - s.w, s.y - s.w, s.z - s.w), hi = mk(s.x + s.w, s.y + s.w, s.z + s.w);
-        blo[g] = make_float4(lo.x, lo.y, lo.z, 0.0f);
-        bhi[g] = make_float4(hi.x, hi.y, hi.z, 0.0f);
-        acc.add(lo, hi);
-    }
-    acc.flush(bounds, bounds_global);
+    acc.block_flush(bounds + 12 * c.slot, bounds);
 }
 
 __device__ __forceinline__ uint64_t expand21(uint64_t v) {
@@ -666,21 +672,9 @@ __global__ void __launch_bounds__(MC_BLOCK) k_macrocells(const float *__restrict
 // Host-side launchers.
 // ---------------------------------------------------------------------------------------
 
-static unsigned prim_grid(int64_t n, int nsm) {
-    unsigned g = (unsigned)std::min<int64_t>(nblk(n, 256), (int64_t)nsm * 8);
-    return g ? g : 1;
-}
-void launch_tri_prims(const float *verts, const int32_t *idx, int64_t n, int64_t nv, uint32_t local0,
-                      float4 *prims, float4 *blo, float4 *bhi, int *bad_index, int *bounds, int *bounds_global,
-                      int nsm, cudaStream_t s) {
-    if (n > 0)
-        k_tri_prims<<<prim_grid(n, nsm), 256, 0, s>>>(verts, idx, n, nv, local0, prims, blo, bhi, bad_index, bounds,
-                                                      bounds_global);
-}
-void launch_sphere_prims(const float4 *sph, int64_t n, uint32_t local0, float4 *prims, float4 *blo, float4 *bhi,
-                         int *bounds, int *bounds_global, int nsm, cudaStream_t s) {
-    if (n > 0)
-        k_sphere_prims<<<prim_grid(n, nsm), 256, 0, s>>>(sph, n, local0, prims, blo, bhi, bounds, bounds_global);
+void launch_part_prims(const PrimChunk *chunks, int nchunks, float4 *prims, float4 *blo, float4 *bhi, int *bounds,
+                       int *bad_index, cudaStream_t s) {
+    if (nchunks > 0) k_part_prims<<<nchunks, 256, 0, s>>>(chunks, prims, blo, bhi, bounds, bad_index);
 }
 void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
                    uint64_t *keys, uint32_t *vals, cudaStream_t s) {
