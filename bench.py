@@ -171,13 +171,15 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    scene = di.config2(nranks=1)
+    scene = make_scene(args.config, 1)
+    if args.flags:
+        scene.frame = di.Frame(**{**scene.frame.__dict__, "flags": scene.frame.flags | args.flags})
     import oracle as orc
     parts = di.union_parts(scene.parts)
     osc = orc.OracleScene(parts, 1)
     P = scene.frame.W * scene.frame.H
     rng = np.random.default_rng(2)
-    npix = int(os.environ.get("DPR_REF_PIXELS", "8192"))
+    npix = min(P, int(os.environ.get("DPR_REF_PIXELS", {"c1": 4096, "c3": 2048}.get(args.config, 8192))))
     times, rays = [], []
     for i in range(args.warmup + args.steps):
         pix = np.sort(rng.choice(P, size=npix, replace=False))
@@ -193,10 +195,13 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * float(np.mean(times)), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "step": f"oracle on {npix} random pixels x 16 spp",
+            "config": {"workload": WORKLOADS[args.config],
+                       "step": f"oracle on {npix} random pixels x {scene.frame.spp} spp",
+                       "frame_flags": int(scene.frame.flags),
                        "est_ms_per_full_frame": 1000 * frame_rays_est / value},
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": os.cpu_count(),
-                             "kind": "oracle", "sample": f"{npix} random pixels x 16 spp per step"},
+                             "kind": "oracle",
+                             "sample": f"{npix} random pixels x {scene.frame.spp} spp per step"},
             "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -215,6 +220,8 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2407_00179_b200 import dpr
     scene = make_scene(args.config, 1 if args.mode == "replicated" else world)
+    if args.flags:
+        scene.frame = di.Frame(**{**scene.frame.__dict__, "flags": scene.frame.flags | args.flags})
     my_parts = [p for p in scene.parts if p.rank == rank or args.mode == "replicated"]
     if args.mode == "replicated":
         my_parts = [di.Part(**{**p.__dict__, "rank": rank}) for p in my_parts]
@@ -359,7 +366,7 @@ def run_gpu(args):
                        "triangles": scene.meta.get("ntris", sum(p.nprims() for p in scene.parts)), "parallelism": f"dp{world} (world partitioned, ray forwarding)",
                        "l2": "inputs larger than L2 (BVH+prims ~1.1 GB, ray queues ~5 GB per step)",
                        "step": "dpr_commit_world (LBVH rebuild) + dpr_render_frame",
-                       "mode": args.mode},
+                       "mode": args.mode, "frame_flags": int(scene.frame.flags)},
             "ms_per_frame": float(np.median(acc["ms_frame"])),
             "ms_build": float(np.median(acc["ms_build"])),
             "rays_per_frame": rays_per_frame,
@@ -392,6 +399,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dpr", choices=["dpr", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--flags", type=int, default=0,
+                    help="extra frame flags: 8 = ring schedule (R-RING), 16 = delta tracking (R-DELTA)")
     ap.add_argument("--mode", default="dp", choices=["dp", "replicated", "composite"],
                     help="dp = ray forwarding over a partitioned world (the method, default); "
                          "replicated = whole world on every rank, pixels split (Barney mode, "

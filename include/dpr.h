@@ -69,6 +69,11 @@ typedef enum { DPR_MEMORY_HOST = 0, DPR_MEMORY_DEVICE = 1 } dpr_memory;
                                       traced by every rank in ring order without culling or
                                       early-out, resolves at the last one; children go home.
                                       Same image, events and occlusion bits as the visit rule */
+#define DPR_FLAG_DELTA 16u          /* volumes by delta tracking with one global majorant instead
+                                      of the P10 per-sample march (NEXT f4; DESIGN.md readings
+                                      R-DELTA, R-LOG): extinction alpha(x)/dt, majorant amax/dt,
+                                      tentative points from the ray's entry into the global grid
+                                      domain, event id VOL_BIT | tentative index */
 #define DPR_FLAG_NO_BACKGROUND 4u  /* misses add no background (set internally for the local
                                       renders of the compositing contrast device) */
 

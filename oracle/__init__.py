@@ -99,6 +99,8 @@ def lib():
                                     ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _P]
         L.or_iso_dir.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                  ctypes.c_uint32, _P]
+        L.or_pln.restype = ctypes.c_float
+        L.or_pln.argtypes = [ctypes.c_float]
         L.or_tf_eval.argtypes = [_P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                  ctypes.c_float, _P]
         L.or_brick_sample.restype = ctypes.c_int
@@ -340,6 +342,11 @@ def iso_dir(seed, p, s, depth):
     out = (ctypes.c_float * 3)()
     lib().or_iso_dir(seed, p, s, depth, out)
     return np.array(out, np.float32)
+
+
+def pln(x: float) -> float:
+    """Reading R-LOG: the pinned binary32 natural log used by delta tracking."""
+    return float(lib().or_pln(float(x)))
 
 
 def tf_eval(tf: np.ndarray, lo, hi, dscale, s):

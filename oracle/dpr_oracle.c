@@ -68,6 +68,7 @@ typedef struct {
     float dt;
     uint64_t seed;
     int32_t flags; /* bit0: jitter fixed at 0.5; bit3: ring schedule (routing simulator);
+                      bit4: delta tracking instead of the P10 march (R-DELTA);
                       bit2: no background (local render of the
                       compositing contrast device) */
 } or_frame;
@@ -337,6 +338,8 @@ typedef struct {
     int *rank_nonempty;
     float ubox[6];         /* union brick domain box (unpadded) */
     int has_volume;
+    float amax;            /* delta tracking majorant: max TF alpha over all bricks */
+    float gdom[6];         /* global grid domain O .. O + (gdims-1) h */
 } OScene;
 
 static double centroid(const OPrim *p, int axis)
@@ -612,6 +615,72 @@ static int brick_march_any(const OBrick *b, v3 o, v3 d, float tmax, float dt, co
     return 0;
 }
 
+/* ------------------------------------------------------------------------------------ */
+/* Delta tracking (NEXT f4; readings R-DELTA and R-LOG).                        */
+/* ------------------------------------------------------------------------------------ */
+/* R-LOG: natural logarithm of x in (0, 1] in binary32, operation by operation (the
+ * fdlibm/Cephes logf reduction; no contraction):
+ *   x = m*2^e, m in [1,2) (from the bits); if m > sqrt2 (0x3fb504f3) then m = m*0.5, e = e+1;
+ *   f = m - 1; s = f/(2+f); z = s*s; w = z*z;
+ *   R = z*(Lg1 + w*Lg3) + w*(Lg2 + w*Lg4);  hfsq = (0.5*f)*f;
+ *   ln x = e*ln2_hi - ((hfsq - (s*(hfsq + R) + e*ln2_lo)) - f). */
+static float pln(float x)
+{
+    const float Lg1 = 0x1.555554p-1f, Lg2 = 0x1.999c26p-2f, Lg3 = 0x1.23d3dcp-2f, Lg4 = 0x1.f13c4cp-3f;
+    const float ln2_hi = 0x1.62e3p-1f, ln2_lo = 0x1.2fefa2p-17f;
+    uint32_t bits;
+    memcpy(&bits, &x, 4);
+    int e = (int)((bits >> 23) & 0xff) - 127;
+    uint32_t mb = (bits & 0x007fffffu) | 0x3f800000u;
+    float m;
+    memcpy(&m, &mb, 4);
+    if (mb > 0x3fb504f3u) { m = m * 0.5f; e = e + 1; }
+    float f = m - 1.0f;
+    float s = f / (2.0f + f);
+    float z = s * s, w = z * z;
+    float R = z * (Lg1 + w * Lg3) + w * (Lg2 + w * Lg4);
+    float hfsq = (0.5f * f) * f;
+    float fe = (float)e;
+    return fe * ln2_hi - ((hfsq - (s * (hfsq + R) + fe * ln2_lo)) - f);
+}
+
+/* R-DELTA (Woodcock tracking with one global majorant).  Extinction mu(x) = alpha(x)/dt
+ * (alpha = the TF opacity of P10, per dt of path); majorant mu_bar = amax/dt.  Tentative
+ * points: t = t_start (entry into the global grid domain, P8 slab, clamped at 0); for
+ * k = 0, 1, ...: (xi_k, zeta_k) = lanes 2(k&1), 2(k&1)+1 of Philox(p, s, depth<<8|purpose,
+ * subhi | k>>1); t += ((0 - ln(1 - xi_k)) * dt) / amax; stop when !(t < min(limit, t_exit));
+ * x = o + t d; the owner brick (half-open) decides: real collision iff zeta_k*amax < alpha(x).
+ * A collision is event VOL_BIT | k with the TF rgb.  Points are generated identically on
+ * every rank; a rank evaluates only the points its own bricks own (rank < 0: all bricks). */
+static int delta_track(const OScene *sc, int rank, v3 o, v3 d, float limit, float dt, const VolKey *k,
+                       OHit *best)
+{
+    if (!sc->has_volume || !(sc->amax > 0.0f)) return 0;
+    float t, t1;
+    if (!slab(sc->gdom, sc->gdom + 3, o, d, INFINITY, &t, &t1)) return 0;
+    float tend = fminf(t1, limit);
+    for (uint32_t kk = 0; kk < (1u << 25); ++kk) {
+        uint32_t x[4];
+        rng4(k->seed, k->p, k->s, k->depth, k->purpose, k->subhi | (kk >> 1), x);
+        float xi = u01(x[2 * (kk & 1)]), zeta = u01(x[2 * (kk & 1) + 1]);
+        float L = 0.0f - pln(1.0f - xi);
+        t = t + (L * dt) / sc->amax;
+        if (!(t < tend)) return 0;
+        v3 pt = sample_p(o, d, t);
+        for (int b = 0; b < sc->nbricks; ++b) {
+            if (rank >= 0 && sc->bricks[b].rank != rank) continue;
+            float rgba[4];
+            if (!brick_sample(&sc->bricks[b], pt, rgba)) continue;
+            if (zeta * sc->amax < rgba[3]) {
+                if (best) { best->t = t; best->id = 0x80000000u | kk; best->n = V3(rgba[0], rgba[1], rgba[2]); }
+                return 1;
+            }
+            break;  /* one owner per point */
+        }
+    }
+    return 0;
+}
+
 /* Union march: one march over the whole volume domain, the owner brick looked up per
  * sample (the merged world of P:357-363 as ONE grid). */
 static const OBrick *union_owner(const OScene *sc, v3 pt)
@@ -769,6 +838,20 @@ OR_EXPORT OScene *or_scene_build(const or_part *parts, int nparts, int nranks)
     sc->has_volume = sc->nbricks > 0;
     for (int c = 0; c < 3; ++c) { sc->ubox[c] = INFINITY; sc->ubox[3 + c] = -INFINITY; }
     for (int b = 0; b < sc->nbricks; ++b) fbox_grow(sc->ubox, sc->ubox + 3, sc->bricks[b].box_lo, sc->bricks[b].box_hi);
+    /* delta tracking (R-DELTA): majorant = max over bricks and TF entries of min(1, a*dscale);
+     * the tentative-point sequence starts where the ray enters the GLOBAL grid domain */
+    sc->amax = 0.0f;
+    for (int b = 0; b < sc->nbricks; ++b)
+        for (int j = 0; j < 256; ++j) {
+            float a = fminf(1.0f, sc->bricks[b].tf[4 * j + 3] * sc->bricks[b].dscale);
+            if (a > sc->amax) sc->amax = a;
+        }
+    if (sc->nbricks > 0)
+        for (int c = 0; c < 3; ++c) {
+            const OBrick *b0 = &sc->bricks[0];
+            sc->gdom[c] = b0->O[c];
+            sc->gdom[3 + c] = b0->O[c] + (float)(b0->gd[c] - 1) * b0->h[c];
+        }
     /* BVHs */
     int64_t *sel = (int64_t *)malloc((size_t)(gid > 0 ? gid : 1) * sizeof(int64_t));
     for (int64_t i = 0; i < gid; ++i) sel[i] = i;
@@ -950,9 +1033,14 @@ static void trace_path_at(const Job *J, int rank, const ORay *ray, const VolKey 
     const OScene *sc = J->sc;
     if (rank < 0) {
         bvh_closest(&sc->ubvh, sc->prims, ray->o, ray->d, ray->tmax, best);
-        union_march_path(sc, ray->o, ray->d, J->fr->dt, vk, best);
+        if (J->fr->flags & 16) delta_track(sc, -1, ray->o, ray->d, best->t, J->fr->dt, vk, best);
+        else union_march_path(sc, ray->o, ray->d, J->fr->dt, vk, best);
     } else {
         bvh_closest(&sc->rbvh[rank], sc->prims, ray->o, ray->d, ray->tmax, best);
+        if (J->fr->flags & 16) {
+            delta_track(sc, rank, ray->o, ray->d, best->t, J->fr->dt, vk, best);
+            return;
+        }
         for (int b = 0; b < sc->nbricks; ++b)
             if (sc->bricks[b].rank == rank) brick_march_path(&sc->bricks[b], ray->o, ray->d, J->fr->dt, vk, best);
     }
@@ -963,9 +1051,11 @@ static int trace_occl_at(const Job *J, int rank, const ORay *ray, const VolKey *
     const OScene *sc = J->sc;
     if (rank < 0) {
         if (bvh_any(&sc->ubvh, sc->prims, ray->o, ray->d, ray->tmax)) return 1;
+        if (J->fr->flags & 16) return delta_track(sc, -1, ray->o, ray->d, ray->tmax, J->fr->dt, vk, NULL);
         return union_march_any(sc, ray->o, ray->d, ray->tmax, J->fr->dt, vk);
     }
     if (bvh_any(&sc->rbvh[rank], sc->prims, ray->o, ray->d, ray->tmax)) return 1;
+    if (J->fr->flags & 16) return delta_track(sc, rank, ray->o, ray->d, ray->tmax, J->fr->dt, vk, NULL);
     for (int b = 0; b < sc->nbricks; ++b)
         if (sc->bricks[b].rank == rank && brick_march_any(&sc->bricks[b], ray->o, ray->d, ray->tmax, J->fr->dt, vk))
             return 1;
@@ -1294,6 +1384,8 @@ OR_EXPORT void or_iso_dir(uint64_t seed, uint32_t p, uint32_t s, uint32_t depth,
     v3 r = iso_dir(seed, p, s, depth);
     out[0] = r.x; out[1] = r.y; out[2] = r.z;
 }
+
+OR_EXPORT float or_pln(float x) { return pln(x); }
 
 OR_EXPORT void or_tf_eval(const float *tf, float lo, float hi, float dscale, float s, float rgba[4])
 {

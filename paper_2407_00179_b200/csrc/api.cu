@@ -46,6 +46,7 @@ struct PartStore {
     int gdims[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, mc_dims[3] = {0, 0, 0};
     float origin[3] = {0, 0, 0}, spacing[3] = {1, 1, 1};
     float tf_lo = 0, tf_hi = 1, dscale = 1;
+    float amax = 0;  // bricks: max over TF entries of min(1, a * dscale)
     int has_hint = 0;
     float hint[6] = {0, 0, 0, 0, 0, 0};
     int64_t nprims() const { return kind == DPR_PART_TRIANGLES ? nt : (kind == DPR_PART_SPHERES ? ns : 0); }
@@ -69,7 +70,7 @@ struct RankInfo {
     int32_t nonempty;
     uint32_t nprims;
     int32_t nparts;
-    int32_t pad;
+    float amax;  // max TF alpha over this rank's bricks (delta-tracking majorant, R-DELTA)
     PartInfo parts[MAXP];
 };
 
@@ -515,6 +516,7 @@ int build_world(Dev *d) {
 // ---------------------------------------------------------------------------------------
 struct FrameCtx {
     Routing R;
+    float amax = 0.0f;  // global delta-tracking majorant
     std::vector<uint32_t> id_base;
     std::vector<uint32_t> part_lo;
     std::vector<float4> part_alb;
@@ -535,6 +537,9 @@ int frame_setup(std::vector<Dev *> &L, FrameCtx &fc) {
         ri.nprims = (uint32_t)d->nprims;
         ri.nparts = (int)d->local_parts.size();
         for (int k = 0; k < ri.nparts; ++k) ri.parts[k] = d->local_parts[k];
+        ri.amax = 0.0f;
+        for (auto &p : d->parts)
+            if (p.kind == DPR_PART_BRICK && p.amax > ri.amax) ri.amax = p.amax;
         sends.push_back(&ri);
     }
     std::vector<std::vector<char>> out;
@@ -551,6 +556,7 @@ int frame_setup(std::vector<Dev *> &L, FrameCtx &fc) {
         fc.id_base[r] = (uint32_t)base;
         base += all[r].nprims;
         fc.R.nonempty[r] = all[r].nonempty;
+        if (all[r].amax > fc.amax) fc.amax = all[r].amax;
         for (int c = 0; c < 3; ++c) {  // P8 padding, f32 host arithmetic
             fc.R.box[r][c] = all[r].box[c] - 1e-4f;
             fc.R.box[r][3 + c] = all[r].box[3 + c] + 1e-4f;
@@ -643,9 +649,9 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     for (int c = 0; c < 3; ++c) {
         a.F.l[c] = f.light_dir[c]; a.F.E[c] = f.E[c]; a.F.A[c] = f.A[c]; a.F.B[c] = f.B[c];
         a.F.cE[c] = d->cam.E[c]; a.F.cL[c] = d->cam.L[c]; a.F.cU[c] = d->cam.U[c]; a.F.cV[c] = d->cam.V[c];
+    }
     a.F.lens_radius = d->cam.lens_radius;
     a.F.focus_dist = d->cam.focus_dist;
-    }
     a.R = fc.R;
     a.R.self = d->rank;
     a.W.wnodes = P<WNode>(d->b_wnodes);
@@ -654,8 +660,14 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.W.nprims = d->nprims;
     a.W.id_base = fc.id_base[d->rank];
     a.W.nbricks = 0;
+    a.W.amax = fc.amax;
     for (auto &p : d->parts) {
         if (p.kind != DPR_PART_BRICK || a.W.nbricks >= MAX_BRICKS) continue;
+        if (a.W.nbricks == 0)
+            for (int c = 0; c < 3; ++c) {  // global grid domain (all bricks share gdims/origin/spacing)
+                a.W.gdom[c] = p.origin[c];
+                a.W.gdom[3 + c] = p.origin[c] + (float)(p.gdims[c] - 1) * p.spacing[c];
+            }
         BrickDev &B = a.W.bricks[a.W.nbricks++];
         for (int c = 0; c < 3; ++c) {
             B.lo[c] = p.lo[c]; B.hi[c] = p.hi[c]; B.mc_dims[c] = p.mc_dims[c];
@@ -1593,6 +1605,10 @@ int dpr_commit_part(dpr_device dev, const dpr_part_desc *part) {
         size_t nvox = (size_t)(p.hi[0] - p.lo[0] + 1) * (p.hi[1] - p.lo[1] + 1) * (p.hi[2] - p.lo[2] + 1);
         RET(copy_in(d, p.vox, part->voxels, sizeof(float) * nvox, part->memory));
         RET(copy_in(d, p.tf, part->tf, sizeof(float) * 4 * 256, part->memory));
+        std::vector<float> tfh(4 * 256);
+        CK(cudaMemcpyAsync(tfh.data(), p.tf.p, sizeof(float) * 4 * 256, cudaMemcpyDeviceToHost, d->stream));
+        CK(cudaStreamSynchronize(d->stream));
+        for (int j = 0; j < 256; ++j) p.amax = std::max(p.amax, std::min(1.0f, tfh[4 * j + 3] * p.dscale));
     }
     d->parts.push_back(p);
     d->world_ready = false;

@@ -284,6 +284,8 @@ struct WorldDev {
     int64_t nprims;
     uint32_t id_base;       // global id of local prim 0 (P12)
     int nbricks;
+    float amax;     // delta tracking majorant (max TF alpha over ALL ranks' bricks; R-DELTA)
+    float gdom[6];  // global grid domain O .. O + (gdims-1) h (tentative points start there)
     BrickDev bricks[MAX_BRICKS];
 };
 

@@ -404,6 +404,82 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
 }
 
 // ---------------------------------------------------------------------------------------
+// Delta tracking (NEXT f4; readings R-DELTA, R-LOG), the alternative to the P10 march:
+// Woodcock tracking with one global majorant amax/dt.  Tentative points are generated from
+// the ray's entry into the GLOBAL grid domain, identically on every rank; a rank evaluates
+// only the points its own bricks own (half-open), so the first real collision over all
+// ranks equals the union's.
+// ---------------------------------------------------------------------------------------
+// R-LOG: binary32 natural log of x in (0, 1], the same operation sequence as the oracle.
+__device__ __forceinline__ float pln(float x) {
+    const float Lg1 = 0x1.555554p-1f, Lg2 = 0x1.999c26p-2f, Lg3 = 0x1.23d3dcp-2f, Lg4 = 0x1.f13c4cp-3f;
+    const float ln2_hi = 0x1.62e3p-1f, ln2_lo = 0x1.2fefa2p-17f;
+    const uint32_t bits = __float_as_uint(x);
+    int e = (int)((bits >> 23) & 0xffu) - 127;
+    const uint32_t mb = (bits & 0x007fffffu) | 0x3f800000u;
+    float m = __uint_as_float(mb);
+    if (mb > 0x3fb504f3u) { m = m * 0.5f; e = e + 1; }
+    const float f = m - 1.0f;
+    const float s = f / (2.0f + f);
+    const float z = s * s, w = z * z;
+    const float R = z * (Lg1 + w * Lg3) + w * (Lg2 + w * Lg4);
+    const float hfsq = (0.5f * f) * f;
+    const float fe = (float)e;
+    return fe * ln2_hi - ((hfsq - (s * (hfsq + R) + fe * ln2_lo)) - f);
+}
+
+template <bool ANY>
+__device__ __noinline__ bool delta_track(const WorldDev &W, f3 o, f3 d, float limit, float dt, uint64_t seed,
+                                         uint32_t p, uint32_t s, uint32_t depth, uint32_t purpose, uint32_t subhi,
+                                         float &t_out, uint32_t &k_out, f3 &rgb_out, uint32_t &nsamples) {
+    if (W.nbricks == 0 || !(W.amax > 0.0f)) return false;
+    float t, t1;
+    if (!slab(W.gdom, W.gdom + 3, o, d, __int_as_float(0x7f800000), t, t1)) return false;
+    const float tend = fminf(t1, limit);
+    uint4 rr = make_uint4(0, 0, 0, 0);
+    for (uint32_t k = 0; k < (1u << 25); ++k) {
+        if (!(k & 1)) rr = rng4(seed, p, s, depth, purpose, subhi | (k >> 1));
+        const float xi = u01((k & 1) ? rr.z : rr.x), zeta = u01((k & 1) ? rr.w : rr.y);
+        const float L = 0.0f - pln(1.0f - xi);
+        t = t + (L * dt) / W.amax;
+        if (!(t < tend)) return false;
+        const f3 pt = mk(o.x + t * d.x, o.y + t * d.y, o.z + t * d.z);
+        for (int b = 0; b < W.nbricks; ++b) {
+            const BrickDev &B = W.bricks[b];
+            const f3 g = mk((pt.x - B.O[0]) / B.h[0], (pt.y - B.O[1]) / B.h[1], (pt.z - B.O[2]) / B.h[2]);
+            if (!(g.x >= (float)B.lo[0] && g.x < (float)B.hi[0] && g.y >= (float)B.lo[1] && g.y < (float)B.hi[1] &&
+                  g.z >= (float)B.lo[2] && g.z < (float)B.hi[2]))
+                continue;
+            const float fx0 = floorf(g.x), fy0 = floorf(g.y), fz0 = floorf(g.z);
+            const int ix = (int)fx0 - B.lo[0], iy = (int)fy0 - B.lo[1], iz = (int)fz0 - B.lo[2];
+            // empty macrocell: alpha == 0 for every point in it, no collision (exact)
+            if (!__ldg(B.mc + ((iz / MC_SIZE) * B.mc_dims[1] + iy / MC_SIZE) * B.mc_dims[0] + ix / MC_SIZE)) break;
+            nsamples++;
+            const int nx = B.hi[0] - B.lo[0] + 1, ny = B.hi[1] - B.lo[1] + 1;
+            const float fx = g.x - fx0, fy = g.y - fy0, fz = g.z - fz0;
+            const float *v = B.vox + (int64_t)ix + (int64_t)nx * ((int64_t)iy + (int64_t)ny * iz);
+            const int64_t sy = nx, sz = (int64_t)nx * ny;
+            float v000 = __ldg(v), v100 = __ldg(v + 1), v010 = __ldg(v + sy), v110 = __ldg(v + sy + 1);
+            float v001 = __ldg(v + sz), v101 = __ldg(v + sz + 1), v011 = __ldg(v + sz + sy),
+                  v111 = __ldg(v + sz + sy + 1);
+            float c00 = lerpf(v000, v100, fx), c10 = lerpf(v010, v110, fx);
+            float c01 = lerpf(v001, v101, fx), c11 = lerpf(v011, v111, fx);
+            float c0 = lerpf(c00, c10, fy), c1 = lerpf(c01, c11, fy);
+            f3 rgb;
+            const float alpha = tf_alpha_rgb(B, lerpf(c0, c1, fz), ANY ? nullptr : &rgb);
+            if (zeta * W.amax < alpha) {
+                t_out = t;
+                k_out = k;
+                if (!ANY) rgb_out = rgb;
+                return true;
+            }
+            break;  // one owner per point
+        }
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------------------
 // a2: primary generation + visibility discard.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ StepArgs A, int s0,
@@ -551,7 +627,14 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
         if (ANY) {
             OcclRec *r = A.Q.occl_in + idx;
             bool occluded = S.h.prim >= 0;
-            if (!occluded && A.W.nbricks > 0) {
+            if (!occluded && A.W.nbricks > 0 && (F.flags & DPR_FLAG_DELTA)) {
+                const uint32_t p = __float_as_uint(r->b.w), meta = __float_as_uint(r->c.w);
+                const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
+                float ti; uint32_t ii; f3 rgb;
+                occluded = delta_track<true>(A.W, S.o, S.d, S.tmax, F.dt, F.seed, p, s, depth,
+                                             slot == 0 ? PUR_VOL_SHADOW : PUR_VOL_AO,
+                                             slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
+            } else if (!occluded && A.W.nbricks > 0) {
                 const uint32_t p = __float_as_uint(r->b.w), meta = __float_as_uint(r->c.w);
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
                 for (int b = 0; b < A.W.nbricks && !occluded; ++b) {
@@ -567,7 +650,15 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
             bool changed = S.h.prim >= 0;
             f3 nrm = mk(0, 0, 0);
             if (changed) nrm = prim_normal(A.W, S.h.prim, S.o, S.d, S.h.t);
-            if (A.W.nbricks > 0) {
+            if (A.W.nbricks > 0 && (F.flags & DPR_FLAG_DELTA)) {
+                const uint32_t p = __float_as_uint(r->c.w), meta = __float_as_uint(r->e.w);
+                const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
+                float ti; uint32_t kk; f3 rgb;
+                if (delta_track<false>(A.W, S.o, S.d, S.h.t, F.dt, F.seed, p, s, depth, PUR_VOL_PATH, 0u, ti, kk,
+                                       rgb, tc.vols)) {
+                    S.h.t = ti; S.h.id = VOL_BIT | kk; nrm = rgb; changed = true;
+                }
+            } else if (A.W.nbricks > 0) {
                 const uint32_t p = __float_as_uint(r->c.w), meta = __float_as_uint(r->e.w);
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
                 for (int b = 0; b < A.W.nbricks; ++b) {

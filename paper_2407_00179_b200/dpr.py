@@ -23,6 +23,7 @@ DPR_MAX_RANKS = 16
 DPR_FLAG_JITTER_CENTER = 1
 DPR_FLAG_DEBUG_DUMPS = 2
 DPR_FLAG_RING = 8
+DPR_FLAG_DELTA = 16
 ERRORS = {-1: "DPR_ERR_INVALID_ARG", -2: "DPR_ERR_STATE", -3: "DPR_ERR_CUDA", -4: "DPR_ERR_NCCL",
           -5: "DPR_ERR_CONSISTENCY", -6: "DPR_ERR_OOM", -7: "DPR_ERR_QUEUE_OVERFLOW"}
 

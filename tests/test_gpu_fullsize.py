@@ -58,6 +58,21 @@ def test_config3_full_size_sampled():
     assert_pixels_close(g[0][pix], o.rgba)
 
 
+def test_config3_delta_tracking_full_size_sampled():
+    """configs[2] (1024^3 volume) with delta tracking (DPR_FLAG_DELTA): whole frame on the
+    GPU, every event / occlusion bit of 2000 sampled pixels against the oracle."""
+    sc = di.config3(nranks=1)
+    fr = di.Frame(**{**sc.frame.__dict__, "flags": sc.frame.flags | 16})
+    g = gpu_render(sc.parts, 1, sc.camera, fr)
+    P = fr.W * fr.H
+    pix = np.unique(np.random.default_rng(5).choice(P, 2000, replace=False))
+    o = oracle_render(sc.parts, 1, sc.camera, fr, pixels=pix, dp=False)
+    assert ((o.events & 0x80000000) != 0).sum() > 50
+    assert np.array_equal(g[1][:, :, pix], o.events)
+    assert np.array_equal(g[2][:, :, pix], o.occl)
+    assert_pixels_close(g[0][pix], o.rgba)
+
+
 @pytest.mark.parametrize("mode", ["sendrecv", "fused"])
 def test_nccl_collectives_single_rank(mode, monkeypatch):
     """DPR_FORCE_NCCL=1: frame-setup allgather, counts allgather / fused step allgather,

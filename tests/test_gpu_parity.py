@@ -254,3 +254,35 @@ def test_ring_schedule_volume_and_config2():
     sc = di.config2(nranks=4, G=41, W=64, H=48, spp=2, spp_batch=2)
     fr = di.Frame(**{**sc.frame.__dict__, "flags": 8})
     assert_parity(gpu_render(sc.parts, 4, sc.camera, fr), oracle_render(sc.parts, 4, sc.camera, fr))
+
+
+@pytest.mark.parametrize("nbricks,nranks", [(1, 1), (4, 2), (8, 4), (8, 8)])
+def test_delta_tracking(nbricks, nranks):
+    """NEXT f4: delta tracking (DPR_FLAG_DELTA; readings R-DELTA, R-LOG): tentative points
+    from the global grid domain entry, pinned log, one global majorant allgathered across
+    ranks; events (VOL_BIT | tentative index), occlusion bits, routing bit-exact."""
+    parts, h = _volume_scene(41, nbricks, nranks, alpha_max=0.3)
+    W = H = 40
+    cam = di.camera_basis((0.3, 1.5, -3.0), (0, -0.2, 0), (0, 1, 0), 50.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=3, spp_batch=2, max_depth=2, ao_k=1, ao_radius=0.3, dt=h,
+                  light_dir=di.f32(di.normalize((0.2, 1, 0.1))), E=(1, 1, 1), A=(0.2, 0.2, 0.2), flags=16)
+    g = gpu_render(parts, nranks, cam, fr)
+    o = oracle_render(parts, nranks, cam, fr)
+    assert ((o.events & 0x80000000) != 0).sum() > 100
+    assert_parity(g, o)
+
+
+def test_delta_tracking_mixed_and_ring():
+    """Delta tracking with surfaces in front of / inside the volume, and combined with the
+    ring schedule."""
+    parts, h = _volume_scene(33, 4, 2, alpha_max=0.3)
+    parts.append(di.Part(1, di.SPHERES, albedo=(0.9, 0.1, 0.1), spheres=di.f32([[0.2, 0.1, 0.0, 0.4]])))
+    v, i = di.quad_tris([(-3, -1.2, -3), (3, -1.2, -3), (3, -1.2, 3), (-3, -1.2, 3)])
+    parts.append(di.Part(0, di.TRIS, albedo=(0.5, 0.5, 0.5), verts=v, idx=i))
+    W = H = 32
+    cam = di.camera_basis((0.3, 1.5, -3.0), (0, -0.5, 0), (0, 1, 0), 50.0, W, H)
+    for flags in (16, 16 | 8):
+        fr = di.Frame(W=W, H=H, spp=2, spp_batch=1, max_depth=3, ao_k=1, ao_radius=0.3, dt=h,
+                      light_dir=di.f32(di.normalize((0.2, 1, 0.1))), E=(1, 1, 1), A=(0.2, 0.2, 0.2),
+                      flags=flags)
+        assert_parity(gpu_render(parts, 2, cam, fr), oracle_render(parts, 2, cam, fr))
