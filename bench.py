@@ -328,18 +328,27 @@ def run_gpu(args):
     fb_host = torch.empty((scene.frame.H, scene.frame.W, 4), dtype=torch.float32).pin_memory()
     d2h = fb_host.numel() * 4 if rank == 0 else 0
 
-    def e2e_step():
+    def commit_inputs():
         dev.clear_parts()
         for q in pinned:
-            dev.commit_part(q)
-        dev.commit_world()
+            dev.commit_part(q, async_copy=True)
+
+    def e2e_step():
+        # software pipeline, one step = upload + build + render + readback: the NEXT step's
+        # mesh upload (pinned host -> device on the library's copy stream) is issued first and
+        # overlaps this step's render (the built world no longer needs the parts); the frame
+        # is read back to pinned host memory; commit_world then waits for the upload and
+        # rebuilds the LBVH for the next step
+        commit_inputs()
         render()
         img = dev.map_frame()
         if img is not None:
             fb_host.copy_(img, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        dev.commit_world()
 
     if not args.no_e2e:
+        commit_inputs()
+        dev.commit_world()
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()
         barrier()

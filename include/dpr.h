@@ -58,7 +58,12 @@ typedef enum {
 } dpr_status;
 
 typedef enum { DPR_PART_TRIANGLES = 0, DPR_PART_SPHERES = 1, DPR_PART_BRICK = 2 } dpr_part_kind;
-typedef enum { DPR_MEMORY_HOST = 0, DPR_MEMORY_DEVICE = 1 } dpr_memory;
+/* HOST: copied before dpr_commit_part returns.  DEVICE: device-to-device copy, stream-ordered.
+ * HOST_ASYNC: (pinned) host memory read by the copy engine on a side stream, overlapping
+ * whatever the device is still rendering; the array must stay valid and unchanged until the
+ * next dpr_commit_world returns (which waits for the copies).  Triangle / sphere arrays only;
+ * bricks are copied as HOST. */
+typedef enum { DPR_MEMORY_HOST = 0, DPR_MEMORY_DEVICE = 1, DPR_MEMORY_HOST_ASYNC = 2 } dpr_memory;
 
 /* frame flags */
 #define DPR_FLAG_JITTER_CENTER 1u  /* camera jitter fixed at 0.5 (test mode) */
@@ -87,7 +92,8 @@ typedef struct {
 } dpr_allocator;
 
 /* One rank-local world part.  Arrays are COPIED at commit (ANARI commit
- * semantics): the caller may free them when dpr_commit_part returns.
+ * semantics): the caller may free them when dpr_commit_part returns (except
+ * DPR_MEMORY_HOST_ASYNC, see dpr_memory).
  *   TRIANGLES: verts float[n_verts][3], idx int32[n_tris][3] (indices into verts).
  *   SPHERES:   spheres float[n_spheres][4] = centre xyz, radius (> 0).
  *   BRICK:     a brick of one global structured grid: gdims (points per axis), origin,
@@ -199,10 +205,13 @@ DPR_API int dpr_release_device(dpr_device dev);
 /* ---- world (local content) ------------------------------------------------- */
 
 /* LOCAL: copy one part (see dpr_part_desc).  Parts are numbered in commit order; global
- * primitive ids are base_rank + local index. */
+ * primitive ids are base_rank + local index.  Parts describe the NEXT world:
+ * the world of the last dpr_commit_world stays renderable while parts are cleared and
+ * committed (so uploads of frame k+1 can overlap the render of frame k). */
 DPR_API int dpr_commit_part(dpr_device dev, const dpr_part_desc *part);
 
-/* LOCAL: drop all committed parts (the next commit_world builds an empty world). */
+/* LOCAL: drop all committed parts (the next commit_world builds an empty world; the current
+ * world, including its bricks, remains renderable until then). */
 DPR_API int dpr_clear_parts(dpr_device dev);
 
 /* LOCAL: (re)build the rank's acceleration structures from the committed parts, on the

@@ -84,6 +84,16 @@ struct StatsMsg {
 struct Dev {
     int rank = 0, nranks = 1, cuda_dev = 0, nsm = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t cstream = nullptr;          // side copy stream for geometry uploads
+    cudaEvent_t copy_ev = nullptr, order_ev = nullptr;
+    bool copy_pending = false;
+    std::vector<Buf> part_pool;              // recycled geometry buffers
+    // the committed world's volume state (renders use it while the parts of the next world
+    // are being committed): bricks, their majorant, and brick buffers of cleared parts that
+    // the committed world still references (freed by the next build)
+    std::vector<BrickDev> wbricks;
+    float amax_local = 0.0f;
+    std::vector<Buf> retired;
     ncclComm_t comm = nullptr;
     LoopGroup *group = nullptr;
     dpr_allocator alloc{};
@@ -268,6 +278,10 @@ int allgather_host(std::vector<Dev *> &L, const std::vector<const void *> &send,
 // ---------------------------------------------------------------------------------------
 int build_world(Dev *d) {
     cudaStream_t s = d->stream;
+    if (d->copy_pending) {  // geometry copied on the side stream (DPR_MEMORY_HOST_ASYNC)
+        CK(cudaStreamWaitEvent(s, d->copy_ev, 0));
+        d->copy_pending = false;
+    }
     int64_t n = 0;
     for (auto &p : d->parts) n += p.nprims();
     if (n >= (int64_t)0x0fffffff) return fail(DPR_ERR_INVALID_ARG, "too many primitives on one rank (max 2^28-2)");
@@ -506,6 +520,26 @@ int build_world(Dev *d) {
         launches++;
     }
     CK(cudaGetLastError());
+    // snapshot of the volume state of this world
+    d->wbricks.clear();
+    d->amax_local = 0.0f;
+    for (auto &p : d->parts) {
+        if (p.kind != DPR_PART_BRICK || (int)d->wbricks.size() >= MAX_BRICKS) continue;
+        BrickDev B;
+        for (int c = 0; c < 3; ++c) {
+            B.lo[c] = p.lo[c]; B.hi[c] = p.hi[c]; B.mc_dims[c] = p.mc_dims[c];
+            B.O[c] = p.origin[c]; B.h[c] = p.spacing[c];
+            B.box_lo[c] = p.origin[c] + (float)p.lo[c] * p.spacing[c];
+            B.box_hi[c] = p.origin[c] + (float)p.hi[c] * p.spacing[c];
+            B.gd[c] = p.gdims[c];
+        }
+        B.vox = P<float>(p.vox); B.mc = P<uint8_t>(p.mc); B.tf = P<float4>(p.tf);
+        B.tf_lo = p.tf_lo; B.tf_hi = p.tf_hi; B.dscale = p.dscale;
+        d->wbricks.push_back(B);
+        d->amax_local = std::max(d->amax_local, p.amax);
+    }
+    for (auto &b : d->retired) dfree(d, b);  // stream-ordered after the renders that used them
+    d->retired.clear();
     d->build_launches = launches;
     d->world_ready = true;
     return DPR_OK;
@@ -537,9 +571,7 @@ int frame_setup(std::vector<Dev *> &L, FrameCtx &fc) {
         ri.nprims = (uint32_t)d->nprims;
         ri.nparts = (int)d->local_parts.size();
         for (int k = 0; k < ri.nparts; ++k) ri.parts[k] = d->local_parts[k];
-        ri.amax = 0.0f;
-        for (auto &p : d->parts)
-            if (p.kind == DPR_PART_BRICK && p.amax > ri.amax) ri.amax = p.amax;
+        ri.amax = d->amax_local;
         sends.push_back(&ri);
     }
     std::vector<std::vector<char>> out;
@@ -661,22 +693,13 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.W.id_base = fc.id_base[d->rank];
     a.W.nbricks = 0;
     a.W.amax = fc.amax;
-    for (auto &p : d->parts) {
-        if (p.kind != DPR_PART_BRICK || a.W.nbricks >= MAX_BRICKS) continue;
+    for (const BrickDev &B : d->wbricks) {
         if (a.W.nbricks == 0)
             for (int c = 0; c < 3; ++c) {  // global grid domain (all bricks share gdims/origin/spacing)
-                a.W.gdom[c] = p.origin[c];
-                a.W.gdom[3 + c] = p.origin[c] + (float)(p.gdims[c] - 1) * p.spacing[c];
+                a.W.gdom[c] = B.O[c];
+                a.W.gdom[3 + c] = B.O[c] + (float)(B.gd[c] - 1) * B.h[c];
             }
-        BrickDev &B = a.W.bricks[a.W.nbricks++];
-        for (int c = 0; c < 3; ++c) {
-            B.lo[c] = p.lo[c]; B.hi[c] = p.hi[c]; B.mc_dims[c] = p.mc_dims[c];
-            B.O[c] = p.origin[c]; B.h[c] = p.spacing[c];
-            B.box_lo[c] = p.origin[c] + (float)p.lo[c] * p.spacing[c];
-            B.box_hi[c] = p.origin[c] + (float)p.hi[c] * p.spacing[c];
-        }
-        B.vox = P<float>(p.vox); B.mc = P<uint8_t>(p.mc); B.tf = P<float4>(p.tf);
-        B.tf_lo = p.tf_lo; B.tf_hi = p.tf_hi; B.dscale = p.dscale;
+        a.W.bricks[a.W.nbricks++] = B;
     }
     a.T.n = (int)fc.part_lo.size();
     a.T.id_lo = P<uint32_t>(d->b_part_lo);
@@ -1171,7 +1194,8 @@ int render_group(std::vector<Dev *> &L) {
 
 int check_part(const dpr_part_desc *p) {
     if (!p) return fail(DPR_ERR_INVALID_ARG, "null part");
-    if (p->memory != DPR_MEMORY_HOST && p->memory != DPR_MEMORY_DEVICE) return fail(DPR_ERR_INVALID_ARG, "bad memory kind");
+    if (p->memory != DPR_MEMORY_HOST && p->memory != DPR_MEMORY_DEVICE && p->memory != DPR_MEMORY_HOST_ASYNC)
+        return fail(DPR_ERR_INVALID_ARG, "bad memory kind");
     switch (p->kind) {
     case DPR_PART_TRIANGLES:
         if (p->n_tris < 0 || p->n_verts < 0 || (p->n_tris > 0 && (!p->verts || !p->idx)))
@@ -1193,10 +1217,46 @@ int check_part(const dpr_part_desc *p) {
     return DPR_OK;
 }
 
+// Bricks (read by the render kernels) and device sources: stream-ordered on the library
+// stream; host sources are complete when this returns.
 int copy_in(Dev *d, Buf &b, const void *src, size_t bytes, int memory) {
     RET(ensure(d, b, bytes));
-    if (bytes)
-        CK(cudaMemcpyAsync(b.p, src, bytes, memory == DPR_MEMORY_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, d->stream));
+    if (!bytes) return DPR_OK;
+    CK(cudaMemcpyAsync(b.p, src, bytes, memory == DPR_MEMORY_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       d->stream));
+    if (memory != DPR_MEMORY_DEVICE) CK(cudaStreamSynchronize(d->stream));
+    return DPR_OK;
+}
+
+// Triangle / sphere arrays (read only by the build): a recycled buffer (its last reader, a
+// build, has completed: dpr_commit_world waits for it) or a new one; host sources are copied
+// on the side copy stream, which overlaps a render still running on the library stream.
+int copy_in_geom(Dev *d, Buf &b, const void *src, size_t bytes, int memory) {
+    if (!bytes) return DPR_OK;
+    int best = -1;
+    for (size_t i = 0; i < d->part_pool.size(); ++i)
+        if (d->part_pool[i].bytes >= bytes && (best < 0 || d->part_pool[i].bytes < d->part_pool[best].bytes))
+            best = (int)i;
+    bool fresh = best < 0;
+    if (!fresh) {
+        b = d->part_pool[best];
+        d->part_pool.erase(d->part_pool.begin() + best);
+    } else {
+        RET(ensure(d, b, bytes));
+    }
+    if (memory == DPR_MEMORY_DEVICE) {
+        if (d->copy_pending) CK(cudaStreamWaitEvent(d->stream, d->copy_ev, 0));  // recycled buffer
+        CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyDeviceToDevice, d->stream));
+        return DPR_OK;
+    }
+    if (fresh) {  // a new allocation is stream-ordered on the library stream: order after it
+        CK(cudaEventRecord(d->order_ev, d->stream));
+        CK(cudaStreamWaitEvent(d->cstream, d->order_ev, 0));
+    }
+    CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, d->cstream));
+    CK(cudaEventRecord(d->copy_ev, d->cstream));
+    d->copy_pending = true;
+    if (memory == DPR_MEMORY_HOST) CK(cudaEventSynchronize(d->copy_ev));
     return DPR_OK;
 }
 
@@ -1208,6 +1268,9 @@ int init_dev(Dev *d, int rank, int nranks, int cuda_device, void *stream, const 
     if (alloc && alloc->alloc && alloc->free) { d->alloc = *alloc; d->has_alloc = true; }
     CK(cudaSetDevice(cuda_device));
     CK(cudaDeviceGetAttribute(&d->nsm, cudaDevAttrMultiProcessorCount, cuda_device));
+    CK(cudaStreamCreateWithFlags(&d->cstream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&d->copy_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&d->order_ev, cudaEventDisableTiming));
     for (int c = 0; c < 3; ++c) { d->box[c] = INFINITY; d->box[3 + c] = -INFINITY; }
     if (const char *e = getenv("DPR_SPW")) d->spw = std::max(1, atoi(e));
     if (const char *e = getenv("DPR_BUILDER"))
@@ -1224,6 +1287,8 @@ void release_bufs(Dev *d) {
     for (Buf *b : cb) dfree(d, *b);
     for (auto &p : d->parts) { dfree(d, p.verts); dfree(d, p.idx); dfree(d, p.spheres); dfree(d, p.vox); dfree(d, p.tf); dfree(d, p.mc); }
     d->parts.clear();
+    for (auto &b : d->retired) dfree(d, b);
+    d->retired.clear();
     Buf *bs[] = {&d->b_prims_u, &d->b_blo, &d->b_bhi, &d->b_keys[0], &d->b_keys[1], &d->b_vals[0],
                  &d->b_vals[1], &d->b_tile, &d->b_left, &d->b_right, &d->b_parent, &d->b_rlo, &d->b_rhi,
                  &d->b_nlo, &d->b_nhi, &d->b_arrive, &d->b_prims, &d->b_slo, &d->b_shi,
@@ -1256,6 +1321,7 @@ Dev *local_view(Dev *d, bool replicated = false) {
     }
     Dev *v = d->lv;
     v->parts = d->parts;  // non-owning copies (detached before release)
+    v->wbricks = d->wbricks; v->amax_local = d->amax_local;
     v->world_ready = d->world_ready; v->nprims = d->nprims; memcpy(v->box, d->box, sizeof(v->box));
     v->nonempty = d->nonempty; v->b_wnodes = d->b_wnodes; v->b_prims_w = d->b_prims_w;
     v->local_parts = d->local_parts; v->wnodes_count = d->wnodes_count; v->bvh_levels = d->bvh_levels;
@@ -1556,8 +1622,14 @@ int dpr_release_device(dpr_device dev) {
     Dev *d = &dev->d;
     cudaSetDevice(d->cuda_dev);
     cudaStreamSynchronize(d->stream);
+    if (d->cstream) cudaStreamSynchronize(d->cstream);
+    for (auto &b : d->part_pool) dfree(d, b);
+    d->part_pool.clear();
     release_bufs(d);
     cudaStreamSynchronize(d->stream);
+    if (d->cstream) cudaStreamDestroy(d->cstream);
+    if (d->copy_ev) cudaEventDestroy(d->copy_ev);
+    if (d->order_ev) cudaEventDestroy(d->order_ev);
     if (d->comm) ncclCommDestroy(d->comm);
     if (d->group) {
         auto &v = d->group->devs;
@@ -1583,11 +1655,11 @@ int dpr_commit_part(dpr_device dev, const dpr_part_desc *part) {
     if (p.kind == DPR_PART_TRIANGLES) {
         p.nv = part->n_verts;
         p.nt = part->n_tris;
-        RET(copy_in(d, p.verts, part->verts, sizeof(float) * 3 * p.nv, part->memory));
-        RET(copy_in(d, p.idx, part->idx, sizeof(int32_t) * 3 * p.nt, part->memory));
+        RET(copy_in_geom(d, p.verts, part->verts, sizeof(float) * 3 * p.nv, part->memory));
+        RET(copy_in_geom(d, p.idx, part->idx, sizeof(int32_t) * 3 * p.nt, part->memory));
     } else if (p.kind == DPR_PART_SPHERES) {
         p.ns = part->n_spheres;
-        RET(copy_in(d, p.spheres, part->spheres, sizeof(float) * 4 * p.ns, part->memory));
+        RET(copy_in_geom(d, p.spheres, part->spheres, sizeof(float) * 4 * p.ns, part->memory));
     } else {
         for (int c = 0; c < 3; ++c) {
             p.gdims[c] = part->gdims[c]; p.lo[c] = part->cell_lo[c]; p.hi[c] = part->cell_hi[c];
@@ -1611,16 +1683,25 @@ int dpr_commit_part(dpr_device dev, const dpr_part_desc *part) {
         for (int j = 0; j < 256; ++j) p.amax = std::max(p.amax, std::min(1.0f, tfh[4 * j + 3] * p.dscale));
     }
     d->parts.push_back(p);
-    d->world_ready = false;
     return DPR_OK;
 }
 
 int dpr_clear_parts(dpr_device dev) {
     if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
     Dev *d = &dev->d;
-    for (auto &p : d->parts) { dfree(d, p.verts); dfree(d, p.idx); dfree(d, p.spheres); dfree(d, p.vox); dfree(d, p.tf); dfree(d, p.mc); }
+    for (auto &p : d->parts) {
+        // geometry arrays are recycled for the next commit (bounded pool); bricks are freed
+        // stream-ordered (a render may still read them)
+        for (Buf *b : {&p.verts, &p.idx, &p.spheres})
+            if (b->p) {
+                if (d->part_pool.size() < 64) { d->part_pool.push_back(*b); *b = Buf(); }
+                else dfree(d, *b);
+            }
+        // bricks: the committed world still renders from them until the next build
+        for (Buf *b : {&p.vox, &p.tf, &p.mc})
+            if (b->p) { d->retired.push_back(*b); *b = Buf(); }
+    }
     d->parts.clear();
-    d->world_ready = false;
     return DPR_OK;
 }
 

@@ -249,6 +249,7 @@ constexpr int LEAF_MAX = DPR_LEAF_MAX;  // <= 4 (2-bit count in the wide-node me
 //   tri:    (v0.xyz, id) (e1.xyz, 0) (e2.xyz, 0)     id = local index
 //   sphere: (c.xyz, id|SPHERE_BIT) (r, 0, 0, 0) (unused)
 struct BrickDev {
+    int gd[3];              // global grid points per axis
     int lo[3], hi[3];       // cell_lo, cell_hi (stored voxels [lo, hi] inclusive)
     int mc_dims[3];         // macrocell grid dims (16^3 cells each)
     float O[3], h[3];       // global origin / spacing

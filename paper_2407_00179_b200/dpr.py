@@ -205,12 +205,13 @@ class TorchAllocator:
         self.struct = dpr_allocator(self._a, self._f, None)
 
 
-def part_desc(p, keep: list, device_arrays: bool = False) -> dpr_part_desc:
-    """dpr_inputs.Part (numpy, host) or a dict of torch CUDA tensors -> dpr_part_desc."""
+def part_desc(p, keep: list, device_arrays: bool = False, async_copy: bool = False) -> dpr_part_desc:
+    """dpr_inputs.Part (numpy, host) or a dict of torch CUDA tensors -> dpr_part_desc.
+    async_copy: DPR_MEMORY_HOST_ASYNC (pinned host arrays, read until dpr_commit_world)."""
     import dpr_inputs as di
     s = dpr_part_desc()
     s.kind = p.kind
-    s.memory = 1 if device_arrays else 0
+    s.memory = 1 if device_arrays else (2 if async_copy and p.kind != di.BRICK else 0)
     s.albedo = (_c.c_float * 3)(*[float(x) for x in p.albedo])
 
     def ptr(a, dtype):
@@ -299,9 +300,12 @@ class Device:
             self.h = None
 
     # -- world ------------------------------------------------------------------------
-    def commit_part(self, part, device_arrays: bool = False):
+    def commit_part(self, part, device_arrays: bool = False, async_copy: bool = False):
+        """async_copy=True: DPR_MEMORY_HOST_ASYNC -- the (pinned) host arrays are uploaded on
+        a side stream overlapping a render in flight; keep them unchanged until
+        commit_world returns."""
         keep: list = []
-        desc = part_desc(part, keep, device_arrays)
+        desc = part_desc(part, keep, device_arrays, async_copy)
         _check(load().dpr_commit_part(self.h, _c.byref(desc)), self.h)
 
     def clear_parts(self):

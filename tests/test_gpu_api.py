@@ -91,3 +91,97 @@ def test_device_memory_parts_and_rebuild():
             dev.release()
     for im in imgs[1:]:
         assert np.allclose(im, imgs[0], atol=1e-6)
+
+
+def test_async_host_commit_and_buffer_recycling():
+    """DPR_MEMORY_HOST_ASYNC: pinned host geometry uploaded on the side copy stream while the
+    previous frame is still rendering, recycled geometry buffers across clear/commit cycles
+    (different sizes, then the same), then a synchronous commit into recycled buffers: every
+    frame equals the synchronous-commit render of the same world, bit for bit."""
+    import torch
+    dpr = _dpr()
+    scA = di.config2(nranks=1, G=41, W=48, H=40, spp=2, spp_batch=2)
+    scB = di.config2(nranks=1, G=33, W=48, H=40, spp=2, spp_batch=2)
+
+    def pinned(parts):
+        out = []
+        for p in parts:
+            q = di.Part(**p.__dict__)
+            if p.kind == di.TRIS:
+                q.verts = torch.from_numpy(np.ascontiguousarray(p.verts)).pin_memory().numpy()
+                q.idx = torch.from_numpy(np.ascontiguousarray(p.idx)).pin_memory().numpy()
+            out.append(q)
+        return out
+
+    fr = di.Frame(**{**scA.frame.__dict__, "flags": scA.frame.flags | dpr.DPR_FLAG_DEBUG_DUMPS})
+
+    def render(dev, parts, mode):
+        dev.clear_parts()
+        for p in parts:
+            dev.commit_part(p, async_copy=(mode == "async"))
+        dev.commit_world()
+        dev.set_camera(scA.camera)
+        dev.set_frame(fr)
+        dev.render_frame()
+        e, o = dev.get_debug(fr.spp, fr.max_depth, fr.W * fr.H)
+        return dev.map_frame().cpu().numpy().copy(), e.cpu().numpy().copy(), o.cpu().numpy().copy()
+
+    def same(a, b):
+        # events / occlusion bits are deterministic; pixels only up to float-atomic order
+        return np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and np.allclose(a[0], b[0], atol=1e-5)
+
+    ref = {}
+    dev = dpr.Device.create(0, 1, 0)
+    try:
+        ref["A"] = render(dev, scA.parts, "sync")
+        ref["B"] = render(dev, scB.parts, "sync")
+    finally:
+        dev.release()
+    dev = dpr.Device.create(0, 1, 0)
+    try:
+        pa, pb = pinned(scA.parts), pinned(scB.parts)
+        for name, parts in [("A", pa), ("B", pb), ("B", pb), ("A", pa), ("A", pa)]:
+            assert same(render(dev, parts, "async"), ref[name]), name
+        assert same(render(dev, scB.parts, "sync"), ref["B"])
+        assert not same(ref["A"], ref["B"])
+    finally:
+        dev.release()
+
+
+def test_committed_world_renders_while_next_parts_are_committed():
+    """The world of the last commit_world stays renderable (bricks included) while the parts
+    of the next world are cleared and committed; commit_world then switches worlds."""
+    dpr = _dpr()
+    G = 25
+    h = float(np.float32(2.0 / (G - 1)))
+    tf = di.default_tf(alpha_max=0.4, s0=0.2)
+    volA = di.Part(0, di.BRICK, gdims=(G,) * 3, origin=(-1, -1, -1), spacing=(h,) * 3,
+                   cell_lo=(0, 0, 0), cell_hi=(G - 1,) * 3, voxels=di.volume_field(G), tf=tf)
+    sphB = di.Part(0, di.SPHERES, albedo=(0.9, 0.2, 0.2), spheres=di.f32([[0, 0, 0, 0.7]]))
+    W = H = 24
+    cam = di.camera_basis((0.3, 1.5, -3.0), (0, -0.2, 0), (0, 1, 0), 50.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=2, spp_batch=2, max_depth=2, ao_k=1, ao_radius=0.3, dt=h,
+                  light_dir=di.f32(di.normalize((0.2, 1, 0.1))), E=(1, 1, 1), A=(0.2, 0.2, 0.2),
+                  flags=dpr.DPR_FLAG_DEBUG_DUMPS)
+    dev = dpr.Device.create(0, 1, 0)
+    try:
+        dev.set_camera(cam)
+        dev.set_frame(fr)
+
+        def frame():
+            dev.render_frame()
+            e, o = dev.get_debug(fr.spp, fr.max_depth, W * H)
+            return e.cpu().numpy().copy()
+
+        dev.commit_part(volA)
+        dev.commit_world()
+        evA = frame()
+        assert ((evA & 0x80000000) != 0).any()
+        dev.clear_parts()
+        dev.commit_part(sphB)
+        assert np.array_equal(frame(), evA)          # still world A (its bricks kept alive)
+        dev.commit_world()
+        evB = frame()
+        assert not ((evB & 0x80000000) != 0).any() and (evB[:, 0] >= 2).any()
+    finally:
+        dev.release()
