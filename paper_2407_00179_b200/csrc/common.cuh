@@ -282,6 +282,7 @@ struct WorldDev {
                        // ptxas keeps the PRMT selector as the immediate operand
     const WNode *wnodes;
     const float4 *prims;
+    const uint32_t *inv;    // local id -> prim index (cooperative prim tests)
     int64_t nprims;
     uint32_t id_base;       // global id of local prim 0 (P12)
     int nbricks;

@@ -593,17 +593,20 @@ void launch_collapse_level(const CollapseArgs &a, const int2 *items, int nitems,
 
 // prims_out[i] = prims_in[perm[i]] (3 float4 each): one thread per float4, coalesced writes.
 // The two permutations compose: wide-node order -> Morton order (perm) -> input order (sortperm).
+// inv[local id] = wide-BVH prim index (the cooperative prim tests resolve a hit by id).
 __global__ void k_permute_prims(const float4 *__restrict__ in, const uint32_t *__restrict__ perm,
-                                const uint32_t *__restrict__ sortperm, int64_t n, float4 *out) {
+                                const uint32_t *__restrict__ sortperm, int64_t n, float4 *out, uint32_t *inv) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 3 * n) return;
     int64_t i = t / 3;
-    out[t] = in[3 * (int64_t)sortperm[perm[i]] + (t - 3 * i)];
+    const uint32_t src = sortperm[perm[i]];
+    out[t] = in[3 * (int64_t)src + (t - 3 * i)];
+    if (t == 3 * i) inv[src] = (uint32_t)i;
 }
 
 void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t *sortperm, int64_t n,
-                          float4 *out, cudaStream_t s) {
-    if (n > 0) k_permute_prims<<<nblk(3 * n, 256), 256, 0, s>>>(in, perm, sortperm, n, out);
+                          float4 *out, uint32_t *inv, cudaStream_t s) {
+    if (n > 0) k_permute_prims<<<nblk(3 * n, 256), 256, 0, s>>>(in, perm, sortperm, n, out, inv);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -140,6 +140,27 @@ struct TraceCounters { uint32_t nodes, tris, sphs, vols; };
 constexpr int REFILL_PATH = DPR_REFILL_PATH, REFILL_OCCL = DPR_REFILL_OCCL;
 constexpr int WSTACK = 32;       // node-group stack entries (wide BVH depth bound)
 
+#ifndef DPR_COOP
+#define DPR_COOP 1
+#endif
+// Warp-cooperative prim tests: per pass every lane hands up to COOP_PER_LANE pending prims to
+// a per-warp list that all 32 lanes test (against the owner lane's ray), then the results are
+// reduced per owner in shared memory.
+#ifndef DPR_COOP_PER_LANE
+#define DPR_COOP_PER_LANE 16
+#endif
+constexpr int COOP_PER_LANE = DPR_COOP_PER_LANE;
+#ifndef DPR_P1_EXIT_ANY
+#define DPR_P1_EXIT_ANY 8
+#endif
+constexpr int P1_EXIT_ANY = DPR_P1_EXIT_ANY;
+struct CoopSmem {
+    uint32_t k[32 * COOP_PER_LANE];
+    uint8_t ow[32 * COOP_PER_LANE];
+    unsigned long long best[32];
+};
+constexpr int PRIM_BY_ID = 0x7fffffff;  // Hit.prim: a local hit, prim index = W.inv[local id]
+
 
 // Traversal state of one ray over the compressed 8-wide BVH.  A "node group" is the set of
 // not-yet-visited internal children of one visited node: (child_base, hit bits in traversal
@@ -189,12 +210,16 @@ __device__ __forceinline__ bool trav_done(const TravState &S) {
 // prim groups.  Both loops are warp-uniform.  Returns true when the lane is finished.
 template <bool ANY>
 __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2 *stack,
-                                          TraceCounters &tc, unsigned *overflow) {
+                                          TraceCounters &tc, unsigned *overflow, CoopSmem &cs) {
     for (;;) {
         // descend while some lane has no prim group yet; lanes that already hold one keep
         // descending speculatively into the second slot (keeps the phase-1 warp full)
         const bool work = (S.ng.y & 0xffu) != 0 || S.sp > 0;
-        if (!__any_sync(FULL, work && S.tm0 == 0)) break;
+        // any-hit rays leave phase 1 once at most P1_EXIT_ANY lanes still lack a prim group
+        // (the cooperative phase 2 is cheap; sweep r01), closest-hit rays when none does
+        const unsigned lacking = __ballot_sync(FULL, work && S.tm0 == 0);
+        if (!lacking) break;
+        if (ANY && __popc(lacking) <= P1_EXIT_ANY && __any_sync(FULL, pending_prims(S) != 0)) break;
 #ifdef DPR_ANYFREE
         if (!(work && (S.tm0 == 0 || S.tm1 == 0 || S.tm2 == 0))) continue;
 #else
@@ -276,6 +301,80 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
             else { S.tb2 = pb; S.tm2 = tmask; }
         }
     }
+#if DPR_COOP
+    // phase 2, warp-cooperative: the pending prims of all lanes are tested by all lanes; the
+    // P9 rule is a total order on (t, global id), so the per-owner minimum is independent of
+    // the order and of which lane tested what (any-hit: an OR).
+    const int lane = threadIdx.x & 31;
+    while (__any_sync(FULL, pending_prims(S) != 0)) {
+        const int c = min(__popc(S.tm0) + __popc(S.tm1) + __popc(S.tm2), COOP_PER_LANE);
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        const int T = __shfl_sync(FULL, x, 31);
+        int pos = x - c;
+        for (int j = 0; j < c; ++j) {
+            if (S.tm0 == 0) {
+                if (S.tm1 != 0) { S.tb0 = S.tb1; S.tm0 = S.tm1; S.tm1 = 0; }
+                else { S.tb0 = S.tb2; S.tm0 = S.tm2; S.tm2 = 0; }
+            }
+            cs.k[pos] = S.tb0 + (uint32_t)(__ffs(S.tm0) - 1);
+            cs.ow[pos] = (uint8_t)lane;
+            ++pos;
+            S.tm0 &= S.tm0 - 1;
+        }
+        cs.best[lane] = ANY ? 0ull : ~0ull;
+        __syncwarp();
+        for (int g0 = 0; g0 < T; g0 += 32) {
+            const int g = g0 + lane;
+            const bool act = g < T;
+            const int k = act ? (int)cs.k[g] : 0;
+            const int ow = act ? (int)cs.ow[g] : lane;
+            const f3 o = mk(__shfl_sync(FULL, S.o.x, ow), __shfl_sync(FULL, S.o.y, ow), __shfl_sync(FULL, S.o.z, ow));
+            const f3 d = mk(__shfl_sync(FULL, S.d.x, ow), __shfl_sync(FULL, S.d.y, ow), __shfl_sync(FULL, S.d.z, ow));
+            const float tmax = __shfl_sync(FULL, S.tmax, ow);
+            if (!act) continue;
+            const float4 *pr = W.prims + 3 * (int64_t)k;
+            const float4 a = __ldg(pr);
+            const uint32_t idw = __float_as_uint(a.w);
+            float t;
+            bool ok;
+            if (idw & SPHERE_BIT) {
+                const float4 b = __ldg(pr + 1);
+                tc.sphs++;
+                ok = sphere_hit(o, d, tmax, xyz(a), b.x, t);
+            } else {
+                const float4 b = __ldg(pr + 1), e = __ldg(pr + 2);
+                tc.tris++;
+                ok = tri_hit(o, d, tmax, xyz(a), xyz(b), xyz(e), t);
+            }
+            if (!ok) continue;
+            if (ANY) cs.best[ow] = 1ull;
+            else atomicMin(&cs.best[ow], ((unsigned long long)__float_as_uint(t) << 32) |
+                                             (unsigned long long)(W.id_base + (idw & ~SPHERE_BIT)));
+        }
+        __syncwarp();
+        const unsigned long long b = cs.best[lane];
+        __syncwarp();  // every lane has read its result before the next pass reuses the list
+        if (ANY) {
+            if (b) {
+                S.h.prim = PRIM_BY_ID;
+                trav_clear(S);
+            }
+        } else if (b != ~0ull) {
+            const float t = __uint_as_float((uint32_t)(b >> 32));
+            const uint32_t gid = (uint32_t)b;
+            if (t < S.h.t || (t == S.h.t && gid < S.h.id)) {
+                S.h.t = t;
+                S.h.id = gid;
+                S.h.prim = PRIM_BY_ID;
+            }
+        }
+    }
+#else
     // phase 2: prim groups (one prim per lane per iteration)
     while (__any_sync(FULL, pending_prims(S) != 0)) {
         if (S.tm0 == 0) {  // take the next pending group (any order is exact)
@@ -312,6 +411,7 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
             S.h.prim = k;
         }
     }
+#endif
     return trav_done(S);
 }
 
@@ -581,6 +681,8 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
     uint32_t *fetch = A.Q.fetch + (ANY ? 1 : 0);
     const float INF = __int_as_float(0x7f800000);
     uint2 stack[WSTACK];
+    __shared__ CoopSmem coop[TRACE_BLOCK / 32];
+    CoopSmem &cs = coop[threadIdx.x >> 5];
     TravState S;
     S.ng = make_uint2(0, 0);
     trav_clear(S);
@@ -620,7 +722,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
             continue;
         }
         if (!alive) trav_clear(S);
-        bool fin = trav_step<ANY>(A.W, S, stack, tc, &A.ctr->overflow);
+        bool fin = trav_step<ANY>(A.W, S, stack, tc, &A.ctr->overflow, cs);
         if (!(alive && fin)) continue;
         // finished: volume march, then write the result back into the record
         alive = false;
@@ -649,7 +751,10 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
             PathRec *r = A.Q.path_in + idx;
             bool changed = S.h.prim >= 0;
             f3 nrm = mk(0, 0, 0);
-            if (changed) nrm = prim_normal(A.W, S.h.prim, S.o, S.d, S.h.t);
+            if (changed) {
+                const int k = S.h.prim == PRIM_BY_ID ? (int)__ldg(A.W.inv + (S.h.id - A.W.id_base)) : S.h.prim;
+                nrm = prim_normal(A.W, k, S.o, S.d, S.h.t);
+            }
             if (A.W.nbricks > 0 && (F.flags & DPR_FLAG_DELTA)) {
                 const uint32_t p = __float_as_uint(r->c.w), meta = __float_as_uint(r->e.w);
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
