@@ -319,11 +319,18 @@ def run_gpu(args):
     h2d = 0
     for p in my_parts:
         q = di.Part(**p.__dict__)
+        def pin(a, dtype):
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype)).pin_memory()
+            return t.numpy(), t.numel() * t.element_size()
         if p.kind == di.TRIS:
-            v = torch.from_numpy(np.ascontiguousarray(p.verts)).pin_memory()
-            i = torch.from_numpy(np.ascontiguousarray(p.idx)).pin_memory()
-            q.verts, q.idx = v.numpy(), i.numpy()
-            h2d += v.numel() * 4 + i.numel() * 4
+            (q.verts, b0), (q.idx, b1) = pin(p.verts, np.float32), pin(p.idx, np.int32)
+            h2d += b0 + b1
+        elif p.kind == di.SPHERES:
+            q.spheres, b0 = pin(p.spheres, np.float32)
+            h2d += b0
+        else:
+            (q.voxels, b0), (q.tf, b1) = pin(p.voxels, np.float32), pin(p.tf, np.float32)
+            h2d += b0 + b1
         pinned.append(q)
     fb_host = torch.empty((scene.frame.H, scene.frame.W, 4), dtype=torch.float32).pin_memory()
     d2h = fb_host.numel() * 4 if rank == 0 else 0
