@@ -149,7 +149,12 @@ constexpr int WSTACK = 32;       // node-group stack entries (wide BVH depth bou
 #ifndef DPR_COOP_PER_LANE
 #define DPR_COOP_PER_LANE 16
 #endif
-constexpr int COOP_PER_LANE = DPR_COOP_PER_LANE;
+#ifndef DPR_COOP_PER_LANE_PATH
+#define DPR_COOP_PER_LANE_PATH DPR_COOP_PER_LANE
+#endif
+constexpr int COOP_PER_LANE = DPR_COOP_PER_LANE > DPR_COOP_PER_LANE_PATH ? DPR_COOP_PER_LANE
+                                                                         : DPR_COOP_PER_LANE_PATH;  // list size
+constexpr int COOP_CAP_ANY = DPR_COOP_PER_LANE, COOP_CAP_PATH = DPR_COOP_PER_LANE_PATH;
 #ifndef DPR_P1_EXIT_ANY
 #define DPR_P1_EXIT_ANY 8
 #endif
@@ -307,7 +312,7 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
     // the order and of which lane tested what (any-hit: an OR).
     const int lane = threadIdx.x & 31;
     while (__any_sync(FULL, pending_prims(S) != 0)) {
-        const int c = min(__popc(S.tm0) + __popc(S.tm1) + __popc(S.tm2), COOP_PER_LANE);
+        const int c = min(__popc(S.tm0) + __popc(S.tm1) + __popc(S.tm2), ANY ? COOP_CAP_ANY : COOP_CAP_PATH);
         int x = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
