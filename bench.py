@@ -306,10 +306,17 @@ def run_gpu(args):
     achieved = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
     tr = profile_traffic()
     traffic = None
+    limiter = None
     if tr and kname in tr:
         traffic = tr[kname].get("dram_bytes_per_launch")
+        if tr[kname].get("issue_active_pct") is not None:
+            # what ncu says actually limits the kernel (the touched-bytes roof is SURVEY 8(d)'s)
+            limiter = {"issue_active_pct": tr[kname]["issue_active_pct"],
+                       "active_threads_per_warp_inst": tr[kname].get("active_threads_per_warp_inst"),
+                       "warps_active_pct": tr[kname].get("warps_active_pct"),
+                       "source": tr[kname].get("source")}
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src, "ncu_limiter": limiter,
                 "alg_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_s * 1000,
                 "share_of_step": (ms / args.steps) / ms_per_step,
                 "other_kernel_ms_per_step": ((acc["ms_occl"] if kname == "k_trace_path" else acc["ms_path"]) / args.steps)}

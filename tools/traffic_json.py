@@ -14,7 +14,15 @@ for r in rows[2:]:
     n = r[hdr.index('Kernel Name')].split('(')[0]
     b = sum(float(r[hdr.index(k)].replace(',', '')) * mult[units[hdr.index(k)]]
             for k in ['dram__bytes_read.sum', 'dram__bytes_write.sum'])
+    def num(k):
+        try:
+            return float(r[hdr.index(k)].replace(',', ''))
+        except (ValueError, IndexError):
+            return None
     out[n] = {"dram_bytes_per_launch": b, "source": f"profiles/{tag}_ncu_trace.txt (ncu --set full, 1 launch)",
-              "version": tag}
+              "version": tag,
+              "issue_active_pct": num('smsp__issue_active.avg.pct_of_peak_sustained_active'),
+              "active_threads_per_warp_inst": num('smsp__thread_inst_executed_per_inst_executed.ratio'),
+              "warps_active_pct": num('sm__warps_active.avg.pct_of_peak_sustained_active')}
 json.dump(out, open('profiles/traffic.json', 'w'), indent=1)
 print(out)
