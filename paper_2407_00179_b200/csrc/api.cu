@@ -611,7 +611,7 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
     const int N = d->nranks;
     int64_t P_ = (int64_t)f.W * f.H;
     int64_t rays = P_ * f.spp_batch;
-    if (rays > 0xfffffff0ll) return fail(DPR_ERR_INVALID_ARG, "W*H*spp_batch too large for 32-bit queues");
+    if (rays > 0xe0000000ll) return fail(DPR_ERR_INVALID_ARG, "W*H*spp_batch too large for 32-bit queues");
     uint32_t pcap = (uint32_t)rays;
     int64_t ocap64 = rays * (1 + f.ao_k) * f.max_depth;
     if (ocap64 > 0xfffffff0ll) ocap64 = 0xfffffff0ll;

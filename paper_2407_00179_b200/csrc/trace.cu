@@ -593,21 +593,24 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
     // rays of a warp are nearly identical for spw > 1 (coherent traversal); warps walk tiles,
     // then sample groups.
     const FrameDev &F = A.F;
-    const int tiles_x = (F.W + tw - 1) / tw, tiles_y = (F.H + th - 1) / th;
-    const int64_t per_group = (int64_t)tiles_x * tiles_y * 32;
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // 32-bit index math (the launcher guarantees < 2^32 threads; 64-bit divisions cost ~10x)
+    const uint32_t tiles_x = ((uint32_t)F.W + tw - 1) / tw, tiles_y = ((uint32_t)F.H + th - 1) / th;
+    const uint32_t per_group = tiles_x * tiles_y * 32u;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     __shared__ uint32_t s_cnt[DPR_MAX_RANKS], s_base[DPR_MAX_RANKS];
     if (threadIdx.x < DPR_MAX_RANKS) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    const bool valid = t < per_group * (nsamp / spw);  // per_group is a multiple of 32
-    const int64_t g = t / per_group;
-    int64_t within = t % per_group;
-    int64_t tile = within >> 5;
-    int li = (int)(within & 31);
-    uint32_t s = (uint32_t)(s0 + g * spw + (li % spw));
-    int pi = li / spw;
-    int x = (int)(tile % tiles_x) * tw + (pi % tw);
-    int y = (int)(tile / tiles_x) * th + (pi / tw);
+    const bool valid = (uint64_t)t < (uint64_t)per_group * (uint32_t)(nsamp / spw);  // per_group: multiple of 32
+    const uint32_t g = t / per_group;
+    const uint32_t within = t - g * per_group;
+    const uint32_t tile = within >> 5;
+    const uint32_t li = within & 31u;
+    const uint32_t ty = tile / tiles_x, tx = tile - ty * tiles_x;
+    const uint32_t pi = li / (uint32_t)spw;
+    uint32_t s = (uint32_t)s0 + g * (uint32_t)spw + (li - pi * (uint32_t)spw);
+    const uint32_t py = pi / (uint32_t)tw;
+    int x = (int)(tx * (uint32_t)tw + (pi - py * (uint32_t)tw));
+    int y = (int)(ty * (uint32_t)th + py);
     bool inimg = valid && x < F.W && y < F.H;
     const int self = A.R.self;
     uint32_t p = (uint32_t)(y * F.W + x);
