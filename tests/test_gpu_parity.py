@@ -286,3 +286,23 @@ def test_delta_tracking_mixed_and_ring():
                       light_dir=di.f32(di.normalize((0.2, 1, 0.1))), E=(1, 1, 1), A=(0.2, 0.2, 0.2),
                       flags=flags)
         assert_parity(gpu_render(parts, 2, cam, fr), oracle_render(parts, 2, cam, fr))
+
+
+def test_limits_and_ragged_batches():
+    """Edge sizes: ao_k = 30 (the maximum: AO slots use bits 1..30 of the occlusion dump),
+    deep paths (max_depth 8) inside a closed sphere (every path ray hits), spp not a multiple
+    of spp_batch (ragged last batch), image size not a multiple of the 8x4 ray tiles."""
+    parts = [di.Part(0, di.SPHERES, albedo=(0.8, 0.7, 0.6), spheres=di.f32([[0, 0, 0, 3.0]])),
+             di.Part(1, di.SPHERES, albedo=(0.2, 0.5, 0.9), spheres=di.f32([[0.4, -0.2, 0.8, 0.5]])),
+             di.Part(1, di.TRIS, albedo=(0.9, 0.9, 0.2),
+                     verts=di.f32([[-1, -1, 1.5], [1, -1, 1.5], [0, 1, 1.5]]), idx=np.array([[0, 1, 2]], np.int32))]
+    W, H = 37, 23
+    cam = di.camera_basis((0, 0, -1.5), (0, 0, 1), (0, 1, 0), 70.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=5, spp_batch=2, max_depth=8, ao_k=30, ao_radius=0.7,
+                  light_dir=di.f32(di.normalize((0.3, 1, -0.2))), E=(1, 1, 1), A=(0.3, 0.3, 0.3),
+                  B=(0.1, 0.1, 0.2))
+    g = gpu_render(parts, 2, cam, fr)
+    o = oracle_render(parts, 2, cam, fr)
+    assert ((o.events[:, 7] >= 2) & ((o.events[:, 7] & 0x80000000) == 0)).any()  # depth-8 hits
+    assert (o.occl >> 30).any()                                                    # AO ray 29 set
+    assert_parity(g, o)
