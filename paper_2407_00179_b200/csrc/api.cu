@@ -1693,6 +1693,9 @@ int dpr_commit_part(dpr_device dev, const dpr_part_desc *part) {
 int dpr_clear_parts(dpr_device dev) {
     if (!valid_dev(dev)) return fail(DPR_ERR_INVALID_ARG, "null device");
     Dev *d = &dev->d;
+    // buffers freed below are stream-ordered on the library stream: order them after any
+    // upload still in flight on the copy stream
+    if (d->copy_pending) CK(cudaStreamWaitEvent(d->stream, d->copy_ev, 0));
     for (auto &p : d->parts) {
         // geometry arrays are recycled for the next commit (bounded pool); bricks are freed
         // stream-ordered (a render may still read them)
