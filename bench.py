@@ -141,6 +141,19 @@ class Clocks:
 
 
 # --------------------------------------------------------------------------------------
+PHASES = ("build", "gen", "trace_path", "trace_occl", "exchange", "reduce")
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample(scene, seconds: float = 12.0):
     """Time the oracle (as it stands) on a random pixel subset of the workload, all samples
     of each pixel (paths are independent under Philox, so a subset is an exact sample)."""
@@ -162,6 +175,7 @@ def oracle_sample(scene, seconds: float = 12.0):
         n = int(min(P, max(2 * n, n * seconds / max(dt, 1e-3) * 1.1)))
     rays = int(r.gen.sum())
     return {"value": rays / dt, "unit": "rays/s", "cores": os.cpu_count(), "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"{n} random pixels x {scene.frame.spp} spp of the workload ({rays} rays) in "
                       f"{dt:.1f} s; oracle BVH build over {osc.nprims} prims {t_build:.1f} s not included",
             "seconds": dt}
@@ -282,6 +296,9 @@ def run_gpu(args):
             acc["steps"] += st["steps"]; acc["exch"] += st["exchanged_bytes_local"]
             acc["ms_exch"] += st["ms_exchange"]
             acc["nodes"] += st["node_visits_local"]; acc["tris"] += st["tri_tests_local"]
+            acc["visits"] = acc.get("visits", 0) + int(np.asarray(st["V"]).sum())
+            for k in PHASES:
+                acc[f"ph_{k}"] = acc.get(f"ph_{k}", 0.0) + st[f"ms_{k}"]
             for k in range(2):
                 for f in ("rays", "nodes", "tris"):
                     acc.setdefault(f"k{k}_{f}", 0)
@@ -391,6 +408,9 @@ def run_gpu(args):
                        "step": "dpr_commit_world (LBVH rebuild) + dpr_render_frame",
                        "mode": args.mode, "frame_flags": int(scene.frame.flags)},
             "ms_per_frame": float(np.median(acc["ms_frame"])),
+            "ms_per_frame_min_max": [float(np.min(acc["ms_frame"])), float(np.max(acc["ms_frame"]))],
+            "ms_per_phase_rank0": {k: acc[f"ph_{k}"] / args.steps for k in PHASES},
+            "ray_visits_per_s": acc["visits"] / (elapsed_ms / 1000.0),
             "ms_build": float(np.median(acc["ms_build"])),
             "rays_per_frame": rays_per_frame,
             "wavefront_steps_per_frame": acc["steps"] / args.steps,
