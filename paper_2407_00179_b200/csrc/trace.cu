@@ -171,8 +171,29 @@ constexpr int PRIM_BY_ID = 0x7fffffff;  // Hit.prim: a local hit, prim index = W
 // not-yet-visited internal children of one visited node: (child_base, hit bits in traversal
 // order s' = slot ^ octant, parent imask).  A "prim group" is a 32-bit mask of prims at
 // prim_base.. of one visited node's hit leaves.
+#ifndef DPR_RAY_SMEM
+#define DPR_RAY_SMEM 1
+#endif
+#if DPR_RAY_SMEM
+// Ray origin, direction and reciprocal direction live in shared memory (SoA, one slot per
+// thread): 9 fewer registers per thread, and the cooperative prim tests read an owner's ray
+// directly instead of shuffling it.
+__shared__ float s_ray[9][TRACE_BLOCK];
+__device__ __forceinline__ f3 ray_o(int t) { return mk(s_ray[0][t], s_ray[1][t], s_ray[2][t]); }
+__device__ __forceinline__ f3 ray_d(int t) { return mk(s_ray[3][t], s_ray[4][t], s_ray[5][t]); }
+__device__ __forceinline__ f3 ray_id(int t) { return mk(s_ray[6][t], s_ray[7][t], s_ray[8][t]); }
+#define RAY_O(S) ray_o(threadIdx.x)
+#define RAY_D(S) ray_d(threadIdx.x)
+#define RAY_ID(S) ray_id(threadIdx.x)
+#else
+#define RAY_O(S) (S).o
+#define RAY_D(S) (S).d
+#define RAY_ID(S) (S).id3
+#endif
 struct TravState {
+#if !DPR_RAY_SMEM
     f3 o, d, id3;
+#endif
     float tmax;
     Hit h;
     uint32_t oct;
@@ -184,11 +205,19 @@ struct TravState {
 };
 
 __device__ __forceinline__ void trav_init(TravState &S, f3 o, f3 d, float tmax, Hit h, int64_t nprims) {
-    S.o = o; S.d = d; S.tmax = tmax; S.h = h;
+    S.tmax = tmax; S.h = h;
     const float tiny = 1e-20f;  // zero direction components -> finite reciprocal (box tests only)
-    S.id3 = mk(1.0f / (fabsf(d.x) > tiny ? d.x : copysignf(tiny, d.x)),
-               1.0f / (fabsf(d.y) > tiny ? d.y : copysignf(tiny, d.y)),
-               1.0f / (fabsf(d.z) > tiny ? d.z : copysignf(tiny, d.z)));
+    const f3 id3 = mk(1.0f / (fabsf(d.x) > tiny ? d.x : copysignf(tiny, d.x)),
+                      1.0f / (fabsf(d.y) > tiny ? d.y : copysignf(tiny, d.y)),
+                      1.0f / (fabsf(d.z) > tiny ? d.z : copysignf(tiny, d.z)));
+#if DPR_RAY_SMEM
+    const int t = threadIdx.x;
+    s_ray[0][t] = o.x; s_ray[1][t] = o.y; s_ray[2][t] = o.z;
+    s_ray[3][t] = d.x; s_ray[4][t] = d.y; s_ray[5][t] = d.z;
+    s_ray[6][t] = id3.x; s_ray[7][t] = id3.y; s_ray[8][t] = id3.z;
+#else
+    S.o = o; S.d = d; S.id3 = id3;
+#endif
     S.oct = (d.x < 0.0f ? 4u : 0u) | (d.y < 0.0f ? 2u : 0u) | (d.z < 0.0f ? 1u : 0u);
     // virtual root group: one internal child (slot 0, imask 1) at index 0
     S.ng = make_uint2(0u, nprims > 0 ? ((1u << S.oct) | (1u << 8)) : 0u);
@@ -251,12 +280,13 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         // t = f*ps + (po - 2^23*ps); rounding that offset costs at most |ps|/2, so near planes
         // use offset - |ps| and far planes offset + |ps|: conservative by construction (the
         // remaining relative error is covered by the (|x|+4)*2^-18 box padding).
-        const float psx = __uint_as_float((bits & 0xffu) << 23) * S.id3.x;
-        const float psy = __uint_as_float(((bits >> 8) & 0xffu) << 23) * S.id3.y;
-        const float psz = __uint_as_float(((bits >> 16) & 0xffu) << 23) * S.id3.z;
-        const float pox = __fmaf_rn(-8388608.0f, psx, (w0.x - S.o.x) * S.id3.x);
-        const float poy = __fmaf_rn(-8388608.0f, psy, (w0.y - S.o.y) * S.id3.y);
-        const float poz = __fmaf_rn(-8388608.0f, psz, (w0.z - S.o.z) * S.id3.z);
+        const f3 rid = RAY_ID(S), ro = RAY_O(S);
+        const float psx = __uint_as_float((bits & 0xffu) << 23) * rid.x;
+        const float psy = __uint_as_float(((bits >> 8) & 0xffu) << 23) * rid.y;
+        const float psz = __uint_as_float(((bits >> 16) & 0xffu) << 23) * rid.z;
+        const float pox = __fmaf_rn(-8388608.0f, psx, (w0.x - ro.x) * rid.x);
+        const float poy = __fmaf_rn(-8388608.0f, psy, (w0.y - ro.y) * rid.y);
+        const float poz = __fmaf_rn(-8388608.0f, psz, (w0.z - ro.z) * rid.z);
         const float onx = pox - fabsf(psx), ofx = pox + fabsf(psx);
         const float ony = poy - fabsf(psy), ofy = poy + fabsf(psy);
         const float onz = poz - fabsf(psz), ofz = poz + fabsf(psz);
@@ -264,9 +294,10 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         uint32_t nx0 = w2.x, nx1 = w2.y, fx0 = w3.z, fx1 = w3.w;
         uint32_t ny0 = w2.z, ny1 = w2.w, fy0 = w4.x, fy1 = w4.y;
         uint32_t nz0 = w3.x, nz1 = w3.y, fz0 = w4.z, fz1 = w4.w;
-        if (S.id3.x < 0.0f) { uint32_t t0 = nx0, t1 = nx1; nx0 = fx0; nx1 = fx1; fx0 = t0; fx1 = t1; }
-        if (S.id3.y < 0.0f) { uint32_t t0 = ny0, t1 = ny1; ny0 = fy0; ny1 = fy1; fy0 = t0; fy1 = t1; }
-        if (S.id3.z < 0.0f) { uint32_t t0 = nz0, t1 = nz1; nz0 = fz0; nz1 = fz1; fz0 = t0; fz1 = t1; }
+        // sign of the reciprocal == sign of the direction == octant bit
+        if (S.oct & 4u) { uint32_t t0 = nx0, t1 = nx1; nx0 = fx0; nx1 = fx1; fx0 = t0; fx1 = t1; }
+        if (S.oct & 2u) { uint32_t t0 = ny0, t1 = ny1; ny0 = fy0; ny1 = fy1; fy0 = t0; fy1 = t1; }
+        if (S.oct & 1u) { uint32_t t0 = nz0, t1 = nz1; nz0 = fz0; nz1 = fz1; fz0 = t0; fz1 = t1; }
         const float bound = ANY ? S.tmax : S.h.t;
         uint32_t hitm = 0;
 #pragma unroll
@@ -338,8 +369,13 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
             const bool act = g < T;
             const int k = act ? (int)cs.k[g] : 0;
             const int ow = act ? (int)cs.ow[g] : lane;
+#if DPR_RAY_SMEM
+            const int wb = threadIdx.x & ~31;
+            const f3 o = ray_o(wb + ow), d = ray_d(wb + ow);
+#else
             const f3 o = mk(__shfl_sync(FULL, S.o.x, ow), __shfl_sync(FULL, S.o.y, ow), __shfl_sync(FULL, S.o.z, ow));
             const f3 d = mk(__shfl_sync(FULL, S.d.x, ow), __shfl_sync(FULL, S.d.y, ow), __shfl_sync(FULL, S.d.z, ow));
+#endif
             const float tmax = __shfl_sync(FULL, S.tmax, ow);
             if (!act) continue;
             const float4 *pr = W.prims + 3 * (int64_t)k;
@@ -397,11 +433,11 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         if (idw & SPHERE_BIT) {
             float4 b = __ldg(pr + 1);
             tc.sphs++;
-            ok = sphere_hit(S.o, S.d, S.tmax, xyz(a), b.x, t);
+            ok = sphere_hit(RAY_O(S), RAY_D(S), S.tmax, xyz(a), b.x, t);
         } else {
             float4 b = __ldg(pr + 1), e = __ldg(pr + 2);
             tc.tris++;
-            ok = tri_hit(S.o, S.d, S.tmax, xyz(a), xyz(b), xyz(e), t);
+            ok = tri_hit(RAY_O(S), RAY_D(S), S.tmax, xyz(a), xyz(b), xyz(e), t);
         }
         if (!ok) continue;
         if (ANY) {
@@ -741,7 +777,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                 const uint32_t p = __float_as_uint(r->b.w), meta = __float_as_uint(r->c.w);
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
                 float ti; uint32_t ii; f3 rgb;
-                occluded = delta_track<true>(A.W, S.o, S.d, S.tmax, F.dt, F.seed, p, s, depth,
+                occluded = delta_track<true>(A.W, RAY_O(S), RAY_D(S), S.tmax, F.dt, F.seed, p, s, depth,
                                              slot == 0 ? PUR_VOL_SHADOW : PUR_VOL_AO,
                                              slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
             } else if (!occluded && A.W.nbricks > 0) {
@@ -749,7 +785,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
                 for (int b = 0; b < A.W.nbricks && !occluded; ++b) {
                     float ti; uint32_t ii; f3 rgb;
-                    occluded = march_brick<true>(A.W.bricks[b], S.o, S.d, S.tmax, S.tmax, F.dt, F.seed, p, s,
+                    occluded = march_brick<true>(A.W.bricks[b], RAY_O(S), RAY_D(S), S.tmax, S.tmax, F.dt, F.seed, p, s,
                                                  depth, slot == 0 ? PUR_VOL_SHADOW : PUR_VOL_AO,
                                                  slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
                 }
@@ -761,13 +797,13 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
             f3 nrm = mk(0, 0, 0);
             if (changed) {
                 const int k = S.h.prim == PRIM_BY_ID ? (int)__ldg(A.W.inv + (S.h.id - A.W.id_base)) : S.h.prim;
-                nrm = prim_normal(A.W, k, S.o, S.d, S.h.t);
+                nrm = prim_normal(A.W, k, RAY_O(S), RAY_D(S), S.h.t);
             }
             if (A.W.nbricks > 0 && (F.flags & DPR_FLAG_DELTA)) {
                 const uint32_t p = __float_as_uint(r->c.w), meta = __float_as_uint(r->e.w);
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
                 float ti; uint32_t kk; f3 rgb;
-                if (delta_track<false>(A.W, S.o, S.d, S.h.t, F.dt, F.seed, p, s, depth, PUR_VOL_PATH, 0u, ti, kk,
+                if (delta_track<false>(A.W, RAY_O(S), RAY_D(S), S.h.t, F.dt, F.seed, p, s, depth, PUR_VOL_PATH, 0u, ti, kk,
                                        rgb, tc.vols)) {
                     S.h.t = ti; S.h.id = VOL_BIT | kk; nrm = rgb; changed = true;
                 }
@@ -776,7 +812,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
                 for (int b = 0; b < A.W.nbricks; ++b) {
                     float ti; uint32_t ii; f3 rgb;
-                    if (march_brick<false>(A.W.bricks[b], S.o, S.d, INF, S.h.t, F.dt, F.seed, p, s, depth,
+                    if (march_brick<false>(A.W.bricks[b], RAY_O(S), RAY_D(S), INF, S.h.t, F.dt, F.seed, p, s, depth,
                                            PUR_VOL_PATH, 0u, ti, ii, rgb, tc.vols)) {
                         S.h.t = ti; S.h.id = VOL_BIT | ii; nrm = rgb; changed = true;
                     }
