@@ -190,6 +190,26 @@ __device__ __forceinline__ f3 ray_id(int t) { return mk(s_ray[6][t], s_ray[7][t]
 #define RAY_D(S) (S).d
 #define RAY_ID(S) (S).id3
 #endif
+#ifndef DPR_SM_STACK
+#define DPR_SM_STACK 0
+#endif
+#if DPR_SM_STACK > 0
+// the first DPR_SM_STACK node-group stack entries of each thread in shared memory (SoA),
+// deeper entries in local memory
+__shared__ uint2 s_stack[DPR_SM_STACK][TRACE_BLOCK];
+__device__ __forceinline__ void stack_push(uint2 *local, int &sp, uint2 v) {
+    if (sp < DPR_SM_STACK) s_stack[sp][threadIdx.x] = v;
+    else local[sp - DPR_SM_STACK] = v;
+    ++sp;
+}
+__device__ __forceinline__ uint2 stack_pop(const uint2 *local, int &sp) {
+    --sp;
+    return sp < DPR_SM_STACK ? s_stack[sp][threadIdx.x] : local[sp - DPR_SM_STACK];
+}
+#else
+__device__ __forceinline__ void stack_push(uint2 *local, int &sp, uint2 v) { local[sp++] = v; }
+__device__ __forceinline__ uint2 stack_pop(const uint2 *local, int &sp) { return local[--sp]; }
+#endif
 struct TravState {
 #if !DPR_RAY_SMEM
     f3 o, d, id3;
@@ -259,14 +279,14 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
 #else
         if (!(work && S.tm2 == 0)) continue;
 #endif
-        if ((S.ng.y & 0xffu) == 0) S.ng = stack[--S.sp];
+        if ((S.ng.y & 0xffu) == 0) S.ng = stack_pop(stack, S.sp);
         uint32_t hits = S.ng.y & 0xffu, pimask = S.ng.y >> 8;
         int sp_ = __ffs(hits) - 1;
         hits &= hits - 1;
         int slot = sp_ ^ (int)S.oct;
         int node = (int)S.ng.x + __popc(pimask & ((1u << slot) - 1u));
         if (hits) {
-            if (S.sp < WSTACK) stack[S.sp++] = make_uint2(S.ng.x, hits | (pimask << 8));
+            if (S.sp < WSTACK) stack_push(stack, S.sp, make_uint2(S.ng.x, hits | (pimask << 8)));
             else atomicOr(overflow, 2u);
         }
         // visit the node: test its (up to) 8 children
