@@ -42,6 +42,7 @@ __device__ __forceinline__ void fb_add(float4 *p, float4 v) {
 // last lane of each run issues ONE float4 atomic (same-address atomics would serialise).
 // All 32 lanes must call; inactive lanes pass active = false.
 __device__ __forceinline__ void fb_add_seg(float4 *fb, uint32_t p, float4 v, bool active) {
+    if (!__any_sync(FULL, active)) return;  // warp-uniform
     const int lane = threadIdx.x & 31;
     const uint32_t key = active ? p : (0x80000000u | (uint32_t)lane);  // unique when inactive
     const uint32_t prev = __shfl_up_sync(FULL, key, 1);
