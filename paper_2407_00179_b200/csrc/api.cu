@@ -692,6 +692,7 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.W.prmt_hi = 0x4b00u;
     a.W.prims = P<float4>(d->b_prims_w);
     a.W.inv = P<uint32_t>(d->b_inv);
+    a.W.nnodes = d->wnodes_count;
     a.W.nprims = d->nprims;
     a.W.id_base = fc.id_base[d->rank];
     a.W.nbricks = 0;
@@ -925,6 +926,7 @@ int render_group(std::vector<Dev *> &L) {
             for (int r = 0; r < N; ++r) { total += rows[3 * r] + rows[3 * r + 1]; ovf |= rows[3 * r + 2]; }
             if (ovf & 1u) return fail(DPR_ERR_QUEUE_OVERFLOW, "ray queue capacity exceeded; lower spp_batch");
             if (ovf & 2u) return fail(DPR_ERR_STATE, "BVH traversal stack overflow");
+            if (ovf & 4u) return fail(DPR_ERR_STATE, "device bounds check failed (DPR_CHECKS build)");
             if (total == 0) break;
             for (size_t i = 0; i < L.size(); ++i) {
                 Dev *d = L[i];
@@ -965,6 +967,7 @@ int render_group(std::vector<Dev *> &L) {
             RET(gather_counts(L, C, ovf));
             if (ovf & 1u) return fail(DPR_ERR_QUEUE_OVERFLOW, "ray queue capacity exceeded; lower spp_batch");
             if (ovf & 2u) return fail(DPR_ERR_STATE, "BVH traversal stack overflow");
+            if (ovf & 4u) return fail(DPR_ERR_STATE, "device bounds check failed (DPR_CHECKS build)");
             int64_t total = 0;
             for (int64_t v : C) total += v;
             if (total == 0) break;

@@ -284,6 +284,7 @@ struct WorldDev {
     const float4 *prims;
     const uint32_t *inv;    // local id -> prim index (cooperative prim tests)
     int64_t nprims;
+    int64_t nnodes;         // wide nodes (bounds checks of DPR_CHECKS builds)
     uint32_t id_base;       // global id of local prim 0 (P12)
     int nbricks;
     float amax;     // delta tracking majorant (max TF alpha over ALL ranks' bricks; R-DELTA)

@@ -291,6 +291,9 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
             else atomicOr(overflow, 2u);
         }
         // visit the node: test its (up to) 8 children
+#ifdef DPR_CHECKS
+        if (node < 0 || node >= W.nnodes) { atomicOr(overflow, 4u); trav_clear(S); S.ng.y = 0; continue; }
+#endif
         const WNode *nd = W.wnodes + node;
         float4 w0 = __ldg(&nd->w0);
         uint4 w1 = __ldg(&nd->w1), w2 = __ldg(&nd->w2), w3 = __ldg(&nd->w3), w4 = __ldg(&nd->w4);
@@ -388,7 +391,10 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         for (int g0 = 0; g0 < T; g0 += 32) {
             const int g = g0 + lane;
             const bool act = g < T;
-            const int k = act ? (int)cs.k[g] : 0;
+            int k = act ? (int)cs.k[g] : 0;
+#ifdef DPR_CHECKS
+            if (act && (k < 0 || k >= W.nprims)) { atomicOr(overflow, 4u); k = 0; }
+#endif
             const int ow = act ? (int)cs.ow[g] : lane;
 #if DPR_RAY_SMEM
             const int wb = threadIdx.x & ~31;
