@@ -180,7 +180,10 @@ class OracleScene:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().or_scene_free(self.h)
+            try:
+                lib().or_scene_free(self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     @property
