@@ -42,6 +42,7 @@ WORKLOADS = {
     "c3": "configs[2]: structured 1024^3 float32 volume split into per-rank bricks, DVR with volume "
           "shadows (1 spp, depth 1), 1920x1080",
     "c4": "configs[3]: 50M spheres in 1000 Gaussian clusters + ~5M-triangle gyroid, 1920x1080, 1 spp, depth 4",
+    "c5": "configs[4]: ~100M-triangle gyroid + 1024^3 volume bricks, 3840x2160, 64 spp (batches of 4), depth 2",
 }
 
 
@@ -56,6 +57,8 @@ def make_scene(cfg: str, world: int):
         return di.config3(nranks=world)
     if cfg == "c4":
         return di.config4(nranks=world)
+    if cfg == "c5":
+        return di.config5(nranks=world)
     # one 16-spp batch on one GPU; 2 batches of 8 spp when the world is split (bounds the
     # per-peer send queues: worst case every ray of a batch goes to one peer)
     return di.config2(nranks=world, spp_batch=16 if world == 1 else 8)
@@ -448,7 +451,7 @@ def main():
                     help="dp = ray forwarding over a partitioned world (the method, default); "
                          "replicated = whole world on every rank, pixels split (Barney mode, "
                          "P:663-668); composite = local renders + deep compositing (P:534-647)")
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"],
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="workload (default c2 = BASELINE configs[1], the metric's workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling)")
