@@ -14,6 +14,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -673,6 +674,45 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
     return DPR_OK;
 }
 
+// Conservative pixel rectangle of the projection of this rank's padded routing box (P8): a
+// primary ray whose first candidate is this rank passes through the box, so its pixel lies in
+// the projection.  Projection in double with a 2-pixel margin; the whole frame when a corner
+// is not in front of the eye, for thin-lens cameras, at N=1, or for an empty rank (then only
+// the pixel owner's misses matter and the rect is empty).
+void gen_rect(const Dev *d, const FrameCtx &fc, int rect[4]) {
+    const int W = d->fr.W, H = d->fr.H;
+    rect[0] = 0; rect[1] = 0; rect[2] = W; rect[3] = H;
+    static const bool off = getenv("DPR_GEN_CULL") && atoi(getenv("DPR_GEN_CULL")) == 0;
+    if (off || fc.R.nranks <= 1 || d->cam.lens_radius > 0.0f) return;
+    if (!fc.R.nonempty[d->rank]) { rect[2] = 0; rect[3] = 0; return; }
+    const dpr_camera_basis &c = d->cam;
+    double U[3], V[3], w[3], uu = 0, vv = 0;
+    for (int k = 0; k < 3; ++k) {
+        U[k] = c.U[k]; V[k] = c.V[k];
+        w[k] = (double)c.L[k] + 0.5 * U[k] + 0.5 * V[k];  // L = w - U/2 - V/2 (P2)
+        uu += U[k] * U[k]; vv += V[k] * V[k];
+    }
+    double wl = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+    double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+    const float *b = fc.R.box[d->rank];
+    for (int m = 0; m < 8; ++m) {
+        double X[3] = {b[(m & 1) ? 3 : 0], b[(m & 2) ? 4 : 1], b[(m & 4) ? 5 : 2]};
+        double rel[3] = {X[0] - c.E[0], X[1] - c.E[1], X[2] - c.E[2]};
+        double lam = (rel[0] * w[0] + rel[1] * w[1] + rel[2] * w[2]) / (wl * wl);
+        if (!(lam > 1e-9)) return;  // a corner at or behind the eye plane: whole frame
+        double su = 0.5 + (rel[0] * U[0] + rel[1] * U[1] + rel[2] * U[2]) / (lam * uu);
+        double sv = 0.5 + (rel[0] * V[0] + rel[1] * V[1] + rel[2] * V[2]) / (lam * vv);
+        x0 = std::min(x0, su * W); x1 = std::max(x1, su * W);
+        y0 = std::min(y0, sv * H); y1 = std::max(y1, sv * H);
+    }
+    rect[0] = (int)std::max(0.0, std::floor(x0) - 2.0);
+    rect[1] = (int)std::max(0.0, std::floor(y0) - 2.0);
+    rect[2] = (int)std::min((double)W, std::ceil(x1) + 2.0);
+    rect[3] = (int)std::min((double)H, std::ceil(y1) + 2.0);
+    if (rect[2] < rect[0]) rect[2] = rect[0];
+    if (rect[3] < rect[1]) rect[3] = rect[1];
+}
+
 StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     StepArgs a;
     memset(&a, 0, sizeof(a));
@@ -686,6 +726,7 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     }
     a.F.lens_radius = d->cam.lens_radius;
     a.F.focus_dist = d->cam.focus_dist;
+    gen_rect(d, fc, a.F.gen_rect);
     a.R = fc.R;
     a.R.self = d->rank;
     a.W.wnodes = P<WNode>(d->b_wnodes);

@@ -79,6 +79,9 @@ struct FrameDev {
     float cE[3], cL[3], cU[3], cV[3];  // camera basis (P2)
     float lens_radius, focus_dist;     // thin lens (reading R-DOF); 0 = pinhole
     int pix_rank, pix_nranks;          // replicated mode: generate only pixels owned by pix_rank
+    int gen_rect[4];                   // pixels [x0,x1) x [y0,y1) whose rays can meet this rank's
+                                       // padded box (conservative screen projection); others are
+                                       // generated only by their pixel owner
 };
 
 struct QueuesDev {

@@ -679,6 +679,10 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
     uint32_t p = (uint32_t)(y * F.W + x);
     if (F.pix_nranks > 1 && inimg)  // replicated mode: pixel ownership split
         inimg = (int)(((int64_t)p * F.pix_nranks) / F.P) == F.pix_rank;
+    // rays outside the projection of this rank's box cannot have it as first candidate: only
+    // their pixel owner generates them (to resolve misses)
+    if (inimg && !(x >= F.gen_rect[0] && x < F.gen_rect[2] && y >= F.gen_rect[1] && y < F.gen_rect[3]))
+        inimg = (int)(((int64_t)p * A.R.nranks) / F.P) == self;
     f3 o = mk(F.cE[0], F.cE[1], F.cE[2]), d = mk(0, 0, 0);
     int first = -2;
     if (inimg) {
