@@ -517,10 +517,9 @@ int build_world(Dev *d) {
         int nx = p.hi[0] - p.lo[0] + 1, ny = p.hi[1] - p.lo[1] + 1, nz = p.hi[2] - p.lo[2] + 1;
         for (int c = 0; c < 3; ++c) p.mc_dims[c] = (p.hi[c] - p.lo[c] + MC_SIZE - 1) / MC_SIZE;
         size_t nm = (size_t)p.mc_dims[0] * p.mc_dims[1] * p.mc_dims[2];
-        RET(ensure(d, p.mc, std::max<size_t>(nm, 1)));
-        launch_macrocells(P<float>(p.vox), nx, ny, nz, p.mc_dims[0], p.mc_dims[1], p.mc_dims[2],
-                          P<float4>(p.tf), p.tf_lo, p.tf_hi, p.dscale, P<uint8_t>(p.mc), s);
-        launches++;
+        RET(ensure(d, p.mc, std::max<size_t>(3 * nm, 1)));  // flags | distance field | scratch
+        launches += launch_macrocells(P<float>(p.vox), nx, ny, nz, p.mc_dims[0], p.mc_dims[1], p.mc_dims[2],
+                                      P<float4>(p.tf), p.tf_lo, p.tf_hi, p.dscale, P<uint8_t>(p.mc), s);
     }
     CK(cudaGetLastError());
     // snapshot of the volume state of this world
@@ -536,7 +535,9 @@ int build_world(Dev *d) {
             B.box_hi[c] = p.origin[c] + (float)p.hi[c] * p.spacing[c];
             B.gd[c] = p.gdims[c];
         }
-        B.vox = P<float>(p.vox); B.mc = P<uint8_t>(p.mc); B.tf = P<float4>(p.tf);
+        B.vox = P<float>(p.vox); B.mc = P<uint8_t>(p.mc);
+        B.mcd = P<uint8_t>(p.mc) + (size_t)p.mc_dims[0] * p.mc_dims[1] * p.mc_dims[2];
+        B.tf = P<float4>(p.tf);
         B.tf_lo = p.tf_lo; B.tf_hi = p.tf_hi; B.dscale = p.dscale;
         d->wbricks.push_back(B);
         d->amax_local = std::max(d->amax_local, p.amax);
@@ -650,7 +651,7 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
     RET(ensure(d, d->b_ctr, sizeof(Counters)));
     RET(ensure(d, d->b_counts, sizeof(uint32_t) * (2 * N + 1)));
     RET(ensure(d, d->b_in_count, sizeof(uint32_t) * 2));
-    RET(ensure(d, d->b_fetch, sizeof(uint32_t) * 2));
+    RET(ensure(d, d->b_fetch, sizeof(uint32_t) * 4));  // trace path/occl, march path/occl
     RET(ensure(d, d->b_part_lo, sizeof(uint32_t) * fc.part_lo.size()));
     RET(ensure(d, d->b_part_alb, sizeof(float4) * fc.part_alb.size()));
     if (!d->h_counts) {
@@ -727,6 +728,7 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.F.lens_radius = d->cam.lens_radius;
     a.F.focus_dist = d->cam.focus_dist;
     gen_rect(d, fc, a.F.gen_rect);
+    a.F.march_inline_min = march_inline_min(d->nsm);
     a.R = fc.R;
     a.R.self = d->rank;
     a.W.wnodes = P<WNode>(d->b_wnodes);
@@ -973,27 +975,27 @@ int render_group(std::vector<Dev *> &L) {
                 Dev *d = L[i];
                 cur[i] ^= 1;
                 const uint32_t n_path = rows[3 * d->rank], n_occl = rows[3 * d->rank + 1];
-                CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 2, d->stream));
+                CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 4, d->stream));
                 StepArgs a = make_args(d, fc, cur[i]);
                 const int grid_r = d->nsm * 8;
                 if (n_path) {
                     cudaEvent_t e0 = next_event(d), e1 = next_event(d);
                     CK(cudaEventRecord(e0, d->stream));
-                    launch_trace_path(a, grid_p[i], d->stream);
+                    const int nk = launch_trace_path(a, grid_p[i], n_path, d->stream);
                     CK(cudaEventRecord(e1, d->stream));
                     launch_shade_path(a, grid_r, d->stream);
                     if (i == 0) t_path.push_back({e0, e1});
-                    launches += 2;
+                    launches += 1 + nk;
                     d->tpl++;
                 }
                 if (n_occl) {
                     cudaEvent_t e0 = next_event(d), e1 = next_event(d);
                     CK(cudaEventRecord(e0, d->stream));
-                    launch_trace_occl(a, grid_o[i], d->stream);
+                    const int nk = launch_trace_occl(a, grid_o[i], n_occl, d->stream);
                     CK(cudaEventRecord(e1, d->stream));
                     launch_resolve_occl(a, grid_r, d->stream);
                     if (i == 0) t_occl.push_back({e0, e1});
-                    launches += 2;
+                    launches += 1 + nk;
                     d->tol++;
                 }
                 CK(cudaGetLastError());
@@ -1077,27 +1079,27 @@ int render_group(std::vector<Dev *> &L) {
                 cur[i] ^= 1;
                 CK(cudaMemcpyAsync(d->b_in_count.p, d->h_in, sizeof(uint32_t) * 2, cudaMemcpyHostToDevice, d->stream));
                 CK(cudaMemsetAsync(d->b_counts.p, 0, sizeof(uint32_t) * (2 * N + 1), d->stream));
-                CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 2, d->stream));
+                CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 4, d->stream));
                 StepArgs a = make_args(d, fc, cur[i]);
                 const int grid_r = d->nsm * 8;
                 if (d->h_in[0]) {
                     cudaEvent_t e0 = next_event(d), e1 = next_event(d);
                     CK(cudaEventRecord(e0, d->stream));
-                    launch_trace_path(a, grid_p[i], d->stream);
+                    const int nk = launch_trace_path(a, grid_p[i], d->h_in[0], d->stream);
                     CK(cudaEventRecord(e1, d->stream));
                     launch_shade_path(a, grid_r, d->stream);
                     if (i == 0) t_path.push_back({e0, e1});
-                    launches += 2;
+                    launches += 1 + nk;
                     d->tpl++;
                 }
                 if (d->h_in[1]) {
                     cudaEvent_t e0 = next_event(d), e1 = next_event(d);
                     CK(cudaEventRecord(e0, d->stream));
-                    launch_trace_occl(a, grid_o[i], d->stream);
+                    const int nk = launch_trace_occl(a, grid_o[i], d->h_in[1], d->stream);
                     CK(cudaEventRecord(e1, d->stream));
                     launch_resolve_occl(a, grid_r, d->stream);
                     if (i == 0) t_occl.push_back({e0, e1});
-                    launches += 2;
+                    launches += 1 + nk;
                     d->tol++;
                 }
                 CK(cudaGetLastError());

@@ -239,6 +239,9 @@ __device__ __forceinline__ f3 iso_dir(uint64_t seed, uint32_t p, uint32_t s, uin
 // ---------------------------------------------------------------------------------------
 // Leaf size bound of the wide-BVH collapse (binary subtrees with <= LEAF_MAX prims become
 // leaf children).
+#ifndef DPR_FILL_LEAVES
+#define DPR_FILL_LEAVES 0
+#endif
 #ifndef DPR_LEAF_MAX
 #define DPR_LEAF_MAX 3
 #endif
@@ -256,11 +259,14 @@ struct BrickDev {
     float box_lo[3], box_hi[3];
     const float *vox;       // x fastest
     const uint8_t *mc;      // 1 = some sample in the macrocell may have alpha > 0
+    const uint8_t *mcd;     // Chebyshev distance (macrocells, capped at MC_DIST_CAP) to the
+                            // nearest macrocell with mc = 1 (0: mc = 1 here)
     const float4 *tf;       // 256 rgba
     float tf_lo, tf_hi, dscale;
 };
 
 constexpr int MC_SIZE = 16;
+constexpr int MC_DIST_PASSES = 8, MC_DIST_CAP = MC_DIST_PASSES + 1;  // exact below the cap
 constexpr int MAX_BRICKS = 8;
 
 // Compressed 8-wide node (80 B; layout in the spirit of Ylitie, Karras, Laine 2017

@@ -64,9 +64,10 @@ void launch_ploc_scan(int *block_counts, int64_t nblocks, int *totals, cudaStrea
 void launch_ploc_write(const PlocArgs &a, const int *clusters, const int *nn, int64_t m, const int *block_offsets,
                        int node_base, int *next_clusters, cudaStream_t s);
 
-void launch_macrocells(const float *vox, int nx, int ny, int nz, int mcx, int mcy, int mcz,
-                       const float4 *tf, float tf_lo, float tf_hi, float dscale, uint8_t *mc,
-                       cudaStream_t s);
+// mc: 3 x (mcx*mcy*mcz) bytes: flags, distance field, scratch; returns kernels launched
+int launch_macrocells(const float *vox, int nx, int ny, int nz, int mcx, int mcy, int mcz,
+                      const float4 *tf, float tf_lo, float tf_hi, float dscale, uint8_t *mc,
+                      cudaStream_t s);
 
 // ---- trace.cu --------------------------------------------------------------------------
 struct FrameDev {
@@ -82,6 +83,8 @@ struct FrameDev {
     int gen_rect[4];                   // pixels [x0,x1) x [y0,y1) whose rays can meet this rank's
                                        // padded box (conservative screen projection); others are
                                        // generated only by their pixel owner
+    uint32_t march_inline_min;         // P10 march inside the trace kernels when the queue holds
+                                       // at least this many rays, else in k_march_* (G lanes/ray)
 };
 
 struct QueuesDev {
@@ -112,8 +115,10 @@ struct StepArgs {
 };
 
 void launch_gen_primary(const StepArgs &a, int s0, int nsamp, int spw_max, cudaStream_t s);
-void launch_trace_path(const StepArgs &a, int grid, cudaStream_t s);
-void launch_trace_occl(const StepArgs &a, int grid, cudaStream_t s);
+// n: input rays (sizes the march launch); returns the number of kernels launched
+uint32_t march_inline_min(int nsm);
+int launch_trace_path(const StepArgs &a, int grid, uint32_t n, cudaStream_t s);
+int launch_trace_occl(const StepArgs &a, int grid, uint32_t n, cudaStream_t s);
 void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s);
 void launch_resolve_occl(const StepArgs &a, int grid, cudaStream_t s);
 int trace_path_occupancy(int block);

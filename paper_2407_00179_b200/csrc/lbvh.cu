@@ -477,6 +477,26 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
         cid[nc] = a.right[c]; bin_child(a, cid[nc], lo[nc], hi[nc], c1[nc]);
         nc++;
     }
+#if DPR_FILL_LEAVES
+    // slots still free and only small subtrees (<= LEAF_MAX prims) left: split them further
+    // (largest area first) so that their prims get their own boxes instead of being tested
+    // together; the tree does not get deeper
+    while (nc < 8) {
+        int best = -1;
+        float ba = -1.0f;
+        for (int i = 0; i < nc; ++i) {
+            if (cid[i] >= a.n - 1) continue;
+            float ex = hi[i][0] - lo[i][0], ey = hi[i][1] - lo[i][1], ez = hi[i][2] - lo[i][2];
+            float area = ex * ey + ey * ez + ez * ex;
+            if (area > ba) { ba = area; best = i; }
+        }
+        if (best < 0) break;
+        int c = cid[best];
+        cid[best] = a.left[c]; bin_child(a, cid[best], lo[best], hi[best], c1[best]);
+        cid[nc] = a.right[c]; bin_child(a, cid[nc], lo[nc], hi[nc], c1[nc]);
+        nc++;
+    }
+#endif
     // node box and octant slot assignment (greedy on dot(child centre - node centre, octant))
     float nlo_[3], nhi_[3];
     for (int c = 0; c < 3; ++c) {
@@ -671,6 +691,31 @@ __global__ void __launch_bounds__(MC_BLOCK) k_macrocells(const float *__restrict
     }
 }
 
+// Macrocell distance field (empty-space jumps of k_march_*): d = 0 where mc = 1, else the
+// Chebyshev distance in macrocells to the nearest mc = 1 cell, capped.  k passes of
+// d <- min(d, 1 + min over the 26 neighbours) from d0 = (mc ? 0 : CAP) give min(true, k+1)
+// exactly when CAP = k+1 (cells farther than k keep CAP <= their true distance), so a
+// distance never overstates the empty box around a cell.  Cells outside the grid hold no
+// owned sample and count as empty.
+__global__ void k_mc_dist_init(const uint8_t *__restrict__ mc, int64_t n, uint8_t *d) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) d[i] = mc[i] ? 0 : (uint8_t)MC_DIST_CAP;
+}
+__global__ void k_mc_dist_pass(const uint8_t *__restrict__ din, int mx, int my, int mz, uint8_t *dout) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)mx * my * mz) return;
+    const int x = (int)(i % mx), y = (int)((i / mx) % my), z = (int)(i / ((int64_t)mx * my));
+    int m = din[i];
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int xx = x + dx, yy = y + dy, zz = z + dz;
+                if (xx < 0 || yy < 0 || zz < 0 || xx >= mx || yy >= my || zz >= mz) continue;
+                m = min(m, 1 + (int)din[((int64_t)zz * my + yy) * mx + xx]);
+            }
+    dout[i] = (uint8_t)m;
+}
+
 // ---------------------------------------------------------------------------------------
 // Host-side launchers.
 // ---------------------------------------------------------------------------------------
@@ -717,11 +762,20 @@ void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, floa
                          cudaStream_t s) {
     if (n > 0) k_gather_prims<<<nblk(n, 256), 256, 0, s>>>(in, perm, n, out, blo, bhi, slo, shi);
 }
-void launch_macrocells(const float *vox, int nx, int ny, int nz, int mcx, int mcy, int mcz,
-                       const float4 *tf, float tf_lo, float tf_hi, float dscale, uint8_t *mc,
-                       cudaStream_t s) {
-    if (mcx > 0 && mcy > 0 && mcz > 0)
-        k_macrocells<<<dim3(mcy, mcz), MC_BLOCK, 0, s>>>(vox, nx, ny, nz, mcx, mcy, mcz, tf, tf_lo, tf_hi, dscale, mc);
+int launch_macrocells(const float *vox, int nx, int ny, int nz, int mcx, int mcy, int mcz,
+                      const float4 *tf, float tf_lo, float tf_hi, float dscale, uint8_t *mc,
+                      cudaStream_t s) {
+    if (!(mcx > 0 && mcy > 0 && mcz > 0)) return 0;
+    k_macrocells<<<dim3(mcy, mcz), MC_BLOCK, 0, s>>>(vox, nx, ny, nz, mcx, mcy, mcz, tf, tf_lo, tf_hi, dscale, mc);
+    // distance field at mc + n (ping-pong with mc + 2n; an even number of passes ends in mc + n)
+    const int64_t n = (int64_t)mcx * mcy * mcz;
+    uint8_t *d0 = mc + n, *d1 = mc + 2 * n;
+    k_mc_dist_init<<<nblk(n, 256), 256, 0, s>>>(mc, n, d0);
+    static_assert(MC_DIST_PASSES % 2 == 0, "result must end in mc + n");
+    for (int k = 0; k < MC_DIST_PASSES; ++k) {
+        k_mc_dist_pass<<<nblk(n, 256), 256, 0, s>>>(k % 2 ? d1 : d0, mcx, mcy, mcz, k % 2 ? d0 : d1);
+    }
+    return 2 + MC_DIST_PASSES;
 }
 
 }  // namespace dpr

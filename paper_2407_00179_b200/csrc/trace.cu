@@ -13,7 +13,10 @@
 // Queues are appended with warp-aggregated atomics (__match_any_sync per destination).
 // All kernels read their input count from device memory, so launch shapes never depend on
 // host-known counts.
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -156,6 +159,12 @@ constexpr int WSTACK = 32;       // node-group stack entries (wide BVH depth bou
 constexpr int COOP_PER_LANE = DPR_COOP_PER_LANE > DPR_COOP_PER_LANE_PATH ? DPR_COOP_PER_LANE
                                                                          : DPR_COOP_PER_LANE_PATH;  // list size
 constexpr int COOP_CAP_ANY = DPR_COOP_PER_LANE, COOP_CAP_PATH = DPR_COOP_PER_LANE_PATH;
+#ifndef DPR_WARP_MARCH
+#define DPR_WARP_MARCH 1
+#endif
+#ifndef DPR_LEAF_UNROLL
+#define DPR_LEAF_UNROLL 0
+#endif
 #ifndef DPR_P1_EXIT_ANY
 #define DPR_P1_EXIT_ANY 8
 #endif
@@ -347,6 +356,16 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         if (S.oct & 2u) ih = ((ih & 0x33u) << 2) | ((ih & 0xccu) >> 2);
         if (S.oct & 1u) ih = ((ih & 0x55u) << 1) | ((ih & 0xaau) >> 1);
         uint32_t ihits = ih, tmask = 0;
+#if DPR_LEAF_UNROLL
+        // branch-free over the 8 slots (no divergence on the number of hit leaves)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t meta = __byte_perm(c < 4 ? w1.z : w1.w, 0u, (uint32_t)(c & 3) | 0x4440u);
+            const uint32_t r = ((2u << ((meta >> 5) & 3u)) - 1u) << (meta & 31u);
+            tmask |= (lh >> c) & 1u ? r : 0u;
+        }
+        lh = 0;
+#endif
         while (lh) {
             const int c = __ffs(lh) - 1;
             lh &= lh - 1;
@@ -570,6 +589,259 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
     }
     return false;
 }
+
+// ---------------------------------------------------------------------------------------
+// The same P10 march in its own kernel (k_march_*, after the surface trace has written
+// bestT / the occlusion flag into the record), G lanes per ray.  The per-lane march inside
+// the traversal kernels held a warp for its longest ray and paid two dependent memory round
+// trips (macrocell byte, then 8 voxels) per sample and one per 16-voxel empty-space jump.
+// Here:
+//  * a group of G lanes marches one ray in chunks of 4G samples: lane l of the group
+//    evaluates samples cb+4l .. cb+4l+3 (one Philox block per lane: P1 counter sub =
+//    subhi | i>>2, word i&3); the macrocell loads of a chunk, then its voxel loads, are in
+//    flight together, and the first colliding sample of the chunk is the lowest (ballot);
+//  * empty space is skipped with a macrocell distance field: d = Chebyshev distance (in
+//    macrocells, capped) to the nearest macrocell that may have alpha > 0, so the ray jumps
+//    to the exit of the (2d-1)^3-macrocell box of empty cells around it (alpha == 0 for every
+//    owned sample in it: exact);
+//  * a group whose ray finished fetches the next ray (persistent loop), so no group waits for
+//    another group's ray.
+// Sample set, arithmetic and decisions are those of march_brick and the oracle's march:
+// the range [i0, i1], owned samples only, skipped samples only where alpha is 0, stop at
+// t_i >= bound; a path ray's result is the first collision over the rank's bricks.
+// ---------------------------------------------------------------------------------------
+struct MarchRay {
+    f3 o, d;
+    float tmax, bound;
+    uint32_t p, s, depth, purpose, subhi;
+    int bi;               // current brick (nbricks = finished)
+    int64_t i, i1;        // next sample, last sample of the current brick's range
+    bool hit;
+    uint32_t hid;         // VOL_BIT | i of the collision
+    f3 rgb;
+};
+
+// Advance to the first brick (from r.bi on) whose padded box the ray crosses; set its range.
+__device__ __forceinline__ void march_begin_brick(const WorldDev &W, MarchRay &r, float dt) {
+    for (; r.bi < W.nbricks; ++r.bi) {
+        const BrickDev &B = W.bricks[r.bi];
+        float plo[3], phi[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { plo[c] = B.box_lo[c] - B.h[c]; phi[c] = B.box_hi[c] + B.h[c]; }
+        float t0, t1;
+        if (!slab(plo, phi, r.o, r.d, r.tmax, t0, t1)) continue;
+        float a = floorf(t0 / dt - 0.5f);
+        float bb = ceilf(t1 / dt);
+        if (bb > 1.0e9f) bb = 1.0e9f;
+        const int64_t i0 = (int64_t)a - 1;
+        r.i = i0 < 0 ? 0 : i0;
+        r.i1 = (int64_t)bb + 1;
+        return;
+    }
+}
+
+template <bool ANY, int G>
+__device__ __forceinline__ void march_groups(const StepArgs &A) {
+    const FrameDev &F = A.F;
+    const WorldDev &W = A.W;
+    const float dt = F.dt;
+    const int lane = threadIdx.x & 31, gl = lane % G, gbase = lane - gl;
+    const uint32_t n_in = A.Q.in_count[ANY ? 1 : 0];
+    uint32_t *fetch = A.Q.fetch + (ANY ? 3 : 2);
+    uint32_t vols = 0;
+    MarchRay r;
+    r.bi = 0; r.i = 0; r.i1 = -1; r.hit = false; r.hid = 0; r.rgb = mk(0, 0, 0);
+    r.o = r.d = mk(0, 0, 0); r.tmax = r.bound = 0.0f; r.p = r.s = r.depth = r.purpose = r.subhi = 0;
+    bool alive = false, exhausted = false;
+    uint32_t idx = 0;
+    for (;;) {
+        // refill: the leaders of finished groups fetch one ray each
+        const unsigned dl = __ballot_sync(FULL, !alive && gl == 0);
+        if (!exhausted && dl) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(fetch, (uint32_t)__popc(dl));
+            base = __shfl_sync(FULL, base, 0);
+            if (base + (uint32_t)__popc(dl) >= n_in) exhausted = true;
+            const uint32_t mine = base + __popc(dl & lanemask_lt());
+            const uint32_t gidx = __shfl_sync(FULL, mine, gbase);
+            if (!alive && gidx < n_in) {
+                idx = gidx;
+                alive = true;
+                r.bi = 0; r.hit = false; r.hid = 0; r.rgb = mk(0, 0, 0);
+                if (ANY) {
+                    const OcclRec *q = A.Q.occl_in + idx;
+                    const float4 a = __ldcg(&q->a), b = __ldcg(&q->b), c = __ldcg(&q->c);
+                    const uint32_t meta = __float_as_uint(c.w), slot = meta >> 24;
+                    r.o = xyz(a); r.d = xyz(b); r.tmax = a.w; r.bound = a.w;
+                    r.p = __float_as_uint(b.w); r.s = meta & 0xffffu; r.depth = (meta >> 16) & 0xffu;
+                    r.purpose = slot == 0 ? PUR_VOL_SHADOW : PUR_VOL_AO;
+                    r.subhi = slot == 0 ? 0u : ((slot - 1) << 24);
+                    if (!(a.w >= 0.0f)) r.bi = W.nbricks;  // occluded by a surface: nothing to do
+                } else {
+                    const PathRec *q = A.Q.path_in + idx;
+                    const float4 a = __ldcg(&q->a), b = __ldcg(&q->b), c = __ldcg(&q->c), e = __ldcg(&q->e);
+                    const uint32_t meta = __float_as_uint(e.w);
+                    r.o = xyz(a); r.d = xyz(b); r.tmax = __int_as_float(0x7f800000); r.bound = a.w;
+                    r.p = __float_as_uint(c.w); r.s = meta & 0xffffu; r.depth = (meta >> 16) & 0xffu;
+                    r.purpose = PUR_VOL_PATH; r.subhi = 0u;
+                }
+                march_begin_brick(W, r, dt);
+            }
+        }
+        if (!__any_sync(FULL, alive)) {
+            if (exhausted) break;
+            continue;
+        }
+        // group-uniform state check (every lane of a group computes the same): 0 idle,
+        // 1 chunk, 2 current brick finished
+        int mode = 0;
+        if (alive) mode = (r.bi >= W.nbricks || r.i > r.i1 || !(sample_t(r.i, dt) < r.bound)) ? 2 : 1;
+        // chunk: samples cb .. cb+4G-1 (those in [i, i1] with t < bound, owned, in a macrocell
+        // that may have alpha > 0); every lane takes part in the ballot and shuffles below
+        const int64_t cb = r.i & ~(int64_t)3;
+        const int64_t jl = cb + 4 * gl;
+        int hk = 4;                  // first colliding sample of this lane (4: none)
+        uint32_t cnt = 0;            // samples this lane evaluated (before / at its collision)
+        float th = 0.0f;
+        f3 rgbh = mk(0, 0, 0);
+        int64_t inext = cb + 4 * G;  // next sample (decided by the group's last lane)
+        if (mode == 1) {
+            const BrickDev &B = W.bricks[r.bi];
+            const int nx = B.hi[0] - B.lo[0] + 1, ny = B.hi[1] - B.lo[1] + 1;
+            const int64_t sy = nx, sz = (int64_t)nx * ny;
+            bool val[4], own3 = false;
+            int dist3 = 0, mc3[3] = {0, 0, 0};
+            float tk[4], fx[4], fy[4], fz[4];
+            const float *vp[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t j = jl + k;
+                tk[k] = sample_t(j, dt);
+                const f3 pt = mk(r.o.x + tk[k] * r.d.x, r.o.y + tk[k] * r.d.y, r.o.z + tk[k] * r.d.z);
+                const f3 g = mk((pt.x - B.O[0]) / B.h[0], (pt.y - B.O[1]) / B.h[1], (pt.z - B.O[2]) / B.h[2]);
+                const bool own = g.x >= (float)B.lo[0] && g.x < (float)B.hi[0] && g.y >= (float)B.lo[1] &&
+                                 g.y < (float)B.hi[1] && g.z >= (float)B.lo[2] && g.z < (float)B.hi[2];
+                const float fx0 = floorf(g.x), fy0 = floorf(g.y), fz0 = floorf(g.z);
+                fx[k] = g.x - fx0; fy[k] = g.y - fy0; fz[k] = g.z - fz0;
+                const int ix = own ? (int)fx0 - B.lo[0] : 0, iy = own ? (int)fy0 - B.lo[1] : 0,
+                          iz = own ? (int)fz0 - B.lo[2] : 0;
+                vp[k] = B.vox + (int64_t)ix + sy * iy + sz * iz;
+                // distance 0 <=> the macrocell may have alpha > 0 (else the sample is skipped: exact)
+                const int dist =
+                    own ? (int)__ldg(B.mcd + ((iz / MC_SIZE) * B.mc_dims[1] + iy / MC_SIZE) * B.mc_dims[0] + ix / MC_SIZE)
+                        : 0;
+                val[k] = own && dist == 0 && j >= r.i && j <= r.i1 && tk[k] < r.bound;
+                if (k == 3) {
+                    own3 = own; dist3 = dist;
+                    mc3[0] = ix / MC_SIZE; mc3[1] = iy / MC_SIZE; mc3[2] = iz / MC_SIZE;
+                }
+            }
+            if (val[0] || val[1] || val[2] || val[3]) {
+                const uint4 rr = rng4(F.seed, r.p, r.s, r.depth, r.purpose, r.subhi | (uint32_t)(jl >> 2));
+                float v[4][8];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float *q = val[k] ? vp[k] : B.vox;
+                    v[k][0] = __ldg(q); v[k][1] = __ldg(q + 1); v[k][2] = __ldg(q + sy); v[k][3] = __ldg(q + sy + 1);
+                    v[k][4] = __ldg(q + sz); v[k][5] = __ldg(q + sz + 1); v[k][6] = __ldg(q + sz + sy);
+                    v[k][7] = __ldg(q + sz + sy + 1);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (!val[k] || hk < 4) continue;
+                    cnt++;
+                    const float c00 = lerpf(v[k][0], v[k][1], fx[k]), c10 = lerpf(v[k][2], v[k][3], fx[k]);
+                    const float c01 = lerpf(v[k][4], v[k][5], fx[k]), c11 = lerpf(v[k][6], v[k][7], fx[k]);
+                    const float c0 = lerpf(c00, c10, fy[k]), c1 = lerpf(c01, c11, fy[k]);
+                    f3 rgb;
+                    const float alpha = tf_alpha_rgb(B, lerpf(c0, c1, fz[k]), ANY ? nullptr : &rgb);
+                    const uint32_t x = k == 0 ? rr.x : (k == 1 ? rr.y : (k == 2 ? rr.z : rr.w));
+                    if (u01(x) < alpha) {
+                        hk = k;
+                        th = tk[k];
+                        if (!ANY) rgbh = rgb;
+                    }
+                }
+            }
+            if (gl == G - 1 && own3 && dist3 > 0) {
+                // the chunk's last sample lies in empty space: every macrocell within Chebyshev
+                // distance dist3-1 of its own is empty, so continue one sample before the ray
+                // leaves that box (the margin of march_brick's jump)
+                float mlo[3], mhi[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int c0 = max(B.lo[c] + (mc3[c] - (dist3 - 1)) * MC_SIZE, B.lo[c]);
+                    const int c1 = min(B.lo[c] + (mc3[c] + dist3) * MC_SIZE, B.hi[c]);
+                    mlo[c] = B.O[c] + (float)c0 * B.h[c];
+                    mhi[c] = B.O[c] + (float)c1 * B.h[c];
+                }
+                float m0, m1;
+                slab(mlo, mhi, r.o, r.d, r.tmax, m0, m1);
+                const int64_t jump = (int64_t)floorf(m1 / dt - 0.5f) - 2;
+                if (jump + 1 > inext) inext = jump + 1;
+            }
+        }
+        // the group's first collision: its lowest lane with a hit
+        const unsigned hm_all = __ballot_sync(FULL, hk < 4);
+        const unsigned hm = G == 32 ? hm_all : (hm_all >> gbase) & ((1u << G) - 1u);
+        const int hl = hm ? __ffs(hm) - 1 : G;
+        const int src = gbase + (hm ? hl : 0);
+        const float t_hit = __shfl_sync(FULL, th, src);
+        const int k_hit = __shfl_sync(FULL, hk, src);
+        f3 rgb_hit = mk(0, 0, 0);
+        if (!ANY) rgb_hit = mk(__shfl_sync(FULL, rgbh.x, src), __shfl_sync(FULL, rgbh.y, src),
+                               __shfl_sync(FULL, rgbh.z, src));
+        const int64_t inext_g = G == 1 ? inext : (int64_t)(((uint64_t)__shfl_sync(FULL, (uint32_t)((uint64_t)inext >> 32), gbase + G - 1) << 32) |
+                                                           __shfl_sync(FULL, (uint32_t)inext, gbase + G - 1));
+        if (mode == 1) {
+            if (gl <= hl) vols += cnt;
+            if (hm) {
+                // collision in this brick: a path ray keeps it as the new bound and goes on with
+                // the next brick (only earlier samples can still win); an occlusion ray is done
+                r.hit = true;
+                r.hid = VOL_BIT | (uint32_t)(cb + 4 * hl + k_hit);
+                r.rgb = rgb_hit;
+                r.bound = t_hit;
+                mode = 2;
+                if (ANY) r.bi = W.nbricks;
+            } else {
+                r.i = inext_g;
+            }
+        }
+        if (mode == 2) {
+            if (r.bi < W.nbricks) {
+                ++r.bi;
+                march_begin_brick(W, r, dt);
+            }
+            if (r.bi >= W.nbricks) {
+                // ray finished: write the result (group leader)
+                if (gl == 0 && r.hit) {
+                    if (ANY) {
+                        A.Q.occl_in[idx].a.w = -1.0f;
+                    } else {
+                        PathRec *q = A.Q.path_in + idx;
+                        q->a.w = r.bound;
+                        q->b.w = __uint_as_float(r.hid);
+                        q->e.x = r.rgb.x; q->e.y = r.rgb.y; q->e.z = r.rgb.z;
+                    }
+                }
+                alive = false;
+            }
+        }
+    }
+    flush(&A.ctr->kc[ANY ? 1 : 0].vols, vols);
+}
+
+#ifndef DPR_MARCH_G
+#define DPR_MARCH_G 0  // 0: chosen per launch from the ray count
+#endif
+#ifndef DPR_MARCH_MINB
+#define DPR_MARCH_MINB 2
+#endif
+template <int G>
+__global__ void __launch_bounds__(256, DPR_MARCH_MINB) k_march_path(const __grid_constant__ StepArgs A) { march_groups<false, G>(A); }
+template <int G>
+__global__ void __launch_bounds__(256, DPR_MARCH_MINB) k_march_occl(const __grid_constant__ StepArgs A) { march_groups<true, G>(A); }
 
 // ---------------------------------------------------------------------------------------
 // Delta tracking (NEXT f4; readings R-DELTA, R-LOG), the alternative to the P10 march:
@@ -811,7 +1083,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                 occluded = delta_track<true>(A.W, RAY_O(S), RAY_D(S), S.tmax, F.dt, F.seed, p, s, depth,
                                              slot == 0 ? PUR_VOL_SHADOW : PUR_VOL_AO,
                                              slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
-            } else if (!occluded && A.W.nbricks > 0) {
+            } else if (!occluded && A.W.nbricks > 0 && n_in >= F.march_inline_min) {
                 const uint32_t p = __float_as_uint(r->b.w), meta = __float_as_uint(r->c.w);
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
                 for (int b = 0; b < A.W.nbricks && !occluded; ++b) {
@@ -838,7 +1110,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                                        rgb, tc.vols)) {
                     S.h.t = ti; S.h.id = VOL_BIT | kk; nrm = rgb; changed = true;
                 }
-            } else if (A.W.nbricks > 0) {
+            } else if (A.W.nbricks > 0 && n_in >= F.march_inline_min) {
                 const uint32_t p = __float_as_uint(r->c.w), meta = __float_as_uint(r->e.w);
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
                 for (int b = 0; b < A.W.nbricks; ++b) {
@@ -1169,11 +1441,65 @@ void launch_gen_primary(const StepArgs &a, int s0, int nsamp, int spw_max, cudaS
     int64_t total = per * (nsamp / spw);
     if (total > 0) k_gen_primary<<<nblk(total, 256), 256, 0, s>>>(a, s0, nsamp, spw, tw, th);
 }
-void launch_trace_path(const StepArgs &a, int grid, cudaStream_t s) {
-    k_trace_path<<<grid, TRACE_BLOCK, 0, s>>>(a);
+// The P10 march: with enough rays to give every lane of the GPU two, per lane inside the
+// trace kernels (all lanes of a warp march together, right after the traversal); with fewer
+// (long marches of few rays would serialise), in k_march_* with G lanes per ray.  Delta
+// tracking always runs inside the trace kernels.
+// Test override DPR_MARCH="<inline_min>[:G]" (e.g. "0": always inline; "1000000000:4":
+// always k_march_* with 4 lanes per ray).
+static int env_march_g() {
+    const char *e = getenv("DPR_MARCH");
+    const char *c = e ? strchr(e, ':') : nullptr;
+    return c ? atoi(c + 1) : 0;
 }
-void launch_trace_occl(const StepArgs &a, int grid, cudaStream_t s) {
+uint32_t march_inline_min(int nsm) {
+    if (const char *e = getenv("DPR_MARCH")) return (uint32_t)strtoul(e, nullptr, 10);
+    return DPR_WARP_MARCH ? (uint32_t)nsm * 1024u * 2u : 0u;
+}
+static bool use_warp_march(const StepArgs &a, uint32_t n) {
+    return a.W.nbricks > 0 && !(a.F.flags & DPR_FLAG_DELTA) && n < a.F.march_inline_min;
+}
+template <int G>
+static void launch_march(const StepArgs &a, bool any, uint32_t n, cudaStream_t s) {
+    static int grid[2] = {0, 0};
+    if (!grid[any]) {
+        int dev = 0, nsm = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (any) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_march_occl<G>, 256, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_march_path<G>, 256, 0);
+        grid[any] = nsm * std::max(1, occ);
+    }
+    // no more groups than rays
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(grid[any], ((int64_t)n * G + 255) / 256));
+    if (any) k_march_occl<G><<<g, 256, 0, s>>>(a);
+    else k_march_path<G><<<g, 256, 0, s>>>(a);
+}
+// G lanes per ray: enough rays to fill the GPU with one lane each -> 1, few rays (long
+// marches would serialise) -> up to a warp per ray
+static void launch_march_any(const StepArgs &a, bool any, uint32_t n, cudaStream_t s) {
+    int G = env_march_g() ? env_march_g() : DPR_MARCH_G;
+    if (G == 0) {  // smallest G in {1, 4, 16->32} with n * G >= march_inline_min
+        G = 1;
+        while (G < 32 && (int64_t)n * G < (int64_t)a.F.march_inline_min) G *= 4;
+        if (G > 32) G = 32;
+    }
+    if (G <= 1) launch_march<1>(a, any, n, s);
+    else if (G <= 4) launch_march<4>(a, any, n, s);
+    else if (G <= 8) launch_march<8>(a, any, n, s);
+    else launch_march<32>(a, any, n, s);
+}
+int launch_trace_path(const StepArgs &a, int grid, uint32_t n, cudaStream_t s) {
+    k_trace_path<<<grid, TRACE_BLOCK, 0, s>>>(a);
+    if (!use_warp_march(a, n)) return 1;
+    launch_march_any(a, false, n, s);
+    return 2;
+}
+int launch_trace_occl(const StepArgs &a, int grid, uint32_t n, cudaStream_t s) {
     k_trace_occl<<<grid, TRACE_BLOCK, 0, s>>>(a);
+    if (!use_warp_march(a, n)) return 1;
+    launch_march_any(a, true, n, s);
+    return 2;
 }
 void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s) {
     k_shade_path<<<grid, 256, 0, s>>>(a);

@@ -84,9 +84,17 @@ def _volume_scene(G, nbricks, nranks, alpha_max=0.6):
     return parts, float(h)
 
 
+MARCH_MODES = {"auto": None, "inline": "0", "group1": "1000000000:1", "group4": "1000000000:4",
+               "group32": "1000000000:32"}
+
+
+@pytest.mark.parametrize("march", list(MARCH_MODES))
 @pytest.mark.parametrize("nbricks,nranks", [(1, 1), (4, 1), (2, 2), (4, 4), (8, 8)])
-def test_volume_bricks(nbricks, nranks):
-    """P10 stochastic DVR + binary volume shadows + isotropic bounce, bricks per rank."""
+def test_volume_bricks(nbricks, nranks, march, monkeypatch):
+    """P10 stochastic DVR + binary volume shadows + isotropic bounce, bricks per rank; the
+    march inside the trace kernels (one lane per ray) and in k_march_* (G lanes per ray)."""
+    if MARCH_MODES[march] is not None:
+        monkeypatch.setenv("DPR_MARCH", MARCH_MODES[march])
     parts, h = _volume_scene(41, nbricks, nranks)
     W = H = 40
     cam = di.camera_basis((0.4, 0.7, 2.6), (0, 0, 0), (0, 1, 0), 40.0, W, H)
