@@ -453,9 +453,11 @@ int build_world(Dev *d) {
                 RET(ensure(d, d->b_arrive, sizeof(int) * (n - 1) + sizeof(int)));
                 int *other = P<int>(d->b_arrive);
                 CK(cudaMemsetAsync(other, 0xff, sizeof(int) * (n - 1), s));
-                launch_agglo(keys, n, P<float4>(d->b_slo), P<float4>(d->b_shi), P<int>(d->b_left), P<int>(d->b_right),
-                             P<int>(d->b_size), P<float4>(d->b_nlo), P<float4>(d->b_nhi), other, other + (n - 1), s);
-                launches++;
+                // the other radix-sort key buffer is free now: per-split prefix lengths
+                uint8_t *split = P<uint8_t>(d->b_keys[keys == P<uint64_t>(d->b_keys[0]) ? 1 : 0]);
+                launches += launch_agglo(keys, split, n, P<float4>(d->b_slo), P<float4>(d->b_shi), P<int>(d->b_left),
+                                         P<int>(d->b_right), P<int>(d->b_size), P<float4>(d->b_nlo),
+                                         P<float4>(d->b_nhi), other, other + (n - 1), s);
                 CK(cudaMemcpyAsync(&root_id, other + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
             } else {

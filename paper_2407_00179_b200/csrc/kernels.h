@@ -32,8 +32,10 @@ void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *
 void launch_refit(int64_t n, const int *left, const int *right, const int *parent,
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
                   cudaStream_t s);
-void launch_agglo(const uint64_t *keys, int64_t n, const float4 *slo, const float4 *shi, int *left, int *right,
-                  int *size, float4 *nlo, float4 *nhi, int *other, int *root_out, cudaStream_t s);
+// split_scratch: >= n-1 bytes (the unused radix-sort key buffer); returns kernels launched
+int launch_agglo(const uint64_t *keys, uint8_t *split_scratch, int64_t n, const float4 *slo, const float4 *shi,
+                 int *left, int *right, int *size, float4 *nlo, float4 *nhi, int *other, int *root_out,
+                 cudaStream_t s);
 void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
                          const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,
                          cudaStream_t s);

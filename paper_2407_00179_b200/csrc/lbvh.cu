@@ -369,9 +369,16 @@ __global__ void k_refit(int64_t n, const int *__restrict__ left, const int *__re
 // right child of internal node l-1; internal node p is the split between leaves p and p+1.
 // The first child to arrive at p deposits its outer range bound and leaves; the second
 // (acq_rel exchange) merges both boxes and continues.  The root is reported in *root_out.
-__global__ void k_agglo(const uint64_t *__restrict__ keys, int64_t n, const float4 *__restrict__ slo,
-                        const float4 *__restrict__ shi, int *left, int *right, int *size, float4 *nlo,
-                        float4 *nhi, int *other, int *root_out) {
+// split[i] = delta(i, i+1) (common-prefix length of adjacent sorted keys, index-augmented),
+// one byte per split: k_agglo reads two bytes per step instead of four 64-bit keys
+__global__ void k_split_delta(const uint64_t *__restrict__ keys, int64_t n, uint8_t *split) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n - 1) split[i] = (uint8_t)delta(keys, n, i, i + 1);
+}
+
+__global__ void k_agglo(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ split, int64_t n,
+                        const float4 *__restrict__ slo, const float4 *__restrict__ shi, int *left, int *right,
+                        int *size, float4 *nlo, float4 *nhi, int *other, int *root_out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int64_t l = i, r = i;
@@ -381,6 +388,7 @@ __global__ void k_agglo(const uint64_t *__restrict__ keys, int64_t n, const floa
         bool is_left;
         if (l == 0) is_left = true;
         else if (r == n - 1) is_left = false;
+        else if (split) is_left = __ldg(split + r) > __ldg(split + l - 1);
         else is_left = delta(keys, n, r, r + 1) > delta(keys, n, l - 1, l);
         const int64_t p = is_left ? r : l - 1;
         if (is_left) left[p] = cur;
@@ -505,13 +513,13 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
     }
     int slot_of[8];
     {
-        float cost[8][8];
+        // cost(i, slot) = +-dx +-dy +-dz by the slot's octant bits, evaluated on the fly (no
+        // 8x8 table in local memory)
+        float dc[8][3];
         for (int i = 0; i < nc; ++i) {
-            float dx = (lo[i][0] + hi[i][0]) - (nlo_[0] + nhi_[0]);
-            float dy = (lo[i][1] + hi[i][1]) - (nlo_[1] + nhi_[1]);
-            float dz = (lo[i][2] + hi[i][2]) - (nlo_[2] + nhi_[2]);
-            for (int sl = 0; sl < 8; ++sl)
-                cost[i][sl] = ((sl & 4) ? dx : -dx) + ((sl & 2) ? dy : -dy) + ((sl & 1) ? dz : -dz);
+            dc[i][0] = (lo[i][0] + hi[i][0]) - (nlo_[0] + nhi_[0]);
+            dc[i][1] = (lo[i][1] + hi[i][1]) - (nlo_[1] + nhi_[1]);
+            dc[i][2] = (lo[i][2] + hi[i][2]) - (nlo_[2] + nhi_[2]);
         }
         unsigned used_slots = 0, done_child = 0;
         for (int k = 0; k < nc; ++k) {
@@ -519,8 +527,12 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
             int bi = 0, bs = 0;
             for (int i = 0; i < nc; ++i) {
                 if (done_child >> i & 1) continue;
-                for (int sl = 0; sl < 8; ++sl)
-                    if (!(used_slots >> sl & 1) && cost[i][sl] > bc) { bc = cost[i][sl]; bi = i; bs = sl; }
+                const float dx = dc[i][0], dy = dc[i][1], dz = dc[i][2];
+#pragma unroll
+                for (int sl = 0; sl < 8; ++sl) {
+                    const float cst = ((sl & 4) ? dx : -dx) + ((sl & 2) ? dy : -dy) + ((sl & 1) ? dz : -dz);
+                    if (!(used_slots >> sl & 1) && cst > bc) { bc = cst; bi = i; bs = sl; }
+                }
             }
             slot_of[bi] = bs;
             used_slots |= 1u << bs;
@@ -753,9 +765,17 @@ void launch_refit(int64_t n, const int *left, const int *right, const int *paren
                   cudaStream_t s) {
     if (n > 1) k_refit<<<nblk(n, 256), 256, 0, s>>>(n, left, right, parent, slo, shi, nlo, nhi, arrive);
 }
-void launch_agglo(const uint64_t *keys, int64_t n, const float4 *slo, const float4 *shi, int *left, int *right,
-                  int *size, float4 *nlo, float4 *nhi, int *other, int *root_out, cudaStream_t s) {
-    if (n > 1) k_agglo<<<nblk(n, 256), 256, 0, s>>>(keys, n, slo, shi, left, right, size, nlo, nhi, other, root_out);
+#ifndef DPR_AGGLO_SPLIT
+#define DPR_AGGLO_SPLIT 1
+#endif
+int launch_agglo(const uint64_t *keys, uint8_t *split_scratch, int64_t n, const float4 *slo, const float4 *shi,
+                 int *left, int *right, int *size, float4 *nlo, float4 *nhi, int *other, int *root_out,
+                 cudaStream_t s) {
+    if (n <= 1) return 0;
+    uint8_t *split = DPR_AGGLO_SPLIT ? split_scratch : nullptr;
+    if (split) k_split_delta<<<nblk(n, 256), 256, 0, s>>>(keys, n, split);
+    k_agglo<<<nblk(n, 256), 256, 0, s>>>(keys, split, n, slo, shi, left, right, size, nlo, nhi, other, root_out);
+    return split ? 2 : 1;
 }
 void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
                          const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,
