@@ -159,6 +159,9 @@ constexpr int WSTACK = 32;       // node-group stack entries (wide BVH depth bou
 constexpr int COOP_PER_LANE = DPR_COOP_PER_LANE > DPR_COOP_PER_LANE_PATH ? DPR_COOP_PER_LANE
                                                                          : DPR_COOP_PER_LANE_PATH;  // list size
 constexpr int COOP_CAP_ANY = DPR_COOP_PER_LANE, COOP_CAP_PATH = DPR_COOP_PER_LANE_PATH;
+#ifndef DPR_ANY_REVERSE
+#define DPR_ANY_REVERSE 1
+#endif
 #ifndef DPR_INLINE_DIST
 #define DPR_INLINE_DIST 1
 #endif
@@ -245,7 +248,9 @@ struct TravState {
     int sp;
 };
 
-__device__ __forceinline__ void trav_init(TravState &S, f3 o, f3 d, float tmax, Hit h, int64_t nprims) {
+// rev = 7: children visited back to front (any-hit rays, DPR_ANY_REVERSE)
+__device__ __forceinline__ void trav_init(TravState &S, f3 o, f3 d, float tmax, Hit h, int64_t nprims,
+                                          uint32_t rev = 0) {
     S.tmax = tmax; S.h = h;
     const float tiny = 1e-20f;  // zero direction components -> finite reciprocal (box tests only)
     const f3 id3 = mk(1.0f / (fabsf(d.x) > tiny ? d.x : copysignf(tiny, d.x)),
@@ -260,8 +265,9 @@ __device__ __forceinline__ void trav_init(TravState &S, f3 o, f3 d, float tmax, 
     S.o = o; S.d = d; S.id3 = id3;
 #endif
     S.oct = (d.x < 0.0f ? 4u : 0u) | (d.y < 0.0f ? 2u : 0u) | (d.z < 0.0f ? 1u : 0u);
+    S.oct |= (S.oct ^ rev) << 3;  // bits 3..5: traversal order (slot s' = position ^ order)
     // virtual root group: one internal child (slot 0, imask 1) at index 0
-    S.ng = make_uint2(0u, nprims > 0 ? ((1u << S.oct) | (1u << 8)) : 0u);
+    S.ng = make_uint2(0u, nprims > 0 ? ((1u << (S.oct >> 3)) | (1u << 8)) : 0u);
     S.tb0 = S.tb1 = S.tb2 = 0;
     S.tm0 = S.tm1 = S.tm2 = 0;
     S.sp = 0;
@@ -304,7 +310,7 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         uint32_t hits = S.ng.y & 0xffu, pimask = S.ng.y >> 8;
         int sp_ = __ffs(hits) - 1;
         hits &= hits - 1;
-        int slot = sp_ ^ (int)S.oct;
+        int slot = sp_ ^ (int)(S.oct >> 3);
         int node = (int)S.ng.x + __popc(pimask & ((1u << slot) - 1u));
         if (hits) {
             if (S.sp < WSTACK) stack_push(stack, S.sp, make_uint2(S.ng.x, hits | (pimask << 8)));
@@ -363,9 +369,10 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         uint32_t ih = hitm & nimask;
         uint32_t lh = hitm & leafm;
         // internal hits into traversal order s' = slot ^ octant (bit permutation)
-        if (S.oct & 4u) ih = ((ih & 0x0fu) << 4) | ((ih & 0xf0u) >> 4);
-        if (S.oct & 2u) ih = ((ih & 0x33u) << 2) | ((ih & 0xccu) >> 2);
-        if (S.oct & 1u) ih = ((ih & 0x55u) << 1) | ((ih & 0xaau) >> 1);
+        const uint32_t ordm = S.oct >> 3;
+        if (ordm & 4u) ih = ((ih & 0x0fu) << 4) | ((ih & 0xf0u) >> 4);
+        if (ordm & 2u) ih = ((ih & 0x33u) << 2) | ((ih & 0xccu) >> 2);
+        if (ordm & 1u) ih = ((ih & 0x55u) << 1) | ((ih & 0xaau) >> 1);
         uint32_t ihits = ih, tmask = 0;
 #if DPR_LEAF_UNROLL
         // branch-free over the 8 slots (no divergence on the number of hit leaves)
@@ -1173,7 +1180,9 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                         const OcclRec *r = A.Q.occl_in + idx;
                         float4 a = __ldcg(&r->a), b = __ldcg(&r->b);
                         Hit h = {a.w, NO_HIT, -1};
-                        trav_init(S, xyz(a), xyz(b), a.w, h, A.W.nprims);
+                        // any-hit order (DPR_ANY_REVERSE): 1 back to front for all, 2 for bounded (AO) rays
+                        const bool rev = DPR_ANY_REVERSE == 1 || (DPR_ANY_REVERSE == 2 && a.w < INF);
+                        trav_init(S, xyz(a), xyz(b), a.w, h, A.W.nprims, rev ? 7u : 0u);
                     } else {
                         const PathRec *r = A.Q.path_in + idx;
                         float4 a = __ldcg(&r->a), b = __ldcg(&r->b);
