@@ -324,10 +324,12 @@ def run_gpu(args):
     avg_s = ms / max(n, 1) / 1000.0
     bytes_per_launch = b / max(n, 1)
     achieved = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
-    tr = profile_traffic()
+    # ncu figures of THIS workload's kernel (profiles/traffic.json is keyed by config, then
+    # kernel; an entry exists only where a --set full capture of that config was committed)
+    tr = (profile_traffic() or {}).get(args.config, {})
     traffic = None
     limiter = None
-    if tr and kname in tr:
+    if kname in tr:
         traffic = tr[kname].get("dram_bytes_per_launch")
         if tr[kname].get("issue_active_pct") is not None:
             # what ncu says actually limits the kernel (the touched-bytes roof is SURVEY 8(d)'s)
