@@ -240,10 +240,10 @@ __device__ __forceinline__ f3 iso_dir(uint64_t seed, uint32_t p, uint32_t s, uin
 // Leaf size bound of the wide-BVH collapse (binary subtrees with <= LEAF_MAX prims become
 // leaf children).
 #ifndef DPR_FILL_LEAVES
-#define DPR_FILL_LEAVES 0
+#define DPR_FILL_LEAVES 1
 #endif
 #ifndef DPR_LEAF_MAX
-#define DPR_LEAF_MAX 3
+#define DPR_LEAF_MAX 4
 #endif
 constexpr int LEAF_MAX = DPR_LEAF_MAX;  // <= 4 (2-bit count in the wide-node meta)
 
