@@ -619,8 +619,200 @@ __global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items,
     a.nodes[wnode] = nd;
 }
 
+// Register-resident collapse (default): the same wide node as k_collapse, but every per-child
+// array is indexed with compile-time indices (unrolled selects), so the child boxes, ids,
+// slot costs and quantised planes stay in registers instead of a 320-B local-memory frame
+// that thrashes L1 at full occupancy.  Internal children are queued in child order instead of
+// slot order (only the next level's item order changes, not the tree).
+__global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const int2 *__restrict__ items, int nitems,
+                                                    int2 *next) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nitems) return;
+    const int wnode = items[t].x, b = items[t].y;
+    int cid[8], c1[8];
+    float lo[8][3], hi[8][3];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        cid[i] = 0; c1[i] = 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { lo[i][c] = 0.0f; hi[i][c] = 0.0f; }
+    }
+    int nc;
+    if (b < 0) {  // single-prim world: the root holds one leaf
+        cid[0] = (int)(a.n - 1);
+        bin_child(a, cid[0], lo[0], hi[0], c1[0]);
+        nc = 1;
+    } else {
+        cid[0] = a.left[b]; bin_child(a, cid[0], lo[0], hi[0], c1[0]);
+        cid[1] = a.right[b]; bin_child(a, cid[1], lo[1], hi[1], c1[1]);
+        nc = 2;
+    }
+    // pass 0: open the largest-area internal child with > LEAF_MAX prims; pass 1
+    // (DPR_FILL_LEAVES): then the largest small subtree, while slots are free
+    for (int pass = 0; pass < (DPR_FILL_LEAVES ? 2 : 1); ++pass) {
+        while (nc < 8) {
+            int best = -1;
+            float ba = -1.0f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (i >= nc || cid[i] >= a.n - 1 || (pass == 0 && c1[i] <= LEAF_MAX)) continue;
+                const float ex = hi[i][0] - lo[i][0], ey = hi[i][1] - lo[i][1], ez = hi[i][2] - lo[i][2];
+                const float area = ex * ey + ey * ez + ez * ex;
+                if (area > ba) { ba = area; best = i; }
+            }
+            if (best < 0) break;
+            int c = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) if (i == best) c = cid[i];
+            const int l = a.left[c], r = a.right[c];
+            float llo[3], lhi[3], rlo[3], rhi[3];
+            int ls, rs;
+            bin_child(a, l, llo, lhi, ls);
+            bin_child(a, r, rlo, rhi, rs);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (i == best) {
+                    cid[i] = l; c1[i] = ls;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) { lo[i][k] = llo[k]; hi[i][k] = lhi[k]; }
+                }
+                if (i == nc) {
+                    cid[i] = r; c1[i] = rs;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) { lo[i][k] = rlo[k]; hi[i][k] = rhi[k]; }
+                }
+            }
+            nc++;
+        }
+    }
+    // node box
+    float nlo_[3], nhi_[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        nlo_[c] = lo[0][c]; nhi_[c] = hi[0][c];
+#pragma unroll
+        for (int i = 1; i < 8; ++i)
+            if (i < nc) { nlo_[c] = fminf(nlo_[c], lo[i][c]); nhi_[c] = fmaxf(nhi_[c], hi[i][c]); }
+    }
+    // octant slot assignment (greedy on dot(child centre - node centre, octant)), as k_collapse
+    int slot_of[8];
+    {
+        float dc[8][3];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            slot_of[i] = 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) dc[i][c] = (lo[i][c] + hi[i][c]) - (nlo_[c] + nhi_[c]);
+        }
+        unsigned used_slots = 0, done_child = 0;
+        for (int k = 0; k < nc; ++k) {
+            float bc = -3.4e38f;
+            int bi = 0, bs = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (i >= nc || (done_child >> i & 1)) continue;
+#pragma unroll
+                for (int sl = 0; sl < 8; ++sl) {
+                    const float cst = ((sl & 4) ? dc[i][0] : -dc[i][0]) + ((sl & 2) ? dc[i][1] : -dc[i][1]) +
+                                      ((sl & 1) ? dc[i][2] : -dc[i][2]);
+                    if (!(used_slots >> sl & 1) && cst > bc) { bc = cst; bi = i; bs = sl; }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) if (i == bi) slot_of[i] = bs;
+            used_slots |= 1u << bs;
+            done_child |= 1u << bi;
+        }
+    }
+    // internal vs leaf children, allocation
+    int n_int = 0, n_prims = 0;
+    unsigned imask = 0, lmask = 0;
+    bool leaf[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        leaf[i] = i < nc && (cid[i] >= a.n - 1 || c1[i] <= LEAF_MAX);
+        if (i >= nc) continue;
+        if (leaf[i]) { n_prims += c1[i]; lmask |= 1u << slot_of[i]; }
+        else { n_int++; imask |= 1u << slot_of[i]; }
+    }
+    const int child_base = n_int ? atomicAdd(&a.counters[1], n_int) : 0;
+    const int prim_base = atomicAdd(&a.counters[2], n_prims);
+    if (child_base + n_int > a.node_cap) { atomicOr(&a.counters[3], 1); return; }
+    // quantisation (outward), as k_collapse
+    float p[3];
+    int e[3];
+    double isc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        p[c] = nlo_[c];
+        const double ext = (double)nhi_[c] - (double)p[c];
+        int ee = -126;
+        if (ext > 0) {
+            int ex;
+            frexp(ext / 255.0, &ex);
+            ee = ex - 1;
+            while (ldexp(255.0, ee) < ext) ee++;
+            if (ee < -126) ee = -126;
+            if (ee > 127) ee = 127;
+        }
+        e[c] = ee;
+        isc[c] = ldexp(1.0, -ee);
+    }
+    uint32_t qw[6][2], mw[2] = {0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) qw[k][0] = qw[k][1] = 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (i >= nc) continue;
+        const int sl = slot_of[i];
+        const int sh = 8 * (sl & 3);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double ql = floor(((double)lo[i][c] - (double)p[c]) * isc[c]);
+            const double qh = ceil(((double)hi[i][c] - (double)p[c]) * isc[c]);
+            const uint32_t bl = (uint32_t)fmin(fmax(ql, 0.0), 255.0), bh = (uint32_t)fmin(fmax(qh, 0.0), 255.0);
+            if (sl < 4) { qw[c][0] |= bl << sh; qw[3 + c][0] |= bh << sh; }
+            else { qw[c][1] |= bl << sh; qw[3 + c][1] |= bh << sh; }
+        }
+        if (!leaf[i]) {
+            const int rank = __popc(imask & ((1u << sl) - 1u));
+            const int k = atomicAdd(&a.counters[0], 1);
+            next[k] = make_int2(child_base + rank, cid[i]);
+        } else {
+            // prims of the leaf children are laid out in slot order
+            int off = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j != i && leaf[j] && slot_of[j] < sl) off += c1[j];
+            const uint32_t m = 0x80u | ((uint32_t)(c1[i] - 1) << 5) | (uint32_t)off;
+            if (sl < 4) mw[0] |= m << sh; else mw[1] |= m << sh;
+            int st[8], sp = 0, k = 0;  // the (<= LEAF_MAX) prims of the binary subtree
+            st[sp++] = cid[i];
+            while (sp) {
+                const int x = st[--sp];
+                if (x >= a.n - 1) a.perm[prim_base + off + k++] = (uint32_t)(x - (a.n - 1));
+                else { st[sp++] = a.right[x]; st[sp++] = a.left[x]; }
+            }
+        }
+    }
+    WNode nd;
+    const uint32_t bits = (uint32_t)(e[0] + 127) | ((uint32_t)(e[1] + 127) << 8) | ((uint32_t)(e[2] + 127) << 16) | (imask << 24);
+    nd.w0 = make_float4(p[0], p[1], p[2], __uint_as_float(bits));
+    nd.w1 = make_uint4((uint32_t)child_base | ((lmask & 0xfu) << 28), (uint32_t)prim_base | ((lmask >> 4) << 28),
+                       mw[0], mw[1]);
+    nd.w2 = make_uint4(qw[0][0], qw[0][1], qw[1][0], qw[1][1]);
+    nd.w3 = make_uint4(qw[2][0], qw[2][1], qw[3][0], qw[3][1]);
+    nd.w4 = make_uint4(qw[4][0], qw[4][1], qw[5][0], qw[5][1]);
+    a.nodes[wnode] = nd;
+}
+
+#ifndef DPR_COLLAPSE_REG
+#define DPR_COLLAPSE_REG 1
+#endif
 void launch_collapse_level(const CollapseArgs &a, const int2 *items, int nitems, int2 *next, cudaStream_t s) {
-    if (nitems > 0) k_collapse<<<nblk(nitems, 128), 128, 0, s>>>(a, items, nitems, next);
+    if (nitems <= 0) return;
+    if (DPR_COLLAPSE_REG) k_collapse_r<<<nblk(nitems, 128), 128, 0, s>>>(a, items, nitems, next);
+    else k_collapse<<<nblk(nitems, 128), 128, 0, s>>>(a, items, nitems, next);
 }
 
 // prims_out[i] = prims_in[perm[i]] (3 float4 each): one thread per float4, coalesced writes.
