@@ -288,6 +288,74 @@ k_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, ui
     }
 }
 
+// Coalesced variant (default): the tile is first ranked into digit order in shared memory
+// (stable: item order within a digit is kept), then written out digit run by digit run, so
+// consecutive threads store to consecutive addresses of a bucket instead of 256 scattered
+// buckets per warp store.
+__global__ void __launch_bounds__(RS_THREADS)
+k_scatter_c(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *kout,
+            uint32_t *vout, int64_t n, int shift, const uint32_t *__restrict__ tile_off, int ntiles,
+            const uint32_t *__restrict__ digit_tot) {
+    __shared__ uint32_t wcnt[RS_THREADS / 32][256];
+    __shared__ uint32_t goff[256], lstart[256];
+    __shared__ uint16_t sidx[RS_TILE];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    {  // global exclusive offset of each digit for this tile, and the tile's local digit starts
+        const uint32_t v = digit_tot[threadIdx.x];
+        const uint32_t mine = tile_off[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+        const uint32_t cnt = (blockIdx.x + 1 < (unsigned)ntiles ? tile_off[(int64_t)threadIdx.x * ntiles + blockIdx.x + 1] : v) - mine;
+        uint32_t x = v, y = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t xs = __shfl_up_sync(0xffffffffu, x, o), ys = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) { x += xs; y += ys; }
+        }
+        if (lane == 31) { wcnt[0][warp] = x; wcnt[1][warp] = y; }
+        __syncthreads();
+        uint32_t wp = 0, wl = 0;
+        for (int w = 0; w < warp; ++w) { wp += wcnt[0][w]; wl += wcnt[1][w]; }
+        goff[threadIdx.x] = wp + x - v + mine;
+        lstart[threadIdx.x] = wl + y - cnt;
+        __syncthreads();
+    }
+    uint32_t run = 0;  // thread = digit: items of this digit ranked so far
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        for (int w = 0; w < RS_THREADS / 32; ++w) wcnt[w][threadIdx.x] = 0;
+        __syncthreads();
+        const int64_t i = base + j * RS_THREADS + threadIdx.x;
+        const bool valid = i < n;
+        const uint64_t k = valid ? kin[i] : 0;
+        const int d = valid ? (int)((k >> shift) & 255) : 256 + lane;  // invalid lanes: unique groups
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rank = __popc(peers & lt);
+        if (valid && rank == 0) wcnt[warp][d] = __popc(peers);
+        __syncthreads();
+        {  // thread = digit: prefix over warps (continuing the previous rounds)
+            uint32_t r = run;
+            for (int w = 0; w < RS_THREADS / 32; ++w) {
+                const uint32_t c = wcnt[w][threadIdx.x];
+                wcnt[w][threadIdx.x] = r;
+                r += c;
+            }
+            run = r;
+        }
+        __syncthreads();
+        if (valid) sidx[lstart[d] + wcnt[warp][d] + rank] = (uint16_t)(j * RS_THREADS + threadIdx.x);
+        __syncthreads();  // wcnt is cleared at the top of the next round
+    }
+    __syncthreads();
+    const int count = (int)min((int64_t)RS_TILE, n - base);
+    for (int i = threadIdx.x; i < count; i += RS_THREADS) {
+        const int64_t gi = base + sidx[i];
+        const uint64_t k = kin[gi];
+        const int d = (int)((k >> shift) & 255);
+        const uint32_t pos = goff[d] + (uint32_t)(i - (int)lstart[d]);
+        kout[pos] = k;
+        vout[pos] = vin[gi];
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // Karras 2012 hierarchy.  Internal nodes 0..n-2; child c < n-1 -> internal, else leaf
 // (c-(n-1)) in sorted order.
@@ -945,7 +1013,11 @@ void launch_radix_pass(const uint64_t *kin, const uint32_t *vin, uint64_t *kout,
     uint32_t *digit_tot = tile_hist + (int64_t)256 * ntiles;  // 256 extra words
     k_tile_hist<<<ntiles, RS_THREADS, 0, s>>>(kin, n, shift, tile_hist, ntiles);
     k_scan_digits<<<256, 1024, 0, s>>>(tile_hist, ntiles, digit_tot);
-    k_scatter<<<ntiles, RS_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, tile_hist, ntiles, digit_tot);
+#ifndef DPR_SCATTER_COALESCED
+#define DPR_SCATTER_COALESCED 1
+#endif
+    if (DPR_SCATTER_COALESCED) k_scatter_c<<<ntiles, RS_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, tile_hist, ntiles, digit_tot);
+    else k_scatter<<<ntiles, RS_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, tile_hist, ntiles, digit_tot);
     *launches += 3;
 }
 void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
