@@ -90,7 +90,9 @@ __device__ __forceinline__ uint32_t block_append(bool want, int dest, uint32_t *
         if (lane == leader) off = atomicAdd(&s_cnt[dest], (uint32_t)__popc(peers));
         off = __shfl_sync(peers, off, leader) + __popc(peers & lanemask_lt());
     }
-    __syncthreads();
+    // the first barrier also tells whether any thread of the block appends (block-uniform
+    // early exit: nothing was added to s_cnt)
+    if (!__syncthreads_or(want)) return 0xffffffffu;
     if ((int)threadIdx.x < nranks) {
         uint32_t c = s_cnt[threadIdx.x];
         uint32_t b = 0;
@@ -1317,8 +1319,7 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
         else if (active) next = next_candidate(A.R, self, o, d, INF, bt);
         bool fwd = active && next >= 0;
         uint32_t pos = 0xffffffffu;
-        if (__syncthreads_or(fwd))
-            pos = block_append(fwd, next, cnt_path, A.Q.path_cap, &A.ctr->overflow, A.ctr->S[K_PATH],
+        pos = block_append(fwd, next, cnt_path, A.Q.path_cap, &A.ctr->overflow, A.ctr->S[K_PATH],
                                self, N, s_cnt, s_base, A.Q.fused);
         if (fwd && pos != 0xffffffffu) {
             PathRec *dst = A.Q.path_out[next] + pos;
@@ -1403,7 +1404,6 @@ __global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid
                     if (A.occl) atomicOr(A.occl + ((int64_t)s * F.max_depth + depth) * F.P + p, 1u << slot);
                 }
             }
-            if (!__syncthreads_or(app)) continue;
             if (is_path) {
                 uint32_t q = block_append(app, first, cnt_path, A.Q.path_cap, &A.ctr->overflow,
                                           A.ctr->S[K_PATH], self, N, s_cnt, s_base, A.Q.fused);
@@ -1479,8 +1479,7 @@ __global__ void __launch_bounds__(256) k_resolve_occl(const __grid_constant__ St
         bool fwd = active && next >= 0;
         warp_count(fwd, (slot == 0 ? K_SHADOW : K_AO) * DPR_MAX_RANKS + next, &A.ctr->S[0][0]);
         uint32_t pos = 0xffffffffu;
-        if (__syncthreads_or(fwd))
-            pos = block_append(fwd, next, cnt_occl, A.Q.occl_cap, &A.ctr->overflow, nullptr, self, N,
+        pos = block_append(fwd, next, cnt_occl, A.Q.occl_cap, &A.ctr->overflow, nullptr, self, N,
                                s_cnt, s_base, A.Q.fused);
         if (fwd && pos != 0xffffffffu) {
             OcclRec *dst = A.Q.occl_out[next] + pos;
