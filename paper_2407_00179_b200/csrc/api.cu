@@ -404,6 +404,7 @@ int build_world(Dev *d) {
                             P<float4>(d->b_bhi), P<float4>(d->b_slo), P<float4>(d->b_shi), s);
         launches++;
         int root_id = 0;
+        const int *root_dev = nullptr;  // device copy of the root id (agglomerative builder)
         if (n > 1) {
             RET(ensure(d, d->b_left, sizeof(int) * (n - 1)));
             RET(ensure(d, d->b_right, sizeof(int) * (n - 1)));
@@ -458,8 +459,7 @@ int build_world(Dev *d) {
                 launches += launch_agglo(keys, split, n, P<float4>(d->b_slo), P<float4>(d->b_shi), P<int>(d->b_left),
                                          P<int>(d->b_right), P<int>(d->b_size), P<float4>(d->b_nlo),
                                          P<float4>(d->b_nhi), other, other + (n - 1), s);
-                CK(cudaMemcpyAsync(&root_id, other + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, s));
-                CK(cudaStreamSynchronize(s));
+                root_dev = other + (n - 1);  // read by the first collapse level on the device
             } else {
                 // Karras 2012 LBVH + bottom-up refit
                 RET(ensure(d, d->b_rlo, sizeof(int) * (n - 1)));
@@ -482,28 +482,38 @@ int build_world(Dev *d) {
         RET(ensure(d, d->b_witems[0], sizeof(int2) * node_cap));
         RET(ensure(d, d->b_witems[1], sizeof(int2) * node_cap));
         RET(ensure(d, d->b_wcnt, sizeof(int) * 4));
-        int h_cnt[4] = {0, 1, 0, 0};
+        // levels are launched in batches without a host round trip: each level kernel reads its
+        // item count from device memory (lvl[L]) and appends the next level's (lvl[L+1])
+        constexpr int MAXL = 120, BATCH = 4;
+        RET(ensure(d, d->b_wcnt, sizeof(int) * (4 + MAXL + BATCH + 1)));
+        int *cnt = P<int>(d->b_wcnt), *lvl = cnt + 4;
+        CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (4 + MAXL + BATCH + 1), s));
+        int h_init[5] = {0, 1, 0, 0, 1};  // counters {-, nodes = 1 (root), prims, overflow}, lvl[0] = 1
+        CK(cudaMemcpyAsync(cnt, h_init, sizeof(h_init), cudaMemcpyHostToDevice, s));
         int2 root = make_int2(0, n > 1 ? root_id : -1);
-        CK(cudaMemcpyAsync(d->b_wcnt.p, h_cnt, sizeof(h_cnt), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(d->b_witems[0].p, &root, sizeof(root), cudaMemcpyHostToDevice, s));
+        if (n > 1 && root_dev)  // agglomerative builder: the root id stays on the device
+            CK(cudaMemcpyAsync(&P<int2>(d->b_witems[0])->y, root_dev, sizeof(int), cudaMemcpyDeviceToDevice, s));
         CollapseArgs ca;
         ca.n = n; ca.left = P<int>(d->b_left); ca.right = P<int>(d->b_right); ca.size = P<int>(d->b_size);
         ca.nlo = P<float4>(d->b_nlo); ca.nhi = P<float4>(d->b_nhi);
         ca.slo = P<float4>(d->b_slo); ca.shi = P<float4>(d->b_shi);
-        ca.perm = P<uint32_t>(d->b_wperm); ca.nodes = P<WNode>(d->b_wnodes); ca.counters = P<int>(d->b_wcnt);
+        ca.perm = P<uint32_t>(d->b_wperm); ca.nodes = P<WNode>(d->b_wnodes); ca.counters = cnt;
         ca.node_cap = node_cap;
-        int nitems = 1, cur_items = 0, levels = 0;
-        while (nitems > 0) {
-            int zero = 0;
-            CK(cudaMemcpyAsync(P<int>(d->b_wcnt), &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-            launch_collapse_level(ca, P<int2>(d->b_witems[cur_items]), nitems, P<int2>(d->b_witems[cur_items ^ 1]), s);
-            launches++;
-            levels++;
-            CK(cudaMemcpyAsync(h_cnt, d->b_wcnt.p, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
+        int h_cnt[4 + MAXL + BATCH + 1];
+        int levels = -1;
+        for (int L = 0; levels < 0; L += BATCH) {
+            if (L >= MAXL) return fail(DPR_ERR_STATE, "wide BVH deeper than the collapse level limit");
+            for (int k = L; k < L + BATCH; ++k) {
+                launch_collapse_level(ca, P<int2>(d->b_witems[k & 1]), lvl + k, P<int2>(d->b_witems[(k + 1) & 1]),
+                                      lvl + k + 1, s);
+                launches++;
+            }
+            CK(cudaMemcpyAsync(h_cnt, cnt, sizeof(int) * (4 + L + BATCH + 1), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             if (h_cnt[3]) return fail(DPR_ERR_STATE, "wide BVH node capacity exceeded");
-            nitems = h_cnt[0];
-            cur_items ^= 1;
+            for (int k = L; k <= L + BATCH; ++k)
+                if (h_cnt[4 + k] == 0) { levels = k; break; }
         }
         if (h_cnt[2] != n) return fail(DPR_ERR_STATE, "wide BVH collapse lost primitives");
         RET(ensure(d, d->b_inv, sizeof(uint32_t) * n));

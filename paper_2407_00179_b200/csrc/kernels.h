@@ -45,10 +45,12 @@ struct CollapseArgs {
     const float4 *nlo, *nhi, *slo, *shi;
     uint32_t *perm;  // per-wide-node contiguous prim order: perm[dst] = sorted prim index
     WNode *nodes;
-    int *counters;
+    int *counters;  // [1] wide nodes allocated, [2] prims placed, [3] capacity overflow
     int node_cap;
 };
-void launch_collapse_level(const CollapseArgs &a, const int2 *items, int nitems, int2 *next, cudaStream_t s);
+// one BFS level of the collapse: *cnt_in items (device memory) -> next, appending to *cnt_out
+void launch_collapse_level(const CollapseArgs &a, const int2 *items, const int *cnt_in, int2 *next, int *cnt_out,
+                           cudaStream_t s);
 void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t *sortperm, int64_t n,
                           float4 *out, uint32_t *inv, cudaStream_t s);
 // ---- ploc.cu: PLOC binary builder (Meister & Bittner 2018) ------------------------------

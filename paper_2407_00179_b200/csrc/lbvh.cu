@@ -503,7 +503,7 @@ __global__ void k_gather_prims(const float4 *__restrict__ in, const uint32_t *__
 
 // ---------------------------------------------------------------------------------------
 // Collapse of the binary LBVH into compressed 8-wide nodes (WNode, common.cuh), one BFS
-// level per launch: each thread turns one binary subtree root into one wide node by
+// level per launch: each item turns one binary subtree root into one wide node by
 // repeatedly opening its largest-area child that is still an internal node with more
 // than LEAF_MAX prims, until 8 children or nothing left to open.  Leaf children's prims
 // are copied contiguously per wide node (prim_base + offset, offset < 32).
@@ -522,180 +522,16 @@ __device__ __forceinline__ void bin_child(const CollapseArgs &a, int id, float l
     hi[0] = pad_hi(h.x); hi[1] = pad_hi(h.y); hi[2] = pad_hi(h.z);
 }
 
-__global__ void k_collapse(const CollapseArgs a, const int2 *__restrict__ items, int nitems, int2 *next) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nitems) return;
-    const int wnode = items[t].x, b = items[t].y;
-    int cid[8], c1[8];  // c1 = subtree prim count
-    float lo[8][3], hi[8][3];
-    int nc = 0;
-    if (b < 0) {  // single-prim world: the root holds one leaf
-        cid[0] = (int)(a.n - 1);
-        bin_child(a, cid[0], lo[0], hi[0], c1[0]);
-        nc = 1;
-    } else {
-        cid[0] = a.left[b]; bin_child(a, cid[0], lo[0], hi[0], c1[0]);
-        cid[1] = a.right[b]; bin_child(a, cid[1], lo[1], hi[1], c1[1]);
-        nc = 2;
-    }
-    while (nc < 8) {
-        int best = -1;
-        float ba = -1.0f;
-        for (int i = 0; i < nc; ++i) {
-            if (cid[i] >= a.n - 1 || c1[i] <= LEAF_MAX) continue;
-            float ex = hi[i][0] - lo[i][0], ey = hi[i][1] - lo[i][1], ez = hi[i][2] - lo[i][2];
-            float area = ex * ey + ey * ez + ez * ex;
-            if (area > ba) { ba = area; best = i; }
-        }
-        if (best < 0) break;
-        int c = cid[best];
-        cid[best] = a.left[c]; bin_child(a, cid[best], lo[best], hi[best], c1[best]);
-        cid[nc] = a.right[c]; bin_child(a, cid[nc], lo[nc], hi[nc], c1[nc]);
-        nc++;
-    }
-#if DPR_FILL_LEAVES
-    // slots still free and only small subtrees (<= LEAF_MAX prims) left: split them further
-    // (largest area first) so that their prims get their own boxes instead of being tested
-    // together; the tree does not get deeper
-    while (nc < 8) {
-        int best = -1;
-        float ba = -1.0f;
-        for (int i = 0; i < nc; ++i) {
-            if (cid[i] >= a.n - 1) continue;
-            float ex = hi[i][0] - lo[i][0], ey = hi[i][1] - lo[i][1], ez = hi[i][2] - lo[i][2];
-            float area = ex * ey + ey * ez + ez * ex;
-            if (area > ba) { ba = area; best = i; }
-        }
-        if (best < 0) break;
-        int c = cid[best];
-        cid[best] = a.left[c]; bin_child(a, cid[best], lo[best], hi[best], c1[best]);
-        cid[nc] = a.right[c]; bin_child(a, cid[nc], lo[nc], hi[nc], c1[nc]);
-        nc++;
-    }
-#endif
-    // node box and octant slot assignment (greedy on dot(child centre - node centre, octant))
-    float nlo_[3], nhi_[3];
-    for (int c = 0; c < 3; ++c) {
-        nlo_[c] = lo[0][c]; nhi_[c] = hi[0][c];
-        for (int i = 1; i < nc; ++i) { nlo_[c] = fminf(nlo_[c], lo[i][c]); nhi_[c] = fmaxf(nhi_[c], hi[i][c]); }
-    }
-    int slot_of[8];
-    {
-        // cost(i, slot) = +-dx +-dy +-dz by the slot's octant bits, evaluated on the fly (no
-        // 8x8 table in local memory)
-        float dc[8][3];
-        for (int i = 0; i < nc; ++i) {
-            dc[i][0] = (lo[i][0] + hi[i][0]) - (nlo_[0] + nhi_[0]);
-            dc[i][1] = (lo[i][1] + hi[i][1]) - (nlo_[1] + nhi_[1]);
-            dc[i][2] = (lo[i][2] + hi[i][2]) - (nlo_[2] + nhi_[2]);
-        }
-        unsigned used_slots = 0, done_child = 0;
-        for (int k = 0; k < nc; ++k) {
-            float bc = -3.4e38f;
-            int bi = 0, bs = 0;
-            for (int i = 0; i < nc; ++i) {
-                if (done_child >> i & 1) continue;
-                const float dx = dc[i][0], dy = dc[i][1], dz = dc[i][2];
-#pragma unroll
-                for (int sl = 0; sl < 8; ++sl) {
-                    const float cst = ((sl & 4) ? dx : -dx) + ((sl & 2) ? dy : -dy) + ((sl & 1) ? dz : -dz);
-                    if (!(used_slots >> sl & 1) && cst > bc) { bc = cst; bi = i; bs = sl; }
-                }
-            }
-            slot_of[bi] = bs;
-            used_slots |= 1u << bs;
-            done_child |= 1u << bi;
-        }
-    }
-    // internal vs leaf children, allocation
-    int n_int = 0, n_prims = 0;
-    unsigned imask = 0;
-    for (int i = 0; i < nc; ++i) {
-        bool leaf = cid[i] >= a.n - 1 || c1[i] <= LEAF_MAX;
-        if (leaf) n_prims += c1[i];
-        else { n_int++; imask |= 1u << slot_of[i]; }
-    }
-    int child_base = n_int ? atomicAdd(&a.counters[1], n_int) : 0;
-    int prim_base = atomicAdd(&a.counters[2], n_prims);
-    if (child_base + n_int > a.node_cap) { atomicOr(&a.counters[3], 1); return; }
-    // quantisation (outward): smallest e with 255 * 2^e >= extent (frexp, no log2); the
-    // per-child planes below multiply by the exact power-of-two reciprocal (no division)
-    float p[3];
-    int e[3];
-    double isc[3];
-    for (int c = 0; c < 3; ++c) {
-        p[c] = nlo_[c];
-        double ext = (double)nhi_[c] - (double)p[c];  // exact (difference of two floats)
-        int ee = -126;
-        if (ext > 0) {
-            int ex;
-            frexp(ext / 255.0, &ex);  // ext/255 in [2^(ex-1), 2^ex)
-            ee = ex - 1;
-            while (ldexp(255.0, ee) < ext) ee++;
-            if (ee < -126) ee = -126;
-            if (ee > 127) ee = 127;
-        }
-        e[c] = ee;
-        isc[c] = ldexp(1.0, -ee);
-    }
-    uint8_t meta[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint8_t q[6][8];
-    for (int k = 0; k < 6; ++k) for (int sl = 0; sl < 8; ++sl) q[k][sl] = 0;
-    int off = 0;
-    // slot-ordered traversal so internal children are stored in slot order
-    for (int sl = 0; sl < 8; ++sl) {
-        int i = -1;
-        for (int j = 0; j < nc; ++j) if (slot_of[j] == sl) i = j;
-        if (i < 0) continue;
-        for (int c = 0; c < 3; ++c) {
-            double ql = floor(((double)lo[i][c] - (double)p[c]) * isc[c]);
-            double qh = ceil(((double)hi[i][c] - (double)p[c]) * isc[c]);
-            q[c][sl] = (uint8_t)fmin(fmax(ql, 0.0), 255.0);
-            q[3 + c][sl] = (uint8_t)fmin(fmax(qh, 0.0), 255.0);
-        }
-        if (imask >> sl & 1) {
-            int rank = __popc(imask & ((1u << sl) - 1));
-            int k = atomicAdd(&a.counters[0], 1);
-            next[k] = make_int2(child_base + rank, cid[i]);
-        } else {
-            int cnt = c1[i];
-            meta[sl] = (uint8_t)(0x80 | ((cnt - 1) << 5) | off);
-            int st[8], sp = 0, k = 0;  // collect the (<= LEAF_MAX) prims of the binary subtree
-            st[sp++] = cid[i];
-            while (sp) {
-                int x = st[--sp];
-                if (x >= a.n - 1) a.perm[prim_base + off + k++] = (uint32_t)(x - (a.n - 1));
-                else { st[sp++] = a.right[x]; st[sp++] = a.left[x]; }
-            }
-            off += cnt;
-        }
-    }
-    auto pack4 = [](const uint8_t *v) {
-        return (uint32_t)v[0] | ((uint32_t)v[1] << 8) | ((uint32_t)v[2] << 16) | ((uint32_t)v[3] << 24);
-    };
-    WNode nd;
-    uint32_t bits = (uint32_t)(e[0] + 127) | ((uint32_t)(e[1] + 127) << 8) | ((uint32_t)(e[2] + 127) << 16) | (imask << 24);
-    nd.w0 = make_float4(p[0], p[1], p[2], __uint_as_float(bits));
-    // leaf-slot mask in the spare top nibbles (child_base, prim_base < 2^28)
-    uint32_t lmask = 0;
-    for (int sl = 0; sl < 8; ++sl) lmask |= (meta[sl] != 0 ? 1u : 0u) << sl;
-    nd.w1 = make_uint4((uint32_t)child_base | ((lmask & 0xfu) << 28), (uint32_t)prim_base | ((lmask >> 4) << 28),
-                       pack4(meta), pack4(meta + 4));
-    nd.w2 = make_uint4(pack4(q[0]), pack4(q[0] + 4), pack4(q[1]), pack4(q[1] + 4));
-    nd.w3 = make_uint4(pack4(q[2]), pack4(q[2] + 4), pack4(q[3]), pack4(q[3] + 4));
-    nd.w4 = make_uint4(pack4(q[4]), pack4(q[4] + 4), pack4(q[5]), pack4(q[5] + 4));
-    a.nodes[wnode] = nd;
-}
-
-// Register-resident collapse (default): the same wide node as k_collapse, but every per-child
-// array is indexed with compile-time indices (unrolled selects), so the child boxes, ids,
-// slot costs and quantised planes stay in registers instead of a 320-B local-memory frame
-// that thrashes L1 at full occupancy.  Internal children are queued in child order instead of
-// slot order (only the next level's item order changes, not the tree).
-__global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const int2 *__restrict__ items, int nitems,
-                                                    int2 *next) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nitems) return;
+// Every per-child array is indexed with compile-time indices (unrolled selects), so the child
+// boxes, ids, slot costs and quantised planes stay in registers (an earlier version indexed
+// them dynamically: a 320-416 B local-memory frame that thrashed L1 at full occupancy).
+// Persistent grid-stride loop over the level's items; the item count is read from device
+// memory (cnt_in) and the next level's items are appended (cnt_out), so several levels are
+// launched back to back without a host round trip.
+__global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const int2 *__restrict__ items,
+                                                    const int *__restrict__ cnt_in, int2 *next, int *cnt_out) {
+  const int nitems = *cnt_in;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nitems; t += gridDim.x * blockDim.x) {
     const int wnode = items[t].x, b = items[t].y;
     int cid[8], c1[8];
     float lo[8][3], hi[8][3];
@@ -762,7 +598,8 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
         for (int i = 1; i < 8; ++i)
             if (i < nc) { nlo_[c] = fminf(nlo_[c], lo[i][c]); nhi_[c] = fmaxf(nhi_[c], hi[i][c]); }
     }
-    // octant slot assignment (greedy on dot(child centre - node centre, octant)), as k_collapse
+    // octant slot assignment: greedy on cost(child, slot) = dot(child centre - node centre,
+    // octant signs of the slot), highest first
     int slot_of[8];
     {
         float dc[8][3];
@@ -806,7 +643,8 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
     const int child_base = n_int ? atomicAdd(&a.counters[1], n_int) : 0;
     const int prim_base = atomicAdd(&a.counters[2], n_prims);
     if (child_base + n_int > a.node_cap) { atomicOr(&a.counters[3], 1); return; }
-    // quantisation (outward), as k_collapse
+    // quantisation (outward): smallest e with 255 * 2^e >= extent (frexp, no log2); the
+    // per-child planes below multiply by the exact power-of-two reciprocal (no division)
     float p[3];
     int e[3];
     double isc[3];
@@ -844,7 +682,7 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
         }
         if (!leaf[i]) {
             const int rank = __popc(imask & ((1u << sl) - 1u));
-            const int k = atomicAdd(&a.counters[0], 1);
+            const int k = atomicAdd(cnt_out, 1);
             next[k] = make_int2(child_base + rank, cid[i]);
         } else {
             // prims of the leaf children are laid out in slot order
@@ -872,15 +710,26 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
     nd.w3 = make_uint4(qw[2][0], qw[2][1], qw[3][0], qw[3][1]);
     nd.w4 = make_uint4(qw[4][0], qw[4][1], qw[5][0], qw[5][1]);
     a.nodes[wnode] = nd;
+  }
 }
 
-#ifndef DPR_COLLAPSE_REG
-#define DPR_COLLAPSE_REG 1
+#ifndef DPR_COLLAPSE_GRID
+#define DPR_COLLAPSE_GRID 16  // resident-grid multiple of the persistent collapse launch
 #endif
-void launch_collapse_level(const CollapseArgs &a, const int2 *items, int nitems, int2 *next, cudaStream_t s) {
-    if (nitems <= 0) return;
-    if (DPR_COLLAPSE_REG) k_collapse_r<<<nblk(nitems, 128), 128, 0, s>>>(a, items, nitems, next);
-    else k_collapse<<<nblk(nitems, 128), 128, 0, s>>>(a, items, nitems, next);
+int collapse_grid() {
+    static int g = 0;
+    if (!g) {
+        int dev = 0, nsm = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collapse_r, 128, 0);
+        g = nsm * std::max(1, occ) * DPR_COLLAPSE_GRID;
+    }
+    return g;
+}
+void launch_collapse_level(const CollapseArgs &a, const int2 *items, const int *cnt_in, int2 *next, int *cnt_out,
+                           cudaStream_t s) {
+    k_collapse_r<<<collapse_grid(), 128, 0, s>>>(a, items, cnt_in, next, cnt_out);
 }
 
 // prims_out[i] = prims_in[perm[i]] (3 float4 each): one thread per float4, coalesced writes.

@@ -167,19 +167,8 @@ constexpr int COOP_CAP_ANY = DPR_COOP_PER_LANE, COOP_CAP_PATH = DPR_COOP_PER_LAN
 #ifndef DPR_INLINE_DIST
 #define DPR_INLINE_DIST 1
 #endif
-#ifndef DPR_INLINE_CHUNK
-#define DPR_INLINE_CHUNK 0
-#endif
-#if DPR_INLINE_CHUNK
-#define MARCH_INLINE march_brick4
-#else
-#define MARCH_INLINE march_brick
-#endif
 #ifndef DPR_WARP_MARCH
 #define DPR_WARP_MARCH 1
-#endif
-#ifndef DPR_LEAF_UNROLL
-#define DPR_LEAF_UNROLL 0
 #endif
 #ifndef DPR_P1_EXIT_ANY
 #define DPR_P1_EXIT_ANY 8
@@ -376,16 +365,6 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         if (ordm & 2u) ih = ((ih & 0x33u) << 2) | ((ih & 0xccu) >> 2);
         if (ordm & 1u) ih = ((ih & 0x55u) << 1) | ((ih & 0xaau) >> 1);
         uint32_t ihits = ih, tmask = 0;
-#if DPR_LEAF_UNROLL
-        // branch-free over the 8 slots (no divergence on the number of hit leaves)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const uint32_t meta = __byte_perm(c < 4 ? w1.z : w1.w, 0u, (uint32_t)(c & 3) | 0x4440u);
-            const uint32_t r = ((2u << ((meta >> 5) & 3u)) - 1u) << (meta & 31u);
-            tmask |= (lh >> c) & 1u ? r : 0u;
-        }
-        lh = 0;
-#endif
         while (lh) {
             const int c = __ffs(lh) - 1;
             lh &= lh - 1;
@@ -621,99 +600,6 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
             if (!ANY) rgb_out = rgb;
             return true;
         }
-    }
-    return false;
-}
-
-// Per-lane P10 march in chunks of 4 samples (one Philox block, the loads of the 4 samples in
-// flight together) with distance-field jumps: the same samples and decisions as march_brick.
-template <bool ANY>
-__device__ __forceinline__ bool march_brick4(const BrickDev &B, f3 o, f3 d, float tmax, float bound, float dt,
-                                             uint64_t seed, uint32_t p, uint32_t s, uint32_t depth,
-                                             uint32_t purpose, uint32_t subhi, float &t_out, uint32_t &i_out,
-                                             f3 &rgb_out, uint32_t &nsamples) {
-    float plo[3], phi[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) { plo[c] = B.box_lo[c] - B.h[c]; phi[c] = B.box_hi[c] + B.h[c]; }
-    float t0, t1;
-    if (!slab(plo, phi, o, d, tmax, t0, t1)) return false;
-    float a = floorf(t0 / dt - 0.5f);
-    float bb = ceilf(t1 / dt);
-    if (bb > 1.0e9f) bb = 1.0e9f;
-    int64_t i = (int64_t)a - 1;
-    if (i < 0) i = 0;
-    const int64_t i1 = (int64_t)bb + 1;
-    const int nx = B.hi[0] - B.lo[0] + 1, ny = B.hi[1] - B.lo[1] + 1;
-    const int64_t sy = nx, sz = (int64_t)nx * ny;
-    while (i <= i1) {
-        if (!(sample_t(i, dt) < bound)) return false;
-        const int64_t cb = i & ~(int64_t)3;
-        bool val[4], own3 = false;
-        int dist3 = 0, mc3[3] = {0, 0, 0};
-        float tk[4], fx[4], fy[4], fz[4];
-        const float *vp[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int64_t j = cb + k;
-            tk[k] = sample_t(j, dt);
-            const f3 pt = mk(o.x + tk[k] * d.x, o.y + tk[k] * d.y, o.z + tk[k] * d.z);
-            const f3 g = mk((pt.x - B.O[0]) / B.h[0], (pt.y - B.O[1]) / B.h[1], (pt.z - B.O[2]) / B.h[2]);
-            const bool own = g.x >= (float)B.lo[0] && g.x < (float)B.hi[0] && g.y >= (float)B.lo[1] &&
-                             g.y < (float)B.hi[1] && g.z >= (float)B.lo[2] && g.z < (float)B.hi[2];
-            const float fx0 = floorf(g.x), fy0 = floorf(g.y), fz0 = floorf(g.z);
-            fx[k] = g.x - fx0; fy[k] = g.y - fy0; fz[k] = g.z - fz0;
-            const int ix = own ? (int)fx0 - B.lo[0] : 0, iy = own ? (int)fy0 - B.lo[1] : 0,
-                      iz = own ? (int)fz0 - B.lo[2] : 0;
-            vp[k] = B.vox + (int64_t)ix + sy * iy + sz * iz;
-            const int dist =
-                own ? (int)__ldg(B.mcd + ((iz / MC_SIZE) * B.mc_dims[1] + iy / MC_SIZE) * B.mc_dims[0] + ix / MC_SIZE) : 0;
-            val[k] = own && dist == 0 && j >= i && j <= i1 && tk[k] < bound;
-            if (k == 3) { own3 = own; dist3 = dist; mc3[0] = ix / MC_SIZE; mc3[1] = iy / MC_SIZE; mc3[2] = iz / MC_SIZE; }
-        }
-        if (val[0] || val[1] || val[2] || val[3]) {
-            const uint4 rr = rng4(seed, p, s, depth, purpose, subhi | (uint32_t)(cb >> 2));
-            float v[4][8];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float *q = val[k] ? vp[k] : B.vox;
-                v[k][0] = __ldg(q); v[k][1] = __ldg(q + 1); v[k][2] = __ldg(q + sy); v[k][3] = __ldg(q + sy + 1);
-                v[k][4] = __ldg(q + sz); v[k][5] = __ldg(q + sz + 1); v[k][6] = __ldg(q + sz + sy);
-                v[k][7] = __ldg(q + sz + sy + 1);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (!val[k]) continue;
-                nsamples++;
-                const float c00 = lerpf(v[k][0], v[k][1], fx[k]), c10 = lerpf(v[k][2], v[k][3], fx[k]);
-                const float c01 = lerpf(v[k][4], v[k][5], fx[k]), c11 = lerpf(v[k][6], v[k][7], fx[k]);
-                const float c0 = lerpf(c00, c10, fy[k]), c1 = lerpf(c01, c11, fy[k]);
-                f3 rgb;
-                const float alpha = tf_alpha_rgb(B, lerpf(c0, c1, fz[k]), ANY ? nullptr : &rgb);
-                const uint32_t x = k == 0 ? rr.x : (k == 1 ? rr.y : (k == 2 ? rr.z : rr.w));
-                if (u01(x) < alpha) {
-                    t_out = tk[k];
-                    i_out = (uint32_t)(cb + k);
-                    if (!ANY) rgb_out = rgb;
-                    return true;
-                }
-            }
-        }
-        int64_t inext = cb + 4;
-        if (own3 && dist3 > 0) {
-            float mlo[3], mhi[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int c0 = max(B.lo[c] + (mc3[c] - (dist3 - 1)) * MC_SIZE, B.lo[c]);
-                const int c1 = min(B.lo[c] + (mc3[c] + dist3) * MC_SIZE, B.hi[c]);
-                mlo[c] = B.O[c] + (float)c0 * B.h[c];
-                mhi[c] = B.O[c] + (float)c1 * B.h[c];
-            }
-            float m0, m1;
-            slab(mlo, mhi, o, d, tmax, m0, m1);
-            const int64_t jump = (int64_t)floorf(m1 / dt - 0.5f) - 2;
-            if (jump + 1 > inext) inext = jump + 1;
-        }
-        i = inext;
     }
     return false;
 }
@@ -1218,7 +1104,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu, slot = meta >> 24;
                 for (int b = 0; b < A.W.nbricks && !occluded; ++b) {
                     float ti; uint32_t ii; f3 rgb;
-                    occluded = MARCH_INLINE<true>(A.W.bricks[b], RAY_O(S), RAY_D(S), S.tmax, S.tmax, F.dt, F.seed, p, s,
+                    occluded = march_brick<true>(A.W.bricks[b], RAY_O(S), RAY_D(S), S.tmax, S.tmax, F.dt, F.seed, p, s,
                                                  depth, slot == 0 ? PUR_VOL_SHADOW : PUR_VOL_AO,
                                                  slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
                 }
@@ -1245,7 +1131,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                 const uint32_t s = meta & 0xffffu, depth = (meta >> 16) & 0xffu;
                 for (int b = 0; b < A.W.nbricks; ++b) {
                     float ti; uint32_t ii; f3 rgb;
-                    if (MARCH_INLINE<false>(A.W.bricks[b], RAY_O(S), RAY_D(S), INF, S.h.t, F.dt, F.seed, p, s, depth,
+                    if (march_brick<false>(A.W.bricks[b], RAY_O(S), RAY_D(S), INF, S.h.t, F.dt, F.seed, p, s, depth,
                                            PUR_VOL_PATH, 0u, ti, ii, rgb, tc.vols)) {
                         S.h.t = ti; S.h.id = VOL_BIT | ii; nrm = rgb; changed = true;
                     }
@@ -1279,9 +1165,12 @@ __global__ void __launch_bounds__(TRACE_BLOCK, TRACE_MINB) k_trace_occl(const __
 // into per-destination queues (warp-aggregated appends; every lane of a warp participates).
 // ---------------------------------------------------------------------------------------
 #ifndef DPR_SHADE_MINB
-#define DPR_SHADE_MINB 4
+#define DPR_SHADE_MINB 8
 #endif
-__global__ void __launch_bounds__(256, DPR_SHADE_MINB) k_shade_path(const __grid_constant__ StepArgs A) {
+#ifndef DPR_SHADE_BLOCK
+#define DPR_SHADE_BLOCK 128
+#endif
+__global__ void __launch_bounds__(DPR_SHADE_BLOCK, DPR_SHADE_MINB) k_shade_path(const __grid_constant__ StepArgs A) {
     const FrameDev &F = A.F;
     const int self = A.R.self, N = A.R.nranks;
     const float INF = __int_as_float(0x7f800000);
@@ -1629,7 +1518,7 @@ int launch_trace_occl(const StepArgs &a, int grid, uint32_t n, cudaStream_t s) {
     return 2;
 }
 void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s) {
-    k_shade_path<<<grid, 256, 0, s>>>(a);
+    k_shade_path<<<grid * (256 / DPR_SHADE_BLOCK), DPR_SHADE_BLOCK, 0, s>>>(a);
 }
 void launch_resolve_occl(const StepArgs &a, int grid, cudaStream_t s) {
     k_resolve_occl<<<grid, 256, 0, s>>>(a);
