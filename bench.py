@@ -324,9 +324,10 @@ def run_gpu(args):
     avg_s = ms / max(n, 1) / 1000.0
     bytes_per_launch = b / max(n, 1)
     achieved = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
-    # ncu figures of THIS workload's kernel (profiles/traffic.json is keyed by config, then
+    # ncu figures of THIS workload's kernel (profiles/traffic.json is keyed by config[+flags][+mode], then
     # kernel; an entry exists only where a --set full capture of that config was committed)
-    tr = (profile_traffic() or {}).get(args.config, {})
+    tkey = args.config + (f"+f{args.flags}" if args.flags else "") + ("" if args.mode == "dp" else f"+{args.mode}")
+    tr = (profile_traffic() or {}).get(tkey, {})
     traffic = None
     limiter = None
     if kname in tr:
