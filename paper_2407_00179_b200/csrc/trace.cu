@@ -32,6 +32,15 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// r = a * b + c on two lanes of a packed fp32x2 (sm_100 FFMA2), b and c broadcast
+__device__ __forceinline__ void ffma2(float &r0, float &r1, float a0, float a1, float b, float c) {
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\tmov.b64 rc, {%5, %5};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(r0), "=f"(r1)
+        : "f"(a0), "f"(a1), "f"(b), "f"(c));
+}
+
 __device__ __forceinline__ void fb_add(float4 *p, float4 v) {
 #if __CUDA_ARCH__ >= 900
     atomicAdd(p, v);
@@ -161,6 +170,9 @@ constexpr int WSTACK = 32;       // node-group stack entries (wide BVH depth bou
 constexpr int COOP_PER_LANE = DPR_COOP_PER_LANE > DPR_COOP_PER_LANE_PATH ? DPR_COOP_PER_LANE
                                                                          : DPR_COOP_PER_LANE_PATH;  // list size
 constexpr int COOP_CAP_ANY = DPR_COOP_PER_LANE, COOP_CAP_PATH = DPR_COOP_PER_LANE_PATH;
+#ifndef DPR_FFMA2
+#define DPR_FFMA2 1
+#endif
 #ifndef DPR_ANY_REVERSE
 #define DPR_ANY_REVERSE 1
 #endif
@@ -343,6 +355,30 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         uint32_t hitm = 0;
 #pragma unroll
         const uint32_t k4b = W.prmt_hi;
+#if DPR_FFMA2
+        // two children per packed fp32x2 FMA (FFMA2: one issue slot, two independently
+        // rounded FMAs -- the same values as two __fmaf_rn)
+        for (int c = 0; c < 8; c += 2) {
+            const uint32_t s0 = (uint32_t)(c & 3) | 0x5440u, s1 = (uint32_t)((c + 1) & 3) | 0x5440u;
+            float tnx[2], tfx[2], tny[2], tfy[2], tnz[2], tfz[2];
+#define DPR_PLANE2(OUT, W0, W1, PS, PO)                                                                    \
+            ffma2(OUT[0], OUT[1], __uint_as_float(__byte_perm(c < 4 ? W0 : W1, k4b, s0)),                 \
+                  __uint_as_float(__byte_perm(c < 4 ? W0 : W1, k4b, s1)), PS, PO)
+            DPR_PLANE2(tnx, nx0, nx1, psx, onx);
+            DPR_PLANE2(tfx, fx0, fx1, psx, ofx);
+            DPR_PLANE2(tny, ny0, ny1, psy, ony);
+            DPR_PLANE2(tfy, fy0, fy1, psy, ofy);
+            DPR_PLANE2(tnz, nz0, nz1, psz, onz);
+            DPR_PLANE2(tfz, fz0, fz1, psz, ofz);
+#undef DPR_PLANE2
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float tn = fmaxf(fmaxf(tnx[h], tny[h]), fmaxf(tnz[h], 0.0f));
+                const float tf = fminf(fminf(tfx[h], tfy[h]), fminf(tfz[h], bound));
+                hitm |= (tn <= tf ? 1u : 0u) << (c + h);
+            }
+        }
+#else
         for (int c = 0; c < 8; ++c) {
             const uint32_t sel = (uint32_t)(c & 3) | 0x5440u;
             float tnx = __fmaf_rn(__uint_as_float(__byte_perm(c < 4 ? nx0 : nx1, k4b, sel)), psx, onx);
@@ -355,6 +391,7 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
             float tf = fminf(fminf(tfx, tfy), fminf(tfz, bound));
             hitm |= (tn <= tf ? 1u : 0u) << c;
         }
+#endif
         // leaf slots (build time mask in the top nibbles of child_base / prim_base)
         const uint32_t leafm = (w1.x >> 28) | ((w1.y >> 24) & 0xf0u);
         uint32_t ih = hitm & nimask;
