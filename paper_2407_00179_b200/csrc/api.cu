@@ -1003,11 +1003,12 @@ int render_group(std::vector<Dev *> &L) {
                 if (n_occl) {
                     cudaEvent_t e0 = next_event(d), e1 = next_event(d);
                     CK(cudaEventRecord(e0, d->stream));
+                    a.F.fuse_resolve = fuse_resolve_ok(a, n_occl);
                     const int nk = launch_trace_occl(a, grid_o[i], n_occl, d->stream);
                     CK(cudaEventRecord(e1, d->stream));
-                    launch_resolve_occl(a, grid_r, d->stream);
+                    if (!a.F.fuse_resolve) launch_resolve_occl(a, grid_r, d->stream);
                     if (i == 0) t_occl.push_back({e0, e1});
-                    launches += 1 + nk;
+                    launches += (a.F.fuse_resolve ? 0 : 1) + nk;
                     d->tol++;
                 }
                 CK(cudaGetLastError());
@@ -1107,11 +1108,12 @@ int render_group(std::vector<Dev *> &L) {
                 if (d->h_in[1]) {
                     cudaEvent_t e0 = next_event(d), e1 = next_event(d);
                     CK(cudaEventRecord(e0, d->stream));
+                    a.F.fuse_resolve = fuse_resolve_ok(a, d->h_in[1]);
                     const int nk = launch_trace_occl(a, grid_o[i], d->h_in[1], d->stream);
                     CK(cudaEventRecord(e1, d->stream));
-                    launch_resolve_occl(a, grid_r, d->stream);
+                    if (!a.F.fuse_resolve) launch_resolve_occl(a, grid_r, d->stream);
                     if (i == 0) t_occl.push_back({e0, e1});
-                    launches += 1 + nk;
+                    launches += (a.F.fuse_resolve ? 0 : 1) + nk;
                     d->tol++;
                 }
                 CK(cudaGetLastError());

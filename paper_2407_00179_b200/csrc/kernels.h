@@ -87,6 +87,8 @@ struct FrameDev {
     int gen_rect[4];                   // pixels [x0,x1) x [y0,y1) whose rays can meet this rank's
                                        // padded box (conservative screen projection); others are
                                        // generated only by their pixel owner
+    int fuse_resolve;                  // k_trace_occl resolves its rays itself (one rank, no ring,
+                                       // no separate march kernel): k_resolve_occl is not launched
     uint32_t march_inline_min;         // P10 march inside the trace kernels when the queue holds
                                        // at least this many rays, else in k_march_* (G lanes/ray)
 };
@@ -121,6 +123,8 @@ struct StepArgs {
 void launch_gen_primary(const StepArgs &a, int s0, int nsamp, int spw_max, cudaStream_t s);
 // n: input rays (sizes the march launch); returns the number of kernels launched
 uint32_t march_inline_min(int nsm);
+// whether the occlusion trace of a queue of n rays resolves them itself (sets a.F.fuse_resolve)
+bool fuse_resolve_ok(const StepArgs &a, uint32_t n);
 int launch_trace_path(const StepArgs &a, int grid, uint32_t n, cudaStream_t s);
 int launch_trace_occl(const StepArgs &a, int grid, uint32_t n, cudaStream_t s);
 void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s);

@@ -1080,6 +1080,11 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
     const float INF = __int_as_float(0x7f800000);
     uint2 stack[WSTACK];
     __shared__ CoopSmem coop[TRACE_BLOCK / 32];
+    __shared__ uint32_t s_vis[2];  // fused resolve: shadow / AO rays resolved by this block
+    if (ANY && F.fuse_resolve) {
+        if (threadIdx.x < 2) s_vis[threadIdx.x] = 0;
+        __syncthreads();
+    }
     CoopSmem &cs = coop[threadIdx.x >> 5];
     TravState S;
     S.ng = make_uint2(0, 0);
@@ -1146,7 +1151,21 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                                                  slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
                 }
             }
-            if (occluded) r->a.w = -1.0f;  // occluded marker for k_resolve_occl
+            if (occluded && !F.fuse_resolve) r->a.w = -1.0f;  // occluded marker for k_resolve_occl
+            if (F.fuse_resolve) {
+                // one rank, no ring: no next candidate exists, so the ray resolves here (what
+                // k_resolve_occl does): visit count, unoccluded -> framebuffer (+ P13 bit)
+                const float4 c = __ldcg(&r->c);
+                const uint32_t p = __float_as_uint(__ldcg(&r->b.w)), meta = __float_as_uint(c.w);
+                const uint32_t slot = meta >> 24;
+                atomicAdd(&s_vis[slot == 0 ? 0 : 1], 1u);
+                if (!occluded) {
+                    fb_add(A.fb + p, make_float4(c.x, c.y, c.z, 0.0f));
+                    if (A.occl)
+                        atomicOr(A.occl + ((int64_t)(meta & 0xffffu) * F.max_depth + ((meta >> 16) & 0xffu)) * F.P + p,
+                                 1u << slot);
+                }
+            }
         } else {
             PathRec *r = A.Q.path_in + idx;
             bool changed = S.h.prim >= 0;
@@ -1180,6 +1199,11 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                 r->e.x = nrm.x; r->e.y = nrm.y; r->e.z = nrm.z;
             }
         }
+    }
+    if (ANY && F.fuse_resolve) {
+        __syncthreads();
+        if (threadIdx.x < 2 && s_vis[threadIdx.x])
+            atomicAdd(&A.ctr->V[threadIdx.x == 0 ? K_SHADOW : K_AO], (unsigned long long)s_vis[threadIdx.x]);
     }
     KernelCounters *kc = &A.ctr->kc[ANY ? 1 : 0];
     flush(&kc->nodes, tc.nodes);
@@ -1511,6 +1535,13 @@ uint32_t march_inline_min(int nsm) {
 }
 static bool use_warp_march(const StepArgs &a, uint32_t n) {
     return a.W.nbricks > 0 && !(a.F.flags & DPR_FLAG_DELTA) && n < a.F.march_inline_min;
+}
+#ifndef DPR_FUSE_RESOLVE
+#define DPR_FUSE_RESOLVE 1
+#endif
+bool fuse_resolve_ok(const StepArgs &a, uint32_t n) {
+    static const bool off = getenv("DPR_NO_FUSE_RESOLVE") != nullptr;
+    return DPR_FUSE_RESOLVE && !off && a.R.nranks == 1 && !(a.F.flags & DPR_FLAG_RING) && !use_warp_march(a, n);
 }
 template <int G>
 static void launch_march(const StepArgs &a, bool any, uint32_t n, cudaStream_t s) {
