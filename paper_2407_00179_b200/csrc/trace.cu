@@ -218,10 +218,11 @@ __device__ __forceinline__ f3 ray_id(int t) { return mk(s_ray[6][t], s_ray[7][t]
 #define RAY_ID(S) (S).id3
 #endif
 #ifndef DPR_SM_STACK
-#define DPR_SM_STACK 0
+#define DPR_SM_STACK 3
 #endif
 #if DPR_SM_STACK > 0
-// the first DPR_SM_STACK node-group stack entries of each thread in shared memory (SoA),
+// the first DPR_SM_STACK node-group stack entries of each thread in shared memory (SoA; sweep
+// r01_smstack: 3 best, 14.67 -> 14.51 ms occlusion trace on configs[1]),
 // deeper entries in local memory
 __shared__ uint2 s_stack[DPR_SM_STACK][TRACE_BLOCK];
 __device__ __forceinline__ void stack_push(uint2 *local, int &sp, uint2 v) {
