@@ -1541,8 +1541,8 @@ static bool use_warp_march(const StepArgs &a, uint32_t n) {
 #define DPR_FUSE_RESOLVE 1
 #endif
 bool fuse_resolve_ok(const StepArgs &a, uint32_t n) {
-    static const bool off = getenv("DPR_NO_FUSE_RESOLVE") != nullptr;
-    return DPR_FUSE_RESOLVE && !off && a.R.nranks == 1 && !(a.F.flags & DPR_FLAG_RING) && !use_warp_march(a, n);
+    // read per call (a few times per frame) so a process can switch it (tests)
+    return DPR_FUSE_RESOLVE && getenv("DPR_NO_FUSE_RESOLVE") == nullptr && a.R.nranks == 1 && !(a.F.flags & DPR_FLAG_RING) && !use_warp_march(a, n);
 }
 template <int G>
 static void launch_march(const StepArgs &a, bool any, uint32_t n, cudaStream_t s) {

@@ -120,6 +120,22 @@ def test_mixed_surfaces_and_volume():
     assert_parity(g, o)
 
 
+def test_occlusion_resolve_fused_and_separate(monkeypatch):
+    """One rank: k_trace_occl resolves its rays itself (fused, the default) or k_resolve_occl
+    does (DPR_NO_FUSE_RESOLVE=1); both equal the oracle (events, occlusion bits, visits V),
+    and the fused frame launches one kernel less per occlusion wavefront."""
+    sc = di.config2(nranks=1, G=41, W=96, H=80, spp=4, spp_batch=2)
+    o = oracle_render(sc.parts, 1, sc.camera, sc.frame)
+    fused = gpu_render(sc.parts, 1, sc.camera, sc.frame)
+    assert_parity(fused, o)
+    monkeypatch.setenv("DPR_NO_FUSE_RESOLVE", "1")
+    sep = gpu_render(sc.parts, 1, sc.camera, sc.frame)
+    assert_parity(sep, o)
+    n_occl = sep[3]["trace_occl_launches"]
+    assert n_occl > 0
+    assert sep[3]["kernel_launches_local"] - fused[3]["kernel_launches_local"] == n_occl
+
+
 @pytest.mark.parametrize("nranks", [1, 4])
 def test_config2_family_small(nranks):
     """configs[1] family at a size the oracle finishes in seconds: ~180k-triangle gyroid,
