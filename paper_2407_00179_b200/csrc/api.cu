@@ -29,6 +29,16 @@ using namespace dpr;
 
 namespace {
 
+// 1/h when h is a normal power of two whose reciprocal is normal (then x/h == x*(1/h) exactly
+// in binary32), else 0 (the kernels then divide)
+float exact_recip_pow2(float h) {
+    uint32_t b;
+    std::memcpy(&b, &h, 4);
+    const uint32_t e = (b >> 23) & 0xffu, m = b & 0x7fffffu;
+    if (m != 0 || e < 1 || e > 253) return 0.0f;
+    return 1.0f / h;
+}
+
 thread_local std::string g_err;
 
 struct Dev;
@@ -551,6 +561,7 @@ int build_world(Dev *d) {
         B.mcd = P<uint8_t>(p.mc) + (size_t)p.mc_dims[0] * p.mc_dims[1] * p.mc_dims[2];
         B.tf = P<float4>(p.tf);
         B.tf_lo = p.tf_lo; B.tf_hi = p.tf_hi; B.dscale = p.dscale;
+        B.tf_rd = exact_recip_pow2(B.tf_hi - B.tf_lo);  // the same binary32 difference as the kernels
         d->wbricks.push_back(B);
         d->amax_local = std::max(d->amax_local, p.amax);
     }

@@ -263,6 +263,7 @@ struct BrickDev {
                             // nearest macrocell with mc = 1 (0: mc = 1 here)
     const float4 *tf;       // 256 rgba
     float tf_lo, tf_hi, dscale;
+    float tf_rd;            // 1/(tf_hi - tf_lo) when that difference is a power of two, else 0
 };
 
 constexpr int MC_SIZE = 16;
@@ -320,8 +321,13 @@ __device__ __forceinline__ f3 part_albedo(const PartTable &T, uint32_t id) {
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ float lerpf(float a, float b, float w) { return a + w * (b - a); }
 
+// x / h with the division replaced by a multiplication by r = 1/h when h is a power of two
+// (r != 0, set by the host): x/h and x*r are then the same real number, rounded once, so the
+// result is bit-identical to the IEEE division (incl. subnormal, overflow, signed-zero cases)
+__device__ __forceinline__ float div_pow2(float x, float h, float r) { return r != 0.0f ? x * r : x / h; }
+
 __device__ __forceinline__ float tf_alpha_rgb(const BrickDev &B, float s, f3 *rgb) {
-    float x = fminf(fmaxf((s - B.tf_lo) / (B.tf_hi - B.tf_lo), 0.0f), 1.0f) * 255.0f;
+    float x = fminf(fmaxf(div_pow2(s - B.tf_lo, B.tf_hi - B.tf_lo, B.tf_rd), 0.0f), 1.0f) * 255.0f;
     int j = (int)floorf(x);
     if (j > 254) j = 254;
     float w = x - (float)j;
