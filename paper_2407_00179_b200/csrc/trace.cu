@@ -406,8 +406,9 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         while (lh) {
             const int c = __ffs(lh) - 1;
             lh &= lh - 1;
-            const uint32_t meta = ((c < 4 ? w1.z : w1.w) >> (8 * (c & 3))) & 0xffu;
-            tmask |= ((1u << (((meta >> 5) & 3u) + 1u)) - 1u) << (meta & 31u);
+            // byte c of {w1.z, w1.w} in the low byte (one PRMT); only bits 0..6 are read below
+            const uint32_t meta = __byte_perm(w1.z, w1.w, (uint32_t)c);
+            tmask |= ((2u << ((meta >> 5) & 3u)) - 1u) << (meta & 31u);
         }
         S.ng = make_uint2(w1.x & 0x0fffffffu, ihits | (nimask << 8));
         if (tmask) {
