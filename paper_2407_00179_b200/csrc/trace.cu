@@ -225,6 +225,22 @@ __device__ __forceinline__ f3 ray_id(int t) { return mk(s_ray[6][t], s_ray[7][t]
 // r01_smstack: 3 best, 14.67 -> 14.51 ms occlusion trace on configs[1]),
 // deeper entries in local memory
 __shared__ uint2 s_stack[DPR_SM_STACK][TRACE_BLOCK];
+#ifndef DPR_PERM_LUT
+#define DPR_PERM_LUT 1
+#endif
+#if DPR_PERM_LUT
+// hit mask -> traversal order (bit i moves to bit i ^ order), one table of 256 per order
+__shared__ uint8_t s_perm[8 * 256];
+__device__ __forceinline__ void perm_init() {
+    for (uint32_t i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
+        const uint32_t o = i >> 8, m = i & 255u;
+        uint32_t r = 0;
+        for (uint32_t b = 0; b < 8; ++b) r |= ((m >> b) & 1u) << (b ^ o);
+        s_perm[i] = (uint8_t)r;
+    }
+    __syncthreads();
+}
+#endif
 __device__ __forceinline__ void stack_push(uint2 *local, int &sp, uint2 v) {
     if (sp < DPR_SM_STACK) s_stack[sp][threadIdx.x] = v;
     else local[sp - DPR_SM_STACK] = v;
@@ -398,10 +414,14 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         uint32_t ih = hitm & nimask;
         uint32_t lh = hitm & leafm;
         // internal hits into traversal order s' = slot ^ octant (bit permutation)
+#if DPR_PERM_LUT
+        ih = s_perm[((S.oct >> 3) << 8) | ih];
+#else
         const uint32_t ordm = S.oct >> 3;
         if (ordm & 4u) ih = ((ih & 0x0fu) << 4) | ((ih & 0xf0u) >> 4);
         if (ordm & 2u) ih = ((ih & 0x33u) << 2) | ((ih & 0xccu) >> 2);
         if (ordm & 1u) ih = ((ih & 0x55u) << 1) | ((ih & 0xaau) >> 1);
+#endif
         uint32_t ihits = ih, tmask = 0;
         while (lh) {
             const int c = __ffs(lh) - 1;
@@ -1087,6 +1107,9 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
         if (threadIdx.x < 2) s_vis[threadIdx.x] = 0;
         __syncthreads();
     }
+#if DPR_PERM_LUT
+    perm_init();
+#endif
     CoopSmem &cs = coop[threadIdx.x >> 5];
     TravState S;
     S.ng = make_uint2(0, 0);
