@@ -225,6 +225,9 @@ __device__ __forceinline__ f3 ray_id(int t) { return mk(s_ray[6][t], s_ray[7][t]
 // r01_smstack: 3 best, 14.67 -> 14.51 ms occlusion trace on configs[1]),
 // deeper entries in local memory
 __shared__ uint2 s_stack[DPR_SM_STACK][TRACE_BLOCK];
+#ifndef DPR_LEAF_BF
+#define DPR_LEAF_BF 0
+#endif
 #ifndef DPR_PERM_LUT
 #define DPR_PERM_LUT 1
 #endif
@@ -423,6 +426,17 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
         if (ordm & 1u) ih = ((ih & 0x55u) << 1) | ((ih & 0xaau) >> 1);
 #endif
         uint32_t ihits = ih, tmask = 0;
+#if DPR_LEAF_BF
+        if (lh) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint32_t meta = __byte_perm(c < 4 ? w1.z : w1.w, 0u, (uint32_t)(c & 3));
+                const uint32_t m = ((2u << ((meta >> 5) & 3u)) - 1u) << (meta & 31u);
+                tmask |= (lh & (1u << c)) ? m : 0u;
+            }
+            lh = 0;
+        }
+#endif
         while (lh) {
             const int c = __ffs(lh) - 1;
             lh &= lh - 1;
