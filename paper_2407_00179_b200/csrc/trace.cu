@@ -183,7 +183,7 @@ constexpr int COOP_CAP_ANY = DPR_COOP_PER_LANE, COOP_CAP_PATH = DPR_COOP_PER_LAN
 #define DPR_WARP_MARCH 1
 #endif
 #ifndef DPR_P1_EXIT_ANY
-#define DPR_P1_EXIT_ANY 8
+#define DPR_P1_EXIT_ANY 4
 #endif
 constexpr int P1_EXIT_ANY = DPR_P1_EXIT_ANY;
 struct CoopSmem {
@@ -218,7 +218,7 @@ __device__ __forceinline__ f3 ray_id(int t) { return mk(s_ray[6][t], s_ray[7][t]
 #define RAY_ID(S) (S).id3
 #endif
 #ifndef DPR_SM_STACK
-#define DPR_SM_STACK 3
+#define DPR_SM_STACK 4
 #endif
 #if DPR_SM_STACK > 0
 // the first DPR_SM_STACK node-group stack entries of each thread in shared memory (SoA; sweep
