@@ -162,7 +162,7 @@ constexpr int WSTACK = 32;       // node-group stack entries (wide BVH depth bou
 // a per-warp list that all 32 lanes test (against the owner lane's ray), then the results are
 // reduced per owner in shared memory.
 #ifndef DPR_COOP_PER_LANE
-#define DPR_COOP_PER_LANE 16
+#define DPR_COOP_PER_LANE 12
 #endif
 #ifndef DPR_COOP_PER_LANE_PATH
 #define DPR_COOP_PER_LANE_PATH DPR_COOP_PER_LANE
