@@ -496,19 +496,33 @@ def boxes_scene(nranks: int = 4, n: int = 4, W: int = 256, H: int = 256, spp: in
 
 
 def routing_hand_case(which: str) -> Scene:
-    """SURVEY 8(c).4 hand cases H1-H3 (1x1 image, jitter 0.5, d = (0,0,1) exactly)."""
+    """SURVEY 8(c).4 hand cases H1-H3 (1x1 image, jitter 0.5, d = (0,0,1) exactly), plus H4:
+    the eye (0.2,0.2,-1) lies inside BOTH padded rank boxes (each rank also owns a tiny
+    triangle at z=-2 off the ray's path), so the primary's entry distance is t0=0 for both
+    ranks -- the equal-t0 tie of the visit key (t0_r, r); and H5: rank 0's square sits at
+    z = 2.0001f, so its padded box is entered at exactly t0 = 3 = bestT of rank 1's hit (the
+    `t0_r <= bestT` bound of P8 taken with equality)."""
     cam = Camera(E=f32((0.2, 0.2, -1)), L=f32((-0.05, -0.05, 1)), U=f32((0.1, 0, 0)),
                  V=f32((0, 0.1, 0)))
+    z0 = 2.0001 if which == "H5" else 3.0
     r0 = Part(rank=0, kind=TRIS, albedo=(0.5, 0.6, 0.7),
-              verts=f32([(-1, -1, 3), (1, -1, 3), (1, 1, 3), (-1, 1, 3)]),
+              verts=f32([(-1, -1, z0), (1, -1, z0), (1, 1, z0), (-1, 1, z0)]),
               idx=np.array([[0, 1, 2], [0, 2, 3]], np.int32))
-    if which in ("H1", "H3"):
+    if which in ("H1", "H3", "H4"):
         r1v = f32([(-.5, -.5, 2), (.5, -.5, 2), (-.5, .5, 2)])
-    else:  # H2: rank 1's triangle covers (0.2, 0.2)
+    else:  # H2, H5: rank 1's triangle covers (0.2, 0.2)
         r1v = f32([(-.5, -.5, 2), (1, -.5, 2), (-.5, 1, 2)])
     r1 = Part(rank=1, kind=TRIS, albedo=(0.9, 0.3, 0.1), verts=r1v,
               idx=np.array([[0, 1, 2]], np.int32))
+    parts = [r0, r1]
+    if which == "H4":
+        parts += [Part(rank=0, kind=TRIS, albedo=(0.1, 0.1, 0.1),
+                       verts=f32([(-1, -1, -2), (-.9, -1, -2), (-1, -.9, -2)]),
+                       idx=np.array([[0, 1, 2]], np.int32)),
+                  Part(rank=1, kind=TRIS, albedo=(0.1, 0.1, 0.1),
+                       verts=f32([(.9, .9, -2), (1, .9, -2), (1, 1, -2)]),
+                       idx=np.array([[0, 1, 2]], np.int32))]
     l = (0, 0, 1) if which == "H3" else (0, 0, -1)
     fr = Frame(W=1, H=1, spp=1, spp_batch=1, max_depth=1, ao_k=0, light_dir=f32(l),
                E=(1, 1, 1), A=(0, 0, 0), B=(0, 0, 0), seed=7, flags=1)
-    return Scene(which, [r0, r1], 2, cam, fr)
+    return Scene(which, parts, 2, cam, fr)

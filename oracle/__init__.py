@@ -22,6 +22,8 @@ import dpr_inputs as di
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dpr_oracle.c")
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# tools/oracle_mutations.py points this at a mutated build (checks that each pin can fail)
+_LIB_OVERRIDE = os.environ.get("DPR_ORACLE_LIB")
 _lib = None
 
 CFLAGS = ["-O2", "-std=c11", "-D_GNU_SOURCE", "-ffp-contract=off", "-fno-fast-math",
@@ -68,8 +70,11 @@ _P = ctypes.c_void_p
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(LIB_PATH)
+        if _LIB_OVERRIDE:
+            L = ctypes.CDLL(_LIB_OVERRIDE)
+        else:
+            build()
+            L = ctypes.CDLL(LIB_PATH)
         L.or_scene_build.restype = _P
         L.or_scene_build.argtypes = [_P, ctypes.c_int, ctypes.c_int]
         L.or_scene_free.argtypes = [_P]
@@ -99,6 +104,13 @@ def lib():
                                     ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _P]
         L.or_iso_dir.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                  ctypes.c_uint32, _P]
+        L.or_ao_dir.argtypes = [_P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                ctypes.c_uint32, ctypes.c_int, _P]
+        L.or_bounce_dir.argtypes = [_P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                    ctypes.c_uint32, _P]
+        L.or_vol_u.restype = ctypes.c_float
+        L.or_vol_u.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                               ctypes.c_int, ctypes.c_int, ctypes.c_int64]
         L.or_pln.restype = ctypes.c_float
         L.or_pln.argtypes = [ctypes.c_float]
         L.or_tf_eval.argtypes = [_P, ctypes.c_float, ctypes.c_float, ctypes.c_float,
@@ -345,6 +357,25 @@ def iso_dir(seed, p, s, depth):
     out = (ctypes.c_float * 3)()
     lib().or_iso_dir(seed, p, s, depth, out)
     return np.array(out, np.float32)
+
+
+def ao_dir(n, seed, p, s, depth, k):
+    """AO ray k's direction as the renderer draws it (P1 purpose 2, sub = (k<<4)|attempt)."""
+    out = (ctypes.c_float * 3)()
+    lib().or_ao_dir(_fa(n), seed, p, s, depth, k, out)
+    return np.array(out, np.float32)
+
+
+def bounce_dir(n, seed, p, s, depth):
+    """The bounce direction as the renderer draws it (P1 purpose 3, sub = attempt)."""
+    out = (ctypes.c_float * 3)()
+    lib().or_bounce_dir(_fa(n), seed, p, s, depth, out)
+    return np.array(out, np.float32)
+
+
+def vol_u(seed, p, s, depth, kind, k, i):
+    """u_i of volume sample i of a ray of kind 0 path / 1 shadow / 2 AO k (P1 4/5/6)."""
+    return float(lib().or_vol_u(seed, p, s, depth, kind, k, i))
 
 
 def pln(x: float) -> float:

@@ -958,10 +958,38 @@ static v3 iso_dir(uint64_t seed, uint32_t p, uint32_t s, uint32_t depth)
     return V3(0.0f, 0.0f, 1.0f);
 }
 
+/* P1 call sites.  Each RNG consumer of the renderer goes through
+ * one of these, and each is exported for the counter-layout pins (tests/test_oracle_rng.py):
+ *   AO ray k of the vertex at depth d:   purpose 2, sub = (k<<4) | attempt
+ *   bounce of the vertex at depth d:     purpose 3, sub = attempt
+ *   volume sample i of a path ray:       purpose 4, sub = i>>2, lane i&3
+ *   volume sample i of a shadow ray:     purpose 5, sub = i>>2, lane i&3
+ *   volume sample i of AO ray k:         purpose 6, sub = (k<<24) | (i>>2), lane i&3 */
+static v3 ao_dir(v3 n, uint64_t seed, uint32_t p, uint32_t s, uint32_t depth, int k)
+{
+    return cosine_dir(n, seed, p, s, depth, PUR_AO, (uint32_t)k << 4);
+}
+
+static v3 bounce_dir(v3 n, uint64_t seed, uint32_t p, uint32_t s, uint32_t depth)
+{
+    return cosine_dir(n, seed, p, s, depth, PUR_BOUNCE, 0);
+}
+
 /* ------------------------------------------------------------------------------------ */
 /* Rendering: a ray tree per (pixel, sample), processed with an explicit stack.          */
 /* ------------------------------------------------------------------------------------ */
 enum { K_PATH = 0, K_SHADOW = 1, K_AO = 2 };
+
+/* The Philox key of the volume samples of a ray of `kind` (P1: purpose 4/5/6; AO ray k
+ * carries k<<24 in the high bits of sub; vol_u adds i>>2 and takes lane i&3). */
+static VolKey vol_key(uint64_t seed, uint32_t p, uint32_t s, uint32_t depth, int kind, int k)
+{
+    VolKey v;
+    v.seed = seed; v.p = p; v.s = s; v.depth = depth;
+    v.purpose = kind == K_PATH ? PUR_VOL_PATH : (kind == K_SHADOW ? PUR_VOL_SHADOW : PUR_VOL_AO);
+    v.subhi = kind == K_AO ? ((uint32_t)k << 24) : 0u;
+    return v;
+}
 
 typedef struct {
     int kind;
@@ -1110,7 +1138,7 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
         if (ray.kind == K_PATH) {
             OHit best;
             hit_none(&best);
-            VolKey vk = {fr->seed, p, s, (uint32_t)ray.depth, PUR_VOL_PATH, 0};
+            VolKey vk = vol_key(fr->seed, p, s, (uint32_t)ray.depth, K_PATH, 0);
             int at = ray.rank;
             if (!dp) {
                 trace_path_at(J, -1, &ray, &vk, &best);
@@ -1156,7 +1184,7 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
                 for (int k = 0; k < fr->ao_k; ++k) {
                     ORay ao; memset(&ao, 0, sizeof(ao));
                     ao.kind = K_AO; ao.o = org;
-                    ao.d = cosine_dir(n, fr->seed, p, s, (uint32_t)ray.depth, PUR_AO, (uint32_t)k << 4);
+                    ao.d = ao_dir(n, fr->seed, p, s, (uint32_t)ray.depth, k);
                     ao.tmax = fr->ao_radius;
                     ao.w = vscale(vmul(br, Am), 1.0f / (float)fr->ao_k);
                     ao.depth = ray.depth; ao.k = k;
@@ -1165,7 +1193,7 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
                 if (ray.depth + 1 < fr->max_depth) {
                     ORay bo; memset(&bo, 0, sizeof(bo));
                     bo.kind = K_PATH; bo.o = org;
-                    bo.d = cosine_dir(n, fr->seed, p, s, (uint32_t)ray.depth, PUR_BOUNCE, 0);
+                    bo.d = bounce_dir(n, fr->seed, p, s, (uint32_t)ray.depth);
                     bo.tmax = INFINITY; bo.w = br; bo.depth = ray.depth + 1;
                     kids[nk++] = bo;
                 }
@@ -1209,9 +1237,7 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
                 stack[sp++] = ch;
             }
         } else {
-            VolKey vk = {fr->seed, p, s, (uint32_t)ray.depth,
-                         ray.kind == K_SHADOW ? PUR_VOL_SHADOW : PUR_VOL_AO,
-                         ray.kind == K_SHADOW ? 0u : ((uint32_t)ray.k << 24)};
+            VolKey vk = vol_key(fr->seed, p, s, (uint32_t)ray.depth, ray.kind, ray.k);
             int occluded = 0;
             if (!dp) {
                 occluded = trace_occl_at(J, -1, &ray, &vk);
@@ -1386,6 +1412,28 @@ OR_EXPORT void or_iso_dir(uint64_t seed, uint32_t p, uint32_t s, uint32_t depth,
 }
 
 OR_EXPORT float or_pln(float x) { return pln(x); }
+
+/* The renderer's RNG call sites (P1 counter layout; pinned against or_philox). */
+OR_EXPORT void or_ao_dir(const float n[3], uint64_t seed, uint32_t p, uint32_t s, uint32_t depth, int k,
+                         float out[3])
+{
+    v3 r = ao_dir(vload(n), seed, p, s, depth, k);
+    out[0] = r.x; out[1] = r.y; out[2] = r.z;
+}
+
+OR_EXPORT void or_bounce_dir(const float n[3], uint64_t seed, uint32_t p, uint32_t s, uint32_t depth,
+                             float out[3])
+{
+    v3 r = bounce_dir(vload(n), seed, p, s, depth);
+    out[0] = r.x; out[1] = r.y; out[2] = r.z;
+}
+
+/* u_i of volume sample i of a ray of kind 0 path / 1 shadow / 2 AO k. */
+OR_EXPORT float or_vol_u(uint64_t seed, uint32_t p, uint32_t s, uint32_t depth, int kind, int k, int64_t i)
+{
+    VolKey v = vol_key(seed, p, s, depth, kind, k);
+    return vol_u(v.seed, v.p, v.s, v.depth, v.purpose, v.subhi, i);
+}
 
 OR_EXPORT void or_tf_eval(const float *tf, float lo, float hi, float dscale, float s, float rgba[4])
 {

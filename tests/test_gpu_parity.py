@@ -30,7 +30,7 @@ def test_config1_two_ranks():
     assert o.S[1].sum() > 0
 
 
-@pytest.mark.parametrize("case", ["H1", "H2", "H3"])
+@pytest.mark.parametrize("case", ["H1", "H2", "H3", "H4", "H5"])
 def test_routing_hand_cases(case):
     sc = di.routing_hand_case(case)
     g = gpu_render(sc.parts, 2, sc.camera, sc.frame)

@@ -117,9 +117,10 @@ def test_shadow_ray_blocked():
     assert abs(r.rgba[0, 0] - 0.5) < 1e-7 and r.occl[0, 0, 0] == 1
 
 
-@pytest.mark.parametrize("case", ["H1", "H2", "H3"])
+@pytest.mark.parametrize("case", ["H1", "H2", "H3", "H4", "H5"])
 def test_routing_hand_cases(case, golden_dir):
-    """P8 routing, hand-derived (tests/golden/routing_hand_cases.json)."""
+    """P8 routing + P8b steps, hand-derived (tests/golden/routing_hand_cases.json); H4 is
+    the equal-t0 rank tie of the visit key (t0_r, r)."""
     g = json.load(open(os.path.join(golden_dir, "routing_hand_cases.json")))[case]
     sc = di.routing_hand_case(case)
     r = _render(sc.parts, 2, sc.camera, sc.frame, dp=True)
@@ -130,6 +131,7 @@ def test_routing_hand_cases(case, golden_dir):
     assert int(r.events[0, 0, 0]) == g["event"]
     assert int(r.occl[0, 0, 0]) == g["occl"]
     assert np.allclose(r.rgba[0], g["rgba"], atol=1e-7)
+    assert r.steps.tolist() == [g["steps"]]
     u = _render(di.union_parts(sc.parts), 1, sc.camera, sc.frame)
     assert np.array_equal(u.events, r.events) and np.allclose(u.rgba, r.rgba, atol=1e-12)
 
