@@ -94,8 +94,12 @@ typedef struct {
 /* One rank-local world part.  Arrays are COPIED at commit (ANARI commit
  * semantics): the caller may free them when dpr_commit_part returns (except
  * DPR_MEMORY_HOST_ASYNC, see dpr_memory).
- *   TRIANGLES: verts float[n_verts][3], idx int32[n_tris][3] (indices into verts).
- *   SPHERES:   spheres float[n_spheres][4] = centre xyz, radius (> 0).
+ *   TRIANGLES: verts float[n_verts][3] (finite), idx int32[n_tris][3] (indices into verts).
+ *              A triangle whose binary32 cross(v1-v0, v2-v0) is exactly zero (no area, no
+ *              normal) is never hit (reading R-DEGEN).
+ *   SPHERES:   spheres float[n_spheres][4] = centre xyz, radius (finite, > 0).
+ *   Indices, finiteness and radii are validated on the GPU by dpr_commit_world
+ *   (DPR_ERR_INVALID_ARG).
  *   BRICK:     a brick of one global structured grid: gdims (points per axis), origin,
  *              spacing (> 0); the brick owns cells [cell_lo, cell_hi) (half-open) and
  *              stores voxels [cell_lo, cell_hi] INCLUSIVE (one ghost layer), x fastest;
@@ -218,9 +222,9 @@ DPR_API int dpr_clear_parts(dpr_device dev);
  * GPU: per-prim AABBs, 63-bit Morton codes, LSD radix sort, Karras hierarchy (or PLOC with
  * env DPR_BUILDER=ploc), bottom-up refit, collapse into a compressed 8-wide BVH ("negligible
  * pre-processing time") and brick macrocells.  May be called again to rebuild
- * from the resident parts.  DPR_ERR_INVALID_ARG if a triangle index is out of range
- * (validated on the GPU here, not at commit_part) or a bounds_hint does not contain its
- * part; the world is then not ready. */
+ * from the resident parts.  DPR_ERR_INVALID_ARG if a triangle index is out of range,
+ * a coordinate is not finite or a sphere radius is not > 0 (validated on the GPU here, not at
+ * commit_part) or a bounds_hint does not contain its part; the world is then not ready. */
 DPR_API int dpr_commit_world(dpr_device dev);
 
 /* COLLECTIVE (getProperty(WAIT) on the world): union of all ranks' world

@@ -147,6 +147,18 @@ static int tri_hit(v3 o, v3 d, float tmax, v3 v0, v3 e1, v3 e2, float *t_out)
     return 1;
 }
 
+/* Edges of a committed triangle (P3 precompute e1 = v1-v0, e2 = v2-v0), with reading
+ * R-DEGEN: a triangle whose binary32 cross(e1, e2) is exactly the zero vector has
+ * no area and no normal; it is stored with e1 = e2 = 0, so P3's det == 0 test always rejects
+ * it (otherwise rounding can make MT report a hit whose normal is 0/0). */
+static void tri_edges(v3 v0, v3 v1, v3 v2, v3 *e1, v3 *e2)
+{
+    *e1 = vsub(v1, v0);
+    *e2 = vsub(v2, v0);
+    v3 ng = vcross(*e1, *e2);
+    if (ng.x == 0.0f && ng.y == 0.0f && ng.z == 0.0f) { *e1 = V3(0, 0, 0); *e2 = V3(0, 0, 0); }
+}
+
 /* Orient a unit normal against the ray: negate if dot(n,d) > 0 (P3). */
 static v3 orient(v3 n, v3 d)
 {
@@ -793,7 +805,12 @@ OR_EXPORT OScene *or_scene_build(const or_part *parts, int nparts, int nranks)
                     v3 v1 = vload(pt->verts + 3 * (int64_t)pt->idx[3 * t + 1]);
                     v3 v2 = vload(pt->verts + 3 * (int64_t)pt->idx[3 * t + 2]);
                     p->type = 0; p->id = (uint32_t)gid; p->part = i;
-                    p->a = v0; p->b = vsub(v1, v0); p->c = vsub(v2, v0);
+                    if (!isfinite(v0.x) || !isfinite(v0.y) || !isfinite(v0.z) || !isfinite(v1.x) ||
+                        !isfinite(v1.y) || !isfinite(v1.z) || !isfinite(v2.x) || !isfinite(v2.y) ||
+                        !isfinite(v2.z))
+                        goto invalid; /* the GPU path rejects it too (DPR_ERR_INVALID_ARG) */
+                    p->a = v0;
+                    tri_edges(v0, v1, v2, &p->b, &p->c);
                     for (int c = 0; c < 3; ++c) {
                         p->lo[c] = fminf(fminf(vget(v0, c), vget(v1, c)), vget(v2, c));
                         p->hi[c] = fmaxf(fmaxf(vget(v0, c), vget(v1, c)), vget(v2, c));
@@ -805,6 +822,8 @@ OR_EXPORT OScene *or_scene_build(const or_part *parts, int nparts, int nranks)
                 for (int64_t s = 0; s < pt->n_spheres; ++s) {
                     OPrim *p = &sc->prims[gid];
                     const float *q = pt->spheres + 4 * s;
+                    if (!isfinite(q[0]) || !isfinite(q[1]) || !isfinite(q[2]) || !isfinite(q[3]) || !(q[3] > 0.0f))
+                        goto invalid; /* radius must be > 0 and finite (dpr.h) */
                     p->type = 1; p->id = (uint32_t)gid; p->part = i;
                     p->a = V3(q[0], q[1], q[2]); p->b = V3(q[3], 0, 0); p->c = V3(0, 0, 0);
                     for (int c = 0; c < 3; ++c) { p->lo[c] = q[c] - q[3]; p->hi[c] = q[c] + q[3]; }
@@ -862,6 +881,10 @@ OR_EXPORT OScene *or_scene_build(const or_part *parts, int nparts, int nranks)
     free(sel);
     free(rank_first);
     return sc;
+invalid:
+    free(rank_first);
+    or_scene_free(sc);
+    return NULL;
 }
 
 OR_EXPORT int64_t or_scene_nprims(const OScene *sc) { return sc->nprims; }
@@ -1367,7 +1390,8 @@ OR_EXPORT float or_u01(uint32_t x) { return u01(x); }
 OR_EXPORT int or_tri_hit(const float o[3], const float d[3], float tmax, const float v0[3],
                          const float v1[3], const float v2[3], float *t, float n[3])
 {
-    v3 a = vload(v0), e1 = vsub(vload(v1), a), e2 = vsub(vload(v2), a);
+    v3 a = vload(v0), e1, e2;
+    tri_edges(a, vload(v1), vload(v2), &e1, &e2);
     if (!tri_hit(vload(o), vload(d), tmax, a, e1, e2, t)) return 0;
     v3 nn = tri_normal(e1, e2, vload(d));
     n[0] = nn.x; n[1] = nn.y; n[2] = nn.z;

@@ -253,10 +253,27 @@ uint64_t fnv1a(const void *p, size_t n, uint64_t h = 1469598103934665603ull) {
     return h;
 }
 
+// Digest of the camera + frame parameters (P:349-353 consistency check), field by field: the
+// structs' padding (dpr_frame_desc has 4 tail bytes after flags) never enters it.
 uint64_t frame_digest(const Dev *d) {
-    uint64_t h = fnv1a(&d->cam, sizeof(d->cam));
-    dpr_frame_desc f = d->fr;
-    return fnv1a(&f, sizeof(f), h);
+    const dpr_camera_basis &c = d->cam;
+    uint64_t h = fnv1a(c.E, sizeof(c.E));
+    h = fnv1a(c.L, sizeof(c.L), h);
+    h = fnv1a(c.U, sizeof(c.U), h);
+    h = fnv1a(c.V, sizeof(c.V), h);
+    h = fnv1a(&c.lens_radius, sizeof(float), h);
+    h = fnv1a(&c.focus_dist, sizeof(float), h);
+    const dpr_frame_desc &f = d->fr;
+    const int32_t ints[6] = {f.W, f.H, f.spp, f.spp_batch, f.max_depth, f.ao_k};
+    h = fnv1a(ints, sizeof(ints), h);
+    h = fnv1a(&f.ao_radius, sizeof(float), h);
+    h = fnv1a(f.light_dir, sizeof(f.light_dir), h);
+    h = fnv1a(f.E, sizeof(f.E), h);
+    h = fnv1a(f.A, sizeof(f.A), h);
+    h = fnv1a(f.B, sizeof(f.B), h);
+    h = fnv1a(&f.dt, sizeof(float), h);
+    h = fnv1a(&f.seed, sizeof(f.seed), h);
+    return fnv1a(&f.flags, sizeof(f.flags), h);
 }
 
 bool valid_dev(dpr_device h) { return h != nullptr; }
@@ -289,6 +306,7 @@ int allgather_host(std::vector<Dev *> &L, const std::vector<const void *> &send,
 // ---------------------------------------------------------------------------------------
 int build_world(Dev *d) {
     cudaStream_t s = d->stream;
+    d->world_ready = false;  // until this build succeeds (dpr.h: a failed commit leaves no world)
     if (d->copy_pending) {  // geometry copied on the side stream (DPR_MEMORY_HOST_ASYNC)
         CK(cudaStreamWaitEvent(s, d->copy_ev, 0));
         d->copy_pending = false;
@@ -355,7 +373,9 @@ int build_world(Dev *d) {
     std::vector<int> bnd(12 * (np + 1) + 1);
     CK(cudaMemcpyAsync(bnd.data(), d->b_bounds.p, bnd.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (bnd[12 * (np + 1)]) return fail(DPR_ERR_INVALID_ARG, "triangle index out of range (checked on the GPU)");
+    if (bnd[12 * (np + 1)] & 1) return fail(DPR_ERR_INVALID_ARG, "triangle index out of range (checked on the GPU)");
+    if (bnd[12 * (np + 1)] & 2)
+        return fail(DPR_ERR_INVALID_ARG, "non-finite vertex / sphere, or sphere radius <= 0 (checked on the GPU)");
     auto ord2f = [](int i) { int j = i >= 0 ? i : i ^ 0x7fffffff; float f; memcpy(&f, &j, 4); return f; };
     // rank box = exact union of prim boxes and brick cell-domain boxes (P8)
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -700,9 +720,14 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
 
 // Conservative pixel rectangle of the projection of this rank's padded routing box (P8): a
 // primary ray whose first candidate is this rank passes through the box, so its pixel lies in
-// the projection.  Projection in double with a 2-pixel margin; the whole frame when a corner
-// is not in front of the eye, for thin-lens cameras, at N=1, or for an empty rank (then only
-// the pixel owner's misses matter and the rect is empty).
+// the projection.  A point X is seen through screen position (sx, sy) iff
+// X - E = lam * (L + sx*U + sy*V) with lam > 0 (P2), i.e. (lam, lam*sx, lam*sy) solves the 3x3
+// system [L U V] * y = X - E -- for ANY basis (sheared / off-axis / cropped image regions
+// included).  With every corner in front (lam > 0; lam is linear, so the whole box is), the
+// box projects into the convex hull of its corners' projections.  Solved in double with a
+// 2-pixel margin; the whole frame when the basis is (nearly) singular, a corner is not in
+// front of the eye, for thin-lens cameras, at N=1; an empty rect for an empty rank (then
+// only the pixel owner's misses matter).
 void gen_rect(const Dev *d, const FrameCtx &fc, int rect[4]) {
     const int W = d->fr.W, H = d->fr.H;
     rect[0] = 0; rect[1] = 0; rect[2] = W; rect[3] = H;
@@ -710,25 +735,34 @@ void gen_rect(const Dev *d, const FrameCtx &fc, int rect[4]) {
     if (off || fc.R.nranks <= 1 || d->cam.lens_radius > 0.0f) return;
     if (!fc.R.nonempty[d->rank]) { rect[2] = 0; rect[3] = 0; return; }
     const dpr_camera_basis &c = d->cam;
-    double U[3], V[3], w[3], uu = 0, vv = 0;
-    for (int k = 0; k < 3; ++k) {
-        U[k] = c.U[k]; V[k] = c.V[k];
-        w[k] = (double)c.L[k] + 0.5 * U[k] + 0.5 * V[k];  // L = w - U/2 - V/2 (P2)
-        uu += U[k] * U[k]; vv += V[k] * V[k];
-    }
-    double wl = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+    // columns L, U, V; inverse by the adjugate (cofactors in double)
+    const double M[3][3] = {{c.L[0], c.U[0], c.V[0]}, {c.L[1], c.U[1], c.V[1]}, {c.L[2], c.U[2], c.V[2]}};
+    double A[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+            A[j][i] = M[i1][j1] * M[i2][j2] - M[i1][j2] * M[i2][j1];  // adj = cofactor^T
+        }
+    const double det = M[0][0] * A[0][0] + M[0][1] * A[1][0] + M[0][2] * A[2][0];
+    double scale = 0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) scale = std::max(scale, std::fabs(M[i][j]));
+    if (!(std::fabs(det) > 1e-9 * scale * scale * scale)) return;  // degenerate basis: whole frame
     double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
     const float *b = fc.R.box[d->rank];
     for (int m = 0; m < 8; ++m) {
         double X[3] = {b[(m & 1) ? 3 : 0], b[(m & 2) ? 4 : 1], b[(m & 4) ? 5 : 2]};
         double rel[3] = {X[0] - c.E[0], X[1] - c.E[1], X[2] - c.E[2]};
-        double lam = (rel[0] * w[0] + rel[1] * w[1] + rel[2] * w[2]) / (wl * wl);
-        if (!(lam > 1e-9)) return;  // a corner at or behind the eye plane: whole frame
-        double su = 0.5 + (rel[0] * U[0] + rel[1] * U[1] + rel[2] * U[2]) / (lam * uu);
-        double sv = 0.5 + (rel[0] * V[0] + rel[1] * V[1] + rel[2] * V[2]) / (lam * vv);
+        double y[3];
+        for (int i = 0; i < 3; ++i) y[i] = (A[i][0] * rel[0] + A[i][1] * rel[1] + A[i][2] * rel[2]) / det;
+        const double lam = y[0];
+        if (!(lam > 1e-9 * std::sqrt(rel[0] * rel[0] + rel[1] * rel[1] + rel[2] * rel[2]) / std::max(scale, 1e-30)))
+            return;  // a corner at or behind the eye plane: whole frame
+        const double su = y[1] / lam, sv = y[2] / lam;
         x0 = std::min(x0, su * W); x1 = std::max(x1, su * W);
         y0 = std::min(y0, sv * H); y1 = std::max(y1, sv * H);
     }
+    if (!(x0 > -1e9 && x1 < 1e9 && y0 > -1e9 && y1 < 1e9)) return;
     rect[0] = (int)std::max(0.0, std::floor(x0) - 2.0);
     rect[1] = (int)std::max(0.0, std::floor(y0) - 2.0);
     rect[2] = (int)std::min((double)W, std::ceil(x1) + 2.0);
@@ -1841,8 +1875,14 @@ int dpr_set_frame(dpr_device dev, const dpr_frame_desc *fr) {
     if (fr->W <= 0 || fr->H <= 0 || fr->spp <= 0 || fr->spp > 65535 || fr->spp_batch <= 0 || fr->max_depth <= 0 ||
         fr->max_depth > 200 || fr->ao_k < 0 || fr->ao_k > 30)
         return fail(DPR_ERR_INVALID_ARG, "bad frame parameters");
-    dev->d.fr = *fr;
-    if (dev->d.fr.spp_batch > fr->spp) dev->d.fr.spp_batch = fr->spp;
+    dpr_frame_desc &f = dev->d.fr;  // field by field: the caller's padding bytes are not copied
+    memset(&f, 0, sizeof(f));
+    f.W = fr->W; f.H = fr->H; f.spp = fr->spp; f.spp_batch = std::min(fr->spp_batch, fr->spp);
+    f.max_depth = fr->max_depth; f.ao_k = fr->ao_k; f.ao_radius = fr->ao_radius;
+    for (int c = 0; c < 3; ++c) {
+        f.light_dir[c] = fr->light_dir[c]; f.E[c] = fr->E[c]; f.A[c] = fr->A[c]; f.B[c] = fr->B[c];
+    }
+    f.dt = fr->dt; f.seed = fr->seed; f.flags = fr->flags;
     dev->d.fr_set = true;
     return DPR_OK;
 }

@@ -100,13 +100,20 @@ __global__ void __launch_bounds__(256) k_part_prims(const PrimChunk *__restrict_
             const float *verts = (const float *)c.src;
             int64_t i0 = c.idx[3 * t], i1 = c.idx[3 * t + 1], i2 = c.idx[3 * t + 2];
             if (i0 < 0 || i0 >= c.nv || i1 < 0 || i1 >= c.nv || i2 < 0 || i2 >= c.nv) {
-                atomicExch(bad_index, 1);
+                atomicOr(bad_index, 1);
                 i0 = i1 = i2 = 0;
             }
             f3 v0 = mk(verts[3 * i0], verts[3 * i0 + 1], verts[3 * i0 + 2]);
             f3 v1 = mk(verts[3 * i1], verts[3 * i1 + 1], verts[3 * i1 + 2]);
             f3 v2 = mk(verts[3 * i2], verts[3 * i2 + 1], verts[3 * i2 + 2]);
             f3 e1 = sub(v1, v0), e2 = sub(v2, v0);
+            if (!(isfinite(v0.x) && isfinite(v0.y) && isfinite(v0.z) && isfinite(v1.x) && isfinite(v1.y) &&
+                  isfinite(v1.z) && isfinite(v2.x) && isfinite(v2.y) && isfinite(v2.z)))
+                atomicOr(bad_index, 2);
+            // reading R-DEGEN: a zero binary32 cross(e1, e2) (no area, no normal) is stored as
+            // e1 = e2 = 0, which P3's det == 0 test always rejects
+            const f3 ng = cross(e1, e2);
+            if (ng.x == 0.0f && ng.y == 0.0f && ng.z == 0.0f) e1 = e2 = mk(0.0f, 0.0f, 0.0f);
             prims[3 * g + 0] = make_float4(v0.x, v0.y, v0.z, __uint_as_float((uint32_t)g));
             prims[3 * g + 1] = make_float4(e1.x, e1.y, e1.z, 0.0f);
             prims[3 * g + 2] = make_float4(e2.x, e2.y, e2.z, 0.0f);
@@ -114,6 +121,8 @@ __global__ void __launch_bounds__(256) k_part_prims(const PrimChunk *__restrict_
             hi = mk(fmaxf(fmaxf(v0.x, v1.x), v2.x), fmaxf(fmaxf(v0.y, v1.y), v2.y), fmaxf(fmaxf(v0.z, v1.z), v2.z));
         } else {
             const float4 s = ((const float4 *)c.src)[t];
+            if (!(isfinite(s.x) && isfinite(s.y) && isfinite(s.z) && isfinite(s.w) && s.w > 0.0f))
+                atomicOr(bad_index, 2);  // radius must be > 0 and finite (dpr.h)
             prims[3 * g + 0] = make_float4(s.x, s.y, s.z, __uint_as_float((uint32_t)g | SPHERE_BIT));
             prims[3 * g + 1] = make_float4(s.w, 0.0f, 0.0f, 0.0f);
             prims[3 * g + 2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);

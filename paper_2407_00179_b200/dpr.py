@@ -24,6 +24,9 @@ DPR_FLAG_JITTER_CENTER = 1
 DPR_FLAG_DEBUG_DUMPS = 2
 DPR_FLAG_RING = 8
 DPR_FLAG_DELTA = 16
+# dpr_part_kind / dpr_memory (include/dpr.h)
+DPR_PART_TRIANGLES, DPR_PART_SPHERES, DPR_PART_BRICK = 0, 1, 2
+DPR_MEMORY_HOST, DPR_MEMORY_DEVICE, DPR_MEMORY_HOST_ASYNC = 0, 1, 2
 ERRORS = {-1: "DPR_ERR_INVALID_ARG", -2: "DPR_ERR_STATE", -3: "DPR_ERR_CUDA", -4: "DPR_ERR_NCCL",
           -5: "DPR_ERR_CONSISTENCY", -6: "DPR_ERR_OOM", -7: "DPR_ERR_QUEUE_OVERFLOW"}
 
@@ -206,12 +209,13 @@ class TorchAllocator:
 
 
 def part_desc(p, keep: list, device_arrays: bool = False, async_copy: bool = False) -> dpr_part_desc:
-    """dpr_inputs.Part (numpy, host) or a dict of torch CUDA tensors -> dpr_part_desc.
+    """A part object (kind, albedo, verts/idx | spheres | brick fields, as dpr_inputs.Part;
+    numpy host arrays or torch CUDA tensors) -> dpr_part_desc.
     async_copy: DPR_MEMORY_HOST_ASYNC (pinned host arrays, read until dpr_commit_world)."""
-    import dpr_inputs as di
     s = dpr_part_desc()
     s.kind = p.kind
-    s.memory = 1 if device_arrays else (2 if async_copy and p.kind != di.BRICK else 0)
+    s.memory = (DPR_MEMORY_DEVICE if device_arrays else
+                DPR_MEMORY_HOST_ASYNC if async_copy and p.kind != DPR_PART_BRICK else DPR_MEMORY_HOST)
     s.albedo = (_c.c_float * 3)(*[float(x) for x in p.albedo])
 
     def ptr(a, dtype):
@@ -224,10 +228,10 @@ def part_desc(p, keep: list, device_arrays: bool = False, async_copy: bool = Fal
         keep.append(a)
         return a.ctypes.data
 
-    if p.kind == di.TRIS:
+    if p.kind == DPR_PART_TRIANGLES:
         s.n_verts, s.verts = int(p.verts.shape[0]), ptr(p.verts, np.float32)
         s.n_tris, s.idx = int(p.idx.shape[0]), ptr(p.idx, np.int32)
-    elif p.kind == di.SPHERES:
+    elif p.kind == DPR_PART_SPHERES:
         s.n_spheres, s.spheres = int(p.spheres.shape[0]), ptr(p.spheres, np.float32)
     else:
         s.gdims = (_c.c_int32 * 3)(*p.gdims)

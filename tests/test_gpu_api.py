@@ -26,6 +26,15 @@ def test_state_errors_and_invalid_index():
             dev.commit_world()                      # index validated on the GPU
         assert e.value.code == -1 and "index" in str(e.value)
         dev.clear_parts()
+        for bad in (di.Part(0, di.SPHERES, spheres=di.f32([[0, 0, 0, 0]])),
+                    di.Part(0, di.SPHERES, spheres=di.f32([[0, np.nan, 0, 1]])),
+                    di.Part(0, di.TRIS, verts=di.f32([(0, 0, 0), (1, np.inf, 0), (0, 1, 0)]),
+                            idx=np.array([[0, 1, 2]], np.int32))):
+            dev.commit_part(bad)
+            with pytest.raises(dpr.DprError) as e:
+                dev.commit_world()                  # finiteness / radius validated on the GPU
+            assert e.value.code == -1 and "finite" in str(e.value)
+            dev.clear_parts()
         hint = di.Part(0, di.SPHERES, spheres=di.f32([[0, 0, 0, 1]]))
         dev.commit_part(hint)
         dev.commit_world()

@@ -330,3 +330,58 @@ def test_limits_and_ragged_batches():
     assert ((o.events[:, 7] >= 2) & ((o.events[:, 7] & 0x80000000) == 0)).any()  # depth-8 hits
     assert (o.occl >> 30).any()                                                    # AO ray 29 set
     assert_parity(g, o)
+
+
+def _with_collinear_triangles(parts, nranks, n=40, seed=9):
+    """Add exactly-collinear triangles (binary32 cross(e1,e2) == 0; reading R-DEGEN) spread
+    through the world: the generators never make them, a user may."""
+    rng = np.random.default_rng(seed)
+    f = np.float32
+    vs = []
+    while len(vs) < n:
+        v0 = rng.uniform(-1, 1, 3).astype(f)
+        e = rng.uniform(-0.4, 0.4, 3).astype(f)
+        v1, v2 = (v0 + e).astype(f), (v0 + f(2) * e).astype(f)  # e2 = 2*e1 exactly
+        e1, e2 = v1 - v0, v2 - v0
+        ng = np.array([e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                       e1[0] * e2[1] - e1[1] * e2[0]], f)
+        if not np.any(ng != 0):
+            vs.append(np.stack([v0, v1, v2]))
+    out = list(parts)
+    for r in range(nranks):
+        tv = np.concatenate(vs[r::nranks]).astype(f)
+        out.append(di.Part(r, di.TRIS, albedo=(0.9, 0.9, 0.9), verts=tv,
+                           idx=np.arange(tv.shape[0], dtype=np.int32).reshape(-1, 3)))
+    return out
+
+
+@pytest.mark.parametrize("nranks", [1, 2])
+def test_zero_area_triangles(nranks):
+    """Reading R-DEGEN on an un-narrowed input: collinear triangles are never hit (no NaN
+    normal, ray or pixel), on the GPU exactly as in the oracle."""
+    parts = _with_collinear_triangles(_random_world(5, nranks), nranks)
+    W = H = 48
+    cam = di.camera_basis((0.3, 0.8, -3.5), (0, 0, 0), (0, 1, 0), 45.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=2, spp_batch=2, max_depth=2, ao_k=2, ao_radius=0.6,
+                  light_dir=di.f32(di.normalize((0.4, 1, -0.3))), E=(1, 1, 1), A=(0.3, 0.3, 0.3))
+    g = gpu_render(parts, nranks, cam, fr)
+    o = oracle_render(parts, nranks, cam, fr)
+    assert np.isfinite(g[0]).all()
+    assert_parity(g, o)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_skewed_camera_basis(nranks):
+    """primary-generation culling (gen_rect) must hold for ANY camera basis -- here
+    an off-axis image region (L shifted by 0.3 U + 0.2 V: U, V no longer perpendicular to the
+    view axis) and a sheared V.  Routing and events bit-exact at N > 1."""
+    parts = _random_world(11, nranks)
+    W, H = 40, 32
+    cam = di.camera_basis((0.3, 0.8, -3.5), (0, 0, 0), (0, 1, 0), 45.0, W, H)
+    L, U, V = (np.asarray(x, np.float64) for x in (cam.L, cam.U, cam.V))
+    cam = di.Camera(E=cam.E, L=di.f32(L + 0.3 * U + 0.2 * V), U=cam.U, V=di.f32(V + 0.25 * U))
+    fr = di.Frame(W=W, H=H, spp=2, spp_batch=1, max_depth=2, ao_k=1, ao_radius=0.5,
+                  light_dir=di.f32(di.normalize((0.4, 1, -0.3))), E=(1, 1, 1), A=(0.3, 0.3, 0.3))
+    g = gpu_render(parts, nranks, cam, fr)
+    o = oracle_render(parts, nranks, cam, fr)
+    assert_parity(g, o)

@@ -254,3 +254,93 @@ def test_sphere_far_tangent_is_box_consistent():
             continue
         p = o.astype(np.float64) + h[0] * d.astype(np.float64)
         assert np.all(np.abs(p - c) <= r * (1 + 1e-3) + 1e-6), (p - c, r)
+
+
+def _plain_p3_hits(o, d, v0, e1, e2):
+    """Input selection only: P3 in binary32 WITHOUT the R-DEGEN rule (edges as given)."""
+    f = np.float32
+
+    def cross(a, b):
+        return np.array([a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2],
+                         a[0] * b[1] - a[1] * b[0]], f)
+
+    def dot(a, b):
+        return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]
+
+    pv = cross(d, e2)
+    det = dot(e1, pv)
+    if det == 0:
+        return False
+    inv = f(1) / det
+    tv = o - v0
+    uu = dot(tv, pv) * inv
+    if uu < 0 or uu > 1:
+        return False
+    qv = cross(tv, e1)
+    vv = dot(d, qv) * inv
+    if vv < 0 or uu + vv > 1:
+        return False
+    return dot(e2, qv) * inv > 0
+
+
+def _collinear_hits(n_want=20, seed=0):
+    """Rays aimed at points of exactly-collinear triangles (binary32 cross(e1,e2) == 0)
+    that plain P3 arithmetic reports as hit (det != 0 by rounding)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    f = np.float32
+    with np.errstate(all="ignore"):
+        while len(out) < n_want:
+            v0 = rng.uniform(-1, 1, 3).astype(f)
+            e = rng.uniform(-1, 1, 3).astype(f)
+            v1 = (v0 + e).astype(f)
+            v2 = (v0 + f(rng.uniform(0.2, 2.0)) * e).astype(f)
+            e1, e2 = v1 - v0, v2 - v0
+            ng = np.array([e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                           e1[0] * e2[1] - e1[1] * e2[0]], f)
+            if np.any(ng != 0):
+                continue
+            pt = (v0 + f(0.3) * (v1 - v0)).astype(f)
+            o = (pt + rng.uniform(-2, 2, 3)).astype(f)
+            d = (pt - o).astype(np.float64)
+            d = (d / np.linalg.norm(d)).astype(f)
+            if _plain_p3_hits(o, d, v0, e1, e2):
+                out.append((o, d, v0, v1, v2))
+    return out
+
+
+def test_zero_area_triangle_never_hit():
+    """Reading R-DEGEN: a triangle whose binary32 cross(e1, e2) is the zero vector has no area
+    and no normal (the P3 normal would be 0/0); it is never hit -- neither by the single
+    intersection test nor inside a rendered world (where such triangles stand in the ray's
+    way of a real one behind them)."""
+    cases = _collinear_hits()
+    for o, d, v0, v1, v2 in cases:
+        assert orc.tri_hit(o, d, v0, v1, v2) is None
+    # a world of only those triangles + a big quad behind them: every ray hits the quad
+    for o, d, v0, v1, v2 in cases[:5]:
+        c = (o + 50 * d.astype(np.float64)).astype(np.float32)
+        u = np.cross(d, [0.3, 0.5, 0.8]); u /= np.linalg.norm(u)
+        w = np.cross(d, u)
+        quad = [c + 40 * (a * u + b * w) for a, b in ((-1, -1), (1, -1), (1, 1), (-1, 1))]
+        qv, qi = di.quad_tris(quad)
+        parts = [di.Part(0, di.TRIS, albedo=(1, 1, 1), verts=di.f32([v0, v1, v2]),
+                         idx=np.array([[0, 1, 2]], np.int32)),
+                 di.Part(0, di.TRIS, albedo=(1, 1, 1), verts=qv, idx=qi)]
+        sc = orc.OracleScene(parts, 1)
+        t, i = sc.closest(o, d)
+        assert i in (1, 2) and 49 < t < 51, (t, i)
+        assert np.isfinite(t)
+
+
+def test_invalid_primitives_rejected():
+    """dpr.h: coordinates must be finite and sphere radii > 0; the oracle refuses such a
+    world as the GPU path does (DPR_ERR_INVALID_ARG)."""
+    ok = di.Part(0, di.SPHERES, spheres=di.f32([[0, 0, 0, 1]]))
+    orc.OracleScene([ok], 1)
+    for sph in ([0, 0, 0, 0], [0, 0, 0, -1], [np.nan, 0, 0, 1], [0, 0, 0, np.inf]):
+        with pytest.raises(ValueError):
+            orc.OracleScene([di.Part(0, di.SPHERES, spheres=di.f32([sph]))], 1)
+    with pytest.raises(ValueError):
+        orc.OracleScene([di.Part(0, di.TRIS, verts=di.f32([(0, 0, 0), (1, np.inf, 0), (0, 1, 0)]),
+                                 idx=np.array([[0, 1, 2]], np.int32))], 1)

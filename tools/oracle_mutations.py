@@ -63,6 +63,8 @@ MUTATIONS = [
      "if (!(t0 <= tbound)) continue;", "if (!(t0 < tbound)) continue;"),
     ("children_same_step", "P8b children traced in the resolving step",
      "ch.step = ray.step + 1;", "ch.step = ray.step;"),
+    ("degenerate_not_zeroed", "R-DEGEN: zero-area triangles keep their edges",
+     "if (ng.x == 0.0f && ng.y == 0.0f && ng.z == 0.0f) { *e1 = V3(0, 0, 0); *e2 = V3(0, 0, 0); }", ""),
     ("forward_double_step", "P8b a forward costs two steps",
      "at = nx;\n                    ray.step++;", "at = nx;\n                    ray.step += 2;"),
 ]
