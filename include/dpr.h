@@ -181,7 +181,21 @@ typedef struct {
     int64_t kernel_rays_local[2], kernel_nodes_local[2], kernel_tris_local[2], kernel_sphs_local[2],
         kernel_vols_local[2];
     int64_t bvh_nodes_local, bvh_levels_local; /* wide-BVH size of this rank's world */
+    int64_t step_loop_device; /* 1: the lock-step loop ran on the device (CUDA graph, no host
+                                 round trip per step); ms_trace_* are then globaltimer spans
+                                 (first CTA start .. last CTA end) and ms_exchange the time in
+                                 the step barrier */
+    int64_t graph_builds;     /* step-loop graphs captured so far on this device */
 } dpr_stats;
+
+/* Host-collective transport: a blocking, collective all-gather supplied by the caller (e.g.
+ * torch.distributed over gloo).  Every rank calls it with the same `bytes`; recv_host receives
+ * nranks*bytes, rank-major; returns 0 on success.  Called from the thread that called the
+ * dpr_* function. */
+typedef struct {
+    int (*allgather)(void *ctx, const void *send_host, void *recv_host, size_t bytes);
+    void *ctx;
+} dpr_host_collectives;
 
 /* ---- device lifetime ------------------------------------------------------------------ */
 
@@ -196,6 +210,16 @@ DPR_API int dpr_get_unique_id(uint8_t out[DPR_UNIQUE_ID_BYTES]);
  * handle; release it with dpr_release_device. */
 DPR_API int dpr_create_device(int rank, int nranks, int cuda_device, const uint8_t *uid,
                       void *cuda_stream, const dpr_allocator *alloc, dpr_device *out);
+
+/* COLLECTIVE: a rank whose control collectives (frame setup, step counts, barriers) go
+ * through `coll` instead of NCCL, and whose ray records move by the fused exchange only:
+ * shading / resolve kernels append straight into the destination rank's queues through CUDA
+ * IPC mappings (system-scope tail atomics), and rank 0 sums the peers' framebuffers through
+ * the same mappings (a7).  Processes may share one GPU (IPC works within a device), which is
+ * how the cross-process data plane is tested on a one-GPU box.  The step loop runs on the
+ * host in this mode (no kernel ever waits for another process).  coll is copied. */
+DPR_API int dpr_create_device_hostcoll(int rank, int nranks, int cuda_device, const dpr_host_collectives *coll,
+                               void *cuda_stream, const dpr_allocator *alloc, dpr_device *out);
 
 /* LOCAL test fixture: nranks virtual ranks in ONE process on ONE GPU (exchange by
  * device-to-device copies instead of NCCL).  out[nranks] receives the handles.  Render
@@ -277,6 +301,18 @@ DPR_API int dpr_get_debug(dpr_device dev, const uint32_t **events, const uint32_
 
 /* LOCAL: statistics of the last render (see dpr_stats). */
 DPR_API int dpr_get_stats(dpr_device dev, dpr_stats *out);
+
+/* LOCAL: per-step records of the last render (P8b lock-step steps, in order over all spp
+ * batches; GLOBAL, gathered over all ranks).  For step k < min(*nsteps, max_steps):
+ *   S_out[k][kind][src][dst]  rays forwarded / spawned src -> dst in step k (int64, N x N)
+ *   V_out[k][kind][r]         traces (visits) at rank r in step k
+ *   ms_out[k]                 step latency: max over ranks of the time from the step's start
+ *                             to its completed step boundary (globaltimer, ms)
+ *   sync_ms_out[k]            max over ranks of the time spent in the step barrier (device
+ *                             loop with peers; 0 otherwise)
+ * Any output may be NULL.  *nsteps = steps recorded (the last slot accumulates beyond 256). */
+DPR_API int dpr_get_step_stats(dpr_device dev, int max_steps, int64_t *S_out, int64_t *V_out, double *ms_out,
+                       double *sync_ms_out, int *nsteps);
 
 /* LOCAL: last error message of this thread ("" if none). */
 DPR_API const char *dpr_last_error(dpr_device dev);

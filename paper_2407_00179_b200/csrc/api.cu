@@ -11,9 +11,13 @@
 //   5. allgather of per-rank counters -> global routing matrices / visits / timings
 // The loopback group runs the same loop over N virtual ranks on one GPU with device copies
 // in place of NCCL (test fixture).
+#include <cuda.h>  // CUdeviceptr / CUresult only (the driver entry point is looked up at run time)
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -40,6 +44,13 @@ float exact_recip_pow2(float h) {
 }
 
 thread_local std::string g_err;
+
+// NVTX ranges (frame, phases, wavefront steps, kernel groups) for nsys timelines; no-ops
+// unless a tool is attached
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 
 struct Dev;
 
@@ -90,6 +101,10 @@ struct StatsMsg {
     int64_t S[3][DPR_MAX_RANKS];
     int64_t gen[3];
     double ms_frame;
+    int64_t nsteps;
+    int64_t stepS[MAX_STEP_REC][3][DPR_MAX_RANKS];  // cumulative after each step (this rank's row)
+    int64_t stepV[MAX_STEP_REC][3];
+    double step_ms[MAX_STEP_REC], step_sync_ms[MAX_STEP_REC];
 };
 
 struct Dev {
@@ -133,13 +148,40 @@ struct Dev {
     uint32_t path_cap = 0, occl_cap = 0;
     uint32_t *h_counts = nullptr;  // pinned: [N][2N+1]
     uint32_t *h_in = nullptr;      // pinned: [2]
+    uint64_t *h_app = nullptr;     // pinned: Counters.app ([2][DPR_MAX_RANKS])
+    uint64_t app_prev[2][DPR_MAX_RANKS] = {};  // host loop: Counters.app at the last boundary
     int frame_done = 0;
     int mapped_w = 0, mapped_h = 0;
     int spw = 16;  // max samples per warp in primary generation (env DPR_SPW; sweep r01)
     // exchange: 0 = per-step counts allgather + grouped ncclSend/ncclRecv (send-recv);
     //           1 = fused: kernels append straight into the destination rank's next queue
     //               (peer pointers, remote tail atomics); env DPR_EXCHANGE=fused|sendrecv
-    int exch = 0;
+    int exch = 1;
+    // step loop of the fused exchange: 1 = device-driven (one CUDA graph per spp batch: a
+    // conditional WHILE node over the step kernels + k_step_end, no host round trip per
+    // step), 0 = host loop (per-step counts to the host); env DPR_STEP_LOOP=host|device.
+    // The send-recv exchange always needs the host (NCCL message sizes are host arguments).
+    int step_loop = 1;
+    Buf b_rec;                                    // StepRec of the current frame
+    Buf b_more;                                   // [2] loop flags of the step graph
+    Buf b_mbox, b_seq;                            // step-barrier mailbox (IPC-exported), sequence
+    uint32_t *peer_mbox[DPR_MAX_RANKS] = {};
+    float4 *peer_fb[DPR_MAX_RANKS] = {};          // host-collective mode: peers' framebuffers / dumps
+    uint32_t *peer_events[DPR_MAX_RANKS] = {}, *peer_occl_dump[DPR_MAX_RANKS] = {};
+    cudaStream_t gstream = nullptr;               // capture stream of the step graph
+    cudaGraph_t graph = nullptr;                  // device-driven step loop (cached per signature)
+    cudaGraphExec_t gexec = nullptr;
+    uint64_t gkey = 0;
+    int64_t graph_kernels = 0;                    // kernel nodes per graph launch (counted at capture)
+    int64_t graph_builds = 0;
+    dpr_host_collectives hc{};                    // host-collective transport (no NCCL)
+    bool has_hc = false;
+    bool broken = false;                          // the communicator was aborted
+    double timeout_s = 600.0;                     // collective / step-barrier timeout
+    // per-step records of the last frame (global: every rank's rows)
+    int64_t nsteps_rec = 0;
+    std::vector<int64_t> step_S, step_V;          // [step][3][N][N], [step][3][N] (per-step deltas)
+    std::vector<double> step_ms, step_sync_ms;    // [step] max over ranks
     Buf b_tails;                                  // [parity][kind] next-queue tails (fused)
     PathRec *peer_path[2][DPR_MAX_RANKS] = {};    // fused: every rank's queues, both parities
     OcclRec *peer_occl[2][DPR_MAX_RANKS] = {};
@@ -281,10 +323,56 @@ bool valid_dev(dpr_device h) { return h != nullptr; }
 // ---------------------------------------------------------------------------------------
 // Collectives (NCCL or loopback).  `L` is the list of local ranks (1 for NCCL mode).
 // ---------------------------------------------------------------------------------------
+// Abort the communicator after an NCCL (async) error or a collective timeout: every later
+// collective call on this device returns DPR_ERR_NCCL (dpr.h: release the device).
+int abort_comm(Dev *d, const std::string &why) {
+    if (d->comm) ncclCommAbort(d->comm);
+    d->comm = nullptr;
+    d->broken = true;
+    return fail(DPR_ERR_NCCL, why + " (communicator aborted)");
+}
+
+// Wait for the device's stream.  With NCCL, poll the stream and ncclCommGetAsyncError, and give
+// up after timeout_s (a dead peer would otherwise hang the collective forever): abort.
+// Test hook DPR_TEST_NCCL_FAULT=1 reports an asynchronous NCCL error at the first poll.
+int wait_stream(Dev *d) {
+    if (!d->comm) {
+        CK(cudaStreamSynchronize(d->stream));
+        return DPR_OK;
+    }
+    const bool fault = getenv("DPR_TEST_NCCL_FAULT") && atoi(getenv("DPR_TEST_NCCL_FAULT")) == 1;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int it = 0;; ++it) {
+        const cudaError_t e = cudaStreamQuery(d->stream);
+        if (e == cudaSuccess) return DPR_OK;
+        if (e != cudaErrorNotReady)
+            return fail(DPR_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+        ncclResult_t ar = ncclSuccess;
+        if (ncclCommGetAsyncError(d->comm, &ar) != ncclSuccess || fault)
+            ar = ncclSystemError;
+        if (ar != ncclSuccess && ar != ncclInProgress)
+            return abort_comm(d, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar));
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > d->timeout_s) return abort_comm(d, "collective timed out");
+        if (it > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Collectives (NCCL, host collectives, or loopback).  `L` is the list of local ranks (1 for
+// NCCL / host-collective mode).
+// ---------------------------------------------------------------------------------------
 int allgather_host(std::vector<Dev *> &L, const std::vector<const void *> &send, size_t bytes,
                    std::vector<std::vector<char>> &out) {
     Dev *d0 = L[0];
     int N = d0->nranks;
+    if (d0->broken) return fail(DPR_ERR_NCCL, "communicator was aborted; release the device");
+    if (d0->has_hc) {  // host-collective transport (blocking, every rank calls it)
+        out.assign(1, std::vector<char>((size_t)N * bytes));
+        if (d0->hc.allgather(d0->hc.ctx, send[0], out[0].data(), bytes) != 0)
+            return fail(DPR_ERR_NCCL, "host-collective allgather failed");
+        return DPR_OK;
+    }
     if (!d0->comm) {  // loopback group or single rank without NCCL
         std::vector<char> all((size_t)N * bytes);
         for (size_t i = 0; i < L.size(); ++i) memcpy(all.data() + (size_t)L[i]->rank * bytes, send[i], bytes);
@@ -297,8 +385,18 @@ int allgather_host(std::vector<Dev *> &L, const std::vector<const void *> &send,
     NK(ncclAllGather(sbuf, rbuf, bytes, ncclUint8, d0->comm, d0->stream));
     out.assign(1, std::vector<char>((size_t)N * bytes));
     CK(cudaMemcpyAsync(out[0].data(), rbuf, bytes * N, cudaMemcpyDeviceToHost, d0->stream));
-    CK(cudaStreamSynchronize(d0->stream));
+    RET(wait_stream(d0));
     return DPR_OK;
+}
+
+// A barrier of the host-collective transport (after the local stream is idle).
+int hc_barrier(Dev *d) {
+    CK(cudaStreamSynchronize(d->stream));
+    std::vector<Dev *> L = {d};
+    const uint32_t one = 1;
+    std::vector<const void *> snd = {&one};
+    std::vector<std::vector<char>> o;
+    return allgather_host(L, snd, sizeof(one), o);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -661,14 +759,25 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
     int64_t ocap64 = rays * (1 + f.ao_k) * f.max_depth;
     if (ocap64 > 0xfffffff0ll) ocap64 = 0xfffffff0ll;
     uint32_t ocap = (uint32_t)ocap64;
-    RET(ensure(d, d->b_fb, sizeof(float4) * P_));
+    // IPC-exported (cudaMalloc'd) buffers: fused queues with NCCL or host collectives; in
+    // host-collective mode also the framebuffer and dumps (rank 0 reduces through mappings)
+    const bool ipc = d->exch && (d->comm || d->has_hc);
+    if (d->has_hc) {
+        RET(ensure_raw(d, d->b_fb, sizeof(float4) * P_, nullptr));
+    } else {
+        RET(ensure(d, d->b_fb, sizeof(float4) * P_));
+    }
     RET(ensure(d, d->b_fb_out, sizeof(float4) * P_));
     if (f.flags & DPR_FLAG_DEBUG_DUMPS) {
         size_t nd = (size_t)f.spp * f.max_depth * P_;
-        RET(ensure(d, d->b_events, sizeof(uint32_t) * nd));
-        RET(ensure(d, d->b_occl, sizeof(uint32_t) * nd));
+        if (d->has_hc) {
+            RET(ensure_raw(d, d->b_events, sizeof(uint32_t) * nd, nullptr));
+            RET(ensure_raw(d, d->b_occl, sizeof(uint32_t) * nd, nullptr));
+        } else {
+            RET(ensure(d, d->b_events, sizeof(uint32_t) * nd));
+            RET(ensure(d, d->b_occl, sizeof(uint32_t) * nd));
+        }
     }
-    const bool ipc = d->exch && d->comm;
     for (int i = 0; i < 2; ++i) {
         if (ipc) {
             RET(ensure_raw(d, d->b_path[i], sizeof(PathRec) * (size_t)pcap, nullptr));
@@ -692,6 +801,8 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
     d->path_cap = pcap;
     d->occl_cap = ocap;
     RET(ensure(d, d->b_ctr, sizeof(Counters)));
+    RET(ensure(d, d->b_rec, sizeof(StepRec)));
+    RET(ensure(d, d->b_more, sizeof(uint32_t) * 4));
     RET(ensure(d, d->b_counts, sizeof(uint32_t) * (2 * N + 1)));
     RET(ensure(d, d->b_in_count, sizeof(uint32_t) * 2));
     RET(ensure(d, d->b_fetch, sizeof(uint32_t) * 4));  // trace path/occl, march path/occl
@@ -700,6 +811,7 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
     if (!d->h_counts) {
         CK(cudaMallocHost(&d->h_counts, sizeof(uint32_t) * DPR_MAX_RANKS * (2 * DPR_MAX_RANKS + 1)));
         CK(cudaMallocHost(&d->h_in, sizeof(uint32_t) * 2));
+        CK(cudaMallocHost(&d->h_app, sizeof(uint64_t) * 2 * DPR_MAX_RANKS));
     }
     cudaStream_t s = d->stream;
     CK(cudaMemcpyAsync(d->b_part_lo.p, fc.part_lo.data(), sizeof(uint32_t) * fc.part_lo.size(), cudaMemcpyHostToDevice, s));
@@ -711,6 +823,10 @@ int frame_buffers(Dev *d, const FrameCtx &fc) {
         CK(cudaMemsetAsync(d->b_occl.p, 0, sizeof(uint32_t) * nd, s));
     }
     CK(cudaMemsetAsync(d->b_ctr.p, 0, sizeof(Counters), s));
+    memset(d->app_prev, 0, sizeof(d->app_prev));
+    CK(cudaMemsetAsync(d->b_rec.p, 0, sizeof(StepRec), s));
+    CK(cudaMemsetAsync(d->b_more.p, 0, sizeof(uint32_t) * 4, s));
+    CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 4, s));
     if (d->want_depth) {
         RET(ensure(d, d->b_depth, sizeof(uint32_t) * P_));
         launch_depth_init(P<uint32_t>(d->b_depth), P_, s);
@@ -786,6 +902,7 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.F.focus_dist = d->cam.focus_dist;
     gen_rect(d, fc, a.F.gen_rect);
     a.F.march_inline_min = march_inline_min(d->nsm);
+    a.F.march_g = march_g_env();
     a.R = fc.R;
     a.R.self = d->rank;
     a.W.wnodes = P<WNode>(d->b_wnodes);
@@ -835,6 +952,8 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.occl = (f.flags & DPR_FLAG_DEBUG_DUMPS) ? P<uint32_t>(d->b_occl) : nullptr;
     a.depth = d->want_depth ? P<uint32_t>(d->b_depth) : nullptr;
     a.ctr = P<Counters>(d->b_ctr);
+    a.rec = P<StepRec>(d->b_rec);
+    a.F.fuse_resolve = fuse_resolve_ok(a);
     return a;
 }
 
@@ -863,7 +982,7 @@ int gather_counts(std::vector<Dev *> &L, std::vector<int64_t> &C, unsigned &over
                            sizeof(uint32_t), cudaMemcpyDeviceToDevice, d0->stream));
         NK(ncclAllGather(d0->b_counts.p, recv, W, ncclUint32, d0->comm, d0->stream));
         CK(cudaMemcpyAsync(d0->h_counts, recv, sizeof(uint32_t) * W * N, cudaMemcpyDeviceToHost, d0->stream));
-        CK(cudaStreamSynchronize(d0->stream));
+        RET(wait_stream(d0));
         for (int r = 0; r < N; ++r) rows[r] = d0->h_counts + (size_t)r * W;
     }
     for (int src = 0; src < N; ++src)
@@ -873,18 +992,57 @@ int gather_counts(std::vector<Dev *> &L, std::vector<int64_t> &C, unsigned &over
     return DPR_OK;
 }
 
-// Fused exchange: every rank learns every rank's next-queue pointers and tails.  Loopback:
-// the virtual ranks' buffers directly.  NCCL mode: cudaIpc handles of the cudaMalloc'd queues
-// are allgathered over NCCL and opened (NVLink peer mappings), re-done when buffers change.
+// Fused exchange: every rank learns every rank's next-queue pointers and tails (and, for the
+// device-driven loop with peers, their step-barrier mailboxes; in host-collective mode their
+// framebuffer / dumps for the a7 reduction).  Loopback: the virtual ranks' buffers directly.
+// One rank without a transport: its own buffers.  NCCL / host collectives: cudaIpc handles of
+// the cudaMalloc'd buffers are allgathered and opened (NVLink peer mappings, or the same
+// device for processes sharing a GPU), re-done when a buffer changes.
+constexpr int IPC_NBUF = 8;  // path[0], path[1], occl[0], occl[1], tails, mbox, fb, events|occl
 struct IpcMsg {
-    cudaIpcMemHandle_t h[5];  // path[0], path[1], occl[0], occl[1], tails
+    cudaIpcMemHandle_t h[IPC_NBUF + 1];
+    uint64_t off[IPC_NBUF + 1];  // buffer offset inside the exported allocation
+    uint32_t have;               // bit k: buffer k exported
     uint64_t sig;
 };
+
+// The driver may place a small cudaMalloc inside a larger allocation; an IPC handle names the
+// whole allocation and opens at its base, so the buffer's offset travels with the handle
+// (cuMemGetAddressRange, looked up through the runtime: no link-time libcuda dependency).
+int alloc_base(void *p, char **base) {
+    typedef CUresult (*Fn)(CUdeviceptr *, size_t *, CUdeviceptr);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess) return fail(DPR_ERR_CUDA, "cuMemGetAddressRange not found");
+        fn = (Fn)f;
+    }
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, (CUdeviceptr)p) != CUDA_SUCCESS) return fail(DPR_ERR_CUDA, "cuMemGetAddressRange failed");
+    *base = (char *)b;
+    return DPR_OK;
+}
+
+int ensure_mbox(Dev *d) {
+    if (d->b_mbox.p) return DPR_OK;
+    const size_t mb = sizeof(uint32_t) * 2 * DPR_MAX_RANKS * 4;
+    if (d->comm || d->has_hc) RET(ensure_raw(d, d->b_mbox, mb, nullptr));
+    else RET(ensure(d, d->b_mbox, mb));
+    RET(ensure(d, d->b_seq, sizeof(uint32_t)));
+    CK(cudaMemsetAsync(d->b_mbox.p, 0, mb, d->stream));
+    CK(cudaMemsetAsync(d->b_seq.p, 0, sizeof(uint32_t), d->stream));
+    CK(cudaStreamSynchronize(d->stream));  // zeroed before any peer can store into it
+    return DPR_OK;
+}
 
 int fused_peers(std::vector<Dev *> &L) {
     Dev *d0 = L[0];
     const int N = d0->nranks;
-    if (d0->group) {
+    for (Dev *d : L) RET(ensure_mbox(d));
+    if (d0->group || (N == 1 && !d0->comm && !d0->has_hc)) {
         for (Dev *d : L)
             for (int r = 0; r < N; ++r) {
                 Dev *q = L[r];
@@ -893,20 +1051,28 @@ int fused_peers(std::vector<Dev *> &L) {
                     d->peer_occl[k][r] = P<OcclRec>(q->b_occlq[k]);
                 }
                 d->peer_tails[r] = P<uint32_t>(q->b_tails);
+                d->peer_mbox[r] = P<uint32_t>(q->b_mbox);
             }
         return DPR_OK;
     }
     Dev *d = d0;
-    void *mine[5] = {d->b_path[0].p, d->b_path[1].p, d->b_occlq[0].p, d->b_occlq[1].p, d->b_tails.p};
+    void *mine[IPC_NBUF + 1] = {d->b_path[0].p, d->b_path[1].p, d->b_occlq[0].p, d->b_occlq[1].p, d->b_tails.p,
+                                d->b_mbox.p, d->has_hc ? d->b_fb.p : nullptr,
+                                d->has_hc ? d->b_events.p : nullptr, d->has_hc ? d->b_occl.p : nullptr};
     uint64_t sig = 1469598103934665603ull;
     for (void *p : mine) sig = fnv1a(&p, sizeof(p), sig);
     IpcMsg msg;
     memset(&msg, 0, sizeof(msg));
-    for (int k = 0; k < 5; ++k) CK(cudaIpcGetMemHandle(&msg.h[k], mine[k]));
+    for (int k = 0; k <= IPC_NBUF; ++k)
+        if (mine[k]) {
+            char *base = nullptr;
+            RET(alloc_base(mine[k], &base));
+            CK(cudaIpcGetMemHandle(&msg.h[k], base));
+            msg.off[k] = (uint64_t)((char *)mine[k] - base);
+            msg.have |= 1u << k;
+        }
     msg.sig = sig;
-    std::vector<const void *> sends = {&msg};
-    std::vector<std::vector<char>> out;
-    // every rank reallocates at the same frames (same frame descriptor); the signature check
+    // every rank reallocates at the same frames (same frame descriptor); the combined signature
     // keeps the (collective) decision identical on all ranks anyway
     uint64_t all_sig = 0;
     {
@@ -916,65 +1082,328 @@ int fused_peers(std::vector<Dev *> &L) {
         for (int r = 0; r < N; ++r) all_sig = fnv1a(so[0].data() + 8 * r, 8, all_sig);
     }
     if (all_sig == d->ipc_sig && d->peer_tails[d->rank]) return DPR_OK;
+    std::vector<const void *> sends = {&msg};
+    std::vector<std::vector<char>> out;
     RET(allgather_host(L, sends, sizeof(IpcMsg), out));
     for (void *p : d->ipc_opened) cudaIpcCloseMemHandle(p);
     d->ipc_opened.clear();
     const IpcMsg *all = reinterpret_cast<const IpcMsg *>(out[0].data());
     for (int r = 0; r < N; ++r) {
-        void *ptr[5];
-        for (int k = 0; k < 5; ++k) {
+        void *ptr[IPC_NBUF + 1];
+        void *opened[IPC_NBUF + 1];  // one mapping per distinct allocation of the peer
+        for (int k = 0; k <= IPC_NBUF; ++k) {
+            ptr[k] = opened[k] = nullptr;
             if (r == d->rank) { ptr[k] = mine[k]; continue; }
-            CK(cudaIpcOpenMemHandle(&ptr[k], all[r].h[k], cudaIpcMemLazyEnablePeerAccess));
-            d->ipc_opened.push_back(ptr[k]);
+            if (!(all[r].have & (1u << k))) continue;
+            for (int j = 0; j < k; ++j)
+                if (opened[j] && memcmp(&all[r].h[j], &all[r].h[k], sizeof(cudaIpcMemHandle_t)) == 0)
+                    opened[k] = opened[j];
+            if (!opened[k]) {
+                CK(cudaIpcOpenMemHandle(&opened[k], all[r].h[k], cudaIpcMemLazyEnablePeerAccess));
+                d->ipc_opened.push_back(opened[k]);
+            }
+            ptr[k] = (char *)opened[k] + all[r].off[k];
         }
         d->peer_path[0][r] = (PathRec *)ptr[0];
         d->peer_path[1][r] = (PathRec *)ptr[1];
         d->peer_occl[0][r] = (OcclRec *)ptr[2];
         d->peer_occl[1][r] = (OcclRec *)ptr[3];
         d->peer_tails[r] = (uint32_t *)ptr[4];
+        d->peer_mbox[r] = (uint32_t *)ptr[5];
+        d->peer_fb[r] = (float4 *)ptr[6];
+        d->peer_events[r] = (uint32_t *)ptr[7];
+        d->peer_occl_dump[r] = (uint32_t *)ptr[8];
     }
     d->ipc_sig = all_sig;
     return DPR_OK;
 }
 
-// Fused step boundary: per-rank next-queue counts (path, occl) + overflow flags of all ranks.
-// NCCL mode: a 3-word allgather on the stream (it also orders every rank's appends of this
-// step before anyone's next step).  rows[r] = {path, occl, overflow}.
-int fused_sync(std::vector<Dev *> &L, const std::vector<int> &cur, std::vector<uint32_t> &rows) {
+// Fused step boundary of the HOST loop.  A queue is complete only when every rank that
+// appends into it has finished its step, so the boundary exchanges what each rank APPENDED
+// in the step, per destination and kind (Counters.app deltas), never a peer's tail: after the
+// exchange (the barrier) every rank knows every queue's length.  Loopback: the local ranks'
+// counters; NCCL / host collectives: an allgather of {appended[2][N], overflow} per rank.
+// in[r] = {path, occl} appended into rank r's next queue; returns the global total.
+struct AppMsg {
+    int64_t app[2][DPR_MAX_RANKS];
+    int64_t ovf;
+};
+
+int fused_sync(std::vector<Dev *> &L, std::vector<uint32_t> &in, int64_t &total, unsigned &ovf) {
     Dev *d0 = L[0];
     const int N = d0->nranks;
-    rows.assign((size_t)3 * N, 0);
-    if (!d0->comm) {
-        for (size_t i = 0; i < L.size(); ++i) {
-            Dev *d = L[i];
-            int nxt = cur[i] ^ 1;
-            CK(cudaMemcpyAsync(d->h_counts, P<uint32_t>(d->b_tails) + 2 * nxt, sizeof(uint32_t) * 2,
-                               cudaMemcpyDeviceToHost, d->stream));
-            CK(cudaMemcpyAsync(d->h_counts + 2, &P<Counters>(d->b_ctr)->overflow, sizeof(uint32_t),
-                               cudaMemcpyDeviceToHost, d->stream));
-        }
-        for (Dev *d : L) CK(cudaStreamSynchronize(d->stream));
-        for (Dev *d : L)
-            for (int k = 0; k < 3; ++k) rows[3 * d->rank + k] = d->h_counts[k];
-        return DPR_OK;
+    std::vector<AppMsg> mine(L.size());
+    for (size_t i = 0; i < L.size(); ++i) {
+        Dev *d = L[i];
+        Counters *c = P<Counters>(d->b_ctr);
+        CK(cudaMemcpyAsync(d->h_app, c->app, sizeof(c->app), cudaMemcpyDeviceToHost, d->stream));
+        CK(cudaMemcpyAsync(d->h_counts, &c->overflow, sizeof(uint32_t), cudaMemcpyDeviceToHost, d->stream));
     }
-    Dev *d = d0;
-    int nxt = cur[0] ^ 1;
-    RET(ensure(d, d->b_scratch, sizeof(uint32_t) * 3 * (N + 1)));
-    uint32_t *sb = P<uint32_t>(d->b_scratch), *rb = sb + 3;
-    CK(cudaMemcpyAsync(sb, P<uint32_t>(d->b_tails) + 2 * nxt, sizeof(uint32_t) * 2, cudaMemcpyDeviceToDevice, d->stream));
-    CK(cudaMemcpyAsync(sb + 2, &P<Counters>(d->b_ctr)->overflow, sizeof(uint32_t), cudaMemcpyDeviceToDevice, d->stream));
-    NK(ncclAllGather(sb, rb, 3, ncclUint32, d->comm, d->stream));
-    CK(cudaMemcpyAsync(d->h_counts, rb, sizeof(uint32_t) * 3 * N, cudaMemcpyDeviceToHost, d->stream));
-    CK(cudaStreamSynchronize(d->stream));
-    for (int k = 0; k < 3 * N; ++k) rows[k] = d->h_counts[k];
+    for (Dev *d : L) CK(cudaStreamSynchronize(d->stream));  // this rank's appends are final
+    for (size_t i = 0; i < L.size(); ++i) {
+        Dev *d = L[i];
+        memset(&mine[i], 0, sizeof(AppMsg));
+        for (int k = 0; k < 2; ++k)
+            for (int r = 0; r < N; ++r) {
+                const uint64_t now = d->h_app[k * DPR_MAX_RANKS + r];
+                mine[i].app[k][r] = (int64_t)(now - d->app_prev[k][r]);
+                d->app_prev[k][r] = now;
+            }
+        mine[i].ovf = d->h_counts[0];
+    }
+    std::vector<const void *> snd;
+    for (auto &m : mine) snd.push_back(&m);
+    std::vector<std::vector<char>> o;
+    RET(allgather_host(L, snd, sizeof(AppMsg), o));  // loopback: a copy; else the barrier
+    const AppMsg *all = reinterpret_cast<const AppMsg *>(o[0].data());
+    in.assign((size_t)2 * N, 0);
+    total = 0;
+    ovf = 0;
+    for (int src = 0; src < N; ++src) {
+        ovf |= (unsigned)all[src].ovf;
+        for (int k = 0; k < 2; ++k)
+            for (int r = 0; r < N; ++r) {
+                in[2 * r + k] += (uint32_t)all[src].app[k][r];
+                total += all[src].app[k][r];
+            }
+    }
     return DPR_OK;
 }
 
+// The step boundary kernel's arguments for the local ranks L; cur[i] = the parity rank i
+// consumed in this step (phase 1) or 1 (phase 0: the batch's primaries are in parity 0).
+StepEndArgs make_step_end(std::vector<Dev *> &L, const std::vector<int> &cur, int phase, bool barrier) {
+    StepEndArgs e;
+    memset(&e, 0, sizeof(e));
+    Dev *d0 = L[0];
+    e.nlocal = (int)L.size();
+    e.nranks = d0->nranks;
+    e.self = d0->rank;
+    e.phase = phase;
+    e.fused = d0->exch;
+    for (size_t i = 0; i < L.size(); ++i) {
+        Dev *d = L[i];
+        if (d->exch) {
+            e.next_tails[i] = P<uint32_t>(d->b_tails) + 2 * (cur[i] ^ 1);
+            e.cons_tails[i] = P<uint32_t>(d->b_tails) + 2 * cur[i];
+        }
+        e.fetch[i] = P<uint32_t>(d->b_fetch);
+        e.ctr[i] = P<Counters>(d->b_ctr);
+        e.rec[i] = P<StepRec>(d->b_rec);
+    }
+    e.barrier = barrier ? 1 : 0;
+    if (barrier) {
+        e.mbox_self = P<uint32_t>(d0->b_mbox);
+        for (int r = 0; r < d0->nranks; ++r) e.mbox_peer[r] = d0->peer_mbox[r];
+        e.seq = P<uint32_t>(d0->b_seq);
+        e.timeout_ns = (unsigned long long)(d0->timeout_s * 1e9);
+    }
+    e.more = P<uint32_t>(d0->b_more);
+    e.more_slot = -1;
+    return e;
+}
+
+// One step's kernels of local rank d, input parity cur.  n_path / n_occl: host-known queue
+// lengths (host loops: empty kinds are skipped, the march variant chosen on the host), or
+// UNKNOWN (device-driven loop: every kernel is launched and decides from the device count).
+constexpr uint32_t UNKNOWN = 0xffffffffu;
+struct StepTimers {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> path, occl;
+};
+int launch_step(Dev *d, const FrameCtx &fc, int cur, uint32_t n_path, uint32_t n_occl, int grid_p, int grid_o,
+                StepTimers *tm, int64_t &launches) {
+    StepArgs a = make_args(d, fc, cur);
+    const int grid_r = d->nsm * 8;
+    const bool dev = n_path == UNKNOWN;
+    if (n_path) {
+        Nvtx r("trace_path+shade");
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (tm) { e0 = next_event(d); e1 = next_event(d); CK(cudaEventRecord(e0, d->stream)); }
+        int nk = 1;
+        if (dev) {
+            k_launch_trace_path(a, grid_p, d->stream);
+            nk += launch_march_variants(a, false, d->stream);
+        } else {
+            nk = launch_trace_path(a, grid_p, n_path, d->stream);
+        }
+        if (tm) { CK(cudaEventRecord(e1, d->stream)); tm->path.push_back({e0, e1}); }
+        launch_shade_path(a, grid_r, d->stream);
+        launches += 1 + nk;
+        d->tpl++;
+    }
+    if (n_occl) {
+        Nvtx r("trace_occl+resolve");
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (tm) { e0 = next_event(d); e1 = next_event(d); CK(cudaEventRecord(e0, d->stream)); }
+        int nk = 1;
+        bool resolve = true;
+        if (dev) {
+            k_launch_trace_occl(a, grid_o, d->stream);
+            nk += launch_march_variants(a, true, d->stream);
+        } else {
+            nk = launch_trace_occl(a, grid_o, n_occl, d->stream);
+            // the host knows the length: skip the resolve launch when the trace resolves itself
+            resolve = !(a.F.fuse_resolve && !march_needed(a, n_occl));
+        }
+        if (tm) { CK(cudaEventRecord(e1, d->stream)); tm->occl.push_back({e0, e1}); }
+        if (resolve) launch_resolve_occl(a, grid_r, d->stream);
+        launches += (resolve ? 1 : 0) + nk;
+        d->tol++;
+    }
+    CK(cudaGetLastError());
+    return DPR_OK;
+}
+
+// Signature of everything the step graph bakes in (kernel arguments of both parities, grids,
+// the step-boundary arguments): the graph is re-captured when it changes.
+uint64_t graph_key(std::vector<Dev *> &L, const FrameCtx &fc, const std::vector<int> &grid_p,
+                   const std::vector<int> &grid_o, bool barrier) {
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < L.size(); ++i)
+        for (int c = 0; c < 2; ++c) {
+            StepArgs a = make_args(L[i], fc, c);
+            h = fnv1a(&a, sizeof(a), h);
+        }
+    for (int c = 0; c < 2; ++c) {
+        std::vector<int> cur(L.size(), c);
+        StepEndArgs e = make_step_end(L, cur, 1, barrier);
+        h = fnv1a(&e, sizeof(e), h);
+    }
+    h = fnv1a(grid_p.data(), sizeof(int) * grid_p.size(), h);
+    h = fnv1a(grid_o.data(), sizeof(int) * grid_o.size(), h);
+    const int b = barrier;
+    return fnv1a(&b, sizeof(b), h);
+}
+
+// Build the device-driven step loop of one spp batch (the batch's primaries are in parity 0):
+//   k_step_end(phase 0) -> k_loop_cond(init) -> WHILE(h_loop) {
+//       step kernels (parity 0) -> k_step_end -> IF(h_if) { step kernels (parity 1) ->
+//       k_step_end } -> k_loop_cond }
+// The loop body is unrolled twice so that every kernel node has fixed arguments (queue
+// parities alternate); each k_step_end decides "another step" on the device.
+int build_step_graph(std::vector<Dev *> &L, const FrameCtx &fc, const std::vector<int> &grid_p,
+                     const std::vector<int> &grid_o, bool barrier) {
+    Dev *d0 = L[0];
+    // capture on the library's own non-blocking stream (the caller's may be the legacy default
+    // stream, which cannot be captured); the graph is launched on the caller's stream
+    if (!d0->gstream) CK(cudaStreamCreateWithFlags(&d0->gstream, cudaStreamNonBlocking));
+    cudaStream_t s = d0->gstream;
+    struct Swap {  // launch_step issues on d->stream: point every local rank at the capture stream
+        std::vector<Dev *> &L;
+        std::vector<cudaStream_t> keep;
+        Swap(std::vector<Dev *> &l, cudaStream_t cs) : L(l) {
+            for (Dev *d : L) { keep.push_back(d->stream); d->stream = cs; }
+        }
+        ~Swap() { for (size_t i = 0; i < L.size(); ++i) L[i]->stream = keep[i]; }
+    } swap(L, s);
+    if (d0->gexec) { cudaGraphExecDestroy(d0->gexec); d0->gexec = nullptr; }
+    if (d0->graph) { cudaGraphDestroy(d0->graph); d0->graph = nullptr; }
+    int64_t kernels = 0;
+    march_grids_init();  // occupancy queries before the capture
+    cudaGraph_t g = nullptr;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_loop;
+    CK(cudaGraphConditionalHandleCreate(&h_loop, g, 0, cudaGraphCondAssignDefault));
+    // top level: initial total, then the WHILE node
+    CK(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    {
+        StepEndArgs e0 = make_step_end(L, std::vector<int>(L.size(), 1), 0, barrier);
+        e0.more_slot = 0;
+        launch_step_end(e0, s);
+        launch_loop_cond(P<uint32_t>(d0->b_more), h_loop, 1, s);
+        kernels += 2;
+    }
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t ndeps = 0;
+    cudaGraph_t cg = nullptr;
+    CK(cudaStreamGetCaptureInfo(s, &st, nullptr, &cg, &deps, &ndeps));
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h_loop;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CK(cudaGraphAddNode(&wnode, cg, deps, ndeps, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    CK(cudaStreamUpdateCaptureDependencies(s, &wnode, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t gout = nullptr;
+    CK(cudaStreamEndCapture(s, &gout));
+    // WHILE body: step A (parity 0) + boundary, IF node, loop condition
+    cudaGraphConditionalHandle h_if;
+    CK(cudaGraphConditionalHandleCreate(&h_if, body, 0, cudaGraphCondAssignDefault));
+    CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    for (size_t i = 0; i < L.size(); ++i) {
+        int64_t l = 0;
+        RET(launch_step(L[i], fc, 0, UNKNOWN, UNKNOWN, grid_p[i], grid_o[i], nullptr, l));
+        kernels += l;
+    }
+    {
+        StepEndArgs e = make_step_end(L, std::vector<int>(L.size(), 0), 1, barrier);
+        e.more_slot = 0;
+        e.set_if = 1;
+        e.h_if = h_if;
+        launch_step_end(e, s);
+        kernels++;
+    }
+    CK(cudaStreamGetCaptureInfo(s, &st, nullptr, &cg, &deps, &ndeps));
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h_if;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    CK(cudaGraphAddNode(&inode, cg, deps, ndeps, &ip));
+    cudaGraph_t ibody = ip.conditional.phGraph_out[0];
+    CK(cudaStreamUpdateCaptureDependencies(s, &inode, 1, cudaStreamSetCaptureDependencies));
+    launch_loop_cond(P<uint32_t>(d0->b_more), h_loop, 0, s);
+    kernels++;
+    CK(cudaStreamEndCapture(s, &gout));
+    // IF body: step B (parity 1) + boundary
+    CK(cudaStreamBeginCaptureToGraph(s, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    for (size_t i = 0; i < L.size(); ++i) {
+        int64_t l = 0;
+        RET(launch_step(L[i], fc, 1, UNKNOWN, UNKNOWN, grid_p[i], grid_o[i], nullptr, l));
+        kernels += l;
+    }
+    {
+        StepEndArgs e = make_step_end(L, std::vector<int>(L.size(), 1), 1, barrier);
+        e.more_slot = 1;
+        launch_step_end(e, s);
+        kernels++;
+    }
+    CK(cudaStreamEndCapture(s, &gout));
+    CK(cudaGraphInstantiate(&d0->gexec, g, 0));
+    d0->graph = g;
+    d0->graph_kernels = kernels;
+    d0->graph_builds++;
+    for (Dev *d : L) { d->tpl = 0; d->tol = 0; }  // launch_step counted the captured launches
+    return DPR_OK;
+}
+
+// a7 in host-collective mode: rank 0 sums the peers' framebuffers (and dumps) through the IPC
+// mappings after a barrier; a second barrier keeps the peers from clearing them too early.
+int hc_reduce(Dev *d, int64_t P_, size_t nd, bool dumps, int64_t &launches) {
+    RET(hc_barrier(d));
+    if (d->rank == 0)
+        for (int r = 1; r < d->nranks; ++r) {
+            launch_fb_accumulate(P<float4>(d->b_fb), d->peer_fb[r], P_, d->stream);
+            launches++;
+            if (dumps) {
+                launch_u32_accumulate(P<uint32_t>(d->b_events), d->peer_events[r], nd, d->stream);
+                launch_u32_accumulate(P<uint32_t>(d->b_occl), d->peer_occl_dump[r], nd, d->stream);
+                launches += 2;
+            }
+        }
+    return hc_barrier(d);
+}
+
 int render_group(std::vector<Dev *> &L) {
+    Nvtx nv_frame("dpr_render_frame");
     Dev *d0 = L[0];
     const int N = d0->nranks;
     for (Dev *d : L) {
+        if (d->broken) return fail(DPR_ERR_NCCL, "communicator was aborted; release the device");
         if (!d->world_ready) return fail(DPR_ERR_STATE, "dpr_commit_world has not been called");
         if (!d->cam_set || !d->fr_set) return fail(DPR_ERR_STATE, "camera and frame must be set before rendering");
         d->ev_used = 0;
@@ -987,13 +1416,18 @@ int render_group(std::vector<Dev *> &L) {
     CK(cudaEventRecord(ev_f0, d0->stream));
     FrameCtx fc;
     memset(&fc.R, 0, sizeof(fc.R));
-    RET(frame_setup(L, fc));
-    for (Dev *d : L) RET(frame_buffers(d, fc));
+    {
+        Nvtx r("frame_setup");
+        RET(frame_setup(L, fc));
+        for (Dev *d : L) RET(frame_buffers(d, fc));
+    }
     const bool fused = d0->exch != 0;
     if (fused) RET(fused_peers(L));
+    // device-driven step loop: fused exchange, not the host-collective transport
+    const bool dev_loop = fused && d0->step_loop && !d0->has_hc;
+    const bool barrier = dev_loop && !d0->group && (N > 1 || d0->comm);
     const int64_t P_ = (int64_t)f.W * f.H;
     const int nb = (f.spp + f.spp_batch - 1) / f.spp_batch;
-    int64_t steps = 0;
     int64_t launches = 0;
     std::vector<int> cur(L.size(), 0);
     std::vector<int> grid_p(L.size()), grid_o(L.size());
@@ -1001,13 +1435,26 @@ int render_group(std::vector<Dev *> &L) {
         grid_p[i] = std::max(1, trace_path_occupancy(TRACE_BLOCK)) * L[i]->nsm;
         grid_o[i] = std::max(1, trace_occl_occupancy(TRACE_BLOCK)) * L[i]->nsm;
     }
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_path, t_occl, t_exch, t_gen;
+    if (dev_loop) {
+        const uint64_t key = graph_key(L, fc, grid_p, grid_o, barrier);
+        if (!d0->gexec || key != d0->gkey) {
+            Nvtx r("build_step_graph");
+            RET(build_step_graph(L, fc, grid_p, grid_o, barrier));
+            d0->gkey = key;
+        }
+    }
+    StepTimers tm;
+    double ms_sync_host = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_exch, t_gen;
     std::vector<int64_t> C;
     for (int b = 0; b < nb; ++b) {
+        Nvtx nv_batch("spp_batch");
         int s0 = b * f.spp_batch, ns = std::min(f.spp_batch, f.spp - s0);
         for (size_t i = 0; i < L.size(); ++i) {
             Dev *d = L[i];
-            if (!fused) CK(cudaMemsetAsync(d->b_counts.p, 0, sizeof(uint32_t) * (2 * N + 1), d->stream));
+            // fused: every batch starts with its primaries in parity 0 (all tails are 0 here)
+            if (fused) cur[i] = 1;
+            else CK(cudaMemsetAsync(d->b_counts.p, 0, sizeof(uint32_t) * (2 * N + 1), d->stream));
             StepArgs a = make_args(d, fc, cur[i]);
             cudaEvent_t e0 = next_event(d), e1 = next_event(d);
             CK(cudaEventRecord(e0, d->stream));
@@ -1017,13 +1464,31 @@ int render_group(std::vector<Dev *> &L) {
             launches++;
             CK(cudaGetLastError());
         }
+        if (dev_loop) {
+            // the whole lock-step loop of the batch on the device: no host round trip per step
+            Nvtx r("step_loop_graph");
+            CK(cudaGraphLaunch(d0->gexec, d0->stream));
+            continue;
+        }
+        {   // host loops: the boundary kernel before the first step (timestamps, fetch heads)
+            StepEndArgs e = make_step_end(L, std::vector<int>(L.size(), 1), 0, false);
+            launch_step_end(e, d0->stream);
+            launches++;
+        }
         while (fused) {
+            Nvtx nv_step("step");
             // step boundary: every rank's next-queue counts (the allgather is the barrier)
-            std::vector<uint32_t> rows;
-            RET(fused_sync(L, cur, rows));
-            unsigned ovf = 0;
+            std::vector<uint32_t> in;
             int64_t total = 0;
-            for (int r = 0; r < N; ++r) { total += rows[3 * r] + rows[3 * r + 1]; ovf |= rows[3 * r + 2]; }
+            unsigned ovf = 0;
+            const auto h0 = std::chrono::steady_clock::now();
+            RET(fused_sync(L, in, total, ovf));
+            ms_sync_host += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+            if (getenv("DPR_DEBUG_STEPS")) {
+                fprintf(stderr, "[dpr rank %d] step boundary:", d0->rank);
+                for (int r = 0; r < N; ++r) fprintf(stderr, " r%d{%u,%u}", r, in[2 * r], in[2 * r + 1]);
+                fprintf(stderr, " ovf %u\n", ovf);
+            }
             if (ovf & 1u) return fail(DPR_ERR_QUEUE_OVERFLOW, "ray queue capacity exceeded; lower spp_batch");
             if (ovf & 2u) return fail(DPR_ERR_STATE, "BVH traversal stack overflow");
             if (ovf & 4u) return fail(DPR_ERR_STATE, "device bounds check failed (DPR_CHECKS build)");
@@ -1031,39 +1496,18 @@ int render_group(std::vector<Dev *> &L) {
             for (size_t i = 0; i < L.size(); ++i) {
                 Dev *d = L[i];
                 cur[i] ^= 1;
-                const uint32_t n_path = rows[3 * d->rank], n_occl = rows[3 * d->rank + 1];
-                CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 4, d->stream));
-                StepArgs a = make_args(d, fc, cur[i]);
-                const int grid_r = d->nsm * 8;
-                if (n_path) {
-                    cudaEvent_t e0 = next_event(d), e1 = next_event(d);
-                    CK(cudaEventRecord(e0, d->stream));
-                    const int nk = launch_trace_path(a, grid_p[i], n_path, d->stream);
-                    CK(cudaEventRecord(e1, d->stream));
-                    launch_shade_path(a, grid_r, d->stream);
-                    if (i == 0) t_path.push_back({e0, e1});
-                    launches += 1 + nk;
-                    d->tpl++;
-                }
-                if (n_occl) {
-                    cudaEvent_t e0 = next_event(d), e1 = next_event(d);
-                    CK(cudaEventRecord(e0, d->stream));
-                    a.F.fuse_resolve = fuse_resolve_ok(a, n_occl);
-                    const int nk = launch_trace_occl(a, grid_o[i], n_occl, d->stream);
-                    CK(cudaEventRecord(e1, d->stream));
-                    if (!a.F.fuse_resolve) launch_resolve_occl(a, grid_r, d->stream);
-                    if (i == 0) t_occl.push_back({e0, e1});
-                    launches += (a.F.fuse_resolve ? 0 : 1) + nk;
-                    d->tol++;
-                }
-                CK(cudaGetLastError());
+                const uint32_t n_path = in[2 * d->rank], n_occl = in[2 * d->rank + 1];
+                RET(launch_step(d, fc, cur[i], n_path, n_occl, grid_p[i], grid_o[i], i == 0 ? &tm : nullptr,
+                                launches));
             }
-            // the consumed queue's tails become the append targets of the step after next
-            for (size_t i = 0; i < L.size(); ++i)
-                CK(cudaMemsetAsync(P<uint32_t>(L[i]->b_tails) + 2 * cur[i], 0, sizeof(uint32_t) * 2, L[i]->stream));
-            steps++;
+            // boundary: per-step snapshot, consumed tails (append targets of the step after next)
+            // and fetch heads reset
+            StepEndArgs e = make_step_end(L, cur, 1, false);
+            launch_step_end(e, d0->stream);
+            launches++;
         }
         while (!fused) {
+            Nvtx nv_step("step");
             unsigned ovf = 0;
             RET(gather_counts(L, C, ovf));
             if (ovf & 1u) return fail(DPR_ERR_QUEUE_OVERFLOW, "ray queue capacity exceeded; lower spp_batch");
@@ -1073,6 +1517,7 @@ int render_group(std::vector<Dev *> &L) {
             for (int64_t v : C) total += v;
             if (total == 0) break;
             // exchange: records for other ranks -> their next input queues
+            Nvtx nv_x("exchange");
             cudaEvent_t ex0 = next_event(d0), ex1 = next_event(d0);
             CK(cudaEventRecord(ex0, d0->stream));
             std::vector<std::vector<int64_t>> offs(L.size() * 2);
@@ -1137,36 +1582,16 @@ int render_group(std::vector<Dev *> &L) {
                 cur[i] ^= 1;
                 CK(cudaMemcpyAsync(d->b_in_count.p, d->h_in, sizeof(uint32_t) * 2, cudaMemcpyHostToDevice, d->stream));
                 CK(cudaMemsetAsync(d->b_counts.p, 0, sizeof(uint32_t) * (2 * N + 1), d->stream));
-                CK(cudaMemsetAsync(d->b_fetch.p, 0, sizeof(uint32_t) * 4, d->stream));
-                StepArgs a = make_args(d, fc, cur[i]);
-                const int grid_r = d->nsm * 8;
-                if (d->h_in[0]) {
-                    cudaEvent_t e0 = next_event(d), e1 = next_event(d);
-                    CK(cudaEventRecord(e0, d->stream));
-                    const int nk = launch_trace_path(a, grid_p[i], d->h_in[0], d->stream);
-                    CK(cudaEventRecord(e1, d->stream));
-                    launch_shade_path(a, grid_r, d->stream);
-                    if (i == 0) t_path.push_back({e0, e1});
-                    launches += 1 + nk;
-                    d->tpl++;
-                }
-                if (d->h_in[1]) {
-                    cudaEvent_t e0 = next_event(d), e1 = next_event(d);
-                    CK(cudaEventRecord(e0, d->stream));
-                    a.F.fuse_resolve = fuse_resolve_ok(a, d->h_in[1]);
-                    const int nk = launch_trace_occl(a, grid_o[i], d->h_in[1], d->stream);
-                    CK(cudaEventRecord(e1, d->stream));
-                    if (!a.F.fuse_resolve) launch_resolve_occl(a, grid_r, d->stream);
-                    if (i == 0) t_occl.push_back({e0, e1});
-                    launches += (a.F.fuse_resolve ? 0 : 1) + nk;
-                    d->tol++;
-                }
-                CK(cudaGetLastError());
+                RET(launch_step(d, fc, cur[i], d->h_in[0], d->h_in[1], grid_p[i], grid_o[i], i == 0 ? &tm : nullptr,
+                                launches));
             }
-            steps++;
+            StepEndArgs e = make_step_end(L, cur, 1, false);
+            launch_step_end(e, d0->stream);
+            launches++;
         }
     }
     // a7: framebuffer (+ dumps) reduction to rank 0, normalisation by spp
+    Nvtx nv_red("reduce");
     cudaEvent_t r0 = next_event(d0), r1 = next_event(d0);
     CK(cudaEventRecord(r0, d0->stream));
     const size_t nd = (size_t)f.spp * f.max_depth * P_;
@@ -1182,6 +1607,8 @@ int render_group(std::vector<Dev *> &L) {
                 launches += 2;
             }
         }
+    } else if (d0->has_hc) {
+        RET(hc_reduce(d0, P_, nd, dumps, launches));
     } else if (d0->comm) {
         Dev *d = d0;
         NK(ncclGroupStart());
@@ -1201,7 +1628,7 @@ int render_group(std::vector<Dev *> &L) {
     CK(cudaEventRecord(r1, d0->stream));
     ev_f1 = next_event(d0);
     CK(cudaEventRecord(ev_f1, d0->stream));
-    CK(cudaStreamSynchronize(d0->stream));
+    RET(wait_stream(d0));
     CK(cudaGetLastError());
     // stats
     auto sum_ms = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v) {
@@ -1213,8 +1640,30 @@ int render_group(std::vector<Dev *> &L) {
     cudaEventElapsedTime(&fms, ev_f0, ev_f1);
     std::vector<StatsMsg> msgs(L.size());
     std::vector<Counters> ctr(L.size());
+    std::vector<StepRec> rec(L.size());
     for (size_t i = 0; i < L.size(); ++i) {
         CK(cudaMemcpy(&ctr[i], L[i]->b_ctr.p, sizeof(Counters), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&rec[i], L[i]->b_rec.p, sizeof(StepRec), cudaMemcpyDeviceToHost));
+    }
+    for (size_t i = 0; i < L.size(); ++i) {
+        if (rec[i].err & 0x100u) return abort_comm(L[i], "step barrier timed out (a peer did not reach the step boundary)");
+        if (rec[i].err & 1u) return fail(DPR_ERR_QUEUE_OVERFLOW, "ray queue capacity exceeded; lower spp_batch");
+        if (rec[i].err & 2u) return fail(DPR_ERR_STATE, "BVH traversal stack overflow");
+        if (rec[i].err & 4u) return fail(DPR_ERR_STATE, "device bounds check failed (DPR_CHECKS build)");
+    }
+    const int64_t steps = rec[0].step;
+    const int nrec = (int)std::min<int64_t>(steps, MAX_STEP_REC);
+    double kt_ms[2] = {0, 0}, sync_ms = 0;
+    if (dev_loop) {  // trace kernels inside the graph: first-start .. last-end globaltimer stamps
+        for (int k = 0; k < nrec; ++k) {
+            for (int q = 0; q < 2; ++q) {
+                const unsigned long long a = ~rec[0].kt[k][q][0], e = rec[0].kt[k][q][1];
+                if (rec[0].kt[k][q][0] && e >= a) kt_ms[q] += (double)(e - a) * 1e-6;
+            }
+            sync_ms += rec[0].t_sync[k] * 1e-6;
+        }
+    }
+    for (size_t i = 0; i < L.size(); ++i) {
         StatsMsg &m = msgs[i];
         memset(&m, 0, sizeof(m));
         for (int k = 0; k < 3; ++k) {
@@ -1223,6 +1672,15 @@ int render_group(std::vector<Dev *> &L) {
             for (int r = 0; r < N; ++r) m.S[k][r] = (int64_t)ctr[i].S[k][r];
         }
         m.ms_frame = fms;
+        m.nsteps = nrec;
+        for (int k = 0; k < nrec; ++k) {
+            for (int q = 0; q < 3; ++q) {
+                for (int r = 0; r < N; ++r) m.stepS[k][q][r] = (int64_t)rec[i].S[k][q][r];
+                m.stepV[k][q] = (int64_t)rec[i].V[k][q];
+            }
+            m.step_ms[k] = (double)(rec[i].t_end[k] - rec[i].t_begin[k]) * 1e-6;
+            m.step_sync_ms[k] = rec[i].t_sync[k] * 1e-6;
+        }
     }
     std::vector<const void *> sends;
     for (auto &m : msgs) sends.push_back(&m);
@@ -1257,6 +1715,24 @@ int render_group(std::vector<Dev *> &L) {
             }
             mx = std::max(mx, all[r].ms_frame);
         }
+        // per-step matrices: deltas of the cumulative snapshots, every rank's row
+        d->nsteps_rec = nrec;
+        d->step_S.assign((size_t)nrec * 3 * N * N, 0);
+        d->step_V.assign((size_t)nrec * 3 * N, 0);
+        d->step_ms.assign(nrec, 0.0);
+        d->step_sync_ms.assign(nrec, 0.0);
+        for (int k = 0; k < nrec; ++k)
+            for (int r = 0; r < N; ++r) {
+                const StatsMsg &m = all[r];
+                for (int q = 0; q < 3; ++q) {
+                    for (int c = 0; c < N; ++c)
+                        d->step_S[(((size_t)k * 3 + q) * N + r) * N + c] =
+                            m.stepS[k][q][c] - (k ? m.stepS[k - 1][q][c] : 0);
+                    d->step_V[((size_t)k * 3 + q) * N + r] = m.stepV[k][q] - (k ? m.stepV[k - 1][q] : 0);
+                }
+                d->step_ms[k] = std::max(d->step_ms[k], m.step_ms[k]);
+                d->step_sync_ms[k] = std::max(d->step_sync_ms[k], m.step_sync_ms[k]);
+            }
         const KernelCounters &a = ctr[i].kc[0], &o = ctr[i].kc[1];
         st.node_visits_local = (int64_t)(a.nodes + o.nodes);
         st.tri_tests_local = (int64_t)(a.tris + o.tris);
@@ -1282,11 +1758,29 @@ int render_group(std::vector<Dev *> &L) {
         st.bvh_levels_local = d->bvh_levels;
         st.ms_frame = fms;
         st.ms_frame_max = mx;
+        st.step_loop_device = dev_loop ? 1 : 0;
+        st.graph_builds = d0->graph_builds;
         if (i == 0) {
             st.ms_gen = sum_ms(t_gen);
-            st.ms_trace_path = sum_ms(t_path);
-            st.ms_trace_occl = sum_ms(t_occl);
-            st.ms_exchange = sum_ms(t_exch);
+            if (dev_loop) {
+                st.ms_trace_path = kt_ms[0];
+                st.ms_trace_occl = kt_ms[1];
+                st.ms_exchange = sync_ms;  // fused: appends are inside the kernels; the barrier
+                st.trace_path_launches = nrec;
+                st.trace_occl_launches = nrec;
+                // graph: per batch 2 (initial boundary + condition); per step its kernels and
+                // boundary; per WHILE iteration one condition kernel (counted on the device)
+                uint32_t iters = 0;
+                CK(cudaMemcpy(&iters, P<uint32_t>(d0->b_more) + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+                const int64_t per_step = (d0->graph_kernels - 5) / 2 + 1;
+                st.kernel_launches_local = d->build_launches + launches + (int64_t)nb * 2 + steps * per_step + iters;
+            } else {
+                st.ms_trace_path = sum_ms(tm.path);
+                st.ms_trace_occl = sum_ms(tm.occl);
+                // send-recv: grouped send/recv (CUDA events); fused host loop: the host-side
+                // step boundary (counts to the host + barrier), wall clock
+                st.ms_exchange = fused ? ms_sync_host : sum_ms(t_exch);
+            }
             float rms = 0;
             cudaEventElapsedTime(&rms, r0, r1);
             st.ms_reduce = rms;
@@ -1383,7 +1877,9 @@ int init_dev(Dev *d, int rank, int nranks, int cuda_device, void *stream, const 
     if (const char *e = getenv("DPR_SPW")) d->spw = std::max(1, atoi(e));
     if (const char *e = getenv("DPR_BUILDER"))
         d->builder = strcmp(e, "ploc") == 0 ? 0 : strcmp(e, "karras") == 0 ? 2 : 1;
-    if (const char *e = getenv("DPR_EXCHANGE")) d->exch = strcmp(e, "fused") == 0 ? 1 : 0;
+    if (const char *e = getenv("DPR_EXCHANGE")) d->exch = strcmp(e, "sendrecv") == 0 ? 0 : 1;
+    if (const char *e = getenv("DPR_STEP_LOOP")) d->step_loop = strcmp(e, "host") == 0 ? 0 : 1;
+    if (const char *e = getenv("DPR_TIMEOUT_S")) d->timeout_s = std::max(0.001, atof(e));
     return DPR_OK;
 }
 
@@ -1410,10 +1906,20 @@ void release_bufs(Dev *d) {
     dfree(d, d->b_tails);
     if (d->h_counts) cudaFreeHost(d->h_counts);
     if (d->h_in) cudaFreeHost(d->h_in);
+    if (d->h_app) cudaFreeHost(d->h_app);
+    d->h_app = nullptr;
     d->h_counts = nullptr;
     d->h_in = nullptr;
     for (auto e : d->ev_pool) cudaEventDestroy(e);
     d->ev_pool.clear();
+    if (d->gexec) cudaGraphExecDestroy(d->gexec);
+    if (d->graph) cudaGraphDestroy(d->graph);
+    if (d->gstream) cudaStreamDestroy(d->gstream);
+    d->gexec = nullptr;
+    d->graph = nullptr;
+    d->gstream = nullptr;
+    Buf *xs[] = {&d->b_rec, &d->b_more, &d->b_mbox, &d->b_seq};
+    for (Buf *b : xs) dfree(d, *b);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1424,7 +1930,8 @@ Dev *local_view(Dev *d, bool replicated = false) {
     if (!d->lv) {
         Dev *v = new Dev();
         v->rank = 0; v->nranks = 1; v->cuda_dev = d->cuda_dev; v->nsm = d->nsm; v->stream = d->stream;
-        v->alloc = d->alloc; v->has_alloc = d->has_alloc; v->exch = 0; v->spw = d->spw;
+        v->alloc = d->alloc; v->has_alloc = d->has_alloc; v->exch = d->exch; v->spw = d->spw;
+        v->step_loop = d->step_loop;
         d->lv = v;
     }
     Dev *v = d->lv;
@@ -1707,6 +2214,35 @@ int dpr_create_device(int rank, int nranks, int cuda_device, const uint8_t *uid,
         }
     }
     *out = h;
+    return DPR_OK;
+}
+
+int dpr_create_device_hostcoll(int rank, int nranks, int cuda_device, const dpr_host_collectives *coll,
+                               void *cuda_stream, const dpr_allocator *alloc, dpr_device *out) {
+    if (!out || !coll || !coll->allgather || nranks < 1 || nranks > DPR_MAX_RANKS || rank < 0 || rank >= nranks)
+        return fail(DPR_ERR_INVALID_ARG, "bad rank/nranks/collectives/out");
+    dpr_device h = new dpr_device_s();
+    int rc = init_dev(&h->d, rank, nranks, cuda_device, cuda_stream, alloc);
+    if (rc != DPR_OK) { delete h; return rc; }
+    h->d.hc = *coll;
+    h->d.has_hc = true;
+    h->d.exch = 1;  // ray records move only by the fused (peer-memory) exchange
+    *out = h;
+    return DPR_OK;
+}
+
+int dpr_get_step_stats(dpr_device dev, int max_steps, int64_t *S_out, int64_t *V_out, double *ms_out,
+                       double *sync_ms_out, int *nsteps) {
+    if (!valid_dev(dev) || max_steps < 0 || !nsteps) return fail(DPR_ERR_INVALID_ARG, "null argument");
+    Dev *d = &dev->d;
+    if (!d->frame_done) return fail(DPR_ERR_STATE, "no frame rendered");
+    const int N = d->nranks;
+    const int n = (int)std::min<int64_t>(d->nsteps_rec, max_steps);
+    if (S_out) memcpy(S_out, d->step_S.data(), sizeof(int64_t) * (size_t)n * 3 * N * N);
+    if (V_out) memcpy(V_out, d->step_V.data(), sizeof(int64_t) * (size_t)n * 3 * N);
+    if (ms_out) memcpy(ms_out, d->step_ms.data(), sizeof(double) * n);
+    if (sync_ms_out) memcpy(sync_ms_out, d->step_sync_ms.data(), sizeof(double) * n);
+    *nsteps = (int)d->nsteps_rec;
     return DPR_OK;
 }
 

@@ -43,6 +43,10 @@ struct Counters {
     unsigned long long S[3][DPR_MAX_RANKS];
     unsigned long long gen[3];
     KernelCounters kc[2];
+    // records this rank appended to each destination's queue, per kind (0 path, 1 occlusion),
+    // self included (cumulative over the frame): a receiver's queue is complete only when every
+    // sender has finished its step, so step boundaries exchange these, never a peer's tail
+    unsigned long long app[2][DPR_MAX_RANKS];
     unsigned int overflow;  // bit0 queue overflow, bit1 traversal stack overflow
     unsigned int pad;
 };

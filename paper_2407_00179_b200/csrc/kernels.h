@@ -87,10 +87,12 @@ struct FrameDev {
     int gen_rect[4];                   // pixels [x0,x1) x [y0,y1) whose rays can meet this rank's
                                        // padded box (conservative screen projection); others are
                                        // generated only by their pixel owner
-    int fuse_resolve;                  // k_trace_occl resolves its rays itself (one rank, no ring,
-                                       // no separate march kernel): k_resolve_occl is not launched
+    int fuse_resolve;                  // k_trace_occl may resolve its rays itself (one rank, no ring);
+                                       // it does unless the queue goes to k_march_occl (decided on
+                                       // the device from the queue length: fuse_resolve_dev)
     uint32_t march_inline_min;         // P10 march inside the trace kernels when the queue holds
                                        // at least this many rays, else in k_march_* (G lanes/ray)
+    int march_g;                       // forced lanes per ray of k_march_* (0: from the ray count)
 };
 
 struct QueuesDev {
@@ -107,6 +109,22 @@ struct QueuesDev {
     uint32_t *fetch;            // [2] persistent-kernel fetch heads
 };
 
+// Per-step record of one rank (device memory, zeroed per frame): the step counter, per-step
+// cumulative routing rows / visits (the per-step matrices of P8b) and globaltimer stamps.
+// Steps beyond MAX_STEP_REC accumulate into the last slot.
+constexpr int MAX_STEP_REC = 256;
+struct StepRec {
+    uint32_t step;                                      // steps completed this frame (all batches)
+    uint32_t err;                                       // overflow bits | 0x100 barrier timeout
+    unsigned long long app_prev[2];                     // appended totals (path, occl) at the last boundary
+    unsigned long long t_begin[MAX_STEP_REC + 1];       // globaltimer when step k could start
+    unsigned long long t_end[MAX_STEP_REC];             // ... when its step boundary completed
+    unsigned long long t_sync[MAX_STEP_REC];            // ns inside the step barrier (fused, N>1)
+    unsigned long long kt[MAX_STEP_REC][2][2];          // trace kernel (path, occl): ~first start, last end
+    unsigned long long S[MAX_STEP_REC][3][DPR_MAX_RANKS];  // cumulative S row of this rank after step k
+    unsigned long long V[MAX_STEP_REC][3];                 // cumulative visits of this rank after step k
+};
+
 struct StepArgs {
     FrameDev F;
     Routing R;
@@ -118,13 +136,53 @@ struct StepArgs {
     uint32_t *occl;
     uint32_t *depth;   // per-pixel min primary hit t (float bits; +inf init) or nullptr
     Counters *ctr;
+    StepRec *rec;      // trace kernels stamp their start / end into rec->kt[rec->step]
 };
+
+// Step boundary (one block): per-step snapshot of the routing rows and visits, reset of the
+// consumed queue tails and fetch heads, the global next-queue total (local ranks, plus the
+// peers' through a mailbox barrier over NVLink peer memory when barrier = 1), and the
+// conditional handles of the device-driven step loop.
+struct StepEndArgs {
+    int nlocal;                               // ranks handled here (loopback: all; else 1)
+    int nranks, self;                         // world size; this rank (barrier mode)
+    int phase;                                // 0: before a batch's first step, 1: end of a step
+    int fused;                                // next counts are the fused tails (local ranks; with
+                                              // the barrier, each rank publishes what IT appended)
+    const uint32_t *next_tails[DPR_MAX_RANKS];  // fused: {path, occl} of the next parity
+    uint32_t *cons_tails[DPR_MAX_RANKS];      // fused: consumed parity tails -> 0 (phase 1)
+    uint32_t *fetch[DPR_MAX_RANKS];           // 4 fetch heads per local rank -> 0
+    const Counters *ctr[DPR_MAX_RANKS];
+    StepRec *rec[DPR_MAX_RANKS];
+    int barrier;                              // 1: exchange counts with the peers (mailboxes)
+    uint32_t *mbox_self;                      // [2][DPR_MAX_RANKS][4] {seq, path, occl, err}
+    uint32_t *mbox_peer[DPR_MAX_RANKS];       // every rank's mailbox (peer mappings; self too)
+    uint32_t *seq;                            // barrier sequence number (persistent)
+    unsigned long long timeout_ns;
+    uint32_t *more;                           // [2]: "another step" flags for the loop graph
+    int more_slot;                            // which flag this boundary writes (-1: none)
+    int set_if;                               // set h_if to "another step"
+    cudaGraphConditionalHandle h_if;
+};
+void launch_step_end(const StepEndArgs &a, cudaStream_t s);
+// WHILE handle of the loop graph := more[0] && more[1] (end of the unrolled double step)
+void launch_loop_cond(uint32_t *more, cudaGraphConditionalHandle h, int init, cudaStream_t s);
 
 void launch_gen_primary(const StepArgs &a, int s0, int nsamp, int spw_max, cudaStream_t s);
 // n: input rays (sizes the march launch); returns the number of kernels launched
 uint32_t march_inline_min(int nsm);
-// whether the occlusion trace of a queue of n rays resolves them itself (sets a.F.fuse_resolve)
-bool fuse_resolve_ok(const StepArgs &a, uint32_t n);
+int march_g_env();  // DPR_MARCH "<min>:G" override of the k_march_* lanes per ray (0: auto)
+// the host-side part of the occlusion trace's own resolve (one rank, no ring, env); the
+// kernel also requires that the queue is not marched by k_march_occl
+bool fuse_resolve_ok(const StepArgs &a);
+// launch every k_march_* variant that a queue of unknown length could need (device loop):
+// each exits unless the device-side choice for the actual length is its own
+int launch_march_variants(const StepArgs &a, bool any, cudaStream_t s);
+bool march_needed(const StepArgs &a, uint32_t n);  // a queue of n rays goes to k_march_*
+void march_grids_init();                            // occupancy-derived grids (before a capture)
+// the trace kernels alone (device loop: the march variants are launched separately)
+void k_launch_trace_path(const StepArgs &a, int grid, cudaStream_t s);
+void k_launch_trace_occl(const StepArgs &a, int grid, cudaStream_t s);
 int launch_trace_path(const StepArgs &a, int grid, uint32_t n, cudaStream_t s);
 int launch_trace_occl(const StepArgs &a, int grid, uint32_t n, cudaStream_t s);
 void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s);

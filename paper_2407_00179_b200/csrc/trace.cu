@@ -86,6 +86,7 @@ __device__ __forceinline__ void warp_count(bool want, int key, unsigned long lon
 // smem: cnt[DPR_MAX_RANKS], base[DPR_MAX_RANKS] provided by the caller.
 __device__ __forceinline__ uint32_t block_append(bool want, int dest, uint32_t *const *counts, uint32_t cap,
                                                  unsigned *overflow, unsigned long long *S_row,
+                                                 unsigned long long *app_row,
                                                  int self, int nranks, uint32_t *s_cnt, uint32_t *s_base,
                                                  int sys_scope) {
     const int lane = threadIdx.x & 31;
@@ -109,6 +110,7 @@ __device__ __forceinline__ uint32_t block_append(bool want, int dest, uint32_t *
             // fused exchange: the counter may live in a peer GPU's memory (NVLink)
             b = sys_scope ? atomicAdd_system(counts[threadIdx.x], c) : atomicAdd(counts[threadIdx.x], c);
             if (S_row && (int)threadIdx.x != self) atomicAdd(&S_row[threadIdx.x], (unsigned long long)c);
+            atomicAdd(&app_row[threadIdx.x], (unsigned long long)c);
         }
         s_base[threadIdx.x] = b;
         s_cnt[threadIdx.x] = 0;
@@ -126,6 +128,42 @@ __device__ __forceinline__ uint32_t block_append(bool want, int dest, uint32_t *
 __device__ __forceinline__ void flush(unsigned long long *dst, uint32_t v) {
     v = __reduce_add_sync(FULL, v);
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, (unsigned long long)v);
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// The P10 march of a queue of n rays runs in k_march_* (G lanes per ray) rather than inside
+// the trace kernels when the rank has bricks, delta tracking is off and the queue is short.
+__device__ __forceinline__ bool warp_march_dev(const StepArgs &A, uint32_t n) {
+    return A.W.nbricks > 0 && !(A.F.flags & DPR_FLAG_DELTA) && n < A.F.march_inline_min;
+}
+// lanes per ray for such a queue: forced, or the smallest of 1, 4, 16 (run as 32) that gives
+// every lane of the GPU two rays' worth of work; dispatched to the variants 1, 4, 8, 32
+__host__ __device__ __forceinline__ int march_variant(int forced, uint32_t n, uint32_t inline_min) {
+    int G = forced;
+    if (G == 0) {
+        G = 1;
+        while (G < 32 && (int64_t)n * G < (int64_t)inline_min) G *= 4;
+        if (G > 32) G = 32;
+    }
+    return G <= 1 ? 1 : (G <= 4 ? 4 : (G <= 8 ? 8 : 32));
+}
+// the occlusion trace resolves its rays itself (host-side conditions, and no k_march_occl)
+__device__ __forceinline__ bool fuse_resolve_dev(const StepArgs &A, uint32_t n) {
+    return A.F.fuse_resolve && !warp_march_dev(A, n);
+}
+
+// trace kernel start / end stamps of the current step (first start via max of ~t)
+__device__ __forceinline__ void stamp_kernel(const StepArgs &A, int kind, bool start) {
+    if (!A.rec || threadIdx.x != 0) return;
+    const uint32_t k = min(A.rec->step, (uint32_t)MAX_STEP_REC - 1);
+    const unsigned long long t = gtimer();
+    if (start) atomicMax(&A.rec->kt[k][kind][0], ~t);
+    else atomicMax(&A.rec->kt[k][kind][1], t);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -734,6 +772,8 @@ __device__ __forceinline__ void march_groups(const StepArgs &A) {
     const float dt = F.dt;
     const int lane = threadIdx.x & 31, gl = lane % G, gbase = lane - gl;
     const uint32_t n_in = A.Q.in_count[ANY ? 1 : 0];
+    // this queue is marched here, by this variant (block-uniform exit otherwise)
+    if (!warp_march_dev(A, n_in) || march_variant(F.march_g, n_in, F.march_inline_min) != G) return;
     uint32_t *fetch = A.Q.fetch + (ANY ? 3 : 2);
     uint32_t vols = 0;
     MarchRay r;
@@ -1092,7 +1132,7 @@ __global__ void __launch_bounds__(256) k_gen_primary(const __grid_constant__ Ste
     if (owner_keep && A.events) A.events[((int64_t)s * F.max_depth) * F.P + p] = 1u;
     uint32_t gen = __popc(__ballot_sync(FULL, keep || owner_keep));
     if ((threadIdx.x & 31) == 0 && gen) atomicAdd(&A.ctr->gen[K_PATH], (unsigned long long)gen);
-    uint32_t pos = block_append(keep, self, A.Q.cnt_path, A.Q.path_cap, &A.ctr->overflow, nullptr, self,
+    uint32_t pos = block_append(keep, self, A.Q.cnt_path, A.Q.path_cap, &A.ctr->overflow, nullptr, A.ctr->app[0], self,
                                 A.R.nranks, s_cnt, s_base, A.Q.fused);
     if (keep && pos != 0xffffffffu) {
         PathRec *r = A.Q.path_out[self] + pos;
@@ -1112,12 +1152,14 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
     const FrameDev &F = A.F;
     const int lane = threadIdx.x & 31;
     const uint32_t n_in = A.Q.in_count[ANY ? 1 : 0];
+    stamp_kernel(A, ANY ? 1 : 0, true);
     uint32_t *fetch = A.Q.fetch + (ANY ? 1 : 0);
     const float INF = __int_as_float(0x7f800000);
+    const bool fuse = ANY && fuse_resolve_dev(A, n_in);
     uint2 stack[WSTACK];
     __shared__ CoopSmem coop[TRACE_BLOCK / 32];
     __shared__ uint32_t s_vis[2];  // fused resolve: shadow / AO rays resolved by this block
-    if (ANY && F.fuse_resolve) {
+    if (fuse) {
         if (threadIdx.x < 2) s_vis[threadIdx.x] = 0;
         __syncthreads();
     }
@@ -1190,8 +1232,8 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
                                                  slot == 0 ? 0u : ((slot - 1) << 24), ti, ii, rgb, tc.vols);
                 }
             }
-            if (occluded && !F.fuse_resolve) r->a.w = -1.0f;  // occluded marker for k_resolve_occl
-            if (F.fuse_resolve) {
+            if (occluded && !fuse) r->a.w = -1.0f;  // occluded marker for k_resolve_occl
+            if (fuse) {
                 // one rank, no ring: no next candidate exists, so the ray resolves here (what
                 // k_resolve_occl does): visit count, unoccluded -> framebuffer (+ P13 bit)
                 const float4 c = __ldcg(&r->c);
@@ -1239,7 +1281,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
             }
         }
     }
-    if (ANY && F.fuse_resolve) {
+    if (fuse) {
         __syncthreads();
         if (threadIdx.x < 2 && s_vis[threadIdx.x])
             atomicAdd(&A.ctr->V[threadIdx.x == 0 ? K_SHADOW : K_AO], (unsigned long long)s_vis[threadIdx.x]);
@@ -1250,6 +1292,8 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
     flush(&kc->sphs, tc.sphs);
     flush(&kc->vols, tc.vols);
     flush(&kc->rin, rin);
+    __syncthreads();
+    stamp_kernel(A, ANY ? 1 : 0, false);
 }
 
 __global__ void __launch_bounds__(TRACE_BLOCK, TRACE_MINB) k_trace_path(const __grid_constant__ StepArgs A) {
@@ -1308,7 +1352,7 @@ __global__ void __launch_bounds__(DPR_SHADE_BLOCK, DPR_SHADE_MINB) k_shade_path(
         else if (active) next = next_candidate(A.R, self, o, d, INF, bt);
         bool fwd = active && next >= 0;
         uint32_t pos = 0xffffffffu;
-        pos = block_append(fwd, next, cnt_path, A.Q.path_cap, &A.ctr->overflow, A.ctr->S[K_PATH],
+        pos = block_append(fwd, next, cnt_path, A.Q.path_cap, &A.ctr->overflow, A.ctr->S[K_PATH], A.ctr->app[0],
                                self, N, s_cnt, s_base, A.Q.fused);
         if (fwd && pos != 0xffffffffu) {
             PathRec *dst = A.Q.path_out[next] + pos;
@@ -1395,7 +1439,7 @@ __global__ void __launch_bounds__(DPR_SHADE_BLOCK, DPR_SHADE_MINB) k_shade_path(
             }
             if (is_path) {
                 uint32_t q = block_append(app, first, cnt_path, A.Q.path_cap, &A.ctr->overflow,
-                                          A.ctr->S[K_PATH], self, N, s_cnt, s_base, A.Q.fused);
+                                          A.ctr->S[K_PATH], A.ctr->app[0], self, N, s_cnt, s_base, A.Q.fused);
                 if (app && q != 0xffffffffu) {
                     PathRec *dst = A.Q.path_out[first] + q;
                     dst->a = make_float4(org.x, org.y, org.z, INF);
@@ -1406,8 +1450,8 @@ __global__ void __launch_bounds__(DPR_SHADE_BLOCK, DPR_SHADE_MINB) k_shade_path(
                 }
             } else {
                 uint32_t q = block_append(app, first, cnt_occl, A.Q.occl_cap, &A.ctr->overflow,
-                                          A.ctr->S[slot == 0 ? K_SHADOW : K_AO], self, N, s_cnt, s_base,
-                                          A.Q.fused);
+                                          A.ctr->S[slot == 0 ? K_SHADOW : K_AO], A.ctr->app[1], self, N, s_cnt,
+                                          s_base, A.Q.fused);
                 if (app && q != 0xffffffffu) {
                     OcclRec *dst = A.Q.occl_out[first] + q;
                     dst->a = make_float4(org.x, org.y, org.z, ctmax);
@@ -1435,6 +1479,7 @@ __global__ void __launch_bounds__(256) k_resolve_occl(const __grid_constant__ St
     const FrameDev &F = A.F;
     const int self = A.R.self, N = A.R.nranks;
     const uint32_t n_in = A.Q.in_count[1];
+    if (fuse_resolve_dev(A, n_in)) return;  // k_trace_occl resolved these rays itself
     uint32_t *const *cnt_occl = A.Q.cnt_occl;
     uint32_t v_s = 0, v_a = 0, rout = 0;
     __shared__ uint32_t s_cnt[DPR_MAX_RANKS], s_base[DPR_MAX_RANKS];
@@ -1468,7 +1513,7 @@ __global__ void __launch_bounds__(256) k_resolve_occl(const __grid_constant__ St
         bool fwd = active && next >= 0;
         warp_count(fwd, (slot == 0 ? K_SHADOW : K_AO) * DPR_MAX_RANKS + next, &A.ctr->S[0][0]);
         uint32_t pos = 0xffffffffu;
-        pos = block_append(fwd, next, cnt_occl, A.Q.occl_cap, &A.ctr->overflow, nullptr, self, N,
+        pos = block_append(fwd, next, cnt_occl, A.Q.occl_cap, &A.ctr->overflow, nullptr, A.ctr->app[1], self, N,
                                s_cnt, s_base, A.Q.fused);
         if (fwd && pos != 0xffffffffu) {
             OcclRec *dst = A.Q.occl_out[next] + pos;
@@ -1537,6 +1582,126 @@ __global__ void k_composite(const float4 *__restrict__ frag_rgba, const float *_
     out[i] = make_float4(cr + t * br, cg + t * bg, cb + t * bb, a);
 }
 
+// ---------------------------------------------------------------------------------------
+// Step boundary (P8b lock-step: "wave-fronts are synchronized ... until all wave-fronts contain
+// zero rays").  One block.  Phase 1 (end of a step): snapshot every local rank's
+// cumulative routing row S[k][self][*] and visits V[k] into its StepRec (the per-step matrices),
+// reset the consumed queue tails (fused exchange) and the persistent kernels' fetch heads, count
+// the step.  Both phases: total of the next queues -- local ranks directly, the other ranks
+// through the mailbox barrier: each rank stores {seq, path, occl, err} into slot [seq&1][self]
+// of EVERY rank's mailbox (NVLink peer mappings; release order after a system fence, so the
+// step's appends into peer queues and the tail resets are visible first) and spins until all
+// N slots of its own mailbox carry seq (acquire).  Double-buffered by seq parity: a rank can be
+// at most one boundary ahead of any other.  A barrier that does not complete within timeout_ns
+// (a dead peer) sets err 0x100 and ends the loop.  Output: more[slot] = "another step", and the
+// IF handle of the device-driven loop.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_step_end(const __grid_constant__ StepEndArgs A) {
+    __shared__ unsigned long long s_tot;
+    __shared__ uint32_t s_err;
+    const int tid = threadIdx.x;
+    if (A.phase == 1) {
+        // snapshots: nlocal x (3 x N S entries + 3 V entries)
+        const int per = 3 * A.nranks + 3;
+        for (int j = tid; j < A.nlocal * per; j += blockDim.x) {
+            const int i = j / per, q = j - i * per;
+            StepRec *R = A.rec[i];
+            const uint32_t k = min(R->step, (uint32_t)MAX_STEP_REC - 1);
+            if (q < 3 * A.nranks) R->S[k][q / A.nranks][q % A.nranks] = A.ctr[i]->S[q / A.nranks][q % A.nranks];
+            else R->V[k][q - 3 * A.nranks] = A.ctr[i]->V[q - 3 * A.nranks];
+        }
+    }
+    if (tid == 0) {
+        unsigned long long tot = 0;
+        uint32_t err = 0;
+        for (int i = 0; i < A.nlocal; ++i) {
+            if (A.fused) tot += (unsigned long long)A.next_tails[i][0] + A.next_tails[i][1];
+            err |= A.ctr[i]->overflow;
+        }
+        s_tot = tot;
+        s_err = err;
+    }
+    if (tid < A.nlocal) {
+        if (A.fused && A.phase == 1) { A.cons_tails[tid][0] = 0u; A.cons_tails[tid][1] = 0u; }
+        for (int w = 0; w < 4; ++w) A.fetch[tid][w] = 0u;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long t_sync = 0;
+        if (A.barrier) {
+            const unsigned long long t0 = gtimer();
+            const uint32_t seq = *A.seq + 1u;
+            *A.seq = seq;
+            const int b = seq & 1u;
+            __threadfence_system();  // appends + tail resets of this step before the mailbox stores
+            // what this rank appended in this step, all destinations (its own tail is not
+            // final until every sender is done; the appends of this rank are): the global
+            // total of the next step's queues is the sum over ranks
+            unsigned long long app[2] = {0, 0};
+            for (int k = 0; k < 2; ++k)
+                for (int r = 0; r < A.nranks; ++r) app[k] += A.ctr[0]->app[k][r];
+            StepRec *R0 = A.rec[0];
+            const uint32_t mine_p = (uint32_t)(app[0] - R0->app_prev[0]), mine_o = (uint32_t)(app[1] - R0->app_prev[1]);
+            R0->app_prev[0] = app[0];
+            R0->app_prev[1] = app[1];
+            for (int r = 0; r < A.nranks; ++r) {
+                uint32_t *slot = A.mbox_peer[r] + ((size_t)b * DPR_MAX_RANKS + A.self) * 4;
+                slot[1] = mine_p; slot[2] = mine_o; slot[3] = s_err;
+                st_release_sys(slot, seq);
+            }
+            unsigned long long tot = 0;
+            uint32_t err = s_err;
+            for (int r = 0; r < A.nranks; ++r) {
+                const uint32_t *slot = A.mbox_self + ((size_t)b * DPR_MAX_RANKS + r) * 4;
+                while (ld_acquire_sys(slot) != seq) {
+                    if (gtimer() - t0 > A.timeout_ns) { err |= 0x100u; break; }
+                }
+                if (err & 0x100u) break;
+                tot += (unsigned long long)slot[1] + slot[2];
+                err |= slot[3];
+            }
+            __threadfence_system();
+            s_tot = tot;
+            s_err = err;
+            t_sync = gtimer() - t0;
+        }
+        const unsigned long long now = gtimer();
+        const uint32_t more = s_tot > 0 && s_err == 0;
+        for (int i = 0; i < A.nlocal; ++i) {
+            StepRec *R = A.rec[i];
+            R->err |= s_err;
+            if (A.phase == 1) {
+                const uint32_t k = min(R->step, (uint32_t)MAX_STEP_REC - 1);
+                R->t_end[k] = now;
+                R->t_sync[k] += t_sync;
+                R->step = R->step + 1;
+            }
+            R->t_begin[min(R->step, (uint32_t)MAX_STEP_REC)] = now;
+        }
+        if (A.more_slot >= 0) A.more[A.more_slot] = more;
+        if (A.set_if) cudaGraphSetConditional(A.h_if, more);
+    }
+}
+
+__global__ void k_loop_cond(uint32_t *more, cudaGraphConditionalHandle h, int init) {
+    cudaGraphSetConditional(h, init ? more[0] : (more[0] && more[1]));
+    if (!init) more[2]++;  // WHILE iterations (launch accounting)
+}
+
+void launch_step_end(const StepEndArgs &a, cudaStream_t s) { k_step_end<<<1, 256, 0, s>>>(a); }
+void launch_loop_cond(uint32_t *more, cudaGraphConditionalHandle h, int init, cudaStream_t s) {
+    k_loop_cond<<<1, 1, 0, s>>>(more, h, init);
+}
+
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 void launch_depth_init(uint32_t *depth, int64_t n, cudaStream_t s) {
@@ -1560,13 +1725,14 @@ void launch_gen_primary(const StepArgs &a, int s0, int nsamp, int spw_max, cudaS
 // The P10 march: with enough rays to give every lane of the GPU two, per lane inside the
 // trace kernels (all lanes of a warp march together, right after the traversal); with fewer
 // (long marches of few rays would serialise), in k_march_* with G lanes per ray.  Delta
-// tracking always runs inside the trace kernels.
-// Test override DPR_MARCH="<inline_min>[:G]" (e.g. "0": always inline; "1000000000:4":
-// always k_march_* with 4 lanes per ray).
-static int env_march_g() {
+// tracking always runs inside the trace kernels.  The choice is made on the device from the
+// queue length (warp_march_dev / march_variant); the host launches the variant(s) that can
+// apply.  Test override DPR_MARCH="<inline_min>[:G]" (e.g. "0": always inline;
+// "1000000000:4": always k_march_* with 4 lanes per ray).
+int march_g_env() {
     const char *e = getenv("DPR_MARCH");
     const char *c = e ? strchr(e, ':') : nullptr;
-    return c ? atoi(c + 1) : 0;
+    return c ? atoi(c + 1) : DPR_MARCH_G;
 }
 uint32_t march_inline_min(int nsm) {
     if (const char *e = getenv("DPR_MARCH")) return (uint32_t)strtoul(e, nullptr, 10);
@@ -1578,12 +1744,12 @@ static bool use_warp_march(const StepArgs &a, uint32_t n) {
 #ifndef DPR_FUSE_RESOLVE
 #define DPR_FUSE_RESOLVE 1
 #endif
-bool fuse_resolve_ok(const StepArgs &a, uint32_t n) {
+bool fuse_resolve_ok(const StepArgs &a) {
     // read per call (a few times per frame) so a process can switch it (tests)
-    return DPR_FUSE_RESOLVE && getenv("DPR_NO_FUSE_RESOLVE") == nullptr && a.R.nranks == 1 && !(a.F.flags & DPR_FLAG_RING) && !use_warp_march(a, n);
+    return DPR_FUSE_RESOLVE && getenv("DPR_NO_FUSE_RESOLVE") == nullptr && a.R.nranks == 1 && !(a.F.flags & DPR_FLAG_RING);
 }
 template <int G>
-static void launch_march(const StepArgs &a, bool any, uint32_t n, cudaStream_t s) {
+static int march_grid(bool any) {
     static int grid[2] = {0, 0};
     if (!grid[any]) {
         int dev = 0, nsm = 0, occ = 0;
@@ -1593,36 +1759,49 @@ static void launch_march(const StepArgs &a, bool any, uint32_t n, cudaStream_t s
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_march_path<G>, 256, 0);
         grid[any] = nsm * std::max(1, occ);
     }
-    // no more groups than rays
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(grid[any], ((int64_t)n * G + 255) / 256));
+    return grid[any];
+}
+// n: known queue length (no more groups than rays), or 0xffffffff (unknown: full grid)
+template <int G>
+static void launch_march(const StepArgs &a, bool any, uint32_t n, cudaStream_t s) {
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(march_grid<G>(any), ((int64_t)n * G + 255) / 256));
     if (any) k_march_occl<G><<<g, 256, 0, s>>>(a);
     else k_march_path<G><<<g, 256, 0, s>>>(a);
 }
-// G lanes per ray: enough rays to fill the GPU with one lane each -> 1, few rays (long
-// marches would serialise) -> up to a warp per ray
-static void launch_march_any(const StepArgs &a, bool any, uint32_t n, cudaStream_t s) {
-    int G = env_march_g() ? env_march_g() : DPR_MARCH_G;
-    if (G == 0) {  // smallest G in {1, 4, 16->32} with n * G >= march_inline_min
-        G = 1;
-        while (G < 32 && (int64_t)n * G < (int64_t)a.F.march_inline_min) G *= 4;
-        if (G > 32) G = 32;
-    }
-    if (G <= 1) launch_march<1>(a, any, n, s);
-    else if (G <= 4) launch_march<4>(a, any, n, s);
-    else if (G <= 8) launch_march<8>(a, any, n, s);
+static void launch_march_g(const StepArgs &a, bool any, int G, uint32_t n, cudaStream_t s) {
+    if (G == 1) launch_march<1>(a, any, n, s);
+    else if (G == 4) launch_march<4>(a, any, n, s);
+    else if (G == 8) launch_march<8>(a, any, n, s);
     else launch_march<32>(a, any, n, s);
 }
 int launch_trace_path(const StepArgs &a, int grid, uint32_t n, cudaStream_t s) {
     k_trace_path<<<grid, TRACE_BLOCK, 0, s>>>(a);
     if (!use_warp_march(a, n)) return 1;
-    launch_march_any(a, false, n, s);
+    launch_march_g(a, false, march_variant(a.F.march_g, n, a.F.march_inline_min), n, s);
     return 2;
 }
 int launch_trace_occl(const StepArgs &a, int grid, uint32_t n, cudaStream_t s) {
     k_trace_occl<<<grid, TRACE_BLOCK, 0, s>>>(a);
     if (!use_warp_march(a, n)) return 1;
-    launch_march_any(a, true, n, s);
+    launch_march_g(a, true, march_variant(a.F.march_g, n, a.F.march_inline_min), n, s);
     return 2;
+}
+bool march_needed(const StepArgs &a, uint32_t n) { return use_warp_march(a, n); }
+void k_launch_trace_path(const StepArgs &a, int grid, cudaStream_t s) { k_trace_path<<<grid, TRACE_BLOCK, 0, s>>>(a); }
+void k_launch_trace_occl(const StepArgs &a, int grid, cudaStream_t s) { k_trace_occl<<<grid, TRACE_BLOCK, 0, s>>>(a); }
+void march_grids_init() {
+    for (int any = 0; any < 2; ++any) {
+        march_grid<1>(any); march_grid<4>(any); march_grid<8>(any); march_grid<32>(any);
+    }
+}
+int launch_march_variants(const StepArgs &a, bool any, cudaStream_t s) {
+    if (a.W.nbricks == 0 || (a.F.flags & DPR_FLAG_DELTA) || a.F.march_inline_min == 0) return 0;
+    if (a.F.march_g) {
+        launch_march_g(a, any, march_variant(a.F.march_g, 0, 0), 0xffffffffu, s);
+        return 1;
+    }
+    for (int G : {1, 4, 32}) launch_march_g(a, any, G, 0xffffffffu, s);
+    return 3;
 }
 void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s) {
     k_shade_path<<<grid * (256 / DPR_SHADE_BLOCK), DPR_SHADE_BLOCK, 0, s>>>(a);

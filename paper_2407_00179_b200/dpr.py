@@ -84,7 +84,8 @@ class dpr_stats(_c.Structure):
                 ("occl_bytes_alg_local", _c.c_int64), ("kernel_rays_local", _c.c_int64 * 2),
                 ("kernel_nodes_local", _c.c_int64 * 2), ("kernel_tris_local", _c.c_int64 * 2),
                 ("kernel_sphs_local", _c.c_int64 * 2), ("kernel_vols_local", _c.c_int64 * 2),
-                ("bvh_nodes_local", _c.c_int64), ("bvh_levels_local", _c.c_int64)]
+                ("bvh_nodes_local", _c.c_int64), ("bvh_levels_local", _c.c_int64),
+                ("step_loop_device", _c.c_int64), ("graph_builds", _c.c_int64)]
 
     def to_dict(self) -> dict:
         n = self.nranks
@@ -99,6 +100,13 @@ class dpr_stats(_c.Structure):
         return d
 
 
+ALLGATHER_FN = _c.CFUNCTYPE(_c.c_int, _P, _P, _P, _c.c_size_t)
+
+
+class dpr_host_collectives(_c.Structure):
+    _fields_ = [("allgather", ALLGATHER_FN), ("ctx", _P)]
+
+
 ALLOC_FN = _c.CFUNCTYPE(_P, _P, _c.c_size_t, _P)
 FREE_FN = _c.CFUNCTYPE(None, _P, _P, _c.c_size_t, _P)
 
@@ -107,13 +115,13 @@ class dpr_allocator(_c.Structure):
     _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("ctx", _P)]
 
 
-EXPORTS = ["dpr_get_unique_id", "dpr_create_device", "dpr_create_loopback_group",
+EXPORTS = ["dpr_get_unique_id", "dpr_create_device", "dpr_create_device_hostcoll", "dpr_create_loopback_group",
            "dpr_release_device", "dpr_commit_part", "dpr_clear_parts", "dpr_commit_world",
            "dpr_get_world_bounds", "dpr_set_camera", "dpr_set_frame", "dpr_render_frame",
            "dpr_render_frame_group", "dpr_render_frame_composite", "dpr_render_frame_composite_group",
            "dpr_render_frame_replicated", "dpr_render_frame_replicated_group",
            "dpr_frame_ready", "dpr_map_frame", "dpr_get_debug",
-           "dpr_get_stats", "dpr_last_error", "dpr_exchange_plan"]
+           "dpr_get_stats", "dpr_get_step_stats", "dpr_last_error", "dpr_exchange_plan"]
 
 _lib = None
 
@@ -129,6 +137,8 @@ def load(path: str = LIB_PATH):
     L.dpr_get_unique_id.argtypes = [_P]
     L.dpr_create_device.argtypes = [_c.c_int, _c.c_int, _c.c_int, _P, _P, _P, _P]
     L.dpr_create_loopback_group.argtypes = [_c.c_int, _c.c_int, _P, _P, _P]
+    L.dpr_create_device_hostcoll.argtypes = [_c.c_int, _c.c_int, _c.c_int, _P, _P, _P, _P]
+    L.dpr_get_step_stats.argtypes = [_P, _c.c_int, _P, _P, _P, _P, _P]
     for n in ("dpr_release_device", "dpr_clear_parts", "dpr_commit_world", "dpr_render_frame",
               "dpr_render_frame_composite", "dpr_render_frame_replicated"):
         getattr(L, n).argtypes = [_P]
@@ -298,6 +308,38 @@ class Device:
             dist.broadcast_object_list(obj, src=0)
         return cls.create(rank, world, cuda_device, obj[0], stream)
 
+    @classmethod
+    def create_hostcoll(cls, cuda_device: int = 0, group=None, stream=None) -> "Device":
+        """dpr_create_device_hostcoll over a torch.distributed (e.g. gloo) group: the control
+        collectives are torch all-gathers of byte tensors, the ray records move through CUDA
+        IPC peer memory (processes may share one GPU)."""
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(cuda_device)
+        stream = stream or torch.cuda.current_stream(cuda_device)
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def _allgather(ctx, send, recv, nbytes):
+            try:
+                src = torch.frombuffer(bytearray(_c.string_at(send, nbytes)), dtype=torch.uint8)
+                out = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(out, src, group=group)
+                allb = torch.cat(out).numpy()  # keep alive across the copy
+                _c.memmove(recv, allb.ctypes.data, nbytes * world)
+                return 0
+            except Exception:  # reported by the library as DPR_ERR_NCCL
+                return 1
+
+        fn = ALLGATHER_FN(_allgather)
+        coll = dpr_host_collectives(fn, None)
+        alloc = TorchAllocator(cuda_device)
+        h = _P()
+        _check(load().dpr_create_device_hostcoll(rank, world, cuda_device, _c.byref(coll), _P(stream.cuda_stream),
+                                                 _c.byref(alloc.struct), _c.byref(h)))
+        dev = cls(h.value, rank, world, alloc, stream)
+        dev._keep += [fn, coll]  # the library keeps the function pointer
+        return dev
+
     def release(self):
         if self.h:
             _check(load().dpr_release_device(self.h))
@@ -368,6 +410,20 @@ class Device:
         st = dpr_stats()
         _check(load().dpr_get_stats(self.h, _c.byref(st)), self.h)
         return st.to_dict()
+
+    def get_step_stats(self, max_steps: int = 256) -> dict:
+        """dpr_get_step_stats: per-step routing matrices S[k][kind][src][dst], visits
+        V[k][kind][rank], step latency and step-barrier time (ms) of the last frame."""
+        n = self.nranks
+        S = np.zeros((max_steps, 3, n, n), np.int64)
+        V = np.zeros((max_steps, 3, n), np.int64)
+        ms = np.zeros(max_steps, np.float64)
+        sync = np.zeros(max_steps, np.float64)
+        ns = _c.c_int(0)
+        _check(load().dpr_get_step_stats(self.h, max_steps, S.ctypes.data, V.ctypes.data, ms.ctypes.data,
+                                         sync.ctypes.data, _c.byref(ns)), self.h)
+        k = min(ns.value, max_steps)
+        return {"nsteps": ns.value, "S": S[:k], "V": V[:k], "ms": ms[:k], "sync_ms": sync[:k]}
 
     def commit_scene_parts(self, parts: Sequence, device_arrays: bool = False):
         for p in parts:

@@ -73,13 +73,15 @@ def test_config3_delta_tracking_full_size_sampled():
     assert_pixels_close(g[0][pix], o.rgba)
 
 
-@pytest.mark.parametrize("mode", ["sendrecv", "fused"])
+@pytest.mark.parametrize("mode", ["sendrecv", "fused", "fused-host"])
 def test_nccl_collectives_single_rank(mode, monkeypatch):
     """DPR_FORCE_NCCL=1: frame-setup allgather, counts allgather / fused step allgather,
-    (empty) grouped exchange, cudaIpc export of the fused queues, and ncclReduce of
-    framebuffer + dumps all run through NCCL with one rank."""
+    (empty) grouped exchange, cudaIpc export of the fused queues, the device-driven step loop
+    with its mailbox step barrier (fused), and ncclReduce of framebuffer + dumps all run
+    through NCCL with one rank."""
     monkeypatch.setenv("DPR_FORCE_NCCL", "1")
-    monkeypatch.setenv("DPR_EXCHANGE", mode)
+    monkeypatch.setenv("DPR_EXCHANGE", mode.split("-")[0])
+    monkeypatch.setenv("DPR_STEP_LOOP", "host" if mode.endswith("host") else "device")
     sc = di.config1()
     parts = di.union_parts(sc.parts)
     g = gpu_render(parts, 1, sc.camera, sc.frame)
@@ -98,3 +100,25 @@ def test_config4_full_size_sampled():
     assert np.array_equal(g[1][:, :, pix], o.events)
     assert np.array_equal(g[2][:, :, pix], o.occl)
     assert_pixels_close(g[0][pix], o.rgba)
+
+
+def test_nccl_async_error_aborts(monkeypatch):
+    """dpr.h DPR_ERR_NCCL "(incl. async errors)": the NCCL waits poll ncclCommGetAsyncError;
+    on an error (injected: DPR_TEST_NCCL_FAULT=1) the communicator is aborted, the render
+    returns DPR_ERR_NCCL, later collectives fail the same way, and release still works."""
+    from paper_2407_00179_b200 import dpr
+    monkeypatch.setenv("DPR_FORCE_NCCL", "1")
+    monkeypatch.setenv("DPR_TEST_NCCL_FAULT", "1")
+    sc = di.config1()
+    dev = dpr.Device.create(0, 1, 0)
+    try:
+        dev.commit_scene_parts(di.union_parts(sc.parts))
+        dev.commit_world()
+        dev.set_camera(sc.camera)
+        dev.set_frame(sc.frame)
+        for _ in range(2):
+            with pytest.raises(dpr.DprError) as e:
+                dev.render_frame()
+            assert e.value.code == -4
+    finally:
+        dev.release()

@@ -192,14 +192,16 @@ def test_config5_family_small():
     assert_parity(g, o)
 
 
-@pytest.mark.parametrize("mode", ["fused", "sendrecv"])
+@pytest.mark.parametrize("mode", ["fused", "fused-host", "sendrecv"])
 @pytest.mark.parametrize("case", ["c1", "random4", "c2x4"])
 def test_exchange_modes(mode, case, monkeypatch):
     """Both exchange implementations give bit-identical routing and images: 'fused' (kernels
     append straight into the destination rank's next queue through peer pointers + remote
-    tail atomics) and 'sendrecv' (counts allgather + grouped send/recv of
-    per-destination send queues)."""
-    monkeypatch.setenv("DPR_EXCHANGE", mode)
+    tail atomics) with the device-driven step loop (a CUDA graph per batch)
+    or the host loop, and 'sendrecv' (counts allgather + grouped send/recv of per-destination
+    send queues)."""
+    monkeypatch.setenv("DPR_EXCHANGE", mode.split("-")[0])
+    monkeypatch.setenv("DPR_STEP_LOOP", "host" if mode.endswith("host") else "device")
     if case == "c1":
         sc = di.config1()
         parts, n, cam, fr = sc.parts, 2, sc.camera, sc.frame
