@@ -225,6 +225,126 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------------------
+SMS, SCHED_PER_SM = 148, 4  # B200: 148 SMs x 4 warp schedulers, one warp-instruction issue / cycle each
+
+
+def kernel_roofline(args, acc, ms_per_step, clocks):
+    """The dominant trace kernel against the roof that binds it.
+
+    Its duration is measured live (per-launch average: CUDA events on the library stream in
+    host loops, globaltimer first-CTA-start .. last-CTA-end stamps inside the device-driven
+    loop's graph, where events cannot be recorded).  Three fractions:
+      touched: SURVEY 8(d) algorithmic bytes (records + 80 B/wide-node visit + 48 B/triangle
+               + 16 B/sphere + 32 B/volume sample, exact device counters) / time vs HBM --
+               most of these bytes hit L1/L2 (the node hierarchy is L2-resident);
+      dram:    ncu dram__bytes_read+write per launch (profiles/traffic.json) / time vs HBM;
+      issue:   ncu smsp__inst_executed per launch / time vs 148 SMs x 4 schedulers x the SM
+               clock sampled during the run -- the roof the kernel actually presses on.
+    "bound" names the largest fraction's roof."""
+    peak, peak_src = measured_peaks()
+    if acc["ms_path"] >= acc["ms_occl"]:
+        kname, ms, n, b = "k_trace_path", acc["ms_path"], acc["n_path"], acc["b_path"]
+    else:
+        kname, ms, n, b = "k_trace_occl", acc["ms_occl"], acc["n_occl"], acc["b_occl"]
+    avg_s = ms / max(n, 1) / 1000.0
+    bytes_per_launch = b / max(n, 1)
+    touched = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
+    tkey = args.config + (f"+f{args.flags}" if args.flags else "") + ("" if args.mode == "dp" else f"+{args.mode}")
+    tr = (profile_traffic() or {}).get(tkey, {}).get(kname, {})
+    traffic = tr.get("dram_bytes_per_launch")
+    clk_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    issue_peak = SMS * SCHED_PER_SM * clk_mhz * 1e6 / 1e9  # G warp-instructions / s
+    inst = tr.get("inst_executed_per_launch")
+    fr = {"touched": touched / peak}
+    out = {"kernel": kname, "avg_launch_ms": avg_s * 1000, "launches_per_step": n / max(args.steps, 1),
+           "share_of_step": (ms / args.steps) / ms_per_step,
+           "other_kernel_ms_per_step": ((acc["ms_occl"] if kname == "k_trace_path" else acc["ms_path"]) / args.steps),
+           "touched": {"bytes_per_launch": bytes_per_launch, "achieved_gbs": touched, "peak_gbs": peak,
+                       "frac": touched / peak},
+           "traffic": traffic, "peak_source": peak_src, "ncu_source": tr.get("source")}
+    if traffic:
+        dram = traffic / avg_s / 1e9
+        fr["dram"] = dram / peak
+        out["dram"] = {"bytes_per_launch": traffic, "achieved_gbs": dram, "peak_gbs": peak, "frac": dram / peak}
+    if inst:
+        ach = inst / avg_s / 1e9
+        fr["issue"] = ach / issue_peak
+        out["issue"] = {"warp_inst_per_launch": inst, "achieved_ginst_s": ach, "peak_ginst_s": issue_peak,
+                        "frac": ach / issue_peak, "sm_mhz": clk_mhz,
+                        "ncu_issue_active_pct": tr.get("issue_active_pct")}
+    if tr.get("active_threads_per_warp_inst") is not None:
+        out["simt_efficiency"] = tr["active_threads_per_warp_inst"] / 32.0
+        out["warps_active_pct"] = tr.get("warps_active_pct")
+    if "issue" in fr and fr["issue"] >= fr.get("dram", 0):
+        out.update(bound="issue", achieved=out["issue"]["achieved_ginst_s"], peak=issue_peak,
+                   unit="Gwarp-inst/s", frac=fr["issue"])
+    elif "dram" in fr:
+        out.update(bound="hbm", achieved=out["dram"]["achieved_gbs"], peak=peak, unit="GB/s", frac=fr["dram"])
+    else:  # no ncu capture of this workload committed: the touched-bytes roof (SURVEY 8(d))
+        out.update(bound="hbm-touched", achieved=touched, peak=peak, unit="GB/s", frac=fr["touched"])
+    out["touched_frac"] = fr["touched"]
+    out["dram_frac"] = fr.get("dram")
+    out["issue_frac"] = fr.get("issue")
+    return out
+
+
+def step_report(dev, world, ms_per_step):
+    """Per-step routing of the last frame (P8b): steps, per-step latency, exchanged bytes per
+    step (rays forwarded / spawned across ranks x record size) and the busiest pair."""
+    ss = dev.get_step_stats()
+    S = ss["S"]
+    if not len(S):
+        return None
+    rec = np.array([64, 48, 48], np.int64)
+    off = S.copy()
+    for r in range(S.shape[2]):
+        off[:, :, r, r] = 0
+    bytes_pair = (off * rec[None, :, None, None]).sum(axis=1)  # [step][src][dst]
+    out_rank = bytes_pair.sum(axis=2)                          # [step][src]
+    in_rank = bytes_pair.sum(axis=1)                           # [step][dst]
+    ms = ss["ms"]
+    busiest = bytes_pair.reshape(len(S), -1).max(axis=1)
+    per_step_max = np.maximum(out_rank.max(axis=1), in_rank.max(axis=1))
+    rate = [float(b / (t * 1e-3) / 1e9) if t > 0 else None for b, t in zip(per_step_max, ms)]
+    return {"n": int(ss["nsteps"]), "ms": [round(float(x), 4) for x in ms],
+            "sync_ms": [round(float(x), 4) for x in ss["sync_ms"]],
+            "exchange_bytes_max_rank": [int(x) for x in per_step_max],
+            "busiest_pair_bytes": [int(x) for x in busiest],
+            "exchange_gbs_per_rank_lower_bound": rate,
+            "nvlink_gbs_per_direction": 900.0,
+            "note": "fused exchange: records are written into peers' queues by the shading / resolve "
+                    "kernels, overlapping the step's compute; the rate is bytes of the busiest rank / "
+                    "whole step time (a lower bound of the link rate)"}
+
+
+def parity_check(dev, scene, rank, world, npix=600):
+    """After the timed region: one frame with the P13 dumps; rank 0 checks sampled pixels bit-exact
+    (events, occlusion bits) and within the north_star tolerance against the oracle's routing
+    simulator over the same partitioned world (tests/ hold the full parity suite)."""
+    fr = di.Frame(**{**scene.frame.__dict__, "flags": scene.frame.flags | 2})
+    dev.set_frame(fr)
+    dev.commit_world()
+    dev.render_frame()
+    res = None
+    if rank == 0:
+        import oracle as orc
+        e, o = dev.get_debug(fr.spp, fr.max_depth, fr.W * fr.H)
+        img = dev.map_frame().reshape(-1, 4).cpu().numpy().astype(np.float64)
+        P = fr.W * fr.H
+        pix = np.sort(np.random.default_rng(9).choice(P, size=min(npix, P), replace=False))
+        ora = orc.render(orc.OracleScene(scene.parts, world), scene.camera, fr, pixels=pix, dp=True)
+        ev = e.cpu().numpy()[:, :, pix]
+        oc = o.cpu().numpy()[:, :, pix]
+        d = np.abs(img[pix] - ora.rgba)
+        res = {"pixels": int(len(pix)), "events_bitexact": bool(np.array_equal(ev, ora.events)),
+               "occl_bitexact": bool(np.array_equal(oc, ora.occl)),
+               "max_abs": float(d.max()), "mean_abs_max_channel": float(d.mean(axis=0).max()),
+               "within_tolerance": bool(d.max() <= 1e-3 and d.mean(axis=0).max() <= 1e-4)}
+        res["ok"] = res["events_bitexact"] and res["occl_bitexact"] and res["within_tolerance"]
+    dev.set_frame(scene.frame)
+    return res
+
+
 def run_gpu(args):
     import torch
     rank, world, local = dist_env()
@@ -234,6 +354,9 @@ def run_gpu(args):
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # the communicator's rank count / transports (NVLS, P2P) in the log; ncclCommCount in the line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2407_00179_b200 import dpr
     scene = make_scene(args.config, 1 if args.mode == "replicated" else world)
@@ -307,6 +430,7 @@ def run_gpu(args):
                     acc.setdefault(f"k{k}_{f}", 0)
                     acc[f"k{k}_{f}"] += st[f"kernel_{f}_local"][k]
             acc["bvh_nodes"] = st["bvh_nodes_local"]; acc["bvh_levels"] = st["bvh_levels_local"]
+            acc["comm_nranks"] = st["comm_nranks"]; acc["step_loop_device"] = st["step_loop_device"]
         e1.record(stream)
         barrier()
     elapsed_ms = max_over_ranks(e0.elapsed_time(e1))
@@ -315,34 +439,10 @@ def run_gpu(args):
     value = rays_per_frame * args.steps / (elapsed_ms / 1000.0)
     ms_per_step = elapsed_ms / args.steps
 
-    # roofline of the dominant kernel (rank 0's launches)
-    peak, peak_src = measured_peaks()
-    if acc["ms_path"] >= acc["ms_occl"]:
-        kname, ms, n, b = "k_trace_path", acc["ms_path"], acc["n_path"], acc["b_path"]
-    else:
-        kname, ms, n, b = "k_trace_occl", acc["ms_occl"], acc["n_occl"], acc["b_occl"]
-    avg_s = ms / max(n, 1) / 1000.0
-    bytes_per_launch = b / max(n, 1)
-    achieved = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
-    # ncu figures of THIS workload's kernel (profiles/traffic.json is keyed by config[+flags][+mode], then
-    # kernel; an entry exists only where a --set full capture of that config was committed)
-    tkey = args.config + (f"+f{args.flags}" if args.flags else "") + ("" if args.mode == "dp" else f"+{args.mode}")
-    tr = (profile_traffic() or {}).get(tkey, {})
-    traffic = None
-    limiter = None
-    if kname in tr:
-        traffic = tr[kname].get("dram_bytes_per_launch")
-        if tr[kname].get("issue_active_pct") is not None:
-            # what ncu says actually limits the kernel (the touched-bytes roof is SURVEY 8(d)'s)
-            limiter = {"issue_active_pct": tr[kname]["issue_active_pct"],
-                       "active_threads_per_warp_inst": tr[kname].get("active_threads_per_warp_inst"),
-                       "warps_active_pct": tr[kname].get("warps_active_pct"),
-                       "source": tr[kname].get("source")}
-    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src, "ncu_limiter": limiter,
-                "alg_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_s * 1000,
-                "share_of_step": (ms / args.steps) / ms_per_step,
-                "other_kernel_ms_per_step": ((acc["ms_occl"] if kname == "k_trace_path" else acc["ms_path"]) / args.steps)}
+    # roofline of the dominant kernel (rank 0's launches; DESIGN.md section 7 "Roofline")
+    roofline = kernel_roofline(args, acc, ms_per_step, clocks)
+
+    steps_detail = step_report(dev, world, ms_per_step)
 
     # ---- e2e: through the public API from pinned HOST buffers ---------------------------
     pinned = []
@@ -398,6 +498,9 @@ def run_gpu(args):
     else:
         e2e_ms = float("nan")
     e2e_value = rays_per_frame * args.steps / (e2e_ms / 1000.0)
+    parity = None
+    if world > 1 and not args.no_parity and args.mode == "dp":
+        parity = parity_check(dev, scene, rank, world)
 
     if rank == 0:
         cpu = None
@@ -433,7 +536,14 @@ def run_gpu(args):
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
             "gpu_launches": int(acc["launches"]),
             "clocks": clocks,
+            "step_loop": "device (CUDA graph per spp batch)" if acc.get("step_loop_device") else "host",
+            "wavefront_steps": steps_detail,
         }
+        if world > 1:
+            line["nccl"] = {"comm_nranks": int(acc.get("comm_nranks", 0)),
+                            "comm_nranks_ok": int(acc.get("comm_nranks", 0)) == world,
+                            "exchange": os.environ.get("DPR_EXCHANGE", "fused")}
+            line["parity"] = parity
         print(json.dumps(line), flush=True)
     dev.release()
     if world > 1:
@@ -458,6 +568,7 @@ def main():
                     help="workload (default c2 = BASELINE configs[1], the metric's workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the N>1 sampled parity check")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -186,6 +186,9 @@ typedef struct {
                                  (first CTA start .. last CTA end) and ms_exchange the time in
                                  the step barrier */
     int64_t graph_builds;     /* step-loop graphs captured so far on this device */
+    int64_t comm_nranks;      /* ranks of the NCCL communicator (ncclCommCount), 0 without NCCL */
+    double ms_kernel_span[2]; /* k_trace_path / k_trace_occl: sum over launches that traced rays
+                                 of the globaltimer span first CTA start .. last CTA end */
 } dpr_stats;
 
 /* Host-collective transport: a blocking, collective all-gather supplied by the caller (e.g.
@@ -316,6 +319,12 @@ DPR_API int dpr_get_step_stats(dpr_device dev, int max_steps, int64_t *S_out, in
 
 /* LOCAL: last error message of this thread ("" if none). */
 DPR_API const char *dpr_last_error(dpr_device dev);
+
+/* LOCAL test of the step barrier of the device-driven loop (the mailbox protocol ranks use
+ * over NVLink peer memory): nranks ranks emulated as the blocks of ONE cooperative kernel on
+ * cuda_device (ranks that spin on each other must be co-resident), iters boundaries with
+ * skewed arrival; *mismatches = boundaries whose gathered sums were wrong (0 expected). */
+DPR_API int dpr_test_step_barrier(int cuda_device, int nranks, int iters, int64_t *mismatches);
 
 /* ---- host-side exchange planning (pure function; used by the render loop) ------------ */
 

@@ -168,7 +168,7 @@ struct Dev {
     uint32_t *peer_mbox[DPR_MAX_RANKS] = {};
     float4 *peer_fb[DPR_MAX_RANKS] = {};          // host-collective mode: peers' framebuffers / dumps
     uint32_t *peer_events[DPR_MAX_RANKS] = {}, *peer_occl_dump[DPR_MAX_RANKS] = {};
-    cudaStream_t gstream = nullptr;               // capture stream of the step graph
+    cudaStream_t gstream = nullptr, gstream2 = nullptr;  // capture streams of the step graph
     cudaGraph_t graph = nullptr;                  // device-driven step loop (cached per signature)
     cudaGraphExec_t gexec = nullptr;
     uint64_t gkey = 0;
@@ -1214,7 +1214,7 @@ int launch_step(Dev *d, const FrameCtx &fc, int cur, uint32_t n_path, uint32_t n
                 StepTimers *tm, int64_t &launches) {
     StepArgs a = make_args(d, fc, cur);
     const int grid_r = d->nsm * 8;
-    const bool dev = n_path == UNKNOWN;
+    const bool dev = n_path == UNKNOWN || n_occl == UNKNOWN;
     if (n_path) {
         Nvtx r("trace_path+shade");
         cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1277,25 +1277,71 @@ uint64_t graph_key(std::vector<Dev *> &L, const FrameCtx &fc, const std::vector<
 
 // Build the device-driven step loop of one spp batch (the batch's primaries are in parity 0):
 //   k_step_end(phase 0) -> k_loop_cond(init) -> WHILE(h_loop) {
-//       step kernels (parity 0) -> k_step_end -> IF(h_if) { step kernels (parity 1) ->
-//       k_step_end } -> k_loop_cond }
+//       step(parity 0) -> k_step_end -> IF(h_if) { step(parity 1) -> k_step_end } -> k_loop_cond }
+//   step(c) = k_set_ifs (from every local rank's input tails) -> per local rank
+//             IF(path queue non-empty) { k_trace_path, k_march_path variants, k_shade_path }
+//             IF(occl queue non-empty) { k_trace_occl, k_march_occl variants, k_resolve_occl }
 // The loop body is unrolled twice so that every kernel node has fixed arguments (queue
-// parities alternate); each k_step_end decides "another step" on the device.
+// parities alternate).  Every decision is taken on the device: "another step" by k_step_end
+// (local tails; the peers' appended counts through the mailbox barrier), which kernel groups
+// run by k_set_ifs (the input tails are final once the boundary is passed), march variants
+// and the occlusion trace's own resolve by the kernels from the queue length.
+int capture_step(std::vector<Dev *> &L, const FrameCtx &fc, int cur, const std::vector<int> &grid_p,
+                 const std::vector<int> &grid_o, cudaGraph_t g, cudaStream_t s, cudaStream_t s2, int64_t &kernels) {
+    // IF handles of this step (created on the graph that holds the IF nodes)
+    IfArgs ia;
+    memset(&ia, 0, sizeof(ia));
+    ia.n = (int)L.size();
+    ia.count = P<uint32_t>(L[0]->b_more) + 3;
+    for (size_t i = 0; i < L.size(); ++i) {
+        ia.tails[i] = P<uint32_t>(L[i]->b_tails) + 2 * cur;
+        for (int k = 0; k < 2; ++k) CK(cudaGraphConditionalHandleCreate(&ia.h[i][k], g, 0, cudaGraphCondAssignDefault));
+        const int mv = march_variants_count(make_args(L[i], fc, cur));
+        ia.kernels[i][0] = ia.kernels[i][1] = 2 + mv;  // trace, march variants, shade / resolve
+    }
+    launch_set_ifs(ia, s);
+    kernels++;
+    for (size_t i = 0; i < L.size(); ++i)
+        for (int k = 0; k < 2; ++k) {
+            cudaStreamCaptureStatus st;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t ndeps = 0;
+            cudaGraph_t cg = nullptr;
+            CK(cudaStreamGetCaptureInfo(s, &st, nullptr, &cg, &deps, &ndeps));
+            cudaGraphNodeParams ip = {};
+            ip.type = cudaGraphNodeTypeConditional;
+            ip.conditional.handle = ia.h[i][k];
+            ip.conditional.type = cudaGraphCondTypeIf;
+            ip.conditional.size = 1;
+            cudaGraphNode_t node;
+            CK(cudaGraphAddNode(&node, cg, deps, ndeps, &ip));
+            CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+            // the group's kernels, captured into the IF body on the second stream
+            cudaGraph_t out = nullptr;
+            CK(cudaStreamBeginCaptureToGraph(s2, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeThreadLocal));
+            Dev *d = L[i];
+            const cudaStream_t keep = d->stream;
+            d->stream = s2;
+            int64_t l = 0;
+            const int rc = launch_step(d, fc, cur, k == 0 ? UNKNOWN : 0, k == 1 ? UNKNOWN : 0, grid_p[i], grid_o[i],
+                                       nullptr, l);
+            d->stream = keep;
+            CK(cudaStreamEndCapture(s2, &out));
+            RET(rc);
+            kernels += l;
+        }
+    return DPR_OK;
+}
+
 int build_step_graph(std::vector<Dev *> &L, const FrameCtx &fc, const std::vector<int> &grid_p,
                      const std::vector<int> &grid_o, bool barrier) {
     Dev *d0 = L[0];
-    // capture on the library's own non-blocking stream (the caller's may be the legacy default
+    // capture on the library's own non-blocking streams (the caller's may be the legacy default
     // stream, which cannot be captured); the graph is launched on the caller's stream
     if (!d0->gstream) CK(cudaStreamCreateWithFlags(&d0->gstream, cudaStreamNonBlocking));
-    cudaStream_t s = d0->gstream;
-    struct Swap {  // launch_step issues on d->stream: point every local rank at the capture stream
-        std::vector<Dev *> &L;
-        std::vector<cudaStream_t> keep;
-        Swap(std::vector<Dev *> &l, cudaStream_t cs) : L(l) {
-            for (Dev *d : L) { keep.push_back(d->stream); d->stream = cs; }
-        }
-        ~Swap() { for (size_t i = 0; i < L.size(); ++i) L[i]->stream = keep[i]; }
-    } swap(L, s);
+    if (!d0->gstream2) CK(cudaStreamCreateWithFlags(&d0->gstream2, cudaStreamNonBlocking));
+    cudaStream_t s = d0->gstream, s2 = d0->gstream2;
     if (d0->gexec) { cudaGraphExecDestroy(d0->gexec); d0->gexec = nullptr; }
     if (d0->graph) { cudaGraphDestroy(d0->graph); d0->graph = nullptr; }
     int64_t kernels = 0;
@@ -1333,46 +1379,42 @@ int build_step_graph(std::vector<Dev *> &L, const FrameCtx &fc, const std::vecto
     cudaGraphConditionalHandle h_if;
     CK(cudaGraphConditionalHandleCreate(&h_if, body, 0, cudaGraphCondAssignDefault));
     CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    for (size_t i = 0; i < L.size(); ++i) {
-        int64_t l = 0;
-        RET(launch_step(L[i], fc, 0, UNKNOWN, UNKNOWN, grid_p[i], grid_o[i], nullptr, l));
-        kernels += l;
-    }
-    {
+    int rc = capture_step(L, fc, 0, grid_p, grid_o, body, s, s2, kernels);
+    if (rc == DPR_OK) {
         StepEndArgs e = make_step_end(L, std::vector<int>(L.size(), 0), 1, barrier);
         e.more_slot = 0;
         e.set_if = 1;
         e.h_if = h_if;
         launch_step_end(e, s);
         kernels++;
+        CK(cudaStreamGetCaptureInfo(s, &st, nullptr, &cg, &deps, &ndeps));
     }
-    CK(cudaStreamGetCaptureInfo(s, &st, nullptr, &cg, &deps, &ndeps));
     cudaGraphNodeParams ip = {};
-    ip.type = cudaGraphNodeTypeConditional;
-    ip.conditional.handle = h_if;
-    ip.conditional.type = cudaGraphCondTypeIf;
-    ip.conditional.size = 1;
     cudaGraphNode_t inode;
-    CK(cudaGraphAddNode(&inode, cg, deps, ndeps, &ip));
-    cudaGraph_t ibody = ip.conditional.phGraph_out[0];
-    CK(cudaStreamUpdateCaptureDependencies(s, &inode, 1, cudaStreamSetCaptureDependencies));
-    launch_loop_cond(P<uint32_t>(d0->b_more), h_loop, 0, s);
-    kernels++;
-    CK(cudaStreamEndCapture(s, &gout));
-    // IF body: step B (parity 1) + boundary
-    CK(cudaStreamBeginCaptureToGraph(s, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    for (size_t i = 0; i < L.size(); ++i) {
-        int64_t l = 0;
-        RET(launch_step(L[i], fc, 1, UNKNOWN, UNKNOWN, grid_p[i], grid_o[i], nullptr, l));
-        kernels += l;
+    if (rc == DPR_OK) {
+        ip.type = cudaGraphNodeTypeConditional;
+        ip.conditional.handle = h_if;
+        ip.conditional.type = cudaGraphCondTypeIf;
+        ip.conditional.size = 1;
+        CK(cudaGraphAddNode(&inode, cg, deps, ndeps, &ip));
+        CK(cudaStreamUpdateCaptureDependencies(s, &inode, 1, cudaStreamSetCaptureDependencies));
+        launch_loop_cond(P<uint32_t>(d0->b_more), h_loop, 0, s);
+        kernels++;
     }
-    {
+    CK(cudaStreamEndCapture(s, &gout));
+    RET(rc);
+    // IF body: step B (parity 1) + boundary
+    cudaGraph_t ibody = ip.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(s, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    rc = capture_step(L, fc, 1, grid_p, grid_o, ibody, s, s2, kernels);
+    if (rc == DPR_OK) {
         StepEndArgs e = make_step_end(L, std::vector<int>(L.size(), 1), 1, barrier);
         e.more_slot = 1;
         launch_step_end(e, s);
         kernels++;
     }
     CK(cudaStreamEndCapture(s, &gout));
+    RET(rc);
     CK(cudaGraphInstantiate(&d0->gexec, g, 0));
     d0->graph = g;
     d0->graph_kernels = kernels;
@@ -1653,15 +1695,17 @@ int render_group(std::vector<Dev *> &L) {
     }
     const int64_t steps = rec[0].step;
     const int nrec = (int)std::min<int64_t>(steps, MAX_STEP_REC);
+    // trace kernels: first-CTA-start .. last-CTA-end globaltimer spans of the launches that
+    // traced rays (the device loop also launches them on empty queues; they exit at once)
     double kt_ms[2] = {0, 0}, sync_ms = 0;
-    if (dev_loop) {  // trace kernels inside the graph: first-start .. last-end globaltimer stamps
-        for (int k = 0; k < nrec; ++k) {
-            for (int q = 0; q < 2; ++q) {
-                const unsigned long long a = ~rec[0].kt[k][q][0], e = rec[0].kt[k][q][1];
-                if (rec[0].kt[k][q][0] && e >= a) kt_ms[q] += (double)(e - a) * 1e-6;
-            }
-            sync_ms += rec[0].t_sync[k] * 1e-6;
+    int64_t kt_n[2] = {0, 0};
+    for (int k = 0; k < nrec; ++k) {
+        for (int q = 0; q < 2; ++q) {
+            const unsigned long long a = ~rec[0].kt[k][q][0], e = rec[0].kt[k][q][1];
+            const bool work = rec[0].rin[k][q] > (k ? rec[0].rin[k - 1][q] : 0ull);
+            if (work && rec[0].kt[k][q][0] && e >= a) { kt_ms[q] += (double)(e - a) * 1e-6; kt_n[q]++; }
         }
+        sync_ms += rec[0].t_sync[k] * 1e-6;
     }
     for (size_t i = 0; i < L.size(); ++i) {
         StatsMsg &m = msgs[i];
@@ -1759,21 +1803,29 @@ int render_group(std::vector<Dev *> &L) {
         st.ms_frame = fms;
         st.ms_frame_max = mx;
         st.step_loop_device = dev_loop ? 1 : 0;
+        if (i == 0) {
+            st.ms_kernel_span[0] = kt_ms[0];
+            st.ms_kernel_span[1] = kt_ms[1];
+        }
         st.graph_builds = d0->graph_builds;
+        if (d->comm) {
+            int cn = 0;
+            if (ncclCommCount(d->comm, &cn) == ncclSuccess) st.comm_nranks = cn;
+        }
         if (i == 0) {
             st.ms_gen = sum_ms(t_gen);
             if (dev_loop) {
                 st.ms_trace_path = kt_ms[0];
                 st.ms_trace_occl = kt_ms[1];
                 st.ms_exchange = sync_ms;  // fused: appends are inside the kernels; the barrier
-                st.trace_path_launches = nrec;
-                st.trace_occl_launches = nrec;
-                // graph: per batch 2 (initial boundary + condition); per step its kernels and
-                // boundary; per WHILE iteration one condition kernel (counted on the device)
-                uint32_t iters = 0;
-                CK(cudaMemcpy(&iters, P<uint32_t>(d0->b_more) + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost));
-                const int64_t per_step = (d0->graph_kernels - 5) / 2 + 1;
-                st.kernel_launches_local = d->build_launches + launches + (int64_t)nb * 2 + steps * per_step + iters;
+                st.trace_path_launches = kt_n[0];  // launches that traced rays
+                st.trace_occl_launches = kt_n[1];
+                // graph: per batch 2 (initial boundary + condition); per step k_set_ifs, the
+                // kernel groups that ran and the boundary; per WHILE iteration one condition
+                // kernel (iterations and group kernels counted on the device)
+                uint32_t cnt[2] = {0, 0};
+                CK(cudaMemcpy(cnt, P<uint32_t>(d0->b_more) + 2, sizeof(cnt), cudaMemcpyDeviceToHost));
+                st.kernel_launches_local = d->build_launches + launches + (int64_t)nb * 2 + steps * 2 + cnt[0] + cnt[1];
             } else {
                 st.ms_trace_path = sum_ms(tm.path);
                 st.ms_trace_occl = sum_ms(tm.occl);
@@ -1915,6 +1967,8 @@ void release_bufs(Dev *d) {
     if (d->gexec) cudaGraphExecDestroy(d->gexec);
     if (d->graph) cudaGraphDestroy(d->graph);
     if (d->gstream) cudaStreamDestroy(d->gstream);
+    if (d->gstream2) cudaStreamDestroy(d->gstream2);
+    d->gstream2 = nullptr;
     d->gexec = nullptr;
     d->graph = nullptr;
     d->gstream = nullptr;
@@ -2243,6 +2297,25 @@ int dpr_get_step_stats(dpr_device dev, int max_steps, int64_t *S_out, int64_t *V
     if (ms_out) memcpy(ms_out, d->step_ms.data(), sizeof(double) * n);
     if (sync_ms_out) memcpy(sync_ms_out, d->step_sync_ms.data(), sizeof(double) * n);
     *nsteps = (int)d->nsteps_rec;
+    return DPR_OK;
+}
+
+int dpr_test_step_barrier(int cuda_device, int nranks, int iters, int64_t *mismatches) {
+    if (nranks < 1 || nranks > DPR_MAX_RANKS || iters < 0 || !mismatches)
+        return fail(DPR_ERR_INVALID_ARG, "bad arguments");
+    CK(cudaSetDevice(cuda_device));
+    const size_t mb = sizeof(uint32_t) * (size_t)nranks * 2 * DPR_MAX_RANKS * 4;
+    char *buf = nullptr;
+    CK(cudaMalloc(&buf, mb + sizeof(uint32_t) * (nranks + 1)));
+    uint32_t *mbox = (uint32_t *)buf, *seq = (uint32_t *)(buf + mb), *bad = seq + nranks;
+    cudaError_t e = cudaMemset(buf, 0, mb + sizeof(uint32_t) * (nranks + 1));
+    if (e == cudaSuccess) e = (cudaError_t)test_step_barrier(nranks, iters, mbox, seq, bad, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    uint32_t hb = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    if (e != cudaSuccess) return fail(DPR_ERR_CUDA, std::string("step barrier test: ") + cudaGetErrorString(e));
+    *mismatches = hb;
     return DPR_OK;
 }
 

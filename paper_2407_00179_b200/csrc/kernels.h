@@ -123,6 +123,7 @@ struct StepRec {
     unsigned long long kt[MAX_STEP_REC][2][2];          // trace kernel (path, occl): ~first start, last end
     unsigned long long S[MAX_STEP_REC][3][DPR_MAX_RANKS];  // cumulative S row of this rank after step k
     unsigned long long V[MAX_STEP_REC][3];                 // cumulative visits of this rank after step k
+    unsigned long long rin[MAX_STEP_REC][2];               // cumulative rays traced (path, occl) after step k
 };
 
 struct StepArgs {
@@ -165,6 +166,20 @@ struct StepEndArgs {
     cudaGraphConditionalHandle h_if;
 };
 void launch_step_end(const StepEndArgs &a, cudaStream_t s);
+// the device loop's per-rank kernel-group conditions: h[i][0] = path queue of local rank i
+// non-empty, h[i][1] = occlusion queue non-empty (tails[i] = {path, occl} input counts)
+struct IfArgs {
+    int n;
+    const uint32_t *tails[DPR_MAX_RANKS];
+    cudaGraphConditionalHandle h[DPR_MAX_RANKS][2];
+    uint32_t kernels[DPR_MAX_RANKS][2];  // kernels in each group (launch accounting)
+    uint32_t *count;                     // += kernels of the groups that run
+};
+int march_variants_count(const StepArgs &a);  // k_march_* launches launch_march_variants makes
+void launch_set_ifs(const IfArgs &a, cudaStream_t s);
+// the mailbox barrier of nranks ranks emulated as one cooperative launch (test); returns a
+// cudaError_t; *bad counts iterations whose sums were wrong
+int test_step_barrier(int nranks, int iters, uint32_t *mbox, uint32_t *seq, uint32_t *bad, cudaStream_t s);
 // WHILE handle of the loop graph := more[0] && more[1] (end of the unrolled double step)
 void launch_loop_cond(uint32_t *more, cudaGraphConditionalHandle h, int init, cudaStream_t s);
 

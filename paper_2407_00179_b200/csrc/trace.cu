@@ -1605,19 +1605,51 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
     return v;
 }
 
+// The mailbox barrier of one rank (one thread): publish {seq, path, occl, err} into slot
+// [seq&1][self] of every rank's mailbox, then wait until every slot [seq&1][*] of its own
+// mailbox carries seq; returns the sums over ranks (err: OR, | 0x100 on timeout).
+__device__ __forceinline__ void mailbox_barrier(uint32_t *mbox_self, uint32_t *const *mbox_peer, uint32_t *seq_ctr,
+                                                int self, int nranks, uint32_t mine_p, uint32_t mine_o,
+                                                uint32_t mine_err, unsigned long long timeout_ns,
+                                                unsigned long long &tot, uint32_t &err) {
+    const unsigned long long t0 = gtimer();
+    const uint32_t seq = *seq_ctr + 1u;
+    *seq_ctr = seq;
+    const int b = seq & 1u;
+    __threadfence_system();  // this rank's appends / tail resets before the mailbox stores
+    for (int r = 0; r < nranks; ++r) {
+        uint32_t *slot = mbox_peer[r] + ((size_t)b * DPR_MAX_RANKS + self) * 4;
+        slot[1] = mine_p; slot[2] = mine_o; slot[3] = mine_err;
+        st_release_sys(slot, seq);
+    }
+    tot = 0;
+    err = mine_err;
+    for (int r = 0; r < nranks; ++r) {
+        const uint32_t *slot = mbox_self + ((size_t)b * DPR_MAX_RANKS + r) * 4;
+        while (ld_acquire_sys(slot) != seq) {
+            if (gtimer() - t0 > timeout_ns) { err |= 0x100u; break; }
+        }
+        if (err & 0x100u) break;
+        tot += (unsigned long long)ld_acquire_sys(slot + 1) + ld_acquire_sys(slot + 2);
+        err |= ld_acquire_sys(slot + 3);
+    }
+    __threadfence_system();
+}
+
 __global__ void __launch_bounds__(256) k_step_end(const __grid_constant__ StepEndArgs A) {
     __shared__ unsigned long long s_tot;
     __shared__ uint32_t s_err;
     const int tid = threadIdx.x;
     if (A.phase == 1) {
         // snapshots: nlocal x (3 x N S entries + 3 V entries)
-        const int per = 3 * A.nranks + 3;
+        const int per = 3 * A.nranks + 5;
         for (int j = tid; j < A.nlocal * per; j += blockDim.x) {
             const int i = j / per, q = j - i * per;
             StepRec *R = A.rec[i];
             const uint32_t k = min(R->step, (uint32_t)MAX_STEP_REC - 1);
             if (q < 3 * A.nranks) R->S[k][q / A.nranks][q % A.nranks] = A.ctr[i]->S[q / A.nranks][q % A.nranks];
-            else R->V[k][q - 3 * A.nranks] = A.ctr[i]->V[q - 3 * A.nranks];
+            else if (q < 3 * A.nranks + 3) R->V[k][q - 3 * A.nranks] = A.ctr[i]->V[q - 3 * A.nranks];
+            else R->rin[k][q - 3 * A.nranks - 3] = A.ctr[i]->kc[q - 3 * A.nranks - 3].rin;
         }
     }
     if (tid == 0) {
@@ -1639,10 +1671,6 @@ __global__ void __launch_bounds__(256) k_step_end(const __grid_constant__ StepEn
         unsigned long long t_sync = 0;
         if (A.barrier) {
             const unsigned long long t0 = gtimer();
-            const uint32_t seq = *A.seq + 1u;
-            *A.seq = seq;
-            const int b = seq & 1u;
-            __threadfence_system();  // appends + tail resets of this step before the mailbox stores
             // what this rank appended in this step, all destinations (its own tail is not
             // final until every sender is done; the appends of this rank are): the global
             // total of the next step's queues is the sum over ranks
@@ -1653,23 +1681,10 @@ __global__ void __launch_bounds__(256) k_step_end(const __grid_constant__ StepEn
             const uint32_t mine_p = (uint32_t)(app[0] - R0->app_prev[0]), mine_o = (uint32_t)(app[1] - R0->app_prev[1]);
             R0->app_prev[0] = app[0];
             R0->app_prev[1] = app[1];
-            for (int r = 0; r < A.nranks; ++r) {
-                uint32_t *slot = A.mbox_peer[r] + ((size_t)b * DPR_MAX_RANKS + A.self) * 4;
-                slot[1] = mine_p; slot[2] = mine_o; slot[3] = s_err;
-                st_release_sys(slot, seq);
-            }
             unsigned long long tot = 0;
-            uint32_t err = s_err;
-            for (int r = 0; r < A.nranks; ++r) {
-                const uint32_t *slot = A.mbox_self + ((size_t)b * DPR_MAX_RANKS + r) * 4;
-                while (ld_acquire_sys(slot) != seq) {
-                    if (gtimer() - t0 > A.timeout_ns) { err |= 0x100u; break; }
-                }
-                if (err & 0x100u) break;
-                tot += (unsigned long long)slot[1] + slot[2];
-                err |= slot[3];
-            }
-            __threadfence_system();
+            uint32_t err = 0;
+            mailbox_barrier(A.mbox_self, A.mbox_peer, A.seq, A.self, A.nranks, mine_p, mine_o, s_err, A.timeout_ns,
+                            tot, err);
             s_tot = tot;
             s_err = err;
             t_sync = gtimer() - t0;
@@ -1692,12 +1707,50 @@ __global__ void __launch_bounds__(256) k_step_end(const __grid_constant__ StepEn
     }
 }
 
+// Test of the mailbox barrier protocol on ONE GPU (B200_PROFILING.md: ranks that wait on one
+// another must be one kernel): block r plays rank r with its own mailbox and sequence counter;
+// every iteration each rank publishes counts f(it, r) after a pseudo-random delay and checks
+// the sums.  mbox: [nranks][2][DPR_MAX_RANKS][4], seq: [nranks], bad: mismatches.
+__global__ void k_barrier_emulate(uint32_t *mbox, uint32_t *seq, int nranks, int iters, uint32_t *bad) {
+    const int r = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    uint32_t *peers[DPR_MAX_RANKS];
+    for (int q = 0; q < nranks; ++q) peers[q] = mbox + (size_t)q * 2 * DPR_MAX_RANKS * 4;
+    for (int it = 0; it < iters; ++it) {
+        uint32_t h = (uint32_t)(it * 2654435761u) ^ (uint32_t)(r * 2246822519u);
+        h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+        const unsigned long long until = gtimer() + (h & 1023u);  // skew the ranks
+        while (gtimer() < until) {}
+        unsigned long long tot = 0, want = 0;
+        uint32_t err = 0;
+        mailbox_barrier(peers[r], peers, seq + r, r, nranks, (uint32_t)(it + 3 * r), (uint32_t)(7 * it + r),
+                        (uint32_t)((it % 5 == 4 && r == nranks - 1) ? 1 : 0), 2000000000ull, tot, err);
+        for (int q = 0; q < nranks; ++q) want += (unsigned long long)(it + 3 * q) + (7ull * it + q);
+        const uint32_t want_err = it % 5 == 4 ? 1u : 0u;
+        if (tot != want || err != want_err) atomicAdd(bad, 1u);
+    }
+}
+
+__global__ void k_set_ifs(const __grid_constant__ IfArgs A) {
+    const int t = threadIdx.x;
+    if (t < 2 * A.n) {
+        const bool run = A.tails[t >> 1][t & 1] > 0u;
+        cudaGraphSetConditional(A.h[t >> 1][t & 1], run);
+        if (run) atomicAdd(A.count, A.kernels[t >> 1][t & 1]);
+    }
+}
+void launch_set_ifs(const IfArgs &a, cudaStream_t s) { k_set_ifs<<<1, 32, 0, s>>>(a); }
+
 __global__ void k_loop_cond(uint32_t *more, cudaGraphConditionalHandle h, int init) {
     cudaGraphSetConditional(h, init ? more[0] : (more[0] && more[1]));
     if (!init) more[2]++;  // WHILE iterations (launch accounting)
 }
 
 void launch_step_end(const StepEndArgs &a, cudaStream_t s) { k_step_end<<<1, 256, 0, s>>>(a); }
+int test_step_barrier(int nranks, int iters, uint32_t *mbox, uint32_t *seq, uint32_t *bad, cudaStream_t s) {
+    void *args[] = {&mbox, &seq, &nranks, &iters, &bad};
+    return (int)cudaLaunchCooperativeKernel((const void *)k_barrier_emulate, dim3(nranks), dim3(32), args, 0, s);
+}
 void launch_loop_cond(uint32_t *more, cudaGraphConditionalHandle h, int init, cudaStream_t s) {
     k_loop_cond<<<1, 1, 0, s>>>(more, h, init);
 }
@@ -1793,6 +1846,10 @@ void march_grids_init() {
     for (int any = 0; any < 2; ++any) {
         march_grid<1>(any); march_grid<4>(any); march_grid<8>(any); march_grid<32>(any);
     }
+}
+int march_variants_count(const StepArgs &a) {
+    if (a.W.nbricks == 0 || (a.F.flags & DPR_FLAG_DELTA) || a.F.march_inline_min == 0) return 0;
+    return a.F.march_g ? 1 : 3;
 }
 int launch_march_variants(const StepArgs &a, bool any, cudaStream_t s) {
     if (a.W.nbricks == 0 || (a.F.flags & DPR_FLAG_DELTA) || a.F.march_inline_min == 0) return 0;

@@ -85,14 +85,15 @@ class dpr_stats(_c.Structure):
                 ("kernel_nodes_local", _c.c_int64 * 2), ("kernel_tris_local", _c.c_int64 * 2),
                 ("kernel_sphs_local", _c.c_int64 * 2), ("kernel_vols_local", _c.c_int64 * 2),
                 ("bvh_nodes_local", _c.c_int64), ("bvh_levels_local", _c.c_int64),
-                ("step_loop_device", _c.c_int64), ("graph_builds", _c.c_int64)]
+                ("step_loop_device", _c.c_int64), ("graph_builds", _c.c_int64),
+                ("comm_nranks", _c.c_int64), ("ms_kernel_span", _c.c_double * 2)]
 
     def to_dict(self) -> dict:
         n = self.nranks
         S = np.frombuffer(self.S, np.int64).reshape(3, R, R)[:, :n, :n].copy()
         V = np.frombuffer(self.V, np.int64).reshape(3, R)[:, :n].copy()
         arrays = ("S", "V", "rays", "kernel_rays_local", "kernel_nodes_local", "kernel_tris_local",
-                  "kernel_sphs_local", "kernel_vols_local")
+                  "kernel_sphs_local", "kernel_vols_local", "ms_kernel_span")
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in arrays}
         for k in arrays[3:]:
             d[k] = list(getattr(self, k))
@@ -121,7 +122,8 @@ EXPORTS = ["dpr_get_unique_id", "dpr_create_device", "dpr_create_device_hostcoll
            "dpr_render_frame_group", "dpr_render_frame_composite", "dpr_render_frame_composite_group",
            "dpr_render_frame_replicated", "dpr_render_frame_replicated_group",
            "dpr_frame_ready", "dpr_map_frame", "dpr_get_debug",
-           "dpr_get_stats", "dpr_get_step_stats", "dpr_last_error", "dpr_exchange_plan"]
+           "dpr_get_stats", "dpr_get_step_stats", "dpr_last_error", "dpr_exchange_plan",
+           "dpr_test_step_barrier"]
 
 _lib = None
 
@@ -139,6 +141,7 @@ def load(path: str = LIB_PATH):
     L.dpr_create_loopback_group.argtypes = [_c.c_int, _c.c_int, _P, _P, _P]
     L.dpr_create_device_hostcoll.argtypes = [_c.c_int, _c.c_int, _c.c_int, _P, _P, _P, _P]
     L.dpr_get_step_stats.argtypes = [_P, _c.c_int, _P, _P, _P, _P, _P]
+    L.dpr_test_step_barrier.argtypes = [_c.c_int, _c.c_int, _c.c_int, _P]
     for n in ("dpr_release_device", "dpr_clear_parts", "dpr_commit_world", "dpr_render_frame",
               "dpr_render_frame_composite", "dpr_render_frame_replicated"):
         getattr(L, n).argtypes = [_P]
@@ -178,6 +181,13 @@ def exchange_plan(nranks: int, rank: int, counts: np.ndarray, capacity: int):
     rc = load().dpr_exchange_plan(nranks, rank, c.ctypes.data, capacity, off.ctypes.data,
                                   _c.byref(tin), _c.byref(gt))
     return rc, off, tin.value, gt.value
+
+
+def test_step_barrier(cuda_device: int, nranks: int, iters: int) -> int:
+    """dpr_test_step_barrier: mismatching boundaries of the emulated mailbox barrier."""
+    m = _c.c_int64(-1)
+    _check(load().dpr_test_step_barrier(cuda_device, nranks, iters, _c.byref(m)))
+    return m.value
 
 
 def get_unique_id() -> bytes:

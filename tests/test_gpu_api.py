@@ -194,3 +194,12 @@ def test_committed_world_renders_while_next_parts_are_committed():
         assert not ((evB & 0x80000000) != 0).any() and (evB[:, 0] >= 2).any()
     finally:
         dev.release()
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 8, 16])
+def test_step_barrier_protocol(nranks):
+    """The mailbox step barrier of the device-driven loop (seq-parity double buffering, release
+    / acquire over peer memory, error OR-ing), all ranks as blocks of ONE cooperative kernel
+    with skewed arrivals: every boundary's gathered sums are right."""
+    dpr = _dpr()
+    assert dpr.test_step_barrier(0, nranks, 2000) == 0

@@ -126,6 +126,10 @@ def test_occlusion_resolve_fused_and_separate(monkeypatch):
     and the fused frame launches one kernel less per occlusion wavefront."""
     sc = di.config2(nranks=1, G=41, W=96, H=80, spp=4, spp_batch=2)
     o = oracle_render(sc.parts, 1, sc.camera, sc.frame)
+    assert_parity(gpu_render(sc.parts, 1, sc.camera, sc.frame), o)  # device-driven loop
+    # launch accounting on the host loop (the device loop launches k_resolve_occl always; it
+    # exits at once when the trace resolved the queue)
+    monkeypatch.setenv("DPR_STEP_LOOP", "host")
     fused = gpu_render(sc.parts, 1, sc.camera, sc.frame)
     assert_parity(fused, o)
     monkeypatch.setenv("DPR_NO_FUSE_RESOLVE", "1")

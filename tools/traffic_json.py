@@ -32,6 +32,9 @@ for r in rows[2:]:
               "version": tag,
               "issue_active_pct": num('smsp__issue_active.avg.pct_of_peak_sustained_active'),
               "active_threads_per_warp_inst": num('smsp__thread_inst_executed_per_inst_executed.ratio'),
-              "warps_active_pct": num('sm__warps_active.avg.pct_of_peak_sustained_active')}
+              "warps_active_pct": num('sm__warps_active.avg.pct_of_peak_sustained_active'),
+              "inst_executed_per_launch": num('smsp__inst_executed.sum'),
+              "ncu_duration_ns": num('gpu__time_duration.sum'),
+              "sm_mhz": num('sm__cycles_elapsed.avg.per_second')}
 json.dump(out, open(path, 'w'), indent=1)
 print(json.dumps(ent, indent=1))
