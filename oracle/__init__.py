@@ -87,6 +87,9 @@ def lib():
         L.or_render_dp.restype = ctypes.c_int
         L.or_render_dp.argtypes = [_P, _P, _P, _P, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P,
                                    ctypes.c_int]
+        L.or_render_dp_steps.restype = ctypes.c_int
+        L.or_render_dp_steps.argtypes = [_P, _P, _P, _P, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P,
+                                         _P, _P, ctypes.c_int, ctypes.c_int]
         L.or_set_brute.argtypes = [ctypes.c_int]
         L.or_render_union_depth.restype = ctypes.c_int
         L.or_render_union_depth.argtypes = [_P, _P, _P, _P, ctypes.c_int64, _P, _P, ctypes.c_int]
@@ -229,11 +232,17 @@ class RenderResult:
     S: Optional[np.ndarray] = None    # (3,N,N) routing matrix
     V: Optional[np.ndarray] = None    # (3,N) visits
     steps: Optional[np.ndarray] = None  # per spp batch
+    S_step: Optional[np.ndarray] = None  # (total steps, 3, N, N): per-step routing (P8b), batches in order
+    V_step: Optional[np.ndarray] = None  # (total steps, 3, N)
+
+
+MAX_STEPS_PER_BATCH = 128
 
 
 def render(scene: OracleScene, cam: di.Camera, fr: di.Frame, pixels=None, dp: bool = False,
-           dumps: bool = True, nthreads: int = 0) -> RenderResult:
-    """Render the listed pixel indices (all samples each); pixels=None -> whole frame."""
+           dumps: bool = True, nthreads: int = 0, step_matrices: bool = False) -> RenderResult:
+    """Render the listed pixel indices (all samples each); pixels=None -> whole frame.
+    step_matrices (dp only): also the per-step routing matrices / visits of P8b."""
     if pixels is None:
         pixels = np.arange(fr.W * fr.H, dtype=np.int64)
     pixels = np.ascontiguousarray(pixels, np.int64)
@@ -247,7 +256,23 @@ def render(scene: OracleScene, cam: di.Camera, fr: di.Frame, pixels=None, dp: bo
     if dp:
         S = np.zeros((3, N, N), np.int64)
         V = np.zeros((3, N), np.int64)
-        steps = np.zeros((fr.spp + fr.spp_batch - 1) // fr.spp_batch, np.int64)
+        nb = (fr.spp + fr.spp_batch - 1) // fr.spp_batch
+        steps = np.zeros(nb, np.int64)
+        if step_matrices:
+            M = MAX_STEPS_PER_BATCH
+            Ss = np.zeros((nb, M, 3, N, N), np.int64)
+            Vs = np.zeros((nb, M, 3, N), np.int64)
+            rc = lib().or_render_dp_steps(scene.h, ctypes.byref(c), ctypes.byref(f), pixels.ctypes.data, n,
+                                          rgba.ctypes.data, _ptr(ev), _ptr(oc), S.ctypes.data, V.ctypes.data,
+                                          gen.ctypes.data, steps.ctypes.data, Ss.ctypes.data, Vs.ctypes.data,
+                                          M, nthreads)
+            if rc != 0:
+                raise ValueError("or_render_dp_steps failed")
+            if steps.max(initial=0) > M:
+                raise ValueError("more steps per batch than MAX_STEPS_PER_BATCH")
+            S_step = np.concatenate([Ss[b, :steps[b]] for b in range(nb)])
+            V_step = np.concatenate([Vs[b, :steps[b]] for b in range(nb)])
+            return RenderResult(rgba, ev, oc, gen, S, V, steps, S_step, V_step)
         rc = lib().or_render_dp(scene.h, ctypes.byref(c), ctypes.byref(f), pixels.ctypes.data, n,
                                 rgba.ctypes.data, _ptr(ev), _ptr(oc), S.ctypes.data,
                                 V.ctypes.data, gen.ctypes.data, steps.ctypes.data, nthreads)

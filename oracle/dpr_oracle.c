@@ -1035,6 +1035,8 @@ typedef struct {
     uint32_t *events, *occl;
     float *depth;         /* optional: per listed pixel, min over samples of the primary event t */
     int64_t *S, *V, *gen, *steps; /* shared outputs, merged under lock */
+    int64_t *S_step, *V_step;     /* optional per-step matrices [batch][step][3][N][N], [batch][step][3][N] */
+    int max_steps;                /* steps recorded per batch (later steps accumulate into the last) */
     int64_t nbatches;
     int64_t next;         /* atomic work counter */
     pthread_mutex_t lock;
@@ -1042,7 +1044,31 @@ typedef struct {
 
 typedef struct {
     int64_t *S, *V, gen[3], *steps;
+    int64_t *S_step, *V_step;
 } Local;
+
+/* P8b per-step counters: a forward or spawn counted in S happens in the exchange of the step
+ * in which its ray was traced (resolving ray's step for children), a visit in the step that
+ * traces it; rays carry their batch-relative step. */
+static void count_S(const Job *J, Local *L, int64_t batch, int step, int kind, int src, int dst)
+{
+    const int N = J->sc->nranks;
+    L->S[(kind * N + src) * N + dst]++;
+    if (L->S_step) {
+        const int k = step < J->max_steps ? step : J->max_steps - 1;
+        L->S_step[(((batch * J->max_steps + k) * 3 + kind) * N + src) * N + dst]++;
+    }
+}
+
+static void count_V(const Job *J, Local *L, int64_t batch, int step, int kind, int rank)
+{
+    const int N = J->sc->nranks;
+    L->V[kind * N + rank]++;
+    if (L->V_step) {
+        const int k = step < J->max_steps ? step : J->max_steps - 1;
+        L->V_step[((batch * J->max_steps + k) * 3 + kind) * N + rank]++;
+    }
+}
 
 #define STACK_MAX 256
 
@@ -1167,13 +1193,13 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
                 trace_path_at(J, -1, &ray, &vk, &best);
             } else {
                 for (;;) {
-                    L->V[K_PATH * N + at]++;
+                    count_V(J, L, batch, ray.step, K_PATH, at);
                     note_step(L, batch, ray.step);
                     trace_path_at(J, at, &ray, &vk, &best);
                     int nx = ring ? ((at + 1) % N == home ? -1 : (at + 1) % N)
                                   : next_candidate(sc, at, ray.o, ray.d, ray.tmax, best.t);
                     if (nx < 0) break;
-                    L->S[(K_PATH * N + at) * N + nx]++;
+                    count_S(J, L, batch, ray.step, K_PATH, at, nx);
                     at = nx;
                     ray.step++;
                 }
@@ -1252,7 +1278,7 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
                         }
                         continue;
                     }
-                    if (first != at) L->S[(ch.kind * N + at) * N + first]++;
+                    if (first != at) count_S(J, L, batch, ray.step, ch.kind, at, first);
                     ch.rank = first;
                     ch.step = ray.step + 1;
                 }
@@ -1267,7 +1293,7 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
             } else {
                 int at = ray.rank;
                 for (;;) {
-                    L->V[ray.kind * N + at]++;
+                    count_V(J, L, batch, ray.step, ray.kind, at);
                     note_step(L, batch, ray.step);
                     if (!occluded && trace_occl_at(J, at, &ray, &vk)) {
                         occluded = 1;
@@ -1276,7 +1302,7 @@ static void render_sample(const Job *J, Local *L, int64_t pi, uint32_t p, uint32
                     int nx = ring ? ((at + 1) % N == home ? -1 : (at + 1) % N)
                                   : next_candidate(sc, at, ray.o, ray.d, ray.tmax, ray.tmax);
                     if (nx < 0) break;
-                    L->S[(ray.kind * N + at) * N + nx]++;
+                    count_S(J, L, batch, ray.step, ray.kind, at, nx);
                     at = nx;
                     ray.step++;
                 }
@@ -1299,6 +1325,9 @@ static void *worker(void *arg)
     L.S = (int64_t *)calloc((size_t)3 * N * N, sizeof(int64_t));
     L.V = (int64_t *)calloc((size_t)3 * N, sizeof(int64_t));
     L.steps = (int64_t *)calloc((size_t)J->nbatches, sizeof(int64_t));
+    const size_t nst = (size_t)J->nbatches * (size_t)(J->max_steps > 0 ? J->max_steps : 1) * 3;
+    if (J->S_step) L.S_step = (int64_t *)calloc(nst * N * N, sizeof(int64_t));
+    if (J->V_step) L.V_step = (int64_t *)calloc(nst * N, sizeof(int64_t));
     for (;;) {
         int64_t i0 = __atomic_fetch_add(&J->next, 16, __ATOMIC_RELAXED);
         if (i0 >= J->npix) break;
@@ -1316,14 +1345,17 @@ static void *worker(void *arg)
     for (int i = 0; i < 3; ++i) if (J->gen) J->gen[i] += L.gen[i];
     for (int64_t b = 0; b < J->nbatches; ++b)
         if (J->steps && J->steps[b] < L.steps[b]) J->steps[b] = L.steps[b];
+    if (J->S_step) for (size_t i = 0; i < nst * N * N; ++i) J->S_step[i] += L.S_step[i];
+    if (J->V_step) for (size_t i = 0; i < nst * N; ++i) J->V_step[i] += L.V_step[i];
     pthread_mutex_unlock(&J->lock);
-    free(L.S); free(L.V); free(L.steps);
+    free(L.S); free(L.V); free(L.steps); free(L.S_step); free(L.V_step);
     return NULL;
 }
 
 static int run(const OScene *sc, const or_camera *cam, const or_frame *fr, const int64_t *pix,
                int64_t npix, int dp, double *rgba, uint32_t *events, uint32_t *occl, int64_t *S,
-               int64_t *V, int64_t *gen, int64_t *steps, int nthreads, float *depth)
+               int64_t *V, int64_t *gen, int64_t *steps, int nthreads, float *depth,
+               int64_t *S_step, int64_t *V_step, int max_steps)
 {
     if (!sc || !cam || !fr || fr->W <= 0 || fr->H <= 0 || fr->spp <= 0 || fr->spp_batch <= 0 ||
         fr->max_depth <= 0 || fr->ao_k < 0 || fr->ao_k > 30)
@@ -1336,6 +1368,9 @@ static int run(const OScene *sc, const or_camera *cam, const or_frame *fr, const
     J.depth = depth;
     if (depth) for (int64_t i = 0; i < npix; ++i) depth[i] = INFINITY;
     J.nbatches = (fr->spp + fr->spp_batch - 1) / fr->spp_batch;
+    J.S_step = S_step; J.V_step = V_step; J.max_steps = max_steps > 0 ? max_steps : 1;
+    if (S_step) memset(S_step, 0, sizeof(int64_t) * (size_t)J.nbatches * J.max_steps * 3 * sc->nranks * sc->nranks);
+    if (V_step) memset(V_step, 0, sizeof(int64_t) * (size_t)J.nbatches * J.max_steps * 3 * sc->nranks);
     pthread_mutex_init(&J.lock, NULL);
     if (events) memset(events, 0, (size_t)fr->spp * fr->max_depth * npix * sizeof(uint32_t));
     if (occl) memset(occl, 0, (size_t)fr->spp * fr->max_depth * npix * sizeof(uint32_t));
@@ -1355,7 +1390,7 @@ OR_EXPORT int or_render_union(const OScene *sc, const or_camera *cam, const or_f
                               const int64_t *pix, int64_t npix, double *rgba, uint32_t *events,
                               uint32_t *occl, int64_t *gen, int nthreads)
 {
-    return run(sc, cam, fr, pix, npix, 0, rgba, events, occl, NULL, NULL, gen, NULL, nthreads, NULL);
+    return run(sc, cam, fr, pix, npix, 0, rgba, events, occl, NULL, NULL, gen, NULL, nthreads, NULL, NULL, NULL, 0);
 }
 
 /* Union renderer with a per-pixel depth output (min over samples of the primary event t,
@@ -1365,7 +1400,7 @@ OR_EXPORT int or_render_union_depth(const OScene *sc, const or_camera *cam, cons
                                     const int64_t *pix, int64_t npix, double *rgba, float *depth,
                                     int nthreads)
 {
-    return run(sc, cam, fr, pix, npix, 0, rgba, NULL, NULL, NULL, NULL, NULL, NULL, nthreads, depth);
+    return run(sc, cam, fr, pix, npix, 0, rgba, NULL, NULL, NULL, NULL, NULL, NULL, nthreads, depth, NULL, NULL, 0);
 }
 
 /* Routing simulator (P8/P8b).  S: 3*N*N, V: 3*N, steps: ceil(spp/spp_batch). */
@@ -1374,7 +1409,19 @@ OR_EXPORT int or_render_dp(const OScene *sc, const or_camera *cam, const or_fram
                            uint32_t *occl, int64_t *S, int64_t *V, int64_t *gen, int64_t *steps,
                            int nthreads)
 {
-    return run(sc, cam, fr, pix, npix, 1, rgba, events, occl, S, V, gen, steps, nthreads, NULL);
+    return run(sc, cam, fr, pix, npix, 1, rgba, events, occl, S, V, gen, steps, nthreads, NULL, NULL, NULL, 0);
+}
+
+/* Routing simulator with the P8b per-step matrices: S_step [nbatches][max_steps][3][N][N] and
+ * V_step [nbatches][max_steps][3][N] (batch-relative steps; steps >= max_steps accumulate into
+ * the last slot).  Their sums over steps are S and V. */
+OR_EXPORT int or_render_dp_steps(const OScene *sc, const or_camera *cam, const or_frame *fr,
+                                 const int64_t *pix, int64_t npix, double *rgba, uint32_t *events,
+                                 uint32_t *occl, int64_t *S, int64_t *V, int64_t *gen, int64_t *steps,
+                                 int64_t *S_step, int64_t *V_step, int max_steps, int nthreads)
+{
+    return run(sc, cam, fr, pix, npix, 1, rgba, events, occl, S, V, gen, steps, nthreads, NULL, S_step, V_step,
+               max_steps);
 }
 
 /* ------------------------------------------------------------------------------------ */

@@ -540,7 +540,7 @@ int build_world(Dev *d) {
             RET(ensure(d, d->b_nlo, sizeof(float4) * (n - 1)));
             RET(ensure(d, d->b_nhi, sizeof(float4) * (n - 1)));
             if (d->builder == 0) {
-                // PLOC (default): locally-ordered agglomerative clustering on the Morton order
+                // PLOC (DPR_BUILDER=ploc): locally-ordered agglomerative clustering on the Morton order
                 RET(ensure(d, d->b_items[0], sizeof(int) * n));  // reused as cluster lists
                 RET(ensure(d, d->b_items[1], sizeof(int) * n));
                 RET(ensure(d, d->b_parent, sizeof(int) * n));     // reused as nearest neighbours

@@ -260,8 +260,8 @@ __device__ __forceinline__ f3 ray_id(int t) { return mk(s_ray[6][t], s_ray[7][t]
 #endif
 #if DPR_SM_STACK > 0
 // the first DPR_SM_STACK node-group stack entries of each thread in shared memory (SoA; sweep
-// r01_smstack: 3 best, 14.67 -> 14.51 ms occlusion trace on configs[1]),
-// deeper entries in local memory
+// r01_smstack: 3 best at first, 14.67 -> 14.51 ms occlusion trace on configs[1]; 4 after the
+// traversal-order table, r01_v12), deeper entries in local memory
 __shared__ uint2 s_stack[DPR_SM_STACK][TRACE_BLOCK];
 #ifndef DPR_LEAF_BF
 #define DPR_LEAF_BF 0

@@ -40,6 +40,7 @@ def gpu_render(parts, nranks, cam, fr, dumps=True, loopback=True, frames=1):
             e, o = devs[0].get_debug(fr.spp, fr.max_depth, fr.W * fr.H)
             ev, oc = e.cpu().numpy(), o.cpu().numpy()
         stats = devs[0].get_stats()
+        stats["step"] = devs[0].get_step_stats()
         others = [d.map_frame() for d in devs[1:]]
         assert all(o is None for o in others)
         torch.cuda.synchronize()
@@ -52,7 +53,7 @@ def gpu_render(parts, nranks, cam, fr, dumps=True, loopback=True, frames=1):
 def oracle_render(parts, nranks, cam, fr, pixels=None, dp=True):
     import oracle as orc
     sc = orc.OracleScene(parts, nranks)
-    return orc.render(sc, cam, fr, pixels=pixels, dp=dp)
+    return orc.render(sc, cam, fr, pixels=pixels, dp=dp, step_matrices=dp)
 
 
 def assert_pixels_close(gpu_rgba, ora_rgba, max_abs=MAX_ABS, mean_abs=MEAN_ABS):
@@ -71,4 +72,8 @@ def assert_parity(gpu, ora, check_routing=True):
         assert np.array_equal(st["S"], ora.S), (st["S"], ora.S)
         assert np.array_equal(st["V"], ora.V), (st["V"], ora.V)
         assert st["steps"] == int(ora.steps.sum()), (st["steps"], ora.steps)
+        if ora.S_step is not None and "step" in st and len(ora.S_step) <= 256:
+            # P8b per-step routing matrices and visits, bit-exact
+            assert np.array_equal(st["step"]["S"], ora.S_step), "per-step S differ"
+            assert np.array_equal(st["step"]["V"], ora.V_step), "per-step V differ"
     assert_pixels_close(rgba, ora.rgba)

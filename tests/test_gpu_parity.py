@@ -391,3 +391,24 @@ def test_skewed_camera_basis(nranks):
     g = gpu_render(parts, nranks, cam, fr)
     o = oracle_render(parts, nranks, cam, fr)
     assert_parity(g, o)
+
+
+@pytest.mark.parametrize("builder", ["ploc", "karras", "agglo"])
+@pytest.mark.parametrize("nranks", [1, 3])
+def test_bvh_builders(builder, nranks, monkeypatch):
+    """Every binary builder that ships in libdpr.so (DPR_BUILDER: agglomerative LBVH, the
+    default; Karras 2012 + bottom-up refit; PLOC) gives the same events, occlusion bits and
+    routing as the oracle (traversal result = brute force over the rank's prims, P9)."""
+    monkeypatch.setenv("DPR_BUILDER", builder)
+    parts = _random_world(21, nranks, ntri=400, nsph=120)
+    W = H = 40
+    cam = di.camera_basis((0.3, 0.8, -3.5), (0, 0, 0), (0, 1, 0), 45.0, W, H)
+    fr = di.Frame(W=W, H=H, spp=2, spp_batch=2, max_depth=2, ao_k=2, ao_radius=0.6,
+                  light_dir=di.f32(di.normalize((0.4, 1, -0.3))), E=(1, 1, 1), A=(0.3, 0.3, 0.3))
+    g = gpu_render(parts, nranks, cam, fr)
+    o = oracle_render(parts, nranks, cam, fr)
+    assert_parity(g, o)
+    sc = di.config2(nranks=nranks, G=41, W=48, H=40, spp=2, spp_batch=2)
+    g = gpu_render(sc.parts, nranks, sc.camera, sc.frame)
+    o = oracle_render(sc.parts, nranks, sc.camera, sc.frame)
+    assert_parity(g, o)

@@ -132,6 +132,13 @@ def test_routing_hand_cases(case, golden_dir):
     assert int(r.occl[0, 0, 0]) == g["occl"]
     assert np.allclose(r.rgba[0], g["rgba"], atol=1e-7)
     assert r.steps.tolist() == [g["steps"]]
+    # per-step matrices (P8b): entries of each step, hand-derived
+    rs = orc.render(orc.OracleScene(sc.parts, 2), sc.camera, sc.frame, dp=True, step_matrices=True)
+    assert len(rs.S_step) == g["steps"]
+    for k in range(g["steps"]):
+        assert sorted(np.argwhere(rs.S_step[k]).tolist()) == sorted(g["S_steps"][k]), k
+        assert (rs.S_step[k][rs.S_step[k] != 0] == 1).all()
+        assert sorted(np.argwhere(rs.V_step[k]).tolist()) == sorted(g["V_steps"][k]), k
     u = _render(di.union_parts(sc.parts), 1, sc.camera, sc.frame)
     assert np.array_equal(u.events, r.events) and np.allclose(u.rgba, r.rgba, atol=1e-12)
 
@@ -207,6 +214,11 @@ def test_partition_independence(nranks, seed):
     _assert_same_image(dpres, u)
     assert dpres.S.sum() > 0
     assert len(dpres.steps) == 2
+    # P8b per-step matrices add up to the frame totals; a step's visits at rank r are the rays
+    # queued for r by the previous step (forwards + spawns into r, or kept primaries at step 0)
+    st = orc.render(orc.OracleScene(parts, nranks), cam, fr, dp=True, step_matrices=True)
+    assert np.array_equal(st.S_step.sum(axis=0), dpres.S) and np.array_equal(st.V_step.sum(axis=0), dpres.V)
+    assert len(st.S_step) == dpres.steps.sum()
 
 
 def _const_volume(G, value, alpha, nbricks=1, nranks=1):

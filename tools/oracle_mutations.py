@@ -65,6 +65,8 @@ MUTATIONS = [
      "ch.step = ray.step + 1;", "ch.step = ray.step;"),
     ("degenerate_not_zeroed", "R-DEGEN: zero-area triangles keep their edges",
      "if (ng.x == 0.0f && ng.y == 0.0f && ng.z == 0.0f) { *e1 = V3(0, 0, 0); *e2 = V3(0, 0, 0); }", ""),
+    ("step_matrix_late", "P8b per-step S recorded in the following step",
+     "L->S_step[(((batch * J->max_steps + k) * 3", "L->S_step[(((batch * J->max_steps + (k + 1 < J->max_steps ? k + 1 : k)) * 3"),
     ("forward_double_step", "P8b a forward costs two steps",
      "at = nx;\n                    ray.step++;", "at = nx;\n                    ray.step += 2;"),
 ]
