@@ -143,9 +143,12 @@ def test_config5_full_size_sampled():
         rgba = dev.map_frame().reshape(-1, 4).cpu().numpy().astype(np.float64)
         P = fr.W * fr.H
         pix = np.sort(np.random.default_rng(9).choice(P, 1000, replace=False))
+        import torch
         ev, oc = dev.get_debug(fr.spp, fr.max_depth, P)
-        ev = ev[:, :, pix].cpu().numpy()
-        oc = oc[:, :, pix].cpu().numpy()
+        ix = torch.as_tensor(pix, device="cuda")
+        # torch has no uint32 gather on CUDA: reinterpret as int32 (same bits)
+        ev = ev.view(torch.int32)[:, :, ix].cpu().numpy().view(np.uint32)
+        oc = oc.view(torch.int32)[:, :, ix].cpu().numpy().view(np.uint32)
         st = dev.get_stats()
     finally:
         dev.release()
