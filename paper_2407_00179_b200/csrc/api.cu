@@ -132,7 +132,7 @@ struct Dev {
     bool nonempty = false;
     Buf b_prims_u, b_blo, b_bhi, b_keys[2], b_vals[2], b_tile, b_left, b_right, b_parent, b_rlo,
         b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_bounds, b_hist, b_wnodes, b_chunks,
-        b_prims_w, b_inv, b_items[2], b_wcnt, b_wperm, b_witems[2], b_size;
+        b_prims_w, b_inv, b_items[2], b_wcnt, b_wperm, b_witems[2], b_size, b_bn;
     int builder = 1;  // 0 PLOC, 1 agglomerative LBVH (default), 2 Karras + refit (env DPR_BUILDER=ploc|karras)
     int build_iters = 0;
     int64_t wnodes_count = 0;
@@ -526,19 +526,23 @@ int build_world(Dev *d) {
         }
         uint64_t *keys = P<uint64_t>(d->b_keys[cur]);
         uint32_t *perm = P<uint32_t>(d->b_vals[cur]);
-        RET(ensure(d, d->b_slo, sizeof(float4) * n));
-        RET(ensure(d, d->b_shi, sizeof(float4) * n));
+        // packed leaf records in Morton order: leaf[2j] = lo, leaf[2j+1] = hi
+        RET(ensure(d, d->b_slo, sizeof(float4) * 2 * n));
+        float4 *leaf = P<float4>(d->b_slo);
         launch_gather_prims(P<float4>(d->b_prims_u), perm, n, nullptr, P<float4>(d->b_blo),
-                            P<float4>(d->b_bhi), P<float4>(d->b_slo), P<float4>(d->b_shi), s);
+                            P<float4>(d->b_bhi), leaf, leaf + 1, s);
         launches++;
         int root_id = 0;
         const int *root_dev = nullptr;  // device copy of the root id (agglomerative builder)
-        if (n > 1) {
+        if (n > 1) RET(ensure(d, d->b_bn, sizeof(BNode) * (n - 1)));
+        if (n > 1 && d->builder != 1) {  // separate arrays of the Karras / PLOC builders
             RET(ensure(d, d->b_left, sizeof(int) * (n - 1)));
             RET(ensure(d, d->b_right, sizeof(int) * (n - 1)));
             RET(ensure(d, d->b_size, sizeof(int) * (n - 1)));
             RET(ensure(d, d->b_nlo, sizeof(float4) * (n - 1)));
             RET(ensure(d, d->b_nhi, sizeof(float4) * (n - 1)));
+        }
+        if (n > 1) {
             if (d->builder == 0) {
                 // PLOC (DPR_BUILDER=ploc): locally-ordered agglomerative clustering on the Morton order
                 RET(ensure(d, d->b_items[0], sizeof(int) * n));  // reused as cluster lists
@@ -547,7 +551,7 @@ int build_world(Dev *d) {
                 int64_t nbmax = ploc_block_count(n);
                 RET(ensure(d, d->b_rlo, sizeof(int) * 2 * nbmax + 16));  // block counts + totals
                 PlocArgs pa;
-                pa.n = n; pa.slo = P<float4>(d->b_slo); pa.shi = P<float4>(d->b_shi);
+                pa.n = n; pa.slo = leaf; pa.shi = leaf + 1;
                 pa.nlo = P<float4>(d->b_nlo); pa.nhi = P<float4>(d->b_nhi);
                 pa.left = P<int>(d->b_left); pa.right = P<int>(d->b_right); pa.size = P<int>(d->b_size);
                 int *cl[2] = {P<int>(d->b_items[0]), P<int>(d->b_items[1])};
@@ -577,6 +581,9 @@ int build_world(Dev *d) {
                 CK(cudaMemcpyAsync(&root_id, cl[c], sizeof(int), cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
                 d->build_iters = iters;
+                launch_pack_bnodes(n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_size), P<float4>(d->b_nlo),
+                                   P<float4>(d->b_nhi), P<BNode>(d->b_bn), s);
+                launches++;
             } else if (d->builder == 1) {
                 // agglomerative LBVH (default): topology + boxes in one bottom-up pass
                 RET(ensure(d, d->b_arrive, sizeof(int) * (n - 1) + sizeof(int)));
@@ -584,9 +591,7 @@ int build_world(Dev *d) {
                 CK(cudaMemsetAsync(other, 0xff, sizeof(int) * (n - 1), s));
                 // the other radix-sort key buffer is free now: per-split prefix lengths
                 uint8_t *split = P<uint8_t>(d->b_keys[keys == P<uint64_t>(d->b_keys[0]) ? 1 : 0]);
-                launches += launch_agglo(keys, split, n, P<float4>(d->b_slo), P<float4>(d->b_shi), P<int>(d->b_left),
-                                         P<int>(d->b_right), P<int>(d->b_size), P<float4>(d->b_nlo),
-                                         P<float4>(d->b_nhi), other, other + (n - 1), s);
+                launches += launch_agglo(keys, split, n, leaf, P<BNode>(d->b_bn), other, other + (n - 1), s);
                 root_dev = other + (n - 1);  // read by the first collapse level on the device
             } else {
                 // Karras 2012 LBVH + bottom-up refit
@@ -597,9 +602,11 @@ int build_world(Dev *d) {
                 CK(cudaMemsetAsync(d->b_arrive.p, 0, sizeof(int) * (n - 1), s));
                 launch_karras(keys, n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_parent),
                               P<int>(d->b_rlo), P<int>(d->b_rhi), P<int>(d->b_size), s);
-                launch_refit(n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_parent), P<float4>(d->b_slo),
-                             P<float4>(d->b_shi), P<float4>(d->b_nlo), P<float4>(d->b_nhi), P<int>(d->b_arrive), s);
-                launches += 2;
+                launch_refit(n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_parent), leaf, leaf + 1,
+                             P<float4>(d->b_nlo), P<float4>(d->b_nhi), P<int>(d->b_arrive), s);
+                launch_pack_bnodes(n, P<int>(d->b_left), P<int>(d->b_right), P<int>(d->b_size), P<float4>(d->b_nlo),
+                                   P<float4>(d->b_nhi), P<BNode>(d->b_bn), s);
+                launches += 3;
             }
         }
         // collapse into compressed 8-wide nodes, one BFS level per launch
@@ -623,9 +630,7 @@ int build_world(Dev *d) {
         if (n > 1 && root_dev)  // agglomerative builder: the root id stays on the device
             CK(cudaMemcpyAsync(&P<int2>(d->b_witems[0])->y, root_dev, sizeof(int), cudaMemcpyDeviceToDevice, s));
         CollapseArgs ca;
-        ca.n = n; ca.left = P<int>(d->b_left); ca.right = P<int>(d->b_right); ca.size = P<int>(d->b_size);
-        ca.nlo = P<float4>(d->b_nlo); ca.nhi = P<float4>(d->b_nhi);
-        ca.slo = P<float4>(d->b_slo); ca.shi = P<float4>(d->b_shi);
+        ca.n = n; ca.bn = P<BNode>(d->b_bn); ca.leaf = leaf;
         ca.perm = P<uint32_t>(d->b_wperm); ca.nodes = P<WNode>(d->b_wnodes); ca.counters = cnt;
         ca.node_cap = node_cap;
         int h_cnt[4 + MAXL + BATCH + 1];
@@ -1948,7 +1953,7 @@ void release_bufs(Dev *d) {
     Buf *bs[] = {&d->b_prims_u, &d->b_blo, &d->b_bhi, &d->b_keys[0], &d->b_keys[1], &d->b_vals[0],
                  &d->b_vals[1], &d->b_tile, &d->b_left, &d->b_right, &d->b_parent, &d->b_rlo, &d->b_rhi,
                  &d->b_nlo, &d->b_nhi, &d->b_arrive, &d->b_prims, &d->b_slo, &d->b_shi,
-                 &d->b_bounds, &d->b_chunks, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_inv, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_witems[0], &d->b_witems[1], &d->b_size, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
+                 &d->b_bounds, &d->b_chunks, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_inv, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_witems[0], &d->b_witems[1], &d->b_size, &d->b_bn, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
                  &d->b_counts, &d->b_in_count, &d->b_fetch, &d->b_part_lo, &d->b_part_alb, &d->b_scratch,
                  &d->b_path[0], &d->b_path[1], &d->b_occlq[0], &d->b_occlq[1]};
     for (Buf *b : bs) dfree(d, *b);

@@ -32,17 +32,24 @@ void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *
 void launch_refit(int64_t n, const int *left, const int *right, const int *parent,
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
                   cudaStream_t s);
-// split_scratch: >= n-1 bytes (the unused radix-sort key buffer); returns kernels launched
-int launch_agglo(const uint64_t *keys, uint8_t *split_scratch, int64_t n, const float4 *slo, const float4 *shi,
-                 int *left, int *right, int *size, float4 *nlo, float4 *nhi, int *other, int *root_out,
-                 cudaStream_t s);
+// Binary node record (32 B, one sector): a = (lo.xyz, left id | min(size, 7) << 29),
+// b = (hi.xyz, right id); ids: internal k in [0, n-1), leaf j -> n-1+j.
+struct BNode { float4 a, b; };
+// split_scratch: >= n-1 bytes (the unused radix-sort key buffer); leaf: packed leaf boxes
+// (leaf[2j] = lo, leaf[2j+1] = hi); returns kernels launched
+int launch_agglo(const uint64_t *keys, uint8_t *split_scratch, int64_t n, const float4 *leaf, BNode *bn,
+                 int *other, int *root_out, cudaStream_t s);
+// BNode records from the separate arrays of the Karras + refit / PLOC builders
+void launch_pack_bnodes(int64_t n, const int *left, const int *right, const int *size, const float4 *nlo,
+                        const float4 *nhi, BNode *bn, cudaStream_t s);
+// slo / shi: the packed leaf records (slo = leaf, shi = leaf + 1; written at stride 2)
 void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
                          const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,
                          cudaStream_t s);
 struct CollapseArgs {
     int64_t n;
-    const int *left, *right, *size;  // binary internal nodes: children, subtree prim counts
-    const float4 *nlo, *nhi, *slo, *shi;
+    const BNode *bn;     // binary internal nodes
+    const float4 *leaf;  // packed leaf boxes (leaf[2j] = lo, leaf[2j+1] = hi)
     uint32_t *perm;  // per-wide-node contiguous prim order: perm[dst] = sorted prim index
     WNode *nodes;
     int *counters;  // [1] wide nodes allocated, [2] prims placed, [3] capacity overflow
@@ -56,7 +63,7 @@ void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t
 // ---- ploc.cu: PLOC binary builder (Meister & Bittner 2018) ------------------------------
 struct PlocArgs {
     int64_t n;
-    const float4 *slo, *shi;  // leaf boxes (Morton order)
+    const float4 *slo, *shi;  // leaf boxes (Morton order), packed records: index 2j
     float4 *nlo, *nhi;        // internal node boxes
     int *left, *right, *size; // internal nodes [0, n-1)
 };

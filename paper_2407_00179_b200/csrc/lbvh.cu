@@ -17,6 +17,8 @@
 //   8. k_macrocells: per 16^3 macrocell "alpha may be > 0" flags for exact empty-space
 //      skipping in bricks
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -424,7 +426,7 @@ __global__ void k_refit(int64_t n, const int *__restrict__ left, const int *__re
         float4 lo = make_float4(0, 0, 0, 0), hi = lo;
         for (int k = 0; k < 2; ++k) {
             float4 a, b;
-            if (c[k] >= n - 1) { a = slo[c[k] - (n - 1)]; b = shi[c[k] - (n - 1)]; }
+            if (c[k] >= n - 1) { a = slo[2 * (c[k] - (n - 1))]; b = shi[2 * (c[k] - (n - 1))]; }
             else { a = __ldcg(nlo + c[k]); b = __ldcg(nhi + c[k]); }
             if (k == 0) { lo = a; hi = b; }
             else {
@@ -453,14 +455,16 @@ __global__ void k_split_delta(const uint64_t *__restrict__ keys, int64_t n, uint
     if (i < n - 1) split[i] = (uint8_t)delta(keys, n, i, i + 1);
 }
 
+// Binary node records (BNode, kernels.h): a = (lo.xyz, left | min(size, 7) << 29), b = (hi.xyz,
+// right) -- one 32-byte sector per node for the collapse and the sibling reads here.  Leaf boxes
+// are packed the same way (leaf[2j] = lo, leaf[2j+1] = hi).
 __global__ void k_agglo(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ split, int64_t n,
-                        const float4 *__restrict__ slo, const float4 *__restrict__ shi, int *left, int *right,
-                        int *size, float4 *nlo, float4 *nhi, int *other, int *root_out) {
+                        const float4 *__restrict__ leaf, BNode *bn, int *other, int *root_out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int64_t l = i, r = i;
     int cur = (int)(n - 1 + i);
-    float4 lo = slo[i], hi = shi[i];
+    float4 lo = leaf[2 * i], hi = leaf[2 * i + 1];
     for (;;) {
         bool is_left;
         if (l == 0) is_left = true;
@@ -468,26 +472,41 @@ __global__ void k_agglo(const uint64_t *__restrict__ keys, const uint8_t *__rest
         else if (split) is_left = __ldg(split + r) > __ldg(split + l - 1);
         else is_left = delta(keys, n, r, r + 1) > delta(keys, n, l - 1, l);
         const int64_t p = is_left ? r : l - 1;
-        if (is_left) left[p] = cur;
-        else right[p] = cur;
+        // my id into p's left / right word (the sibling that finishes p reads it)
+        if (is_left) __stcg(reinterpret_cast<float *>(&bn[p].a) + 3, __int_as_float(cur));
+        else __stcg(reinterpret_cast<float *>(&bn[p].b) + 3, __int_as_float(cur));
         int prev;
         const int val = is_left ? (int)l : (int)r;
         asm volatile("atom.exch.acq_rel.gpu.b32 %0, [%1], %2;" : "=r"(prev) : "l"(other + p), "r"(val) : "memory");
         if (prev < 0) return;  // first arrival: the sibling finishes the node
-        const int sib = is_left ? __ldcg(right + p) : __ldcg(left + p);
+        const int sib = is_left ? __float_as_int(__ldcg(reinterpret_cast<const float *>(&bn[p].b) + 3))
+                                : __float_as_int(__ldcg(reinterpret_cast<const float *>(&bn[p].a) + 3)) & 0x1fffffff;
         float4 a, b;
-        if (sib >= n - 1) { a = slo[sib - (n - 1)]; b = shi[sib - (n - 1)]; }
-        else { a = __ldcg(nlo + sib); b = __ldcg(nhi + sib); }
+        if (sib >= n - 1) { a = leaf[2 * (sib - (n - 1))]; b = leaf[2 * (sib - (n - 1)) + 1]; }
+        else { a = __ldcg(&bn[sib].a); b = __ldcg(&bn[sib].b); }
         lo = make_float4(fminf(lo.x, a.x), fminf(lo.y, a.y), fminf(lo.z, a.z), 0.0f);
         hi = make_float4(fmaxf(hi.x, b.x), fmaxf(hi.y, b.y), fmaxf(hi.z, b.z), 0.0f);
         if (is_left) r = prev;
         else l = prev;
-        __stcg(nlo + p, lo);
-        __stcg(nhi + p, hi);
-        size[p] = (int)(r - l + 1);
+        const uint32_t cap = (uint32_t)(r - l + 1 < 7 ? r - l + 1 : 7);
+        const uint32_t lid = (uint32_t)(is_left ? cur : sib), rid = (uint32_t)(is_left ? sib : cur);
+        __stcg(&bn[p].a, make_float4(lo.x, lo.y, lo.z, __uint_as_float(lid | (cap << 29))));
+        __stcg(&bn[p].b, make_float4(hi.x, hi.y, hi.z, __uint_as_float(rid)));
         cur = (int)p;
         if (l == 0 && r == n - 1) { *root_out = cur; return; }
     }
+}
+
+// Packed records from the separate arrays of the Karras + refit and PLOC builders.
+__global__ void k_pack_bnodes(int64_t n, const int *__restrict__ left, const int *__restrict__ right,
+                              const int *__restrict__ size, const float4 *__restrict__ nlo,
+                              const float4 *__restrict__ nhi, BNode *bn) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n - 1) return;
+    const float4 lo = nlo[p], hi = nhi[p];
+    const uint32_t cap = (uint32_t)min(size[p], 7);
+    bn[p].a = make_float4(lo.x, lo.y, lo.z, __uint_as_float((uint32_t)left[p] | (cap << 29)));
+    bn[p].b = make_float4(hi.x, hi.y, hi.z, __uint_as_float((uint32_t)right[p]));
 }
 
 // Outward padding: |x| + 4 scaled by 2^-18 (>= 1.5e-5 absolute).  Covers the FMA box test
@@ -506,8 +525,8 @@ __global__ void k_gather_prims(const float4 *__restrict__ in, const uint32_t *__
         out[3 * i + 1] = in[3 * (int64_t)s + 1];
         out[3 * i + 2] = in[3 * (int64_t)s + 2];
     }
-    slo[i] = blo[s];
-    shi[i] = bhi[s];
+    slo[2 * i] = blo[s];  // packed leaf record: lo at 2i, hi at 2i + 1 (slo + 1 == shi)
+    shi[2 * i] = bhi[s];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -518,46 +537,66 @@ __global__ void k_gather_prims(const float4 *__restrict__ in, const uint32_t *__
 // are copied contiguously per wide node (prim_base + offset, offset < 32).
 // ---------------------------------------------------------------------------------------
 
-// Binary node ids: internal k in [0, n-1), leaf (sorted prim) j -> n-1+j.  sz = prim count.
-__device__ __forceinline__ void bin_child(const CollapseArgs &a, int id, float lo[3], float hi[3], int &sz) {
+// Binary node ids: internal k in [0, n-1), leaf (sorted prim) j -> n-1+j.  One 32-byte
+// record per node (BNode; leaves: a.leaf[2j], a.leaf[2j+1]); sz = min(prim count, 7).
+__device__ __forceinline__ void bin_child(const CollapseArgs &a, int id, float lo[3], float hi[3], int &sz,
+                                          uint32_t &cl, uint32_t &cr) {
     float4 l, h;
     if (id >= a.n - 1) {
-        int j = id - (int)(a.n - 1);
-        l = a.slo[j]; h = a.shi[j]; sz = 1;
+        const int64_t j = id - (a.n - 1);
+        l = __ldg(a.leaf + 2 * j); h = __ldg(a.leaf + 2 * j + 1); sz = 1; cl = cr = 0;
     } else {
-        l = a.nlo[id]; h = a.nhi[id]; sz = a.size[id];
+        l = __ldg(&a.bn[id].a); h = __ldg(&a.bn[id].b);
+        const uint32_t w = __float_as_uint(l.w);
+        sz = (int)(w >> 29); cl = w & 0x1fffffffu; cr = __float_as_uint(h.w);
     }
     lo[0] = pad_lo(l.x); lo[1] = pad_lo(l.y); lo[2] = pad_lo(l.z);
     hi[0] = pad_hi(h.x); hi[1] = pad_hi(h.y); hi[2] = pad_hi(h.z);
 }
 
+// One thread per wide node.  (A variant with a group of 8 lanes per node -- one child per
+// lane, group reductions -- used 48 instead of 158 registers but executed ~2000 instructions
+// per node and ran slower: 7.4 vs 5.7 ms per configs[3] build, r02.)
 // Every per-child array is indexed with compile-time indices (unrolled selects), so the child
 // boxes, ids, slot costs and quantised planes stay in registers (an earlier version indexed
 // them dynamically: a 320-416 B local-memory frame that thrashed L1 at full occupancy).
 // Persistent grid-stride loop over the level's items; the item count is read from device
 // memory (cnt_in) and the next level's items are appended (cnt_out), so several levels are
 // launched back to back without a host round trip.
-__global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const int2 *__restrict__ items,
+#ifndef DPR_COLLAPSE_MINB
+#define DPR_COLLAPSE_MINB 4  // 128 registers (4 blocks / SM; 1: 164 registers, 3 blocks): r02 sweep
+#endif
+__global__ void __launch_bounds__(128, DPR_COLLAPSE_MINB) k_collapse_r(const CollapseArgs a, const int2 *__restrict__ items,
                                                     const int *__restrict__ cnt_in, int2 *next, int *cnt_out) {
   const int nitems = *cnt_in;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nitems; t += gridDim.x * blockDim.x) {
-    const int wnode = items[t].x, b = items[t].y;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count (the allocation below is one atomic per warp and counter: with one
+  // per node the three counters took ~30M same-address atomics per configs[3] build)
+  for (int t0 = (int)((blockIdx.x * blockDim.x + threadIdx.x) & ~31u); t0 < nitems; t0 += gridDim.x * blockDim.x) {
+    const int t = t0 + lane;
+    const bool live = t < nitems;
+    const int2 item = live ? items[t] : make_int2(0, 0);
+    const int wnode = item.x, b = item.y;
     int cid[8], c1[8];
+    uint32_t ccl[8], ccr[8];  // children ids of each child (packed records: no extra load)
     float lo[8][3], hi[8][3];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        cid[i] = 0; c1[i] = 0;
+        cid[i] = 0; c1[i] = 0; ccl[i] = ccr[i] = 0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) { lo[i][c] = 0.0f; hi[i][c] = 0.0f; }
     }
-    int nc;
-    if (b < 0) {  // single-prim world: the root holds one leaf
+    int nc = 0;
+    if (!live) {
+    } else if (b < 0) {  // single-prim world: the root holds one leaf
         cid[0] = (int)(a.n - 1);
-        bin_child(a, cid[0], lo[0], hi[0], c1[0]);
+        bin_child(a, cid[0], lo[0], hi[0], c1[0], ccl[0], ccr[0]);
         nc = 1;
     } else {
-        cid[0] = a.left[b]; bin_child(a, cid[0], lo[0], hi[0], c1[0]);
-        cid[1] = a.right[b]; bin_child(a, cid[1], lo[1], hi[1], c1[1]);
+        cid[0] = (int)(__float_as_uint(__ldg(&a.bn[b].a.w)) & 0x1fffffffu);
+        cid[1] = (int)__float_as_uint(__ldg(&a.bn[b].b.w));
+        bin_child(a, cid[0], lo[0], hi[0], c1[0], ccl[0], ccr[0]);
+        bin_child(a, cid[1], lo[1], hi[1], c1[1], ccl[1], ccr[1]);
         nc = 2;
     }
     // pass 0: open the largest-area internal child with > LEAF_MAX prims; pass 1
@@ -574,23 +613,23 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
                 if (area > ba) { ba = area; best = i; }
             }
             if (best < 0) break;
-            int c = 0;
+            int l = 0, r = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) if (i == best) c = cid[i];
-            const int l = a.left[c], r = a.right[c];
+            for (int i = 0; i < 8; ++i) if (i == best) { l = (int)ccl[i]; r = (int)ccr[i]; }
             float llo[3], lhi[3], rlo[3], rhi[3];
             int ls, rs;
-            bin_child(a, l, llo, lhi, ls);
-            bin_child(a, r, rlo, rhi, rs);
+            uint32_t lcl, lcr, rcl, rcr;
+            bin_child(a, l, llo, lhi, ls, lcl, lcr);
+            bin_child(a, r, rlo, rhi, rs, rcl, rcr);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 if (i == best) {
-                    cid[i] = l; c1[i] = ls;
+                    cid[i] = l; c1[i] = ls; ccl[i] = lcl; ccr[i] = lcr;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) { lo[i][k] = llo[k]; hi[i][k] = lhi[k]; }
                 }
                 if (i == nc) {
-                    cid[i] = r; c1[i] = rs;
+                    cid[i] = r; c1[i] = rs; ccl[i] = rcl; ccr[i] = rcr;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) { lo[i][k] = rlo[k]; hi[i][k] = rhi[k]; }
                 }
@@ -618,6 +657,22 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
 #pragma unroll
             for (int c = 0; c < 3; ++c) dc[i][c] = (lo[i][c] + hi[i][c]) - (nlo_[c] + nhi_[c]);
         }
+        // the same greedy (global maximum over unassigned children x free slots, first child
+        // then first slot on ties), with each child's best free slot cached and recomputed only
+        // when another child takes it (the full 8 x 8 rescan per assignment was a fifth of the
+        // kernel's instructions)
+        float bcst[8];
+        int bsl[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            bcst[i] = -3.4e38f; bsl[i] = 0;
+#pragma unroll
+            for (int sl = 0; sl < 8; ++sl) {
+                const float cst = ((sl & 4) ? dc[i][0] : -dc[i][0]) + ((sl & 2) ? dc[i][1] : -dc[i][1]) +
+                                  ((sl & 1) ? dc[i][2] : -dc[i][2]);
+                if (cst > bcst[i]) { bcst[i] = cst; bsl[i] = sl; }
+            }
+        }
         unsigned used_slots = 0, done_child = 0;
         for (int k = 0; k < nc; ++k) {
             float bc = -3.4e38f;
@@ -625,17 +680,23 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 if (i >= nc || (done_child >> i & 1)) continue;
-#pragma unroll
-                for (int sl = 0; sl < 8; ++sl) {
-                    const float cst = ((sl & 4) ? dc[i][0] : -dc[i][0]) + ((sl & 2) ? dc[i][1] : -dc[i][1]) +
-                                      ((sl & 1) ? dc[i][2] : -dc[i][2]);
-                    if (!(used_slots >> sl & 1) && cst > bc) { bc = cst; bi = i; bs = sl; }
-                }
+                if (bcst[i] > bc) { bc = bcst[i]; bi = i; bs = bsl[i]; }
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) if (i == bi) slot_of[i] = bs;
             used_slots |= 1u << bs;
             done_child |= 1u << bi;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (i >= nc || (done_child >> i & 1) || bsl[i] != bs) continue;
+                bcst[i] = -3.4e38f;
+#pragma unroll
+                for (int sl = 0; sl < 8; ++sl) {
+                    const float cst = ((sl & 4) ? dc[i][0] : -dc[i][0]) + ((sl & 2) ? dc[i][1] : -dc[i][1]) +
+                                      ((sl & 1) ? dc[i][2] : -dc[i][2]);
+                    if (!(used_slots >> sl & 1) && cst > bcst[i]) { bcst[i] = cst; bsl[i] = sl; }
+                }
+            }
         }
     }
     // internal vs leaf children, allocation
@@ -649,9 +710,29 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
         if (leaf[i]) { n_prims += c1[i]; lmask |= 1u << slot_of[i]; }
         else { n_int++; imask |= 1u << slot_of[i]; }
     }
-    const int child_base = n_int ? atomicAdd(&a.counters[1], n_int) : 0;
-    const int prim_base = atomicAdd(&a.counters[2], n_prims);
-    if (child_base + n_int > a.node_cap) { atomicOr(&a.counters[3], 1); return; }
+    int child_base, prim_base, out_base;
+    {
+        int xi = n_int, xp = n_prims;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yi = __shfl_up_sync(0xffffffffu, xi, o), yp = __shfl_up_sync(0xffffffffu, xp, o);
+            if (lane >= o) { xi += yi; xp += yp; }
+        }
+        int bi = 0, bp = 0, bo = 0;
+        if (lane == 31) {
+            bi = xi ? atomicAdd(&a.counters[1], xi) : 0;
+            bp = xp ? atomicAdd(&a.counters[2], xp) : 0;
+            bo = xi ? atomicAdd(cnt_out, xi) : 0;
+        }
+        bi = __shfl_sync(0xffffffffu, bi, 31);
+        bp = __shfl_sync(0xffffffffu, bp, 31);
+        bo = __shfl_sync(0xffffffffu, bo, 31);
+        child_base = bi + xi - n_int;
+        prim_base = bp + xp - n_prims;
+        out_base = bo + xi - n_int;
+    }
+    if (!live) continue;
+    if (child_base + n_int > a.node_cap) { atomicOr(&a.counters[3], 1); continue; }
     // quantisation (outward): smallest e with 255 * 2^e >= extent (frexp, no log2); the
     // per-child planes below multiply by the exact power-of-two reciprocal (no division)
     float p[3];
@@ -691,8 +772,7 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
         }
         if (!leaf[i]) {
             const int rank = __popc(imask & ((1u << sl) - 1u));
-            const int k = atomicAdd(cnt_out, 1);
-            next[k] = make_int2(child_base + rank, cid[i]);
+            next[out_base + rank] = make_int2(child_base + rank, cid[i]);
         } else {
             // prims of the leaf children are laid out in slot order
             int off = 0;
@@ -706,7 +786,10 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
             while (sp) {
                 const int x = st[--sp];
                 if (x >= a.n - 1) a.perm[prim_base + off + k++] = (uint32_t)(x - (a.n - 1));
-                else { st[sp++] = a.right[x]; st[sp++] = a.left[x]; }
+                else {
+                    st[sp++] = (int)__float_as_uint(__ldg(&a.bn[x].b.w));
+                    st[sp++] = (int)(__float_as_uint(__ldg(&a.bn[x].a.w)) & 0x1fffffffu);
+                }
             }
         }
     }
@@ -722,8 +805,9 @@ __global__ void __launch_bounds__(128) k_collapse_r(const CollapseArgs a, const 
   }
 }
 
+
 #ifndef DPR_COLLAPSE_GRID
-#define DPR_COLLAPSE_GRID 16  // resident-grid multiple of the persistent collapse launch
+#define DPR_COLLAPSE_GRID 8  // resident-grid multiple of the persistent collapse launch (r02 sweep: 1, 4, 8)
 #endif
 int collapse_grid() {
     static int g = 0;
@@ -890,14 +974,17 @@ void launch_refit(int64_t n, const int *left, const int *right, const int *paren
 #ifndef DPR_AGGLO_SPLIT
 #define DPR_AGGLO_SPLIT 1
 #endif
-int launch_agglo(const uint64_t *keys, uint8_t *split_scratch, int64_t n, const float4 *slo, const float4 *shi,
-                 int *left, int *right, int *size, float4 *nlo, float4 *nhi, int *other, int *root_out,
-                 cudaStream_t s) {
+int launch_agglo(const uint64_t *keys, uint8_t *split_scratch, int64_t n, const float4 *leaf, BNode *bn,
+                 int *other, int *root_out, cudaStream_t s) {
     if (n <= 1) return 0;
     uint8_t *split = DPR_AGGLO_SPLIT ? split_scratch : nullptr;
     if (split) k_split_delta<<<nblk(n, 256), 256, 0, s>>>(keys, n, split);
-    k_agglo<<<nblk(n, 256), 256, 0, s>>>(keys, split, n, slo, shi, left, right, size, nlo, nhi, other, root_out);
+    k_agglo<<<nblk(n, 256), 256, 0, s>>>(keys, split, n, leaf, bn, other, root_out);
     return split ? 2 : 1;
+}
+void launch_pack_bnodes(int64_t n, const int *left, const int *right, const int *size, const float4 *nlo,
+                        const float4 *nhi, BNode *bn, cudaStream_t s) {
+    if (n > 1) k_pack_bnodes<<<nblk(n - 1, 256), 256, 0, s>>>(n, left, right, size, nlo, nhi, bn);
 }
 void launch_gather_prims(const float4 *in, const uint32_t *perm, int64_t n, float4 *out,
                          const float4 *blo, const float4 *bhi, float4 *slo, float4 *shi,

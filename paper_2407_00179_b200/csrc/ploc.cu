@@ -28,7 +28,7 @@ constexpr int PLOC_BLOCK = 1024;
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 __device__ __forceinline__ void node_box(const PlocArgs &a, int id, float4 &lo, float4 &hi) {
-    if (id >= a.n - 1) { lo = a.slo[id - (a.n - 1)]; hi = a.shi[id - (a.n - 1)]; }
+    if (id >= a.n - 1) { lo = a.slo[2 * (id - (a.n - 1))]; hi = a.shi[2 * (id - (a.n - 1))]; }  // packed leaf records
     else { lo = a.nlo[id]; hi = a.nhi[id]; }
 }
 
