@@ -454,19 +454,20 @@ int build_world(Dev *d) {
         launches++;
     }
     // Morton keys + all digit histograms
-    std::vector<unsigned long long> hist(8 * 256, 0);
+    std::vector<unsigned long long> hist(MKEY_DIGITS * 256, 0);
     if (n > 0) {
         for (int i = 0; i < 2; ++i) {
-            RET(ensure(d, d->b_keys[i], sizeof(uint64_t) * n));
+            RET(ensure(d, d->b_keys[i], sizeof(mkey_t) * std::max<int64_t>(n, 2)));
             RET(ensure(d, d->b_vals[i], sizeof(uint32_t) * n));
         }
         launch_morton(P<float4>(d->b_blo), P<float4>(d->b_bhi), n, P<int>(d->b_bounds),
-                      P<uint64_t>(d->b_keys[0]), P<uint32_t>(d->b_vals[0]), s);
-        RET(ensure(d, d->b_hist, sizeof(unsigned long long) * 8 * 256));
-        CK(cudaMemsetAsync(d->b_hist.p, 0, sizeof(unsigned long long) * 8 * 256, s));
-        launch_digit_hist_all(P<uint64_t>(d->b_keys[0]), n, P<unsigned long long>(d->b_hist), d->nsm, s);
+                      P<mkey_t>(d->b_keys[0]), P<uint32_t>(d->b_vals[0]), s);
+        RET(ensure(d, d->b_hist, sizeof(unsigned long long) * MKEY_DIGITS * 256));
+        CK(cudaMemsetAsync(d->b_hist.p, 0, sizeof(unsigned long long) * MKEY_DIGITS * 256, s));
+        launch_digit_hist_all(P<mkey_t>(d->b_keys[0]), n, P<unsigned long long>(d->b_hist), d->nsm, s);
         launches += 2;
-        CK(cudaMemcpyAsync(hist.data(), d->b_hist.p, sizeof(unsigned long long) * 8 * 256, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hist.data(), d->b_hist.p, sizeof(unsigned long long) * MKEY_DIGITS * 256,
+                           cudaMemcpyDeviceToHost, s));
     }
     std::vector<int> bnd(12 * (np + 1) + 1);
     CK(cudaMemcpyAsync(bnd.data(), d->b_bounds.p, bnd.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -515,16 +516,16 @@ int build_world(Dev *d) {
         int cur = 0;
         int64_t ntiles = radix_tiles(n);
         RET(ensure(d, d->b_tile, sizeof(uint32_t) * 256 * (ntiles + 1)));
-        for (int pass = 0; pass < 8; ++pass) {
+        for (int pass = 0; pass < MKEY_DIGITS; ++pass) {
             bool constant = false;
             for (int b = 0; b < 256; ++b) if (hist[pass * 256 + b] == (unsigned long long)n) constant = true;
             if (constant) continue;
-            launch_radix_pass(P<uint64_t>(d->b_keys[cur]), P<uint32_t>(d->b_vals[cur]),
-                              P<uint64_t>(d->b_keys[cur ^ 1]), P<uint32_t>(d->b_vals[cur ^ 1]), n,
+            launch_radix_pass(P<mkey_t>(d->b_keys[cur]), P<uint32_t>(d->b_vals[cur]),
+                              P<mkey_t>(d->b_keys[cur ^ 1]), P<uint32_t>(d->b_vals[cur ^ 1]), n,
                               8 * pass, P<uint32_t>(d->b_tile), s, &launches);
             cur ^= 1;
         }
-        uint64_t *keys = P<uint64_t>(d->b_keys[cur]);
+        mkey_t *keys = P<mkey_t>(d->b_keys[cur]);
         uint32_t *perm = P<uint32_t>(d->b_vals[cur]);
         // packed leaf records in Morton order: leaf[2j] = lo, leaf[2j+1] = hi
         RET(ensure(d, d->b_slo, sizeof(float4) * 2 * n));
@@ -590,7 +591,7 @@ int build_world(Dev *d) {
                 int *other = P<int>(d->b_arrive);
                 CK(cudaMemsetAsync(other, 0xff, sizeof(int) * (n - 1), s));
                 // the other radix-sort key buffer is free now: per-split prefix lengths
-                uint8_t *split = P<uint8_t>(d->b_keys[keys == P<uint64_t>(d->b_keys[0]) ? 1 : 0]);
+                uint8_t *split = P<uint8_t>(d->b_keys[keys == P<mkey_t>(d->b_keys[0]) ? 1 : 0]);
                 launches += launch_agglo(keys, split, n, leaf, P<BNode>(d->b_bn), other, other + (n - 1), s);
                 root_dev = other + (n - 1);  // read by the first collapse level on the device
             } else {

@@ -7,6 +7,10 @@
 
 namespace dpr {
 
+// Morton key of a prim's centroid: 10 bits per axis, 30 bits (LSD radix sort, 4 digit passes)
+typedef uint32_t mkey_t;
+constexpr int MKEY_DIGITS = 4;
+
 // ---- lbvh.cu ---------------------------------------------------------------------------
 // one block of k_part_prims: prims [start, start+count) of one part (global ids g0...)
 struct PrimChunk {
@@ -21,13 +25,13 @@ constexpr int PRIM_CHUNK = 4096;
 void launch_part_prims(const PrimChunk *chunks, int nchunks, float4 *prims, float4 *blo, float4 *bhi, int *bounds,
                        int *bad_index, cudaStream_t s);
 void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
-                   uint64_t *keys, uint32_t *vals, cudaStream_t s);
-void launch_digit_hist_all(const uint64_t *keys, int64_t n, unsigned long long *hist, int nsm,
+                   mkey_t *keys, uint32_t *vals, cudaStream_t s);
+void launch_digit_hist_all(const mkey_t *keys, int64_t n, unsigned long long *hist, int nsm,
                            cudaStream_t s);
 int64_t radix_tiles(int64_t n);
-void launch_radix_pass(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout,
+void launch_radix_pass(const mkey_t *kin, const uint32_t *vin, mkey_t *kout, uint32_t *vout,
                        int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches);
-void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
+void launch_karras(const mkey_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
                    int *rhi, int *size, cudaStream_t s);
 void launch_refit(int64_t n, const int *left, const int *right, const int *parent,
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
@@ -37,7 +41,7 @@ void launch_refit(int64_t n, const int *left, const int *right, const int *paren
 struct BNode { float4 a, b; };
 // split_scratch: >= n-1 bytes (the unused radix-sort key buffer); leaf: packed leaf boxes
 // (leaf[2j] = lo, leaf[2j+1] = hi); returns kernels launched
-int launch_agglo(const uint64_t *keys, uint8_t *split_scratch, int64_t n, const float4 *leaf, BNode *bn,
+int launch_agglo(const mkey_t *keys, uint8_t *split_scratch, int64_t n, const float4 *leaf, BNode *bn,
                  int *other, int *root_out, cudaStream_t s);
 // BNode records from the separate arrays of the Karras + refit / PLOC builders
 void launch_pack_bnodes(int64_t n, const int *left, const int *right, const int *size, const float4 *nlo,

@@ -30,8 +30,10 @@ namespace dpr {
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 #ifndef DPR_MORTON_BITS
-#define DPR_MORTON_BITS 10
+#define DPR_MORTON_BITS 10  // per axis; 30-bit codes in 32-bit keys (r01: 21 bits/axis in 64-bit keys
+                            // traced no faster and doubled the sort's key traffic)
 #endif
+static_assert(DPR_MORTON_BITS <= 10, "Morton keys are 32-bit");
 
 __device__ __forceinline__ int f2ord(float f) {
     int i = __float_as_int(f);
@@ -138,34 +140,31 @@ __global__ void __launch_bounds__(256) k_part_prims(const PrimChunk *__restrict_
     acc.block_flush(bounds + 12 * c.slot, bounds);
 }
 
-__device__ __forceinline__ uint64_t expand21(uint64_t v) {
-    v &= 0x1fffffull;
-    v = (v | v << 32) & 0x1f00000000ffffull;
-    v = (v | v << 16) & 0x1f0000ff0000ffull;
-    v = (v | v << 8) & 0x100f00f00f00f00full;
-    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
-    v = (v | v << 2) & 0x1249249249249249ull;
+__device__ __forceinline__ uint32_t expand10(uint32_t v) {  // bit i -> bit 3i (10 bits)
+    v &= 0x3ffu;
+    v = (v | v << 16) & 0x030000ffu;
+    v = (v | v << 8) & 0x0300f00fu;
+    v = (v | v << 4) & 0x030c30c3u;
+    v = (v | v << 2) & 0x09249249u;
     return v;
 }
 
 __global__ void k_morton(const float4 *__restrict__ blo, const float4 *__restrict__ bhi, int64_t n,
-                         const int *__restrict__ bounds, uint64_t *keys, uint32_t *vals) {
+                         const int *__restrict__ bounds, mkey_t *keys, uint32_t *vals) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float4 lo = blo[i], hi = bhi[i];
     float c[3] = {(lo.x + hi.x) * 0.5f, (lo.y + hi.y) * 0.5f, (lo.z + hi.z) * 0.5f};
-    uint64_t q[3];
+    uint32_t q[3];
     for (int a = 0; a < 3; ++a) {
         float mn = ord2f(bounds[6 + a]), mx = ord2f(bounds[9 + a]);
         float ext = mx - mn;
-        // DPR_MORTON_BITS per axis (<= 21); high digit passes of the radix sort are skipped
-        // automatically when the keys are shorter (constant digits)
         const float cells = (float)(1u << DPR_MORTON_BITS);
         float x = ext > 0.0f ? (c[a] - mn) / ext * cells : 0.0f;
         x = fminf(fmaxf(x, 0.0f), cells - 1.0f);
-        q[a] = (uint64_t)x;
+        q[a] = (uint32_t)x;
     }
-    keys[i] = (expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]);
+    keys[i] = (expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]);
     vals[i] = (uint32_t)i;
 }
 
@@ -177,22 +176,22 @@ constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 
 // All 8 digit histograms in one read of the keys (to find constant-digit passes).
-__global__ void k_digit_hist_all(const uint64_t *__restrict__ keys, int64_t n,
-                                 unsigned long long *hist /*8*256*/) {
-    __shared__ unsigned int h[8][256];
-    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+__global__ void k_digit_hist_all(const mkey_t *__restrict__ keys, int64_t n,
+                                 unsigned long long *hist /*MKEY_DIGITS*256*/) {
+    __shared__ unsigned int h[MKEY_DIGITS][256];
+    for (int i = threadIdx.x; i < MKEY_DIGITS * 256; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t k = keys[i];
-        for (int p = 0; p < 8; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255], 1u);
+        const mkey_t k = keys[i];
+        for (int p = 0; p < MKEY_DIGITS; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255], 1u);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
+    for (int i = threadIdx.x; i < MKEY_DIGITS * 256; i += blockDim.x)
         if ((&h[0][0])[i]) atomicAdd(&hist[i], (unsigned long long)(&h[0][0])[i]);
 }
 
-__global__ void k_tile_hist(const uint64_t *__restrict__ keys, int64_t n, int shift,
+__global__ void k_tile_hist(const mkey_t *__restrict__ keys, int64_t n, int shift,
                             uint32_t *tile_hist, int ntiles) {
     __shared__ unsigned int h[256];
     h[threadIdx.x] = 0;
@@ -245,7 +244,7 @@ __global__ void __launch_bounds__(1024) k_scan_digits(uint32_t *tile_hist, int n
 }
 
 __global__ void __launch_bounds__(RS_THREADS)
-k_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *kout,
+k_scatter(const mkey_t *__restrict__ kin, const uint32_t *__restrict__ vin, mkey_t *kout,
           uint32_t *vout, int64_t n, int shift, const uint32_t *__restrict__ tile_off, int ntiles,
           const uint32_t *__restrict__ digit_tot) {
     __shared__ uint32_t wcnt[RS_THREADS / 32][256];
@@ -273,7 +272,7 @@ k_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, ui
         __syncthreads();
         int64_t i = base + j * RS_THREADS + threadIdx.x;
         bool valid = i < n;
-        uint64_t k = valid ? kin[i] : 0;
+        mkey_t k = valid ? kin[i] : 0;
         uint32_t v = valid ? vin[i] : 0;
         int d = valid ? (int)((k >> shift) & 255) : 256 + lane;  // invalid lanes: unique groups
         unsigned peers = __match_any_sync(0xffffffffu, d);
@@ -304,7 +303,7 @@ k_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, ui
 // consecutive threads store to consecutive addresses of a bucket instead of 256 scattered
 // buckets per warp store.
 __global__ void __launch_bounds__(RS_THREADS)
-k_scatter_c(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *kout,
+k_scatter_c(const mkey_t *__restrict__ kin, const uint32_t *__restrict__ vin, mkey_t *kout,
             uint32_t *vout, int64_t n, int shift, const uint32_t *__restrict__ tile_off, int ntiles,
             const uint32_t *__restrict__ digit_tot) {
     __shared__ uint32_t wcnt[RS_THREADS / 32][256];
@@ -336,7 +335,7 @@ k_scatter_c(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, 
         __syncthreads();
         const int64_t i = base + j * RS_THREADS + threadIdx.x;
         const bool valid = i < n;
-        const uint64_t k = valid ? kin[i] : 0;
+        const mkey_t k = valid ? kin[i] : 0;
         const int d = valid ? (int)((k >> shift) & 255) : 256 + lane;  // invalid lanes: unique groups
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const uint32_t rank = __popc(peers & lt);
@@ -359,7 +358,7 @@ k_scatter_c(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, 
     const int count = (int)min((int64_t)RS_TILE, n - base);
     for (int i = threadIdx.x; i < count; i += RS_THREADS) {
         const int64_t gi = base + sidx[i];
-        const uint64_t k = kin[gi];
+        const mkey_t k = kin[gi];
         const int d = (int)((k >> shift) & 255);
         const uint32_t pos = goff[d] + (uint32_t)(i - (int)lstart[d]);
         kout[pos] = k;
@@ -371,14 +370,15 @@ k_scatter_c(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, 
 // Karras 2012 hierarchy.  Internal nodes 0..n-2; child c < n-1 -> internal, else leaf
 // (c-(n-1)) in sorted order.
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ int delta(const uint64_t *keys, int64_t n, int64_t i, int64_t j) {
+// common-prefix length of sorted keys i, j, augmented by the index for equal keys
+__device__ __forceinline__ int delta(const mkey_t *keys, int64_t n, int64_t i, int64_t j) {
     if (j < 0 || j >= n) return -1;
-    uint64_t a = keys[i], b = keys[j];
-    if (a == b) return 64 + __clz((uint32_t)(i ^ j));
-    return __clzll(a ^ b);
+    const mkey_t a = keys[i], b = keys[j];
+    if (a == b) return 32 + __clz((uint32_t)(i ^ j));
+    return __clz(a ^ b);
 }
 
-__global__ void k_karras(const uint64_t *__restrict__ keys, int64_t n, int *left, int *right,
+__global__ void k_karras(const mkey_t *__restrict__ keys, int64_t n, int *left, int *right,
                          int *parent, int *rlo, int *rhi, int *size) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n - 1) return;
@@ -450,7 +450,7 @@ __global__ void k_refit(int64_t n, const int *__restrict__ left, const int *__re
 // (acq_rel exchange) merges both boxes and continues.  The root is reported in *root_out.
 // split[i] = delta(i, i+1) (common-prefix length of adjacent sorted keys, index-augmented),
 // one byte per split: k_agglo reads two bytes per step instead of four 64-bit keys
-__global__ void k_split_delta(const uint64_t *__restrict__ keys, int64_t n, uint8_t *split) {
+__global__ void k_split_delta(const mkey_t *__restrict__ keys, int64_t n, uint8_t *split) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n - 1) split[i] = (uint8_t)delta(keys, n, i, i + 1);
 }
@@ -458,7 +458,7 @@ __global__ void k_split_delta(const uint64_t *__restrict__ keys, int64_t n, uint
 // Binary node records (BNode, kernels.h): a = (lo.xyz, left | min(size, 7) << 29), b = (hi.xyz,
 // right) -- one 32-byte sector per node for the collapse and the sibling reads here.  Leaf boxes
 // are packed the same way (leaf[2j] = lo, leaf[2j+1] = hi).
-__global__ void k_agglo(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ split, int64_t n,
+__global__ void k_agglo(const mkey_t *__restrict__ keys, const uint8_t *__restrict__ split, int64_t n,
                         const float4 *__restrict__ leaf, BNode *bn, int *other, int *root_out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -939,17 +939,17 @@ void launch_part_prims(const PrimChunk *chunks, int nchunks, float4 *prims, floa
     if (nchunks > 0) k_part_prims<<<nchunks, 256, 0, s>>>(chunks, prims, blo, bhi, bounds, bad_index);
 }
 void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
-                   uint64_t *keys, uint32_t *vals, cudaStream_t s) {
+                   mkey_t *keys, uint32_t *vals, cudaStream_t s) {
     if (n > 0) k_morton<<<nblk(n, 256), 256, 0, s>>>(blo, bhi, n, bounds, keys, vals);
 }
-void launch_digit_hist_all(const uint64_t *keys, int64_t n, unsigned long long *hist, int nsm,
+void launch_digit_hist_all(const mkey_t *keys, int64_t n, unsigned long long *hist, int nsm,
                            cudaStream_t s) {
     unsigned g = (unsigned)std::min<int64_t>(nblk(n, 256), (int64_t)nsm * 4);
     if (g == 0) g = 1;
     k_digit_hist_all<<<g, 256, 0, s>>>(keys, n, hist);
 }
 int64_t radix_tiles(int64_t n) { return (n + RS_TILE - 1) / RS_TILE; }
-void launch_radix_pass(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout,
+void launch_radix_pass(const mkey_t *kin, const uint32_t *vin, mkey_t *kout, uint32_t *vout,
                        int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches) {
     int ntiles = (int)radix_tiles(n);
     uint32_t *digit_tot = tile_hist + (int64_t)256 * ntiles;  // 256 extra words
@@ -962,7 +962,7 @@ void launch_radix_pass(const uint64_t *kin, const uint32_t *vin, uint64_t *kout,
     else k_scatter<<<ntiles, RS_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, tile_hist, ntiles, digit_tot);
     *launches += 3;
 }
-void launch_karras(const uint64_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
+void launch_karras(const mkey_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
                    int *rhi, int *size, cudaStream_t s) {
     if (n > 1) k_karras<<<nblk(n - 1, 256), 256, 0, s>>>(keys, n, left, right, parent, rlo, rhi, size);
 }
@@ -974,7 +974,7 @@ void launch_refit(int64_t n, const int *left, const int *right, const int *paren
 #ifndef DPR_AGGLO_SPLIT
 #define DPR_AGGLO_SPLIT 1
 #endif
-int launch_agglo(const uint64_t *keys, uint8_t *split_scratch, int64_t n, const float4 *leaf, BNode *bn,
+int launch_agglo(const mkey_t *keys, uint8_t *split_scratch, int64_t n, const float4 *leaf, BNode *bn,
                  int *other, int *root_out, cudaStream_t s) {
     if (n <= 1) return 0;
     uint8_t *split = DPR_AGGLO_SPLIT ? split_scratch : nullptr;
