@@ -686,6 +686,7 @@ int build_world(Dev *d) {
         B.tf = P<float4>(p.tf);
         B.tf_lo = p.tf_lo; B.tf_hi = p.tf_hi; B.dscale = p.dscale;
         B.tf_rd = exact_recip_pow2(B.tf_hi - B.tf_lo);  // the same binary32 difference as the kernels
+
         d->wbricks.push_back(B);
         d->amax_local = std::max(d->amax_local, p.amax);
     }

@@ -270,6 +270,14 @@ struct BrickDev {
     float tf_rd;            // 1/(tf_hi - tf_lo) when that difference is a power of two, else 0
 };
 
+// P10 grid coordinate g = (p - O) / h (IEEE division, global origin / spacing).  (A division-
+// free form, q1 = fma(fma(-q0, h, x), RN(1/h), q0), checked exhaustively equal to x / h for
+// every binary32 |x| in [2^-100, 4] at configs[2]'s h, ran slower in the march kernels at the
+// 64-register cap: 2.85 vs 2.76 ms, r02.)
+__device__ __forceinline__ f3 grid_coord(const BrickDev &B, f3 pt) {
+    return mk((pt.x - B.O[0]) / B.h[0], (pt.y - B.O[1]) / B.h[1], (pt.z - B.O[2]) / B.h[2]);
+}
+
 constexpr int MC_SIZE = 16;
 constexpr int MC_DIST_PASSES = 8, MC_DIST_CAP = MC_DIST_PASSES + 1;  // exact below the cap
 constexpr int MAX_BRICKS = 8;

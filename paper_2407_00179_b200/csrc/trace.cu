@@ -158,8 +158,11 @@ __device__ __forceinline__ bool fuse_resolve_dev(const StepArgs &A, uint32_t n) 
 }
 
 // trace kernel start / end stamps of the current step (first start via max of ~t)
+#ifndef DPR_STAMPS
+#define DPR_STAMPS 1
+#endif
 __device__ __forceinline__ void stamp_kernel(const StepArgs &A, int kind, bool start) {
-    if (!A.rec || threadIdx.x != 0) return;
+    if (!DPR_STAMPS || !A.rec || (threadIdx.x & 31) != 0 || (start && threadIdx.x != 0)) return;
     const uint32_t k = min(A.rec->step, (uint32_t)MAX_STEP_REC - 1);
     const unsigned long long t = gtimer();
     if (start) atomicMax(&A.rec->kt[k][kind][0], ~t);
@@ -647,7 +650,7 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
         float ti = sample_t(i, dt);
         if (!(ti < bound)) return false;
         f3 pt = mk(o.x + ti * d.x, o.y + ti * d.y, o.z + ti * d.z);
-        f3 g = mk((pt.x - B.O[0]) / B.h[0], (pt.y - B.O[1]) / B.h[1], (pt.z - B.O[2]) / B.h[2]);
+        f3 g = grid_coord(B, pt);
         if (!(g.x >= (float)B.lo[0] && g.x < (float)B.hi[0] && g.y >= (float)B.lo[1] &&
               g.y < (float)B.hi[1] && g.z >= (float)B.lo[2] && g.z < (float)B.hi[2]))
             continue;
@@ -845,7 +848,7 @@ __device__ __forceinline__ void march_groups(const StepArgs &A) {
                 const int64_t j = jl + k;
                 tk[k] = sample_t(j, dt);
                 const f3 pt = mk(r.o.x + tk[k] * r.d.x, r.o.y + tk[k] * r.d.y, r.o.z + tk[k] * r.d.z);
-                const f3 g = mk((pt.x - B.O[0]) / B.h[0], (pt.y - B.O[1]) / B.h[1], (pt.z - B.O[2]) / B.h[2]);
+                const f3 g = grid_coord(B, pt);
                 const bool own = g.x >= (float)B.lo[0] && g.x < (float)B.hi[0] && g.y >= (float)B.lo[1] &&
                                  g.y < (float)B.hi[1] && g.z >= (float)B.lo[2] && g.z < (float)B.hi[2];
                 const float fx0 = floorf(g.x), fy0 = floorf(g.y), fz0 = floorf(g.z);
@@ -1013,7 +1016,7 @@ __device__ __noinline__ bool delta_track(const WorldDev &W, f3 o, f3 d, float li
         const f3 pt = mk(o.x + t * d.x, o.y + t * d.y, o.z + t * d.z);
         for (int b = 0; b < W.nbricks; ++b) {
             const BrickDev &B = W.bricks[b];
-            const f3 g = mk((pt.x - B.O[0]) / B.h[0], (pt.y - B.O[1]) / B.h[1], (pt.z - B.O[2]) / B.h[2]);
+            const f3 g = grid_coord(B, pt);
             if (!(g.x >= (float)B.lo[0] && g.x < (float)B.hi[0] && g.y >= (float)B.lo[1] && g.y < (float)B.hi[1] &&
                   g.z >= (float)B.lo[2] && g.z < (float)B.hi[2]))
                 continue;
@@ -1292,8 +1295,7 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
     flush(&kc->sphs, tc.sphs);
     flush(&kc->vols, tc.vols);
     flush(&kc->rin, rin);
-    __syncthreads();
-    stamp_kernel(A, ANY ? 1 : 0, false);
+    stamp_kernel(A, ANY ? 1 : 0, false);  // each warp at its exit: the last one is the kernel's end
 }
 
 __global__ void __launch_bounds__(TRACE_BLOCK, TRACE_MINB) k_trace_path(const __grid_constant__ StepArgs A) {
@@ -1756,6 +1758,7 @@ void launch_loop_cond(uint32_t *more, cudaGraphConditionalHandle h, int init, cu
 }
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
 
 void launch_depth_init(uint32_t *depth, int64_t n, cudaStream_t s) {
     if (n > 0) k_depth_init<<<nblk(n, 256), 256, 0, s>>>(depth, n);
