@@ -15,6 +15,6 @@ CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e
 $CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/${TAG}_launches_${CFG}.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "launches rc=$?"
-$CMD > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k "$KRE" -s 2 -c 3 \
+$CMD > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k "$KRE" -s ${NCU_SKIP:-2} -c ${NCU_COUNT:-3} \
   -o gpurun_out/${TAG}_${CFG} $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"

@@ -18,6 +18,7 @@ out = json.load(open(path)) if os.path.exists(path) else {}
 if out and not all(isinstance(v, dict) and all(isinstance(x, dict) for x in v.values()) for v in out.values()):
     out = {}  # old flat layout (kernel -> figures) is replaced
 ent = out.setdefault(cfg, {})
+acc = {}
 for r in rows[2:]:
     n = r[hdr.index('Kernel Name')].split('(')[0].split('<')[0].replace('void ', '').strip()
     b = sum(float(r[hdr.index(k)].replace(',', '')) * mult[units[hdr.index(k)]]
@@ -28,13 +29,21 @@ for r in rows[2:]:
             return float(r[hdr.index(k)].replace(',', ''))
         except (ValueError, IndexError):
             return None
-    ent[n] = {"dram_bytes_per_launch": b, "source": f"{summary} (ncu --set full, 1 launch)",
-              "version": tag,
-              "issue_active_pct": num('smsp__issue_active.avg.pct_of_peak_sustained_active'),
-              "active_threads_per_warp_inst": num('smsp__thread_inst_executed_per_inst_executed.ratio'),
-              "warps_active_pct": num('sm__warps_active.avg.pct_of_peak_sustained_active'),
-              "inst_executed_per_launch": num('smsp__inst_executed.sum'),
-              "ncu_duration_ns": num('gpu__time_duration.sum'),
-              "sm_mhz": num('sm__cycles_elapsed.avg.per_second')}
+    a = acc.setdefault(n, {"n": 0, "bytes": 0.0, "inst": 0.0, "issue": 0.0, "simt": 0.0, "warps": 0.0,
+                           "dur": 0.0})
+    a["n"] += 1
+    a["bytes"] += b
+    a["inst"] += num('smsp__inst_executed.sum') or 0.0
+    a["issue"] += num('smsp__issue_active.avg.pct_of_peak_sustained_active') or 0.0
+    a["simt"] += num('smsp__thread_inst_executed_per_inst_executed.ratio') or 0.0
+    a["warps"] += num('sm__warps_active.avg.pct_of_peak_sustained_active') or 0.0
+    a["dur"] += num('gpu__time_duration.sum') or 0.0
+# per-launch averages over the captured launches of each kernel (launch-weighted)
+for n, a in acc.items():
+    k = a["n"]
+    ent[n] = {"dram_bytes_per_launch": a["bytes"] / k, "source": f"{summary} (ncu --set full, {k} launch(es))",
+              "version": tag, "issue_active_pct": a["issue"] / k, "active_threads_per_warp_inst": a["simt"] / k,
+              "warps_active_pct": a["warps"] / k, "inst_executed_per_launch": a["inst"] / k,
+              "ncu_duration_per_launch": a["dur"] / k, "launches": k}
 json.dump(out, open(path, 'w'), indent=1)
 print(json.dumps(ent, indent=1))
