@@ -51,7 +51,12 @@ typedef enum {
     DPR_ERR_INVALID_ARG = -1,   /* bad pointer/size/enum; nothing was changed */
     DPR_ERR_STATE = -2,         /* call not valid now (e.g. render before commit_world) */
     DPR_ERR_CUDA = -3,          /* a CUDA runtime error; the device should be released */
-    DPR_ERR_NCCL = -4,          /* an NCCL error (incl. async errors); release the device */
+    DPR_ERR_NCCL = -4,          /* an NCCL error, incl. asynchronous ones (polled with
+                                   ncclCommGetAsyncError while waiting), a collective that did not
+                                   complete within DPR_TIMEOUT_S seconds (default 600), or a
+                                   device step barrier that did not complete within
+                                   min(DPR_TIMEOUT_S, 60) s (a dead peer): the communicator is
+                                   aborted; every later collective returns this; release the device */
     DPR_ERR_CONSISTENCY = -5,   /* camera/frame parameters differ between ranks */
     DPR_ERR_OOM = -6,           /* device allocation failed */
     DPR_ERR_QUEUE_OVERFLOW = -7 /* a ray queue exceeded its capacity; lower spp_batch */

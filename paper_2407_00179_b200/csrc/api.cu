@@ -457,7 +457,7 @@ int build_world(Dev *d) {
     std::vector<unsigned long long> hist(MKEY_DIGITS * 256, 0);
     if (n > 0) {
         for (int i = 0; i < 2; ++i) {
-            RET(ensure(d, d->b_keys[i], sizeof(mkey_t) * std::max<int64_t>(n, 2)));
+            RET(ensure(d, d->b_keys[i], sizeof(mkey_t) * n + 64));  // + the agglomeration fetch counter
             RET(ensure(d, d->b_vals[i], sizeof(uint32_t) * n));
         }
         launch_morton(P<float4>(d->b_blo), P<float4>(d->b_bhi), n, P<int>(d->b_bounds),
@@ -1136,7 +1136,7 @@ struct AppMsg {
     int64_t ovf;
 };
 
-int fused_sync(std::vector<Dev *> &L, std::vector<uint32_t> &in, int64_t &total, unsigned &ovf) {
+int fused_sync(std::vector<Dev *> &L, std::vector<uint32_t> &in, int64_t &total, unsigned &ovf, double &ms_coll) {
     Dev *d0 = L[0];
     const int N = d0->nranks;
     std::vector<AppMsg> mine(L.size());
@@ -1161,7 +1161,9 @@ int fused_sync(std::vector<Dev *> &L, std::vector<uint32_t> &in, int64_t &total,
     std::vector<const void *> snd;
     for (auto &m : mine) snd.push_back(&m);
     std::vector<std::vector<char>> o;
+    const auto c0 = std::chrono::steady_clock::now();  // the exchange proper: after the local sync
     RET(allgather_host(L, snd, sizeof(AppMsg), o));  // loopback: a copy; else the barrier
+    ms_coll += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
     const AppMsg *all = reinterpret_cast<const AppMsg *>(o[0].data());
     in.assign((size_t)2 * N, 0);
     total = 0;
@@ -1203,7 +1205,7 @@ StepEndArgs make_step_end(std::vector<Dev *> &L, const std::vector<int> &cur, in
         e.mbox_self = P<uint32_t>(d0->b_mbox);
         for (int r = 0; r < d0->nranks; ++r) e.mbox_peer[r] = d0->peer_mbox[r];
         e.seq = P<uint32_t>(d0->b_seq);
-        e.timeout_ns = (unsigned long long)(d0->timeout_s * 1e9);
+        e.timeout_ns = (unsigned long long)(std::min(d0->timeout_s, 60.0) * 1e9);  // one step boundary
     }
     e.more = P<uint32_t>(d0->b_more);
     e.more_slot = -1;
@@ -1530,9 +1532,7 @@ int render_group(std::vector<Dev *> &L) {
             std::vector<uint32_t> in;
             int64_t total = 0;
             unsigned ovf = 0;
-            const auto h0 = std::chrono::steady_clock::now();
-            RET(fused_sync(L, in, total, ovf));
-            ms_sync_host += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+            RET(fused_sync(L, in, total, ovf, ms_sync_host));
             if (getenv("DPR_DEBUG_STEPS")) {
                 fprintf(stderr, "[dpr rank %d] step boundary:", d0->rank);
                 for (int r = 0; r < N; ++r) fprintf(stderr, " r%d{%u,%u}", r, in[2 * r], in[2 * r + 1]);
@@ -1837,7 +1837,7 @@ int render_group(std::vector<Dev *> &L) {
                 st.ms_trace_path = sum_ms(tm.path);
                 st.ms_trace_occl = sum_ms(tm.occl);
                 // send-recv: grouped send/recv (CUDA events); fused host loop: the host-side
-                // step boundary (counts to the host + barrier), wall clock
+                // boundary collective (after the local stream is idle), wall clock
                 st.ms_exchange = fused ? ms_sync_host : sum_ms(t_exch);
             }
             float rms = 0;

@@ -497,6 +497,85 @@ __global__ void k_agglo(const mkey_t *__restrict__ keys, const uint8_t *__restri
     }
 }
 
+// The same agglomeration as a persistent kernel with per-lane leaf replacement: a lane whose
+// climb ends (first arrival at a node) starts the next leaf of its warp's pool at once, so the
+// warp's lanes stay busy (one thread per leaf retires half its warp after the first step and
+// ran at 6.4/32 active lanes).  Any order of leaf starts builds the same tree: a node is
+// finished by whichever child arrives second.  fetch: leaf counter (zeroed by the launcher).
+__global__ void __launch_bounds__(256) k_agglo_p(const uint8_t *__restrict__ split, int64_t n,
+                                                 const float4 *__restrict__ leaf, BNode *bn, int *other,
+                                                 int *root_out, unsigned long long *fetch) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    bool alive = false, exhausted = false;
+    int64_t l = 0, r = 0, pool = 0, pool_end = 0;
+    int cur = 0;
+    float4 lo = make_float4(0, 0, 0, 0), hi = lo;
+    for (;;) {
+        const unsigned dead = __ballot_sync(0xffffffffu, !alive);
+        if (dead && !exhausted) {
+            // refill the dead lanes from the warp's pool (64 leaves per fetch)
+            int need = __popc(dead);
+            while (need > 0 && !exhausted) {
+                if (pool >= pool_end) {
+                    unsigned long long b = 0;
+                    if (lane == 0) b = atomicAdd(fetch, 64ull);
+                    b = __shfl_sync(0xffffffffu, b, 0);
+                    if ((int64_t)b >= n) { exhausted = true; break; }
+                    pool = (int64_t)b;
+                    pool_end = (int64_t)b + 64 < n ? (int64_t)b + 64 : n;
+                }
+                const unsigned want = __ballot_sync(0xffffffffu, !alive);
+                const int64_t avail = pool_end - pool;
+                const int take = (int)(avail < (int64_t)__popc(want) ? avail : (int64_t)__popc(want));
+                const int rank = __popc(want & lt);
+                if (!alive && rank < take) {
+                    const int64_t i = pool + rank;
+                    l = r = i;
+                    cur = (int)(n - 1 + i);
+                    lo = leaf[2 * i];
+                    hi = leaf[2 * i + 1];
+                    alive = true;
+                }
+                pool += take;
+                need -= take;
+            }
+        }
+        if (!__any_sync(0xffffffffu, alive)) {
+            if (exhausted) break;
+            continue;
+        }
+        if (!alive) continue;
+        // one climbing step (k_agglo's loop body)
+        bool is_left;
+        if (l == 0) is_left = true;
+        else if (r == n - 1) is_left = false;
+        else is_left = __ldg(split + r) > __ldg(split + l - 1);
+        const int64_t p = is_left ? r : l - 1;
+        if (is_left) __stcg(reinterpret_cast<float *>(&bn[p].a) + 3, __int_as_float(cur));
+        else __stcg(reinterpret_cast<float *>(&bn[p].b) + 3, __int_as_float(cur));
+        int prev;
+        const int val = is_left ? (int)l : (int)r;
+        asm volatile("atom.exch.acq_rel.gpu.b32 %0, [%1], %2;" : "=r"(prev) : "l"(other + p), "r"(val) : "memory");
+        if (prev < 0) { alive = false; continue; }  // first arrival: the sibling finishes the node
+        const int sib = is_left ? __float_as_int(__ldcg(reinterpret_cast<const float *>(&bn[p].b) + 3))
+                                : __float_as_int(__ldcg(reinterpret_cast<const float *>(&bn[p].a) + 3)) & 0x1fffffff;
+        float4 a, b;
+        if (sib >= n - 1) { a = leaf[2 * (sib - (n - 1))]; b = leaf[2 * (sib - (n - 1)) + 1]; }
+        else { a = __ldcg(&bn[sib].a); b = __ldcg(&bn[sib].b); }
+        lo = make_float4(fminf(lo.x, a.x), fminf(lo.y, a.y), fminf(lo.z, a.z), 0.0f);
+        hi = make_float4(fmaxf(hi.x, b.x), fmaxf(hi.y, b.y), fmaxf(hi.z, b.z), 0.0f);
+        if (is_left) r = prev;
+        else l = prev;
+        const uint32_t cap = (uint32_t)(r - l + 1 < 7 ? r - l + 1 : 7);
+        const uint32_t lid = (uint32_t)(is_left ? cur : sib), rid = (uint32_t)(is_left ? sib : cur);
+        __stcg(&bn[p].a, make_float4(lo.x, lo.y, lo.z, __uint_as_float(lid | (cap << 29))));
+        __stcg(&bn[p].b, make_float4(hi.x, hi.y, hi.z, __uint_as_float(rid)));
+        cur = (int)p;
+        if (l == 0 && r == n - 1) { *root_out = cur; alive = false; }
+    }
+}
+
 // Packed records from the separate arrays of the Karras + refit and PLOC builders.
 __global__ void k_pack_bnodes(int64_t n, const int *__restrict__ left, const int *__restrict__ right,
                               const int *__restrict__ size, const float4 *__restrict__ nlo,
@@ -564,10 +643,25 @@ __device__ __forceinline__ void bin_child(const CollapseArgs &a, int id, float l
 // memory (cnt_in) and the next level's items are appended (cnt_out), so several levels are
 // launched back to back without a host round trip.
 #ifndef DPR_COLLAPSE_MINB
-#define DPR_COLLAPSE_MINB 4  // 128 registers (4 blocks / SM; 1: 164 registers, 3 blocks): r02 sweep
+#define DPR_COLLAPSE_MINB 6
 #endif
-__global__ void __launch_bounds__(128, DPR_COLLAPSE_MINB) k_collapse_r(const CollapseArgs a, const int2 *__restrict__ items,
+constexpr int CB = 128;  // collapse block
+// Per-thread child state in shared memory, [field][child][thread] (conflict-free: a warp's
+// threads read the same child slot of consecutive threads), so a child is inserted with one
+// store per field at a dynamic index instead of unrolled selects over 8 register slots (those
+// selects were most of the register version's instructions at 164 registers / 18% occupancy).
+// Kept in registers: each child's box area, capped size and internal flag (the argmax inputs).
+struct CollapseSmem {
+    int cid[8][CB];
+    uint32_t ccl[8][CB], ccr[8][CB];
+    float lo[3][8][CB], hi[3][8][CB];
+};
+
+__global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const CollapseArgs a, const int2 *__restrict__ items,
                                                     const int *__restrict__ cnt_in, int2 *next, int *cnt_out) {
+  extern __shared__ __align__(16) unsigned char collapse_smem[];
+  CollapseSmem &S = *reinterpret_cast<CollapseSmem *>(collapse_smem);
+  const int tid = threadIdx.x;
   const int nitems = *cnt_in;
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count (the allocation below is one atomic per warp and counter: with one
@@ -577,26 +671,35 @@ __global__ void __launch_bounds__(128, DPR_COLLAPSE_MINB) k_collapse_r(const Col
     const bool live = t < nitems;
     const int2 item = live ? items[t] : make_int2(0, 0);
     const int wnode = item.x, b = item.y;
-    int cid[8], c1[8];
-    uint32_t ccl[8], ccr[8];  // children ids of each child (packed records: no extra load)
-    float lo[8][3], hi[8][3];
+    float area[8];
+    int c1[8];
+    unsigned inner_m = 0;  // bit i: child i is an internal binary node
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        cid[i] = 0; c1[i] = 0; ccl[i] = ccr[i] = 0;
+    for (int i = 0; i < 8; ++i) { area[i] = 0.0f; c1[i] = 0; }
+    auto put = [&](int i, int id) -> void {  // load child id into slot i (smem + registers)
+        float lo3[3], hi3[3];
+        int sz;
+        uint32_t cl, cr;
+        bin_child(a, id, lo3, hi3, sz, cl, cr);
+        S.cid[i][tid] = id; S.ccl[i][tid] = cl; S.ccr[i][tid] = cr;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) { lo[i][c] = 0.0f; hi[i][c] = 0.0f; }
-    }
+        for (int c = 0; c < 3; ++c) { S.lo[c][i][tid] = lo3[c]; S.hi[c][i][tid] = hi3[c]; }
+        const float ex = hi3[0] - lo3[0], ey = hi3[1] - lo3[1], ez = hi3[2] - lo3[2];
+        const float ar = ex * ey + ey * ez + ez * ex;
+        const bool in = id < a.n - 1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k == i) { area[k] = ar; c1[k] = sz; }
+        inner_m = in ? (inner_m | (1u << i)) : (inner_m & ~(1u << i));
+    };
     int nc = 0;
     if (!live) {
     } else if (b < 0) {  // single-prim world: the root holds one leaf
-        cid[0] = (int)(a.n - 1);
-        bin_child(a, cid[0], lo[0], hi[0], c1[0], ccl[0], ccr[0]);
+        put(0, (int)(a.n - 1));
         nc = 1;
     } else {
-        cid[0] = (int)(__float_as_uint(__ldg(&a.bn[b].a.w)) & 0x1fffffffu);
-        cid[1] = (int)__float_as_uint(__ldg(&a.bn[b].b.w));
-        bin_child(a, cid[0], lo[0], hi[0], c1[0], ccl[0], ccr[0]);
-        bin_child(a, cid[1], lo[1], hi[1], c1[1], ccl[1], ccr[1]);
+        put(0, (int)(__float_as_uint(__ldg(&a.bn[b].a.w)) & 0x1fffffffu));
+        put(1, (int)__float_as_uint(__ldg(&a.bn[b].b.w)));
         nc = 2;
     }
     // pass 0: open the largest-area internal child with > LEAF_MAX prims; pass 1
@@ -607,71 +710,45 @@ __global__ void __launch_bounds__(128, DPR_COLLAPSE_MINB) k_collapse_r(const Col
             float ba = -1.0f;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                if (i >= nc || cid[i] >= a.n - 1 || (pass == 0 && c1[i] <= LEAF_MAX)) continue;
-                const float ex = hi[i][0] - lo[i][0], ey = hi[i][1] - lo[i][1], ez = hi[i][2] - lo[i][2];
-                const float area = ex * ey + ey * ez + ez * ex;
-                if (area > ba) { ba = area; best = i; }
+                if (i >= nc || !(inner_m >> i & 1) || (pass == 0 && c1[i] <= LEAF_MAX)) continue;
+                if (area[i] > ba) { ba = area[i]; best = i; }
             }
             if (best < 0) break;
-            int l = 0, r = 0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) if (i == best) { l = (int)ccl[i]; r = (int)ccr[i]; }
-            float llo[3], lhi[3], rlo[3], rhi[3];
-            int ls, rs;
-            uint32_t lcl, lcr, rcl, rcr;
-            bin_child(a, l, llo, lhi, ls, lcl, lcr);
-            bin_child(a, r, rlo, rhi, rs, rcl, rcr);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (i == best) {
-                    cid[i] = l; c1[i] = ls; ccl[i] = lcl; ccr[i] = lcr;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) { lo[i][k] = llo[k]; hi[i][k] = lhi[k]; }
-                }
-                if (i == nc) {
-                    cid[i] = r; c1[i] = rs; ccl[i] = rcl; ccr[i] = rcr;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) { lo[i][k] = rlo[k]; hi[i][k] = rhi[k]; }
-                }
-            }
+            const int l = (int)S.ccl[best][tid], r = (int)S.ccr[best][tid];
+            put(best, l);
+            put(nc, r);
             nc++;
         }
     }
     // node box
     float nlo_[3], nhi_[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        nlo_[c] = lo[0][c]; nhi_[c] = hi[0][c];
+    for (int c = 0; c < 3; ++c) { nlo_[c] = __int_as_float(0x7f800000); nhi_[c] = -__int_as_float(0x7f800000); }
+    for (int i = 0; i < nc; ++i)
 #pragma unroll
-        for (int i = 1; i < 8; ++i)
-            if (i < nc) { nlo_[c] = fminf(nlo_[c], lo[i][c]); nhi_[c] = fmaxf(nhi_[c], hi[i][c]); }
-    }
+        for (int c = 0; c < 3; ++c) { nlo_[c] = fminf(nlo_[c], S.lo[c][i][tid]); nhi_[c] = fmaxf(nhi_[c], S.hi[c][i][tid]); }
     // octant slot assignment: greedy on cost(child, slot) = dot(child centre - node centre,
-    // octant signs of the slot), highest first
+    // octant signs of the slot), highest first; each child's best free slot is cached and
+    // recomputed only when another child takes it (the same result as the full rescan)
     int slot_of[8];
     {
-        float dc[8][3];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            slot_of[i] = 0;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) dc[i][c] = (lo[i][c] + hi[i][c]) - (nlo_[c] + nhi_[c]);
-        }
-        // the same greedy (global maximum over unassigned children x free slots, first child
-        // then first slot on ties), with each child's best free slot cached and recomputed only
-        // when another child takes it (the full 8 x 8 rescan per assignment was a fifth of the
-        // kernel's instructions)
         float bcst[8];
         int bsl[8];
+        auto best_free = [&](int i, unsigned used, float &bc, int &bs) -> void {
+            float dc[3];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            bcst[i] = -3.4e38f; bsl[i] = 0;
+            for (int c = 0; c < 3; ++c) dc[c] = (S.lo[c][i][tid] + S.hi[c][i][tid]) - (nlo_[c] + nhi_[c]);
+            bc = -3.4e38f; bs = 0;
 #pragma unroll
             for (int sl = 0; sl < 8; ++sl) {
-                const float cst = ((sl & 4) ? dc[i][0] : -dc[i][0]) + ((sl & 2) ? dc[i][1] : -dc[i][1]) +
-                                  ((sl & 1) ? dc[i][2] : -dc[i][2]);
-                if (cst > bcst[i]) { bcst[i] = cst; bsl[i] = sl; }
+                const float cst = ((sl & 4) ? dc[0] : -dc[0]) + ((sl & 2) ? dc[1] : -dc[1]) + ((sl & 1) ? dc[2] : -dc[2]);
+                if (!(used >> sl & 1) && cst > bc) { bc = cst; bs = sl; }
             }
+        };
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            slot_of[i] = 0; bcst[i] = -3.4e38f; bsl[i] = 0;
+            if (i < nc) best_free(i, 0u, bcst[i], bsl[i]);
         }
         unsigned used_slots = 0, done_child = 0;
         for (int k = 0; k < nc; ++k) {
@@ -689,25 +766,18 @@ __global__ void __launch_bounds__(128, DPR_COLLAPSE_MINB) k_collapse_r(const Col
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 if (i >= nc || (done_child >> i & 1) || bsl[i] != bs) continue;
-                bcst[i] = -3.4e38f;
-#pragma unroll
-                for (int sl = 0; sl < 8; ++sl) {
-                    const float cst = ((sl & 4) ? dc[i][0] : -dc[i][0]) + ((sl & 2) ? dc[i][1] : -dc[i][1]) +
-                                      ((sl & 1) ? dc[i][2] : -dc[i][2]);
-                    if (!(used_slots >> sl & 1) && cst > bcst[i]) { bcst[i] = cst; bsl[i] = sl; }
-                }
+                best_free(i, used_slots, bcst[i], bsl[i]);
             }
         }
     }
     // internal vs leaf children, allocation
     int n_int = 0, n_prims = 0;
-    unsigned imask = 0, lmask = 0;
-    bool leaf[8];
+    unsigned imask = 0, lmask = 0, leaf_m = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        leaf[i] = i < nc && (cid[i] >= a.n - 1 || c1[i] <= LEAF_MAX);
         if (i >= nc) continue;
-        if (leaf[i]) { n_prims += c1[i]; lmask |= 1u << slot_of[i]; }
+        const bool lf = !(inner_m >> i & 1) || c1[i] <= LEAF_MAX;
+        if (lf) { n_prims += c1[i]; lmask |= 1u << slot_of[i]; leaf_m |= 1u << i; }
         else { n_int++; imask |= 1u << slot_of[i]; }
     }
     int child_base, prim_base, out_base;
@@ -764,25 +834,26 @@ __global__ void __launch_bounds__(128, DPR_COLLAPSE_MINB) k_collapse_r(const Col
         const int sh = 8 * (sl & 3);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const double ql = floor(((double)lo[i][c] - (double)p[c]) * isc[c]);
-            const double qh = ceil(((double)hi[i][c] - (double)p[c]) * isc[c]);
+            const double ql = floor(((double)S.lo[c][i][tid] - (double)p[c]) * isc[c]);
+            const double qh = ceil(((double)S.hi[c][i][tid] - (double)p[c]) * isc[c]);
             const uint32_t bl = (uint32_t)fmin(fmax(ql, 0.0), 255.0), bh = (uint32_t)fmin(fmax(qh, 0.0), 255.0);
             if (sl < 4) { qw[c][0] |= bl << sh; qw[3 + c][0] |= bh << sh; }
             else { qw[c][1] |= bl << sh; qw[3 + c][1] |= bh << sh; }
         }
-        if (!leaf[i]) {
+        const int cidi = S.cid[i][tid];
+        if (!(leaf_m >> i & 1)) {
             const int rank = __popc(imask & ((1u << sl) - 1u));
-            next[out_base + rank] = make_int2(child_base + rank, cid[i]);
+            next[out_base + rank] = make_int2(child_base + rank, cidi);
         } else {
             // prims of the leaf children are laid out in slot order
             int off = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-                if (j != i && leaf[j] && slot_of[j] < sl) off += c1[j];
+                if (j != i && (leaf_m >> j & 1) && slot_of[j] < sl) off += c1[j];
             const uint32_t m = 0x80u | ((uint32_t)(c1[i] - 1) << 5) | (uint32_t)off;
             if (sl < 4) mw[0] |= m << sh; else mw[1] |= m << sh;
             int st[8], sp = 0, k = 0;  // the (<= LEAF_MAX) prims of the binary subtree
-            st[sp++] = cid[i];
+            st[sp++] = cidi;
             while (sp) {
                 const int x = st[--sp];
                 if (x >= a.n - 1) a.perm[prim_base + off + k++] = (uint32_t)(x - (a.n - 1));
@@ -805,7 +876,6 @@ __global__ void __launch_bounds__(128, DPR_COLLAPSE_MINB) k_collapse_r(const Col
   }
 }
 
-
 #ifndef DPR_COLLAPSE_GRID
 #define DPR_COLLAPSE_GRID 8  // resident-grid multiple of the persistent collapse launch (r02 sweep: 1, 4, 8)
 #endif
@@ -815,32 +885,39 @@ int collapse_grid() {
         int dev = 0, nsm = 0, occ = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collapse_r, 128, 0);
+        cudaFuncSetAttribute(k_collapse_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollapseSmem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collapse_r, CB, sizeof(CollapseSmem));
         g = nsm * std::max(1, occ) * DPR_COLLAPSE_GRID;
     }
     return g;
 }
 void launch_collapse_level(const CollapseArgs &a, const int2 *items, const int *cnt_in, int2 *next, int *cnt_out,
                            cudaStream_t s) {
-    k_collapse_r<<<collapse_grid(), 128, 0, s>>>(a, items, cnt_in, next, cnt_out);
+    const int g = collapse_grid();
+    k_collapse_r<<<g, CB, sizeof(CollapseSmem), s>>>(a, items, cnt_in, next, cnt_out);
 }
 
 // prims_out[i] = prims_in[perm[i]] (3 float4 each): one thread per float4, coalesced writes.
 // The two permutations compose: wide-node order -> Morton order (perm) -> input order (sortperm).
 // inv[local id] = wide-BVH prim index (the cooperative prim tests resolve a hit by id).
+// One thread per prim: its three records' loads in flight together (the random gather), one
+// index lookup per prim, 48 contiguous bytes per thread out.
 __global__ void k_permute_prims(const float4 *__restrict__ in, const uint32_t *__restrict__ perm,
                                 const uint32_t *__restrict__ sortperm, int64_t n, float4 *out, uint32_t *inv) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= 3 * n) return;
-    int64_t i = t / 3;
-    const uint32_t src = sortperm[perm[i]];
-    out[t] = in[3 * (int64_t)src + (t - 3 * i)];
-    if (t == 3 * i) inv[src] = (uint32_t)i;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t src = __ldg(sortperm + __ldg(perm + i));
+    const float4 *q = in + 3 * (int64_t)src;
+    const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    out[3 * i] = a;
+    out[3 * i + 1] = b;
+    out[3 * i + 2] = c;
+    inv[src] = (uint32_t)i;
 }
 
 void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t *sortperm, int64_t n,
                           float4 *out, uint32_t *inv, cudaStream_t s) {
-    if (n > 0) k_permute_prims<<<nblk(3 * n, 256), 256, 0, s>>>(in, perm, sortperm, n, out, inv);
+    if (n > 0) k_permute_prims<<<nblk(n, 256), 256, 0, s>>>(in, perm, sortperm, n, out, inv);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -974,11 +1051,29 @@ void launch_refit(int64_t n, const int *left, const int *right, const int *paren
 #ifndef DPR_AGGLO_SPLIT
 #define DPR_AGGLO_SPLIT 1
 #endif
+#ifndef DPR_AGGLO_PERSIST
+#define DPR_AGGLO_PERSIST 1
+#endif
 int launch_agglo(const mkey_t *keys, uint8_t *split_scratch, int64_t n, const float4 *leaf, BNode *bn,
                  int *other, int *root_out, cudaStream_t s) {
     if (n <= 1) return 0;
     uint8_t *split = DPR_AGGLO_SPLIT ? split_scratch : nullptr;
     if (split) k_split_delta<<<nblk(n, 256), 256, 0, s>>>(keys, n, split);
+    if (DPR_AGGLO_PERSIST && split) {
+        // fetch counter: the 8 bytes after the split bytes (the scratch holds 4n bytes)
+        unsigned long long *fetch = reinterpret_cast<unsigned long long *>(split + ((n + 15) & ~(int64_t)7));
+        cudaMemsetAsync(fetch, 0, sizeof(unsigned long long), s);
+        static int grid = 0;
+        if (!grid) {
+            int dev = 0, nsm = 0, occ = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_agglo_p, 256, 0);
+            grid = nsm * std::max(1, occ);
+        }
+        k_agglo_p<<<grid, 256, 0, s>>>(split, n, leaf, bn, other, root_out, fetch);
+        return 3;
+    }
     k_agglo<<<nblk(n, 256), 256, 0, s>>>(keys, split, n, leaf, bn, other, root_out);
     return split ? 2 : 1;
 }

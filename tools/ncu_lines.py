@@ -7,8 +7,11 @@ from collections import defaultdict
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
-                      "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):  # exported on the GPU box by tools/ncu_capture.sh (one kernel)
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
+                          "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 inst = defaultdict(float)
 stall = defaultdict(float)
 text = {}

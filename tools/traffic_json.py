@@ -9,7 +9,10 @@ import sys
 
 rep, tag, cfg = sys.argv[1], sys.argv[2], sys.argv[3]
 summary = sys.argv[4] if len(sys.argv) > 4 else f"profiles/{tag}_ncu_{cfg}.txt"
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):  # `ncu -i REP --page raw --csv` output written on the GPU box
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units = rows[0], rows[1]
 mult = {'Gbyte': 1e9, 'Mbyte': 1e6, 'Kbyte': 1e3, 'byte': 1}
