@@ -509,6 +509,7 @@ __global__ void __launch_bounds__(256) k_agglo_p(const uint8_t *__restrict__ spl
     const unsigned lt = (1u << lane) - 1u;
     bool alive = false, exhausted = false;
     int64_t l = 0, r = 0, pool = 0, pool_end = 0;
+    int64_t chunk = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 64;
     int cur = 0;
     float4 lo = make_float4(0, 0, 0, 0), hi = lo;
     for (;;) {
@@ -518,12 +519,13 @@ __global__ void __launch_bounds__(256) k_agglo_p(const uint8_t *__restrict__ spl
             int need = __popc(dead);
             while (need > 0 && !exhausted) {
                 if (pool >= pool_end) {
-                    unsigned long long b = 0;
-                    if (lane == 0) b = atomicAdd(fetch, 64ull);
-                    b = __shfl_sync(0xffffffffu, b, 0);
-                    if ((int64_t)b >= n) { exhausted = true; break; }
-                    pool = (int64_t)b;
-                    pool_end = (int64_t)b + 64 < n ? (int64_t)b + 64 : n;
+                    // the warp's next chunk of 64 leaves, interleaved over all warps (no shared
+                    // counter: one fetch atomic per chunk was a third of the stalls)
+                    const int64_t b = chunk;
+                    chunk += (int64_t)gridDim.x * (blockDim.x >> 5) * 64;
+                    if (b >= n) { exhausted = true; break; }
+                    pool = b;
+                    pool_end = b + 64 < n ? b + 64 : n;
                 }
                 const unsigned want = __ballot_sync(0xffffffffu, !alive);
                 const int64_t avail = pool_end - pool;
@@ -729,7 +731,7 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
         for (int c = 0; c < 3; ++c) { nlo_[c] = fminf(nlo_[c], S.lo[c][i][tid]); nhi_[c] = fmaxf(nhi_[c], S.hi[c][i][tid]); }
     // octant slot assignment: greedy on cost(child, slot) = dot(child centre - node centre,
     // octant signs of the slot), highest first; each child's best free slot is cached and
-    // recomputed only when another child takes it (the same result as the full rescan)
+    // recomputed only when another child takes it
     int slot_of[8];
     {
         float bcst[8];
@@ -745,10 +747,19 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
                 if (!(used >> sl & 1) && cst > bc) { bc = cst; bs = sl; }
             }
         };
+        // with every slot free, a child's best slot is the octant of its offset and its cost
+        // |dx| + |dy| + |dz| (rounding is monotone; exact ties may pick another octant than
+        // the full scan's lowest index: a different, equally valid slot order)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             slot_of[i] = 0; bcst[i] = -3.4e38f; bsl[i] = 0;
-            if (i < nc) best_free(i, 0u, bcst[i], bsl[i]);
+            if (i < nc) {
+                float dc[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) dc[c] = (S.lo[c][i][tid] + S.hi[c][i][tid]) - (nlo_[c] + nhi_[c]);
+                bcst[i] = (fabsf(dc[0]) + fabsf(dc[1])) + fabsf(dc[2]);
+                bsl[i] = (dc[0] > 0.0f ? 4 : 0) | (dc[1] > 0.0f ? 2 : 0) | (dc[2] > 0.0f ? 1 : 0);
+            }
         }
         unsigned used_slots = 0, done_child = 0;
         for (int k = 0; k < nc; ++k) {

@@ -7,6 +7,9 @@
 TAG=$1; CFG=$2; KRE=$3; SKIP=$4; COUNT=$5; SRCK=$6; shift 6
 CMD=${@:-python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e}
 mkdir -p gpurun_out
+# kernel nodes of CUDA graphs with conditional nodes cannot be profiled: the step loop runs on
+# the host here (the same kernels as the device-driven loop, ordinary launches)
+export DPR_STEP_LOOP=host
 $CMD > gpurun_out/plain_${CFG}.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --set full --clock-control none --import-source on -k "$KRE" -s $SKIP -c $COUNT -o /tmp/${TAG}_${CFG} $CMD > gpurun_out/ncu_${CFG}.log 2>&1
 echo "ncu rc=$?"

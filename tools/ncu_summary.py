@@ -1,9 +1,13 @@
-"""Print the key metrics + top stall reasons of every kernel in an ncu report."""
+"""Print the key metrics + top stall reasons of every kernel in an ncu report (or its raw-page
+CSV export)."""
 import csv
 import subprocess
 import sys
 
-raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if sys.argv[1].endswith(".csv"):  # raw page exported on the GPU box (tools/ncu_capture.sh)
+    raw = open(sys.argv[1]).read()
+else:
+    raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units = rows[0], rows[1]
 keys = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'lts__t_sector_hit_rate.pct',

@@ -11,7 +11,9 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
 timeout 900 python bench.py --config $CFG --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_${CFG}.json 2> gpurun_out/${TAG}_bench_${CFG}.err
 echo "bench rc=$?"; cat gpurun_out/${TAG}_bench_${CFG}.json
-CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+# ncu cannot profile kernel nodes of graphs with conditional nodes: profile the host step loop
+# (the same kernels, ordinary launches)
+CMD="env DPR_STEP_LOOP=host python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 $CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/${TAG}_launches_${CFG}.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "launches rc=$?"
