@@ -37,7 +37,8 @@ void launch_refit(int64_t n, const int *left, const int *right, const int *paren
                   const float4 *slo, const float4 *shi, float4 *nlo, float4 *nhi, int *arrive,
                   cudaStream_t s);
 // Binary node record (32 B, one sector): a = (lo.xyz, left id | min(size, 7) << 29),
-// b = (hi.xyz, right id); ids: internal k in [0, n-1), leaf j -> n-1+j.
+// b = (hi.xyz, right id | off << 29), off = p - (first sorted leaf) for nodes of <= 7 leaves
+// of the agglomerative tree, else 7; ids: internal k in [0, n-1), leaf j -> n-1+j.
 struct BNode { float4 a, b; };
 // split_scratch: >= n-1 bytes (the unused radix-sort key buffer); leaf: packed leaf boxes
 // (leaf[2j] = lo, leaf[2j+1] = hi); returns kernels launched

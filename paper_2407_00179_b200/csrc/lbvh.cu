@@ -450,14 +450,20 @@ __global__ void k_refit(int64_t n, const int *__restrict__ left, const int *__re
 // (acq_rel exchange) merges both boxes and continues.  The root is reported in *root_out.
 // split[i] = delta(i, i+1) (common-prefix length of adjacent sorted keys, index-augmented),
 // one byte per split: k_agglo reads two bytes per step instead of four 64-bit keys
+__device__ __forceinline__ uint32_t range_off(int64_t p, int64_t l, int64_t r) {
+    return r - l + 1 <= 7 ? (uint32_t)(p - l) : 7u;
+}
 __global__ void k_split_delta(const mkey_t *__restrict__ keys, int64_t n, uint8_t *split) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n - 1) split[i] = (uint8_t)delta(keys, n, i, i + 1);
 }
 
 // Binary node records (BNode, kernels.h): a = (lo.xyz, left | min(size, 7) << 29), b = (hi.xyz,
-// right) -- one 32-byte sector per node for the collapse and the sibling reads here.  Leaf boxes
-// are packed the same way (leaf[2j] = lo, leaf[2j+1] = hi).
+// right | off << 29) -- one 32-byte sector per node for the collapse and the sibling reads here.
+// Leaf boxes are packed the same way (leaf[2j] = lo, leaf[2j+1] = hi).
+// off: a node p of this tree covers the sorted leaves [l, r] with p in [l, r); for nodes of at
+// most 7 leaves off = p - l (< 6), so the collapse lists a small subtree's prims as l.. l+size-1
+// without walking it; 7 = not recorded (larger nodes; the Karras and PLOC records).
 __global__ void k_agglo(const mkey_t *__restrict__ keys, const uint8_t *__restrict__ split, int64_t n,
                         const float4 *__restrict__ leaf, BNode *bn, int *other, int *root_out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -491,7 +497,7 @@ __global__ void k_agglo(const mkey_t *__restrict__ keys, const uint8_t *__restri
         const uint32_t cap = (uint32_t)(r - l + 1 < 7 ? r - l + 1 : 7);
         const uint32_t lid = (uint32_t)(is_left ? cur : sib), rid = (uint32_t)(is_left ? sib : cur);
         __stcg(&bn[p].a, make_float4(lo.x, lo.y, lo.z, __uint_as_float(lid | (cap << 29))));
-        __stcg(&bn[p].b, make_float4(hi.x, hi.y, hi.z, __uint_as_float(rid)));
+        __stcg(&bn[p].b, make_float4(hi.x, hi.y, hi.z, __uint_as_float(rid | (range_off(p, l, r) << 29))));
         cur = (int)p;
         if (l == 0 && r == n - 1) { *root_out = cur; return; }
     }
@@ -501,10 +507,10 @@ __global__ void k_agglo(const mkey_t *__restrict__ keys, const uint8_t *__restri
 // climb ends (first arrival at a node) starts the next leaf of its warp's pool at once, so the
 // warp's lanes stay busy (one thread per leaf retires half its warp after the first step and
 // ran at 6.4/32 active lanes).  Any order of leaf starts builds the same tree: a node is
-// finished by whichever child arrives second.  fetch: leaf counter (zeroed by the launcher).
+// finished by whichever child arrives second.
 __global__ void __launch_bounds__(256) k_agglo_p(const uint8_t *__restrict__ split, int64_t n,
                                                  const float4 *__restrict__ leaf, BNode *bn, int *other,
-                                                 int *root_out, unsigned long long *fetch) {
+                                                 int *root_out) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     bool alive = false, exhausted = false;
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(256) k_agglo_p(const uint8_t *__restrict__ spl
         const uint32_t cap = (uint32_t)(r - l + 1 < 7 ? r - l + 1 : 7);
         const uint32_t lid = (uint32_t)(is_left ? cur : sib), rid = (uint32_t)(is_left ? sib : cur);
         __stcg(&bn[p].a, make_float4(lo.x, lo.y, lo.z, __uint_as_float(lid | (cap << 29))));
-        __stcg(&bn[p].b, make_float4(hi.x, hi.y, hi.z, __uint_as_float(rid)));
+        __stcg(&bn[p].b, make_float4(hi.x, hi.y, hi.z, __uint_as_float(rid | (range_off(p, l, r) << 29))));
         cur = (int)p;
         if (l == 0 && r == n - 1) { *root_out = cur; alive = false; }
     }
@@ -587,7 +593,7 @@ __global__ void k_pack_bnodes(int64_t n, const int *__restrict__ left, const int
     const float4 lo = nlo[p], hi = nhi[p];
     const uint32_t cap = (uint32_t)min(size[p], 7);
     bn[p].a = make_float4(lo.x, lo.y, lo.z, __uint_as_float((uint32_t)left[p] | (cap << 29)));
-    bn[p].b = make_float4(hi.x, hi.y, hi.z, __uint_as_float((uint32_t)right[p]));
+    bn[p].b = make_float4(hi.x, hi.y, hi.z, __uint_as_float((uint32_t)right[p] | (7u << 29)));
 }
 
 // Outward padding: |x| + 4 scaled by 2^-18 (>= 1.5e-5 absolute).  Covers the FMA box test
@@ -701,7 +707,7 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
         nc = 1;
     } else {
         put(0, (int)(__float_as_uint(__ldg(&a.bn[b].a.w)) & 0x1fffffffu));
-        put(1, (int)__float_as_uint(__ldg(&a.bn[b].b.w)));
+        put(1, (int)(__float_as_uint(__ldg(&a.bn[b].b.w)) & 0x1fffffffu));
         nc = 2;
     }
     // pass 0: open the largest-area internal child with > LEAF_MAX prims; pass 1
@@ -716,7 +722,7 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
                 if (area[i] > ba) { ba = area[i]; best = i; }
             }
             if (best < 0) break;
-            const int l = (int)S.ccl[best][tid], r = (int)S.ccr[best][tid];
+            const int l = (int)S.ccl[best][tid], r = (int)(S.ccr[best][tid] & 0x1fffffffu);
             put(best, l);
             put(nc, r);
             nc++;
@@ -863,14 +869,24 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
                 if (j != i && (leaf_m >> j & 1) && slot_of[j] < sl) off += c1[j];
             const uint32_t m = 0x80u | ((uint32_t)(c1[i] - 1) << 5) | (uint32_t)off;
             if (sl < 4) mw[0] |= m << sh; else mw[1] |= m << sh;
-            int st[8], sp = 0, k = 0;  // the (<= LEAF_MAX) prims of the binary subtree
-            st[sp++] = cidi;
-            while (sp) {
-                const int x = st[--sp];
-                if (x >= a.n - 1) a.perm[prim_base + off + k++] = (uint32_t)(x - (a.n - 1));
-                else {
-                    st[sp++] = (int)__float_as_uint(__ldg(&a.bn[x].b.w));
-                    st[sp++] = (int)(__float_as_uint(__ldg(&a.bn[x].a.w)) & 0x1fffffffu);
+            // the (<= LEAF_MAX) prims of the binary subtree, in sorted order: a contiguous
+            // range when the record holds its offset, else a walk of the subtree
+            const uint32_t roff = S.ccr[i][tid] >> 29;
+            if (cidi >= a.n - 1) {
+                a.perm[prim_base + off] = (uint32_t)(cidi - (a.n - 1));
+            } else if (roff != 7u) {
+                const uint32_t l0 = (uint32_t)cidi - roff;
+                for (int k = 0; k < c1[i]; ++k) a.perm[prim_base + off + k] = l0 + (uint32_t)k;
+            } else {
+                int st[8], sp = 0, k = 0;
+                st[sp++] = cidi;
+                while (sp) {
+                    const int x = st[--sp];
+                    if (x >= a.n - 1) a.perm[prim_base + off + k++] = (uint32_t)(x - (a.n - 1));
+                    else {
+                        st[sp++] = (int)(__float_as_uint(__ldg(&a.bn[x].b.w)) & 0x1fffffffu);
+                        st[sp++] = (int)(__float_as_uint(__ldg(&a.bn[x].a.w)) & 0x1fffffffu);
+                    }
                 }
             }
         }
@@ -1071,9 +1087,6 @@ int launch_agglo(const mkey_t *keys, uint8_t *split_scratch, int64_t n, const fl
     uint8_t *split = DPR_AGGLO_SPLIT ? split_scratch : nullptr;
     if (split) k_split_delta<<<nblk(n, 256), 256, 0, s>>>(keys, n, split);
     if (DPR_AGGLO_PERSIST && split) {
-        // fetch counter: the 8 bytes after the split bytes (the scratch holds 4n bytes)
-        unsigned long long *fetch = reinterpret_cast<unsigned long long *>(split + ((n + 15) & ~(int64_t)7));
-        cudaMemsetAsync(fetch, 0, sizeof(unsigned long long), s);
         static int grid = 0;
         if (!grid) {
             int dev = 0, nsm = 0, occ = 0;
@@ -1082,8 +1095,10 @@ int launch_agglo(const mkey_t *keys, uint8_t *split_scratch, int64_t n, const fl
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_agglo_p, 256, 0);
             grid = nsm * std::max(1, occ);
         }
-        k_agglo_p<<<grid, 256, 0, s>>>(split, n, leaf, bn, other, root_out, fetch);
-        return 3;
+        // a resident grid, or one 64-leaf chunk per warp when the tree is small
+        const int64_t need = (n + 8 * 64 - 1) / (8 * 64);
+        k_agglo_p<<<(int)std::min<int64_t>(grid, need), 256, 0, s>>>(split, n, leaf, bn, other, root_out);
+        return 2;
     }
     k_agglo<<<nblk(n, 256), 256, 0, s>>>(keys, split, n, leaf, bn, other, root_out);
     return split ? 2 : 1;
