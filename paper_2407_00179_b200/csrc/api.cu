@@ -132,7 +132,7 @@ struct Dev {
     bool nonempty = false;
     Buf b_prims_u, b_blo, b_bhi, b_keys[2], b_vals[2], b_tile, b_left, b_right, b_parent, b_rlo,
         b_rhi, b_nlo, b_nhi, b_arrive, b_prims, b_slo, b_shi, b_bounds, b_hist, b_wnodes, b_chunks,
-        b_prims_w, b_inv, b_items[2], b_wcnt, b_wperm, b_witems[2], b_size, b_bn;
+        b_prims_w, b_items[2], b_wcnt, b_wperm, b_witems[2], b_size, b_bn;
     int builder = 1;  // 0 PLOC, 1 agglomerative LBVH (default), 2 Karras + refit (env DPR_BUILDER=ploc|karras)
     int build_iters = 0;
     int64_t wnodes_count = 0;
@@ -650,9 +650,7 @@ int build_world(Dev *d) {
                 if (h_cnt[4 + k] == 0) { levels = k; break; }
         }
         if (h_cnt[2] != n) return fail(DPR_ERR_STATE, "wide BVH collapse lost primitives");
-        RET(ensure(d, d->b_inv, sizeof(uint32_t) * n));
-        launch_permute_prims(P<float4>(d->b_prims_u), P<uint32_t>(d->b_wperm), perm, n, P<float4>(d->b_prims_w),
-                             P<uint32_t>(d->b_inv), s);
+        launch_permute_prims(P<float4>(d->b_prims_u), P<uint32_t>(d->b_wperm), perm, n, P<float4>(d->b_prims_w), s);
         launches++;
         d->wnodes_count = h_cnt[1];
         d->bvh_levels = levels;
@@ -915,7 +913,7 @@ StepArgs make_args(Dev *d, const FrameCtx &fc, int cur) {
     a.W.wnodes = P<WNode>(d->b_wnodes);
     a.W.prmt_hi = 0x4b00u;
     a.W.prims = P<float4>(d->b_prims_w);
-    a.W.inv = P<uint32_t>(d->b_inv);
+    a.W.prims_in = P<float4>(d->b_prims_u);
     a.W.nnodes = d->wnodes_count;
     a.W.nprims = d->nprims;
     a.W.id_base = fc.id_base[d->rank];
@@ -1955,7 +1953,7 @@ void release_bufs(Dev *d) {
     Buf *bs[] = {&d->b_prims_u, &d->b_blo, &d->b_bhi, &d->b_keys[0], &d->b_keys[1], &d->b_vals[0],
                  &d->b_vals[1], &d->b_tile, &d->b_left, &d->b_right, &d->b_parent, &d->b_rlo, &d->b_rhi,
                  &d->b_nlo, &d->b_nhi, &d->b_arrive, &d->b_prims, &d->b_slo, &d->b_shi,
-                 &d->b_bounds, &d->b_chunks, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_inv, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_witems[0], &d->b_witems[1], &d->b_size, &d->b_bn, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
+                 &d->b_bounds, &d->b_chunks, &d->b_hist, &d->b_wnodes, &d->b_prims_w, &d->b_items[0], &d->b_items[1], &d->b_wcnt, &d->b_wperm, &d->b_witems[0], &d->b_witems[1], &d->b_size, &d->b_bn, &d->b_fb, &d->b_fb_out, &d->b_events, &d->b_occl, &d->b_ctr,
                  &d->b_counts, &d->b_in_count, &d->b_fetch, &d->b_part_lo, &d->b_part_alb, &d->b_scratch,
                  &d->b_path[0], &d->b_path[1], &d->b_occlq[0], &d->b_occlq[1]};
     for (Buf *b : bs) dfree(d, *b);
@@ -1999,7 +1997,7 @@ Dev *local_view(Dev *d, bool replicated = false) {
     v->parts = d->parts;  // non-owning copies (detached before release)
     v->wbricks = d->wbricks; v->amax_local = d->amax_local;
     v->world_ready = d->world_ready; v->nprims = d->nprims; memcpy(v->box, d->box, sizeof(v->box));
-    v->nonempty = d->nonempty; v->b_wnodes = d->b_wnodes; v->b_prims_w = d->b_prims_w; v->b_inv = d->b_inv;
+    v->nonempty = d->nonempty; v->b_wnodes = d->b_wnodes; v->b_prims_w = d->b_prims_w; v->b_prims_u = d->b_prims_u;
     v->local_parts = d->local_parts; v->wnodes_count = d->wnodes_count; v->bvh_levels = d->bvh_levels;
     v->build_launches = 0;
     v->cam = d->cam; v->cam_set = d->cam_set;
@@ -2106,7 +2104,7 @@ void release_local_view(Dev *d) {
     v->parts.clear();
     v->b_wnodes = Buf();
     v->b_prims_w = Buf();
-    v->b_inv = Buf();
+    v->b_prims_u = Buf();
     release_bufs(v);
     delete v;
     d->lv = nullptr;

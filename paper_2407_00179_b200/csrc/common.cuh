@@ -301,7 +301,8 @@ struct WorldDev {
                        // ptxas keeps the PRMT selector as the immediate operand
     const WNode *wnodes;
     const float4 *prims;
-    const uint32_t *inv;    // local id -> prim index (cooperative prim tests)
+    const float4 *prims_in;  // the same records in input order (index = local id): the normal of a
+                             // hit found by the cooperative tests, which report (t, id)
     int64_t nprims;
     int64_t nnodes;         // wide nodes (bounds checks of DPR_CHECKS builds)
     uint32_t id_base;       // global id of local prim 0 (P12)

@@ -64,7 +64,7 @@ struct CollapseArgs {
 void launch_collapse_level(const CollapseArgs &a, const int2 *items, const int *cnt_in, int2 *next, int *cnt_out,
                            cudaStream_t s);
 void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t *sortperm, int64_t n,
-                          float4 *out, uint32_t *inv, cudaStream_t s);
+                          float4 *out, cudaStream_t s);
 // ---- ploc.cu: PLOC binary builder (Meister & Bittner 2018) ------------------------------
 struct PlocArgs {
     int64_t n;

@@ -924,13 +924,14 @@ void launch_collapse_level(const CollapseArgs &a, const int2 *items, const int *
     k_collapse_r<<<g, CB, sizeof(CollapseSmem), s>>>(a, items, cnt_in, next, cnt_out);
 }
 
-// prims_out[i] = prims_in[perm[i]] (3 float4 each): one thread per float4, coalesced writes.
-// The two permutations compose: wide-node order -> Morton order (perm) -> input order (sortperm).
-// inv[local id] = wide-BVH prim index (the cooperative prim tests resolve a hit by id).
-// One thread per prim: its three records' loads in flight together (the random gather), one
-// index lookup per prim, 48 contiguous bytes per thread out.
+// prims_out[i] = prims_in[perm[i]] (3 float4 each).  The two permutations compose: wide-node
+// order -> Morton order (perm) -> input order (sortperm).  One thread per prim: its three
+// records' loads in flight together (the random gather), 48 contiguous bytes per thread out.
+// (An inverse table local id -> prim index was scattered here until r02; the cooperative prim
+// tests now record the winning prim index themselves -- the random 4-byte scatter cost a
+// 64-byte DRAM read-modify-write per prim.)
 __global__ void k_permute_prims(const float4 *__restrict__ in, const uint32_t *__restrict__ perm,
-                                const uint32_t *__restrict__ sortperm, int64_t n, float4 *out, uint32_t *inv) {
+                                const uint32_t *__restrict__ sortperm, int64_t n, float4 *out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t src = __ldg(sortperm + __ldg(perm + i));
@@ -939,12 +940,11 @@ __global__ void k_permute_prims(const float4 *__restrict__ in, const uint32_t *_
     out[3 * i] = a;
     out[3 * i + 1] = b;
     out[3 * i + 2] = c;
-    inv[src] = (uint32_t)i;
 }
 
 void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t *sortperm, int64_t n,
-                          float4 *out, uint32_t *inv, cudaStream_t s) {
-    if (n > 0) k_permute_prims<<<nblk(n, 256), 256, 0, s>>>(in, perm, sortperm, n, out, inv);
+                          float4 *out, cudaStream_t s) {
+    if (n > 0) k_permute_prims<<<nblk(n, 256), 256, 0, s>>>(in, perm, sortperm, n, out);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -232,7 +232,7 @@ struct CoopSmem {
     uint8_t ow[32 * COOP_PER_LANE];
     unsigned long long best[32];
 };
-constexpr int PRIM_BY_ID = 0x7fffffff;  // Hit.prim: a local hit, prim index = W.inv[local id]
+constexpr int PRIM_BY_ID = 0x7fffffff;  // Hit.prim: a local hit found by id (record W.prims_in[local id])
 
 
 // Traversal state of one ray over the compressed 8-wide BVH.  A "node group" is the set of
@@ -615,8 +615,8 @@ __device__ __forceinline__ bool trav_step(const WorldDev &W, TravState &S, uint2
     return trav_done(S);
 }
 
-__device__ __forceinline__ f3 prim_normal(const WorldDev &W, int k, f3 o, f3 d, float t) {
-    const float4 *pr = W.prims + 3 * (int64_t)k;
+__device__ __forceinline__ f3 prim_normal(const float4 *prims, int64_t k, f3 o, f3 d, float t) {
+    const float4 *pr = prims + 3 * k;
     float4 a = __ldg(pr), b = __ldg(pr + 1);
     if (__float_as_uint(a.w) & SPHERE_BIT) return sphere_normal(o, d, t, xyz(a), b.x);
     float4 e = __ldg(pr + 2);
@@ -1255,8 +1255,9 @@ __device__ __forceinline__ void trace_loop(const StepArgs &A) {
             bool changed = S.h.prim >= 0;
             f3 nrm = mk(0, 0, 0);
             if (changed) {
-                const int k = S.h.prim == PRIM_BY_ID ? (int)__ldg(A.W.inv + (S.h.id - A.W.id_base)) : S.h.prim;
-                nrm = prim_normal(A.W, k, RAY_O(S), RAY_D(S), S.h.t);
+                const bool by_id = S.h.prim == PRIM_BY_ID;
+                nrm = prim_normal(by_id ? A.W.prims_in : A.W.prims, by_id ? (int64_t)(S.h.id - A.W.id_base) : S.h.prim,
+                                  RAY_O(S), RAY_D(S), S.h.t);
             }
             if (A.W.nbricks > 0 && (F.flags & DPR_FLAG_DELTA)) {
                 const uint32_t p = __float_as_uint(r->c.w), meta = __float_as_uint(r->e.w);
