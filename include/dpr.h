@@ -331,6 +331,14 @@ DPR_API const char *dpr_last_error(dpr_device dev);
  * skewed arrival; *mismatches = boundaries whose gathered sums were wrong (0 expected). */
 DPR_API int dpr_test_step_barrier(int cuda_device, int nranks, int iters, int64_t *mismatches);
 
+/* LOCAL test of the LBVH builder's key sort (north star subsystem (1): "Morton codes, radix
+ * sort"): the library's LSD radix passes (all four 8-bit digits, the default scatter kernel)
+ * over n 32-bit keys.  keys, perm_out: DEVICE pointers on cuda_device (n elements each; the keys
+ * are not modified).  perm_out[i] = index of the i-th key in ascending order, equal keys in
+ * input order (stable), i.e. the order the build's Morton sort produces.  n >= 0; n > 2^30 or
+ * NULL pointers with n > 0 -> DPR_ERR_INVALID_ARG.  Synchronous. */
+DPR_API int dpr_test_radix_sort(int cuda_device, const uint32_t *keys, int64_t n, uint32_t *perm_out);
+
 /* ---- host-side exchange planning (pure function; used by the render loop) ------------ */
 
 /* Given the gathered per-destination counts of one ray kind, counts[src*nranks + dst]

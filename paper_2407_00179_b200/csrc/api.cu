@@ -2324,6 +2324,37 @@ int dpr_test_step_barrier(int cuda_device, int nranks, int iters, int64_t *misma
     return DPR_OK;
 }
 
+int dpr_test_radix_sort(int cuda_device, const uint32_t *keys, int64_t n, uint32_t *perm_out) {
+    if (n < 0 || n > ((int64_t)1 << 30) || (n > 0 && (!keys || !perm_out)))
+        return fail(DPR_ERR_INVALID_ARG, "bad arguments");
+    if (n == 0) return DPR_OK;
+    static_assert(sizeof(mkey_t) == sizeof(uint32_t), "32-bit Morton keys");
+    CK(cudaSetDevice(cuda_device));
+    const int64_t ntiles = radix_tiles(n);
+    char *buf = nullptr;
+    const size_t kv = sizeof(uint32_t) * (size_t)n;
+    CK(cudaMalloc(&buf, 4 * kv + sizeof(uint32_t) * 256 * (ntiles + 1)));
+    mkey_t *k[2] = {(mkey_t *)buf, (mkey_t *)(buf + kv)};
+    uint32_t *v[2] = {(uint32_t *)(buf + 2 * kv), (uint32_t *)(buf + 3 * kv)};
+    uint32_t *tile = (uint32_t *)(buf + 4 * kv);
+    cudaError_t e = cudaMemcpy(k[0], keys, kv, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) {
+        launch_iota(v[0], n, 0);
+        e = cudaGetLastError();
+    }
+    int launches = 0, cur = 0;
+    for (int pass = 0; pass < MKEY_DIGITS && e == cudaSuccess; ++pass) {
+        launch_radix_pass(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, 8 * pass, tile, 0, &launches);
+        cur ^= 1;
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(perm_out, v[cur], kv, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(buf);
+    if (e != cudaSuccess) return fail(DPR_ERR_CUDA, std::string("radix sort test: ") + cudaGetErrorString(e));
+    return DPR_OK;
+}
+
 int dpr_create_loopback_group(int nranks, int cuda_device, void *cuda_stream, const dpr_allocator *alloc,
                               dpr_device *out) {
     if (!out || nranks < 1 || nranks > DPR_MAX_RANKS) return fail(DPR_ERR_INVALID_ARG, "bad nranks/out");

@@ -29,6 +29,7 @@ void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *b
 void launch_digit_hist_all(const mkey_t *keys, int64_t n, unsigned long long *hist, int nsm,
                            cudaStream_t s);
 int64_t radix_tiles(int64_t n);
+void launch_iota(uint32_t *v, int64_t n, cudaStream_t s);  // v[i] = i (the sort test's values)
 void launch_radix_pass(const mkey_t *kin, const uint32_t *vin, mkey_t *kout, uint32_t *vout,
                        int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches);
 void launch_karras(const mkey_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,

@@ -172,7 +172,10 @@ __global__ void k_morton(const float4 *__restrict__ blo, const float4 *__restric
 // LSD radix sort, 8-bit digits.
 // ---------------------------------------------------------------------------------------
 constexpr int RS_THREADS = 256;
-constexpr int RS_ITEMS = 16;
+#ifndef DPR_RS_ITEMS
+#define DPR_RS_ITEMS 8  // r02 sweep (warp-ranked scatter, configs[3] build): 4 14.28, 6 13.76, 8 13.57, 10 13.63, 12 13.84, 16 13.72 ms
+#endif
+constexpr int RS_ITEMS = DPR_RS_ITEMS;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 
 // All 8 digit histograms in one read of the keys (to find constant-digit passes).
@@ -363,6 +366,107 @@ k_scatter_c(const mkey_t *__restrict__ kin, const uint32_t *__restrict__ vin, mk
         const uint32_t pos = goff[d] + (uint32_t)(i - (int)lstart[d]);
         kout[pos] = k;
         vout[pos] = vin[gi];
+    }
+}
+
+// Warp-ranked variant (default): each warp owns a contiguous 512-key slice of the tile and
+// loads its 16 keys and values per lane up front (coalesced, 32 loads in flight per thread);
+// keys are ranked within the warp by match_any against per-warp digit counters (no block
+// barrier per round), one per-digit prefix over the 8 warps orders the warps' runs, and the
+// tile is staged in digit order in shared memory and written out bucket run by bucket run (no
+// global gather).  Item order inside a digit is the input order (warp slices in order, inside a
+// slice key it*32 + lane): stable, the same permutation as k_scatter_c.
+__global__ void __launch_bounds__(RS_THREADS)
+k_scatter_w(const mkey_t *__restrict__ kin, const uint32_t *__restrict__ vin, mkey_t *kout,
+            uint32_t *vout, int64_t n, int shift, const uint32_t *__restrict__ tile_off, int ntiles,
+            const uint32_t *__restrict__ digit_tot) {
+    constexpr int NW = RS_THREADS / 32, PER_WARP = RS_TILE / NW, IT = PER_WARP / 32;
+    __shared__ uint32_t wcnt[NW][256];
+    __shared__ uint32_t goff[256], lstart[256];
+    __shared__ mkey_t skey[RS_TILE];
+    __shared__ uint32_t sval[RS_TILE];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    const int64_t wbase = base + (int64_t)warp * PER_WARP;
+    mkey_t key[IT];
+    uint32_t val[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+        const int64_t i = wbase + it * 32 + lane;
+        key[it] = i < n ? __ldg(kin + i) : 0;
+        val[it] = i < n ? __ldg(vin + i) : 0;
+    }
+#pragma unroll
+    for (int w = 0; w < NW; ++w) wcnt[w][threadIdx.x] = 0;
+    {  // global exclusive offset of each digit for this tile, and the tile's local digit starts
+        const uint32_t v = digit_tot[threadIdx.x];
+        const uint32_t mine = tile_off[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+        const uint32_t cnt = (blockIdx.x + 1 < (unsigned)ntiles ? tile_off[(int64_t)threadIdx.x * ntiles + blockIdx.x + 1] : v) - mine;
+        uint32_t x = v, y = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t xs = __shfl_up_sync(0xffffffffu, x, o), ys = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) { x += xs; y += ys; }
+        }
+        __shared__ uint32_t wsum[2][NW];
+        if (lane == 31) { wsum[0][warp] = x; wsum[1][warp] = y; }
+        __syncthreads();
+        uint32_t wp = 0, wl = 0;
+        for (int w = 0; w < warp; ++w) { wp += wsum[0][w]; wl += wsum[1][w]; }
+        goff[threadIdx.x] = wp + x - v + mine;
+        lstart[threadIdx.x] = wl + y - cnt;
+    }
+    // rank inside the warp (wcnt[warp][*] is private to this warp: __syncwarp ordering only);
+    // the IT match_any instructions are independent and issued first (their latency overlaps)
+    uint32_t lrank[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+        const bool valid = wbase + it * 32 + lane < n;
+        lrank[it] = __match_any_sync(0xffffffffu, valid ? (int)((key[it] >> shift) & 255) : 256 + lane);
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+        const bool valid = wbase + it * 32 + lane < n;
+        const int d = valid ? (int)((key[it] >> shift) & 255) : 256 + lane;
+        const unsigned peers = lrank[it];
+        const int leader = __ffs(peers) - 1;
+        uint32_t before = 0;
+        if (valid && lane == leader) {
+            before = wcnt[warp][d];
+            wcnt[warp][d] = before + __popc(peers);
+        }
+        before = __shfl_sync(0xffffffffu, before, leader);
+        lrank[it] = before + __popc(peers & lt);
+        __syncwarp();
+    }
+    __syncthreads();
+    {  // thread = digit: exclusive prefix of the warps' counts
+        uint32_t r = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t c = wcnt[w][threadIdx.x];
+            wcnt[w][threadIdx.x] = r;
+            r += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+        if (wbase + it * 32 + lane < n) {
+            const int d = (int)((key[it] >> shift) & 255);
+            const uint32_t li = lstart[d] + wcnt[warp][d] + lrank[it];
+            skey[li] = key[it];
+            sval[li] = val[it];
+        }
+    }
+    __syncthreads();
+    const int count = (int)min((int64_t)RS_TILE, n - base);
+    for (int i = threadIdx.x; i < count; i += RS_THREADS) {
+        const mkey_t k = skey[i];
+        const int d = (int)((k >> shift) & 255);
+        const uint32_t pos = goff[d] + (uint32_t)(i - (int)lstart[d]);
+        kout[pos] = k;
+        vout[pos] = sval[i];
     }
 }
 
@@ -1053,6 +1157,13 @@ void launch_digit_hist_all(const mkey_t *keys, int64_t n, unsigned long long *hi
     k_digit_hist_all<<<g, 256, 0, s>>>(keys, n, hist);
 }
 int64_t radix_tiles(int64_t n) { return (n + RS_TILE - 1) / RS_TILE; }
+__global__ void k_iota(uint32_t *v, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (uint32_t)i;
+}
+void launch_iota(uint32_t *v, int64_t n, cudaStream_t s) {
+    if (n > 0) k_iota<<<nblk(n, 256), 256, 0, s>>>(v, n);
+}
 void launch_radix_pass(const mkey_t *kin, const uint32_t *vin, mkey_t *kout, uint32_t *vout,
                        int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches) {
     int ntiles = (int)radix_tiles(n);
@@ -1060,9 +1171,10 @@ void launch_radix_pass(const mkey_t *kin, const uint32_t *vin, mkey_t *kout, uin
     k_tile_hist<<<ntiles, RS_THREADS, 0, s>>>(kin, n, shift, tile_hist, ntiles);
     k_scan_digits<<<256, 1024, 0, s>>>(tile_hist, ntiles, digit_tot);
 #ifndef DPR_SCATTER_COALESCED
-#define DPR_SCATTER_COALESCED 1
+#define DPR_SCATTER_COALESCED 2  // 2 warp-ranked, 1 ranked per round, 0 direct
 #endif
-    if (DPR_SCATTER_COALESCED) k_scatter_c<<<ntiles, RS_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, tile_hist, ntiles, digit_tot);
+    if (DPR_SCATTER_COALESCED == 2) k_scatter_w<<<ntiles, RS_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, tile_hist, ntiles, digit_tot);
+    else if (DPR_SCATTER_COALESCED) k_scatter_c<<<ntiles, RS_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, tile_hist, ntiles, digit_tot);
     else k_scatter<<<ntiles, RS_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, tile_hist, ntiles, digit_tot);
     *launches += 3;
 }

@@ -123,7 +123,7 @@ EXPORTS = ["dpr_get_unique_id", "dpr_create_device", "dpr_create_device_hostcoll
            "dpr_render_frame_replicated", "dpr_render_frame_replicated_group",
            "dpr_frame_ready", "dpr_map_frame", "dpr_get_debug",
            "dpr_get_stats", "dpr_get_step_stats", "dpr_last_error", "dpr_exchange_plan",
-           "dpr_test_step_barrier"]
+           "dpr_test_step_barrier", "dpr_test_radix_sort"]
 
 _lib = None
 
@@ -142,6 +142,7 @@ def load(path: str = LIB_PATH):
     L.dpr_create_device_hostcoll.argtypes = [_c.c_int, _c.c_int, _c.c_int, _P, _P, _P, _P]
     L.dpr_get_step_stats.argtypes = [_P, _c.c_int, _P, _P, _P, _P, _P]
     L.dpr_test_step_barrier.argtypes = [_c.c_int, _c.c_int, _c.c_int, _P]
+    L.dpr_test_radix_sort.argtypes = [_c.c_int, _P, _c.c_int64, _P]
     for n in ("dpr_release_device", "dpr_clear_parts", "dpr_commit_world", "dpr_render_frame",
               "dpr_render_frame_composite", "dpr_render_frame_replicated"):
         getattr(L, n).argtypes = [_P]
@@ -188,6 +189,11 @@ def test_step_barrier(cuda_device: int, nranks: int, iters: int) -> int:
     m = _c.c_int64(-1)
     _check(load().dpr_test_step_barrier(cuda_device, nranks, iters, _c.byref(m)))
     return m.value
+
+
+def test_radix_sort(cuda_device: int, keys_ptr: int, n: int, perm_ptr: int) -> None:
+    """dpr_test_radix_sort: the build's stable LSD key sort; keys / perm are device pointers."""
+    _check(load().dpr_test_radix_sort(cuda_device, keys_ptr, n, perm_ptr))
 
 
 def get_unique_id() -> bytes:

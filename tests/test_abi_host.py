@@ -21,7 +21,7 @@ def test_library_exports_every_declared_symbol():
     dpr = _lib()
     hdr = open(os.path.join(ROOT, "include", "dpr.h")).read()
     declared = set(re.findall(r"^DPR_API\s+(?:int|const char \*)\s*(dpr_\w+)\(", hdr, re.M))
-    assert len(declared) == 25
+    assert len(declared) == 26
     L = dpr.load()
     missing = [n for n in declared if not hasattr(L, n)]
     assert not missing

@@ -203,3 +203,34 @@ def test_step_barrier_protocol(nranks):
     with skewed arrivals: every boundary's gathered sums are right."""
     dpr = _dpr()
     assert dpr.test_step_barrier(0, nranks, 2000) == 0
+
+
+@pytest.mark.parametrize("n", [1, 7, 4095, 4096, 4097, 3 * 4096 + 17, (1 << 20) + 333])
+@pytest.mark.parametrize("dist", ["uniform30", "few", "high_digit", "equal"])
+def test_radix_sort_stable(n, dist):
+    """The LBVH builder's key sort (north star subsystem (1)): ascending keys, equal keys in
+    input order -- the stable argsort -- over ragged tile counts and duplicate-heavy keys."""
+    import torch
+    dpr = _dpr()
+    rng = np.random.default_rng(n + len(dist))
+    if dist == "uniform30":
+        k = rng.integers(0, 1 << 30, n, dtype=np.uint32)
+    elif dist == "few":
+        k = rng.integers(0, 16, n, dtype=np.uint32) * np.uint32(0x01010101)
+    elif dist == "high_digit":
+        k = (rng.integers(0, 64, n, dtype=np.uint32) << np.uint32(24)) | np.uint32(5)
+    else:
+        k = np.full(n, 0x2aaaaaaa, np.uint32)
+    kd = torch.from_numpy(k.view(np.int32)).cuda()
+    pd = torch.empty(n, dtype=torch.int32, device="cuda")
+    dpr.test_radix_sort(0, kd.data_ptr(), n, pd.data_ptr())
+    perm = pd.cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(perm, np.argsort(k, kind="stable").astype(np.uint32))
+    assert np.array_equal(kd.cpu().numpy().view(np.uint32), k)   # keys untouched
+
+
+def test_radix_sort_args():
+    dpr = _dpr()
+    dpr.test_radix_sort(0, 0, 0, 0)                  # n = 0: nothing to do
+    with pytest.raises(dpr.DprError):
+        dpr.test_radix_sort(0, 0, 5, 0)
