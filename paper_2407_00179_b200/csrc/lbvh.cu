@@ -730,16 +730,16 @@ __global__ void k_gather_prims(const float4 *__restrict__ in, const uint32_t *__
 
 // Binary node ids: internal k in [0, n-1), leaf (sorted prim) j -> n-1+j.  One 32-byte
 // record per node (BNode; leaves: a.leaf[2j], a.leaf[2j+1]); sz = min(prim count, 7).
-__device__ __forceinline__ void bin_child(const CollapseArgs &a, int id, float lo[3], float hi[3], int &sz,
-                                          uint32_t &cl, uint32_t &cr) {
+// cl: left id | min(size, 7) << 29 (a leaf: size 1), cr: right id | range offset << 29
+__device__ __forceinline__ void bin_child(const CollapseArgs &a, int id, float lo[3], float hi[3], uint32_t &cl,
+                                          uint32_t &cr) {
     float4 l, h;
     if (id >= a.n - 1) {
         const int64_t j = id - (a.n - 1);
-        l = __ldg(a.leaf + 2 * j); h = __ldg(a.leaf + 2 * j + 1); sz = 1; cl = cr = 0;
+        l = __ldg(a.leaf + 2 * j); h = __ldg(a.leaf + 2 * j + 1); cl = 1u << 29; cr = 0;
     } else {
         l = __ldg(&a.bn[id].a); h = __ldg(&a.bn[id].b);
-        const uint32_t w = __float_as_uint(l.w);
-        sz = (int)(w >> 29); cl = w & 0x1fffffffu; cr = __float_as_uint(h.w);
+        cl = __float_as_uint(l.w); cr = __float_as_uint(h.w);
     }
     lo[0] = pad_lo(l.x); lo[1] = pad_lo(l.y); lo[2] = pad_lo(l.z);
     hi[0] = pad_hi(h.x); hi[1] = pad_hi(h.y); hi[2] = pad_hi(h.z);
@@ -762,7 +762,8 @@ constexpr int CB = 128;  // collapse block
 // threads read the same child slot of consecutive threads), so a child is inserted with one
 // store per field at a dynamic index instead of unrolled selects over 8 register slots (those
 // selects were most of the register version's instructions at 164 registers / 18% occupancy).
-// Kept in registers: each child's box area, capped size and internal flag (the argmax inputs).
+// Kept in registers: each child's argmax key (box area) and the internal / large bit masks;
+// the capped sizes ride in the top bits of ccl.
 struct CollapseSmem {
     int cid[8][CB];
     uint32_t ccl[8][CB], ccr[8][CB];
@@ -783,26 +784,29 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
     const bool live = t < nitems;
     const int2 item = live ? items[t] : make_int2(0, 0);
     const int wnode = item.x, b = item.y;
-    float area[8];
-    int c1[8];
-    unsigned inner_m = 0;  // bit i: child i is an internal binary node
+    // argmax keys: box area with the low 4 mantissa bits replaced by 8 | (7 - i) (> 0, ties
+    // to the lowest child index); bit masks of internal children and of those with more than
+    // LEAF_MAX prims; sizes live in the top bits of ccl
+    uint32_t akey[8];
+    unsigned inner_m = 0, big_m = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { area[i] = 0.0f; c1[i] = 0; }
+    for (int i = 0; i < 8; ++i) akey[i] = 0;
     auto put = [&](int i, int id) -> void {  // load child id into slot i (smem + registers)
         float lo3[3], hi3[3];
-        int sz;
         uint32_t cl, cr;
-        bin_child(a, id, lo3, hi3, sz, cl, cr);
+        bin_child(a, id, lo3, hi3, cl, cr);
         S.cid[i][tid] = id; S.ccl[i][tid] = cl; S.ccr[i][tid] = cr;
 #pragma unroll
         for (int c = 0; c < 3; ++c) { S.lo[c][i][tid] = lo3[c]; S.hi[c][i][tid] = hi3[c]; }
         const float ex = hi3[0] - lo3[0], ey = hi3[1] - lo3[1], ez = hi3[2] - lo3[2];
         const float ar = ex * ey + ey * ez + ez * ex;
-        const bool in = id < a.n - 1;
+        const uint32_t key = (__float_as_uint(ar) & ~15u) | 8u | (uint32_t)(7 - i);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (k == i) { area[k] = ar; c1[k] = sz; }
+            if (k == i) akey[k] = key;
+        const bool in = id < a.n - 1, big = in && (int)(cl >> 29) > LEAF_MAX;
         inner_m = in ? (inner_m | (1u << i)) : (inner_m & ~(1u << i));
+        big_m = big ? (big_m | (1u << i)) : (big_m & ~(1u << i));
     };
     int nc = 0;
     if (!live) {
@@ -818,15 +822,13 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
     // (DPR_FILL_LEAVES): then the largest small subtree, while slots are free
     for (int pass = 0; pass < (DPR_FILL_LEAVES ? 2 : 1); ++pass) {
         while (nc < 8) {
-            int best = -1;
-            float ba = -1.0f;
+            const unsigned elig = (pass == 0 ? (inner_m & big_m) : inner_m) & ((1u << nc) - 1u);
+            if (!elig) break;
+            uint32_t m = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (i >= nc || !(inner_m >> i & 1) || (pass == 0 && c1[i] <= LEAF_MAX)) continue;
-                if (area[i] > ba) { ba = area[i]; best = i; }
-            }
-            if (best < 0) break;
-            const int l = (int)S.ccl[best][tid], r = (int)(S.ccr[best][tid] & 0x1fffffffu);
+            for (int i = 0; i < 8; ++i) m = max(m, (elig >> i & 1) ? akey[i] : 0u);
+            const int best = 7 - (int)(m & 7u);
+            const int l = (int)(S.ccl[best][tid] & 0x1fffffffu), r = (int)(S.ccr[best][tid] & 0x1fffffffu);
             put(best, l);
             put(nc, r);
             nc++;
@@ -846,6 +848,9 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
     {
         float bcst[8];
         int bsl[8];
+        // (a variant walking a child's slots in falling cost order -- its octant with the sign
+        // flips ordered by the flipped |offset| sum -- ran slower: 13.7 vs 12.8 ms per
+        // configs[3] build, r02)
         auto best_free = [&](int i, unsigned used, float &bc, int &bs) -> void {
             float dc[3];
 #pragma unroll
@@ -858,8 +863,7 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
             }
         };
         // with every slot free, a child's best slot is the octant of its offset and its cost
-        // |dx| + |dy| + |dz| (rounding is monotone; exact ties may pick another octant than
-        // the full scan's lowest index: a different, equally valid slot order)
+        // |dx| + |dy| + |dz|
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             slot_of[i] = 0; bcst[i] = -3.4e38f; bsl[i] = 0;
@@ -894,13 +898,17 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
     // internal vs leaf children, allocation
     int n_int = 0, n_prims = 0;
     unsigned imask = 0, lmask = 0, leaf_m = 0;
+    unsigned long long szslot = 0;  // byte s: prims of the leaf child in slot s
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         if (i >= nc) continue;
-        const bool lf = !(inner_m >> i & 1) || c1[i] <= LEAF_MAX;
-        if (lf) { n_prims += c1[i]; lmask |= 1u << slot_of[i]; leaf_m |= 1u << i; }
-        else { n_int++; imask |= 1u << slot_of[i]; }
+        if (!(big_m >> i & 1)) {
+            const uint32_t sz = S.ccl[i][tid] >> 29;
+            n_prims += (int)sz; lmask |= 1u << slot_of[i]; leaf_m |= 1u << i;
+            szslot |= (unsigned long long)sz << (8 * slot_of[i]);
+        } else { n_int++; imask |= 1u << slot_of[i]; }
     }
+    const unsigned long long szpre = szslot * 0x0101010101010101ull;  // byte s: prims in slots <= s
     int child_base, prim_base, out_base;
     {
         int xi = n_int, xp = n_prims;
@@ -928,7 +936,7 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
     // per-child planes below multiply by the exact power-of-two reciprocal (no division)
     float p[3];
     int e[3];
-    double isc[3];
+    float isc[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         p[c] = nlo_[c];
@@ -943,7 +951,7 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
             if (ee > 127) ee = 127;
         }
         e[c] = ee;
-        isc[c] = ldexp(1.0, -ee);
+        isc[c] = ldexpf(1.0f, -ee);  // extents of finite boxes keep ee <= 122: a normal float
     }
     uint32_t qw[6][2], mw[2] = {0u, 0u};
 #pragma unroll
@@ -955,9 +963,12 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
         const int sh = 8 * (sl & 3);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const double ql = floor(((double)S.lo[c][i][tid] - (double)p[c]) * isc[c]);
-            const double qh = ceil(((double)S.hi[c][i][tid] - (double)p[c]) * isc[c]);
-            const uint32_t bl = (uint32_t)fmin(fmax(ql, 0.0), 255.0), bh = (uint32_t)fmin(fmax(qh, 0.0), 255.0);
+            // floor / ceil of the exact (child - node) / 2^e: the difference rounded down (up)
+            // lands on the same side of every plane k * 2^e (k <= 255: a float), and the
+            // power-of-two scaling is exact -- the same planes as the exact computation
+            const float ql = floorf(__fsub_rd(S.lo[c][i][tid], p[c]) * isc[c]);
+            const float qh = ceilf(__fsub_ru(S.hi[c][i][tid], p[c]) * isc[c]);
+            const uint32_t bl = (uint32_t)fminf(fmaxf(ql, 0.0f), 255.0f), bh = (uint32_t)fminf(fmaxf(qh, 0.0f), 255.0f);
             if (sl < 4) { qw[c][0] |= bl << sh; qw[3 + c][0] |= bh << sh; }
             else { qw[c][1] |= bl << sh; qw[3 + c][1] |= bh << sh; }
         }
@@ -967,11 +978,9 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
             next[out_base + rank] = make_int2(child_base + rank, cidi);
         } else {
             // prims of the leaf children are laid out in slot order
-            int off = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (j != i && (leaf_m >> j & 1) && slot_of[j] < sl) off += c1[j];
-            const uint32_t m = 0x80u | ((uint32_t)(c1[i] - 1) << 5) | (uint32_t)off;
+            const int off = sl ? (int)((szpre >> (8 * (sl - 1))) & 0xffu) : 0;
+            const int ci = (int)(S.ccl[i][tid] >> 29);
+            const uint32_t m = 0x80u | ((uint32_t)(ci - 1) << 5) | (uint32_t)off;
             if (sl < 4) mw[0] |= m << sh; else mw[1] |= m << sh;
             // the (<= LEAF_MAX) prims of the binary subtree, in sorted order: a contiguous
             // range when the record holds its offset, else a walk of the subtree
@@ -980,7 +989,7 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
                 a.perm[prim_base + off] = (uint32_t)(cidi - (a.n - 1));
             } else if (roff != 7u) {
                 const uint32_t l0 = (uint32_t)cidi - roff;
-                for (int k = 0; k < c1[i]; ++k) a.perm[prim_base + off + k] = l0 + (uint32_t)k;
+                for (int k = 0; k < ci; ++k) a.perm[prim_base + off + k] = l0 + (uint32_t)k;
             } else {
                 int st[8], sp = 0, k = 0;
                 st[sp++] = cidi;
