@@ -587,13 +587,15 @@ int build_world(Dev *d) {
                 launches++;
             } else if (d->builder == 1) {
                 // agglomerative LBVH (default): topology + boxes in one bottom-up pass
-                RET(ensure(d, d->b_arrive, sizeof(int) * (n - 1) + sizeof(int)));
-                int *other = P<int>(d->b_arrive);
-                CK(cudaMemsetAsync(other, 0xff, sizeof(int) * (n - 1), s));
+                // exchange words: 8 bytes per internal node (all ones = no arrival yet), then the root id
+                RET(ensure(d, d->b_arrive, sizeof(unsigned long long) * (n - 1) + sizeof(int)));
+                unsigned long long *other = P<unsigned long long>(d->b_arrive);
+                CK(cudaMemsetAsync(other, 0xff, sizeof(unsigned long long) * (n - 1), s));
                 // the other radix-sort key buffer is free now: per-split prefix lengths
                 uint8_t *split = P<uint8_t>(d->b_keys[keys == P<mkey_t>(d->b_keys[0]) ? 1 : 0]);
-                launches += launch_agglo(keys, split, n, leaf, P<BNode>(d->b_bn), other, other + (n - 1), s);
-                root_dev = other + (n - 1);  // read by the first collapse level on the device
+                int *root = reinterpret_cast<int *>(other + (n - 1));
+                launches += launch_agglo(keys, split, n, leaf, P<BNode>(d->b_bn), other, root, s);
+                root_dev = root;  // read by the first collapse level on the device
             } else {
                 // Karras 2012 LBVH + bottom-up refit
                 RET(ensure(d, d->b_rlo, sizeof(int) * (n - 1)));

@@ -44,7 +44,7 @@ struct BNode { float4 a, b; };
 // split_scratch: >= n-1 bytes (the unused radix-sort key buffer); leaf: packed leaf boxes
 // (leaf[2j] = lo, leaf[2j+1] = hi); returns kernels launched
 int launch_agglo(const mkey_t *keys, uint8_t *split_scratch, int64_t n, const float4 *leaf, BNode *bn,
-                 int *other, int *root_out, cudaStream_t s);
+                 void *other, int *root_out, cudaStream_t s);
 // BNode records from the separate arrays of the Karras + refit / PLOC builders
 void launch_pack_bnodes(int64_t n, const int *left, const int *right, const int *size, const float4 *nlo,
                         const float4 *nhi, BNode *bn, cudaStream_t s);

@@ -612,9 +612,11 @@ __global__ void k_agglo(const mkey_t *__restrict__ keys, const uint8_t *__restri
 // warp's lanes stay busy (one thread per leaf retires half its warp after the first step and
 // ran at 6.4/32 active lanes).  Any order of leaf starts builds the same tree: a node is
 // finished by whichever child arrives second.
+// The exchange word is 64-bit: (outer range bound << 32) | child id, so the second arrival
+// learns its sibling's id from the exchange itself (no separate id store and reload).
 __global__ void __launch_bounds__(256) k_agglo_p(const uint8_t *__restrict__ split, int64_t n,
-                                                 const float4 *__restrict__ leaf, BNode *bn, int *other,
-                                                 int *root_out) {
+                                                 const float4 *__restrict__ leaf, BNode *bn,
+                                                 unsigned long long *other, int *root_out) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     bool alive = false, exhausted = false;
@@ -664,14 +666,11 @@ __global__ void __launch_bounds__(256) k_agglo_p(const uint8_t *__restrict__ spl
         else if (r == n - 1) is_left = false;
         else is_left = __ldg(split + r) > __ldg(split + l - 1);
         const int64_t p = is_left ? r : l - 1;
-        if (is_left) __stcg(reinterpret_cast<float *>(&bn[p].a) + 3, __int_as_float(cur));
-        else __stcg(reinterpret_cast<float *>(&bn[p].b) + 3, __int_as_float(cur));
-        int prev;
-        const int val = is_left ? (int)l : (int)r;
-        asm volatile("atom.exch.acq_rel.gpu.b32 %0, [%1], %2;" : "=r"(prev) : "l"(other + p), "r"(val) : "memory");
-        if (prev < 0) { alive = false; continue; }  // first arrival: the sibling finishes the node
-        const int sib = is_left ? __float_as_int(__ldcg(reinterpret_cast<const float *>(&bn[p].b) + 3))
-                                : __float_as_int(__ldcg(reinterpret_cast<const float *>(&bn[p].a) + 3)) & 0x1fffffff;
+        const unsigned long long val = ((unsigned long long)(uint32_t)(is_left ? l : r) << 32) | (uint32_t)cur;
+        unsigned long long got;
+        asm volatile("atom.exch.acq_rel.gpu.b64 %0, [%1], %2;" : "=l"(got) : "l"(other + p), "l"(val) : "memory");
+        if (got == ~0ull) { alive = false; continue; }  // first arrival: the sibling finishes the node
+        const int prev = (int)(got >> 32), sib = (int)(uint32_t)got;
         float4 a, b;
         if (sib >= n - 1) { a = leaf[2 * (sib - (n - 1))]; b = leaf[2 * (sib - (n - 1)) + 1]; }
         else { a = __ldcg(&bn[sib].a); b = __ldcg(&bn[sib].b); }
@@ -1203,7 +1202,7 @@ void launch_refit(int64_t n, const int *left, const int *right, const int *paren
 #define DPR_AGGLO_PERSIST 1
 #endif
 int launch_agglo(const mkey_t *keys, uint8_t *split_scratch, int64_t n, const float4 *leaf, BNode *bn,
-                 int *other, int *root_out, cudaStream_t s) {
+                 void *other, int *root_out, cudaStream_t s) {
     if (n <= 1) return 0;
     uint8_t *split = DPR_AGGLO_SPLIT ? split_scratch : nullptr;
     if (split) k_split_delta<<<nblk(n, 256), 256, 0, s>>>(keys, n, split);
@@ -1218,10 +1217,11 @@ int launch_agglo(const mkey_t *keys, uint8_t *split_scratch, int64_t n, const fl
         }
         // a resident grid, or one 64-leaf chunk per warp when the tree is small
         const int64_t need = (n + 8 * 64 - 1) / (8 * 64);
-        k_agglo_p<<<(int)std::min<int64_t>(grid, need), 256, 0, s>>>(split, n, leaf, bn, other, root_out);
+        k_agglo_p<<<(int)std::min<int64_t>(grid, need), 256, 0, s>>>(split, n, leaf, bn,
+                                                                       static_cast<unsigned long long *>(other), root_out);
         return 2;
     }
-    k_agglo<<<nblk(n, 256), 256, 0, s>>>(keys, split, n, leaf, bn, other, root_out);
+    k_agglo<<<nblk(n, 256), 256, 0, s>>>(keys, split, n, leaf, bn, static_cast<int *>(other), root_out);
     return split ? 2 : 1;
 }
 void launch_pack_bnodes(int64_t n, const int *left, const int *right, const int *size, const float4 *nlo,
