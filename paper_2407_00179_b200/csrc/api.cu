@@ -622,10 +622,14 @@ int build_world(Dev *d) {
         RET(ensure(d, d->b_wcnt, sizeof(int) * 4));
         // levels are launched in batches without a host round trip: each level kernel reads its
         // item count from device memory (lvl[L]) and appends the next level's (lvl[L+1])
-        constexpr int MAXL = 120, BATCH = 4;
-        RET(ensure(d, d->b_wcnt, sizeof(int) * (4 + MAXL + BATCH + 1)));
+        // the first batch covers the expected depth (log8 n + 3 levels: 9 of 10M prims, 11 of 55M),
+        // so the usual build makes one host round trip here; then batches of 4
+        constexpr int MAXL = 120, BATCH = 4, MAXB = 32;
+        int first_batch = 3;
+        for (int64_t m = 1; m < n && first_batch < MAXB; m *= 8) first_batch++;
+        RET(ensure(d, d->b_wcnt, sizeof(int) * (4 + MAXL + MAXB + 1)));
         int *cnt = P<int>(d->b_wcnt), *lvl = cnt + 4;
-        CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (4 + MAXL + BATCH + 1), s));
+        CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (4 + MAXL + MAXB + 1), s));
         int h_init[5] = {0, 1, 0, 0, 1};  // counters {-, nodes = 1 (root), prims, overflow}, lvl[0] = 1
         CK(cudaMemcpyAsync(cnt, h_init, sizeof(h_init), cudaMemcpyHostToDevice, s));
         int2 root = make_int2(0, n > 1 ? root_id : -1);
@@ -636,19 +640,19 @@ int build_world(Dev *d) {
         ca.n = n; ca.bn = P<BNode>(d->b_bn); ca.leaf = leaf;
         ca.perm = P<uint32_t>(d->b_wperm); ca.nodes = P<WNode>(d->b_wnodes); ca.counters = cnt;
         ca.node_cap = node_cap;
-        int h_cnt[4 + MAXL + BATCH + 1];
+        int h_cnt[4 + MAXL + MAXB + 1];
         int levels = -1;
-        for (int L = 0; levels < 0; L += BATCH) {
+        for (int L = 0, B = first_batch; levels < 0; L += B, B = BATCH) {
             if (L >= MAXL) return fail(DPR_ERR_STATE, "wide BVH deeper than the collapse level limit");
-            for (int k = L; k < L + BATCH; ++k) {
+            for (int k = L; k < L + B; ++k) {
                 launch_collapse_level(ca, P<int2>(d->b_witems[k & 1]), lvl + k, P<int2>(d->b_witems[(k + 1) & 1]),
                                       lvl + k + 1, s);
                 launches++;
             }
-            CK(cudaMemcpyAsync(h_cnt, cnt, sizeof(int) * (4 + L + BATCH + 1), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(h_cnt, cnt, sizeof(int) * (4 + L + B + 1), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             if (h_cnt[3]) return fail(DPR_ERR_STATE, "wide BVH node capacity exceeded");
-            for (int k = L; k <= L + BATCH; ++k)
+            for (int k = L; k <= L + B; ++k)
                 if (h_cnt[4 + k] == 0) { levels = k; break; }
         }
         if (h_cnt[2] != n) return fail(DPR_ERR_STATE, "wide BVH collapse lost primitives");
