@@ -422,8 +422,7 @@ int build_world(Dev *d) {
     CK(cudaMemcpyAsync(d->b_bounds.p, binit.data(), binit.size() * sizeof(int), cudaMemcpyHostToDevice, s));
     if (n > 0) {
         RET(ensure(d, d->b_prims_u, sizeof(float4) * 3 * n));
-        RET(ensure(d, d->b_blo, sizeof(float4) * n));
-        RET(ensure(d, d->b_bhi, sizeof(float4) * n));
+        RET(ensure(d, d->b_blo, sizeof(float4) * 2 * n));  // prim boxes, lo / hi interleaved (32 B each)
     }
     int64_t off = 0;
     int launches = 0;
@@ -450,7 +449,7 @@ int build_world(Dev *d) {
         RET(ensure(d, d->b_chunks, sizeof(PrimChunk) * chunks.size()));
         CK(cudaMemcpyAsync(d->b_chunks.p, chunks.data(), sizeof(PrimChunk) * chunks.size(), cudaMemcpyHostToDevice, s));
         launch_part_prims(P<PrimChunk>(d->b_chunks), (int)chunks.size(), P<float4>(d->b_prims_u), P<float4>(d->b_blo),
-                          P<float4>(d->b_bhi), P<int>(d->b_bounds), P<int>(d->b_bounds) + 12 * (np + 1), s);
+                          P<float4>(d->b_blo) + 1, P<int>(d->b_bounds), P<int>(d->b_bounds) + 12 * (np + 1), s);
         launches++;
     }
     // Morton keys + all digit histograms
@@ -460,7 +459,7 @@ int build_world(Dev *d) {
             RET(ensure(d, d->b_keys[i], sizeof(mkey_t) * n + 64));  // + the agglomeration fetch counter
             RET(ensure(d, d->b_vals[i], sizeof(uint32_t) * n));
         }
-        launch_morton(P<float4>(d->b_blo), P<float4>(d->b_bhi), n, P<int>(d->b_bounds),
+        launch_morton(P<float4>(d->b_blo), P<float4>(d->b_blo) + 1, n, P<int>(d->b_bounds),
                       P<mkey_t>(d->b_keys[0]), P<uint32_t>(d->b_vals[0]), s);
         RET(ensure(d, d->b_hist, sizeof(unsigned long long) * MKEY_DIGITS * 256));
         CK(cudaMemsetAsync(d->b_hist.p, 0, sizeof(unsigned long long) * MKEY_DIGITS * 256, s));
@@ -531,7 +530,7 @@ int build_world(Dev *d) {
         RET(ensure(d, d->b_slo, sizeof(float4) * 2 * n));
         float4 *leaf = P<float4>(d->b_slo);
         launch_gather_prims(P<float4>(d->b_prims_u), perm, n, nullptr, P<float4>(d->b_blo),
-                            P<float4>(d->b_bhi), leaf, leaf + 1, s);
+                            P<float4>(d->b_blo) + 1, leaf, leaf + 1, s);
         launches++;
         int root_id = 0;
         const int *root_dev = nullptr;  // device copy of the root id (agglomerative builder)

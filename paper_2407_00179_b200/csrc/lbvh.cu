@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(256) k_part_prims(const PrimChunk *__restrict_
             lo = mk(s.x - s.w, s.y - s.w, s.z - s.w);
             hi = mk(s.x + s.w, s.y + s.w, s.z + s.w);
         }
-        blo[g] = make_float4(lo.x, lo.y, lo.z, 0.0f);
-        bhi[g] = make_float4(hi.x, hi.y, hi.z, 0.0f);
+        blo[2 * g] = make_float4(lo.x, lo.y, lo.z, 0.0f);  // interleaved: bhi == blo + 1
+        bhi[2 * g] = make_float4(hi.x, hi.y, hi.z, 0.0f);
         acc.add(lo, hi);
     }
     acc.block_flush(bounds + 12 * c.slot, bounds);
@@ -153,7 +153,7 @@ __global__ void k_morton(const float4 *__restrict__ blo, const float4 *__restric
                          const int *__restrict__ bounds, mkey_t *keys, uint32_t *vals) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float4 lo = blo[i], hi = bhi[i];
+    float4 lo = blo[2 * i], hi = bhi[2 * i];
     float c[3] = {(lo.x + hi.x) * 0.5f, (lo.y + hi.y) * 0.5f, (lo.z + hi.z) * 0.5f};
     uint32_t q[3];
     for (int a = 0; a < 3; ++a) {
@@ -715,8 +715,8 @@ __global__ void k_gather_prims(const float4 *__restrict__ in, const uint32_t *__
         out[3 * i + 1] = in[3 * (int64_t)s + 1];
         out[3 * i + 2] = in[3 * (int64_t)s + 2];
     }
-    slo[2 * i] = blo[s];  // packed leaf record: lo at 2i, hi at 2i + 1 (slo + 1 == shi)
-    shi[2 * i] = bhi[s];
+    slo[2 * i] = blo[2 * (int64_t)s];  // packed leaf record: lo at 2i, hi at 2i + 1 (slo + 1 == shi);
+    shi[2 * i] = bhi[2 * (int64_t)s];  // the input boxes are interleaved the same way (one sector)
 }
 
 // ---------------------------------------------------------------------------------------
