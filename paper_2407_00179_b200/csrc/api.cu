@@ -658,6 +658,10 @@ int build_world(Dev *d) {
         launch_permute_prims(P<float4>(d->b_prims_u), P<uint32_t>(d->b_wperm), perm, n, P<float4>(d->b_prims_w), s);
         launches++;
         d->wnodes_count = h_cnt[1];
+#ifdef DPR_COLLAPSE_STATS
+        fprintf(stderr, "collapse: %d wide nodes, %.3f children per node, %.3f prims per leaf child\n", h_cnt[1],
+                (double)h_cnt[0] / h_cnt[1], (double)n / (h_cnt[0] - (h_cnt[1] - 1)));
+#endif
         d->bvh_levels = levels;
     }
     // bricks: macrocells

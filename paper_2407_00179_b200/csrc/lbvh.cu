@@ -931,6 +931,9 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
     }
     if (!live) continue;
     if (child_base + n_int > a.node_cap) { atomicOr(&a.counters[3], 1); continue; }
+#ifdef DPR_COLLAPSE_STATS
+    atomicAdd(&a.counters[0], nc);
+#endif
     // quantisation (outward): smallest e with 255 * 2^e >= extent (frexp, no log2); the
     // per-child planes below multiply by the exact power-of-two reciprocal (no division)
     float p[3];

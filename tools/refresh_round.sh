@@ -1,18 +1,24 @@
 #!/bin/bash
 # Full evidence refresh for one tag (under gpurun, from the repo root):
 #   bash tools/refresh_round.sh TAG
-# configs[1], configs[2], configs[3]: bench line + launch list + ncu --set full of the trace
-# kernels (tools/profile_round.sh); configs[0], configs[2] delta tracking, configs[4]: bench
-# lines; the reference arm line; configs[3]'s LBVH build kernels under ncu.
+# Bench lines of every workload + the reference arm (tools/bench_all.sh), then per configs[1],
+# configs[2], configs[3]: the ncu launch list of one host-loop step and an ncu --set full
+# capture of the trace / march kernels exported to CSV (tools/ncu_capture.sh), and configs[3]'s
+# LBVH build kernels under ncu.  Every ncu command runs after the same command exited 0 alone.
 TAG=$1
 mkdir -p gpurun_out
-bash tools/profile_round.sh $TAG c2 regex:k_trace
-bash tools/profile_round.sh $TAG c3
-NCU_SKIP=0 NCU_COUNT=8 bash tools/profile_round.sh $TAG c4 regex:k_trace_path
-timeout 600 python bench.py --config c1 --steps 20 --warmup 5 > gpurun_out/${TAG}_bench_c1.json 2>/dev/null; echo "c1 rc=$?"
-timeout 600 python bench.py --config c3 --flags 16 --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_c3_delta.json 2>/dev/null; echo "c3 delta rc=$?"
-timeout 1200 python bench.py --config c5 --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_c5.json 2>/dev/null; echo "c5 rc=$?"
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_bench_reference_arm.json 2>/dev/null; echo "ref rc=$?"
-python tools/build_only.py c4 2 > gpurun_out/plain_b.log 2>&1 && ncu --set full --clock-control none --import-source on \
-  -k "regex:k_collapse_r|k_agglo|k_permute_prims|k_scatter_c|k_part_prims|k_gather_prims" -c 24 \
-  -o gpurun_out/${TAG}_build_c4 python tools/build_only.py c4 1 > gpurun_out/ncu_build.log 2>&1; echo "build ncu rc=$?"
+bash tools/bench_all.sh $TAG
+export DPR_STEP_LOOP=host
+for C in c2 c3 c4; do
+  CMD="python bench.py --config $C --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+  $CMD > gpurun_out/plain_l_$C.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/${TAG}_launches_$C.csv $CMD > gpurun_out/ncu_launches_$C.log 2>&1
+  echo "launches $C rc=$?"
+done
+bash tools/ncu_capture.sh $TAG c2 "regex:k_trace" 2 2 "k_trace_occl k_trace_path"
+bash tools/ncu_capture.sh $TAG c3 "regex:k_trace|k_march" 2 3 "k_trace_path k_march_occl"
+bash tools/ncu_capture.sh $TAG c4 "regex:k_trace_path" 0 8 "k_trace_path"
+bash tools/ncu_capture.sh $TAG c4b "regex:k_collapse_r|k_agglo_p|k_permute_prims|k_scatter_w|k_part_prims|k_gather_prims|k_tile_hist|k_morton" 0 30 "k_collapse_r k_agglo_p" python tools/build_only.py c4 1
+# ncu source pages run to tens of MB: compressed so gpurun_out stays under the return cap
+find gpurun_out -name "${TAG}_*.csv" -size +1M -exec gzip -f {} \;
+ls -la gpurun_out | grep $TAG
