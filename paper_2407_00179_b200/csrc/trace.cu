@@ -640,14 +640,15 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
     float a = floorf(t0 / dt - 0.5f);
     float bb = ceilf(t1 / dt);
     if (bb > 1.0e9f) bb = 1.0e9f;
-    int64_t i0 = (int64_t)a - 1;
-    if (i0 < 0) i0 = 0;
-    int64_t i1 = (int64_t)bb + 1;
+    // 32-bit sample indices (|i| <= 1e9 + 1 by the clamp above; a < 0 clamps to 0): the same
+    // values and the same float conversions as 64-bit ones, without the 64-bit convert
+    int i0 = a > 0.0f ? (int)fminf(a, 2.0e9f) - 1 : 0;  // a > 2e9: i0 > i1, no sample (as int64)
+    const int i1 = (int)bb + 1;
     const int nx = B.hi[0] - B.lo[0] + 1, ny = B.hi[1] - B.lo[1] + 1;
     uint4 rr = make_uint4(0, 0, 0, 0);
-    int64_t rblk = -1;
-    for (int64_t i = i0; i <= i1; ++i) {
-        float ti = sample_t(i, dt);
+    int rblk = -1;
+    for (int i = i0; i <= i1; ++i) {
+        float ti = ((float)i + 0.5f) * dt;  // sample_t
         if (!(ti < bound)) return false;
         f3 pt = mk(o.x + ti * d.x, o.y + ti * d.y, o.z + ti * d.z);
         f3 g = grid_coord(B, pt);
@@ -656,7 +657,7 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
             continue;
         float fx0 = floorf(g.x), fy0 = floorf(g.y), fz0 = floorf(g.z);
         int ix = (int)fx0 - B.lo[0], iy = (int)fy0 - B.lo[1], iz = (int)fz0 - B.lo[2];
-        const int mx = ix / MC_SIZE, my = iy / MC_SIZE, mz = iz / MC_SIZE;
+        const int mx = (int)((unsigned)ix / MC_SIZE), my = (int)((unsigned)iy / MC_SIZE), mz = (int)((unsigned)iz / MC_SIZE);  // >= 0 here
 #if DPR_INLINE_DIST
         // macrocell distance field: every macrocell within Chebyshev distance dist-1 is empty
         const int dist = __ldg(B.mcd + (mz * B.mc_dims[1] + my) * B.mc_dims[0] + mx);
@@ -686,7 +687,9 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
 #endif
             float m0, m1;
             slab(mlo, mhi, o, d, tmax, m0, m1);
-            const int64_t jump = (int64_t)floorf(m1 / dt - 0.5f) - 2;
+            // (int64)jf - 2 as before for jf < 2e9 (NaN converts to 0 either way); beyond, past i1
+            const float jf = floorf(m1 / dt - 0.5f);
+            const int jump = !(jf >= 2.0e9f) ? (int)jf - 2 : i1;
             if (jump > i) i = jump;  // loop ++i resumes at jump + 1
             continue;
         }
