@@ -110,6 +110,8 @@ typedef struct {
  *              stores voxels [cell_lo, cell_hi] INCLUSIVE (one ghost layer), x fastest;
  *              tf float[256][4] rgba over [tf_lo, tf_hi], alpha scaled by density_scale
  *              (SURVEY P10).  All bricks of a world must share gdims/origin/spacing.
+ *              A brick stores fewer than 2^31 voxel rows (y extent * z extent, each
+ *              cell_hi - cell_lo + 1; else DPR_ERR_INVALID_ARG).
  *   albedo: matte rgb for TRIANGLES / SPHERES.
  *   bounds_hint: optional app-provided box (S8.2 "box3 boundingBox"); it is
  *   only VALIDATED to contain the part (DPR_ERR_INVALID_ARG otherwise), never used for

@@ -1878,6 +1878,8 @@ int check_part(const dpr_part_desc *p) {
             if (p->cell_lo[c] < 0 || p->cell_hi[c] <= p->cell_lo[c] || p->cell_hi[c] > p->gdims[c] - 1 || !(p->spacing[c] > 0))
                 return fail(DPR_ERR_INVALID_ARG, "brick part: bad cell range / spacing");
         if (!(p->tf_hi > p->tf_lo)) return fail(DPR_ERR_INVALID_ARG, "brick part: tf_hi must exceed tf_lo");
+        if ((int64_t)(p->cell_hi[1] - p->cell_lo[1] + 1) * (p->cell_hi[2] - p->cell_lo[2] + 1) >= ((int64_t)1 << 31))
+            return fail(DPR_ERR_INVALID_ARG, "brick part: more than 2^31 - 1 voxel rows (y * z extent)");
         break;
     default:
         return fail(DPR_ERR_INVALID_ARG, "bad part kind");

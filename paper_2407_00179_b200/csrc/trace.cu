@@ -645,6 +645,8 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
     int i0 = a > 0.0f ? (int)fminf(a, 2.0e9f) - 1 : 0;  // a > 2e9: i0 > i1, no sample (as int64)
     const int i1 = (int)bb + 1;
     const int nx = B.hi[0] - B.lo[0] + 1, ny = B.hi[1] - B.lo[1] + 1;
+    const float glx = (float)B.lo[0], ghx = (float)B.hi[0], gly = (float)B.lo[1], ghy = (float)B.hi[1],
+                glz = (float)B.lo[2], ghz = (float)B.hi[2];
     uint4 rr = make_uint4(0, 0, 0, 0);
     int rblk = -1;
     for (int i = i0; i <= i1; ++i) {
@@ -652,9 +654,7 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
         if (!(ti < bound)) return false;
         f3 pt = mk(o.x + ti * d.x, o.y + ti * d.y, o.z + ti * d.z);
         f3 g = grid_coord(B, pt);
-        if (!(g.x >= (float)B.lo[0] && g.x < (float)B.hi[0] && g.y >= (float)B.lo[1] &&
-              g.y < (float)B.hi[1] && g.z >= (float)B.lo[2] && g.z < (float)B.hi[2]))
-            continue;
+        if (!(g.x >= glx && g.x < ghx && g.y >= gly && g.y < ghy && g.z >= glz && g.z < ghz)) continue;
         float fx0 = floorf(g.x), fy0 = floorf(g.y), fz0 = floorf(g.z);
         int ix = (int)fx0 - B.lo[0], iy = (int)fy0 - B.lo[1], iz = (int)fz0 - B.lo[2];
         const int mx = (int)((unsigned)ix / MC_SIZE), my = (int)((unsigned)iy / MC_SIZE), mz = (int)((unsigned)iz / MC_SIZE);  // >= 0 here
@@ -695,7 +695,7 @@ __device__ __forceinline__ bool march_brick(const BrickDev &B, f3 o, f3 d, float
         }
         nsamples++;
         float fx = g.x - fx0, fy = g.y - fy0, fz = g.z - fz0;
-        const float *v = B.vox + (int64_t)ix + (int64_t)nx * ((int64_t)iy + (int64_t)ny * iz);
+        const float *v = B.vox + (int64_t)ix + (int64_t)nx * (iy + ny * iz);  // ny * nz < 2^31 (dpr.h brick limits)
         const int64_t sy = nx, sz = (int64_t)nx * ny;
         float v000 = __ldg(v), v100 = __ldg(v + 1), v010 = __ldg(v + sy), v110 = __ldg(v + sy + 1);
         float v001 = __ldg(v + sz), v101 = __ldg(v + sz + 1), v011 = __ldg(v + sz + sy),
@@ -1030,7 +1030,7 @@ __device__ __noinline__ bool delta_track(const WorldDev &W, f3 o, f3 d, float li
             nsamples++;
             const int nx = B.hi[0] - B.lo[0] + 1, ny = B.hi[1] - B.lo[1] + 1;
             const float fx = g.x - fx0, fy = g.y - fy0, fz = g.z - fz0;
-            const float *v = B.vox + (int64_t)ix + (int64_t)nx * ((int64_t)iy + (int64_t)ny * iz);
+            const float *v = B.vox + (int64_t)ix + (int64_t)nx * (iy + ny * iz);  // ny * nz < 2^31 (dpr.h brick limits)
             const int64_t sy = nx, sz = (int64_t)nx * ny;
             float v000 = __ldg(v), v100 = __ldg(v + 1), v010 = __ldg(v + sy), v110 = __ldg(v + sy + 1);
             float v001 = __ldg(v + sz), v101 = __ldg(v + sz + 1), v011 = __ldg(v + sz + sy),
