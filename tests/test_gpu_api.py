@@ -234,3 +234,20 @@ def test_radix_sort_args():
     dpr.test_radix_sort(0, 0, 0, 0)                  # n = 0: nothing to do
     with pytest.raises(dpr.DprError):
         dpr.test_radix_sort(0, 0, 5, 0)
+
+
+def test_brick_row_limit():
+    """dpr.h BRICK: a brick stores fewer than 2^31 voxel rows (y * z extent); larger ones are
+    rejected at commit_part, before the voxel array is read (the march indexes rows in 32 bits)."""
+    dpr = _dpr()
+    G = 70000
+    tf = di.default_tf()
+    big = di.Part(0, di.BRICK, gdims=(4, G, G), origin=(0, 0, 0), spacing=(1e-3,) * 3,
+                  cell_lo=(0, 0, 0), cell_hi=(3, 46341, 46341), voxels=np.zeros(8, np.float32), tf=tf)
+    dev = dpr.Device.create(0, 1, 0)
+    try:
+        with pytest.raises(dpr.DprError) as e:
+            dev.commit_part(big)
+        assert e.value.code == -1 and "rows" in str(e.value)
+    finally:
+        dev.release()
