@@ -1052,6 +1052,7 @@ int ensure_mbox(Dev *d) {
     return DPR_OK;
 }
 
+constexpr int FUSED_UNAVAILABLE = 1;  // fused_peers: no peer mappings on some rank (all ranks agree)
 int fused_peers(std::vector<Dev *> &L) {
     Dev *d0 = L[0];
     const int N = d0->nranks;
@@ -1102,7 +1103,8 @@ int fused_peers(std::vector<Dev *> &L) {
     for (void *p : d->ipc_opened) cudaIpcCloseMemHandle(p);
     d->ipc_opened.clear();
     const IpcMsg *all = reinterpret_cast<const IpcMsg *>(out[0].data());
-    for (int r = 0; r < N; ++r) {
+    cudaError_t open_err = cudaSuccess;
+    for (int r = 0; r < N && open_err == cudaSuccess; ++r) {
         void *ptr[IPC_NBUF + 1];
         void *opened[IPC_NBUF + 1];  // one mapping per distinct allocation of the peer
         for (int k = 0; k <= IPC_NBUF; ++k) {
@@ -1113,11 +1115,13 @@ int fused_peers(std::vector<Dev *> &L) {
                 if (opened[j] && memcmp(&all[r].h[j], &all[r].h[k], sizeof(cudaIpcMemHandle_t)) == 0)
                     opened[k] = opened[j];
             if (!opened[k]) {
-                CK(cudaIpcOpenMemHandle(&opened[k], all[r].h[k], cudaIpcMemLazyEnablePeerAccess));
+                open_err = cudaIpcOpenMemHandle(&opened[k], all[r].h[k], cudaIpcMemLazyEnablePeerAccess);
+                if (open_err != cudaSuccess) break;
                 d->ipc_opened.push_back(opened[k]);
             }
             ptr[k] = (char *)opened[k] + all[r].off[k];
         }
+        if (open_err != cudaSuccess) break;
         d->peer_path[0][r] = (PathRec *)ptr[0];
         d->peer_path[1][r] = (PathRec *)ptr[1];
         d->peer_occl[0][r] = (OcclRec *)ptr[2];
@@ -1127,6 +1131,29 @@ int fused_peers(std::vector<Dev *> &L) {
         d->peer_fb[r] = (float4 *)ptr[6];
         d->peer_events[r] = (uint32_t *)ptr[7];
         d->peer_occl_dump[r] = (uint32_t *)ptr[8];
+    }
+    // every rank learns whether every rank mapped every peer: if one could not (no peer access
+    // between some pair of GPUs), all ranks switch to the send/recv exchange together
+    {
+        (void)cudaGetLastError();
+        // test hook: DPR_TEST_FUSED_FAIL=<rank> makes that rank report a failed mapping
+        if (const char *e = getenv("DPR_TEST_FUSED_FAIL"))
+            if (atoi(e) == d->rank) open_err = cudaErrorPeerAccessUnsupported;
+        const int ok = open_err == cudaSuccess ? 1 : 0;
+        std::vector<const void *> sg = {&ok};
+        std::vector<std::vector<char>> so;
+        RET(allgather_host(L, sg, sizeof(int), so));
+        bool all_ok = true;
+        for (int r = 0; r < N; ++r) all_ok = all_ok && reinterpret_cast<const int *>(so[0].data())[r] != 0;
+        if (!all_ok) {
+            for (void *p : d->ipc_opened) cudaIpcCloseMemHandle(p);
+            d->ipc_opened.clear();
+            d->ipc_sig = 0;
+            if (d->has_hc)  // the host-collective transport has no other data plane
+                return fail(DPR_ERR_CUDA, std::string("fused exchange: peer mapping failed: ") +
+                                              cudaGetErrorString(open_err == cudaSuccess ? cudaErrorPeerAccessUnsupported : open_err));
+            return FUSED_UNAVAILABLE;
+        }
     }
     d->ipc_sig = all_sig;
     return DPR_OK;
@@ -1479,8 +1506,18 @@ int render_group(std::vector<Dev *> &L) {
         RET(frame_setup(L, fc));
         for (Dev *d : L) RET(frame_buffers(d, fc));
     }
-    const bool fused = d0->exch != 0;
-    if (fused) RET(fused_peers(L));
+    bool fused = d0->exch != 0;
+    if (fused) {
+        const int rc = fused_peers(L);
+        if (rc == FUSED_UNAVAILABLE) {
+            // collective fallback (decided identically on every rank): NCCL send/recv from now on
+            for (Dev *d : L) d->exch = 0;
+            for (Dev *d : L) RET(frame_buffers(d, fc));
+            fused = false;
+        } else {
+            RET(rc);
+        }
+    }
     // device-driven step loop: fused exchange, not the host-collective transport
     const bool dev_loop = fused && d0->step_loop && !d0->has_hc;
     const bool barrier = dev_loop && !d0->group && (N > 1 || d0->comm);

@@ -89,6 +89,22 @@ def test_nccl_collectives_single_rank(mode, monkeypatch):
     assert_parity(g, o)
 
 
+def test_fused_exchange_falls_back_to_sendrecv(monkeypatch):
+    """When some rank cannot map its peers' queues (no peer access between two GPUs; injected:
+    DPR_TEST_FUSED_FAIL=<rank>), every rank agrees through one allgather and the frame runs on
+    the NCCL send/recv exchange instead (host step loop), with the same parity."""
+    monkeypatch.setenv("DPR_FORCE_NCCL", "1")
+    monkeypatch.setenv("DPR_EXCHANGE", "fused")
+    monkeypatch.setenv("DPR_STEP_LOOP", "device")
+    monkeypatch.setenv("DPR_TEST_FUSED_FAIL", "0")
+    sc = di.config1()
+    parts = di.union_parts(sc.parts)
+    g = gpu_render(parts, 1, sc.camera, sc.frame, frames=2)
+    o = oracle_render(parts, 1, sc.camera, sc.frame)
+    assert_parity(g, o)
+    assert g[3]["step_loop_device"] == 0
+
+
 def test_config4_full_size_sampled():
     """configs[3] at full size on one rank (50M spheres in 1000 cluster parts + ~5M
     triangles, 1920x1080, depth 4): every event/occlusion bit of 1500 sampled pixels."""
