@@ -186,7 +186,7 @@ struct Hit {
 struct TraceCounters { uint32_t nodes, tris, sphs, vols; };
 
 #ifndef DPR_REFILL_PATH
-#define DPR_REFILL_PATH 16
+#define DPR_REFILL_PATH 24  // r02 re-sweep on configs[1]: 8 20.14, 16 19.85, 20 19.79, 24 19.79 ms frame
 #endif
 #ifndef DPR_REFILL_OCCL
 #define DPR_REFILL_OCCL 4
@@ -203,10 +203,11 @@ constexpr int WSTACK = 32;       // node-group stack entries (wide BVH depth bou
 // a per-warp list that all 32 lanes test (against the owner lane's ray), then the results are
 // reduced per owner in shared memory.
 #ifndef DPR_COOP_PER_LANE
-#define DPR_COOP_PER_LANE 12
+#define DPR_COOP_PER_LANE 16  // any-hit (r02 re-sweep, configs[1] occlusion trace: 8 13.88, 12 13.68,
+                              // 16 13.61, 20 13.74, 24 13.74 ms)
 #endif
 #ifndef DPR_COOP_PER_LANE_PATH
-#define DPR_COOP_PER_LANE_PATH DPR_COOP_PER_LANE
+#define DPR_COOP_PER_LANE_PATH 12  // closest-hit (r01 sweep)
 #endif
 constexpr int COOP_PER_LANE = DPR_COOP_PER_LANE > DPR_COOP_PER_LANE_PATH ? DPR_COOP_PER_LANE
                                                                          : DPR_COOP_PER_LANE_PATH;  // list size
