@@ -875,7 +875,12 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
             }
         }
         unsigned used_slots = 0, done_child = 0;
-        for (int k = 0; k < nc; ++k) {
+        // lazy greedy: a child's cached (cost, slot) is an upper bound of its best free slot
+        // (costs only fall as slots fill); the largest cached entry is assigned if its slot is
+        // still free, else recomputed and the selection repeated -- the same greedy choice,
+        // recomputing only the children that come up instead of every child that lost a slot
+        // (configs[3] build 12.44 -> 12.03 ms, r02)
+        for (int k = 0; k < nc;) {
             float bc = -3.4e38f;
             int bi = 0, bs = 0;
 #pragma unroll
@@ -883,15 +888,18 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
                 if (i >= nc || (done_child >> i & 1)) continue;
                 if (bcst[i] > bc) { bc = bcst[i]; bi = i; bs = bsl[i]; }
             }
+            if (used_slots >> bs & 1) {
+                float nc_; int ns_;
+                best_free(bi, used_slots, nc_, ns_);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) if (i == bi) { bcst[i] = nc_; bsl[i] = ns_; }
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i) if (i == bi) slot_of[i] = bs;
             used_slots |= 1u << bs;
             done_child |= 1u << bi;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (i >= nc || (done_child >> i & 1) || bsl[i] != bs) continue;
-                best_free(i, used_slots, bcst[i], bsl[i]);
-            }
+            ++k;
         }
     }
     // internal vs leaf children, allocation
