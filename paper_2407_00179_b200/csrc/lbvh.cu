@@ -845,8 +845,15 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
     // recomputed only when another child takes it
     int slot_of[8];
     {
-        float bcst[8];
-        int bsl[8];
+        // candidate keys: the cost as an order-preserving integer with its low 6 bits replaced by
+        // (slot << 3) | (7 - child), so one integer max picks the child (ties: lowest index)
+        // and carries its slot; 0 = assigned / absent
+        uint32_t pk[8];
+        auto pack = [](float c, int sl, int i) -> uint32_t {
+            const uint32_t u = __float_as_uint(c);
+            const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+            return (o & ~63u) | ((uint32_t)sl << 3) | (uint32_t)(7 - i);
+        };
         // (a variant walking a child's slots in falling cost order -- its octant with the sign
         // flips ordered by the flipped |offset| sum -- ran slower: 13.7 vs 12.8 ms per
         // configs[3] build, r02)
@@ -865,40 +872,37 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
         // |dx| + |dy| + |dz|
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            slot_of[i] = 0; bcst[i] = -3.4e38f; bsl[i] = 0;
+            slot_of[i] = 0; pk[i] = 0;
             if (i < nc) {
                 float dc[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) dc[c] = (S.lo[c][i][tid] + S.hi[c][i][tid]) - (nlo_[c] + nhi_[c]);
-                bcst[i] = (fabsf(dc[0]) + fabsf(dc[1])) + fabsf(dc[2]);
-                bsl[i] = (dc[0] > 0.0f ? 4 : 0) | (dc[1] > 0.0f ? 2 : 0) | (dc[2] > 0.0f ? 1 : 0);
+                pk[i] = pack((fabsf(dc[0]) + fabsf(dc[1])) + fabsf(dc[2]),
+                             (dc[0] > 0.0f ? 4 : 0) | (dc[1] > 0.0f ? 2 : 0) | (dc[2] > 0.0f ? 1 : 0), i);
             }
         }
-        unsigned used_slots = 0, done_child = 0;
+        unsigned used_slots = 0;
         // lazy greedy: a child's cached (cost, slot) is an upper bound of its best free slot
         // (costs only fall as slots fill); the largest cached entry is assigned if its slot is
         // still free, else recomputed and the selection repeated -- the same greedy choice,
         // recomputing only the children that come up instead of every child that lost a slot
         // (configs[3] build 12.44 -> 12.03 ms, r02)
         for (int k = 0; k < nc;) {
-            float bc = -3.4e38f;
-            int bi = 0, bs = 0;
+            uint32_t m = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (i >= nc || (done_child >> i & 1)) continue;
-                if (bcst[i] > bc) { bc = bcst[i]; bi = i; bs = bsl[i]; }
-            }
+            for (int i = 0; i < 8; ++i) m = max(m, pk[i]);
+            const int bi = 7 - (int)(m & 7u), bs = (int)((m >> 3) & 7u);
             if (used_slots >> bs & 1) {
                 float nc_; int ns_;
                 best_free(bi, used_slots, nc_, ns_);
+                const uint32_t nk = pack(nc_, ns_, bi);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) if (i == bi) { bcst[i] = nc_; bsl[i] = ns_; }
+                for (int i = 0; i < 8; ++i) if (i == bi) pk[i] = nk;
                 continue;
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) if (i == bi) slot_of[i] = bs;
+            for (int i = 0; i < 8; ++i) if (i == bi) { slot_of[i] = bs; pk[i] = 0; }
             used_slots |= 1u << bs;
-            done_child |= 1u << bi;
             ++k;
         }
     }
