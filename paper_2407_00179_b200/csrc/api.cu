@@ -645,7 +645,7 @@ int build_world(Dev *d) {
             if (L >= MAXL) return fail(DPR_ERR_STATE, "wide BVH deeper than the collapse level limit");
             for (int k = L; k < L + B; ++k) {
                 launch_collapse_level(ca, P<int2>(d->b_witems[k & 1]), lvl + k, P<int2>(d->b_witems[(k + 1) & 1]),
-                                      lvl + k + 1, s);
+                                      lvl + k + 1, k, s);
                 launches++;
             }
             CK(cudaMemcpyAsync(h_cnt, cnt, sizeof(int) * (4 + L + B + 1), cudaMemcpyDeviceToHost, s));

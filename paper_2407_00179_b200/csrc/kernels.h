@@ -63,7 +63,7 @@ struct CollapseArgs {
 };
 // one BFS level of the collapse: *cnt_in items (device memory) -> next, appending to *cnt_out
 void launch_collapse_level(const CollapseArgs &a, const int2 *items, const int *cnt_in, int2 *next, int *cnt_out,
-                           cudaStream_t s);
+                           int level, cudaStream_t s);
 void launch_permute_prims(const float4 *in, const uint32_t *perm, const uint32_t *sortperm, int64_t n,
                           float4 *out, cudaStream_t s);
 // ---- ploc.cu: PLOC binary builder (Meister & Bittner 2018) ------------------------------

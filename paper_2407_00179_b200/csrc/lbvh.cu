@@ -1046,8 +1046,11 @@ int collapse_grid() {
     return g;
 }
 void launch_collapse_level(const CollapseArgs &a, const int2 *items, const int *cnt_in, int2 *next, int *cnt_out,
-                           cudaStream_t s) {
-    const int g = collapse_grid();
+                           int level, cudaStream_t s) {
+    // level k holds at most 8^k wide nodes: the first levels get a grid of that size instead
+    // of the resident grid (a 7K-block launch that finds one item costs ~20 us)
+    int g = collapse_grid();
+    if (level < 8) g = std::min<int64_t>(g, std::max<int64_t>(1, (((int64_t)1 << (3 * level)) + CB - 1) / CB));
     k_collapse_r<<<g, CB, sizeof(CollapseSmem), s>>>(a, items, cnt_in, next, cnt_out);
 }
 
