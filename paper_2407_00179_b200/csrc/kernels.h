@@ -217,11 +217,14 @@ void launch_shade_path(const StepArgs &a, int grid, cudaStream_t s);
 void launch_resolve_occl(const StepArgs &a, int grid, cudaStream_t s);
 int trace_path_occupancy(int block);
 int trace_occl_occupancy(int block);
-constexpr int TRACE_BLOCK = 128;
-#ifndef DPR_TRACE_MINB
-#define DPR_TRACE_MINB 8
+#ifndef DPR_TRACE_BLOCK
+#define DPR_TRACE_BLOCK 256  // r02 re-sweep (configs[1] frame): 64 19.96, 128 19.75, 256 19.66 ms
 #endif
-constexpr int TRACE_MINB = DPR_TRACE_MINB;  // 8 x 128 threads per SM -> <= 64 registers (sweep r01)
+constexpr int TRACE_BLOCK = DPR_TRACE_BLOCK;
+#ifndef DPR_TRACE_MINB
+#define DPR_TRACE_MINB (1024 / DPR_TRACE_BLOCK)
+#endif
+constexpr int TRACE_MINB = DPR_TRACE_MINB;  // 1024 threads per SM -> <= 64 registers (sweep r01)
 
 void launch_fb_accumulate(float4 *dst, const float4 *src, int64_t n, cudaStream_t s);
 void launch_u32_accumulate(uint32_t *dst, const uint32_t *src, int64_t n, cudaStream_t s);

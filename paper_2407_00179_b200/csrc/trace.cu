@@ -260,12 +260,12 @@ __device__ __forceinline__ f3 ray_id(int t) { return mk(s_ray[6][t], s_ray[7][t]
 #define RAY_ID(S) (S).id3
 #endif
 #ifndef DPR_SM_STACK
-#define DPR_SM_STACK 4
+#define DPR_SM_STACK 5  // r02 re-sweep with 256-thread CTAs: 3 19.89, 4 19.75, 5 19.64, 6 19.83 ms
 #endif
 #if DPR_SM_STACK > 0
 // the first DPR_SM_STACK node-group stack entries of each thread in shared memory (SoA; sweep
 // r01_smstack: 3 best at first, 14.67 -> 14.51 ms occlusion trace on configs[1]; 4 after the
-// traversal-order table, r01_v12), deeper entries in local memory
+// traversal-order table, r01_v12; 5 with 256-thread CTAs, r02), deeper entries in local memory
 __shared__ uint2 s_stack[DPR_SM_STACK][TRACE_BLOCK];
 #ifndef DPR_LEAF_BF
 #define DPR_LEAF_BF 0
