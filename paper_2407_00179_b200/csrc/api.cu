@@ -459,12 +459,12 @@ int build_world(Dev *d) {
             RET(ensure(d, d->b_keys[i], sizeof(mkey_t) * n + 64));  // + the agglomeration fetch counter
             RET(ensure(d, d->b_vals[i], sizeof(uint32_t) * n));
         }
-        launch_morton(P<float4>(d->b_blo), P<float4>(d->b_blo) + 1, n, P<int>(d->b_bounds),
-                      P<mkey_t>(d->b_keys[0]), P<uint32_t>(d->b_vals[0]), s);
         RET(ensure(d, d->b_hist, sizeof(unsigned long long) * MKEY_DIGITS * 256));
         CK(cudaMemsetAsync(d->b_hist.p, 0, sizeof(unsigned long long) * MKEY_DIGITS * 256, s));
-        launch_digit_hist_all(P<mkey_t>(d->b_keys[0]), n, P<unsigned long long>(d->b_hist), d->nsm, s);
-        launches += 2;
+        RET(ensure(d, d->b_tile, sizeof(uint32_t) * 256 * (radix_tiles(n) + 1)));
+        launch_morton_h(P<float4>(d->b_blo), P<float4>(d->b_blo) + 1, n, P<int>(d->b_bounds), P<mkey_t>(d->b_keys[0]),
+                        P<uint32_t>(d->b_vals[0]), P<uint32_t>(d->b_tile), P<unsigned long long>(d->b_hist), s);
+        launches += 1;
         CK(cudaMemcpyAsync(hist.data(), d->b_hist.p, sizeof(unsigned long long) * MKEY_DIGITS * 256,
                            cudaMemcpyDeviceToHost, s));
     }
@@ -513,15 +513,14 @@ int build_world(Dev *d) {
     if (n > 0) {
         // LSD radix sort; constant-digit passes skipped (order preserved by stability)
         int cur = 0;
-        int64_t ntiles = radix_tiles(n);
-        RET(ensure(d, d->b_tile, sizeof(uint32_t) * 256 * (ntiles + 1)));
         for (int pass = 0; pass < MKEY_DIGITS; ++pass) {
             bool constant = false;
             for (int b = 0; b < 256; ++b) if (hist[pass * 256 + b] == (unsigned long long)n) constant = true;
             if (constant) continue;
+            // pass 0's tile histogram came with the Morton codes (keys still in input order)
             launch_radix_pass(P<mkey_t>(d->b_keys[cur]), P<uint32_t>(d->b_vals[cur]),
                               P<mkey_t>(d->b_keys[cur ^ 1]), P<uint32_t>(d->b_vals[cur ^ 1]), n,
-                              8 * pass, P<uint32_t>(d->b_tile), s, &launches);
+                              8 * pass, P<uint32_t>(d->b_tile), s, &launches, pass == 0);
             cur ^= 1;
         }
         mkey_t *keys = P<mkey_t>(d->b_keys[cur]);

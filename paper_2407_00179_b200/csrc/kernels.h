@@ -24,14 +24,15 @@ struct PrimChunk {
 constexpr int PRIM_CHUNK = 4096;
 void launch_part_prims(const PrimChunk *chunks, int nchunks, float4 *prims, float4 *blo, float4 *bhi, int *bounds,
                        int *bad_index, cudaStream_t s);
-void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
-                   mkey_t *keys, uint32_t *vals, cudaStream_t s);
-void launch_digit_hist_all(const mkey_t *keys, int64_t n, unsigned long long *hist, int nsm,
-                           cudaStream_t s);
 int64_t radix_tiles(int64_t n);
 void launch_iota(uint32_t *v, int64_t n, cudaStream_t s);  // v[i] = i (the sort test's values)
 void launch_radix_pass(const mkey_t *kin, const uint32_t *vin, mkey_t *kout, uint32_t *vout,
-                       int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches);
+                       int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches,
+                       bool hist_ready = false);  // hist_ready: tile_hist already holds this pass's tile counts
+// Morton codes fused with the first pass's tile histogram and all digits' totals (hist_all,
+// zeroed by the caller)
+void launch_morton_h(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds, mkey_t *keys, uint32_t *vals,
+                     uint32_t *tile_hist0, unsigned long long *hist_all, cudaStream_t s);
 void launch_karras(const mkey_t *keys, int64_t n, int *left, int *right, int *parent, int *rlo,
                    int *rhi, int *size, cudaStream_t s);
 void launch_refit(int64_t n, const int *left, const int *right, const int *parent,

@@ -149,24 +149,6 @@ __device__ __forceinline__ uint32_t expand10(uint32_t v) {  // bit i -> bit 3i (
     return v;
 }
 
-__global__ void k_morton(const float4 *__restrict__ blo, const float4 *__restrict__ bhi, int64_t n,
-                         const int *__restrict__ bounds, mkey_t *keys, uint32_t *vals) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float4 lo = blo[2 * i], hi = bhi[2 * i];
-    float c[3] = {(lo.x + hi.x) * 0.5f, (lo.y + hi.y) * 0.5f, (lo.z + hi.z) * 0.5f};
-    uint32_t q[3];
-    for (int a = 0; a < 3; ++a) {
-        float mn = ord2f(bounds[6 + a]), mx = ord2f(bounds[9 + a]);
-        float ext = mx - mn;
-        const float cells = (float)(1u << DPR_MORTON_BITS);
-        float x = ext > 0.0f ? (c[a] - mn) / ext * cells : 0.0f;
-        x = fminf(fmaxf(x, 0.0f), cells - 1.0f);
-        q[a] = (uint32_t)x;
-    }
-    keys[i] = (expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]);
-    vals[i] = (uint32_t)i;
-}
 
 // ---------------------------------------------------------------------------------------
 // LSD radix sort, 8-bit digits.
@@ -178,20 +160,49 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_ITEMS = DPR_RS_ITEMS;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 
-// All 8 digit histograms in one read of the keys (to find constant-digit passes).
-__global__ void k_digit_hist_all(const mkey_t *__restrict__ keys, int64_t n,
-                                 unsigned long long *hist /*MKEY_DIGITS*256*/) {
+
+// Morton codes of one radix tile per block (RS_TILE keys), fused with the sort's histograms:
+// the tile's digit-0 counts (the first pass's tile histogram) and all digits' totals (constant-
+// digit detection and the passes' digit totals), so neither needs its own read of the keys.
+__global__ void __launch_bounds__(RS_THREADS) k_morton_h(const float4 *__restrict__ blo, const float4 *__restrict__ bhi,
+                                                          int64_t n, const int *__restrict__ bounds, mkey_t *keys,
+                                                          uint32_t *vals, uint32_t *tile_hist0, int ntiles,
+                                                          unsigned long long *hist_all) {
     __shared__ unsigned int h[MKEY_DIGITS][256];
     for (int i = threadIdx.x; i < MKEY_DIGITS * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+    float mn[3], sc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        mn[a] = ord2f(bounds[6 + a]);
+        sc[a] = ord2f(bounds[9 + a]) - mn[a];
+    }
     __syncthreads();
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const mkey_t k = keys[i];
+    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const int64_t i = base + j * RS_THREADS + threadIdx.x;
+        if (i >= n) break;
+        const float4 lo = blo[2 * i], hi = bhi[2 * i];
+        const float c[3] = {(lo.x + hi.x) * 0.5f, (lo.y + hi.y) * 0.5f, (lo.z + hi.z) * 0.5f};
+        uint32_t q[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float ext = sc[a];
+            const float cells = (float)(1u << DPR_MORTON_BITS);
+            float x = ext > 0.0f ? (c[a] - mn[a]) / ext * cells : 0.0f;
+            x = fminf(fmaxf(x, 0.0f), cells - 1.0f);
+            q[a] = (uint32_t)x;
+        }
+        const mkey_t k = (expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]);
+        keys[i] = k;
+        vals[i] = (uint32_t)i;
+#pragma unroll
         for (int p = 0; p < MKEY_DIGITS; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255], 1u);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < MKEY_DIGITS * 256; i += blockDim.x)
-        if ((&h[0][0])[i]) atomicAdd(&hist[i], (unsigned long long)(&h[0][0])[i]);
+    tile_hist0[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[0][threadIdx.x];
+#pragma unroll
+    for (int p = 0; p < MKEY_DIGITS; ++p)
+        if (h[p][threadIdx.x]) atomicAdd(&hist_all[p * 256 + threadIdx.x], (unsigned long long)h[p][threadIdx.x]);
 }
 
 __global__ void k_tile_hist(const mkey_t *__restrict__ keys, int64_t n, int shift,
@@ -1172,15 +1183,12 @@ void launch_part_prims(const PrimChunk *chunks, int nchunks, float4 *prims, floa
                        int *bad_index, cudaStream_t s) {
     if (nchunks > 0) k_part_prims<<<nchunks, 256, 0, s>>>(chunks, prims, blo, bhi, bounds, bad_index);
 }
-void launch_morton(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds,
-                   mkey_t *keys, uint32_t *vals, cudaStream_t s) {
-    if (n > 0) k_morton<<<nblk(n, 256), 256, 0, s>>>(blo, bhi, n, bounds, keys, vals);
-}
-void launch_digit_hist_all(const mkey_t *keys, int64_t n, unsigned long long *hist, int nsm,
-                           cudaStream_t s) {
-    unsigned g = (unsigned)std::min<int64_t>(nblk(n, 256), (int64_t)nsm * 4);
-    if (g == 0) g = 1;
-    k_digit_hist_all<<<g, 256, 0, s>>>(keys, n, hist);
+void launch_morton_h(const float4 *blo, const float4 *bhi, int64_t n, const int *bounds, mkey_t *keys, uint32_t *vals,
+                     uint32_t *tile_hist0, unsigned long long *hist_all, cudaStream_t s) {
+    if (n > 0) {
+        const int ntiles = (int)radix_tiles(n);
+        k_morton_h<<<ntiles, RS_THREADS, 0, s>>>(blo, bhi, n, bounds, keys, vals, tile_hist0, ntiles, hist_all);
+    }
 }
 int64_t radix_tiles(int64_t n) { return (n + RS_TILE - 1) / RS_TILE; }
 __global__ void k_iota(uint32_t *v, int64_t n) {
@@ -1191,10 +1199,11 @@ void launch_iota(uint32_t *v, int64_t n, cudaStream_t s) {
     if (n > 0) k_iota<<<nblk(n, 256), 256, 0, s>>>(v, n);
 }
 void launch_radix_pass(const mkey_t *kin, const uint32_t *vin, mkey_t *kout, uint32_t *vout,
-                       int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches) {
+                       int64_t n, int shift, uint32_t *tile_hist, cudaStream_t s, int *launches, bool hist_ready) {
     int ntiles = (int)radix_tiles(n);
     uint32_t *digit_tot = tile_hist + (int64_t)256 * ntiles;  // 256 extra words
-    k_tile_hist<<<ntiles, RS_THREADS, 0, s>>>(kin, n, shift, tile_hist, ntiles);
+    if (!hist_ready) k_tile_hist<<<ntiles, RS_THREADS, 0, s>>>(kin, n, shift, tile_hist, ntiles);
+    else *launches -= 1;
     k_scan_digits<<<256, 1024, 0, s>>>(tile_hist, ntiles, digit_tot);
 #ifndef DPR_SCATTER_COALESCED
 #define DPR_SCATTER_COALESCED 2  // 2 warp-ranked, 1 ranked per round, 0 direct

@@ -18,7 +18,7 @@ done
 bash tools/ncu_capture.sh $TAG c2 "regex:k_trace" 2 2 "k_trace_occl k_trace_path"
 bash tools/ncu_capture.sh $TAG c3 "regex:k_trace|k_march" 2 3 "k_trace_path k_march_occl"
 bash tools/ncu_capture.sh $TAG c4 "regex:k_trace_path" 0 8 "k_trace_path"
-bash tools/ncu_capture.sh $TAG c4b "regex:k_collapse_r|k_agglo_p|k_permute_prims|k_scatter_w|k_part_prims|k_gather_prims|k_tile_hist|k_morton" 0 30 "k_collapse_r k_agglo_p" python tools/build_only.py c4 1
+bash tools/ncu_capture.sh $TAG c4b "regex:k_collapse_r|k_agglo_p|k_permute_prims|k_scatter_w|k_part_prims|k_gather_prims|k_tile_hist|k_morton_h" 0 30 "k_collapse_r k_agglo_p" python tools/build_only.py c4 1
 # ncu source pages run to tens of MB: compressed so gpurun_out stays under the return cap
 find gpurun_out -name "${TAG}_*.csv" -size +1M -exec gzip -f {} \;
 ls -la gpurun_out | grep $TAG
