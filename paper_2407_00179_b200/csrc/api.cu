@@ -452,25 +452,23 @@ int build_world(Dev *d) {
                           P<float4>(d->b_blo) + 1, P<int>(d->b_bounds), P<int>(d->b_bounds) + 12 * (np + 1), s);
         launches++;
     }
-    // Morton keys + all digit histograms
-    std::vector<unsigned long long> hist(MKEY_DIGITS * 256, 0);
+    // Morton keys (+ the first radix pass's tile histogram)
     if (n > 0) {
         for (int i = 0; i < 2; ++i) {
             RET(ensure(d, d->b_keys[i], sizeof(mkey_t) * n + 64));  // + the agglomeration fetch counter
             RET(ensure(d, d->b_vals[i], sizeof(uint32_t) * n));
         }
-        RET(ensure(d, d->b_hist, sizeof(unsigned long long) * MKEY_DIGITS * 256));
-        CK(cudaMemsetAsync(d->b_hist.p, 0, sizeof(unsigned long long) * MKEY_DIGITS * 256, s));
         RET(ensure(d, d->b_tile, sizeof(uint32_t) * 256 * (radix_tiles(n) + 1)));
         launch_morton_h(P<float4>(d->b_blo), P<float4>(d->b_blo) + 1, n, P<int>(d->b_bounds), P<mkey_t>(d->b_keys[0]),
-                        P<uint32_t>(d->b_vals[0]), P<uint32_t>(d->b_tile), P<unsigned long long>(d->b_hist), s);
+                        P<uint32_t>(d->b_vals[0]), P<uint32_t>(d->b_tile), nullptr, s);
         launches += 1;
-        CK(cudaMemcpyAsync(hist.data(), d->b_hist.p, sizeof(unsigned long long) * MKEY_DIGITS * 256,
-                           cudaMemcpyDeviceToHost, s));
     }
+    // part bounds + validation flags: read back without a wait here; checked after the build's
+    // first host synchronisation (the collapse level counts), so the GPU runs the whole build
+    // without draining in between (a failed check then leaves no world, as before)
     std::vector<int> bnd(12 * (np + 1) + 1);
     CK(cudaMemcpyAsync(bnd.data(), d->b_bounds.p, bnd.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    auto finish_bounds = [&]() -> int {
     if (bnd[12 * (np + 1)] & 1) return fail(DPR_ERR_INVALID_ARG, "triangle index out of range (checked on the GPU)");
     if (bnd[12 * (np + 1)] & 2)
         return fail(DPR_ERR_INVALID_ARG, "non-finite vertex / sphere, or sphere radius <= 0 (checked on the GPU)");
@@ -510,13 +508,12 @@ int build_world(Dev *d) {
     if ((int)d->local_parts.size() > MAXP) return fail(DPR_ERR_INVALID_ARG, "too many parts on one rank");
     d->nonempty = lo[0] <= hi[0];
     for (int c = 0; c < 3; ++c) { d->box[c] = lo[c]; d->box[3 + c] = hi[c]; }
+    return DPR_OK;
+    };
     if (n > 0) {
-        // LSD radix sort; constant-digit passes skipped (order preserved by stability)
+        // LSD radix sort, all four passes (a constant digit is an identity pass: stable)
         int cur = 0;
         for (int pass = 0; pass < MKEY_DIGITS; ++pass) {
-            bool constant = false;
-            for (int b = 0; b < 256; ++b) if (hist[pass * 256 + b] == (unsigned long long)n) constant = true;
-            if (constant) continue;
             // pass 0's tile histogram came with the Morton codes (keys still in input order)
             launch_radix_pass(P<mkey_t>(d->b_keys[cur]), P<uint32_t>(d->b_vals[cur]),
                               P<mkey_t>(d->b_keys[cur ^ 1]), P<uint32_t>(d->b_vals[cur ^ 1]), n,
@@ -653,6 +650,7 @@ int build_world(Dev *d) {
             for (int k = L; k <= L + B; ++k)
                 if (h_cnt[4 + k] == 0) { levels = k; break; }
         }
+        RET(finish_bounds());
         if (h_cnt[2] != n) return fail(DPR_ERR_STATE, "wide BVH collapse lost primitives");
         launch_permute_prims(P<float4>(d->b_prims_u), P<uint32_t>(d->b_wperm), perm, n, P<float4>(d->b_prims_w), s);
         launches++;
@@ -662,6 +660,9 @@ int build_world(Dev *d) {
                 (double)h_cnt[0] / h_cnt[1], (double)n / (h_cnt[0] - (h_cnt[1] - 1)));
 #endif
         d->bvh_levels = levels;
+    } else {
+        CK(cudaStreamSynchronize(s));
+        RET(finish_bounds());
     }
     // bricks: macrocells
     for (auto &p : d->parts) {

@@ -195,14 +195,19 @@ __global__ void __launch_bounds__(RS_THREADS) k_morton_h(const float4 *__restric
         const mkey_t k = (expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]);
         keys[i] = k;
         vals[i] = (uint32_t)i;
+        if (hist_all) {
 #pragma unroll
-        for (int p = 0; p < MKEY_DIGITS; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255], 1u);
+            for (int p = 1; p < MKEY_DIGITS; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255], 1u);
+        }
+        atomicAdd(&h[0][k & 255], 1u);
     }
     __syncthreads();
     tile_hist0[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[0][threadIdx.x];
+    if (hist_all) {
 #pragma unroll
-    for (int p = 0; p < MKEY_DIGITS; ++p)
-        if (h[p][threadIdx.x]) atomicAdd(&hist_all[p * 256 + threadIdx.x], (unsigned long long)h[p][threadIdx.x]);
+        for (int p = 0; p < MKEY_DIGITS; ++p)
+            if (h[p][threadIdx.x]) atomicAdd(&hist_all[p * 256 + threadIdx.x], (unsigned long long)h[p][threadIdx.x]);
+    }
 }
 
 __global__ void k_tile_hist(const mkey_t *__restrict__ keys, int64_t n, int shift,
