@@ -2,19 +2,22 @@
 //
 // The paper's method needs only "negligible pre-processing" (S2.2): each rank
 // builds a local structure over its own parts.  B200 has no RT cores, so the
-// structure and its traversal are hand-written: a linear BVH (Karras 2012, "Maximizing
-// parallelism in the construction of BVHs, octrees and k-d trees"):
+// structure and its traversal are hand-written: a linear BVH (Karras 2012; built bottom-up in
+// one pass after Apetrei 2014), collapsed into a compressed 8-wide BVH:
 //   1. k_part_prims: prim records + exact AABBs (min/max, no rounding) of every part in one
 //      launch (one block per chunk), and in the same pass each part's and the rank's box and
 //      centroid box (order-preserving integer atomics after a block reduction)
-//   3. k_morton: 63-bit Morton code of the centroid (21 bits per axis)
-//   4. LSD radix sort of (key u64, index u32), 8-bit digits, stable per-tile ranking with
-//      warp match + shared-memory digit prefix; passes whose digit is constant are skipped
-//   5. k_karras: internal nodes, duplicate keys broken by index
-//   6. k_refit: bottom-up boxes with arrival counters
-//   7. k_collapse: compressed 8-wide nodes (WNode) by greedy opening of the largest child,
-//      child boxes padded outward then quantised outward (conservative traversal)
-//   8. k_macrocells: per 16^3 macrocell "alpha may be > 0" flags for exact empty-space
+//   2. k_morton_h: 30-bit Morton code of the centroid (10 bits per axis) in a 32-bit key,
+//      one radix tile per block, with the first pass's tile histogram
+//   3. LSD radix sort of (key u32, index u32): 4 passes of 8-bit digits, warp-ranked stable
+//      scatter staged in shared memory (k_tile_hist, k_scan_digits, k_scatter_w)
+//   4. k_split_delta + k_agglo_p: agglomerative radix tree (persistent, 64-bit exchange words),
+//      packed 32-byte node records (k_karras + k_refit and PLOC selectable)
+//   5. k_collapse_r: compressed 8-wide nodes (WNode) by greedy opening of the largest child,
+//      child boxes padded outward then quantised outward (conservative traversal), octant
+//      slots by a lazy greedy; one BFS level per launch
+//   6. k_permute_prims: prim records into wide-leaf order
+//   7. k_macrocells: per 16^3 macrocell "alpha may be > 0" flags for exact empty-space
 //      skipping in bricks
 #include <algorithm>
 #include <cstdlib>
