@@ -780,12 +780,14 @@ constexpr int CB = 128;  // collapse block
 // threads read the same child slot of consecutive threads), so a child is inserted with one
 // store per field at a dynamic index instead of unrolled selects over 8 register slots (those
 // selects were most of the register version's instructions at 164 registers / 18% occupancy).
-// Kept in registers: each child's argmax key (box area) and the internal / large bit masks;
+// Also in shared memory: each child's argmax key (box area; 8 register selects per insert
+// before, configs[3] build 11.78 -> 11.66 ms); in registers: the internal / large bit masks;
 // the capped sizes ride in the top bits of ccl.
 struct CollapseSmem {
     int cid[8][CB];
     uint32_t ccl[8][CB], ccr[8][CB];
     float lo[3][8][CB], hi[3][8][CB];
+    uint32_t akey[8][CB];  // argmax keys: box area | 8 | (7 - child)
 };
 
 __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const CollapseArgs a, const int2 *__restrict__ items,
@@ -805,10 +807,9 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
     // argmax keys: box area with the low 4 mantissa bits replaced by 8 | (7 - i) (> 0, ties
     // to the lowest child index); bit masks of internal children and of those with more than
     // LEAF_MAX prims; sizes live in the top bits of ccl
-    uint32_t akey[8];
     unsigned inner_m = 0, big_m = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) akey[i] = 0;
+    for (int i = 0; i < 8; ++i) S.akey[i][tid] = 0;
     auto put = [&](int i, int id) -> void {  // load child id into slot i (smem + registers)
         float lo3[3], hi3[3];
         uint32_t cl, cr;
@@ -819,9 +820,7 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
         const float ex = hi3[0] - lo3[0], ey = hi3[1] - lo3[1], ez = hi3[2] - lo3[2];
         const float ar = ex * ey + ey * ez + ez * ex;
         const uint32_t key = (__float_as_uint(ar) & ~15u) | 8u | (uint32_t)(7 - i);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (k == i) akey[k] = key;
+        S.akey[i][tid] = key;
         const bool in = id < a.n - 1, big = in && (int)(cl >> 29) > LEAF_MAX;
         inner_m = in ? (inner_m | (1u << i)) : (inner_m & ~(1u << i));
         big_m = big ? (big_m | (1u << i)) : (big_m & ~(1u << i));
@@ -844,7 +843,7 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
             if (!elig) break;
             uint32_t m = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) m = max(m, (elig >> i & 1) ? akey[i] : 0u);
+            for (int i = 0; i < 8; ++i) m = max(m, (elig >> i & 1) ? S.akey[i][tid] : 0u);
             const int best = 7 - (int)(m & 7u);
             const int l = (int)(S.ccl[best][tid] & 0x1fffffffu), r = (int)(S.ccr[best][tid] & 0x1fffffffu);
             put(best, l);
