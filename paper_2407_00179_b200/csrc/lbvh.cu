@@ -863,10 +863,10 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
     // recomputed only when another child takes it
     int slot_of[8];
     {
-        // candidate keys: the cost as an order-preserving integer with its low 6 bits replaced by
-        // (slot << 3) | (7 - child), so one integer max picks the child (ties: lowest index)
-        // and carries its slot; 0 = assigned / absent
-        uint32_t pk[8];
+        // candidate keys (in S.akey, free after the opening phase): the cost as an
+        // order-preserving integer with its low 6 bits replaced by (slot << 3) | (7 - child), so
+        // one integer max picks the child (ties: lowest index) and carries its slot; an assigned
+        // child's entry holds its slot (0..7, below every key), an absent child's 0
         auto pack = [](float c, int sl, int i) -> uint32_t {
             const uint32_t u = __float_as_uint(c);
             const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
@@ -890,14 +890,15 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
         // |dx| + |dy| + |dz|
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            slot_of[i] = 0; pk[i] = 0;
+            uint32_t key = 0;
             if (i < nc) {
                 float dc[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) dc[c] = (S.lo[c][i][tid] + S.hi[c][i][tid]) - (nlo_[c] + nhi_[c]);
-                pk[i] = pack((fabsf(dc[0]) + fabsf(dc[1])) + fabsf(dc[2]),
-                             (dc[0] > 0.0f ? 4 : 0) | (dc[1] > 0.0f ? 2 : 0) | (dc[2] > 0.0f ? 1 : 0), i);
+                key = pack((fabsf(dc[0]) + fabsf(dc[1])) + fabsf(dc[2]),
+                           (dc[0] > 0.0f ? 4 : 0) | (dc[1] > 0.0f ? 2 : 0) | (dc[2] > 0.0f ? 1 : 0), i);
             }
+            S.akey[i][tid] = key;
         }
         unsigned used_slots = 0;
         // lazy greedy: a child's cached (cost, slot) is an upper bound of its best free slot
@@ -908,21 +909,20 @@ __global__ void __launch_bounds__(CB, DPR_COLLAPSE_MINB) k_collapse_r(const Coll
         for (int k = 0; k < nc;) {
             uint32_t m = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) m = max(m, pk[i]);
+            for (int i = 0; i < 8; ++i) m = max(m, S.akey[i][tid]);
             const int bi = 7 - (int)(m & 7u), bs = (int)((m >> 3) & 7u);
             if (used_slots >> bs & 1) {
                 float nc_; int ns_;
                 best_free(bi, used_slots, nc_, ns_);
-                const uint32_t nk = pack(nc_, ns_, bi);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) if (i == bi) pk[i] = nk;
+                S.akey[bi][tid] = pack(nc_, ns_, bi);
                 continue;
             }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) if (i == bi) { slot_of[i] = bs; pk[i] = 0; }
+            S.akey[bi][tid] = (uint32_t)bs;
             used_slots |= 1u << bs;
             ++k;
         }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) slot_of[i] = i < nc ? (int)S.akey[i][tid] : 0;
     }
     // internal vs leaf children, allocation
     int n_int = 0, n_prims = 0;
